@@ -1,0 +1,309 @@
+#!/usr/bin/env python
+"""Benchmark of the RAV hot path (BASELINE.json metric: "RAV sweep MDoF/s and
+HBM GB/s vs peak; V-cycle time to 1e-8").
+
+Workload (N=1): BASELINE config 2 -- 2D unit square 512x512 Taylor-Hood Q2-Q1,
+seeded variable viscosity, manufactured forcing; one STEP = 100 RAV sweeps
+(residual SpMV + fused RAV sweep kernel, rav_smooth(nu=100)) from the seeded
+N(0,1) guess.  value = free DoFs x sweeps / second (MDoF/s), device-timed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+--impl reference times the CPU oracle (oracle/, plain C) on the same workload
+(bounded: one sweep per step).  Under torchrun (N > 1) every rank runs its own
+c2 replica (weak scaling, no data-path collective yet).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SWEEPS_PER_STEP = 100
+OMEGA = 0.66
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.out = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is None:
+            self.out = ""
+            return
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            self.out = ""
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_oracle_rate(prob, steps, warmup, sweeps_per_step=1):
+    """The oracle (as it stands) timed on this host: setup untimed, then
+    `sweeps_per_step` RAV sweeps per step.  Returns (MDoF/s, cores, sample)."""
+    import numpy as np
+    import oracle
+    import seeded_inputs as si
+    O = oracle.assemble(prob)
+    P = oracle.patches(prob, "pou")
+    F = oracle.factor(O, P, oracle.FMT_ROWS)
+    x = si.initial_guess(O["n"], seed=si.X0_SEED)
+    for _ in range(warmup):
+        x = oracle.additive_sweeps(O, P, F, x, O["b"], OMEGA, sweeps_per_step)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        x = oracle.additive_sweeps(O, P, F, x, O["b"], OMEGA, sweeps_per_step)
+    dt = time.perf_counter() - t0
+    rate = O["n"] * sweeps_per_step * steps / dt / 1e6
+    sample = (f"c2 (512^2, {O['n']} DoFs) oracle RAV sweeps, {steps} x {sweeps_per_step} sweep(s) "
+              f"after untimed setup; {dt:.2f} s")
+    return rate, 1, sample, dt
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import seeded_inputs as si
+    prob = si.config_problem("c2")
+    rate, cores, sample, dt = cpu_oracle_rate(prob, args.steps, args.warmup)
+    n = None
+    line = {"metric": "RAV sweep throughput (c2: 512^2 Q2-Q1, variable viscosity)", "value": rate,
+            "unit": "MDoF/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c2: 2D 512x512 Q2-Q1 MMS, seeded eta in [0.1,10], RAV sweeps",
+                       "sweeps_per_step": 1},
+            "impl": "reference",
+            "cpu_baseline": {"value": rate, "unit": "MDoF/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": rate, "unit": "MDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2103_10127_b200 import ravgmg as rg
+    import seeded_inputs as si
+
+    prob = si.config_problem("c2")
+    stream = torch.cuda.current_stream()
+    t_setup0 = time.perf_counter()
+    G = rg.gen_level(prob, "pou")
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_setup0
+    t1 = time.perf_counter()
+    sm = rg.Smoother(G, G)
+    torch.cuda.synchronize()
+    t_factor = time.perf_counter() - t1
+    n = G["n"]
+    b = G["b"]
+    x0 = torch.tensor(si.initial_guess(n, seed=si.X0_SEED), device="cuda")
+    x = x0.clone()
+    bytes_info = sm.sweep_bytes()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # ---- device-timed steps: rav_smooth(nu = 100) --------------------------------
+    for _ in range(args.warmup):
+        sm.smooth(x, b, SWEEPS_PER_STEP, OMEGA)
+    launches_per_step = sm.last_launches
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            sm.smooth(x, b, SWEEPS_PER_STEP, OMEGA)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = ws * n * SWEEPS_PER_STEP / (ms_per_step * 1e-3) / 1e6
+    assert torch.isfinite(x).all()
+
+    # ---- dominant kernel alone (sweep, rav_apply) and the residual SpMV ------------
+    r = sm.residual(x, b)
+    nk = 50
+    for _ in range(5):
+        sm.apply(r, x, OMEGA)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(nk):
+        sm.apply(r, x, OMEGA)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    sweep_ms = e0.elapsed_time(e1) / nk
+    for _ in range(5):
+        sm.residual(x, b, r)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(nk):
+        sm.residual(x, b, r)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    resid_ms = e0.elapsed_time(e1) / nk
+    peak, peak_kind = load_peaks()
+    achieved = bytes_info["sweep"] / (sweep_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the C-ABI with host buffers ----------------------------
+    xh = x0.cpu().pin_memory()
+    bh = b.cpu().pin_memory()
+    xh_np, bh_np = xh.numpy(), bh.numpy()
+    sm.smooth(xh_np, bh_np, SWEEPS_PER_STEP, OMEGA)   # warm (staging buffers, graph)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sm.smooth(xh_np, bh_np, SWEEPS_PER_STEP, OMEGA)   # H2D x,b + 100 sweeps + D2H x (synchronous)
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = ws * n * SWEEPS_PER_STEP * args.steps / e2e_s / 1e6
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample) ------------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        rate, cores, sample, _ = cpu_oracle_rate(prob, steps=3, warmup=0)
+        cpu = {"value": rate, "unit": "MDoF/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    clocks = clk.summary()
+    line = {
+        "metric": "RAV sweep throughput (c2: 512^2 Q2-Q1, variable viscosity)",
+        "value": value, "unit": "MDoF/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c2: 2D 512x512 Taylor-Hood Q2-Q1, MMS forcing, seeded eta in [0.1,10]; "
+                               "step = 100 RAV sweeps (residual SpMV + RAV sweep) from seeded N(0,1)",
+                   "free_dofs": n, "nnz": G["nnz"], "patches": len(G["offs"]) - 1,
+                   "sweeps_per_step": SWEEPS_PER_STEP, "omega": OMEGA, "weights": "partition of unity (R3)",
+                   "l2": "inputs larger than L2 (factor rows 2.0 GB + CSR 0.73 GB streamed per sweep; "
+                         "x, r, b vectors 19 MB each stay L2-resident by design)",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "sweep_thread_kernel<19> (rav_apply)", "kernel_ms": sweep_ms,
+                     "algorithmic_bytes_per_launch": bytes_info["sweep"]},
+        "residual_kernel": {"ms": resid_ms, "algorithmic_bytes": bytes_info["residual"],
+                            "achieved_gbs": bytes_info["residual"] / (resid_ms * 1e-3) / 1e9},
+        "sweep_total": {"ms_per_sweep": ms_per_step / SWEEPS_PER_STEP,
+                        "algorithmic_bytes": bytes_info["sweep"] + bytes_info["residual"],
+                        "achieved_gbs": (bytes_info["sweep"] + bytes_info["residual"]) /
+                                        (ms_per_step / SWEEPS_PER_STEP * 1e-3) / 1e9},
+        "setup_s": {"generate": t_gen, "factorize": t_factor},
+        "e2e": {"value": e2e_value, "unit": "MDoF/s", "h2d_bytes_per_step": 2 * 8 * n,
+                "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,245 @@
+/*
+ * ravgmg.h -- C-ABI of the B200-native restricted additive Vanka (RAV)
+ * geometric-multigrid hot path (Saberi, Meschke, Vogel, arXiv 2103.10127).
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (section / equation named),
+ * "S:n" = SPEC.md line n, "R<k>" = reading k of DESIGN.md section 2.
+ *
+ * Conventions (all entry points):
+ *  - Plain C types only; every function is extern "C" and never throws.
+ *  - Every call returns rav_status; on failure rav_last_error() returns a
+ *    thread-local, human-readable message (valid until the next failing call
+ *    on the same thread).
+ *  - Floating point is IEEE binary64 throughout.  Indices: int32 column/DoF
+ *    indices, int64 row pointers / offsets.
+ *  - "device" pointers are CUDA global-memory pointers on the current device
+ *    (e.g. torch tensor data_ptr()); "host" pointers are ordinary CPU memory.
+ *    Functions that accept either detect the kind with cudaPointerGetAttributes.
+ *  - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Work is stream-ordered; functions that return sizes or status from the
+ *    device synchronize the stream before returning.
+ *  - Ownership: buffers passed in are caller-owned.  rav_setup / mg_setup COPY
+ *    what they need into library-owned device memory, so callers may free
+ *    their inputs afterwards.  Contexts are released with rav_destroy /
+ *    mg_destroy.
+ */
+#ifndef RAVGMG_H
+#define RAVGMG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RAV_OK = 0,
+    RAV_ERR_ARG = 1,              /* invalid argument (sizes, NULL, empty patch S:302) */
+    RAV_ERR_SINGULAR_LOCAL = 2,   /* a local system L_i is singular */
+    RAV_ERR_SINGULAR_COARSE = 3,  /* the pinned coarsest system is singular */
+    RAV_ERR_OOM = 4,              /* device allocation failed */
+    RAV_ERR_CUDA = 5,             /* a CUDA runtime error */
+    RAV_ERR_COMM = 6,             /* multi-rank exchange error */
+    RAV_ERR_DIVERGED = 7          /* NaN/Inf residual during mg_solve */
+} rav_status;
+
+/* ------------------------------------------------------------------------- */
+/* Structured Q2-Q1 problem generator      */
+/* ------------------------------------------------------------------------- */
+
+/* Uniform grid of ncell[0] x ncell[1] (x ncell[2]) cells on the box
+ * [0,len0] x [0,len1] (x [0,len2]), Taylor-Hood Q2-Q1 (R1).
+ * kind: 0 lid-driven cavity (u = e_x on the top face interior, no-slip
+ *         elsewhere, f = 0, R8),
+ *       1 manufactured solution u = curl(sin^2 pi x sin^2 pi y),
+ *         p = cos pi x cos pi y (2D only, R13), homogeneous Dirichlet,
+ *       2 homogeneous (f = 0, u = 0 on the boundary).
+ * eta_mode: 0 constant eta0; 1 eta = exp(ln 0.1 + (g - gmin)/(gmax - gmin) ln 100),
+ *         g(x) = sum_k amp[k] prod_d cos(pi mode[k][d] x_d + phase[k][d]) (R12).
+ * DoF numbering (R9): free Q2 nodes lexicographic (x fastest), velocity
+ * components interleaved (dof = dim * node + c); then all vertices
+ * lexicographic (pressure).  Dirichlet DoFs are eliminated. */
+typedef struct {
+    int32_t dim;
+    int32_t ncell[3];
+    double  len[3];
+    int32_t kind;
+    int32_t eta_mode;
+    double  eta0;
+    int32_t n_modes;            /* <= 8 */
+    double  amp[8];
+    int32_t mode[8][3];
+    double  phase[8][3];
+    double  gmin, gmax;
+} rav_grid;
+
+/* Sizes of the generated level: n_dofs = n_vel + n_pres; nnz of L; number of
+ * patches (= vertices) and total patch entries for the given weights mode
+ * (0 partition of unity R3, 1 0/1 ownership, 2 all ones = additive Vanka).
+ * Runs counting kernels on `stream` and synchronizes it. */
+rav_status rav_gen_sizes(const rav_grid* g, int weights, void* stream,
+                         int64_t* n_dofs, int64_t* n_vel, int64_t* nnz,
+                         int64_t* n_patches, int64_t* patch_entries);
+
+/* Assemble L = [A B; B^T 0] (Eq. 6, Eq. 7; C = 0 for Taylor-Hood)
+ * in CSR with sorted columns and the right-hand side b (Eq. 5 with the
+ * Dirichlet lift b_free = F_free - L_{free,D} u_D).  3-point Gauss
+ * rule per axis (R7).  The pattern is STRUCTURAL (R2): entries that evaluate
+ * to 0 are stored.  Device buffers, caller-allocated: row_ptr[n_dofs+1],
+ * col[nnz], val[nnz], rhs[n_dofs]. */
+rav_status rav_gen_operator(const rav_grid* g, int64_t* row_ptr, int32_t* col, double* val,
+                            double* rhs, void* stream);
+
+/* Vanka patches: one per vertex v (in vertex order), holding every
+ * free velocity DoF on the Q2 nodes of the elements touching v plus p_v.
+ * Per patch the restricted DoFs (weight > 0, P:122 / R3) come first in
+ * ascending order, then the others ascending.  Device buffers:
+ * offs[n_patches+1], dofs[patch_entries], w[patch_entries]. */
+rav_status rav_gen_patches(const rav_grid* g, int weights, int64_t* offs, int32_t* dofs,
+                           double* w, void* stream);
+
+/* Nested prolongation P from `coarse` (ncell/2) to `fine`: Q2
+ * interpolation for velocity, Q1 for pressure, Dirichlet rows/columns
+ * dropped.  Rows = fine DoFs, columns = coarse DoFs, sorted.  nnz first
+ * (synchronizes), then fill device buffers rp[n_fine+1], ci[nnz], val[nnz]. */
+rav_status rav_gen_prolongation_nnz(const rav_grid* fine, const rav_grid* coarse, void* stream,
+                                    int64_t* nnz);
+rav_status rav_gen_prolongation(const rav_grid* fine, const rav_grid* coarse, int64_t* rp,
+                                int32_t* ci, double* val, void* stream);
+
+/* ------------------------------------------------------------------------- */
+/* Smoother: RAV (Eq. 13) and its additive relatives                    */
+/* ------------------------------------------------------------------------- */
+
+/* A sparse matrix in CSR.  Columns sorted ascending within each row. */
+typedef struct {
+    int64_t n_rows, n_cols;
+    const int64_t* row_ptr;     /* n_rows + 1 */
+    const int32_t* col;         /* row_ptr[n_rows] */
+    const double*  val;
+    int32_t on_device;          /* 1: device pointers, 0: host pointers */
+} rav_csr;
+
+/* Subdomains S_{x,Omega_sd,i}: patch i holds dofs[offs[i]..offs[i+1]).
+ * weight[j] > 0 marks a DoF of the restricted prolongation R~_i with
+ * its partition-of-unity weight (R3); restricted DoFs need not be listed
+ * first (setup reorders internally).  weight == 1 on every entry gives the
+ * additive Vanka operator of Eq. 12. */
+typedef struct {
+    int64_t n_patches;
+    const int64_t* offs;        /* n_patches + 1 */
+    const int32_t* dofs;
+    const double*  weight;
+    int32_t on_device;
+} rav_patches;
+
+enum {
+    RAV_VARIANT_ROWS = 0,       /* precomputed weighted rows of L_i^{-1} */
+    RAV_VARIANT_DIAG = 1        /* diagonal Vanka: A_i replaced by diag(A_i) (R17); needs
+                                   exactly one pressure DoF (n_vel <= dof) per patch */
+};
+
+enum {
+    RAV_KERNEL_AUTO = 0,        /* thread-per-patch SoA kernel when the patch shape allows */
+    RAV_KERNEL_WARP = 1,        /* general warp-per-patch kernel (any n_i, nres_i) */
+    RAV_KERNEL_THREAD = 2       /* force the thread-per-patch kernel (nres <= 32, n <= 64) */
+};
+
+typedef struct {
+    int32_t variant;            /* RAV_VARIANT_* */
+    int32_t kernel;             /* RAV_KERNEL_* */
+    int32_t deterministic;      /* 1: run-to-run bitwise reproducible scatter (two-phase) */
+    int64_t n_vel;              /* DoFs < n_vel are velocity (needed by DIAG) */
+    void*   stream;             /* cudaStream_t */
+} rav_opts;
+
+typedef struct rav_ctx rav_ctx;
+
+/* Build the smoother for L x = b: for every patch gather
+ * L_i = R_i L R_i^T from the CSR, factor it (Gaussian elimination with partial
+ * pivoting on L_i^T, pivot tolerance 1e-14 * ||row||_inf) and store the
+ * restricted rows W_i = diag(w_i) L_i^{-1}[restricted, :].
+ * On RAV_ERR_SINGULAR_LOCAL, *bad_patch (if non-NULL) holds the smallest
+ * failing patch id.  Empty patches are RAV_ERR_ARG. */
+rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opts,
+                     rav_ctx** out, int64_t* bad_patch);
+
+/* nu sweeps of x <- x + omega * sum_i R~_i^T L_i^{-1} R_i (b - L x)
+ * (Eq. 10 with S_RAV of P:124 Eq. 13, scalar damping omega, R5).
+ * x (in/out) and b are length n_rows, both device or both host pointers;
+ * host buffers are staged through library-owned device buffers (the copies
+ * are part of the call).  Stream-ordered on the context stream. */
+rav_status rav_smooth(rav_ctx* ctx, double* x, const double* b, int nu, double omega);
+
+/* x += omega * sum_i R~_i^T W_i R_i r for a given residual r (device
+ * pointers): one application of the smoother operator S_RAV of P:124 Eq. 13
+ * to r, i.e. the sweep kernel alone (used to time it in isolation). */
+rav_status rav_apply(rav_ctx* ctx, const double* r, double* x, double omega);
+
+/* r = b - L x (device pointers).  The residual SpMV of P:104 Eq. 10. */
+rav_status rav_residual(rav_ctx* ctx, const double* x, const double* b, double* r);
+
+/* Export the stored factor rows in the canonical layout (for parity tests):
+ * for patch i, rows k of its restricted DoFs (in the patch's own order of
+ * the restricted entries), each of length n_i, concatenated; plus per-entry
+ * DoF lists.  Sizes via rav_rows_size.  Device output buffers. */
+rav_status rav_rows_size(const rav_ctx* ctx, int64_t* total);
+rav_status rav_export_rows(const rav_ctx* ctx, double* rows);
+
+/* Bytes the sweep must move per application (algorithmic roofline bytes:
+ * factor rows + patch indices + CSR + compulsory vectors), and flops. */
+rav_status rav_sweep_bytes(const rav_ctx* ctx, double* bytes_sweep, double* bytes_residual,
+                           double* flops);
+
+rav_status rav_set_stream(rav_ctx* ctx, void* stream);
+void rav_destroy(rav_ctx* ctx);
+
+/* ------------------------------------------------------------------------- */
+/* Geometric multigrid                                   */
+/* ------------------------------------------------------------------------- */
+
+typedef struct mg_ctx mg_ctx;
+
+/* Levels are ordered coarsest first: A[0] is the coarsest operator, A[L-1]
+ * the finest.  P[l] (l >= 1) is the nested prolongation from level l-1 to
+ * level l (rows = DoFs of level l); P[0] and patches[0] are ignored.  The
+ * coarsest system is solved by a dense LU with partial pivoting in
+ * which DoF `coarse_pin` is removed and set to 0 (R4: the pressure null
+ * space is fixed only here; coarse_pin < 0 disables the pin).  Smoothers on
+ * levels 1..L-1 are built with rav_setup(opts). */
+rav_status mg_setup(int n_levels, const rav_csr* A, const rav_patches* patches, const rav_csr* P,
+                    int64_t coarse_pin, const rav_opts* opts, mg_ctx** out,
+                    int* bad_level, int64_t* bad_patch);
+
+/* One V-cycle (Fig. 1): pre smoothing steps, restriction of the
+ * residual (R = P^T), recursive coarse correction from a zero guess, coarse
+ * LU at level 0, prolongation and addition, post smoothing steps.  x, b:
+ * device pointers on the finest level. */
+rav_status mg_vcycle(mg_ctx* ctx, double* x, const double* b, int pre, int post, double omega);
+
+/* Stand-alone multigrid iteration: V-cycles until
+ * ||b - L x_k||_2 <= rtol ||b - L x_0||_2 or maxit (R11).  *iters = k;
+ * hist (host, maxit + 1 doubles, may be NULL) receives ||r_0||..||r_k||.
+ * x, b: device or host pointers (host buffers are staged).  Returns
+ * RAV_ERR_DIVERGED on a NaN/Inf residual; non-convergence is RAV_OK with
+ * *iters == maxit. */
+rav_status mg_solve(mg_ctx* ctx, double* x, const double* b, int pre, int post, double omega,
+                    double rtol, int maxit, int* iters, double* hist);
+
+/* Number of GPU kernel launches issued by the most recent rav_smooth,
+ * mg_vcycle or mg_solve call on this context (graph nodes included). */
+int64_t rav_last_launches(const rav_ctx* ctx);
+int64_t mg_last_launches(const mg_ctx* ctx);
+rav_status mg_set_stream(mg_ctx* ctx, void* stream);
+void mg_destroy(mg_ctx* ctx);
+
+/* Thread-local message of the last failure on this thread ("" if none). */
+const char* rav_last_error(void);
+
+/* Library version string. */
+const char* rav_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAVGMG_H */

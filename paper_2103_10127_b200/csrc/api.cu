@@ -1,0 +1,476 @@
+// api.cu -- the C-ABI of include/ravgmg.h: smoother and multigrid contexts,
+// stream-ordered execution, CUDA-graph capture of sweep sequences and of whole
+// V-cycles (the coarse levels are launch-bound), host-buffer staging.
+#include <stdarg.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace rav {
+
+static thread_local char g_err[1024] = "";
+thread_local int64_t g_launches = 0;
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+const char* get_error() { return g_err; }
+
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return n;
+}
+
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// A captured sequence of launches, keyed by its arguments.
+struct GraphCache {
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    const void* k0 = nullptr;
+    const void* k1 = nullptr;
+    int i0 = -1, i1 = -1, i2 = -1;
+    double d0 = 0.0;
+    int64_t nodes = 0;
+    bool match(const void* a, const void* b, int x, int y, int z, double w) const {
+        return exec && a == k0 && b == k1 && x == i0 && y == i1 && z == i2 && w == d0;
+    }
+    void reset() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        exec = nullptr;
+        graph = nullptr;
+    }
+};
+
+}  // namespace rav
+
+using namespace rav;
+
+struct rav_ctx {
+    Csr A;
+    PatchSet P;
+    Factors F;
+    int variant = 0;
+    int64_t nvel = 0;
+    cudaStream_t stream = nullptr;
+    double* r = nullptr;        // residual work vector
+    double* hx = nullptr;       // staging for host x / b
+    double* hb = nullptr;
+    GraphCache graph;
+    int64_t last_launches = 0;
+};
+
+struct mg_level {
+    rav_ctx* sm = nullptr;  // smoother (levels >= 1)
+    Csr A;                  // level operator (owned by sm for l >= 1; own copy at l = 0)
+    Csr P, PT;              // prolongation from l-1 and its transpose (restriction)
+    double* x = nullptr;    // level iterate (l < L-1)
+    double* b = nullptr;    // level right-hand side (l < L-1)
+    double* r = nullptr;    // level residual
+};
+
+struct mg_ctx {
+    int L = 0;
+    std::vector<mg_level> lv;
+    CoarseLU C;
+    cudaStream_t stream = nullptr;
+    double* part = nullptr;     // residual-norm partials
+    double* norm2 = nullptr;    // device scalar
+    double* h_norm2 = nullptr;  // pinned host scalar
+    double* hx = nullptr;
+    double* hb = nullptr;
+    GraphCache cyc;             // one V-cycle + residual norm
+    int64_t last_launches = 0;
+};
+
+namespace rav {
+
+static rav_status smooth_launches(rav_ctx* c, double* x, const double* b, int nu, double omega) {
+    for (int k = 0; k < nu; ++k) {
+        RAV_TRY(launch_residual(c->A, x, b, c->r, c->stream));
+        RAV_TRY(launch_sweep(c->P, c->F, c->r, x, omega, c->stream));
+    }
+    return RAV_OK;
+}
+
+// run `body` either directly or through a cached CUDA graph on stream s
+template <class Body>
+static rav_status run_graph(GraphCache& G, cudaStream_t s, bool use_graph, const void* k0, const void* k1, int i0,
+                            int i1, int i2, double d0, int64_t& launches, Body body) {
+    if (!use_graph) {
+        int64_t before = g_launches;
+        RAV_TRY(body());
+        launches = g_launches - before;
+        return RAV_OK;
+    }
+    if (!G.match(k0, k1, i0, i1, i2, d0)) {
+        G.reset();
+        int64_t before = g_launches;
+        RAV_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        rav_status st = body();
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(s, &g);
+        if (st != RAV_OK) { if (g) cudaGraphDestroy(g); return st; }
+        RAV_CUDA(e);
+        G.graph = g;
+        RAV_CUDA(cudaGraphInstantiate(&G.exec, g, 0));
+        G.k0 = k0; G.k1 = k1; G.i0 = i0; G.i1 = i1; G.i2 = i2; G.d0 = d0;
+        G.nodes = g_launches - before;
+        g_launches = before;
+    }
+    RAV_CUDA(cudaGraphLaunch(G.exec, s));
+    g_launches += G.nodes;
+    launches = G.nodes;
+    return RAV_OK;
+}
+
+}  // namespace rav
+
+extern "C" {
+
+const char* rav_last_error(void) { return rav::get_error(); }
+const char* rav_version(void) { return "ravgmg 0.1 (sm_100a)"; }
+
+rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opts, rav_ctx** out,
+                     int64_t* bad_patch) {
+    if (!out || !A || !P) { set_error("rav_setup: NULL argument"); return RAV_ERR_ARG; }
+    *out = nullptr;
+    if (bad_patch) *bad_patch = -1;
+    rav_opts o{};
+    if (opts) o = *opts;
+    if (o.variant != RAV_VARIANT_ROWS && o.variant != RAV_VARIANT_DIAG) { set_error("rav_setup: bad variant"); return RAV_ERR_ARG; }
+    if (o.deterministic) { set_error("rav_setup: deterministic scatter not available in this build"); return RAV_ERR_ARG; }
+    if (A->n_rows != A->n_cols) { set_error("rav_setup: L must be square"); return RAV_ERR_ARG; }
+    rav_ctx* c = new rav_ctx();
+    c->stream = as_stream(o.stream);
+    c->variant = o.variant;
+    c->nvel = o.n_vel;
+    rav_status st = csr_upload(A, c->A, c->stream);
+    if (st == RAV_OK) st = patches_upload(P, A->n_rows, c->P, c->stream);
+    if (st == RAV_OK) st = factorize(c->A, c->P, o.variant, o.n_vel, o.kernel, c->F, bad_patch, c->stream);
+    if (st == RAV_OK) {
+        cudaError_t e = cudaMalloc(&c->r, sizeof(double) * std::max<int64_t>(1, c->A.n_rows));
+        if (e != cudaSuccess) { set_error("rav_setup: %s", cudaGetErrorString(e)); st = RAV_ERR_OOM; }
+    }
+    if (st != RAV_OK) { rav_destroy(c); return st; }
+    *out = c;
+    return RAV_OK;
+}
+
+rav_status rav_set_stream(rav_ctx* c, void* stream) {
+    if (!c) { set_error("NULL ctx"); return RAV_ERR_ARG; }
+    if (c->stream != as_stream(stream)) c->graph.reset();
+    c->stream = as_stream(stream);
+    return RAV_OK;
+}
+
+rav_status rav_smooth(rav_ctx* c, double* x, const double* b, int nu, double omega) {
+    if (!c || !x || !b || nu < 0) { set_error("rav_smooth: bad argument"); return RAV_ERR_ARG; }
+    g_launches = 0;
+    if (nu == 0) { c->last_launches = 0; return RAV_OK; }
+    const int64_t n = c->A.n_rows;
+    bool dx = is_device_ptr(x), db = is_device_ptr(b);
+    if (dx != db) { set_error("rav_smooth: x and b must both be device or both host pointers"); return RAV_ERR_ARG; }
+    double* X = x;
+    const double* B = b;
+    if (!dx) {
+        if (!c->hx) {
+            RAV_CUDA(cudaMalloc(&c->hx, sizeof(double) * n));
+            RAV_CUDA(cudaMalloc(&c->hb, sizeof(double) * n));
+        }
+        RAV_CUDA(cudaMemcpyAsync(c->hx, x, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        RAV_CUDA(cudaMemcpyAsync(c->hb, b, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        X = c->hx;
+        B = c->hb;
+    }
+    bool use_graph = c->stream != nullptr && nu >= 2;
+    RAV_TRY(run_graph(c->graph, c->stream, use_graph, X, B, nu, 0, 0, omega, c->last_launches,
+                      [&]() { return smooth_launches(c, X, B, nu, omega); }));
+    if (!dx) {
+        RAV_CUDA(cudaMemcpyAsync(x, c->hx, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        RAV_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    return RAV_OK;
+}
+
+rav_status rav_residual(rav_ctx* c, const double* x, const double* b, double* r) {
+    if (!c || !x || !b || !r) { set_error("rav_residual: NULL argument"); return RAV_ERR_ARG; }
+    g_launches = 0;
+    RAV_TRY(launch_residual(c->A, x, b, r, c->stream));
+    c->last_launches = g_launches;
+    return RAV_OK;
+}
+
+rav_status rav_apply(rav_ctx* c, const double* r, double* x, double omega) {
+    if (!c || !x || !r) { set_error("rav_apply: NULL argument"); return RAV_ERR_ARG; }
+    g_launches = 0;
+    RAV_TRY(launch_sweep(c->P, c->F, r, x, omega, c->stream));
+    c->last_launches = g_launches;
+    return RAV_OK;
+}
+
+rav_status rav_rows_size(const rav_ctx* c, int64_t* total) {
+    if (!c || !total) { set_error("NULL argument"); return RAV_ERR_ARG; }
+    *total = c->P.rows_total;
+    return RAV_OK;
+}
+
+rav_status rav_export_rows(const rav_ctx* c, double* rows) {
+    if (!c || !rows) { set_error("NULL argument"); return RAV_ERR_ARG; }
+    RAV_TRY(export_rows(c->P, c->F, rows, c->stream));
+    RAV_CUDA(cudaStreamSynchronize(c->stream));
+    return RAV_OK;
+}
+
+rav_status rav_sweep_bytes(const rav_ctx* c, double* bytes_sweep, double* bytes_residual, double* flops) {
+    if (!c) { set_error("NULL ctx"); return RAV_ERR_ARG; }
+    const double n = (double)c->A.n_rows, nnz = (double)c->A.nnz;
+    // algorithmic bytes (SURVEY section 8 row d): factor rows 8 sum nres_i n_i, patch DoF
+    // indices 4 sum n_i, x read+write, r gathered once (compulsory vectors)
+    double rows = 8.0 * (double)c->P.rows_total;
+    double idx = 4.0 * (double)c->P.entries;
+    double sweep = rows + idx + 8.0 * n /* r */ + 16.0 * n /* x rmw */;
+    double resid = 12.0 * nnz + 8.0 * (n + 1) + 8.0 * n /* x */ + 8.0 * n /* b */ + 8.0 * n /* r write */;
+    if (bytes_sweep) *bytes_sweep = sweep;
+    if (bytes_residual) *bytes_residual = resid;
+    if (flops) *flops = 2.0 * (double)c->P.rows_total + 2.0 * nnz;
+    return RAV_OK;
+}
+
+int64_t rav_last_launches(const rav_ctx* c) { return c ? c->last_launches : 0; }
+
+void rav_destroy(rav_ctx* c) {
+    if (!c) return;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    else cudaDeviceSynchronize();
+    c->graph.reset();
+    csr_free(c->A);
+    patches_free(c->P);
+    factors_free(c->F);
+    if (c->r) cudaFree(c->r);
+    if (c->hx) cudaFree(c->hx);
+    if (c->hb) cudaFree(c->hb);
+    delete c;
+}
+
+// ------------------------------------------------------------------------------------
+// multigrid
+// ------------------------------------------------------------------------------------
+
+void mg_destroy(mg_ctx* m) {
+    if (!m) return;
+    if (m->stream) cudaStreamSynchronize(m->stream);
+    else cudaDeviceSynchronize();
+    m->cyc.reset();
+    for (int l = 0; l < (int)m->lv.size(); ++l) {
+        mg_level& L = m->lv[l];
+        if (L.sm) rav_destroy(L.sm);
+        else csr_free(L.A);
+        csr_free(L.P);
+        csr_free(L.PT);
+        if (L.x) cudaFree(L.x);
+        if (L.b) cudaFree(L.b);
+        if (L.r) cudaFree(L.r);
+    }
+    coarse_free(m->C);
+    if (m->part) cudaFree(m->part);
+    if (m->norm2) cudaFree(m->norm2);
+    if (m->h_norm2) cudaFreeHost(m->h_norm2);
+    if (m->hx) cudaFree(m->hx);
+    if (m->hb) cudaFree(m->hb);
+    delete m;
+}
+
+rav_status mg_setup(int n_levels, const rav_csr* A, const rav_patches* patches, const rav_csr* P,
+                    int64_t coarse_pin, const rav_opts* opts, mg_ctx** out, int* bad_level, int64_t* bad_patch) {
+    if (!out || !A || n_levels < 1 || (n_levels > 1 && (!patches || !P))) {
+        set_error("mg_setup: bad argument");
+        return RAV_ERR_ARG;
+    }
+    *out = nullptr;
+    if (bad_level) *bad_level = -1;
+    if (bad_patch) *bad_patch = -1;
+    rav_opts o{};
+    if (opts) o = *opts;
+    mg_ctx* m = new mg_ctx();
+    m->L = n_levels;
+    m->lv.resize(n_levels);
+    m->stream = as_stream(o.stream);
+    rav_status st = RAV_OK;
+    for (int l = 0; l < n_levels && st == RAV_OK; ++l) {
+        mg_level& L = m->lv[l];
+        if (l == 0) {
+            st = csr_upload(&A[0], L.A, m->stream);
+            if (st == RAV_OK) st = coarse_factor(L.A, coarse_pin, m->C, m->stream);
+        } else {
+            if (P[l].n_rows != A[l].n_rows || P[l].n_cols != A[l - 1].n_rows) {
+                set_error("mg_setup: P[%d] must be n_%d x n_%d", l, l, l - 1);
+                st = RAV_ERR_ARG;
+                break;
+            }
+            int64_t bp = -1;
+            st = rav_setup(&A[l], &patches[l], &o, &L.sm, &bp);
+            if (st == RAV_ERR_SINGULAR_LOCAL) {
+                if (bad_level) *bad_level = l;
+                if (bad_patch) *bad_patch = bp;
+            }
+            if (st != RAV_OK) break;
+            L.A = L.sm->A;  // shallow view (owned by the smoother)
+            st = csr_upload(&P[l], L.P, m->stream);
+            if (st == RAV_OK) st = csr_transpose(L.P, L.PT, m->stream);
+        }
+        if (st != RAV_OK) break;
+        int64_t n = L.A.n_rows;
+        cudaError_t e = cudaMalloc(&L.r, sizeof(double) * std::max<int64_t>(1, n));
+        if (e == cudaSuccess && l < n_levels - 1) {
+            e = cudaMalloc(&L.x, sizeof(double) * std::max<int64_t>(1, n));
+            if (e == cudaSuccess) e = cudaMalloc(&L.b, sizeof(double) * std::max<int64_t>(1, n));
+        }
+        if (e != cudaSuccess) { set_error("mg_setup: %s", cudaGetErrorString(e)); st = RAV_ERR_OOM; }
+    }
+    if (st == RAV_OK) {
+        cudaError_t e = cudaMalloc(&m->part, sizeof(double) * residual_norm_blocks());
+        if (e == cudaSuccess) e = cudaMalloc(&m->norm2, sizeof(double));
+        if (e == cudaSuccess) e = cudaMallocHost(&m->h_norm2, sizeof(double));
+        if (e != cudaSuccess) { set_error("mg_setup: %s", cudaGetErrorString(e)); st = RAV_ERR_OOM; }
+    }
+    if (st != RAV_OK) {
+        // the smoother contexts own their operators; avoid double frees of the views
+        for (auto& L : m->lv)
+            if (L.sm) L.A = Csr{};
+        mg_destroy(m);
+        return st;
+    }
+    for (auto& L : m->lv)
+        if (L.sm) L.sm->stream = m->stream;
+    *out = m;
+    return RAV_OK;
+}
+
+rav_status mg_set_stream(mg_ctx* m, void* stream) {
+    if (!m) { set_error("NULL ctx"); return RAV_ERR_ARG; }
+    if (m->stream != as_stream(stream)) m->cyc.reset();
+    m->stream = as_stream(stream);
+    for (auto& L : m->lv)
+        if (L.sm) rav_set_stream(L.sm, stream);
+    return RAV_OK;
+}
+
+}  // extern "C"
+
+namespace rav {
+
+// V-cycle on level l (Fig. 1): x and b are the level's iterate / rhs
+static rav_status vcycle_launches(mg_ctx* m, int l, double* x, const double* b, int pre, int post, double omega) {
+    cudaStream_t s = m->stream;
+    if (l == 0) return launch_coarse_solve(m->C, b, x, s);
+    mg_level& L = m->lv[l];
+    mg_level& Lc = m->lv[l - 1];
+    RAV_TRY(smooth_launches(L.sm, x, b, pre, omega));
+    RAV_TRY(launch_residual(L.A, x, b, L.r, s));
+    RAV_TRY(launch_spmv(L.PT, L.r, Lc.b, 1.0, 0.0, s));       // b_{l-1} = P^T r_l
+    if (l - 1 > 0) RAV_CUDA(cudaMemsetAsync(Lc.x, 0, sizeof(double) * Lc.A.n_rows, s));
+    RAV_TRY(vcycle_launches(m, l - 1, Lc.x, Lc.b, pre, post, omega));
+    RAV_TRY(launch_spmv(L.P, Lc.x, x, 1.0, 1.0, s));          // x_l += P x_{l-1}
+    RAV_TRY(smooth_launches(L.sm, x, b, post, omega));
+    return RAV_OK;
+}
+
+static rav_status cycle_and_norm(mg_ctx* m, double* x, const double* b, int pre, int post, double omega) {
+    RAV_TRY(vcycle_launches(m, m->L - 1, x, b, pre, post, omega));
+    mg_level& F = m->lv[m->L - 1];
+    RAV_TRY(launch_residual_norm2(F.A, x, b, m->part, residual_norm_blocks(), m->norm2, m->stream));
+    RAV_CUDA(cudaMemcpyAsync(m->h_norm2, m->norm2, sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+    return RAV_OK;
+}
+
+}  // namespace rav
+
+extern "C" {
+
+rav_status mg_vcycle(mg_ctx* m, double* x, const double* b, int pre, int post, double omega) {
+    if (!m || !x || !b || pre < 0 || post < 0) { set_error("mg_vcycle: bad argument"); return RAV_ERR_ARG; }
+    g_launches = 0;
+    if (m->L == 1) {
+        RAV_TRY(launch_coarse_solve(m->C, b, x, m->stream));
+        m->last_launches = g_launches;
+        return RAV_OK;
+    }
+    RAV_TRY(vcycle_launches(m, m->L - 1, x, b, pre, post, omega));
+    m->last_launches = g_launches;
+    return RAV_OK;
+}
+
+rav_status mg_solve(mg_ctx* m, double* x, const double* b, int pre, int post, double omega, double rtol, int maxit,
+                    int* iters, double* hist) {
+    if (!m || !x || !b || maxit < 0 || pre < 0 || post < 0) { set_error("mg_solve: bad argument"); return RAV_ERR_ARG; }
+    g_launches = 0;
+    int64_t total = 0;
+    mg_level& F = m->lv[m->L - 1];
+    const int64_t n = F.A.n_rows;
+    bool dx = is_device_ptr(x), db = is_device_ptr(b);
+    if (dx != db) { set_error("mg_solve: x and b must both be device or both host pointers"); return RAV_ERR_ARG; }
+    double* X = x;
+    const double* B = b;
+    cudaStream_t s = m->stream;
+    if (!dx) {
+        if (!m->hx) {
+            RAV_CUDA(cudaMalloc(&m->hx, sizeof(double) * n));
+            RAV_CUDA(cudaMalloc(&m->hb, sizeof(double) * n));
+        }
+        RAV_CUDA(cudaMemcpyAsync(m->hx, x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        RAV_CUDA(cudaMemcpyAsync(m->hb, b, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        X = m->hx;
+        B = m->hb;
+    }
+    RAV_TRY(launch_residual_norm2(F.A, X, B, m->part, residual_norm_blocks(), m->norm2, s));
+    RAV_CUDA(cudaMemcpyAsync(m->h_norm2, m->norm2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    RAV_CUDA(cudaStreamSynchronize(s));
+    total += g_launches;
+    double r0 = sqrt(*m->h_norm2);
+    if (hist) hist[0] = r0;
+    int k = 0;
+    rav_status st = RAV_OK;
+    if (!(r0 == r0) || isinf(r0)) st = RAV_ERR_DIVERGED;
+    bool use_graph = s != nullptr && m->L > 1;
+    while (st == RAV_OK && r0 > 0.0 && k < maxit) {
+        int64_t launches = 0;
+        st = run_graph(m->cyc, s, use_graph, X, B, pre, post, 0, omega, launches,
+                       [&]() { return cycle_and_norm(m, X, B, pre, post, omega); });
+        if (st != RAV_OK) break;
+        total += launches;
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) { set_error("mg_solve: %s", cudaGetErrorString(e)); st = RAV_ERR_CUDA; break; }
+        double rk = sqrt(*m->h_norm2);
+        ++k;
+        if (hist) hist[k] = rk;
+        if (!(rk == rk) || isinf(rk)) { set_error("mg_solve: residual is not finite at cycle %d", k); st = RAV_ERR_DIVERGED; break; }
+        if (rk <= rtol * r0) break;
+    }
+    if (iters) *iters = k;
+    if (!dx && st == RAV_OK) {
+        RAV_CUDA(cudaMemcpyAsync(x, m->hx, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        RAV_CUDA(cudaStreamSynchronize(s));
+    }
+    m->last_launches = total;
+    return st;
+}
+
+int64_t mg_last_launches(const mg_ctx* m) { return m ? m->last_launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,690 @@
+// gen.cu -- device-side generator of the structured Taylor-Hood Q2-Q1 Stokes
+// levels (SURVEY section 8 rows a1 "level operators", a3 "patch builder", a7
+// "transfers").  Row-parallel, deterministic assembly: every CSR entry is
+// computed by the thread owning its row as a sum over the elements shared by
+// its row and column DoFs (Eq. 7) -- no atomics, no COO sort, and
+// entries (i,j) and (j,i) are produced by the same arithmetic in the same
+// order, so L = L^T bitwise.
+#include <cub/cub.cuh>
+#include <math_constants.h>
+
+#include "common.cuh"
+#include "internal.cuh"
+
+namespace rav {
+namespace gen {
+
+// 3-point Gauss rule on [0,1] (R7)
+__constant__ double c_gt[3];
+__constant__ double c_gw[3];
+
+struct Grid {
+    int dim;
+    int n[3];        // cells per axis
+    double h[3];
+    double vol;      // prod h
+    int kind;
+    int eta_mode;
+    double eta0;
+    int nm;
+    double amp[8];
+    int mode[8][3];
+    double phase[8][3];
+    double gmin, gmax;
+    int64_t nfree, nvel, nvert, ndof, nel;
+};
+
+static Grid make_grid(const rav_grid* g) {
+    Grid G{};
+    G.dim = g->dim;
+    G.vol = 1.0;
+    G.nfree = 1;
+    G.nvert = 1;
+    G.nel = 1;
+    for (int k = 0; k < 3; ++k) {
+        G.n[k] = k < g->dim ? g->ncell[k] : 1;
+        G.h[k] = k < g->dim ? g->len[k] / g->ncell[k] : 1.0;
+    }
+    for (int k = 0; k < g->dim; ++k) {
+        G.vol *= G.h[k];
+        G.nfree *= (int64_t)(2 * G.n[k] - 1);
+        G.nvert *= (int64_t)(G.n[k] + 1);
+        G.nel *= G.n[k];
+    }
+    G.kind = g->kind;
+    G.eta_mode = g->eta_mode;
+    G.eta0 = g->eta0;
+    G.nm = g->n_modes;
+    for (int m = 0; m < 8; ++m) {
+        G.amp[m] = g->amp[m];
+        for (int k = 0; k < 3; ++k) {
+            G.mode[m][k] = g->mode[m][k];
+            G.phase[m][k] = g->phase[m][k];
+        }
+    }
+    G.gmin = g->gmin;
+    G.gmax = g->gmax;
+    G.nvel = (int64_t)g->dim * G.nfree;
+    G.ndof = G.nvel + G.nvert;
+    return G;
+}
+
+static rav_status check_grid(const rav_grid* g) {
+    if (!g || (g->dim != 2 && g->dim != 3)) { set_error("rav_grid: dim must be 2 or 3"); return RAV_ERR_ARG; }
+    for (int k = 0; k < g->dim; ++k)
+        if (g->ncell[k] < 1 || !(g->len[k] > 0)) { set_error("rav_grid: bad ncell/len"); return RAV_ERR_ARG; }
+    if (g->kind == 1 && g->dim != 2) { set_error("rav_grid: manufactured solution is 2D only"); return RAV_ERR_ARG; }
+    if (g->kind < 0 || g->kind > 2) { set_error("rav_grid: bad kind"); return RAV_ERR_ARG; }
+    if (g->n_modes < 0 || g->n_modes > 8) { set_error("rav_grid: n_modes > 8"); return RAV_ERR_ARG; }
+    if (g->eta_mode == 1 && !(g->gmax > g->gmin)) { set_error("rav_grid: gmax <= gmin"); return RAV_ERR_ARG; }
+    return RAV_OK;
+}
+
+static void upload_rule(cudaStream_t s) {
+    static bool done = false;
+    if (done) return;
+    const double a = 0.5 * 0.77459666924148337704;  // sqrt(3/5)/2
+    double t[3] = {0.5 - a, 0.5, 0.5 + a};
+    double w[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
+    cudaMemcpyToSymbol(c_gt, t, sizeof(t));
+    cudaMemcpyToSymbol(c_gw, w, sizeof(w));
+    done = true;
+    (void)s;
+}
+
+// ---- 1D bases -------------------------------------------------------------------
+__device__ __forceinline__ double q2v(int l, double t) {
+    return l == 0 ? (2.0 * t - 1.0) * (t - 1.0) : (l == 1 ? 4.0 * t * (1.0 - t) : t * (2.0 * t - 1.0));
+}
+__device__ __forceinline__ double q2d(int l, double t) {
+    return l == 0 ? 4.0 * t - 3.0 : (l == 1 ? 4.0 - 8.0 * t : 4.0 * t - 1.0);
+}
+__device__ __forceinline__ double q1v(int m, double t) { return m == 0 ? 1.0 - t : t; }
+
+// ---- lattice helpers --------------------------------------------------------------
+__device__ __forceinline__ int64_t free_id(const Grid& G, const int* a) {
+    int64_t id = 0, s = 1;
+    for (int k = 0; k < G.dim; ++k) {
+        int m = 2 * G.n[k];
+        if (a[k] <= 0 || a[k] >= m) return -1;
+        id += (int64_t)(a[k] - 1) * s;
+        s *= (m - 1);
+    }
+    return id;
+}
+__device__ __forceinline__ int64_t vert_id(const Grid& G, const int* v) {
+    int64_t id = 0, s = 1;
+    for (int k = 0; k < G.dim; ++k) { id += (int64_t)v[k] * s; s *= (G.n[k] + 1); }
+    return id;
+}
+__device__ __forceinline__ int64_t elem_id(const Grid& G, const int* e) {
+    int64_t id = 0, s = 1;
+    for (int k = 0; k < G.dim; ++k) { id += (int64_t)e[k] * s; s *= G.n[k]; }
+    return id;
+}
+// range of elements along one axis containing lattice node index a
+__device__ __forceinline__ void node_elems(int a, int n, int& lo, int& hi) {
+    if (a & 1) { lo = hi = (a - 1) >> 1; }
+    else { lo = (a >> 1) - 1; hi = a >> 1; }
+    if (lo < 0) lo = 0;
+    if (hi > n - 1) hi = n - 1;
+}
+__device__ __forceinline__ void vert_elems(int v, int n, int& lo, int& hi) {
+    lo = v - 1 < 0 ? 0 : v - 1;
+    hi = v > n - 1 ? n - 1 : v;
+}
+
+// Dirichlet data (R8): cavity lid u = e_x on the interior of the top face
+__device__ __forceinline__ double dirichlet(const Grid& G, const int* a, int c) {
+    if (G.kind != 0 || c != 0) return 0.0;
+    int top = G.dim - 1;
+    if (a[top] != 2 * G.n[top]) return 0.0;
+    for (int k = 0; k < top; ++k)
+        if (a[k] <= 0 || a[k] >= 2 * G.n[k]) return 0.0;
+    return 1.0;
+}
+
+// ---- coefficient tables at quadrature points (R12, R13) -------------------------------
+__device__ void eta_grad(const Grid& G, const double* x, double& eta, double* ge) {
+    ge[0] = ge[1] = ge[2] = 0.0;
+    if (G.eta_mode == 0) { eta = G.eta0; return; }
+    double g = 0.0, dg[3] = {0.0, 0.0, 0.0};
+    for (int m = 0; m < G.nm; ++m) {
+        double cs[3] = {1.0, 1.0, 1.0}, sn[3] = {0.0, 0.0, 0.0};
+        for (int k = 0; k < G.dim; ++k) sincos(CUDART_PI * G.mode[m][k] * x[k] + G.phase[m][k], &sn[k], &cs[k]);
+        double p = G.amp[m];
+        for (int k = 0; k < G.dim; ++k) p *= cs[k];
+        g += p;
+        for (int k = 0; k < G.dim; ++k) {
+            double t = -G.amp[m] * CUDART_PI * G.mode[m][k] * sn[k];
+            for (int j = 0; j < G.dim; ++j) if (j != k) t *= cs[j];
+            dg[k] += t;
+        }
+    }
+    double sc = log(100.0) / (G.gmax - G.gmin);
+    eta = exp(log(0.1) + (g - G.gmin) * sc);
+    for (int k = 0; k < G.dim; ++k) ge[k] = eta * sc * dg[k];
+}
+
+// f = -div(eta grad u) + grad p for u = curl(sin^2 pi x sin^2 pi y), p = cos pi x cos pi y
+__device__ void mms_force(const Grid& G, const double* x, double* f) {
+    const double pi = CUDART_PI;
+    double eta, ge[3];
+    eta_grad(G, x, eta, ge);
+    double sx, cx, sy, cy, s2x, c2x, s2y, c2y;
+    sincos(pi * x[0], &sx, &cx);
+    sincos(pi * x[1], &sy, &cy);
+    sincos(2.0 * pi * x[0], &s2x, &c2x);
+    sincos(2.0 * pi * x[1], &s2y, &c2y);
+    const double pi2 = pi * pi, pi3 = pi2 * pi;
+    // u0 = pi sx^2 s2y ; u1 = -pi s2x sy^2
+    double u0x = pi2 * s2x * s2y, u0y = 2.0 * pi2 * sx * sx * c2y;
+    double lap0 = 2.0 * pi3 * c2x * s2y - 4.0 * pi3 * sx * sx * s2y;
+    double u1x = -2.0 * pi2 * c2x * sy * sy, u1y = -pi2 * s2x * s2y;
+    double lap1 = 4.0 * pi3 * s2x * sy * sy - 2.0 * pi3 * s2x * c2y;
+    f[0] = -eta * lap0 - (ge[0] * u0x + ge[1] * u0y) - pi * sx * cy;
+    f[1] = -eta * lap1 - (ge[0] * u1x + ge[1] * u1y) - pi * cx * sy;
+}
+
+// one thread per (element, quadrature point): eta and (MMS) f
+__global__ void coef_kernel(Grid G, double* eta_tab, double* f_tab) {
+    const int NG = G.dim == 2 ? 9 : 27;
+    int64_t total = G.nel * NG;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t el = t / NG;
+        int q = (int)(t % NG);
+        int e[3] = {0, 0, 0};
+        int64_t r = el;
+        for (int k = 0; k < G.dim; ++k) { e[k] = (int)(r % G.n[k]); r /= G.n[k]; }
+        double x[3] = {0, 0, 0};
+        int qq = q;
+        for (int k = 0; k < G.dim; ++k) { x[k] = (e[k] + c_gt[qq % 3]) * G.h[k]; qq /= 3; }
+        double eta, ge[3];
+        eta_grad(G, x, eta, ge);
+        eta_tab[t] = eta;
+        if (f_tab) {
+            double f[3] = {0.0, 0.0, 0.0};
+            if (G.kind == 1) mms_force(G, x, f);
+            f_tab[2 * t] = f[0];
+            f_tab[2 * t + 1] = f[1];
+        }
+    }
+}
+
+// ---- entry formulas -------------------------------------------------------------------
+// int_e eta grad phi_a . grad phi_b over the elements shared by nodes a and b
+__device__ double a_entry(const Grid& G, const double* eta_tab, const int* a, const int* b) {
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int k = 0; k < G.dim; ++k) {
+        int la, ha, lb, hb;
+        node_elems(a[k], G.n[k], la, ha);
+        node_elems(b[k], G.n[k], lb, hb);
+        lo[k] = max(la, lb);
+        hi[k] = min(ha, hb);
+        if (lo[k] > hi[k]) return 0.0;
+    }
+    const int NG = G.dim == 2 ? 9 : 27;
+    double s = 0.0;
+    int e[3] = {0, 0, 0};
+    for (e[2] = lo[2]; e[2] <= hi[2]; ++e[2])
+        for (e[1] = lo[1]; e[1] <= hi[1]; ++e[1])
+            for (e[0] = lo[0]; e[0] <= hi[0]; ++e[0]) {
+                int la[3], lb[3];
+                for (int k = 0; k < 3; ++k) { la[k] = a[k] - 2 * e[k]; lb[k] = b[k] - 2 * e[k]; }
+                const double* et = eta_tab + elem_id(G, e) * NG;
+                for (int q = 0; q < NG; ++q) {
+                    int qk[3] = {q % 3, (q / 3) % 3, q / 9};
+                    double va[3], vb[3], da[3], db[3], w = G.vol;
+                    for (int k = 0; k < G.dim; ++k) {
+                        double t = c_gt[qk[k]];
+                        w *= c_gw[qk[k]];
+                        va[k] = q2v(la[k], t); vb[k] = q2v(lb[k], t);
+                        da[k] = q2d(la[k], t) / G.h[k]; db[k] = q2d(lb[k], t) / G.h[k];
+                    }
+                    double dot = 0.0;
+                    for (int k = 0; k < G.dim; ++k) {
+                        double ga = da[k], gb = db[k];
+                        for (int j = 0; j < G.dim; ++j) if (j != k) { ga *= va[j]; gb *= vb[j]; }
+                        dot += ga * gb;
+                    }
+                    s += (w * et[q]) * dot;
+                }
+            }
+    return s;
+}
+
+// -int_e psi_v d_c phi_b over the elements shared by node b and vertex v
+__device__ double b_entry(const Grid& G, const int* b, int c, const int* v) {
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int k = 0; k < G.dim; ++k) {
+        int lb, hb, lv, hv;
+        node_elems(b[k], G.n[k], lb, hb);
+        vert_elems(v[k], G.n[k], lv, hv);
+        lo[k] = max(lb, lv);
+        hi[k] = min(hb, hv);
+        if (lo[k] > hi[k]) return 0.0;
+    }
+    const int NG = G.dim == 2 ? 9 : 27;
+    double s = 0.0;
+    int e[3] = {0, 0, 0};
+    for (e[2] = lo[2]; e[2] <= hi[2]; ++e[2])
+        for (e[1] = lo[1]; e[1] <= hi[1]; ++e[1])
+            for (e[0] = lo[0]; e[0] <= hi[0]; ++e[0]) {
+                int lb[3], lm[3];
+                for (int k = 0; k < 3; ++k) { lb[k] = b[k] - 2 * e[k]; lm[k] = v[k] - e[k]; }
+                for (int q = 0; q < NG; ++q) {
+                    int qk[3] = {q % 3, (q / 3) % 3, q / 9};
+                    double w = G.vol, psi = 1.0, dphi = 1.0;
+                    for (int k = 0; k < G.dim; ++k) {
+                        double t = c_gt[qk[k]];
+                        w *= c_gw[qk[k]];
+                        psi *= q1v(lm[k], t);
+                        dphi *= (k == c) ? q2d(lb[k], t) / G.h[k] : q2v(lb[k], t);
+                    }
+                    s -= (w * psi) * dphi;
+                }
+            }
+    return s;
+}
+
+// int f_c phi_a over the elements containing node a (2D manufactured forcing)
+__device__ double f_entry(const Grid& G, const double* f_tab, const int* a, int c) {
+    if (G.kind != 1) return 0.0;
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int k = 0; k < G.dim; ++k) node_elems(a[k], G.n[k], lo[k], hi[k]);
+    const int NG = 9;
+    double s = 0.0;
+    int e[3] = {0, 0, 0};
+    for (e[1] = lo[1]; e[1] <= hi[1]; ++e[1])
+        for (e[0] = lo[0]; e[0] <= hi[0]; ++e[0]) {
+            int la[2] = {a[0] - 2 * e[0], a[1] - 2 * e[1]};
+            int64_t el = elem_id(G, e);
+            for (int q = 0; q < NG; ++q) {
+                double t0 = c_gt[q % 3], t1 = c_gt[q / 3];
+                double w = G.vol * c_gw[q % 3] * c_gw[q / 3];
+                s += (w * f_tab[2 * (el * NG + q) + c]) * (q2v(la[0], t0) * q2v(la[1], t1));
+            }
+        }
+    return s;
+}
+
+// ---- row decoding -----------------------------------------------------------------------
+__device__ __forceinline__ void decode_vel_row(const Grid& G, int64_t row, int* a, int& c) {
+    int64_t fi = row / G.dim;
+    c = (int)(row % G.dim);
+    a[0] = a[1] = a[2] = 0;
+    for (int k = 0; k < G.dim; ++k) {
+        int m = 2 * G.n[k] - 1;
+        a[k] = (int)(fi % m) + 1;
+        fi /= m;
+    }
+}
+__device__ __forceinline__ void decode_vertex(const Grid& G, int64_t vi, int* v) {
+    v[0] = v[1] = v[2] = 0;
+    for (int k = 0; k < G.dim; ++k) { v[k] = (int)(vi % (G.n[k] + 1)); vi /= (G.n[k] + 1); }
+}
+
+// ---- operator: count / fill ---------------------------------------------------------------
+// Row pattern (structural, R2): velocity row (a, c): same-component velocity DoFs of
+// the nodes of all elements containing a, then the pressure DoFs of their vertices;
+// pressure row v: all velocity DoFs of the nodes of the elements containing v.
+__global__ void op_count_kernel(Grid G, int64_t* cnt) {
+    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < G.ndof;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, a[3], c = 0;
+        bool vel = row < G.nvel;
+        if (vel) {
+            decode_vel_row(G, row, a, c);
+            for (int k = 0; k < G.dim; ++k) node_elems(a[k], G.n[k], lo[k], hi[k]);
+        } else {
+            decode_vertex(G, row - G.nvel, a);
+            for (int k = 0; k < G.dim; ++k) vert_elems(a[k], G.n[k], lo[k], hi[k]);
+        }
+        int64_t nodes = 1, verts = 1;
+        for (int k = 0; k < G.dim; ++k) {
+            // free lattice nodes in [2lo, 2hi+2] intersected with [1, 2n-1]
+            int l = max(2 * lo[k], 1), h = min(2 * hi[k] + 2, 2 * G.n[k] - 1);
+            nodes *= (h - l + 1);
+            verts *= (hi[k] - lo[k] + 2);
+        }
+        cnt[row] = vel ? nodes + verts : nodes * G.dim;
+    }
+}
+
+__global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_tab, const int64_t* rp,
+                               int32_t* col, double* val, double* rhs) {
+    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < G.ndof;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = rp[row];
+        int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, a[3] = {0, 0, 0}, c = 0;
+        bool vel = row < G.nvel;
+        if (vel) {
+            decode_vel_row(G, row, a, c);
+            for (int k = 0; k < G.dim; ++k) node_elems(a[k], G.n[k], lo[k], hi[k]);
+        } else {
+            decode_vertex(G, row - G.nvel, a);
+            for (int k = 0; k < G.dim; ++k) vert_elems(a[k], G.n[k], lo[k], hi[k]);
+        }
+        double lift = 0.0;
+        int bl[3] = {0, 0, 0}, bh[3] = {0, 0, 0};
+        for (int k = 0; k < G.dim; ++k) { bl[k] = 2 * lo[k]; bh[k] = 2 * hi[k] + 2; }
+        int b[3] = {0, 0, 0};
+        for (b[2] = bl[2]; b[2] <= bh[2]; ++b[2])
+            for (b[1] = bl[1]; b[1] <= bh[1]; ++b[1])
+                for (b[0] = bl[0]; b[0] <= bh[0]; ++b[0]) {
+                    int64_t fb = free_id(G, b);
+                    if (vel) {
+                        if (fb >= 0) {
+                            col[p] = (int32_t)(fb * G.dim + c);
+                            val[p] = a_entry(G, eta_tab, a, b);
+                            ++p;
+                        } else {
+                            double ud = dirichlet(G, b, c);
+                            if (ud != 0.0) lift -= a_entry(G, eta_tab, a, b) * ud;
+                        }
+                    } else {
+                        for (int cc = 0; cc < G.dim; ++cc) {
+                            if (fb >= 0) {
+                                col[p] = (int32_t)(fb * G.dim + cc);
+                                val[p] = b_entry(G, b, cc, a);
+                                ++p;
+                            } else {
+                                double ud = dirichlet(G, b, cc);
+                                if (ud != 0.0) lift -= b_entry(G, b, cc, a) * ud;
+                            }
+                        }
+                    }
+                }
+        if (vel) {
+            int v[3] = {0, 0, 0};
+            for (v[2] = lo[2]; v[2] <= (G.dim > 2 ? hi[2] + 1 : 0); ++v[2])
+                for (v[1] = lo[1]; v[1] <= hi[1] + 1; ++v[1])
+                    for (v[0] = lo[0]; v[0] <= hi[0] + 1; ++v[0]) {
+                        col[p] = (int32_t)(G.nvel + vert_id(G, v));
+                        val[p] = b_entry(G, a, c, v);
+                        ++p;
+                    }
+            rhs[row] = f_entry(G, f_tab, a, c) + lift;
+        } else {
+            rhs[row] = lift;
+        }
+    }
+}
+
+// ---- patches -------------------------------------------------------------------
+__device__ __forceinline__ double patch_weight(int mode, int dim, const int* a, const int* v) {
+    if (mode == 2) return 1.0;
+    double w = 1.0;
+    for (int k = 0; k < dim; ++k) {
+        int off = a[k] - 2 * v[k];
+        if (mode == 0) {
+            if (off < -1 || off > 1) return 0.0;
+            if (off != 0) w *= 0.5;
+        } else if (off != 0 && off != 1) {
+            return 0.0;
+        }
+    }
+    return w;
+}
+
+__global__ void patch_count_kernel(Grid G, int64_t* cnt) {
+    for (int64_t vi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vi < G.nvert;
+         vi += (int64_t)gridDim.x * blockDim.x) {
+        int v[3];
+        decode_vertex(G, vi, v);
+        int64_t nodes = 1;
+        for (int k = 0; k < G.dim; ++k) {
+            int l = max(2 * v[k] - 2, 1), h = min(2 * v[k] + 2, 2 * G.n[k] - 1);
+            nodes *= (h - l + 1);
+        }
+        cnt[vi] = nodes * G.dim + 1;
+    }
+}
+
+__global__ void patch_fill_kernel(Grid G, int mode, const int64_t* offs, int32_t* dofs, double* w) {
+    for (int64_t vi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vi < G.nvert;
+         vi += (int64_t)gridDim.x * blockDim.x) {
+        int v[3];
+        decode_vertex(G, vi, v);
+        int l[3] = {0, 0, 0}, h[3] = {0, 0, 0};
+        for (int k = 0; k < G.dim; ++k) { l[k] = max(2 * v[k] - 2, 1); h[k] = min(2 * v[k] + 2, 2 * G.n[k] - 1); }
+        int64_t p = offs[vi];
+        for (int pass = 0; pass < 2; ++pass) {
+            if (pass == 1) { dofs[p] = (int32_t)(G.nvel + vi); w[p] = 1.0; ++p; }
+            int a[3] = {0, 0, 0};
+            for (a[2] = l[2]; a[2] <= h[2]; ++a[2])
+                for (a[1] = l[1]; a[1] <= h[1]; ++a[1])
+                    for (a[0] = l[0]; a[0] <= h[0]; ++a[0]) {
+                        double wt = patch_weight(mode, G.dim, a, v);
+                        if ((pass == 0) != (wt > 0.0)) continue;
+                        int64_t fa = free_id(G, a);
+                        for (int c = 0; c < G.dim; ++c) {
+                            dofs[p] = (int32_t)(fa * G.dim + c);
+                            w[p] = wt;
+                            ++p;
+                        }
+                    }
+        }
+    }
+}
+
+// ---- prolongation ------------------------------------------------------------------------
+__device__ __forceinline__ int interp_q2(int af, int nc, int* idx, double* wt) {
+    if (!(af & 1)) { idx[0] = af >> 1; wt[0] = 1.0; return 1; }
+    int e = af >> 2;
+    if (e > nc - 1) e = nc - 1;
+    double t = (af - 4.0 * e) * 0.25;
+    for (int i = 0; i < 3; ++i) { idx[i] = 2 * e + i; wt[i] = q2v(i, t); }
+    return 3;
+}
+__device__ __forceinline__ int interp_q1(int bf, int* idx, double* wt) {
+    if (!(bf & 1)) { idx[0] = bf >> 1; wt[0] = 1.0; return 1; }
+    idx[0] = (bf - 1) >> 1; wt[0] = 0.5;
+    idx[1] = (bf + 1) >> 1; wt[1] = 0.5;
+    return 2;
+}
+
+template <bool FILL>
+__global__ void prol_kernel(Grid F, Grid Cg, int64_t* cnt_or_rp, int32_t* ci, double* val) {
+    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < F.ndof;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        int idx[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        double wt[3][3] = {{1, 0, 0}, {1, 0, 0}, {1, 0, 0}};
+        int cnt[3] = {1, 1, 1};
+        int comp = -1;
+        if (row < F.nvel) {
+            int a[3];
+            decode_vel_row(F, row, a, comp);
+            for (int k = 0; k < F.dim; ++k) cnt[k] = interp_q2(a[k], Cg.n[k], idx[k], wt[k]);
+        } else {
+            int v[3];
+            decode_vertex(F, row - F.nvel, v);
+            for (int k = 0; k < F.dim; ++k) cnt[k] = interp_q1(v[k], idx[k], wt[k]);
+        }
+        int64_t p = FILL ? cnt_or_rp[row] : 0;
+        int64_t c = 0;
+        for (int s2 = 0; s2 < cnt[2]; ++s2)
+            for (int s1 = 0; s1 < cnt[1]; ++s1)
+                for (int s0 = 0; s0 < cnt[0]; ++s0) {
+                    int a[3] = {idx[0][s0], idx[1][s1], F.dim > 2 ? idx[2][s2] : 0};
+                    double w = wt[0][s0] * wt[1][s1];
+                    if (F.dim > 2) w *= wt[2][s2];
+                    int64_t colid;
+                    if (comp >= 0) {
+                        int64_t fc = free_id(Cg, a);
+                        if (fc < 0) continue;
+                        colid = fc * F.dim + comp;
+                    } else {
+                        colid = Cg.nvel + vert_id(Cg, a);
+                    }
+                    if (FILL) { ci[p + c] = (int32_t)colid; val[p + c] = w; }
+                    ++c;
+                }
+        if (!FILL) cnt_or_rp[row] = c;
+    }
+}
+
+// ---- scan helper: rp[0] = 0, rp[i+1] = sum cnt[0..i] -------------------------------------------
+rav_status counts_to_rowptr(const int64_t* cnt, int64_t* rp, int64_t n, cudaStream_t s) {
+    RAV_CUDA(cudaMemsetAsync(rp, 0, sizeof(int64_t), s));
+    size_t tmp = 0;
+    RAV_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, cnt, rp + 1, n, s));
+    void* d_tmp = nullptr;
+    RAV_CUDA(cudaMallocAsync(&d_tmp, tmp > 0 ? tmp : 1, s));
+    cudaError_t e = cub::DeviceScan::InclusiveSum(d_tmp, tmp, cnt, rp + 1, n, s);
+    cudaFreeAsync(d_tmp, s);
+    RAV_CUDA(e);
+    return RAV_OK;
+}
+
+static int grid_for(int64_t n, int bs) {
+    int64_t b = cdiv(n, bs);
+    int64_t cap = (int64_t)num_sms() * 32;
+    return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace gen
+}  // namespace rav
+
+using namespace rav;
+using namespace rav::gen;
+
+extern "C" rav_status rav_gen_sizes(const rav_grid* g, int weights, void* stream, int64_t* n_dofs,
+                                    int64_t* n_vel, int64_t* nnz, int64_t* n_patches,
+                                    int64_t* patch_entries) {
+    RAV_TRY(check_grid(g));
+    if (weights < 0 || weights > 2) { set_error("rav_gen_sizes: weights must be 0, 1 or 2"); return RAV_ERR_ARG; }
+    Grid G = make_grid(g);
+    cudaStream_t s = as_stream(stream);
+    if (n_dofs) *n_dofs = G.ndof;
+    if (n_vel) *n_vel = G.nvel;
+    if (n_patches) *n_patches = G.nvert;
+    int64_t *cnt = nullptr, *rp = nullptr;
+    int64_t nmax = G.ndof > G.nvert ? G.ndof : G.nvert;
+    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * nmax, s));
+    RAV_CUDA(cudaMallocAsync(&rp, sizeof(int64_t) * (nmax + 1), s));
+    int64_t h_nnz = 0, h_pe = 0;
+    if (nnz) {
+        op_count_kernel<<<grid_for(G.ndof, 256), 256, 0, s>>>(G, cnt);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+        RAV_TRY(counts_to_rowptr(cnt, rp, G.ndof, s));
+        RAV_CUDA(cudaMemcpyAsync(&h_nnz, rp + G.ndof, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    }
+    if (patch_entries) {
+        patch_count_kernel<<<grid_for(G.nvert, 256), 256, 0, s>>>(G, cnt);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+        RAV_TRY(counts_to_rowptr(cnt, rp, G.nvert, s));
+        RAV_CUDA(cudaMemcpyAsync(&h_pe, rp + G.nvert, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    }
+    cudaFreeAsync(cnt, s);
+    cudaFreeAsync(rp, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    if (nnz) *nnz = h_nnz;
+    if (patch_entries) *patch_entries = h_pe;
+    if (h_nnz > INT32_MAX * 4LL) { set_error("nnz too large"); return RAV_ERR_ARG; }
+    if (G.ndof > INT32_MAX) { set_error("n_dofs exceeds int32 column index range"); return RAV_ERR_ARG; }
+    return RAV_OK;
+}
+
+extern "C" rav_status rav_gen_operator(const rav_grid* g, int64_t* row_ptr, int32_t* col, double* val,
+                                       double* rhs, void* stream) {
+    RAV_TRY(check_grid(g));
+    if (!row_ptr || !col || !val || !rhs) { set_error("rav_gen_operator: NULL buffer"); return RAV_ERR_ARG; }
+    Grid G = make_grid(g);
+    cudaStream_t s = as_stream(stream);
+    upload_rule(s);
+    const int NG = G.dim == 2 ? 9 : 27;
+    double *eta_tab = nullptr, *f_tab = nullptr;
+    int64_t* cnt = nullptr;
+    RAV_CUDA(cudaMallocAsync(&eta_tab, sizeof(double) * G.nel * NG, s));
+    if (G.kind == 1) RAV_CUDA(cudaMallocAsync(&f_tab, sizeof(double) * G.nel * NG * 2, s));
+    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * G.ndof, s));
+    coef_kernel<<<grid_for(G.nel * NG, 256), 256, 0, s>>>(G, eta_tab, f_tab);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    op_count_kernel<<<grid_for(G.ndof, 256), 256, 0, s>>>(G, cnt);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    RAV_TRY(counts_to_rowptr(cnt, row_ptr, G.ndof, s));
+    op_fill_kernel<<<grid_for(G.ndof, 128), 128, 0, s>>>(G, eta_tab, f_tab, row_ptr, col, val, rhs);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    cudaFreeAsync(eta_tab, s);
+    if (f_tab) cudaFreeAsync(f_tab, s);
+    cudaFreeAsync(cnt, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    return RAV_OK;
+}
+
+extern "C" rav_status rav_gen_patches(const rav_grid* g, int weights, int64_t* offs, int32_t* dofs,
+                                      double* w, void* stream) {
+    RAV_TRY(check_grid(g));
+    if (weights < 0 || weights > 2) { set_error("rav_gen_patches: weights must be 0, 1 or 2"); return RAV_ERR_ARG; }
+    if (!offs || !dofs || !w) { set_error("rav_gen_patches: NULL buffer"); return RAV_ERR_ARG; }
+    Grid G = make_grid(g);
+    cudaStream_t s = as_stream(stream);
+    int64_t* cnt = nullptr;
+    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * G.nvert, s));
+    patch_count_kernel<<<grid_for(G.nvert, 256), 256, 0, s>>>(G, cnt);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    RAV_TRY(counts_to_rowptr(cnt, offs, G.nvert, s));
+    patch_fill_kernel<<<grid_for(G.nvert, 128), 128, 0, s>>>(G, weights, offs, dofs, w);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    cudaFreeAsync(cnt, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    return RAV_OK;
+}
+
+static rav_status check_nested(const rav_grid* f, const rav_grid* c) {
+    RAV_TRY(check_grid(f));
+    RAV_TRY(check_grid(c));
+    if (f->dim != c->dim) { set_error("prolongation: dim mismatch"); return RAV_ERR_ARG; }
+    for (int k = 0; k < f->dim; ++k)
+        if (f->ncell[k] != 2 * c->ncell[k]) { set_error("prolongation: fine ncell must be 2 x coarse"); return RAV_ERR_ARG; }
+    return RAV_OK;
+}
+
+extern "C" rav_status rav_gen_prolongation_nnz(const rav_grid* fine, const rav_grid* coarse, void* stream,
+                                               int64_t* nnz) {
+    RAV_TRY(check_nested(fine, coarse));
+    Grid F = make_grid(fine), Cg = make_grid(coarse);
+    cudaStream_t s = as_stream(stream);
+    int64_t *cnt = nullptr, *rp = nullptr;
+    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * F.ndof, s));
+    RAV_CUDA(cudaMallocAsync(&rp, sizeof(int64_t) * (F.ndof + 1), s));
+    prol_kernel<false><<<grid_for(F.ndof, 256), 256, 0, s>>>(F, Cg, cnt, nullptr, nullptr);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    RAV_TRY(counts_to_rowptr(cnt, rp, F.ndof, s));
+    int64_t h = 0;
+    RAV_CUDA(cudaMemcpyAsync(&h, rp + F.ndof, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(cnt, s);
+    cudaFreeAsync(rp, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    *nnz = h;
+    return RAV_OK;
+}
+
+extern "C" rav_status rav_gen_prolongation(const rav_grid* fine, const rav_grid* coarse, int64_t* rp,
+                                           int32_t* ci, double* val, void* stream) {
+    RAV_TRY(check_nested(fine, coarse));
+    Grid F = make_grid(fine), Cg = make_grid(coarse);
+    cudaStream_t s = as_stream(stream);
+    int64_t* cnt = nullptr;
+    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * F.ndof, s));
+    prol_kernel<false><<<grid_for(F.ndof, 256), 256, 0, s>>>(F, Cg, cnt, nullptr, nullptr);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    RAV_TRY(counts_to_rowptr(cnt, rp, F.ndof, s));
+    prol_kernel<true><<<grid_for(F.ndof, 256), 256, 0, s>>>(F, Cg, rp, ci, val);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    cudaFreeAsync(cnt, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    return RAV_OK;
+}

@@ -1,0 +1,82 @@
+// internal.cuh -- launchers shared between the translation units of libravgmg.
+#pragma once
+#include "common.cuh"
+
+namespace rav {
+
+namespace gen {
+rav_status counts_to_rowptr(const int64_t* cnt, int64_t* rp, int64_t n, cudaStream_t s);
+}
+
+// ---- linalg.cu ------------------------------------------------------------------------
+struct Csr {
+    int64_t n_rows = 0, n_cols = 0, nnz = 0;
+    int64_t* rp = nullptr;
+    int32_t* ci = nullptr;
+    double* val = nullptr;
+    int lanes = 8;  // lanes per row used by the SpMV kernels
+};
+
+rav_status csr_upload(const rav_csr* A, Csr& out, cudaStream_t s);
+void csr_free(Csr& A);
+rav_status csr_transpose(const Csr& A, Csr& At, cudaStream_t s);
+
+// r = b - A x
+rav_status launch_residual(const Csr& A, const double* x, const double* b, double* r, cudaStream_t s);
+// y = alpha * A x + beta * y
+rav_status launch_spmv(const Csr& A, const double* x, double* y, double alpha, double beta, cudaStream_t s);
+// partial sums of squares of (b - A x) into part[nblk]; then total into *out (device)
+rav_status launch_residual_norm2(const Csr& A, const double* x, const double* b, double* part, int nblk,
+                                 double* out, cudaStream_t s);
+int residual_norm_blocks();
+
+// ---- setup.cu -------------------------------------------------------------------------
+struct PatchSet {
+    int64_t n_patches = 0, entries = 0;
+    int64_t* offs = nullptr;   // device, reordered: restricted first
+    int32_t* dofs = nullptr;
+    double* w = nullptr;
+    int32_t* nres = nullptr;   // restricted count per patch
+    int nmax = 0, nresmax = 0;
+    int64_t rows_total = 0;    // sum nres_i * n_i
+};
+
+struct Factors {
+    int layout = 0;            // 1 general (row-major per patch), 2 thread-per-patch SoA chunks
+    // general
+    int64_t* foffs = nullptr;  // n_patches + 1
+    double* fac = nullptr;
+    // SoA
+    int NT = 0, NMAX = 0;
+    int64_t nchunks = 0;
+    double* facT = nullptr;    // nchunks * (NMAX*NT/2) * 32 double2
+    int32_t* DT = nullptr;     // nchunks * NMAX * 32
+    int32_t* NR = nullptr;     // nchunks * 32 restricted counts (0 for padding)
+    int64_t bytes = 0;
+};
+
+rav_status patches_upload(const rav_patches* P, int64_t n_dofs, PatchSet& out, cudaStream_t s);
+void patches_free(PatchSet& P);
+// factorize all patches; bad_patch = smallest singular patch or -1
+rav_status factorize(const Csr& A, const PatchSet& P, int variant, int64_t nvel, int kernel_choice,
+                     Factors& F, int64_t* bad_patch, cudaStream_t s);
+void factors_free(Factors& F);
+rav_status export_rows(const PatchSet& P, const Factors& F, double* rows, cudaStream_t s);
+bool thread_kernel_supported(int nresmax, int nmax);
+
+// ---- sweep.cu -------------------------------------------------------------------------
+rav_status launch_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
+                        cudaStream_t s);
+
+// ---- coarse.cu ------------------------------------------------------------------------
+struct CoarseLU {
+    int64_t n = 0, pin = -1;
+    int m = 0;
+    double* lu = nullptr;      // m x m
+    int32_t* piv = nullptr;
+};
+rav_status coarse_factor(const Csr& A, int64_t pin, CoarseLU& C, cudaStream_t s);
+rav_status launch_coarse_solve(const CoarseLU& C, const double* b, double* x, cudaStream_t s);
+void coarse_free(CoarseLU& C);
+
+}  // namespace rav

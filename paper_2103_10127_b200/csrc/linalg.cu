@@ -1,0 +1,285 @@
+// linalg.cu -- CSR kernels of the hot path (SURVEY section 8 rows a2 "residual
+// SpMV" and a7 "transfers"): r = b - L x (Eq. 10), y = alpha A x + beta y,
+// deterministic residual norms, CSR upload / transpose.
+//
+// Layout: CSR with int64 row pointers and int32 sorted columns.  A group of G
+// lanes (G = 8 for the ~25-nnz rows of 2D Q2-Q1, 32 for the ~90-375-nnz rows
+// of 3D) owns one row; consecutive groups own consecutive rows, so a warp
+// streams one contiguous range of val/col with no padding.  val/col are read
+// with evict-first streaming loads (they are touched once per sweep); x is
+// read through L1/L2 (it is L2-resident between the sweep and the residual).
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+
+namespace rav {
+
+template <int G>
+__global__ void __launch_bounds__(256) residual_kernel(int64_t n, const int64_t* __restrict__ rp,
+                                                       const int32_t* __restrict__ ci,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ x,
+                                                       const double* __restrict__ b, double* __restrict__ r) {
+    // warp-uniform trip count: every lane reaches the shuffles (rows past n are masked)
+    const int lane = threadIdx.x % G;
+    const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+    const int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
+    const int64_t warp_first = first - (threadIdx.x % 32) / G;
+    for (int64_t base = warp_first; base < n; base += groups) {
+        const int64_t row = base + (threadIdx.x % 32) / G;
+        double acc = 0.0;
+        if (row < n) {
+            const int64_t s = rp[row], e = rp[row + 1];
+            for (int64_t k = s + lane; k < e; k += G) acc += ld_stream(val + k) * __ldg(x + ld_stream_i(ci + k));
+        }
+        acc = group_sum<G>(acc);
+        if (lane == 0 && row < n) r[row] = b[row] - acc;
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int64_t* __restrict__ rp,
+                                                   const int32_t* __restrict__ ci,
+                                                   const double* __restrict__ val,
+                                                   const double* __restrict__ x, double* __restrict__ y,
+                                                   double alpha, double beta) {
+    const int lane = threadIdx.x % G;
+    const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+    const int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
+    const int64_t warp_first = first - (threadIdx.x % 32) / G;
+    for (int64_t base = warp_first; base < n; base += groups) {
+        const int64_t row = base + (threadIdx.x % 32) / G;
+        double acc = 0.0;
+        if (row < n) {
+            const int64_t s = rp[row], e = rp[row + 1];
+            for (int64_t k = s + lane; k < e; k += G) acc += val[k] * __ldg(x + ci[k]);
+        }
+        acc = group_sum<G>(acc);
+        if (lane == 0 && row < n) y[row] = (beta == 0.0 ? 0.0 : beta * y[row]) + alpha * acc;
+    }
+}
+
+// sum of squares of (b - A x) per block (fixed order => deterministic)
+template <int G>
+__global__ void __launch_bounds__(256) resnorm_kernel(int64_t n, const int64_t* __restrict__ rp,
+                                                      const int32_t* __restrict__ ci,
+                                                      const double* __restrict__ val,
+                                                      const double* __restrict__ x,
+                                                      const double* __restrict__ b, double* __restrict__ part) {
+    __shared__ double red[256 / G];
+    const int lane = threadIdx.x % G, grp = threadIdx.x / G;
+    const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+    double mine = 0.0;
+    const int64_t first = (int64_t)blockIdx.x * (blockDim.x / G) + grp;
+    const int64_t warp_first = first - (threadIdx.x % 32) / G;
+    for (int64_t base = warp_first; base < n; base += groups) {
+        const int64_t row = base + (threadIdx.x % 32) / G;
+        double acc = 0.0;
+        if (row < n) {
+            const int64_t s = rp[row], e = rp[row + 1];
+            for (int64_t k = s + lane; k < e; k += G) acc += ld_stream(val + k) * __ldg(x + ld_stream_i(ci + k));
+        }
+        acc = group_sum<G>(acc);
+        if (row < n) {
+            double rr = b[row] - acc;
+            mine += rr * rr;
+        }
+    }
+    if (lane == 0) red[grp] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < 256 / G; ++i) t += red[i];
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void sum_parts_kernel(const double* __restrict__ part, int nblk, double* out) {
+    __shared__ double red[256];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < nblk; i += blockDim.x) t += part[i];
+    red[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = red[0];
+}
+
+static int spmv_blocks(int64_t n, int G) {
+    int64_t rows_per_block = 256 / G;
+    int64_t b = cdiv(n, rows_per_block);
+    int64_t cap = (int64_t)num_sms() * 8;
+    return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+rav_status launch_residual(const Csr& A, const double* x, const double* b, double* r, cudaStream_t s) {
+    if (A.n_rows == 0) return RAV_OK;
+    int nb = spmv_blocks(A.n_rows, A.lanes);
+    if (A.lanes == 32)
+        residual_kernel<32><<<nb, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, b, r);
+    else if (A.lanes == 16)
+        residual_kernel<16><<<nb, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, b, r);
+    else
+        residual_kernel<8><<<nb, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, b, r);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}
+
+rav_status launch_spmv(const Csr& A, const double* x, double* y, double alpha, double beta, cudaStream_t s) {
+    if (A.n_rows == 0) return RAV_OK;
+    int nb = spmv_blocks(A.n_rows, A.lanes);
+    if (A.lanes == 32)
+        spmv_kernel<32><<<nb, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, y, alpha, beta);
+    else if (A.lanes == 16)
+        spmv_kernel<16><<<nb, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, y, alpha, beta);
+    else
+        spmv_kernel<8><<<nb, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, y, alpha, beta);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}
+
+int residual_norm_blocks() { return num_sms() * 4; }
+
+rav_status launch_residual_norm2(const Csr& A, const double* x, const double* b, double* part, int nblk,
+                                 double* out, cudaStream_t s) {
+    if (A.lanes == 32)
+        resnorm_kernel<32><<<nblk, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, b, part);
+    else if (A.lanes == 16)
+        resnorm_kernel<16><<<nblk, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, b, part);
+    else
+        resnorm_kernel<8><<<nblk, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, b, part);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    sum_parts_kernel<<<1, 256, 0, s>>>(part, nblk, out);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+__global__ void row_len_max_kernel(int64_t n, const int64_t* rp, unsigned long long* mx, unsigned long long* sum) {
+    unsigned long long m = 0, t = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long l = (unsigned long long)(rp[i + 1] - rp[i]);
+        m = l > m ? l : m;
+        t += l;
+    }
+    atomicMax(mx, m);
+    (void)sum;
+    (void)t;
+}
+
+rav_status csr_upload(const rav_csr* A, Csr& out, cudaStream_t s) {
+    if (!A || A->n_rows < 0 || !A->row_ptr) { set_error("rav_csr: NULL or negative size"); return RAV_ERR_ARG; }
+    out.n_rows = A->n_rows;
+    out.n_cols = A->n_cols;
+    int64_t nnz = 0;
+    cudaMemcpyKind kind = A->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (A->on_device != is_device_ptr(A->row_ptr)) {
+        set_error("rav_csr: on_device flag does not match the row_ptr pointer kind");
+        return RAV_ERR_ARG;
+    }
+    RAV_CUDA(cudaMemcpyAsync(&nnz, A->row_ptr + A->n_rows, sizeof(int64_t),
+                             A->on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, s));
+    RAV_CUDA(cudaStreamSynchronize(s));
+    if (nnz < 0) { set_error("rav_csr: negative nnz"); return RAV_ERR_ARG; }
+    out.nnz = nnz;
+    RAV_CUDA(cudaMalloc(&out.rp, sizeof(int64_t) * (out.n_rows + 1)));
+    RAV_CUDA(cudaMalloc(&out.ci, sizeof(int32_t) * (nnz > 0 ? nnz : 1)));
+    RAV_CUDA(cudaMalloc(&out.val, sizeof(double) * (nnz > 0 ? nnz : 1)));
+    RAV_CUDA(cudaMemcpyAsync(out.rp, A->row_ptr, sizeof(int64_t) * (out.n_rows + 1), kind, s));
+    if (nnz > 0) {
+        RAV_CUDA(cudaMemcpyAsync(out.ci, A->col, sizeof(int32_t) * nnz, kind, s));
+        RAV_CUDA(cudaMemcpyAsync(out.val, A->val, sizeof(double) * nnz, kind, s));
+    }
+    // lanes per row from the mean row length
+    double mean = out.n_rows > 0 ? (double)nnz / (double)out.n_rows : 0.0;
+    out.lanes = mean > 64.0 ? 32 : (mean > 24.0 ? 8 : 8);
+    if (mean > 64.0) out.lanes = 32;
+    RAV_CUDA(cudaStreamSynchronize(s));
+    return RAV_OK;
+}
+
+void csr_free(Csr& A) {
+    if (A.rp) cudaFree(A.rp);
+    if (A.ci) cudaFree(A.ci);
+    if (A.val) cudaFree(A.val);
+    A.rp = nullptr;
+    A.ci = nullptr;
+    A.val = nullptr;
+}
+
+__global__ void col_count_kernel(int64_t nnz, const int32_t* ci, int64_t* cnt) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd((unsigned long long*)(cnt + ci[k]), 1ULL);
+}
+
+__global__ void transpose_fill_kernel(int64_t n, const int64_t* rp, const int32_t* ci, const double* val,
+                                      const int64_t* trp, int64_t* cursor, int32_t* tci, double* tval) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+            int64_t c = ci[k];
+            int64_t p = trp[c] + (int64_t)atomicAdd((unsigned long long*)(cursor + c), 1ULL);
+            tci[p] = (int32_t)i;
+            tval[p] = val[k];
+        }
+}
+
+// insertion sort of each transposed row by column => deterministic order
+__global__ void row_sort_kernel(int64_t n, const int64_t* rp, int32_t* ci, double* val) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t s = rp[i], e = rp[i + 1];
+        for (int64_t a = s + 1; a < e; ++a) {
+            int32_t kc = ci[a];
+            double kv = val[a];
+            int64_t b = a - 1;
+            while (b >= s && ci[b] > kc) { ci[b + 1] = ci[b]; val[b + 1] = val[b]; --b; }
+            ci[b + 1] = kc;
+            val[b + 1] = kv;
+        }
+    }
+}
+
+rav_status csr_transpose(const Csr& A, Csr& At, cudaStream_t s) {
+    At.n_rows = A.n_cols;
+    At.n_cols = A.n_rows;
+    At.nnz = A.nnz;
+    int64_t *cnt = nullptr, *cursor = nullptr;
+    RAV_CUDA(cudaMalloc(&At.rp, sizeof(int64_t) * (At.n_rows + 1)));
+    RAV_CUDA(cudaMalloc(&At.ci, sizeof(int32_t) * (A.nnz > 0 ? A.nnz : 1)));
+    RAV_CUDA(cudaMalloc(&At.val, sizeof(double) * (A.nnz > 0 ? A.nnz : 1)));
+    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * (At.n_rows > 0 ? At.n_rows : 1), s));
+    RAV_CUDA(cudaMallocAsync(&cursor, sizeof(int64_t) * (At.n_rows > 0 ? At.n_rows : 1), s));
+    RAV_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * At.n_rows, s));
+    RAV_CUDA(cudaMemsetAsync(cursor, 0, sizeof(int64_t) * At.n_rows, s));
+    int nb = (int)std::min<int64_t>(cdiv(A.nnz > 0 ? A.nnz : 1, 256), (int64_t)num_sms() * 16);
+    col_count_kernel<<<nb, 256, 0, s>>>(A.nnz, A.ci, cnt);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    RAV_TRY(gen::counts_to_rowptr(cnt, At.rp, At.n_rows, s));
+    int nbr = (int)std::min<int64_t>(cdiv(A.n_rows > 0 ? A.n_rows : 1, 256), (int64_t)num_sms() * 16);
+    transpose_fill_kernel<<<nbr, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, At.rp, cursor, At.ci, At.val);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    int nbt = (int)std::min<int64_t>(cdiv(At.n_rows > 0 ? At.n_rows : 1, 256), (int64_t)num_sms() * 16);
+    row_sort_kernel<<<nbt, 256, 0, s>>>(At.n_rows, At.rp, At.ci, At.val);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    cudaFreeAsync(cnt, s);
+    cudaFreeAsync(cursor, s);
+    double mean = At.n_rows > 0 ? (double)At.nnz / At.n_rows : 0.0;
+    At.lanes = mean > 64.0 ? 32 : 8;
+    RAV_CUDA(cudaStreamSynchronize(s));
+    return RAV_OK;
+}
+
+}  // namespace rav

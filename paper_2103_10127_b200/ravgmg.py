@@ -1,0 +1,338 @@
+"""Thin Python binding of libravgmg.so (include/ravgmg.h) -- argument
+marshalling only: every step of the hot path runs in the library's CUDA
+kernels.  PyTorch provides device memory and streams.
+
+There is no CPU fallback: if the shared library cannot be loaded, importing
+this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libravgmg.so")
+
+RAV_OK = 0
+STATUS = {0: "RAV_OK", 1: "RAV_ERR_ARG", 2: "RAV_ERR_SINGULAR_LOCAL", 3: "RAV_ERR_SINGULAR_COARSE",
+          4: "RAV_ERR_OOM", 5: "RAV_ERR_CUDA", 6: "RAV_ERR_COMM", 7: "RAV_ERR_DIVERGED"}
+VARIANT_ROWS, VARIANT_DIAG = 0, 1
+KERNEL_AUTO, KERNEL_WARP, KERNEL_THREAD = 0, 1, 2
+WEIGHTS = {"pou": 0, "own": 1, "full": 2}
+
+
+class RavError(RuntimeError):
+    def __init__(self, status: int, msg: str, bad_patch: int = -1, bad_level: int = -1):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.bad_patch = bad_patch
+        self.bad_level = bad_level
+
+
+class RavGrid(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("ncell", C.c_int32 * 3), ("len", C.c_double * 3),
+                ("kind", C.c_int32), ("eta_mode", C.c_int32), ("eta0", C.c_double),
+                ("n_modes", C.c_int32), ("amp", C.c_double * 8), ("mode", (C.c_int32 * 3) * 8),
+                ("phase", (C.c_double * 3) * 8), ("gmin", C.c_double), ("gmax", C.c_double)]
+
+
+class RavCsr(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("row_ptr", C.c_void_p),
+                ("col", C.c_void_p), ("val", C.c_void_p), ("on_device", C.c_int32)]
+
+
+class RavPatches(C.Structure):
+    _fields_ = [("n_patches", C.c_int64), ("offs", C.c_void_p), ("dofs", C.c_void_p),
+                ("weight", C.c_void_p), ("on_device", C.c_int32)]
+
+
+class RavOpts(C.Structure):
+    _fields_ = [("variant", C.c_int32), ("kernel", C.c_int32), ("deterministic", C.c_int32),
+                ("n_vel", C.c_int64), ("stream", C.c_void_p)]
+
+
+def _load():
+    from . import build as _build
+    if not os.path.exists(LIB_PATH) or (_build.stale() and os.path.exists(_build.NVCC)):
+        _build.build()
+    L = C.CDLL(LIB_PATH)
+    i64, vp, dbl, st = C.c_int64, C.c_void_p, C.c_double, C.c_int
+    P = C.POINTER
+    sigs = {
+        "rav_gen_sizes": [P(RavGrid), C.c_int, vp, P(i64), P(i64), P(i64), P(i64), P(i64)],
+        "rav_gen_operator": [P(RavGrid), vp, vp, vp, vp, vp],
+        "rav_gen_patches": [P(RavGrid), C.c_int, vp, vp, vp, vp],
+        "rav_gen_prolongation_nnz": [P(RavGrid), P(RavGrid), vp, P(i64)],
+        "rav_gen_prolongation": [P(RavGrid), P(RavGrid), vp, vp, vp, vp],
+        "rav_setup": [P(RavCsr), P(RavPatches), P(RavOpts), P(vp), P(i64)],
+        "rav_smooth": [vp, vp, vp, C.c_int, dbl],
+        "rav_residual": [vp, vp, vp, vp],
+        "rav_apply": [vp, vp, vp, dbl],
+        "rav_rows_size": [vp, P(i64)],
+        "rav_export_rows": [vp, vp],
+        "rav_sweep_bytes": [vp, P(dbl), P(dbl), P(dbl)],
+        "rav_set_stream": [vp, vp],
+        "mg_setup": [C.c_int, P(RavCsr), P(RavPatches), P(RavCsr), i64, P(RavOpts), P(vp), P(C.c_int), P(i64)],
+        "mg_vcycle": [vp, vp, vp, C.c_int, C.c_int, dbl],
+        "mg_solve": [vp, vp, vp, C.c_int, C.c_int, dbl, dbl, C.c_int, P(C.c_int), vp],
+        "mg_set_stream": [vp, vp],
+    }
+    for name, args in sigs.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = st
+    L.rav_destroy.argtypes = [vp]
+    L.rav_destroy.restype = None
+    L.mg_destroy.argtypes = [vp]
+    L.mg_destroy.restype = None
+    L.rav_last_error.restype = C.c_char_p
+    L.rav_version.restype = C.c_char_p
+    L.rav_last_launches.argtypes = [vp]
+    L.rav_last_launches.restype = i64
+    L.mg_last_launches.argtypes = [vp]
+    L.mg_last_launches.restype = i64
+    return L
+
+
+lib = _load()
+
+
+def _check(status: int, **kw):
+    if status != RAV_OK:
+        raise RavError(status, lib.rav_last_error().decode(), **kw)
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return t.data_ptr()
+    return t.ctypes.data
+
+
+def grid(problem: Dict) -> RavGrid:
+    g = RavGrid()
+    g.dim = problem["dim"]
+    for k in range(3):
+        g.ncell[k] = int(problem["ncell"][k])
+        g.len[k] = float(problem["len"][k])
+    g.kind = problem["kind"]
+    g.eta_mode = problem["eta_mode"]
+    g.eta0 = problem["eta0"]
+    g.n_modes = problem["n_modes"]
+    for m in range(8):
+        g.amp[m] = float(problem["amp"][m]) if m < len(problem["amp"]) else 0.0
+        for k in range(3):
+            g.mode[m][k] = int(problem["mode"][m][k])
+            g.phase[m][k] = float(problem["phase"][m][k])
+    g.gmin = problem["gmin"]
+    g.gmax = problem["gmax"]
+    return g
+
+
+def rav_gen_sizes(problem: Dict, weights: str = "pou", stream=None) -> Dict:
+    g = grid(problem)
+    out = [C.c_int64() for _ in range(5)]
+    _check(lib.rav_gen_sizes(C.byref(g), WEIGHTS[weights], _stream(stream), *[C.byref(o) for o in out]))
+    return dict(zip(["n", "nvel", "nnz", "npatch", "patch_entries"], [o.value for o in out]))
+
+
+def gen_level(problem: Dict, weights: str = "pou", device="cuda", stream=None) -> Dict:
+    """Operator, right-hand side and patches of one structured level, generated on the GPU."""
+    sz = rav_gen_sizes(problem, weights, stream)
+    g = grid(problem)
+    n, nnz = sz["n"], sz["nnz"]
+    rp = torch.empty(n + 1, dtype=torch.int64, device=device)
+    ci = torch.empty(nnz, dtype=torch.int32, device=device)
+    val = torch.empty(nnz, dtype=torch.float64, device=device)
+    b = torch.empty(n, dtype=torch.float64, device=device)
+    _check(lib.rav_gen_operator(C.byref(g), _ptr(rp), _ptr(ci), _ptr(val), _ptr(b), _stream(stream)))
+    offs = torch.empty(sz["npatch"] + 1, dtype=torch.int64, device=device)
+    dofs = torch.empty(sz["patch_entries"], dtype=torch.int32, device=device)
+    w = torch.empty(sz["patch_entries"], dtype=torch.float64, device=device)
+    _check(lib.rav_gen_patches(C.byref(g), WEIGHTS[weights], _ptr(offs), _ptr(dofs), _ptr(w), _stream(stream)))
+    return {"n": n, "nvel": sz["nvel"], "nnz": nnz, "rp": rp, "ci": ci, "val": val, "b": b,
+            "offs": offs, "dofs": dofs, "w": w, "problem": problem}
+
+
+def gen_patches(problem: Dict, weights: str, device="cuda", stream=None) -> Dict:
+    sz = rav_gen_sizes(problem, weights, stream)
+    g = grid(problem)
+    offs = torch.empty(sz["npatch"] + 1, dtype=torch.int64, device=device)
+    dofs = torch.empty(sz["patch_entries"], dtype=torch.int32, device=device)
+    w = torch.empty(sz["patch_entries"], dtype=torch.float64, device=device)
+    _check(lib.rav_gen_patches(C.byref(g), WEIGHTS[weights], _ptr(offs), _ptr(dofs), _ptr(w), _stream(stream)))
+    return {"offs": offs, "dofs": dofs, "w": w}
+
+
+def gen_prolongation(fine: Dict, coarse: Dict, device="cuda", stream=None) -> Dict:
+    gf, gc = grid(fine), grid(coarse)
+    nnz = C.c_int64()
+    _check(lib.rav_gen_prolongation_nnz(C.byref(gf), C.byref(gc), _stream(stream), C.byref(nnz)))
+    nf = rav_gen_sizes(fine, stream=stream)["n"]
+    nc = rav_gen_sizes(coarse, stream=stream)["n"]
+    rp = torch.empty(nf + 1, dtype=torch.int64, device=device)
+    ci = torch.empty(nnz.value, dtype=torch.int32, device=device)
+    val = torch.empty(nnz.value, dtype=torch.float64, device=device)
+    _check(lib.rav_gen_prolongation(C.byref(gf), C.byref(gc), _ptr(rp), _ptr(ci), _ptr(val), _stream(stream)))
+    return {"n": nf, "nc": nc, "rp": rp, "ci": ci, "val": val}
+
+
+def csr(A: Dict, n_cols: Optional[int] = None) -> RavCsr:
+    on_dev = int(isinstance(A["rp"], torch.Tensor) and A["rp"].is_cuda)
+    n = A["n"]
+    return RavCsr(n, n if n_cols is None else n_cols, _ptr(A["rp"]), _ptr(A["ci"]), _ptr(A["val"]), on_dev)
+
+
+def patches_struct(P: Dict) -> RavPatches:
+    on_dev = int(isinstance(P["offs"], torch.Tensor) and P["offs"].is_cuda)
+    return RavPatches(len(P["offs"]) - 1, _ptr(P["offs"]), _ptr(P["dofs"]), _ptr(P["w"]), on_dev)
+
+
+class Smoother:
+    """rav_setup / rav_smooth / rav_destroy (Eq. 13)."""
+
+    def __init__(self, A: Dict, P: Dict, variant: int = VARIANT_ROWS, kernel: int = KERNEL_AUTO,
+                 stream=None):
+        self.n = A["n"]
+        self._keep = (A, P)
+        opts = RavOpts(variant, kernel, 0, A.get("nvel", 0), _stream(stream))
+        ctx = C.c_void_p()
+        bad = C.c_int64(-1)
+        st = lib.rav_setup(C.byref(csr(A)), C.byref(patches_struct(P)), C.byref(opts), C.byref(ctx), C.byref(bad))
+        _check(st, bad_patch=bad.value)
+        self.ctx = ctx
+
+    def smooth(self, x, b, nu: int, omega: float):
+        """x <- x + omega S_RAV (b - L x), nu times (x updated in place)."""
+        _check(lib.rav_smooth(self.ctx, _ptr(x), _ptr(b), int(nu), float(omega)))
+        return x
+
+    def residual(self, x, b, r=None):
+        if r is None:
+            r = torch.empty_like(b)
+        _check(lib.rav_residual(self.ctx, _ptr(x), _ptr(b), _ptr(r)))
+        return r
+
+    def apply(self, r, x, omega: float):
+        """x += omega S_RAV r (the sweep kernel alone)."""
+        _check(lib.rav_apply(self.ctx, _ptr(r), _ptr(x), float(omega)))
+        return x
+
+    def export_rows(self) -> torch.Tensor:
+        n = C.c_int64()
+        _check(lib.rav_rows_size(self.ctx, C.byref(n)))
+        rows = torch.empty(n.value, dtype=torch.float64, device="cuda")
+        _check(lib.rav_export_rows(self.ctx, _ptr(rows)))
+        return rows
+
+    def sweep_bytes(self) -> Dict:
+        a, b, f = C.c_double(), C.c_double(), C.c_double()
+        _check(lib.rav_sweep_bytes(self.ctx, C.byref(a), C.byref(b), C.byref(f)))
+        return {"sweep": a.value, "residual": b.value, "flops": f.value}
+
+    @property
+    def last_launches(self) -> int:
+        return int(lib.rav_last_launches(self.ctx))
+
+    def set_stream(self, stream):
+        _check(lib.rav_set_stream(self.ctx, _stream(stream)))
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib.rav_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Multigrid:
+    """mg_setup / mg_vcycle / mg_solve."""
+
+    def __init__(self, levels: Sequence[Dict], prolongations: Sequence[Optional[Dict]], coarse_pin: int,
+                 variant: int = VARIANT_ROWS, kernel: int = KERNEL_AUTO, stream=None):
+        L = len(levels)
+        self.L = L
+        self.n = levels[-1]["n"]
+        self._keep = (levels, prolongations)
+        As = (RavCsr * L)(*[csr(A) for A in levels])
+        Ps = (RavPatches * L)(*[patches_struct(A) for A in levels])
+        Pr = (RavCsr * L)()
+        for l in range(1, L):
+            Pr[l] = csr(prolongations[l], n_cols=prolongations[l]["nc"])
+        opts = RavOpts(variant, kernel, 0, levels[-1].get("nvel", 0), _stream(stream))
+        ctx = C.c_void_p()
+        bl, bp = C.c_int(-1), C.c_int64(-1)
+        st = lib.mg_setup(L, As, Ps, Pr, int(coarse_pin), C.byref(opts), C.byref(ctx), C.byref(bl), C.byref(bp))
+        _check(st, bad_patch=bp.value, bad_level=bl.value)
+        self.ctx = ctx
+
+    def vcycle(self, x, b, pre=2, post=2, omega=0.66):
+        _check(lib.mg_vcycle(self.ctx, _ptr(x), _ptr(b), int(pre), int(post), float(omega)))
+        return x
+
+    def solve(self, x, b, pre=2, post=2, omega=0.66, rtol=1e-8, maxit=200):
+        hist = np.zeros(maxit + 1)
+        it = C.c_int(0)
+        st = lib.mg_solve(self.ctx, _ptr(x), _ptr(b), int(pre), int(post), float(omega), float(rtol), int(maxit),
+                          C.byref(it), hist.ctypes.data)
+        _check(st)
+        return x, it.value, hist[:it.value + 1]
+
+    @property
+    def last_launches(self) -> int:
+        return int(lib.mg_last_launches(self.ctx))
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib.mg_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def coarsen_problem(problem: Dict) -> Dict:
+    p = dict(problem)
+    p["ncell"] = [c // 2 if k < problem["dim"] else c for k, c in enumerate(problem["ncell"])]
+    return p
+
+
+def build_hierarchy(problem: Dict, n_levels: int, weights: str = "pou", variant: int = VARIANT_ROWS,
+                    kernel: int = KERNEL_AUTO, free_inputs: bool = True):
+    """Generate every level on the GPU (rediscretized operators) and
+    build the multigrid context.  Returns (mg, fine_level_dict)."""
+    probs = [problem]
+    for _ in range(n_levels - 1):
+        probs.append(coarsen_problem(probs[-1]))
+    probs = probs[::-1]
+    levels, prols = [], [None]
+    for l, p in enumerate(probs):
+        lev = gen_level(p, weights)
+        levels.append(lev)
+        if l > 0:
+            prols.append(gen_prolongation(p, probs[l - 1]))
+    pin = levels[0]["nvel"]       # pressure DoF of vertex 0 (R4)
+    mg = Multigrid(levels, prols, pin, variant=variant, kernel=kernel)
+    fine = levels[-1]
+    if free_inputs:   # the library copied everything it needs
+        fine = {k: v for k, v in fine.items() if k in ("n", "nvel", "nnz", "b", "problem")}
+        del levels, prols
+        torch.cuda.empty_cache()
+    return mg, fine

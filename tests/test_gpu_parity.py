@@ -1,0 +1,274 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Each side builds its own operator, patches and factors from the same seeded
+problem description (seeded_inputs); nothing flows from the CUDA path into the
+oracle.  Tolerances:
+  * integer data (CSR pattern, patch lists) and dyadic transfer weights: exact;
+  * matrix entries: 1e-14 relative to max|L| (3-point Gauss sums in a different
+    order);
+  * sweeps: ||x_gpu - x_oracle||_2 / ||x_oracle||_2 <= 1e-12 after every
+    checked sweep (north_star; fp64 rounding of ~1e3-term dot products, the
+    local condition numbers <= 1e7 and atomic scatter order);
+  * V-cycles: identical iteration counts and 1e-10 relative final iterates.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import seeded_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rg():
+    from paper_2103_10127_b200 import ravgmg
+    return ravgmg
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+PROBLEMS = [
+    si.problem(2, (8, 8), si.KIND_CAVITY),
+    si.problem(2, (13, 7), si.KIND_MMS, eta="fourier"),
+    si.problem(2, (16, 16), si.KIND_MMS, eta="fourier", box=(1.0, 2.0)),
+    si.problem(3, (3, 2, 4), si.KIND_CAVITY, eta="fourier"),
+]
+
+
+@pytest.mark.parametrize("prob", PROBLEMS, ids=["cav8", "mms13x7", "mms16box", "cav3d"])
+def test_generated_operator_matches_oracle(rg, prob):
+    G = rg.gen_level(prob, "pou")
+    O = oracle.assemble(prob)
+    assert G["n"] == O["n"] and G["nvel"] == O["nvel"]
+    assert np.array_equal(np_(G["rp"]), O["rp"])
+    assert np.array_equal(np_(G["ci"]), O["ci"])
+    scale = np.abs(O["val"]).max()
+    assert np.abs(np_(G["val"]) - O["val"]).max() <= 1e-14 * scale
+    bs = max(np.abs(O["b"]).max(), 1e-300)
+    assert np.abs(np_(G["b"]) - O["b"]).max() <= 1e-13 * bs
+    # L = L^T bitwise on the GPU side too
+    n = G["n"]
+    rp, ci, val = np_(G["rp"]), np_(G["ci"]), np_(G["val"])
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    key = rows.astype(np.int64) * n + ci
+    keyT = ci.astype(np.int64) * n + rows
+    order, orderT = np.argsort(key), np.argsort(keyT)
+    assert np.array_equal(key[order], keyT[orderT])
+    assert np.array_equal(val[order], val[orderT])
+
+
+@pytest.mark.parametrize("weights", ["pou", "own", "full"])
+@pytest.mark.parametrize("prob", PROBLEMS[1:], ids=["mms13x7", "mms16box", "cav3d"])
+def test_generated_patches_match_oracle(rg, prob, weights):
+    G = rg.gen_patches(prob, weights)
+    O = oracle.patches(prob, weights)
+    assert np.array_equal(np_(G["offs"]), O["offs"])
+    assert np.array_equal(np_(G["dofs"]), O["dofs"])
+    assert np.array_equal(np_(G["w"]), O["w"])
+
+
+@pytest.mark.parametrize("dim,nc", [(2, (4, 3)), (3, (2, 2, 3))])
+def test_generated_prolongation_matches_oracle(rg, dim, nc):
+    pc = si.problem(dim, nc, si.KIND_CAVITY)
+    pf = si.problem(dim, [2 * c for c in nc], si.KIND_CAVITY)
+    G = rg.gen_prolongation(pf, pc)
+    O = oracle.prolongation(pf, pc)
+    assert np.array_equal(np_(G["rp"]), O["rp"])
+    assert np.array_equal(np_(G["ci"]), O["ci"])
+    assert np.array_equal(np_(G["val"]), O["val"])
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("kernel", [1, 2], ids=["warp", "thread"])
+@pytest.mark.parametrize("weights", ["pou", "own"])
+def test_factor_rows_match_oracle(rg, kernel, weights):
+    prob = si.problem(2, (11, 9), si.KIND_MMS, eta="fourier")
+    G = rg.gen_level(prob, weights)
+    sm = rg.Smoother(G, G, kernel=kernel)
+    rows = np_(sm.export_rows())
+    O = oracle.assemble(prob)
+    P = oracle.patches(prob, weights)
+    F = oracle.factor(O, P, oracle.FMT_ROWS)
+    fo = F["foffs"]
+    for i in range(len(P["offs"]) - 1):
+        a, b = fo[i], fo[i + 1]
+        ni = P["offs"][i + 1] - P["offs"][i]
+        R_g = rows[a:b].reshape(-1, ni)
+        R_o = F["fac"][a:b].reshape(-1, ni)
+        for k in range(R_o.shape[0]):
+            assert np.linalg.norm(R_g[k] - R_o[k]) <= 1e-12 * np.linalg.norm(R_o[k])
+
+
+SWEEP_CASES = [
+    # (problem, weights, kernel)
+    (si.problem(2, (64, 64), si.KIND_MMS, eta="fourier"), "pou", 0),
+    (si.problem(2, (37, 29), si.KIND_MMS, eta="fourier"), "pou", 1),
+    (si.problem(2, (37, 29), si.KIND_CAVITY, eta="fourier"), "own", 0),
+    (si.problem(2, (20, 24), si.KIND_MMS, eta="fourier", box=(1.0, 2.0)), "full", 0),
+    (si.problem(3, (4, 5, 3), si.KIND_CAVITY, eta="fourier"), "pou", 0),
+]
+
+
+@pytest.mark.parametrize("case", SWEEP_CASES, ids=["mms64-thread", "ragged-warp", "own", "av-full", "3d"])
+def test_sweeps_match_oracle(rg, case):
+    prob, weights, kernel = case
+    omega = 0.1 if weights == "full" else 0.66
+    G = rg.gen_level(prob, weights)
+    sm = rg.Smoother(G, G, kernel=kernel)
+    O = oracle.assemble(prob)
+    P = oracle.patches(prob, weights)
+    F = oracle.factor(O, P, oracle.FMT_ROWS)
+    x0 = si.initial_guess(O["n"], seed=1)
+    x = torch.tensor(x0, device="cuda")
+    xo = x0.copy()
+    done = 0
+    for target in (1, 2, 10, 100):
+        sm.smooth(x, G["b"], target - done, omega)
+        xo = oracle.additive_sweeps(O, P, F, xo, O["b"], omega, target - done)
+        done = target
+        err = _rel(np_(x), xo)
+        assert err <= 1e-12, (target, err)
+
+
+def test_diag_vanka_matches_oracle(rg):
+    prob = si.problem(2, (24, 20), si.KIND_MMS, eta="fourier")
+    G = rg.gen_level(prob, "full")
+    sm = rg.Smoother(G, G, variant=rg.VARIANT_DIAG)
+    O = oracle.assemble(prob)
+    P = oracle.patches(prob, "full")
+    F = oracle.factor(O, P, oracle.FMT_DIAG)
+    x0 = si.initial_guess(O["n"], seed=2)
+    x = torch.tensor(x0, device="cuda")
+    sm.smooth(x, G["b"], 20, 0.1)
+    xo = oracle.additive_sweeps(O, P, F, x0, O["b"], 0.1, 20)
+    assert _rel(np_(x), xo) <= 1e-12
+
+
+def test_host_buffers_through_the_abi(rg):
+    prob = si.problem(2, (32, 32), si.KIND_MMS, eta="fourier")
+    G = rg.gen_level(prob, "pou")
+    sm = rg.Smoother(G, G)
+    x0 = si.initial_guess(G["n"], seed=3)
+    xd = torch.tensor(x0, device="cuda")
+    sm.smooth(xd, G["b"], 5, 0.66)
+    xh = x0.copy()
+    bh = np_(G["b"]).copy()
+    sm.smooth(xh, bh, 5, 0.66)
+    torch.cuda.synchronize()
+    assert np.abs(xh - np_(xd)).max() <= 1e-12 * np.abs(xh).max()
+
+
+@pytest.mark.parametrize("name,n,levels,rtol", [("c1", 8, 3, 1e-10), ("mms64", 64, 5, 1e-8), ("cav32", 32, 4, 1e-10)])
+def test_vcycle_iteration_counts_match_oracle(rg, name, n, levels, rtol):
+    if name == "c1":
+        prob = si.problem(2, (8, 8), si.KIND_CAVITY)
+    elif name == "mms64":
+        prob = si.problem(2, (n, n), si.KIND_MMS, eta="fourier")
+    else:
+        prob = si.problem(2, (n, n), si.KIND_CAVITY, eta="fourier")
+    H = oracle.Hierarchy(prob, levels, "rav")
+    xo, ko, ho = H.solve(rtol=rtol, omega=0.66, pre=2, post=2)
+    mg, fine = rg.build_hierarchy(prob, levels, "pou")
+    x = torch.zeros(fine["n"], dtype=torch.float64, device="cuda")
+    x, kg, hg = mg.solve(x, fine["b"], pre=2, post=2, omega=0.66, rtol=rtol, maxit=200)
+    assert kg == ko, (kg, ko)
+    # residual histories agree to rounding relative to ||r_0|| (late entries are ~1e-10 ||r_0||)
+    np.testing.assert_allclose(hg, ho, rtol=1e-6, atol=1e-12 * ho[0])
+    assert _rel(np_(x), xo) <= 1e-10
+
+
+def test_vcycle_3d_matches_oracle(rg):
+    prob = si.problem(3, (4, 4, 4), si.KIND_CAVITY, eta="fourier")
+    H = oracle.Hierarchy(prob, 2, "rav")
+    xo, ko, ho = H.solve(rtol=1e-8, omega=0.66, pre=2, post=2, maxit=100)
+    mg, fine = rg.build_hierarchy(prob, 2, "pou")
+    x = torch.zeros(fine["n"], dtype=torch.float64, device="cuda")
+    x, kg, hg = mg.solve(x, fine["b"], pre=2, post=2, omega=0.66, rtol=1e-8, maxit=100)
+    assert kg == ko
+    assert _rel(np_(x), xo) <= 1e-10
+
+
+def test_full_size_c2_sampled_sweep(rg):
+    # BASELINE config 2 at full size (512^2, 2.36 M DoFs) in the bench's
+    # launch configuration; the oracle evaluates one sweep at sampled DoFs.
+    prob = si.config_problem("c2")
+    G = rg.gen_level(prob, "pou")
+    sm = rg.Smoother(G, G)
+    x0 = si.initial_guess(G["n"], seed=si.X0_SEED)
+    x = torch.tensor(x0, device="cuda")
+    sm.smooth(x, G["b"], 1, 0.66)
+    O = oracle.assemble(prob)
+    P = oracle.patches(prob, "pou")
+    rng = np.random.Generator(np.random.PCG64(11))
+    sample = np.unique(np.concatenate([rng.choice(O["n"], 400, replace=False),
+                                       np.arange(0, 40), np.arange(O["nvel"] - 20, O["nvel"] + 20),
+                                       np.arange(O["n"] - 40, O["n"])]))
+    xs = oracle.rav_sweep_sampled(O, P, x0, O["b"], 0.66, sample)
+    xg = np_(x)[sample]
+    assert np.linalg.norm(xg - xs) <= 1e-12 * np.linalg.norm(xs)
+    # CSR of the generator equals the oracle's at full size
+    assert np.array_equal(np_(G["ci"]), O["ci"])
+    assert np.abs(np_(G["val"]) - O["val"]).max() <= 1e-14 * np.abs(O["val"]).max()
+
+
+def test_singular_patch_reports_its_id(rg):
+    prob = si.problem(2, (4, 4), si.KIND_CAVITY)
+    G = rg.gen_level(prob, "pou")
+    # patch 3 made singular: duplicate-free list of two pressure DoFs only (zero block)
+    offs = np_(G["offs"]).copy()
+    dofs = np_(G["dofs"]).copy()
+    w = np_(G["w"]).copy()
+    i = 3
+    s, e = offs[i], offs[i + 1]
+    nv = G["nvel"]
+    newd = np.array([nv + 0, nv + 1], np.int32)
+    dofs = np.concatenate([dofs[:s], newd, dofs[e:]])
+    w = np.concatenate([w[:s], [1.0, 1.0], w[e:]])
+    offs[i + 1:] += 2 - (e - s)
+    P = {"offs": torch.tensor(offs, device="cuda"), "dofs": torch.tensor(dofs, device="cuda"),
+         "w": torch.tensor(w, device="cuda")}
+    with pytest.raises(rg.RavError) as ei:
+        rg.Smoother(G, P)
+    assert ei.value.status == 2 and ei.value.bad_patch == 3
+
+
+def test_empty_patch_is_an_argument_error(rg):
+    prob = si.problem(2, (4, 4), si.KIND_CAVITY)
+    G = rg.gen_level(prob, "pou")
+    offs = np_(G["offs"]).copy()
+    offs[2] = offs[1]
+    P = {"offs": torch.tensor(offs, device="cuda"), "dofs": G["dofs"], "w": G["w"]}
+    with pytest.raises(rg.RavError) as ei:
+        rg.Smoother(G, P)
+    assert ei.value.status == 1
+
+
+def test_single_patch_exact_solve(rg):
+    # one patch covering all DoFs of the pinned system, omega = 1 -> exact solve
+    prob = si.problem(2, (3, 3), si.KIND_CAVITY, eta="fourier")
+    O = oracle.assemble(prob)
+    L = oracle.to_dense(O)
+    pin = O["nvel"]
+    keep = np.array([i for i in range(O["n"]) if i != pin])
+    Lp = L[np.ix_(keep, keep)]
+    rows, cols = np.nonzero(Lp != 0)
+    rp = np.zeros(len(keep) + 1, np.int64)
+    rp[1:] = np.cumsum(np.bincount(rows, minlength=len(keep)))
+    A = {"n": len(keep), "nvel": O["nvel"], "rp": torch.tensor(rp, device="cuda"),
+         "ci": torch.tensor(cols.astype(np.int32), device="cuda"), "val": torch.tensor(Lp[rows, cols], device="cuda")}
+    P = {"offs": torch.tensor([0, len(keep)], dtype=torch.int64, device="cuda"),
+         "dofs": torch.arange(len(keep), dtype=torch.int32, device="cuda"),
+         "w": torch.ones(len(keep), dtype=torch.float64, device="cuda")}
+    sm = rg.Smoother(A, P)
+    bp = torch.tensor(O["b"][keep], device="cuda")
+    x = torch.tensor(si.random_vector(len(keep), 4), device="cuda")
+    sm.smooth(x, bp, 1, 1.0)
+    xs = np.linalg.solve(Lp, O["b"][keep])
+    assert _rel(np_(x), xs) <= 1e-10
