@@ -140,9 +140,11 @@ enum {
 };
 
 enum {
-    RAV_KERNEL_AUTO = 0,        /* thread-per-patch SoA kernel when the patch shape allows */
-    RAV_KERNEL_WARP = 1,        /* general warp-per-patch kernel (any n_i, nres_i) */
-    RAV_KERNEL_THREAD = 2       /* force the thread-per-patch kernel (nres <= 32, n <= 64) */
+    RAV_KERNEL_AUTO = 0,        /* RAV_KERNEL_SYM when the patch shape allows, else WARP */
+    RAV_KERNEL_WARP = 1,        /* general warp-per-patch kernel (any n_i, nres_i), rows row-major */
+    RAV_KERNEL_THREAD = 2,      /* thread-per-patch kernel, full weighted rows (nres <= 32, n <= 64) */
+    RAV_KERNEL_SYM = 3          /* thread-per-patch kernel storing the symmetric restricted block of
+                                   L_i^{-1} once (upper triangle) + weights: 17% fewer bytes in 2D */
 };
 
 typedef struct {
@@ -186,8 +188,12 @@ rav_status rav_residual(rav_ctx* ctx, const double* x, const double* b, double* 
 rav_status rav_rows_size(const rav_ctx* ctx, int64_t* total);
 rav_status rav_export_rows(const rav_ctx* ctx, double* rows);
 
-/* Bytes the sweep must move per application (algorithmic roofline bytes:
- * factor rows + patch indices + CSR + compulsory vectors), and flops. */
+/* Algorithmic roofline bytes of one application (SURVEY section 8 row d):
+ * bytes_sweep = factor bytes of the stored format (RAV_KERNEL_SYM: the
+ * symmetric restricted block once + one weight per restricted row; other
+ * kernels: 8 sum nres_i n_i) + 4 sum n_i (patch DoF lists) + vectors (r read,
+ * x read + write); bytes_residual = 12 nnz + 8 (n+1) + 32 n (CSR, x, b, r);
+ * flops = 2 sum nres_i n_i + 2 nnz. */
 rav_status rav_sweep_bytes(const rav_ctx* ctx, double* bytes_sweep, double* bytes_residual,
                            double* flops);
 

@@ -161,6 +161,7 @@ rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opt
     c->variant = o.variant;
     c->nvel = o.n_vel;
     rav_status st = csr_upload(A, c->A, c->stream);
+    if (st == RAV_OK) st = sell_build(c->A, c->stream);
     if (st == RAV_OK) st = patches_upload(P, A->n_rows, c->P, c->stream);
     if (st == RAV_OK) st = factorize(c->A, c->P, o.variant, o.n_vel, o.kernel, c->F, bad_patch, c->stream);
     if (st == RAV_OK) {
@@ -242,7 +243,9 @@ rav_status rav_sweep_bytes(const rav_ctx* c, double* bytes_sweep, double* bytes_
     const double n = (double)c->A.n_rows, nnz = (double)c->A.nnz;
     // algorithmic bytes (SURVEY section 8 row d): factor rows 8 sum nres_i n_i, patch DoF
     // indices 4 sum n_i, x read+write, r gathered once (compulsory vectors)
-    double rows = 8.0 * (double)c->P.rows_total;
+    // layout 3 streams the symmetric restricted block once (+ one weight per restricted row)
+    double rows = c->F.layout == 3 ? 8.0 * (double)(c->P.sym_total + c->P.nres_total)
+                                   : 8.0 * (double)c->P.rows_total;
     double idx = 4.0 * (double)c->P.entries;
     double sweep = rows + idx + 8.0 * n /* r */ + 16.0 * n /* x rmw */;
     double resid = 12.0 * nnz + 8.0 * (n + 1) + 8.0 * n /* x */ + 8.0 * n /* b */ + 8.0 * n /* r write */;

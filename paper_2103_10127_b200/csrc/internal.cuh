@@ -9,13 +9,32 @@ rav_status counts_to_rowptr(const int64_t* cnt, int64_t* rp, int64_t n, cudaStre
 }
 
 // ---- linalg.cu ------------------------------------------------------------------------
+// SELL-32-sigma copy of a square operator for the residual kernel (sell.cu):
+// rows sorted by length (descending) inside windows of SIGMA rows, slices of
+// 32 rows stored column-major (entry k of slot l at sptr[s] + 32 k + l), padded
+// with (col = row, val = 0) to the slice's longest row.
+struct Sell {
+    int64_t nslices = 0;
+    int64_t* sptr = nullptr;   // nslices + 1
+    int32_t* col = nullptr;
+    double* val = nullptr;
+    int32_t* perm = nullptr;   // slot -> row
+    int64_t stored = 0;        // sptr[nslices] (padded entries)
+};
+
 struct Csr {
     int64_t n_rows = 0, n_cols = 0, nnz = 0;
     int64_t* rp = nullptr;
     int32_t* ci = nullptr;
     double* val = nullptr;
-    int lanes = 8;  // lanes per row used by the SpMV kernels
+    int lanes = 8;  // lanes per row used by the row-group SpMV kernels
+    Sell sell;      // built for smoother operators (rav_setup); empty otherwise
 };
+rav_status sell_build(Csr& A, cudaStream_t s);
+void sell_free(Sell& S);
+// r = b - A x via the SELL copy; if part != nullptr also per-block sums of r^2 (nblk blocks)
+rav_status launch_sell_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
+                                cudaStream_t s);
 
 rav_status csr_upload(const rav_csr* A, Csr& out, cudaStream_t s);
 void csr_free(Csr& A);
@@ -39,6 +58,8 @@ struct PatchSet {
     int32_t* nres = nullptr;   // restricted count per patch
     int nmax = 0, nresmax = 0;
     int64_t rows_total = 0;    // sum nres_i * n_i
+    int64_t nres_total = 0;    // sum nres_i
+    int64_t sym_total = 0;     // sum nres_i (nres_i + 1) / 2 + nres_i (n_i - nres_i)
 };
 
 struct Factors {
@@ -47,7 +68,8 @@ struct Factors {
     int64_t* foffs = nullptr;  // n_patches + 1
     double* fac = nullptr;
     // SoA
-    int NT = 0, NMAX = 0;
+    int NT = 0, NMAX = 0, NTRI = 0;
+    double* WT = nullptr;      // layout 3: nchunks * NT * 32 row weights
     int64_t nchunks = 0;
     double* facT = nullptr;    // nchunks * (NMAX*NT/2) * 32 double2
     int32_t* DT = nullptr;     // nchunks * NMAX * 32

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int64_t* __r
     }
 }
 
+
 // sum of squares of (b - A x) per block (fixed order => deterministic)
 template <int G>
 __global__ void __launch_bounds__(256) resnorm_kernel(int64_t n, const int64_t* __restrict__ rp,
@@ -116,6 +117,7 @@ static int spmv_blocks(int64_t n, int G) {
 
 rav_status launch_residual(const Csr& A, const double* x, const double* b, double* r, cudaStream_t s) {
     if (A.n_rows == 0) return RAV_OK;
+    if (A.sell.nslices > 0) return launch_sell_residual(A, x, b, r, nullptr, 0, s);
     int nb = spmv_blocks(A.n_rows, A.lanes);
     if (A.lanes == 32)
         residual_kernel<32><<<nb, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, b, r);
@@ -146,6 +148,13 @@ int residual_norm_blocks() { return num_sms() * 4; }
 
 rav_status launch_residual_norm2(const Csr& A, const double* x, const double* b, double* part, int nblk,
                                  double* out, cudaStream_t s) {
+    if (A.sell.nslices > 0) {
+        RAV_TRY(launch_sell_residual(A, x, b, nullptr, part, nblk, s));
+        sum_parts_kernel<<<1, 256, 0, s>>>(part, nblk, out);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+        return RAV_OK;
+    }
     if (A.lanes == 32)
         resnorm_kernel<32><<<nblk, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, b, part);
     else if (A.lanes == 16)
@@ -210,6 +219,7 @@ rav_status csr_upload(const rav_csr* A, Csr& out, cudaStream_t s) {
 }
 
 void csr_free(Csr& A) {
+    sell_free(A.sell);
     if (A.rp) cudaFree(A.rp);
     if (A.ci) cudaFree(A.ci);
     if (A.val) cudaFree(A.val);

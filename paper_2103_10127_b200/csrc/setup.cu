@@ -19,6 +19,7 @@
 //     DT[(chunk*NMAX + j)*32 + lane].
 #include <algorithm>
 #include <cub/cub.cuh>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -126,6 +127,20 @@ rav_status patches_upload(const rav_patches* P, int64_t n_dofs, PatchSet& out, c
     out.nmax = (int)h_stats[0];
     out.nresmax = (int)h_stats[1];
     out.rows_total = h_sum;
+    {   // host-side totals for the byte model (sum nres, sum of the symmetric-format entries)
+        std::vector<int32_t> hn(out.n_patches);
+        std::vector<int64_t> ho(out.n_patches + 1);
+        RAV_CUDA(cudaMemcpy(hn.data(), out.nres, sizeof(int32_t) * out.n_patches, cudaMemcpyDeviceToHost));
+        RAV_CUDA(cudaMemcpy(ho.data(), out.offs, sizeof(int64_t) * (out.n_patches + 1), cudaMemcpyDeviceToHost));
+        int64_t sm = 0, ss = 0;
+        for (int64_t i = 0; i < out.n_patches; ++i) {
+            int64_t m = hn[i], n = ho[i + 1] - ho[i];
+            sm += m;
+            ss += m * (m + 1) / 2 + m * (n - m);
+        }
+        out.nres_total = sm;
+        out.sym_total = ss;
+    }
     if (out.nresmax < 1) { set_error("rav_patches: no restricted DoF (weight > 0) in any patch"); return RAV_ERR_ARG; }
     return RAV_OK;
 }
@@ -158,10 +173,11 @@ struct FactorArgs {
     int layout;         // 1 general, 2 SoA
     const int64_t* foffs;
     double* fac;
-    int NT, NMAX;
+    int NT, NMAX, NTRI;
     double* facT;
     int32_t* DT;
     int32_t* NR;
+    double* WT;
     double* gscratch;   // when not using smem: per-CTA slot of nmax*ld doubles
     unsigned long long* bad;
 };
@@ -298,7 +314,7 @@ __global__ void __launch_bounds__(FT) factor_kernel(FactorArgs a) {
                 int k = t / n, j = t % n;
                 dst[t] = a.pw[off + k] * aug[(size_t)j * ld + n + k];
             }
-        } else {
+        } else if (a.layout == 2) {
             const int64_t chunk = i >> 5;
             const int lane = (int)(i & 31);
             const int64_t pairs = (int64_t)a.NMAX * a.NT / 2;
@@ -310,6 +326,32 @@ __global__ void __launch_bounds__(FT) factor_kernel(FactorArgs a) {
             }
             for (int j = tid; j < a.NMAX; j += FT)
                 a.DT[(chunk * a.NMAX + j) * 32 + lane] = j < n ? ldofs[j] : ldofs[0];
+            if (tid == 0) a.NR[i] = m;
+        } else {
+            // layout 3 (symmetric): the restricted x restricted block of L_i^{-1} is symmetric
+            // (L_i = R_i L R_i^T with L symmetric), so columns j < NT keep only rows k <= j
+            // (entry e = j(j+1)/2 + k, taken from row k); columns j >= NT keep rows k < NT
+            // (entry e = NTRI + (j - NT) NT + k).  Values are UNweighted rows of L_i^{-1};
+            // the weights w_k go to WT and are applied once per row in the sweep.
+            const int64_t chunk = i >> 5;
+            const int lane = (int)(i & 31);
+            const int NT = a.NT;
+            const int64_t pairs = ((int64_t)a.NTRI + (int64_t)(a.NMAX - NT) * NT) / 2;
+            double* base = a.facT + chunk * pairs * 64;
+            for (int t = tid; t < m * n; t += FT) {
+                int k = t / n, j = t % n;
+                int64_t e;
+                if (j < NT) {
+                    if (k > j) continue;           // stored from row j (j < k < m)
+                    e = (int64_t)j * (j + 1) / 2 + k;
+                } else {
+                    e = a.NTRI + (int64_t)(j - NT) * NT + k;
+                }
+                base[((e >> 1) * 32 + lane) * 2 + (e & 1)] = aug[(size_t)j * ld + n + k];
+            }
+            for (int j = tid; j < a.NMAX; j += FT)
+                a.DT[(chunk * a.NMAX + j) * 32 + lane] = j < n ? ldofs[j] : ldofs[0];
+            for (int k = tid; k < m; k += FT) a.WT[(chunk * NT + k) * 32 + lane] = a.pw[off + k];
             if (tid == 0) a.NR[i] = m;
         }
     }
@@ -344,11 +386,38 @@ rav_status factorize(const Csr& A, const PatchSet& P, int variant, int64_t nvel,
     a.ld = P.nmax + P.nresmax;
     if ((a.ld & 15) == 0) a.ld += 1;   // avoid power-of-two strides in shared memory
     bool use_thread = kernel_choice != RAV_KERNEL_WARP && thread_kernel_supported(P.nresmax, P.nmax);
-    if (kernel_choice == RAV_KERNEL_THREAD && !use_thread) {
-        set_error("thread-per-patch kernel needs nres <= 32 and n <= 64 (got %d, %d)", P.nresmax, P.nmax);
+    if ((kernel_choice == RAV_KERNEL_THREAD || kernel_choice == RAV_KERNEL_SYM) && !use_thread) {
+        set_error("thread-per-patch kernels need nres <= 32 and n <= 64 (got %d, %d)", P.nresmax, P.nmax);
         return RAV_ERR_ARG;
     }
-    if (use_thread) {
+    if (use_thread && kernel_choice != RAV_KERNEL_THREAD) {
+        F.layout = 3;
+        F.NT = pick_NT(P.nresmax);
+        F.NMAX = std::max(F.NT, P.nmax);
+        if ((F.NMAX - F.NT) & 1) F.NMAX += 1;
+        F.NTRI = F.NT * (F.NT + 1) / 2;
+        F.NTRI += F.NTRI & 1;
+        F.nchunks = cdiv(P.n_patches, 32);
+        int64_t pairs = ((int64_t)F.NTRI + (int64_t)(F.NMAX - F.NT) * F.NT) / 2;
+        size_t fac_bytes = sizeof(double) * 2 * pairs * 32 * F.nchunks;
+        RAV_CUDA(cudaMalloc(&F.facT, fac_bytes));
+        RAV_CUDA(cudaMalloc(&F.DT, sizeof(int32_t) * F.NMAX * 32 * F.nchunks));
+        RAV_CUDA(cudaMalloc(&F.NR, sizeof(int32_t) * 32 * F.nchunks));
+        RAV_CUDA(cudaMalloc(&F.WT, sizeof(double) * F.NT * 32 * F.nchunks));
+        RAV_CUDA(cudaMemsetAsync(F.facT, 0, fac_bytes, s));
+        RAV_CUDA(cudaMemsetAsync(F.DT, 0, sizeof(int32_t) * F.NMAX * 32 * F.nchunks, s));
+        RAV_CUDA(cudaMemsetAsync(F.NR, 0, sizeof(int32_t) * 32 * F.nchunks, s));
+        RAV_CUDA(cudaMemsetAsync(F.WT, 0, sizeof(double) * F.NT * 32 * F.nchunks, s));
+        F.bytes = (int64_t)fac_bytes + sizeof(int32_t) * F.NMAX * 32 * F.nchunks + sizeof(double) * F.NT * 32 * F.nchunks;
+        a.layout = 3;
+        a.NT = F.NT;
+        a.NMAX = F.NMAX;
+        a.NTRI = F.NTRI;
+        a.facT = F.facT;
+        a.DT = F.DT;
+        a.NR = F.NR;
+        a.WT = F.WT;
+    } else if (use_thread) {
         F.layout = 2;
         F.NT = pick_NT(P.nresmax);
         F.NMAX = (P.nmax + 1) & ~1;
@@ -433,6 +502,7 @@ void factors_free(Factors& F) {
     if (F.facT) cudaFree(F.facT);
     if (F.DT) cudaFree(F.DT);
     if (F.NR) cudaFree(F.NR);
+    if (F.WT) cudaFree(F.WT);
     F = Factors{};
 }
 
@@ -454,6 +524,26 @@ __global__ void export_soa_kernel(int64_t np, const int64_t* offs, const int32_t
     }
 }
 
+// layout 3 -> W[k][j] = w_k * Linv[k][j] (mirrored triangle for restricted columns)
+__global__ void export_sym_kernel(int64_t np, const int64_t* offs, const int32_t* nres, const int64_t* roffs,
+                                  int NT, int NMAX, int NTRI, const double* facT, const double* WT, double* rows) {
+    for (int64_t i = blockIdx.x; i < np; i += gridDim.x) {
+        int n = (int)(offs[i + 1] - offs[i]);
+        int m = nres[i];
+        const int64_t chunk = i >> 5;
+        const int lane = (int)(i & 31);
+        const int64_t pairs = ((int64_t)NTRI + (int64_t)(NMAX - NT) * NT) / 2;
+        const double* base = facT + chunk * pairs * 64;
+        for (int t = threadIdx.x; t < m * n; t += blockDim.x) {
+            int k = t / n, j = t % n;
+            int64_t e;
+            if (j < NT) e = k <= j ? (int64_t)j * (j + 1) / 2 + k : (int64_t)k * (k + 1) / 2 + j;
+            else e = NTRI + (int64_t)(j - NT) * NT + k;
+            rows[roffs[i] + t] = WT[(chunk * NT + k) * 32 + lane] * base[((e >> 1) * 32 + lane) * 2 + (e & 1)];
+        }
+    }
+}
+
 rav_status export_rows(const PatchSet& P, const Factors& F, double* rows, cudaStream_t s) {
     if (F.layout == 1) {
         RAV_CUDA(cudaMemcpyAsync(rows, F.fac, sizeof(double) * P.rows_total, cudaMemcpyDeviceToDevice, s));
@@ -467,7 +557,11 @@ rav_status export_rows(const PatchSet& P, const Factors& F, double* rows, cudaSt
     count_launch();
     RAV_TRY(gen::counts_to_rowptr(sz, roffs, P.n_patches, s));
     int g = (int)std::min<int64_t>(P.n_patches, (int64_t)num_sms() * 8);
-    export_soa_kernel<<<g, 128, 0, s>>>(P.n_patches, P.offs, P.nres, roffs, F.NT, F.NMAX, F.facT, rows);
+    if (F.layout == 3)
+        export_sym_kernel<<<g, 128, 0, s>>>(P.n_patches, P.offs, P.nres, roffs, F.NT, F.NMAX, F.NTRI, F.facT, F.WT,
+                                            rows);
+    else
+        export_soa_kernel<<<g, 128, 0, s>>>(P.n_patches, P.offs, P.nres, roffs, F.NT, F.NMAX, F.facT, rows);
     count_launch();
     RAV_CHECK_LAUNCH();
     cudaFreeAsync(sz, s);

@@ -86,7 +86,7 @@ def _rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-@pytest.mark.parametrize("kernel", [1, 2], ids=["warp", "thread"])
+@pytest.mark.parametrize("kernel", [1, 2, 3], ids=["warp", "thread", "sym"])
 @pytest.mark.parametrize("weights", ["pou", "own"])
 def test_factor_rows_match_oracle(rg, kernel, weights):
     prob = si.problem(2, (11, 9), si.KIND_MMS, eta="fourier")
@@ -113,10 +113,13 @@ SWEEP_CASES = [
     (si.problem(2, (37, 29), si.KIND_CAVITY, eta="fourier"), "own", 0),
     (si.problem(2, (20, 24), si.KIND_MMS, eta="fourier", box=(1.0, 2.0)), "full", 0),
     (si.problem(3, (4, 5, 3), si.KIND_CAVITY, eta="fourier"), "pou", 0),
+    (si.problem(2, (33, 31), si.KIND_MMS, eta="fourier"), "pou", 2),
+    (si.problem(2, (64, 48), si.KIND_CAVITY, eta="fourier"), "pou", 3),
 ]
 
 
-@pytest.mark.parametrize("case", SWEEP_CASES, ids=["mms64-thread", "ragged-warp", "own", "av-full", "3d"])
+@pytest.mark.parametrize("case", SWEEP_CASES, ids=["mms64-auto", "ragged-warp", "own", "av-full", "3d",
+                                                   "rows-thread", "cav-sym"])
 def test_sweeps_match_oracle(rg, case):
     prob, weights, kernel = case
     omega = 0.1 if weights == "full" else 0.66
