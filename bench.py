@@ -141,6 +141,50 @@ def run_reference(args):
     return 0
 
 
+def run_vcycle_c3(rg, si, stream, dist):
+    """mg_solve on BASELINE config 3: 2048^2 MMS, seeded eta, 10 levels (4^2
+    coarsest), V(2,2)-RAV, omega 0.66, x0 = 0, to ||r|| <= 1e-8 ||r0||.
+    Device-timed with CUDA events around mg_solve (which reads back one norm
+    per cycle for the stopping test)."""
+    import torch
+    c = si.CONFIGS["c3"]
+    prob = si.config_problem("c3")
+    t0 = time.perf_counter()
+    mg, fine = rg.build_hierarchy(prob, c["levels"], "pou")
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    b = fine["b"]
+    x = torch.zeros(fine["n"], dtype=torch.float64, device="cuda")
+    mg.solve(x, b, pre=c["pre"], post=c["post"], omega=c["omega"], rtol=c["rtol"], maxit=3)  # warm (graph capture)
+    times, iters, hist = [], None, None
+    for _ in range(3):
+        x.zero_()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        x, iters, hist = mg.solve(x, b, pre=c["pre"], post=c["post"], omega=c["omega"], rtol=c["rtol"], maxit=100)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    t = min(times)
+    if dist is not None:
+        tt = torch.tensor([t], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    launches = mg.last_launches
+    rho = (hist[-1] / hist[0]) ** (1.0 / max(iters, 1))
+    out = {"config": "c3: 2048^2 Q2-Q1 MMS, seeded eta, 10 levels (4^2 coarsest), V(2,2)-RAV omega 0.66, x0 = 0",
+           "free_dofs": fine["n"], "rtol": c["rtol"], "cycles": iters, "converged": bool(hist[-1] <= c["rtol"] * hist[0]),
+           "time_to_rtol_s": t, "ms_per_cycle": t / max(iters, 1) * 1e3, "avg_reduction_factor": rho,
+           "setup_s": setup_s, "gpu_launches": launches, "timing": "CUDA events around mg_solve, best of 3"}
+    mg.close()
+    del mg, fine, x, b
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_gpu(args):
     import numpy as np
     import torch
@@ -154,7 +198,9 @@ def run_gpu(args):
     import seeded_inputs as si
 
     prob = si.config_problem("c2")
-    stream = torch.cuda.current_stream()
+    # a non-default stream: the library captures sweep sequences / V-cycles as CUDA graphs on it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     t_setup0 = time.perf_counter()
     G = rg.gen_level(prob, "pou")
     torch.cuda.synchronize()
@@ -164,6 +210,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     t_factor = time.perf_counter() - t1
     n = G["n"]
+    nnz_c2, npatch_c2 = G["nnz"], len(G["offs"]) - 1
     b = G["b"]
     x0 = torch.tensor(si.initial_guess(n, seed=si.X0_SEED), device="cuda")
     x = x0.clone()
@@ -246,6 +293,13 @@ def run_gpu(args):
         e2e_s = float(t.item())
     e2e_value = ws * n * SWEEPS_PER_STEP * args.steps / e2e_s / 1e6
 
+    # ---- V-cycle time to 1e-8 on c3 (2048^2, 10 levels), BASELINE metric part 2 ------
+    vcyc = None
+    if not args.no_vcycle:
+        del sm, G
+        torch.cuda.empty_cache()
+        vcyc = run_vcycle_c3(rg, si, stream, dist)
+
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample) ------------------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -260,7 +314,7 @@ def run_gpu(args):
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": "c2: 2D 512x512 Taylor-Hood Q2-Q1, MMS forcing, seeded eta in [0.1,10]; "
                                "step = 100 RAV sweeps (residual SpMV + RAV sweep) from seeded N(0,1)",
-                   "free_dofs": n, "nnz": G["nnz"], "patches": len(G["offs"]) - 1,
+                   "free_dofs": n, "nnz": nnz_c2, "patches": npatch_c2,
                    "sweeps_per_step": SWEEPS_PER_STEP, "omega": OMEGA, "weights": "partition of unity (R3)",
                    "l2": "inputs larger than L2 (factor rows 2.0 GB + CSR 0.73 GB streamed per sweep; "
                          "x, r, b vectors 19 MB each stay L2-resident by design)",
@@ -283,6 +337,8 @@ def run_gpu(args):
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if vcyc is not None:
+        line["vcycle"] = vcyc
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -297,6 +353,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-vcycle", action="store_true", help="skip the c3 V-cycle time-to-1e-8 measurement")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -143,16 +143,26 @@ enum {
     RAV_KERNEL_AUTO = 0,        /* RAV_KERNEL_SYM when the patch shape allows, else WARP */
     RAV_KERNEL_WARP = 1,        /* general warp-per-patch kernel (any n_i, nres_i), rows row-major */
     RAV_KERNEL_THREAD = 2,      /* thread-per-patch kernel, full weighted rows (nres <= 32, n <= 64) */
-    RAV_KERNEL_SYM = 3          /* thread-per-patch kernel storing the symmetric restricted block of
+    RAV_KERNEL_SYM = 3,         /* thread-per-patch kernel storing the symmetric restricted block of
                                    L_i^{-1} once (upper triangle) + weights: 17% fewer bytes in 2D */
+    RAV_KERNEL_SCHUR = 4        /* factored rows (needs block_dim > 0): every patch must hold one
+                                   pressure DoF p and complete velocity nodes, with velocity block
+                                   I_d (x) A_s (no cross-component coupling) and symmetric B; then
+                                   L_i^{-1} = [I(x)A_s^{-1} + g S^{-1} g^T, -g S^{-1}; -S^{-1} g^T,
+                                   S^{-1}] (g = A_s^{-1} b, S = L_pp - b^T g) and only the restricted
+                                   rows of A_s^{-1}, g and 1/S are stored (2D: 4x fewer bytes than
+                                   rows; 3D: 8x).  AUTO tries it first when block_dim > 0 and falls
+                                   back to SYM / WARP when any patch lacks the structure. */
 };
 
 typedef struct {
     int32_t variant;            /* RAV_VARIANT_* */
     int32_t kernel;             /* RAV_KERNEL_* */
     int32_t deterministic;      /* 1: run-to-run bitwise reproducible scatter (two-phase) */
-    int64_t n_vel;              /* DoFs < n_vel are velocity (needed by DIAG) */
+    int64_t n_vel;              /* DoFs < n_vel are velocity (needed by DIAG and SCHUR) */
     void*   stream;             /* cudaStream_t */
+    int32_t block_dim;          /* velocity components interleaved as dof = block_dim * node + c
+                                   (enables RAV_KERNEL_SCHUR); 0 = unknown */
 } rav_opts;
 
 typedef struct rav_ctx rav_ctx;
@@ -214,6 +224,8 @@ typedef struct mg_ctx mg_ctx;
  * space is fixed only here; coarse_pin < 0 disables the pin).  Smoothers on
  * levels 1..L-1 are built with rav_setup(opts). */
 rav_status mg_setup(int n_levels, const rav_csr* A, const rav_patches* patches, const rav_csr* P,
+                    const int64_t* n_vel /* per level (DoFs < n_vel[l] are velocity), NULL =
+                                            opts->n_vel on every level */,
                     int64_t coarse_pin, const rav_opts* opts, mg_ctx** out,
                     int* bad_level, int64_t* bad_patch);
 

@@ -163,7 +163,23 @@ rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opt
     rav_status st = csr_upload(A, c->A, c->stream);
     if (st == RAV_OK) st = sell_build(c->A, c->stream);
     if (st == RAV_OK) st = patches_upload(P, A->n_rows, c->P, c->stream);
-    if (st == RAV_OK) st = factorize(c->A, c->P, o.variant, o.n_vel, o.kernel, c->F, bad_patch, c->stream);
+    bool done = false;
+    if (st == RAV_OK && o.variant == RAV_VARIANT_ROWS && o.block_dim > 0 &&
+        (o.kernel == RAV_KERNEL_AUTO || o.kernel == RAV_KERNEL_SCHUR)) {
+        st = schur_factorize(c->A, c->P, o.n_vel, o.block_dim, o.kernel, c->F, bad_patch, &done, c->stream);
+        if (st == RAV_OK && !done && o.kernel == RAV_KERNEL_SCHUR) {
+            set_error("rav_setup: RAV_KERNEL_SCHUR requested but the patches lack the I_d (x) A_s / one-pressure structure");
+            st = RAV_ERR_ARG;
+        }
+    }
+    if (st == RAV_OK && !done) {
+        if (o.kernel == RAV_KERNEL_SCHUR) {
+            set_error("rav_setup: RAV_KERNEL_SCHUR needs variant ROWS and block_dim > 0");
+            st = RAV_ERR_ARG;
+        } else {
+            st = factorize(c->A, c->P, o.variant, o.n_vel, o.kernel, c->F, bad_patch, c->stream);
+        }
+    }
     if (st == RAV_OK) {
         cudaError_t e = cudaMalloc(&c->r, sizeof(double) * std::max<int64_t>(1, c->A.n_rows));
         if (e != cudaSuccess) { set_error("rav_setup: %s", cudaGetErrorString(e)); st = RAV_ERR_OOM; }
@@ -233,7 +249,8 @@ rav_status rav_rows_size(const rav_ctx* c, int64_t* total) {
 
 rav_status rav_export_rows(const rav_ctx* c, double* rows) {
     if (!c || !rows) { set_error("NULL argument"); return RAV_ERR_ARG; }
-    RAV_TRY(export_rows(c->P, c->F, rows, c->stream));
+    if (c->F.layout >= 4) RAV_TRY(export_schur_rows(c->P, c->F, c->nvel, rows, c->stream));
+    else RAV_TRY(export_rows(c->P, c->F, rows, c->stream));
     RAV_CUDA(cudaStreamSynchronize(c->stream));
     return RAV_OK;
 }
@@ -247,6 +264,10 @@ rav_status rav_sweep_bytes(const rav_ctx* c, double* bytes_sweep, double* bytes_
     double rows = c->F.layout == 3 ? 8.0 * (double)(c->P.sym_total + c->P.nres_total)
                                    : 8.0 * (double)c->P.rows_total;
     double idx = 4.0 * (double)c->P.entries;
+    if (c->F.layout >= 4) {   // Schur formats: factored rows + node indices (counted at setup)
+        rows = (double)c->F.alg_bytes;
+        idx = 0.0;
+    }
     double sweep = rows + idx + 8.0 * n /* r */ + 16.0 * n /* x rmw */;
     double resid = 12.0 * nnz + 8.0 * (n + 1) + 8.0 * n /* x */ + 8.0 * n /* b */ + 8.0 * n /* r write */;
     if (bytes_sweep) *bytes_sweep = sweep;
@@ -300,7 +321,8 @@ void mg_destroy(mg_ctx* m) {
 }
 
 rav_status mg_setup(int n_levels, const rav_csr* A, const rav_patches* patches, const rav_csr* P,
-                    int64_t coarse_pin, const rav_opts* opts, mg_ctx** out, int* bad_level, int64_t* bad_patch) {
+                    const int64_t* n_vel, int64_t coarse_pin, const rav_opts* opts, mg_ctx** out, int* bad_level,
+                    int64_t* bad_patch) {
     if (!out || !A || n_levels < 1 || (n_levels > 1 && (!patches || !P))) {
         set_error("mg_setup: bad argument");
         return RAV_ERR_ARG;
@@ -327,7 +349,9 @@ rav_status mg_setup(int n_levels, const rav_csr* A, const rav_patches* patches, 
                 break;
             }
             int64_t bp = -1;
-            st = rav_setup(&A[l], &patches[l], &o, &L.sm, &bp);
+            rav_opts ol = o;
+            if (n_vel) ol.n_vel = n_vel[l];
+            st = rav_setup(&A[l], &patches[l], &ol, &L.sm, &bp);
             if (st == RAV_ERR_SINGULAR_LOCAL) {
                 if (bad_level) *bad_level = l;
                 if (bad_patch) *bad_patch = bp;

@@ -69,7 +69,14 @@ struct Factors {
     double* fac = nullptr;
     // SoA
     int NT = 0, NMAX = 0, NTRI = 0;
-    double* WT = nullptr;      // layout 3: nchunks * NT * 32 row weights
+    double* WT = nullptr;      // layout 3: nchunks * NT * 32 row weights; layout 4: aux (weights, w_p, 1/S)
+    // Schur formats (schur.cu): layout 4 thread SoA chunks, layout 5 per patch (warp kernel)
+    int MT = 0, D = 0, NN = 0;
+    int64_t pairs = 0;
+    int32_t* PD = nullptr;     // pressure DoF per patch slot
+    int32_t* nodes = nullptr;  // layout 5: node dofs per patch
+    int64_t* nodeoffs = nullptr;
+    int64_t alg_bytes = 0;     // algorithmic bytes of the stored factor data (per application)
     int64_t nchunks = 0;
     double* facT = nullptr;    // nchunks * (NMAX*NT/2) * 32 double2
     int32_t* DT = nullptr;     // nchunks * NMAX * 32
@@ -85,6 +92,15 @@ rav_status factorize(const Csr& A, const PatchSet& P, int variant, int64_t nvel,
 void factors_free(Factors& F);
 rav_status export_rows(const PatchSet& P, const Factors& F, double* rows, cudaStream_t s);
 bool thread_kernel_supported(int nresmax, int nmax);
+
+// ---- schur.cu -------------------------------------------------------------------------
+// Try the factored Schur format (velocity block I_D (x) A_s, one pressure DoF per patch).
+// *applicable = false (and F untouched) when the structure does not hold.
+rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D, int kernel_choice, Factors& F,
+                           int64_t* bad_patch, bool* applicable, cudaStream_t s);
+rav_status launch_schur_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
+                              cudaStream_t s);
+rav_status export_schur_rows(const PatchSet& P, const Factors& F, int64_t nvel, double* rows, cudaStream_t s);
 
 // ---- sweep.cu -------------------------------------------------------------------------
 rav_status launch_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,

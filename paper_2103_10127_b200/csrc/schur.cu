@@ -1,0 +1,810 @@
+// schur.cu -- factored ("Schur") format of the restricted rows of L_i^{-1} for
+// Vanka patches of Taylor-Hood-type saddle-point operators (SURVEY section 8
+// rows a4/a5; P:114 L_i = R_i L R_i^T, Eq. 13).
+//
+// A Vanka patch holds one pressure DoF p and the velocity DoFs of nn nodes.
+// For the Laplacian-form viscous term (Eq. 7) the velocity block of L is
+// I_d (x) A_s (the same scalar matrix for every component, no coupling between
+// components), so with b the velocity-pressure column of L_i and c = L_pp:
+//
+//   L_i = [ I_d(x)A_s  b ]      L_i^{-1} = [ I(x)A_s^{-1} + g S^{-1} g^T   -g S^{-1} ]
+//         [ b^T        c ]                 [ -S^{-1} g^T                    S^{-1}  ]
+//
+// g = (I(x)A_s^{-1}) b, S = c - b^T g (the Schur complement of the pressure DoF).
+// Applied to r_i = (r_u, r_p):  t = S^{-1} (g^T r_u - r_p),
+//   du_(k,c) = (A_s^{-1} r_c)_k + g_(k,c) t,   dp = -t,
+// which is exactly row (k,c) / row p of L_i^{-1} times r_i.  Only the restricted
+// rows of A_s^{-1} (restricted nodes k, P:122 / R3), g, 1/S and the weights are
+// stored: 2D PoU 240 doubles per patch instead of 969 rows entries (3D: 3779
+// instead of 30832).  setup verifies the structure on every patch and the
+// caller falls back to the generic row formats when it does not hold.
+//
+// The setup solves A_s [G | Y] = [b_0 .. b_{d-1} | e_k (k restricted)] by
+// Gaussian elimination with partial pivoting in shared memory (one CTA per
+// patch; 2D nn = 25, 3D nn = 125).
+#include <algorithm>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace rav {
+
+constexpr int ST = 128;
+
+struct SchurArgs {
+    const int64_t* rp;
+    const int32_t* ci;
+    const double* val;
+    int64_t np;
+    const int64_t* poffs;
+    const int32_t* pdofs;
+    const double* pw;
+    int64_t nvel;
+    int D;           // velocity components (interleaved: dof = D * node + c)
+    int nnmax;       // max nodes per patch
+    int mnmax;       // max restricted nodes per patch
+    int ld;          // leading dimension of the augmented matrix (>= nnmax + D + mnmax)
+    int layout;      // 4: thread SoA chunks, 5: per-patch (warp kernel)
+    // thread layout (4)
+    int MT, NN;
+    int64_t pairs;   // double2 pairs per chunk
+    double* facT;
+    int32_t* ND;     // [chunk][NN][32] node dof (component 0)
+    int32_t* PD;     // [chunk][32] pressure dof
+    int32_t* NR;     // [chunk][32] restricted node count
+    double* AUX;     // [chunk][MT + 2][32]: w_k (k < MT), w_p, 1/S
+    // per-patch layout (5)
+    const int64_t* foffs;  // per patch: Y (MT x nn col-major, stride MT), g (nn*D), aux (MT + 2)
+    double* fac;
+    int32_t* nodes;  // per patch node dofs: nodeoffs[i] ... (nn_i)
+    const int64_t* nodeoffs;
+    int32_t* pdof;   // per patch pressure dof
+    int32_t* nres_nodes;
+    unsigned int* fail;          // bit 0: structure does not hold; bit 1: singular
+    unsigned long long* bad;     // smallest singular patch
+    unsigned long long* alg;     // sum of algorithmic bytes of the stored data
+};
+
+__device__ __forceinline__ int64_t tri_col_start(int j, int D) { return (int64_t)j * (j + 1) / 2 + (int64_t)j * D; }
+
+__global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
+    extern __shared__ double smem[];
+    const int tid = threadIdx.x;
+    const int D = a.D;
+    double* M = smem;                                         // nnmax x ld
+    double* rn = M + (size_t)a.nnmax * a.ld;                  // nnmax
+    double* bcol = rn + a.nnmax;                              // nnmax * D (B column of L_i)
+    double* wnode = bcol + (size_t)a.nnmax * D;               // nnmax weights (per node)
+    int32_t* ndof = (int32_t*)(wnode + a.nnmax);              // nnmax: dof of component 0
+    int32_t* snode = ndof + a.nnmax;                          // sorted node ids (dof / D)
+    int32_t* sperm = snode + a.nnmax;                         // local index of sorted entry
+    __shared__ int s_nn, s_mn, s_pd, s_fail, s_piv;
+    __shared__ double s_wp, s_cpp;
+
+    for (int64_t i = blockIdx.x; i < a.np; i += gridDim.x) {
+        const int64_t off = a.poffs[i];
+        const int n = (int)(a.poffs[i + 1] - off);
+        __syncthreads();
+        if (tid == 0) {
+            // node table + structure checks (sequential: n <= a few hundred)
+            int nn = 0, mn = 0, pd = -1, fail = 0, cnt = 0, cur = -1;
+            double wcur = 0.0, wp = 0.0;
+            bool in_rest = true;
+            for (int t = 0; t < n && !fail; ++t) {
+                const int dof = a.pdofs[off + t];
+                const double w = a.pw[off + t];
+                if (dof >= a.nvel) {
+                    if (pd >= 0) fail = 1;
+                    pd = dof;
+                    wp = w;
+                    continue;
+                }
+                const int node = dof / D, c = dof % D;
+                if (node != cur) {
+                    if (cur >= 0 && cnt != D) fail = 1;
+                    if (c != 0 || nn >= a.nnmax) { fail = 1; break; }
+                    cur = node;
+                    cnt = 1;
+                    wcur = w;
+                    ndof[nn] = dof;
+                    wnode[nn] = w;
+                    if (w > 0.0) {
+                        if (!in_rest) fail = 1;   // restricted nodes must come first
+                        ++mn;
+                    } else {
+                        in_rest = false;
+                    }
+                    ++nn;
+                } else {
+                    if (c != cnt || w != wcur) fail = 1;
+                    ++cnt;
+                }
+            }
+            if (cur >= 0 && cnt != D) fail = 1;
+            if (pd < 0 || nn < 1 || mn > a.mnmax) fail = 1;
+            s_nn = nn;
+            s_mn = mn;
+            s_pd = pd;
+            s_wp = wp;
+            s_cpp = 0.0;
+            s_fail = fail;
+        }
+        __syncthreads();
+        if (s_fail) {
+            if (tid == 0) atomicOr(a.fail, 1u);
+            continue;
+        }
+        const int nn = s_nn, mn = s_mn, pd = s_pd;
+        const int W = nn + D + mn, ld = a.ld;
+        for (int t = tid; t < nn * ld; t += ST) M[t] = 0.0;
+        for (int t = tid; t < nn * D; t += ST) bcol[t] = 0.0;
+        for (int t = tid; t < nn; t += ST) {
+            const int nd = ndof[t] / D;
+            int rank = 0;
+            for (int u = 0; u < nn; ++u) rank += (ndof[u] / D < nd);
+            snode[rank] = nd;
+            sperm[rank] = t;
+        }
+        __syncthreads();
+        // gather A_s (component 0 rows), the B column, and verify components 1..D-1
+        for (int t = tid; t < nn * D; t += ST) {
+            const int j = t / D, c = t % D;
+            const int row = ndof[j] + c;
+            for (int64_t k = a.rp[row]; k < a.rp[row + 1]; ++k) {
+                const int col = a.ci[k];
+                const double v = a.val[k];
+                if (col == pd) { bcol[j * D + c] = v; continue; }
+                if (col >= a.nvel) continue;    // other pressure DoFs are outside the patch
+                const int cn = col / D, cc = col % D;
+                int lo = 0, hi = nn - 1, pos = -1;
+                while (lo <= hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (snode[mid] == cn) { pos = mid; break; }
+                    if (snode[mid] < cn) lo = mid + 1; else hi = mid - 1;
+                }
+                if (pos < 0) continue;
+                const int l = sperm[pos];
+                if (cc != c) {
+                    if (v != 0.0) atomicOr((unsigned int*)&s_fail, 1u);
+                    continue;
+                }
+                if (c == 0) M[(size_t)j * ld + l] = v;
+            }
+        }
+        __syncthreads();
+        for (int t = tid; t < nn * (D - 1); t += ST) {
+            const int j = t / (D - 1), c = 1 + t % (D - 1);
+            const int row = ndof[j] + c;
+            for (int64_t k = a.rp[row]; k < a.rp[row + 1]; ++k) {
+                const int col = a.ci[k];
+                if (col >= a.nvel || col % D != c) continue;
+                const int cn = col / D;
+                int lo = 0, hi = nn - 1, pos = -1;
+                while (lo <= hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (snode[mid] == cn) { pos = mid; break; }
+                    if (snode[mid] < cn) lo = mid + 1; else hi = mid - 1;
+                }
+                if (pos < 0) continue;
+                if (M[(size_t)j * ld + sperm[pos]] != a.val[k]) atomicOr((unsigned int*)&s_fail, 1u);
+            }
+        }
+        // pressure row: symmetric B and C_pp
+        if (tid == 0) {
+            for (int64_t k = a.rp[pd]; k < a.rp[pd + 1]; ++k) {
+                const int col = a.ci[k];
+                if (col == pd) { s_cpp = a.val[k]; continue; }
+                if (col >= a.nvel) continue;
+                const int cn = col / D, cc = col % D;
+                int lo = 0, hi = nn - 1, pos = -1;
+                while (lo <= hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (snode[mid] == cn) { pos = mid; break; }
+                    if (snode[mid] < cn) lo = mid + 1; else hi = mid - 1;
+                }
+                if (pos < 0) continue;
+                if (bcol[sperm[pos] * D + cc] != a.val[k]) s_fail = 1;
+            }
+        }
+        __syncthreads();
+        if (s_fail) {
+            if (tid == 0) atomicOr(a.fail, 1u);
+            continue;
+        }
+        // right-hand sides: B columns, then e_k for the restricted nodes
+        for (int t = tid; t < nn * D; t += ST) M[(size_t)(t / D) * ld + nn + (t % D)] = bcol[t];
+        for (int k = tid; k < mn; k += ST) M[(size_t)k * ld + nn + D + k] = 1.0;
+        for (int r = tid; r < nn; r += ST) {
+            double mx = 0.0;
+            for (int c = 0; c < nn; ++c) mx = fmax(mx, fabs(M[(size_t)r * ld + c]));
+            rn[r] = mx;
+        }
+        __syncthreads();
+        // Gaussian elimination with partial pivoting (A_s symmetric: A_s^T = A_s)
+        for (int c = 0; c < nn; ++c) {
+            if (tid < 32) {
+                double best = -1.0;
+                int bi = c;
+                for (int r = c + tid; r < nn; r += 32) {
+                    double v = fabs(M[(size_t)r * ld + c]);
+                    if (v > best) { best = v; bi = r; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+                }
+                if (tid == 0) {
+                    s_piv = bi;
+                    if (!(best > 1e-14 * rn[bi])) s_fail = 2;
+                }
+            }
+            __syncthreads();
+            if (s_fail) break;
+            const int p = s_piv;
+            if (p != c) {
+                for (int t = c + tid; t < W; t += ST) {
+                    double u = M[(size_t)c * ld + t];
+                    M[(size_t)c * ld + t] = M[(size_t)p * ld + t];
+                    M[(size_t)p * ld + t] = u;
+                }
+                if (tid == 0) { double u = rn[c]; rn[c] = rn[p]; rn[p] = u; }
+            }
+            __syncthreads();
+            const double inv = 1.0 / M[(size_t)c * ld + c];
+            const int nr = nn - c - 1, ncol = W - c - 1;
+            for (int t = tid; t < nr * ncol; t += ST) {
+                const int r = c + 1 + t / ncol, col = c + 1 + t % ncol;
+                M[(size_t)r * ld + col] -= (M[(size_t)r * ld + c] * inv) * M[(size_t)c * ld + col];
+            }
+            __syncthreads();
+        }
+        if (s_fail) {
+            if (tid == 0) { atomicOr(a.fail, 2u); atomicMin(a.bad, (unsigned long long)i); }
+            continue;
+        }
+        const int nrhs = D + mn;
+        for (int c = nn - 1; c >= 0; --c) {
+            for (int t = tid; t < nrhs; t += ST) M[(size_t)c * ld + nn + t] /= M[(size_t)c * ld + c];
+            __syncthreads();
+            for (int t = tid; t < c * nrhs; t += ST) {
+                const int r = t / nrhs, k = t % nrhs;
+                M[(size_t)r * ld + nn + k] -= M[(size_t)r * ld + c] * M[(size_t)c * ld + nn + k];
+            }
+            __syncthreads();
+        }
+        // Schur complement S = c - b^T g (one warp)
+        if (tid < 32) {
+            double s = 0.0, sa = 0.0;
+            for (int t = tid; t < nn * D; t += 32) {
+                const double pr = bcol[t] * M[(size_t)(t / D) * ld + nn + (t % D)];
+                s += pr;
+                sa += fabs(pr);
+            }
+            s = warp_sum(s);
+            sa = warp_sum(sa);
+            if (tid == 0) {
+                const double S = s_cpp - s;
+                if (!(fabs(S) > 1e-14 * (sa + fabs(s_cpp)))) s_fail = 2;
+                rn[0] = 1.0 / S;   // reuse rn[0] for 1/S
+            }
+        }
+        __syncthreads();
+        if (s_fail) {
+            if (tid == 0) { atomicOr(a.fail, 2u); atomicMin(a.bad, (unsigned long long)i); }
+            continue;
+        }
+        const double Sinv = rn[0];
+        if (tid == 0) {   // algorithmic bytes: A_s^{-1} restricted rows (triangle in layout 4), g, weights, 1/S, indices
+            const unsigned long long yb = a.layout == 4 ? (unsigned long long)mn * (mn + 1) / 2 + (unsigned long long)mn * (nn - mn)
+                                                        : (unsigned long long)mn * nn;
+            atomicAdd(a.alg, 8ull * (yb + (unsigned long long)nn * D + mn + 2) + 4ull * (nn + 1));
+        }
+        // Y[k][j] = (A_s^{-1})_{kj} = M[j][nn + D + k];  g[j][c] = M[j][nn + c]
+        if (a.layout == 4) {
+            const int64_t chunk = i >> 5;
+            const int lane = (int)(i & 31);
+            double* base = a.facT + chunk * a.pairs * 64;
+            const int MT = a.MT;
+            const int64_t tri = tri_col_start(MT, D);
+            const int64_t tri_pad = tri + (tri & 1);
+            // entries: column j < MT: Y[0..j][j], g[j][0..D-1]; column j >= MT: Y[0..MT-1][j], g[j][.]
+            for (int t = tid; t < nn * (MT + D); t += ST) {
+                const int j = t / (MT + D), q = t % (MT + D);
+                int64_t e;
+                double v;
+                if (q < MT) {
+                    const int k = q;
+                    if (j < MT && k > j) continue;
+                    v = k < mn ? M[(size_t)j * ld + nn + D + k] : 0.0;
+                    e = j < MT ? tri_col_start(j, D) + k : tri_pad + (int64_t)(j - MT) * (MT + D) + k;
+                } else {
+                    const int c = q - MT;
+                    v = M[(size_t)j * ld + nn + c];
+                    e = j < MT ? tri_col_start(j, D) + (j + 1) + c : tri_pad + (int64_t)(j - MT) * (MT + D) + MT + c;
+                }
+                base[((e >> 1) * 32 + lane) * 2 + (e & 1)] = v;
+            }
+            for (int j = tid; j < a.NN; j += ST)
+                a.ND[(chunk * a.NN + j) * 32 + lane] = j < nn ? ndof[j] : ndof[0];
+            for (int k = tid; k < MT; k += ST)
+                a.AUX[(chunk * (MT + 2) + k) * 32 + lane] = k < mn ? wnode[k] : 0.0;
+            if (tid == 0) {
+                a.AUX[(chunk * (MT + 2) + MT) * 32 + lane] = s_wp;
+                a.AUX[(chunk * (MT + 2) + MT + 1) * 32 + lane] = Sinv;
+                a.PD[chunk * 32 + lane] = pd;
+                a.NR[chunk * 32 + lane] = mn;
+            }
+        } else {
+            const int MT = a.MT;
+            double* Y = a.fac + a.foffs[i];            // MT x nn, column-major (stride MT)
+            double* g = Y + (size_t)MT * nn;           // nn * D
+            double* aux = g + (size_t)nn * D;          // MT weights, w_p, 1/S
+            for (int t = tid; t < nn * MT; t += ST) {
+                const int j = t / MT, k = t % MT;
+                Y[t] = k < mn ? M[(size_t)j * ld + nn + D + k] : 0.0;
+            }
+            for (int t = tid; t < nn * D; t += ST) g[t] = M[(size_t)(t / D) * ld + nn + (t % D)];
+            for (int k = tid; k < MT; k += ST) aux[k] = k < mn ? wnode[k] : 0.0;
+            for (int j = tid; j < nn; j += ST) a.nodes[a.nodeoffs[i] + j] = ndof[j];
+            if (tid == 0) {
+                aux[MT] = s_wp;
+                aux[MT + 1] = Sinv;
+                a.pdof[i] = pd;
+                a.nres_nodes[i] = mn;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// sweeps
+// ------------------------------------------------------------------------------------
+
+// one patch per thread (2D): MT restricted nodes, D components, NN nodes per patch (runtime)
+template <int MT, int D>
+__global__ void __launch_bounds__(128) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
+                                                                 const double2* __restrict__ W,
+                                                                 const int32_t* __restrict__ ND,
+                                                                 const int32_t* __restrict__ PD,
+                                                                 const int32_t* __restrict__ NR,
+                                                                 const double* __restrict__ AUX,
+                                                                 const double* __restrict__ r,
+                                                                 double* __restrict__ x, double omega) {
+    constexpr int TRI = MT * (MT + 1) / 2 + MT * D;
+    constexpr int TRI_PAD = TRI + (TRI & 1);
+    constexpr int RC = MT + D;   // entries per rectangular column
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t chunk = i >> 5;
+    const int lane = threadIdx.x & 31;
+    if (chunk >= nchunks) return;
+    const double2* wp = W + chunk * pairs * 32 + lane;
+    const int32_t* np_ = ND + chunk * (int64_t)NN * 32 + lane;
+    double acc[MT][D], rr[MT][D], gR[MT][D];
+    double gacc = 0.0;
+#pragma unroll
+    for (int k = 0; k < MT; ++k) {
+        const int nd = __ldcs(np_ + k * 32);
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            acc[k][c] = 0.0;
+            rr[k][c] = __ldg(r + nd + c);
+        }
+    }
+    double2 pv = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < MT; ++j) {
+        constexpr int dummy = 0;
+        (void)dummy;
+#pragma unroll
+        for (int q = 0; q <= j + D; ++q) {
+            const int e = j * (j + 1) / 2 + j * D + q;
+            if ((e & 1) == 0) pv = __ldcs(wp + (e >> 1) * 32);
+            const double v = (e & 1) ? pv.y : pv.x;
+            if (q <= j) {
+                const int k = q;
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    acc[k][c] = fma(v, rr[j][c], acc[k][c]);
+                    if (k != j) acc[j][c] = fma(v, rr[k][c], acc[j][c]);
+                }
+            } else {
+                const int c = q - j - 1;
+                gR[j][c] = v;
+                gacc = fma(v, rr[j][c], gacc);
+            }
+        }
+    }
+    // rectangular columns, two at a time (2 * RC entries = RC pairs)
+    const double2* wq0 = wp + (TRI_PAD / 2) * 32;
+    for (int j0 = MT; j0 < NN; j0 += 2) {
+        double ra[D], rb[D];
+        const int n0 = __ldcs(np_ + j0 * 32), n1 = __ldcs(np_ + (j0 + 1) * 32);
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            ra[c] = __ldg(r + n0 + c);
+            rb[c] = __ldg(r + n1 + c);
+        }
+        const double2* wq = wq0 + (int64_t)((j0 - MT) / 2) * RC * 32;
+#pragma unroll
+        for (int p = 0; p < RC; ++p) {
+            const double2 v2 = __ldcs(wq + p * 32);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int e = 2 * p + h;
+                const double v = h ? v2.y : v2.x;
+                const bool second = e >= RC;
+                const int q = second ? e - RC : e;
+                if (q < MT) {
+#pragma unroll
+                    for (int c = 0; c < D; ++c) acc[q][c] = fma(v, second ? rb[c] : ra[c], acc[q][c]);
+                } else {
+                    gacc = fma(v, second ? rb[q - MT] : ra[q - MT], gacc);
+                }
+            }
+        }
+    }
+    const double* aux = AUX + chunk * (MT + 2) * 32 + lane;
+    const int pd = PD[i];
+    const double t = aux[(MT + 1) * 32] * (gacc - __ldg(r + pd));
+    if (i >= np) return;   // padding slots of the last chunk
+    const int m = NR[i];
+#pragma unroll
+    for (int k = 0; k < MT; ++k) {
+        if (k < m) {
+            const double wk = omega * aux[k * 32];
+            const int nd = np_[k * 32];
+#pragma unroll
+            for (int c = 0; c < D; ++c) atomicAdd(x + nd + c, wk * fma(gR[k][c], t, acc[k][c]));
+        }
+    }
+    const double wpr = aux[MT * 32];
+    if (wpr != 0.0) atomicAdd(x + pd, omega * wpr * (-t));
+}
+
+// one patch per warp (3D and large patches): lane k owns restricted node k
+template <int D>
+__global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int MT, int nnmax,
+                                                               const int64_t* __restrict__ foffs,
+                                                               const int64_t* __restrict__ nodeoffs,
+                                                               const int32_t* __restrict__ nodes,
+                                                               const int32_t* __restrict__ pdof,
+                                                               const int32_t* __restrict__ nresn,
+                                                               const double* __restrict__ fac,
+                                                               const double* __restrict__ r, double* __restrict__ x,
+                                                               double omega) {
+    extern __shared__ double sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* rl = sm + (size_t)warp * nnmax * D;
+    for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < np; i += (int64_t)gridDim.x * 8) {
+        const int64_t no = nodeoffs[i];
+        const int nn = (int)(nodeoffs[i + 1] - no);
+        for (int t = lane; t < nn * D; t += 32) rl[t] = __ldg(r + nodes[no + t / D] + (t % D));
+        __syncwarp();
+        const double* Y = fac + foffs[i];
+        const double* g = Y + (size_t)MT * nn;
+        const double* aux = g + (size_t)nn * D;
+        double acc[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc[c] = 0.0;
+        if (lane < MT) {
+            for (int j = 0; j < nn; ++j) {
+                const double y = __ldcs(Y + (size_t)j * MT + lane);
+#pragma unroll
+                for (int c = 0; c < D; ++c) acc[c] = fma(y, rl[j * D + c], acc[c]);
+            }
+        }
+        double gs = 0.0;
+        for (int t = lane; t < nn * D; t += 32) gs = fma(__ldcs(g + t), rl[t], gs);
+        gs = warp_sum(gs);
+        const double t = aux[MT + 1] * (gs - __ldg(r + pdof[i]));
+        if (lane < nresn[i]) {
+            const double wk = omega * aux[lane];
+            const int nd = nodes[no + lane];
+#pragma unroll
+            for (int c = 0; c < D; ++c) atomicAdd(x + nd + c, wk * fma(g[lane * D + c], t, acc[c]));
+        }
+        if (lane == 0) atomicAdd(x + pdof[i], omega * aux[MT] * (-t));
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------
+
+static int pick_MT(int mnmax) {
+    static const int cand[] = {1, 2, 4, 9, 16, 27, 32};
+    for (int c : cand)
+        if (c >= mnmax) return c;
+    return -1;
+}
+
+rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D, int kernel_choice, Factors& F,
+                           int64_t* bad_patch, bool* applicable, cudaStream_t s) {
+    *applicable = false;
+    if (D < 1 || D > 3 || nvel <= 0) return RAV_OK;
+    // node bounds from the patch sizes (one pressure DoF per patch)
+    const int nnmax = (P.nmax - 1) / D;
+    const int mnmax = std::max(1, (P.nresmax - 1) / D);
+    if (nnmax < 1 || nnmax > 200) return RAV_OK;
+    const int MT = pick_MT(mnmax);
+    if (MT < 0) return RAV_OK;
+    SchurArgs a{};
+    a.rp = A.rp;
+    a.ci = A.ci;
+    a.val = A.val;
+    a.np = P.n_patches;
+    a.poffs = P.offs;
+    a.pdofs = P.dofs;
+    a.pw = P.w;
+    a.nvel = nvel;
+    a.D = D;
+    a.nnmax = nnmax;
+    a.mnmax = MT;
+    a.ld = nnmax + D + MT;
+    if ((a.ld & 15) == 0) a.ld += 1;
+    a.MT = MT;
+    const bool thread = kernel_choice != RAV_KERNEL_WARP && D == 2 && MT <= 9 && nnmax <= 32;
+    F.nchunks = cdiv(P.n_patches, 32);
+    if (thread) {
+        F.layout = 4;
+        F.MT = MT;
+        F.D = D;
+        F.NN = std::max(MT, nnmax);
+        if ((F.NN - MT) & 1) F.NN += 1;
+        int64_t tri = (int64_t)MT * (MT + 1) / 2 + (int64_t)MT * D;
+        tri += tri & 1;
+        F.pairs = (tri + (int64_t)(F.NN - MT) * (MT + D)) / 2;
+        size_t fb = sizeof(double) * 2 * F.pairs * 32 * F.nchunks;
+        RAV_CUDA(cudaMalloc(&F.facT, fb));
+        RAV_CUDA(cudaMalloc(&F.DT, sizeof(int32_t) * F.NN * 32 * F.nchunks));
+        RAV_CUDA(cudaMalloc(&F.PD, sizeof(int32_t) * 32 * F.nchunks));
+        RAV_CUDA(cudaMalloc(&F.NR, sizeof(int32_t) * 32 * F.nchunks));
+        RAV_CUDA(cudaMalloc(&F.WT, sizeof(double) * (MT + 2) * 32 * F.nchunks));
+        RAV_CUDA(cudaMemsetAsync(F.facT, 0, fb, s));
+        RAV_CUDA(cudaMemsetAsync(F.DT, 0, sizeof(int32_t) * F.NN * 32 * F.nchunks, s));
+        RAV_CUDA(cudaMemsetAsync(F.PD, 0, sizeof(int32_t) * 32 * F.nchunks, s));
+        RAV_CUDA(cudaMemsetAsync(F.NR, 0, sizeof(int32_t) * 32 * F.nchunks, s));
+        RAV_CUDA(cudaMemsetAsync(F.WT, 0, sizeof(double) * (MT + 2) * 32 * F.nchunks, s));
+        F.bytes = (int64_t)fb;
+        a.layout = 4;
+        a.NN = F.NN;
+        a.pairs = F.pairs;
+        a.facT = F.facT;
+        a.ND = F.DT;
+        a.PD = F.PD;
+        a.NR = F.NR;
+        a.AUX = F.WT;
+    } else {
+        F.layout = 5;
+        F.MT = MT;
+        F.D = D;
+        F.NN = nnmax;
+        // per-patch sizes: nn_i = (n_i - 1) / D nodes -> MT*nn + nn*D + MT + 2 doubles
+        std::vector<int64_t> ho(P.n_patches + 1), fo(P.n_patches + 1), no(P.n_patches + 1);
+        RAV_CUDA(cudaMemcpy(ho.data(), P.offs, sizeof(int64_t) * (P.n_patches + 1), cudaMemcpyDeviceToHost));
+        fo[0] = 0;
+        no[0] = 0;
+        for (int64_t i = 0; i < P.n_patches; ++i) {
+            const int64_t nn = (ho[i + 1] - ho[i] - 1) / D;
+            int64_t sz = (int64_t)MT * nn + nn * D + MT + 2;
+            sz += sz & 1;
+            fo[i + 1] = fo[i] + sz;
+            no[i + 1] = no[i] + nn;
+        }
+        RAV_CUDA(cudaMalloc(&F.foffs, sizeof(int64_t) * (P.n_patches + 1)));
+        RAV_CUDA(cudaMalloc(&F.nodeoffs, sizeof(int64_t) * (P.n_patches + 1)));
+        RAV_CUDA(cudaMalloc(&F.fac, sizeof(double) * std::max<int64_t>(1, fo.back())));
+        RAV_CUDA(cudaMalloc(&F.nodes, sizeof(int32_t) * std::max<int64_t>(1, no.back())));
+        RAV_CUDA(cudaMalloc(&F.PD, sizeof(int32_t) * P.n_patches));
+        RAV_CUDA(cudaMalloc(&F.NR, sizeof(int32_t) * P.n_patches));
+        RAV_CUDA(cudaMemcpy(F.foffs, fo.data(), sizeof(int64_t) * (P.n_patches + 1), cudaMemcpyHostToDevice));
+        RAV_CUDA(cudaMemcpy(F.nodeoffs, no.data(), sizeof(int64_t) * (P.n_patches + 1), cudaMemcpyHostToDevice));
+        RAV_CUDA(cudaMemsetAsync(F.fac, 0, sizeof(double) * std::max<int64_t>(1, fo.back()), s));
+        F.bytes = (int64_t)sizeof(double) * fo.back() + sizeof(int32_t) * no.back();
+        a.layout = 5;
+        a.foffs = F.foffs;
+        a.fac = F.fac;
+        a.nodes = F.nodes;
+        a.nodeoffs = F.nodeoffs;
+        a.pdof = F.PD;
+        a.nres_nodes = F.NR;
+    }
+    unsigned int* fail = nullptr;
+    unsigned long long* bad = nullptr;
+    unsigned long long* alg = nullptr;
+    RAV_CUDA(cudaMallocAsync(&fail, sizeof(unsigned int), s));
+    RAV_CUDA(cudaMallocAsync(&bad, sizeof(unsigned long long), s));
+    RAV_CUDA(cudaMallocAsync(&alg, sizeof(unsigned long long), s));
+    RAV_CUDA(cudaMemsetAsync(fail, 0, sizeof(unsigned int), s));
+    RAV_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+    RAV_CUDA(cudaMemsetAsync(alg, 0, sizeof(unsigned long long), s));
+    a.fail = fail;
+    a.bad = bad;
+    a.alg = alg;
+    const size_t shmem = sizeof(double) * ((size_t)a.nnmax * a.ld + a.nnmax + (size_t)a.nnmax * D + a.nnmax) +
+                         sizeof(int32_t) * 3 * a.nnmax + 64;
+    if (shmem > 220 * 1024) {
+        factors_free(F);
+        cudaFreeAsync(fail, s);
+        cudaFreeAsync(bad, s);
+        return RAV_OK;
+    }
+    if (shmem > 48 * 1024)
+        RAV_CUDA(cudaFuncSetAttribute(schur_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(16, (220 * 1024) / shmem));
+    const int grid = (int)std::min<int64_t>(P.n_patches, (int64_t)num_sms() * per_sm);
+    schur_factor_kernel<<<grid, ST, shmem, s>>>(a);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    unsigned int h_fail = 0;
+    unsigned long long h_bad = 0, h_alg = 0;
+    RAV_CUDA(cudaMemcpyAsync(&h_fail, fail, sizeof(h_fail), cudaMemcpyDeviceToHost, s));
+    RAV_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof(h_bad), cudaMemcpyDeviceToHost, s));
+    RAV_CUDA(cudaMemcpyAsync(&h_alg, alg, sizeof(h_alg), cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(fail, s);
+    cudaFreeAsync(bad, s);
+    cudaFreeAsync(alg, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    F.alg_bytes = (int64_t)h_alg;
+    if (h_fail & 1u) {   // structure does not hold: caller uses the generic formats
+        factors_free(F);
+        return RAV_OK;
+    }
+    *applicable = true;
+    if (h_fail & 2u) {
+        if (bad_patch) *bad_patch = (int64_t)h_bad;
+        set_error("singular local system in patch %lld", (long long)h_bad);
+        return RAV_ERR_SINGULAR_LOCAL;
+    }
+    if (bad_patch) *bad_patch = -1;
+    return RAV_OK;
+}
+
+// ---- canonical rows export (parity tests): W[a][b] = w_a * (L_i^{-1})[a][b] ------------
+struct SchurView {
+    int layout, MT, D, NN;
+    int64_t pairs;
+    const double* facT;
+    const int32_t* ND;
+    const double* AUX;
+    const int64_t* foffs;
+    const double* fac;
+    const int32_t* nodes;
+    const int64_t* nodeoffs;
+};
+
+__device__ double sv_entry(const SchurView& v, int64_t i, int64_t e) {
+    const int64_t chunk = i >> 5;
+    const int lane = (int)(i & 31);
+    return v.facT[((chunk * v.pairs + (e >> 1)) * 32 + lane) * 2 + (e & 1)];
+}
+__device__ double sv_Y(const SchurView& v, int64_t i, int nn, int k, int j) {   // (A_s^{-1})_{kj}, k restricted
+    if (v.layout == 5) return v.fac[v.foffs[i] + (int64_t)j * v.MT + k];
+    const int64_t tri = tri_col_start(v.MT, v.D), tri_pad = tri + (tri & 1);
+    if (j < v.MT) {
+        if (k <= j) return sv_entry(v, i, tri_col_start(j, v.D) + k);
+        return sv_entry(v, i, tri_col_start(k, v.D) + j);
+    }
+    return sv_entry(v, i, tri_pad + (int64_t)(j - v.MT) * (v.MT + v.D) + k);
+}
+__device__ double sv_g(const SchurView& v, int64_t i, int nn, int j, int c) {
+    if (v.layout == 5) return v.fac[v.foffs[i] + (int64_t)v.MT * nn + (int64_t)j * v.D + c];
+    const int64_t tri = tri_col_start(v.MT, v.D), tri_pad = tri + (tri & 1);
+    if (j < v.MT) return sv_entry(v, i, tri_col_start(j, v.D) + j + 1 + c);
+    return sv_entry(v, i, tri_pad + (int64_t)(j - v.MT) * (v.MT + v.D) + v.MT + c);
+}
+__device__ double sv_aux(const SchurView& v, int64_t i, int nn, int q) {   // q < MT: w_k; MT: w_p; MT+1: 1/S
+    if (v.layout == 5) return v.fac[v.foffs[i] + (int64_t)v.MT * nn + (int64_t)nn * v.D + q];
+    const int64_t chunk = i >> 5;
+    return v.AUX[(chunk * (v.MT + 2) + q) * 32 + (i & 31)];
+}
+
+__global__ void export_schur_kernel(int64_t np, const int64_t* offs, const int32_t* dofs, const double* w,
+                                    const int64_t* roffs, int64_t nvel, SchurView v, double* rows) {
+    for (int64_t i = blockIdx.x; i < np; i += gridDim.x) {
+        const int64_t off = offs[i];
+        const int n = (int)(offs[i + 1] - off);
+        const int D = v.D;
+        const int nn = (n - 1) / D;
+        int m = 0;
+        for (int t = 0; t < n; ++t) m += w[off + t] > 0.0;
+        const double Sinv = sv_aux(v, i, nn, v.MT + 1);
+        // local DoF -> node index: restricted nodes first in patch order; node j of DoF = rank among nodes
+        for (int t = threadIdx.x; t < m * n; t += blockDim.x) {
+            const int ra = t / n, cb = t % n;
+            const int da = dofs[off + ra], db = dofs[off + cb];
+            // node index of a velocity DoF: count distinct nodes before it in patch order
+            auto node_of = [&](int idx) {
+                int cnt = 0, prev = -1;
+                for (int u = 0; u <= idx; ++u) {
+                    const int du = dofs[off + u];
+                    if (du >= nvel) continue;
+                    const int nd = du / D;
+                    if (nd != prev) { ++cnt; prev = nd; }
+                }
+                return cnt - 1;
+            };
+            double val;
+            if (da < nvel) {
+                const int k = node_of(ra), ca = da % D;
+                const double wk = w[off + ra];
+                if (db < nvel) {
+                    const int j = node_of(cb), cc = db % D;
+                    val = (ca == cc ? sv_Y(v, i, nn, k, j) : 0.0) + sv_g(v, i, nn, k, ca) * Sinv * sv_g(v, i, nn, j, cc);
+                } else {
+                    val = -sv_g(v, i, nn, k, ca) * Sinv;
+                }
+                val *= wk;
+            } else {
+                const double wp = w[off + ra];
+                if (db < nvel) val = -Sinv * sv_g(v, i, nn, node_of(cb), db % D);
+                else val = Sinv;
+                val *= wp;
+            }
+            rows[roffs[i] + t] = val;
+        }
+    }
+}
+
+__global__ void rows_size_kernel(int64_t np, const int64_t* offs, const int32_t* nres, int64_t* sz);
+
+rav_status export_schur_rows(const PatchSet& P, const Factors& F, int64_t nvel, double* rows, cudaStream_t s) {
+    int64_t *sz = nullptr, *roffs = nullptr;
+    RAV_CUDA(cudaMallocAsync(&sz, sizeof(int64_t) * P.n_patches, s));
+    RAV_CUDA(cudaMallocAsync(&roffs, sizeof(int64_t) * (P.n_patches + 1), s));
+    const int nb = (int)std::min<int64_t>(cdiv(P.n_patches, 256), (int64_t)num_sms() * 16);
+    rows_size_kernel<<<nb, 256, 0, s>>>(P.n_patches, P.offs, P.nres, sz);
+    count_launch();
+    RAV_TRY(gen::counts_to_rowptr(sz, roffs, P.n_patches, s));
+    SchurView v{F.layout, F.MT, F.D, F.NN, F.pairs, F.facT, F.DT, F.WT, F.foffs, F.fac, F.nodes, F.nodeoffs};
+    const int g = (int)std::min<int64_t>(P.n_patches, (int64_t)num_sms() * 8);
+    export_schur_kernel<<<g, 128, 0, s>>>(P.n_patches, P.offs, P.dofs, P.w, roffs, nvel, v, rows);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    cudaFreeAsync(sz, s);
+    cudaFreeAsync(roffs, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    return RAV_OK;
+}
+
+template <int MT>
+static void launch_schur_thread(int64_t np, const Factors& F, const double* r, double* x, double omega,
+                                cudaStream_t s) {
+    const int blocks = (int)cdiv(F.nchunks * 32, 128);
+    schur_sweep_thread_kernel<MT, 2><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
+                                                            reinterpret_cast<const double2*>(F.facT), F.DT, F.PD,
+                                                            F.NR, F.WT, r, x, omega);
+}
+
+rav_status launch_schur_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
+                              cudaStream_t s) {
+    if (F.layout == 4) {
+        switch (F.MT) {
+            case 1: launch_schur_thread<1>(P.n_patches, F, r, x, omega, s); break;
+            case 2: launch_schur_thread<2>(P.n_patches, F, r, x, omega, s); break;
+            case 4: launch_schur_thread<4>(P.n_patches, F, r, x, omega, s); break;
+            case 9: launch_schur_thread<9>(P.n_patches, F, r, x, omega, s); break;
+            default: set_error("schur thread kernel: unsupported MT %d", F.MT); return RAV_ERR_ARG;
+        }
+    } else {
+        const size_t shmem = sizeof(double) * (size_t)F.NN * F.D * 8;
+        const int blocks = (int)std::min<int64_t>(cdiv(P.n_patches, 8), (int64_t)num_sms() * 16);
+        if (F.D == 3)
+            schur_sweep_warp_kernel<3><<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs,
+                                                                  F.nodes, F.PD, F.NR, F.fac, r, x, omega);
+        else if (F.D == 2)
+            schur_sweep_warp_kernel<2><<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs,
+                                                                  F.nodes, F.PD, F.NR, F.fac, r, x, omega);
+        else
+            schur_sweep_warp_kernel<1><<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs,
+                                                                  F.nodes, F.PD, F.NR, F.fac, r, x, omega);
+    }
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}
+
+}  // namespace rav

@@ -503,6 +503,9 @@ void factors_free(Factors& F) {
     if (F.DT) cudaFree(F.DT);
     if (F.NR) cudaFree(F.NR);
     if (F.WT) cudaFree(F.WT);
+    if (F.PD) cudaFree(F.PD);
+    if (F.nodes) cudaFree(F.nodes);
+    if (F.nodeoffs) cudaFree(F.nodeoffs);
     F = Factors{};
 }
 

@@ -21,7 +21,7 @@ RAV_OK = 0
 STATUS = {0: "RAV_OK", 1: "RAV_ERR_ARG", 2: "RAV_ERR_SINGULAR_LOCAL", 3: "RAV_ERR_SINGULAR_COARSE",
           4: "RAV_ERR_OOM", 5: "RAV_ERR_CUDA", 6: "RAV_ERR_COMM", 7: "RAV_ERR_DIVERGED"}
 VARIANT_ROWS, VARIANT_DIAG = 0, 1
-KERNEL_AUTO, KERNEL_WARP, KERNEL_THREAD = 0, 1, 2
+KERNEL_AUTO, KERNEL_WARP, KERNEL_THREAD, KERNEL_SYM, KERNEL_SCHUR = 0, 1, 2, 3, 4
 WEIGHTS = {"pou": 0, "own": 1, "full": 2}
 
 
@@ -52,7 +52,7 @@ class RavPatches(C.Structure):
 
 class RavOpts(C.Structure):
     _fields_ = [("variant", C.c_int32), ("kernel", C.c_int32), ("deterministic", C.c_int32),
-                ("n_vel", C.c_int64), ("stream", C.c_void_p)]
+                ("n_vel", C.c_int64), ("stream", C.c_void_p), ("block_dim", C.c_int32)]
 
 
 def _load():
@@ -76,7 +76,8 @@ def _load():
         "rav_export_rows": [vp, vp],
         "rav_sweep_bytes": [vp, P(dbl), P(dbl), P(dbl)],
         "rav_set_stream": [vp, vp],
-        "mg_setup": [C.c_int, P(RavCsr), P(RavPatches), P(RavCsr), i64, P(RavOpts), P(vp), P(C.c_int), P(i64)],
+        "mg_setup": [C.c_int, P(RavCsr), P(RavPatches), P(RavCsr), P(i64), i64, P(RavOpts), P(vp), P(C.c_int),
+                     P(i64)],
         "mg_vcycle": [vp, vp, vp, C.c_int, C.c_int, dbl],
         "mg_solve": [vp, vp, vp, C.c_int, C.c_int, dbl, dbl, C.c_int, P(C.c_int), vp],
         "mg_set_stream": [vp, vp],
@@ -202,10 +203,12 @@ class Smoother:
     """rav_setup / rav_smooth / rav_destroy (Eq. 13)."""
 
     def __init__(self, A: Dict, P: Dict, variant: int = VARIANT_ROWS, kernel: int = KERNEL_AUTO,
-                 stream=None):
+                 stream=None, block_dim: Optional[int] = None):
         self.n = A["n"]
         self._keep = (A, P)
-        opts = RavOpts(variant, kernel, 0, A.get("nvel", 0), _stream(stream))
+        if block_dim is None:   # the generator's interleaved velocity numbering (R9)
+            block_dim = A["problem"]["dim"] if "problem" in A else 0
+        opts = RavOpts(variant, kernel, 0, A.get("nvel", 0), _stream(stream), int(block_dim))
         ctx = C.c_void_p()
         bad = C.c_int64(-1)
         st = lib.rav_setup(C.byref(csr(A)), C.byref(patches_struct(P)), C.byref(opts), C.byref(ctx), C.byref(bad))
@@ -263,7 +266,8 @@ class Multigrid:
     """mg_setup / mg_vcycle / mg_solve (P:84-90, P:132-134)."""
 
     def __init__(self, levels: Sequence[Dict], prolongations: Sequence[Optional[Dict]], coarse_pin: int,
-                 variant: int = VARIANT_ROWS, kernel: int = KERNEL_AUTO, stream=None):
+                 variant: int = VARIANT_ROWS, kernel: int = KERNEL_AUTO, stream=None,
+                 block_dim: Optional[int] = None):
         L = len(levels)
         self.L = L
         self.n = levels[-1]["n"]
@@ -273,10 +277,15 @@ class Multigrid:
         Pr = (RavCsr * L)()
         for l in range(1, L):
             Pr[l] = csr(prolongations[l], n_cols=prolongations[l]["nc"])
-        opts = RavOpts(variant, kernel, 0, levels[-1].get("nvel", 0), _stream(stream))
+        if block_dim is None:
+            block_dim = levels[-1]["problem"]["dim"] if "problem" in levels[-1] else 0
+        opts = RavOpts(variant, kernel, 0, levels[-1].get("nvel", 0), _stream(stream), int(block_dim))
+        nvel = (C.c_int64 * L)(*[int(A.get("nvel", 0)) for A in levels])
+        self._keep = (levels, prolongations, nvel)
         ctx = C.c_void_p()
         bl, bp = C.c_int(-1), C.c_int64(-1)
-        st = lib.mg_setup(L, As, Ps, Pr, int(coarse_pin), C.byref(opts), C.byref(ctx), C.byref(bl), C.byref(bp))
+        st = lib.mg_setup(L, As, Ps, Pr, nvel, int(coarse_pin), C.byref(opts), C.byref(ctx), C.byref(bl),
+                          C.byref(bp))
         _check(st, bad_patch=bp.value, bad_level=bl.value)
         self.ctx = ctx
 
