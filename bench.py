@@ -141,14 +141,21 @@ def run_reference(args):
     return 0
 
 
-def run_vcycle_c3(rg, si, stream, dist):
-    """mg_solve on BASELINE config 3: 2048^2 MMS, seeded eta, 10 levels (4^2
-    coarsest), V(2,2)-RAV, omega 0.66, x0 = 0, to ||r|| <= 1e-8 ||r0||.
-    Device-timed with CUDA events around mg_solve (which reads back one norm
-    per cycle for the stopping test)."""
+VCYCLE_DESC = {
+    "c3": "c3: 2048^2 Q2-Q1 MMS, seeded eta, 10 levels (4^2 coarsest), V(2,2)-RAV omega 0.66, x0 = 0",
+    "c4": "c4: 32^3 Q2-Q1 lid-driven cavity, seeded eta, 5 levels (2^3 coarsest, reading R14), "
+          "V(2,2)-RAV omega 0.66, x0 = 0",
+}
+
+
+def run_vcycle(name, rg, si, stream, dist):
+    """mg_solve on a BASELINE V-cycle config (c3: 2048^2 MMS, 10 levels; c4:
+    32^3 cavity, 5 levels), V(2,2)-RAV, omega 0.66, x0 = 0, to ||r|| <= 1e-8
+    ||r0||.  Device-timed with CUDA events around mg_solve (which reads back
+    one norm per cycle for the stopping test)."""
     import torch
-    c = si.CONFIGS["c3"]
-    prob = si.config_problem("c3")
+    c = si.CONFIGS[name]
+    prob = si.config_problem(name)
     t0 = time.perf_counter()
     mg, fine = rg.build_hierarchy(prob, c["levels"], "pou")
     torch.cuda.synchronize()
@@ -175,8 +182,7 @@ def run_vcycle_c3(rg, si, stream, dist):
         t = float(tt.item())
     launches = mg.last_launches
     rho = (hist[-1] / hist[0]) ** (1.0 / max(iters, 1))
-    out = {"config": "c3: 2048^2 Q2-Q1 MMS, seeded eta, 10 levels (4^2 coarsest), V(2,2)-RAV omega 0.66, x0 = 0",
-           "free_dofs": fine["n"], "rtol": c["rtol"], "cycles": iters, "converged": bool(hist[-1] <= c["rtol"] * hist[0]),
+    out = {"config": VCYCLE_DESC[name], "free_dofs": fine["n"], "rtol": c["rtol"], "cycles": iters, "converged": bool(hist[-1] <= c["rtol"] * hist[0]),
            "time_to_rtol_s": t, "ms_per_cycle": t / max(iters, 1) * 1e3, "avg_reduction_factor": rho,
            "setup_s": setup_s, "gpu_launches": launches, "timing": "CUDA events around mg_solve, best of 3"}
     mg.close()
@@ -269,11 +275,15 @@ def run_gpu(args):
     resid_ms = e0.elapsed_time(e1) / nk
     peak, peak_kind = load_peaks()
     achieved = bytes_info["sweep"] / (sweep_ms * 1e-3) / 1e9
+    kernel_name = sm.kernel_name
+    # DRAM traffic per launch from the committed ncu capture of this same kernel (or null)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "sweep_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("bytes_per_launch")
+            tj = json.load(open(tpath))
+            if kernel_name.split(" ")[0] in tj.get("kernel", ""):
+                traffic = tj.get("bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -298,7 +308,7 @@ def run_gpu(args):
     if not args.no_vcycle:
         del sm, G
         torch.cuda.empty_cache()
-        vcyc = run_vcycle_c3(rg, si, stream, dist)
+        vcyc = {name: run_vcycle(name, rg, si, stream, dist) for name in ("c3", "c4")}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample) ------------------
     cpu = None
@@ -321,7 +331,7 @@ def run_gpu(args):
                    "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "sweep_thread_kernel<19> (rav_apply)", "kernel_ms": sweep_ms,
+                     "kernel": kernel_name + " via rav_apply", "kernel_ms": sweep_ms,
                      "algorithmic_bytes_per_launch": bytes_info["sweep"]},
         "residual_kernel": {"ms": resid_ms, "algorithmic_bytes": bytes_info["residual"],
                             "achieved_gbs": bytes_info["residual"] / (resid_ms * 1e-3) / 1e9},

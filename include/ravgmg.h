@@ -207,6 +207,9 @@ rav_status rav_export_rows(const rav_ctx* ctx, double* rows);
 rav_status rav_sweep_bytes(const rav_ctx* ctx, double* bytes_sweep, double* bytes_residual,
                            double* flops);
 
+/* Name of the sweep kernel / factor format chosen by rav_setup (static string). */
+const char* rav_kernel_name(const rav_ctx* ctx);
+
 rav_status rav_set_stream(rav_ctx* ctx, void* stream);
 void rav_destroy(rav_ctx* ctx);
 

@@ -278,6 +278,18 @@ rav_status rav_sweep_bytes(const rav_ctx* c, double* bytes_sweep, double* bytes_
 
 int64_t rav_last_launches(const rav_ctx* c) { return c ? c->last_launches : 0; }
 
+const char* rav_kernel_name(const rav_ctx* c) {
+    if (!c) return "";
+    switch (c->F.layout) {
+        case 1: return "sweep_warp_kernel (rows, row-major per patch)";
+        case 2: return "sweep_thread_kernel (rows, SoA chunks)";
+        case 3: return "sweep_sym_kernel (symmetric restricted block, SoA chunks)";
+        case 4: return "schur_sweep_thread_kernel (factored Schur rows, SoA chunks)";
+        case 5: return "schur_sweep_warp_kernel (factored Schur rows, per patch)";
+        default: return "unknown";
+    }
+}
+
 void rav_destroy(rav_ctx* c) {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);

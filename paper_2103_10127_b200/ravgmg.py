@@ -90,6 +90,8 @@ def _load():
     L.rav_destroy.restype = None
     L.mg_destroy.argtypes = [vp]
     L.mg_destroy.restype = None
+    L.rav_kernel_name.argtypes = [vp]
+    L.rav_kernel_name.restype = C.c_char_p
     L.rav_last_error.restype = C.c_char_p
     L.rav_version.restype = C.c_char_p
     L.rav_last_launches.argtypes = [vp]
@@ -246,6 +248,10 @@ class Smoother:
     @property
     def last_launches(self) -> int:
         return int(lib.rav_last_launches(self.ctx))
+
+    @property
+    def kernel_name(self) -> str:
+        return lib.rav_kernel_name(self.ctx).decode()
 
     def set_stream(self, stream):
         _check(lib.rav_set_stream(self.ctx, _stream(stream)))
