@@ -134,9 +134,16 @@ typedef struct {
 } rav_patches;
 
 enum {
-    RAV_VARIANT_ROWS = 0,       /* precomputed weighted rows of L_i^{-1} */
-    RAV_VARIANT_DIAG = 1        /* diagonal Vanka: A_i replaced by diag(A_i) (R17); needs
-                                   exactly one pressure DoF (n_vel <= dof) per patch */
+    RAV_VARIANT_ROWS = 0,       /* additive: RAV (Eq. 13) / AV (Eq. 12) from the weights */
+    RAV_VARIANT_DIAG = 1,       /* diagonal Vanka: A_i replaced by diag(A_i) (R17); closed form
+                                   when block_dim > 0 and the patch structure allows it */
+    RAV_VARIANT_MV = 2          /* multiplicative Vanka (Eq. 11) in colours (R10): per colour
+                                   all patches relax concurrently with a fresh local residual
+                                   (Eq. 15) and full prolongation R_i^T; needs block_dim > 0,
+                                   the Schur structure and rav_set_colors.  Same-colour patches
+                                   must share no DoF and not be coupled through L (the caller's
+                                   colouring guarantees it; then the result equals sequential MV
+                                   in colour-major order). */
 };
 
 enum {
@@ -206,6 +213,11 @@ rav_status rav_export_rows(const rav_ctx* ctx, double* rows);
  * flops = 2 sum nres_i n_i + 2 nnz. */
 rav_status rav_sweep_bytes(const rav_ctx* ctx, double* bytes_sweep, double* bytes_residual,
                            double* flops);
+
+/* Colouring for RAV_VARIANT_MV (host arrays): colour c holds patches
+ * patch_ids[color_offs[c] .. color_offs[c+1]) and colours run in order c = 0,
+ * 1, ...; patch_ids must be a permutation of 0..n_patches-1.  Copied. */
+rav_status rav_set_colors(rav_ctx* ctx, int n_colors, const int64_t* color_offs, const int32_t* patch_ids);
 
 /* Name of the sweep kernel / factor format chosen by rav_setup (static string). */
 const char* rav_kernel_name(const rav_ctx* ctx);

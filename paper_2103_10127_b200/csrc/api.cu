@@ -73,6 +73,9 @@ struct rav_ctx {
     double* hb = nullptr;
     GraphCache graph;
     int64_t last_launches = 0;
+    // multicoloured MV (RAV_VARIANT_MV): colour c = patches plist[coffs[c] .. coffs[c+1])
+    std::vector<int64_t> coffs;
+    int32_t* plist = nullptr;
 };
 
 struct mg_level {
@@ -102,6 +105,12 @@ namespace rav {
 
 static rav_status smooth_launches(rav_ctx* c, double* x, const double* b, int nu, double omega) {
     for (int k = 0; k < nu; ++k) {
+        if (c->variant == RAV_VARIANT_MV) {   // colour by colour, fresh local residuals (Eq. 11, 15)
+            for (size_t q = 0; q + 1 < c->coffs.size(); ++q)
+                RAV_TRY(launch_mv_color(c->A, c->F, c->coffs[q + 1] - c->coffs[q], c->plist + c->coffs[q], b, x,
+                                        omega, c->stream));
+            continue;
+        }
         RAV_TRY(launch_residual(c->A, x, b, c->r, c->stream));
         RAV_TRY(launch_sweep(c->P, c->F, c->r, x, omega, c->stream));
     }
@@ -153,7 +162,10 @@ rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opt
     if (bad_patch) *bad_patch = -1;
     rav_opts o{};
     if (opts) o = *opts;
-    if (o.variant != RAV_VARIANT_ROWS && o.variant != RAV_VARIANT_DIAG) { set_error("rav_setup: bad variant"); return RAV_ERR_ARG; }
+    if (o.variant != RAV_VARIANT_ROWS && o.variant != RAV_VARIANT_DIAG && o.variant != RAV_VARIANT_MV) {
+        set_error("rav_setup: bad variant");
+        return RAV_ERR_ARG;
+    }
     if (o.deterministic) { set_error("rav_setup: deterministic scatter not available in this build"); return RAV_ERR_ARG; }
     if (A->n_rows != A->n_cols) { set_error("rav_setup: L must be square"); return RAV_ERR_ARG; }
     rav_ctx* c = new rav_ctx();
@@ -161,14 +173,16 @@ rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opt
     c->variant = o.variant;
     c->nvel = o.n_vel;
     rav_status st = csr_upload(A, c->A, c->stream);
-    if (st == RAV_OK) st = sell_build(c->A, c->stream);
+    if (st == RAV_OK && o.variant != RAV_VARIANT_MV) st = sell_build(c->A, c->stream);
     if (st == RAV_OK) st = patches_upload(P, A->n_rows, c->P, c->stream);
     bool done = false;
-    if (st == RAV_OK && o.variant == RAV_VARIANT_ROWS && o.block_dim > 0 &&
-        (o.kernel == RAV_KERNEL_AUTO || o.kernel == RAV_KERNEL_SCHUR)) {
-        st = schur_factorize(c->A, c->P, o.n_vel, o.block_dim, o.kernel, c->F, bad_patch, &done, c->stream);
-        if (st == RAV_OK && !done && o.kernel == RAV_KERNEL_SCHUR) {
-            set_error("rav_setup: RAV_KERNEL_SCHUR requested but the patches lack the I_d (x) A_s / one-pressure structure");
+    const bool want_schur = o.block_dim > 0 && (o.kernel == RAV_KERNEL_AUTO || o.kernel == RAV_KERNEL_SCHUR);
+    if (st == RAV_OK && (want_schur || o.variant == RAV_VARIANT_MV)) {
+        const int mode = o.variant == RAV_VARIANT_DIAG ? 1 : (o.variant == RAV_VARIANT_MV ? 2 : 0);
+        st = schur_factorize(c->A, c->P, o.n_vel, o.block_dim, o.kernel, mode, c->F, bad_patch, &done, c->stream);
+        if (st == RAV_OK && !done && (o.kernel == RAV_KERNEL_SCHUR || o.variant == RAV_VARIANT_MV)) {
+            set_error("rav_setup: %s needs block_dim > 0 and patches with one pressure DoF and an I_d (x) A_s "
+                      "velocity block", o.variant == RAV_VARIANT_MV ? "RAV_VARIANT_MV" : "RAV_KERNEL_SCHUR");
             st = RAV_ERR_ARG;
         }
     }
@@ -186,6 +200,26 @@ rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opt
     }
     if (st != RAV_OK) { rav_destroy(c); return st; }
     *out = c;
+    return RAV_OK;
+}
+
+rav_status rav_set_colors(rav_ctx* c, int n_colors, const int64_t* color_offs, const int32_t* patch_ids) {
+    if (!c || n_colors < 1 || !color_offs || !patch_ids) { set_error("rav_set_colors: bad argument"); return RAV_ERR_ARG; }
+    if (color_offs[0] != 0 || color_offs[n_colors] != c->P.n_patches) {
+        set_error("rav_set_colors: colours must partition the %lld patches", (long long)c->P.n_patches);
+        return RAV_ERR_ARG;
+    }
+    std::vector<char> seen(c->P.n_patches, 0);
+    for (int64_t q = 0; q < c->P.n_patches; ++q) {
+        const int32_t i = patch_ids[q];
+        if (i < 0 || i >= c->P.n_patches || seen[i]) { set_error("rav_set_colors: not a permutation"); return RAV_ERR_ARG; }
+        seen[i] = 1;
+    }
+    c->coffs.assign(color_offs, color_offs + n_colors + 1);
+    if (c->plist) cudaFree(c->plist);
+    RAV_CUDA(cudaMalloc(&c->plist, sizeof(int32_t) * c->P.n_patches));
+    RAV_CUDA(cudaMemcpy(c->plist, patch_ids, sizeof(int32_t) * c->P.n_patches, cudaMemcpyHostToDevice));
+    c->graph.reset();
     return RAV_OK;
 }
 
@@ -215,7 +249,11 @@ rav_status rav_smooth(rav_ctx* c, double* x, const double* b, int nu, double ome
         X = c->hx;
         B = c->hb;
     }
-    bool use_graph = c->stream != nullptr && nu >= 2;
+    if (c->variant == RAV_VARIANT_MV && c->coffs.empty()) {
+        set_error("rav_smooth: RAV_VARIANT_MV needs rav_set_colors first");
+        return RAV_ERR_ARG;
+    }
+    bool use_graph = c->stream != nullptr && (nu >= 2 || c->variant == RAV_VARIANT_MV);
     RAV_TRY(run_graph(c->graph, c->stream, use_graph, X, B, nu, 0, 0, omega, c->last_launches,
                       [&]() { return smooth_launches(c, X, B, nu, omega); }));
     if (!dx) {
@@ -249,6 +287,10 @@ rav_status rav_rows_size(const rav_ctx* c, int64_t* total) {
 
 rav_status rav_export_rows(const rav_ctx* c, double* rows) {
     if (!c || !rows) { set_error("NULL argument"); return RAV_ERR_ARG; }
+    if (c->F.layout == 6) {
+        set_error("rav_export_rows: not available for the diagonal-Vanka format");
+        return RAV_ERR_ARG;
+    }
     if (c->F.layout >= 4) RAV_TRY(export_schur_rows(c->P, c->F, c->nvel, rows, c->stream));
     else RAV_TRY(export_rows(c->P, c->F, rows, c->stream));
     RAV_CUDA(cudaStreamSynchronize(c->stream));
@@ -285,7 +327,9 @@ const char* rav_kernel_name(const rav_ctx* c) {
         case 2: return "sweep_thread_kernel (rows, SoA chunks)";
         case 3: return "sweep_sym_kernel (symmetric restricted block, SoA chunks)";
         case 4: return "schur_sweep_thread_kernel (factored Schur rows, SoA chunks)";
-        case 5: return "schur_sweep_warp_kernel (factored Schur rows, per patch)";
+        case 5: return c->variant == RAV_VARIANT_MV ? "mv_color_kernel (multicoloured MV, full Schur rows)"
+                                                    : "schur_sweep_warp_kernel (factored Schur rows, per patch)";
+        case 6: return "diag_sweep_kernel (diagonal Vanka, closed form)";
         default: return "unknown";
     }
 }
@@ -301,6 +345,7 @@ void rav_destroy(rav_ctx* c) {
     if (c->r) cudaFree(c->r);
     if (c->hx) cudaFree(c->hx);
     if (c->hb) cudaFree(c->hb);
+    if (c->plist) cudaFree(c->plist);
     delete c;
 }
 

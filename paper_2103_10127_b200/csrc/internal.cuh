@@ -77,6 +77,7 @@ struct Factors {
     int32_t* nodes = nullptr;  // layout 5: node dofs per patch
     int64_t* nodeoffs = nullptr;
     int64_t alg_bytes = 0;     // algorithmic bytes of the stored factor data (per application)
+    int mode = 0;              // schur_factorize mode
     int64_t nchunks = 0;
     double* facT = nullptr;    // nchunks * (NMAX*NT/2) * 32 double2
     int32_t* DT = nullptr;     // nchunks * NMAX * 32
@@ -96,8 +97,13 @@ bool thread_kernel_supported(int nresmax, int nmax);
 // ---- schur.cu -------------------------------------------------------------------------
 // Try the factored Schur format (velocity block I_D (x) A_s, one pressure DoF per patch).
 // *applicable = false (and F untouched) when the structure does not hold.
-rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D, int kernel_choice, Factors& F,
-                           int64_t* bad_patch, bool* applicable, cudaStream_t s);
+// mode: 0 restricted rows (RAV / AV), 1 diagonal Vanka (layout 6), 2 full rows for multicoloured MV
+rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D, int kernel_choice, int mode,
+                           Factors& F, int64_t* bad_patch, bool* applicable, cudaStream_t s);
+rav_status launch_diag_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
+                             cudaStream_t s);
+rav_status launch_mv_color(const Csr& A, const Factors& F, int64_t ncol, const int32_t* plist, const double* b,
+                           double* x, double omega, cudaStream_t s);
 rav_status launch_schur_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
                               cudaStream_t s);
 rav_status export_schur_rows(const PatchSet& P, const Factors& F, int64_t nvel, double* rows, cudaStream_t s);

@@ -44,7 +44,7 @@ struct SchurArgs {
     int nnmax;       // max nodes per patch
     int mnmax;       // max restricted nodes per patch
     int ld;          // leading dimension of the augmented matrix (>= nnmax + D + mnmax)
-    int layout;      // 4: thread SoA chunks, 5: per-patch (warp kernel)
+    int layout;      // 4: thread SoA chunks, 5: per-patch (warp kernel), 6: diagonal Vanka (per patch)
     // thread layout (4)
     int MT, NN;
     int64_t pairs;   // double2 pairs per chunk
@@ -209,6 +209,46 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
         __syncthreads();
         if (s_fail) {
             if (tid == 0) atomicOr(a.fail, 1u);
+            continue;
+        }
+        if (a.layout == 6) {
+            // diagonal Vanka (R17): A_s -> diag(A_s); closed form g_j = b_j / a_jj,
+            // S = c - sum b_j g_j; per patch [1/a_jj (nn) | g (nn*D) | w (nn) | w_p | 1/S]
+            double* base = a.fac + a.foffs[i];
+            double* g = base + nn;
+            double* aux = g + (size_t)nn * D;
+            for (int t = tid; t < nn; t += ST) {
+                const double dj = M[(size_t)t * ld + t];
+                base[t] = 1.0 / dj;
+                if (!(fabs(dj) > 0.0)) atomicOr((unsigned int*)&s_fail, 2u);
+                aux[t] = wnode[t];
+            }
+            for (int t = tid; t < nn * D; t += ST) g[t] = bcol[t] / M[(size_t)(t / D) * ld + (t / D)];
+            for (int j = tid; j < nn; j += ST) a.nodes[a.nodeoffs[i] + j] = ndof[j];
+            __syncthreads();
+            if (tid < 32) {
+                double sacc = 0.0, sa = 0.0;
+                for (int t = tid; t < nn * D; t += 32) {
+                    const double pr = bcol[t] * g[t];
+                    sacc += pr;
+                    sa += fabs(pr);
+                }
+                sacc = warp_sum(sacc);
+                sa = warp_sum(sa);
+                if (tid == 0) {
+                    const double S = s_cpp - sacc;
+                    if (!(fabs(S) > 1e-14 * (sa + fabs(s_cpp)))) s_fail = 2;
+                    aux[nn] = s_wp;
+                    aux[nn + 1] = 1.0 / S;
+                    a.pdof[i] = pd;
+                    a.nres_nodes[i] = mn;
+                    atomicAdd(a.alg, 8ull * ((unsigned long long)nn * (D + 2) + 2) + 4ull * (nn + 1));
+                }
+            }
+            __syncthreads();
+            if (s_fail) {
+                if (tid == 0) { atomicOr(a.fail, 2u); atomicMin(a.bad, (unsigned long long)i); }
+            }
             continue;
         }
         // right-hand sides: B columns, then e_k for the restricted nodes
@@ -521,16 +561,17 @@ static int pick_MT(int mnmax) {
     return -1;
 }
 
-rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D, int kernel_choice, Factors& F,
-                           int64_t* bad_patch, bool* applicable, cudaStream_t s) {
+rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D, int kernel_choice, int mode,
+                           Factors& F, int64_t* bad_patch, bool* applicable, cudaStream_t s) {
     *applicable = false;
     if (D < 1 || D > 3 || nvel <= 0) return RAV_OK;
     // node bounds from the patch sizes (one pressure DoF per patch)
     const int nnmax = (P.nmax - 1) / D;
     const int mnmax = std::max(1, (P.nresmax - 1) / D);
     if (nnmax < 1 || nnmax > 200) return RAV_OK;
-    const int MT = pick_MT(mnmax);
+    const int MT = mode == 1 ? 1 : pick_MT(mnmax);
     if (MT < 0) return RAV_OK;
+    if (mode == 2) kernel_choice = RAV_KERNEL_WARP;   // MV: per-patch layout (full rows)
     SchurArgs a{};
     a.rp = A.rp;
     a.ci = A.ci;
@@ -546,9 +587,40 @@ rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D,
     a.ld = nnmax + D + MT;
     if ((a.ld & 15) == 0) a.ld += 1;
     a.MT = MT;
-    const bool thread = kernel_choice != RAV_KERNEL_WARP && D == 2 && MT <= 9 && nnmax <= 32;
+    if (mode == 1) a.mnmax = nnmax;   // diagonal Vanka: any number of weighted nodes
+    const bool thread = mode == 0 && kernel_choice != RAV_KERNEL_WARP && D == 2 && MT <= 9 && nnmax <= 32;
     F.nchunks = cdiv(P.n_patches, 32);
-    if (thread) {
+    F.mode = mode;
+    if (mode == 1) {
+        F.layout = 6;
+        F.D = D;
+        F.NN = nnmax;
+        std::vector<int64_t> ho(P.n_patches + 1), fo(P.n_patches + 1), no(P.n_patches + 1);
+        RAV_CUDA(cudaMemcpy(ho.data(), P.offs, sizeof(int64_t) * (P.n_patches + 1), cudaMemcpyDeviceToHost));
+        fo[0] = 0;
+        no[0] = 0;
+        for (int64_t i = 0; i < P.n_patches; ++i) {
+            const int64_t nn = (ho[i + 1] - ho[i] - 1) / D;
+            fo[i + 1] = fo[i] + nn * (D + 2) + 2;
+            no[i + 1] = no[i] + nn;
+        }
+        RAV_CUDA(cudaMalloc(&F.foffs, sizeof(int64_t) * (P.n_patches + 1)));
+        RAV_CUDA(cudaMalloc(&F.nodeoffs, sizeof(int64_t) * (P.n_patches + 1)));
+        RAV_CUDA(cudaMalloc(&F.fac, sizeof(double) * std::max<int64_t>(1, fo.back())));
+        RAV_CUDA(cudaMalloc(&F.nodes, sizeof(int32_t) * std::max<int64_t>(1, no.back())));
+        RAV_CUDA(cudaMalloc(&F.PD, sizeof(int32_t) * P.n_patches));
+        RAV_CUDA(cudaMalloc(&F.NR, sizeof(int32_t) * P.n_patches));
+        RAV_CUDA(cudaMemcpy(F.foffs, fo.data(), sizeof(int64_t) * (P.n_patches + 1), cudaMemcpyHostToDevice));
+        RAV_CUDA(cudaMemcpy(F.nodeoffs, no.data(), sizeof(int64_t) * (P.n_patches + 1), cudaMemcpyHostToDevice));
+        F.bytes = (int64_t)sizeof(double) * fo.back() + sizeof(int32_t) * no.back();
+        a.layout = 6;
+        a.foffs = F.foffs;
+        a.fac = F.fac;
+        a.nodes = F.nodes;
+        a.nodeoffs = F.nodeoffs;
+        a.pdof = F.PD;
+        a.nres_nodes = F.NR;
+    } else if (thread) {
         F.layout = 4;
         F.MT = MT;
         F.D = D;
@@ -767,6 +839,136 @@ rav_status export_schur_rows(const PatchSet& P, const Factors& F, int64_t nvel, 
     cudaFreeAsync(sz, s);
     cudaFreeAsync(roffs, s);
     RAV_CUDA(cudaStreamSynchronize(s));
+    return RAV_OK;
+}
+
+// ---- diagonal Vanka sweep (R17, layout 6): one warp per patch, lanes over nodes ------------
+//   t = S^{-1} (g^T r_u - r_p),  du_j = r_j / a_jj + g_j t  (weights w_j),  dp = -t
+template <int D>
+__global__ void __launch_bounds__(256) diag_sweep_kernel(int64_t np, const int64_t* __restrict__ foffs,
+                                                         const int64_t* __restrict__ nodeoffs,
+                                                         const int32_t* __restrict__ nodes,
+                                                         const int32_t* __restrict__ pdof,
+                                                         const double* __restrict__ fac,
+                                                         const double* __restrict__ r, double* __restrict__ x,
+                                                         double omega) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < np; i += (int64_t)gridDim.x * 8) {
+        const int64_t no = nodeoffs[i];
+        const int nn = (int)(nodeoffs[i + 1] - no);
+        const double* dinv = fac + foffs[i];
+        const double* g = dinv + nn;
+        const double* aux = g + (size_t)nn * D;
+        double gs = 0.0;
+        for (int t = lane; t < nn * D; t += 32) gs = fma(__ldcs(g + t), __ldg(r + nodes[no + t / D] + t % D), gs);
+        gs = warp_sum(gs);
+        const int pd = pdof[i];
+        const double t = aux[nn + 1] * (gs - __ldg(r + pd));
+        for (int j = lane; j < nn; j += 32) {
+            const double wj = aux[j];
+            if (wj == 0.0) continue;
+            const int nd = nodes[no + j];
+            const double dj = __ldcs(dinv + j);
+#pragma unroll
+            for (int c = 0; c < D; ++c)
+                atomicAdd(x + nd + c, omega * wj * fma(g[j * D + c], t, dj * __ldg(r + nd + c)));
+        }
+        if (lane == 0 && aux[nn] != 0.0) atomicAdd(x + pd, omega * aux[nn] * (-t));
+    }
+}
+
+// ---- multicoloured multiplicative Vanka (Eq. 11, R10): one colour per launch --------
+// Patches of one colour share no DoF and are not coupled through L, so they are
+// relaxed concurrently; each computes a fresh local residual on its own rows
+// (Eq. 15) and applies the full L_i^{-1} (Schur form, all nodes) with
+// prolongation R_i^T.  Result = sequential MV in colour order.
+template <int D>
+__global__ void __launch_bounds__(256) mv_color_kernel(int64_t ncol, const int32_t* __restrict__ plist, int MT,
+                                                       int nnmax, const int64_t* __restrict__ foffs,
+                                                       const int64_t* __restrict__ nodeoffs,
+                                                       const int32_t* __restrict__ nodes,
+                                                       const int32_t* __restrict__ pdof,
+                                                       const double* __restrict__ fac,
+                                                       const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ b, double* __restrict__ x,
+                                                       double omega) {
+    extern __shared__ double sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* rl = sm + (size_t)warp * (nnmax * D + 1);
+    for (int64_t q = (int64_t)blockIdx.x * 8 + warp; q < ncol; q += (int64_t)gridDim.x * 8) {
+        const int64_t i = plist[q];
+        const int64_t no = nodeoffs[i];
+        const int nn = (int)(nodeoffs[i + 1] - no);
+        const int pd = pdof[i];
+        // fresh local residual on the patch rows (Eq. 15)
+        for (int t = lane; t <= nn * D; t += 32) {
+            const int row = t < nn * D ? nodes[no + t / D] + t % D : pd;
+            double s = 0.0;
+            for (int64_t k = rp[row]; k < rp[row + 1]; ++k) s = fma(val[k], x[ci[k]], s);
+            rl[t] = b[row] - s;
+        }
+        __syncwarp();
+        const double* Y = fac + foffs[i];
+        const double* g = Y + (size_t)MT * nn;
+        const double* aux = g + (size_t)nn * D;
+        double gs = 0.0;
+        for (int t = lane; t < nn * D; t += 32) gs = fma(g[t], rl[t], gs);
+        gs = warp_sum(gs);
+        const double tt = aux[MT + 1] * (gs - rl[nn * D]);
+        for (int k0 = 0; k0 < nn; k0 += 32) {
+            const int k = k0 + lane;
+            double acc[D];
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[c] = 0.0;
+            if (k < nn)
+                for (int j = 0; j < nn; ++j) {
+                    const double y = Y[(size_t)j * MT + k];
+#pragma unroll
+                    for (int c = 0; c < D; ++c) acc[c] = fma(y, rl[j * D + c], acc[c]);
+                }
+            __syncwarp();
+            if (k < nn) {
+                const int nd = nodes[no + k];
+#pragma unroll
+                for (int c = 0; c < D; ++c) x[nd + c] += omega * fma(g[k * D + c], tt, acc[c]);
+            }
+        }
+        if (lane == 0) x[pd] += omega * (-tt);
+        __syncwarp();
+    }
+}
+
+rav_status launch_diag_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
+                             cudaStream_t s) {
+    const int blocks = (int)std::min<int64_t>(cdiv(P.n_patches, 8), (int64_t)num_sms() * 16);
+    if (F.D == 3)
+        diag_sweep_kernel<3><<<blocks, 256, 0, s>>>(P.n_patches, F.foffs, F.nodeoffs, F.nodes, F.PD, F.fac, r, x, omega);
+    else if (F.D == 2)
+        diag_sweep_kernel<2><<<blocks, 256, 0, s>>>(P.n_patches, F.foffs, F.nodeoffs, F.nodes, F.PD, F.fac, r, x, omega);
+    else
+        diag_sweep_kernel<1><<<blocks, 256, 0, s>>>(P.n_patches, F.foffs, F.nodeoffs, F.nodes, F.PD, F.fac, r, x, omega);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}
+
+rav_status launch_mv_color(const Csr& A, const Factors& F, int64_t ncol, const int32_t* plist, const double* b,
+                           double* x, double omega, cudaStream_t s) {
+    if (ncol <= 0) return RAV_OK;
+    const size_t shmem = sizeof(double) * (size_t)(F.NN * F.D + 1) * 8;
+    const int blocks = (int)std::min<int64_t>(cdiv(ncol, 8), (int64_t)num_sms() * 16);
+    if (F.D == 3)
+        mv_color_kernel<3><<<blocks, 256, shmem, s>>>(ncol, plist, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD, F.fac,
+                                                      A.rp, A.ci, A.val, b, x, omega);
+    else if (F.D == 2)
+        mv_color_kernel<2><<<blocks, 256, shmem, s>>>(ncol, plist, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD, F.fac,
+                                                      A.rp, A.ci, A.val, b, x, omega);
+    else
+        mv_color_kernel<1><<<blocks, 256, shmem, s>>>(ncol, plist, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD, F.fac,
+                                                      A.rp, A.ci, A.val, b, x, omega);
+    count_launch();
+    RAV_CHECK_LAUNCH();
     return RAV_OK;
 }
 

@@ -172,6 +172,7 @@ static void launch_sym(const Factors& F, const double* r, double* x, double omeg
 
 rav_status launch_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
                         cudaStream_t s) {
+    if (F.layout == 6) return launch_diag_sweep(P, F, r, x, omega, s);
     if (F.layout >= 4) return launch_schur_sweep(P, F, r, x, omega, s);
     if (F.layout == 3) {
         switch (F.NT) {

@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libravgmg.so")
 RAV_OK = 0
 STATUS = {0: "RAV_OK", 1: "RAV_ERR_ARG", 2: "RAV_ERR_SINGULAR_LOCAL", 3: "RAV_ERR_SINGULAR_COARSE",
           4: "RAV_ERR_OOM", 5: "RAV_ERR_CUDA", 6: "RAV_ERR_COMM", 7: "RAV_ERR_DIVERGED"}
-VARIANT_ROWS, VARIANT_DIAG = 0, 1
+VARIANT_ROWS, VARIANT_DIAG, VARIANT_MV = 0, 1, 2
 KERNEL_AUTO, KERNEL_WARP, KERNEL_THREAD, KERNEL_SYM, KERNEL_SCHUR = 0, 1, 2, 3, 4
 WEIGHTS = {"pou": 0, "own": 1, "full": 2}
 
@@ -76,6 +76,7 @@ def _load():
         "rav_export_rows": [vp, vp],
         "rav_sweep_bytes": [vp, P(dbl), P(dbl), P(dbl)],
         "rav_set_stream": [vp, vp],
+        "rav_set_colors": [vp, C.c_int, vp, vp],
         "mg_setup": [C.c_int, P(RavCsr), P(RavPatches), P(RavCsr), P(i64), i64, P(RavOpts), P(vp), P(C.c_int),
                      P(i64)],
         "mg_vcycle": [vp, vp, vp, C.c_int, C.c_int, dbl],
@@ -253,6 +254,12 @@ class Smoother:
     def kernel_name(self) -> str:
         return lib.rav_kernel_name(self.ctx).decode()
 
+    def set_colors(self, offs: np.ndarray, ids: np.ndarray):
+        offs = np.ascontiguousarray(offs, dtype=np.int64)
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        self._colors = (offs, ids)
+        _check(lib.rav_set_colors(self.ctx, len(offs) - 1, offs.ctypes.data, ids.ctypes.data))
+
     def set_stream(self, stream):
         _check(lib.rav_set_stream(self.ctx, _stream(stream)))
 
@@ -321,6 +328,24 @@ class Multigrid:
             self.close()
         except Exception:
             pass
+
+
+def multicolor(problem: Dict):
+    """4^d colouring of the vertex patches (R10): colour (i mod 4) + 4 (j mod 4)
+    [+ 16 (k mod 4)], patches ascending inside each colour.  Returns (offs, ids)."""
+    dim = problem["dim"]
+    nv = [problem["ncell"][k] + 1 for k in range(dim)]
+    idx = np.arange(int(np.prod(nv)))
+    color = np.zeros_like(idx)
+    r, mult = idx.copy(), 1
+    for k in range(dim):
+        color += (r % nv[k]) % 4 * mult
+        r //= nv[k]
+        mult *= 4
+    ids = np.argsort(color, kind="stable").astype(np.int32)
+    offs = np.zeros(4 ** dim + 1, np.int64)
+    offs[1:] = np.cumsum(np.bincount(color, minlength=4 ** dim))
+    return offs, ids
 
 
 def coarsen_problem(problem: Dict) -> Dict:
