@@ -71,6 +71,20 @@ typedef struct {
     int32_t mode[8][3];
     double  phase[8][3];
     double  gmin, gmax;
+    /* Slab window along the LAST axis (multi-GPU, SURVEY section 8 row e).  win = 0:
+     * the whole grid.  win = 1: the level is generated for one rank.  Ranges are
+     * inclusive, in global lattice indices of the last axis (Q2 node layers run
+     * 0..2n, vertex layers 0..n).  Local DoFs = free nodes with last index in
+     * [node_lo, node_hi] (a contiguous range of the global velocity numbering,
+     * same order) followed by vertices in [vert_lo, vert_hi]; rows are assembled
+     * only for nodes in [rnode_lo, rnode_hi] and vertices in [rvert_lo,
+     * rvert_hi] (other rows are empty, b = 0); patches exist for the vertices in
+     * [pvert_lo, pvert_hi].  Columns must fall inside the window (else
+     * RAV_ERR_ARG).  Transfers are not windowed. */
+    int32_t win;
+    int32_t node_lo, node_hi, vert_lo, vert_hi;
+    int32_t rnode_lo, rnode_hi, rvert_lo, rvert_hi;
+    int32_t pvert_lo, pvert_hi;
 } rav_grid;
 
 /* Sizes of the generated level: n_dofs = n_vel + n_pres; nnz of L; number of
@@ -258,6 +272,17 @@ rav_status mg_vcycle(mg_ctx* ctx, double* x, const double* b, int pre, int post,
  * *iters == maxit. */
 rav_status mg_solve(mg_ctx* ctx, double* x, const double* b, int pre, int post, double omega,
                     double rtol, int maxit, int* iters, double* hist);
+
+/* ------------------------------------------------------------------------- */
+/* Exchange helpers for the slab-partitioned sweep (SURVEY section 8 row e)    */
+/* ------------------------------------------------------------------------- */
+/* Device pointers, stream-ordered.  op: 0 gather  dst[k] = src[idx[k]]
+ *                                       1 scatter dst[idx[k]] = src[k]
+ *                                       2 scatter-add dst[idx[k]] += src[k]
+ *                                         (indices unique within one call)
+ *                                       3 fill dst[idx[k]] = value (src unused) */
+rav_status rav_index_op(int op, const double* src, const int32_t* idx, int64_t n, double* dst, double value,
+                        void* stream);
 
 /* Number of GPU kernel launches issued by the most recent rav_smooth,
  * mg_vcycle or mg_solve call on this context (graph nodes included). */

@@ -32,6 +32,13 @@ struct Grid {
     double phase[8][3];
     double gmin, gmax;
     int64_t nfree, nvel, nvert, ndof, nel;
+    // window along the last axis (rav_grid.win); whole grid when win == 0
+    int last;
+    int64_t nlow_free, nlow_vert;   // free nodes / vertices per layer of the last axis
+    int64_t vel_off, vert_off;      // global velocity-DoF / vertex offsets of the window
+    int64_t nvel_loc, nvert_loc, ndof_loc;
+    int rnode_lo, rnode_hi, rvert_lo, rvert_hi;
+    int64_t patch_off, npatch;      // first global vertex with a patch, number of patches
 };
 
 static Grid make_grid(const rav_grid* g) {
@@ -66,7 +73,40 @@ static Grid make_grid(const rav_grid* g) {
     G.gmax = g->gmax;
     G.nvel = (int64_t)g->dim * G.nfree;
     G.ndof = G.nvel + G.nvert;
+    G.last = g->dim - 1;
+    G.nlow_free = G.nfree / (2 * G.n[G.last] - 1);
+    G.nlow_vert = G.nvert / (G.n[G.last] + 1);
+    int node_lo = 1, node_hi = 2 * G.n[G.last] - 1, vert_lo = 0, vert_hi = G.n[G.last];
+    G.rnode_lo = node_lo; G.rnode_hi = node_hi; G.rvert_lo = vert_lo; G.rvert_hi = vert_hi;
+    int pv_lo = 0, pv_hi = G.n[G.last];
+    if (g->win) {
+        node_lo = std::max(1, g->node_lo);
+        node_hi = std::min(2 * G.n[G.last] - 1, g->node_hi);
+        vert_lo = std::max(0, g->vert_lo);
+        vert_hi = std::min(G.n[G.last], g->vert_hi);
+        G.rnode_lo = g->rnode_lo; G.rnode_hi = g->rnode_hi;
+        G.rvert_lo = g->rvert_lo; G.rvert_hi = g->rvert_hi;
+        pv_lo = std::max(0, g->pvert_lo);
+        pv_hi = std::min(G.n[G.last], g->pvert_hi);
+    }
+    G.vel_off = (int64_t)g->dim * G.nlow_free * (node_lo - 1);
+    G.nvel_loc = (int64_t)g->dim * G.nlow_free * std::max(0, node_hi - node_lo + 1);
+    G.vert_off = G.nlow_vert * vert_lo;
+    G.nvert_loc = G.nlow_vert * std::max(0, vert_hi - vert_lo + 1);
+    G.ndof_loc = G.nvel_loc + G.nvert_loc;
+    G.patch_off = G.nlow_vert * pv_lo;
+    G.npatch = G.nlow_vert * std::max(0, pv_hi - pv_lo + 1);
     return G;
+}
+
+// local index of a global velocity DoF / vertex in the window, -1 outside
+__device__ __forceinline__ int64_t loc_vel(const Grid& G, int64_t gdof) {
+    const int64_t l = gdof - G.vel_off;
+    return (l >= 0 && l < G.nvel_loc) ? l : -1;
+}
+__device__ __forceinline__ int64_t loc_vert(const Grid& G, int64_t vid) {
+    const int64_t l = vid - G.vert_off;
+    return (l >= 0 && l < G.nvert_loc) ? G.nvel_loc + l : -1;
 }
 
 static rav_status check_grid(const rav_grid* g) {
@@ -77,6 +117,10 @@ static rav_status check_grid(const rav_grid* g) {
     if (g->kind < 0 || g->kind > 2) { set_error("rav_grid: bad kind"); return RAV_ERR_ARG; }
     if (g->n_modes < 0 || g->n_modes > 8) { set_error("rav_grid: n_modes > 8"); return RAV_ERR_ARG; }
     if (g->eta_mode == 1 && !(g->gmax > g->gmin)) { set_error("rav_grid: gmax <= gmin"); return RAV_ERR_ARG; }
+    if (g->win && (g->node_lo > g->node_hi || g->vert_lo > g->vert_hi || g->pvert_lo > g->pvert_hi)) {
+        set_error("rav_grid: empty window");
+        return RAV_ERR_ARG;
+    }
     return RAV_OK;
 }
 
@@ -329,17 +373,28 @@ __device__ __forceinline__ void decode_vertex(const Grid& G, int64_t vi, int* v)
 // Row pattern (structural, R2): velocity row (a, c): same-component velocity DoFs of
 // the nodes of all elements containing a, then the pressure DoFs of their vertices;
 // pressure row v: all velocity DoFs of the nodes of the elements containing v.
+// decode a LOCAL row of the window: velocity (node a, component c) or vertex a;
+// false when the row lies outside the row window (empty row)
+__device__ __forceinline__ bool decode_local_row(const Grid& G, int64_t row, int* a, int& c, bool& vel) {
+    vel = row < G.nvel_loc;
+    if (vel) {
+        decode_vel_row(G, row + G.vel_off, a, c);
+        return a[G.last] >= G.rnode_lo && a[G.last] <= G.rnode_hi;
+    }
+    decode_vertex(G, row - G.nvel_loc + G.vert_off, a);
+    c = 0;
+    return a[G.last] >= G.rvert_lo && a[G.last] <= G.rvert_hi;
+}
+
 __global__ void op_count_kernel(Grid G, int64_t* cnt) {
-    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < G.ndof;
+    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < G.ndof_loc;
          row += (int64_t)gridDim.x * blockDim.x) {
-        int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, a[3], c = 0;
-        bool vel = row < G.nvel;
-        if (vel) {
-            decode_vel_row(G, row, a, c);
-            for (int k = 0; k < G.dim; ++k) node_elems(a[k], G.n[k], lo[k], hi[k]);
-        } else {
-            decode_vertex(G, row - G.nvel, a);
-            for (int k = 0; k < G.dim; ++k) vert_elems(a[k], G.n[k], lo[k], hi[k]);
+        int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, a[3] = {0, 0, 0}, c = 0;
+        bool vel;
+        if (!decode_local_row(G, row, a, c, vel)) { cnt[row] = 0; continue; }
+        for (int k = 0; k < G.dim; ++k) {
+            if (vel) node_elems(a[k], G.n[k], lo[k], hi[k]);
+            else vert_elems(a[k], G.n[k], lo[k], hi[k]);
         }
         int64_t nodes = 1, verts = 1;
         for (int k = 0; k < G.dim; ++k) {
@@ -353,18 +408,16 @@ __global__ void op_count_kernel(Grid G, int64_t* cnt) {
 }
 
 __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_tab, const int64_t* rp,
-                               int32_t* col, double* val, double* rhs) {
-    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < G.ndof;
+                               int32_t* col, double* val, double* rhs, unsigned int* err) {
+    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < G.ndof_loc;
          row += (int64_t)gridDim.x * blockDim.x) {
         int64_t p = rp[row];
         int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}, a[3] = {0, 0, 0}, c = 0;
-        bool vel = row < G.nvel;
-        if (vel) {
-            decode_vel_row(G, row, a, c);
-            for (int k = 0; k < G.dim; ++k) node_elems(a[k], G.n[k], lo[k], hi[k]);
-        } else {
-            decode_vertex(G, row - G.nvel, a);
-            for (int k = 0; k < G.dim; ++k) vert_elems(a[k], G.n[k], lo[k], hi[k]);
+        bool vel;
+        if (!decode_local_row(G, row, a, c, vel)) { rhs[row] = 0.0; continue; }
+        for (int k = 0; k < G.dim; ++k) {
+            if (vel) node_elems(a[k], G.n[k], lo[k], hi[k]);
+            else vert_elems(a[k], G.n[k], lo[k], hi[k]);
         }
         double lift = 0.0;
         int bl[3] = {0, 0, 0}, bh[3] = {0, 0, 0};
@@ -376,7 +429,9 @@ __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_ta
                     int64_t fb = free_id(G, b);
                     if (vel) {
                         if (fb >= 0) {
-                            col[p] = (int32_t)(fb * G.dim + c);
+                            const int64_t lc = loc_vel(G, fb * G.dim + c);
+                            if (lc < 0) atomicOr(err, 1u);
+                            col[p] = (int32_t)lc;
                             val[p] = a_entry(G, eta_tab, a, b);
                             ++p;
                         } else {
@@ -386,7 +441,9 @@ __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_ta
                     } else {
                         for (int cc = 0; cc < G.dim; ++cc) {
                             if (fb >= 0) {
-                                col[p] = (int32_t)(fb * G.dim + cc);
+                                const int64_t lc = loc_vel(G, fb * G.dim + cc);
+                                if (lc < 0) atomicOr(err, 1u);
+                                col[p] = (int32_t)lc;
                                 val[p] = b_entry(G, b, cc, a);
                                 ++p;
                             } else {
@@ -401,7 +458,9 @@ __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_ta
             for (v[2] = lo[2]; v[2] <= (G.dim > 2 ? hi[2] + 1 : 0); ++v[2])
                 for (v[1] = lo[1]; v[1] <= hi[1] + 1; ++v[1])
                     for (v[0] = lo[0]; v[0] <= hi[0] + 1; ++v[0]) {
-                        col[p] = (int32_t)(G.nvel + vert_id(G, v));
+                        const int64_t lc = loc_vert(G, vert_id(G, v));
+                        if (lc < 0) atomicOr(err, 1u);
+                        col[p] = (int32_t)lc;
                         val[p] = b_entry(G, a, c, v);
                         ++p;
                     }
@@ -429,29 +488,37 @@ __device__ __forceinline__ double patch_weight(int mode, int dim, const int* a, 
 }
 
 __global__ void patch_count_kernel(Grid G, int64_t* cnt) {
-    for (int64_t vi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vi < G.nvert;
-         vi += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t pi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pi < G.npatch;
+         pi += (int64_t)gridDim.x * blockDim.x) {
         int v[3];
-        decode_vertex(G, vi, v);
+        decode_vertex(G, pi + G.patch_off, v);
         int64_t nodes = 1;
         for (int k = 0; k < G.dim; ++k) {
             int l = max(2 * v[k] - 2, 1), h = min(2 * v[k] + 2, 2 * G.n[k] - 1);
             nodes *= (h - l + 1);
         }
-        cnt[vi] = nodes * G.dim + 1;
+        cnt[pi] = nodes * G.dim + 1;
     }
 }
 
-__global__ void patch_fill_kernel(Grid G, int mode, const int64_t* offs, int32_t* dofs, double* w) {
-    for (int64_t vi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vi < G.nvert;
-         vi += (int64_t)gridDim.x * blockDim.x) {
+__global__ void patch_fill_kernel(Grid G, int mode, const int64_t* offs, int32_t* dofs, double* w,
+                                  unsigned int* err) {
+    for (int64_t pi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pi < G.npatch;
+         pi += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t vi = pi + G.patch_off;
         int v[3];
         decode_vertex(G, vi, v);
         int l[3] = {0, 0, 0}, h[3] = {0, 0, 0};
         for (int k = 0; k < G.dim; ++k) { l[k] = max(2 * v[k] - 2, 1); h[k] = min(2 * v[k] + 2, 2 * G.n[k] - 1); }
-        int64_t p = offs[vi];
+        int64_t p = offs[pi];
         for (int pass = 0; pass < 2; ++pass) {
-            if (pass == 1) { dofs[p] = (int32_t)(G.nvel + vi); w[p] = 1.0; ++p; }
+            if (pass == 1) {
+                const int64_t lp = loc_vert(G, vi);
+                if (lp < 0) atomicOr(err, 1u);
+                dofs[p] = (int32_t)lp;
+                w[p] = 1.0;
+                ++p;
+            }
             int a[3] = {0, 0, 0};
             for (a[2] = l[2]; a[2] <= h[2]; ++a[2])
                 for (a[1] = l[1]; a[1] <= h[1]; ++a[1])
@@ -460,7 +527,9 @@ __global__ void patch_fill_kernel(Grid G, int mode, const int64_t* offs, int32_t
                         if ((pass == 0) != (wt > 0.0)) continue;
                         int64_t fa = free_id(G, a);
                         for (int c = 0; c < G.dim; ++c) {
-                            dofs[p] = (int32_t)(fa * G.dim + c);
+                            const int64_t lc = loc_vel(G, fa * G.dim + c);
+                            if (lc < 0) atomicOr(err, 1u);
+                            dofs[p] = (int32_t)lc;
                             w[p] = wt;
                             ++p;
                         }
@@ -557,27 +626,27 @@ extern "C" rav_status rav_gen_sizes(const rav_grid* g, int weights, void* stream
     if (weights < 0 || weights > 2) { set_error("rav_gen_sizes: weights must be 0, 1 or 2"); return RAV_ERR_ARG; }
     Grid G = make_grid(g);
     cudaStream_t s = as_stream(stream);
-    if (n_dofs) *n_dofs = G.ndof;
-    if (n_vel) *n_vel = G.nvel;
-    if (n_patches) *n_patches = G.nvert;
+    if (n_dofs) *n_dofs = G.ndof_loc;
+    if (n_vel) *n_vel = G.nvel_loc;
+    if (n_patches) *n_patches = G.npatch;
     int64_t *cnt = nullptr, *rp = nullptr;
-    int64_t nmax = G.ndof > G.nvert ? G.ndof : G.nvert;
+    int64_t nmax = std::max<int64_t>(1, std::max(G.ndof_loc, G.npatch));
     RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * nmax, s));
     RAV_CUDA(cudaMallocAsync(&rp, sizeof(int64_t) * (nmax + 1), s));
     int64_t h_nnz = 0, h_pe = 0;
-    if (nnz) {
-        op_count_kernel<<<grid_for(G.ndof, 256), 256, 0, s>>>(G, cnt);
+    if (nnz && G.ndof_loc > 0) {
+        op_count_kernel<<<grid_for(G.ndof_loc, 256), 256, 0, s>>>(G, cnt);
         count_launch();
         RAV_CHECK_LAUNCH();
-        RAV_TRY(counts_to_rowptr(cnt, rp, G.ndof, s));
-        RAV_CUDA(cudaMemcpyAsync(&h_nnz, rp + G.ndof, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        RAV_TRY(counts_to_rowptr(cnt, rp, G.ndof_loc, s));
+        RAV_CUDA(cudaMemcpyAsync(&h_nnz, rp + G.ndof_loc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     }
-    if (patch_entries) {
-        patch_count_kernel<<<grid_for(G.nvert, 256), 256, 0, s>>>(G, cnt);
+    if (patch_entries && G.npatch > 0) {
+        patch_count_kernel<<<grid_for(G.npatch, 256), 256, 0, s>>>(G, cnt);
         count_launch();
         RAV_CHECK_LAUNCH();
-        RAV_TRY(counts_to_rowptr(cnt, rp, G.nvert, s));
-        RAV_CUDA(cudaMemcpyAsync(&h_pe, rp + G.nvert, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        RAV_TRY(counts_to_rowptr(cnt, rp, G.npatch, s));
+        RAV_CUDA(cudaMemcpyAsync(&h_pe, rp + G.npatch, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     }
     cudaFreeAsync(cnt, s);
     cudaFreeAsync(rp, s);
@@ -585,7 +654,7 @@ extern "C" rav_status rav_gen_sizes(const rav_grid* g, int weights, void* stream
     if (nnz) *nnz = h_nnz;
     if (patch_entries) *patch_entries = h_pe;
     if (h_nnz > INT32_MAX * 4LL) { set_error("nnz too large"); return RAV_ERR_ARG; }
-    if (G.ndof > INT32_MAX) { set_error("n_dofs exceeds int32 column index range"); return RAV_ERR_ARG; }
+    if (G.ndof_loc > INT32_MAX) { set_error("n_dofs exceeds int32 column index range"); return RAV_ERR_ARG; }
     return RAV_OK;
 }
 
@@ -599,23 +668,30 @@ extern "C" rav_status rav_gen_operator(const rav_grid* g, int64_t* row_ptr, int3
     const int NG = G.dim == 2 ? 9 : 27;
     double *eta_tab = nullptr, *f_tab = nullptr;
     int64_t* cnt = nullptr;
+    unsigned int* err = nullptr;
     RAV_CUDA(cudaMallocAsync(&eta_tab, sizeof(double) * G.nel * NG, s));
     if (G.kind == 1) RAV_CUDA(cudaMallocAsync(&f_tab, sizeof(double) * G.nel * NG * 2, s));
-    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * G.ndof, s));
+    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * std::max<int64_t>(1, G.ndof_loc), s));
+    RAV_CUDA(cudaMallocAsync(&err, sizeof(unsigned int), s));
+    RAV_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
     coef_kernel<<<grid_for(G.nel * NG, 256), 256, 0, s>>>(G, eta_tab, f_tab);
     count_launch();
     RAV_CHECK_LAUNCH();
-    op_count_kernel<<<grid_for(G.ndof, 256), 256, 0, s>>>(G, cnt);
+    op_count_kernel<<<grid_for(G.ndof_loc, 256), 256, 0, s>>>(G, cnt);
     count_launch();
     RAV_CHECK_LAUNCH();
-    RAV_TRY(counts_to_rowptr(cnt, row_ptr, G.ndof, s));
-    op_fill_kernel<<<grid_for(G.ndof, 128), 128, 0, s>>>(G, eta_tab, f_tab, row_ptr, col, val, rhs);
+    RAV_TRY(counts_to_rowptr(cnt, row_ptr, G.ndof_loc, s));
+    op_fill_kernel<<<grid_for(G.ndof_loc, 128), 128, 0, s>>>(G, eta_tab, f_tab, row_ptr, col, val, rhs, err);
     count_launch();
     RAV_CHECK_LAUNCH();
+    unsigned int h_err = 0;
+    RAV_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(h_err), cudaMemcpyDeviceToHost, s));
     cudaFreeAsync(eta_tab, s);
     if (f_tab) cudaFreeAsync(f_tab, s);
     cudaFreeAsync(cnt, s);
+    cudaFreeAsync(err, s);
     RAV_CUDA(cudaStreamSynchronize(s));
+    if (h_err) { set_error("rav_gen_operator: a row of the row window couples outside the DoF window"); return RAV_ERR_ARG; }
     return RAV_OK;
 }
 
@@ -627,16 +703,23 @@ extern "C" rav_status rav_gen_patches(const rav_grid* g, int weights, int64_t* o
     Grid G = make_grid(g);
     cudaStream_t s = as_stream(stream);
     int64_t* cnt = nullptr;
-    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * G.nvert, s));
-    patch_count_kernel<<<grid_for(G.nvert, 256), 256, 0, s>>>(G, cnt);
+    unsigned int* err = nullptr;
+    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * std::max<int64_t>(1, G.npatch), s));
+    RAV_CUDA(cudaMallocAsync(&err, sizeof(unsigned int), s));
+    RAV_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
+    patch_count_kernel<<<grid_for(G.npatch, 256), 256, 0, s>>>(G, cnt);
     count_launch();
     RAV_CHECK_LAUNCH();
-    RAV_TRY(counts_to_rowptr(cnt, offs, G.nvert, s));
-    patch_fill_kernel<<<grid_for(G.nvert, 128), 128, 0, s>>>(G, weights, offs, dofs, w);
+    RAV_TRY(counts_to_rowptr(cnt, offs, G.npatch, s));
+    patch_fill_kernel<<<grid_for(G.npatch, 128), 128, 0, s>>>(G, weights, offs, dofs, w, err);
     count_launch();
     RAV_CHECK_LAUNCH();
+    unsigned int h_err = 0;
+    RAV_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(h_err), cudaMemcpyDeviceToHost, s));
     cudaFreeAsync(cnt, s);
+    cudaFreeAsync(err, s);
     RAV_CUDA(cudaStreamSynchronize(s));
+    if (h_err) { set_error("rav_gen_patches: a patch reaches outside the DoF window"); return RAV_ERR_ARG; }
     return RAV_OK;
 }
 
@@ -644,6 +727,7 @@ static rav_status check_nested(const rav_grid* f, const rav_grid* c) {
     RAV_TRY(check_grid(f));
     RAV_TRY(check_grid(c));
     if (f->dim != c->dim) { set_error("prolongation: dim mismatch"); return RAV_ERR_ARG; }
+    if (f->win || c->win) { set_error("prolongation: windowed grids are not supported"); return RAV_ERR_ARG; }
     for (int k = 0; k < f->dim; ++k)
         if (f->ncell[k] != 2 * c->ncell[k]) { set_error("prolongation: fine ncell must be 2 x coarse"); return RAV_ERR_ARG; }
     return RAV_OK;

@@ -169,6 +169,18 @@ rav_status launch_residual_norm2(const Csr& A, const double* x, const double* b,
     return RAV_OK;
 }
 
+// pack / unpack for the slab exchanges
+__global__ void index_op_kernel(int op, const double* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                                double* __restrict__ dst, double value) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = idx[k];
+        if (op == 0) dst[k] = src[i];
+        else if (op == 1) dst[i] = src[k];
+        else if (op == 2) dst[i] += src[k];
+        else dst[i] = value;
+    }
+}
+
 static bool is_device_ptr(const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
@@ -293,3 +305,19 @@ rav_status csr_transpose(const Csr& A, Csr& At, cudaStream_t s) {
 }
 
 }  // namespace rav
+
+extern "C" rav_status rav_index_op(int op, const double* src, const int32_t* idx, int64_t n, double* dst,
+                                   double value, void* stream) {
+    using namespace rav;
+    if (op < 0 || op > 3 || n < 0 || (n > 0 && (!idx || !dst || (op != 3 && !src)))) {
+        set_error("rav_index_op: bad argument");
+        return RAV_ERR_ARG;
+    }
+    g_launches = 0;
+    if (n == 0) return RAV_OK;
+    const int blocks = (int)std::min<int64_t>(cdiv(n, 256), (int64_t)num_sms() * 8);
+    index_op_kernel<<<blocks, 256, 0, as_stream(stream)>>>(op, src, idx, n, dst, value);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}

@@ -37,7 +37,13 @@ class RavGrid(C.Structure):
     _fields_ = [("dim", C.c_int32), ("ncell", C.c_int32 * 3), ("len", C.c_double * 3),
                 ("kind", C.c_int32), ("eta_mode", C.c_int32), ("eta0", C.c_double),
                 ("n_modes", C.c_int32), ("amp", C.c_double * 8), ("mode", (C.c_int32 * 3) * 8),
-                ("phase", (C.c_double * 3) * 8), ("gmin", C.c_double), ("gmax", C.c_double)]
+                ("phase", (C.c_double * 3) * 8), ("gmin", C.c_double), ("gmax", C.c_double),
+                ("win", C.c_int32), ("node_lo", C.c_int32), ("node_hi", C.c_int32), ("vert_lo", C.c_int32),
+                ("vert_hi", C.c_int32), ("rnode_lo", C.c_int32), ("rnode_hi", C.c_int32),
+                ("rvert_lo", C.c_int32), ("rvert_hi", C.c_int32), ("pvert_lo", C.c_int32), ("pvert_hi", C.c_int32)]
+
+WINDOW_KEYS = ("node_lo", "node_hi", "vert_lo", "vert_hi", "rnode_lo", "rnode_hi", "rvert_lo", "rvert_hi",
+               "pvert_lo", "pvert_hi")
 
 
 class RavCsr(C.Structure):
@@ -77,6 +83,7 @@ def _load():
         "rav_sweep_bytes": [vp, P(dbl), P(dbl), P(dbl)],
         "rav_set_stream": [vp, vp],
         "rav_set_colors": [vp, C.c_int, vp, vp],
+        "rav_index_op": [C.c_int, vp, vp, i64, vp, dbl, vp],
         "mg_setup": [C.c_int, P(RavCsr), P(RavPatches), P(RavCsr), P(i64), i64, P(RavOpts), P(vp), P(C.c_int),
                      P(i64)],
         "mg_vcycle": [vp, vp, vp, C.c_int, C.c_int, dbl],
@@ -140,6 +147,11 @@ def grid(problem: Dict) -> RavGrid:
             g.phase[m][k] = float(problem["phase"][m][k])
     g.gmin = problem["gmin"]
     g.gmax = problem["gmax"]
+    win = problem.get("window")
+    if win is not None:   # slab window of one rank (dist.py)
+        g.win = 1
+        for k in WINDOW_KEYS:
+            setattr(g, k, int(win[k]))
     return g
 
 
@@ -328,6 +340,15 @@ class Multigrid:
             self.close()
         except Exception:
             pass
+
+
+def index_op(op: int, src, idx, dst, value: float = 0.0, stream=None):
+    """rav_index_op: 0 gather dst[k] = src[idx[k]], 1 scatter dst[idx[k]] = src[k],
+    2 scatter-add, 3 fill dst[idx[k]] = value (device tensors)."""
+    n = idx.numel()
+    _check(lib.rav_index_op(int(op), _ptr(src) if src is not None else None, _ptr(idx), int(n), _ptr(dst),
+                            float(value), _stream(stream)))
+    return dst
 
 
 def multicolor(problem: Dict):
