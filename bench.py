@@ -191,6 +191,86 @@ def run_vcycle(name, rg, si, stream, dist):
     return out
 
 
+def run_c5_smoothers(rg, si, stream):
+    """BASELINE config 5 on one GPU: 2048^2 MMS with seeded eta, 50 sweeps each of
+    RAV (omega 0.66), diagonal Vanka (omega 0.1) and multicoloured MV (omega
+    0.66) from the seeded N(0,1) guess: time per sweep, MDoF/s and the residual
+    reduction ||b - L x_50|| / ||b - L x_0|| ("runtime per iteration")."""
+    import torch
+    prob = si.config_problem("c5")
+    out = {"config": "c5 (1 GPU): 2048^2 Q2-Q1 MMS, seeded eta, 50 sweeps from seeded N(0,1)"}
+    x0 = None
+    for name, weights, variant, omega in (("rav", "pou", rg.VARIANT_ROWS, 0.66),
+                                          ("diag_vanka", "full", rg.VARIANT_DIAG, 0.1),
+                                          ("mv_color", "full", rg.VARIANT_MV, 0.66)):
+        G = rg.gen_level(prob, weights)
+        t0 = time.perf_counter()
+        sm = rg.Smoother(G, G, variant=variant)
+        if variant == rg.VARIANT_MV:
+            sm.set_colors(*rg.multicolor(prob))
+        torch.cuda.synchronize()
+        setup_s = time.perf_counter() - t0
+        if x0 is None:
+            x0 = torch.tensor(si.initial_guess(G["n"], seed=si.X0_SEED), device="cuda")
+        b = G["b"]
+        r0 = float(torch.linalg.vector_norm(sm.residual(x0, b)))
+        x = x0.clone()
+        sm.smooth(x, b, 50, omega)     # warm-up (graph capture)
+        x = x0.clone()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sm.smooth(x, b, 50, omega)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 50
+        r50 = float(torch.linalg.vector_norm(sm.residual(x, b)))
+        out[name] = {"ms_per_sweep": ms, "mdofs": G["n"] / (ms * 1e-3) / 1e6, "omega": omega,
+                     "residual_reduction_50": r50 / r0, "setup_s": setup_s, "kernel": sm.kernel_name,
+                     "factor_bytes_per_sweep": sm.sweep_bytes()["sweep"]}
+        sm.close()
+        del sm, G, x, b
+        torch.cuda.empty_cache()
+    return out
+
+
+def run_vcycle_smoothers(rg, si, stream):
+    """The paper's smoother comparison (Figs. 4-5) as GPU V-cycles:
+    512^2 MMS with seeded eta, 8 levels (4^2 coarsest), x0 = 0, rtol 1e-8;
+    RAV / MV (0.66, V(2,2)), diagonal Vanka (0.1, V(2,2)), AV (0.1, V(3,3))."""
+    import torch
+    prob = si.problem(2, (512, 512), si.KIND_MMS, eta="fourier")
+    out = {"config": "512^2 Q2-Q1 MMS, seeded eta, 8 levels, x0 = 0, rtol 1e-8"}
+    for name, weights, variant, omega, pre in (("rav", "pou", rg.VARIANT_ROWS, 0.66, 2),
+                                               ("mv_color", "full", rg.VARIANT_MV, 0.66, 2),
+                                               ("diag_vanka", "full", rg.VARIANT_DIAG, 0.1, 2),
+                                               ("av", "full", rg.VARIANT_ROWS, 0.1, 3)):
+        mg, fine = rg.build_hierarchy(prob, 8, weights, variant=variant)
+        x = torch.zeros(fine["n"], dtype=torch.float64, device="cuda")
+        mg.solve(x, fine["b"], pre=pre, post=pre, omega=omega, rtol=1e-8, maxit=2)   # warm
+        x.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        try:
+            x, k, h = mg.solve(x, fine["b"], pre=pre, post=pre, omega=omega, rtol=1e-8, maxit=400)
+        except rg.RavError as err:   # diagonal Vanka diverges on this problem (oracle too)
+            torch.cuda.synchronize()
+            out[name] = {"converged": False, "diverged": str(err)[:120], "pre_post": pre, "omega": omega}
+            mg.close()
+            continue
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        out[name] = {"cycles": k, "converged": bool(h[-1] <= 1e-8 * h[0]), "time_s": t,
+                     "ms_per_cycle": t / max(k, 1) * 1e3, "pre_post": pre, "omega": omega,
+                     "avg_reduction_factor": (h[-1] / h[0]) ** (1.0 / max(k, 1))}
+        mg.close()
+        del mg, fine, x
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_gpu_dist(args):
     """N > 1 (torchrun): weak scaling of the c2 workload, one 512^2 block per GPU
     stacked along y (BASELINE config 5's layout): the finest level is
@@ -421,6 +501,10 @@ def run_gpu(args):
         del sm, G
         torch.cuda.empty_cache()
         vcyc = {name: run_vcycle(name, rg, si, stream, dist) for name in ("c3", "c4")}
+    extra = {}
+    if not args.no_smoothers and ws == 1:
+        extra["c5_smoothers"] = run_c5_smoothers(rg, si, stream)
+        extra["vcycle_smoothers"] = run_vcycle_smoothers(rg, si, stream)
 
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample) ------------------
     cpu = None
@@ -461,6 +545,7 @@ def run_gpu(args):
         line["cpu_baseline"] = cpu
     if vcyc is not None:
         line["vcycle"] = vcyc
+    line.update(extra)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -476,6 +561,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-vcycle", action="store_true", help="skip the c3 V-cycle time-to-1e-8 measurement")
+    ap.add_argument("--no-smoothers", action="store_true", help="skip the c5 / V-cycle smoother comparisons")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -284,6 +284,11 @@ rav_status mg_solve(mg_ctx* ctx, double* x, const double* b, int pre, int post, 
 rav_status rav_index_op(int op, const double* src, const int32_t* idx, int64_t n, double* dst, double value,
                         void* stream);
 
+/* Colouring of the smoother on level `level` (1 .. n_levels-1) for
+ * RAV_VARIANT_MV (same contract as rav_set_colors). */
+rav_status mg_set_colors(mg_ctx* ctx, int level, int n_colors, const int64_t* color_offs,
+                         const int32_t* patch_ids);
+
 /* Number of GPU kernel launches issued by the most recent rav_smooth,
  * mg_vcycle or mg_solve call on this context (graph nodes included). */
 int64_t rav_last_launches(const rav_ctx* ctx);

@@ -557,4 +557,11 @@ rav_status mg_solve(mg_ctx* m, double* x, const double* b, int pre, int post, do
 
 int64_t mg_last_launches(const mg_ctx* m) { return m ? m->last_launches : 0; }
 
+rav_status mg_set_colors(mg_ctx* m, int level, int n_colors, const int64_t* color_offs, const int32_t* patch_ids) {
+    if (!m || level < 1 || level >= m->L) { set_error("mg_set_colors: bad level"); return RAV_ERR_ARG; }
+    RAV_TRY(rav_set_colors(m->lv[level].sm, n_colors, color_offs, patch_ids));
+    m->cyc.reset();
+    return RAV_OK;
+}
+
 }  // extern "C"

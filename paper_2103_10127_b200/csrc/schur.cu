@@ -403,8 +403,8 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
 // ------------------------------------------------------------------------------------
 
 // one patch per thread (2D): MT restricted nodes, D components, NN nodes per patch (runtime)
-template <int MT, int D>
-__global__ void __launch_bounds__(128) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
+template <int MT, int D, int MINB>
+__global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
                                                                  const double2* __restrict__ W,
                                                                  const int32_t* __restrict__ ND,
                                                                  const int32_t* __restrict__ PD,
@@ -976,9 +976,26 @@ template <int MT>
 static void launch_schur_thread(int64_t np, const Factors& F, const double* r, double* x, double omega,
                                 cudaStream_t s) {
     const int blocks = (int)cdiv(F.nchunks * 32, 128);
-    schur_sweep_thread_kernel<MT, 2><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
-                                                            reinterpret_cast<const double2*>(F.facT), F.DT, F.PD,
-                                                            F.NR, F.WT, r, x, omega);
+    static const int minb = [] {
+        const char* e = getenv("RAV_SCHUR_MINB");
+        return e ? atoi(e) : 4;
+    }();
+    if (minb >= 6)
+        schur_sweep_thread_kernel<MT, 2, 6><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
+                                                                   reinterpret_cast<const double2*>(F.facT), F.DT,
+                                                                   F.PD, F.NR, F.WT, r, x, omega);
+    else if (minb == 5)
+        schur_sweep_thread_kernel<MT, 2, 5><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
+                                                                   reinterpret_cast<const double2*>(F.facT), F.DT,
+                                                                   F.PD, F.NR, F.WT, r, x, omega);
+    else if (minb >= 4)
+        schur_sweep_thread_kernel<MT, 2, 4><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
+                                                                   reinterpret_cast<const double2*>(F.facT), F.DT,
+                                                                   F.PD, F.NR, F.WT, r, x, omega);
+    else
+        schur_sweep_thread_kernel<MT, 2, 1><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
+                                                                   reinterpret_cast<const double2*>(F.facT), F.DT,
+                                                                   F.PD, F.NR, F.WT, r, x, omega);
 }
 
 rav_status launch_schur_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,

@@ -83,6 +83,7 @@ def _load():
         "rav_sweep_bytes": [vp, P(dbl), P(dbl), P(dbl)],
         "rav_set_stream": [vp, vp],
         "rav_set_colors": [vp, C.c_int, vp, vp],
+        "mg_set_colors": [vp, C.c_int, C.c_int, vp, vp],
         "rav_index_op": [C.c_int, vp, vp, i64, vp, dbl, vp],
         "mg_setup": [C.c_int, P(RavCsr), P(RavPatches), P(RavCsr), P(i64), i64, P(RavOpts), P(vp), P(C.c_int),
                      P(i64)],
@@ -314,6 +315,11 @@ class Multigrid:
         _check(st, bad_patch=bp.value, bad_level=bl.value)
         self.ctx = ctx
 
+    def set_colors(self, level: int, offs: np.ndarray, ids: np.ndarray):
+        offs = np.ascontiguousarray(offs, dtype=np.int64)
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        _check(lib.mg_set_colors(self.ctx, int(level), len(offs) - 1, offs.ctypes.data, ids.ctypes.data))
+
     def vcycle(self, x, b, pre=2, post=2, omega=0.66):
         _check(lib.mg_vcycle(self.ctx, _ptr(x), _ptr(b), int(pre), int(post), float(omega)))
         return x
@@ -391,6 +397,9 @@ def build_hierarchy(problem: Dict, n_levels: int, weights: str = "pou", variant:
             prols.append(gen_prolongation(p, probs[l - 1]))
     pin = levels[0]["nvel"]       # pressure DoF of vertex 0 (R4)
     mg = Multigrid(levels, prols, pin, variant=variant, kernel=kernel)
+    if variant == VARIANT_MV:     # colour every smoothed level (R10)
+        for l in range(1, len(probs)):
+            mg.set_colors(l, *multicolor(probs[l]))
     fine = levels[-1]
     if free_inputs:   # the library copied everything it needs
         fine = {k: v for k, v in fine.items() if k in ("n", "nvel", "nnz", "b", "problem")}
