@@ -173,7 +173,9 @@ rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opt
     c->variant = o.variant;
     c->nvel = o.n_vel;
     rav_status st = csr_upload(A, c->A, c->stream);
-    if (st == RAV_OK && o.variant != RAV_VARIANT_MV) st = sell_build(c->A, c->stream);
+    if (st == RAV_OK && o.variant != RAV_VARIANT_MV && o.block_dim > 0 && o.kernel != RAV_KERNEL_WARP)
+        st = nb_build(c->A, o.n_vel, o.block_dim, c->stream);
+    if (st == RAV_OK && o.variant != RAV_VARIANT_MV && c->A.nb.nslices == 0) st = sell_build(c->A, c->stream);
     if (st == RAV_OK) st = patches_upload(P, A->n_rows, c->P, c->stream);
     bool done = false;
     const bool want_schur = o.block_dim > 0 && (o.kernel == RAV_KERNEL_AUTO || o.kernel == RAV_KERNEL_SCHUR);
@@ -312,6 +314,8 @@ rav_status rav_sweep_bytes(const rav_ctx* c, double* bytes_sweep, double* bytes_
     }
     double sweep = rows + idx + 8.0 * n /* r */ + 16.0 * n /* x rmw */;
     double resid = 12.0 * nnz + 8.0 * (n + 1) + 8.0 * n /* x */ + 8.0 * n /* b */ + 8.0 * n /* r write */;
+    if (c->A.nb.nslices > 0)   // node-blocked copy: its own entries + per-row permutation + vectors
+        resid = (double)c->A.nb.bytes + 4.0 * (double)c->A.nb.nblock + 24.0 * (double)c->A.nb.nslices + 24.0 * n;
     if (bytes_sweep) *bytes_sweep = sweep;
     if (bytes_residual) *bytes_residual = resid;
     if (flops) *flops = 2.0 * (double)c->P.rows_total + 2.0 * nnz;

@@ -22,6 +22,18 @@ struct Sell {
     int64_t stored = 0;        // sptr[nslices] (padded entries)
 };
 
+// node-blocked copy (nb.cu) for operators whose velocity block is I_d (x) A_s
+struct NodeBlocked {
+    int D = 0;
+    int64_t nnodes = 0, nblock = 0, nslices = 0, nvel = 0;
+    int32_t* perm = nullptr;   // slot -> block row (node rows first, then pressure rows)
+    int32_t *wa = nullptr, *wb = nullptr;
+    int64_t *cptr = nullptr, *vptr = nullptr;
+    int32_t* col = nullptr;
+    double* val = nullptr;
+    int64_t bytes = 0;
+};
+
 struct Csr {
     int64_t n_rows = 0, n_cols = 0, nnz = 0;
     int64_t* rp = nullptr;
@@ -29,9 +41,14 @@ struct Csr {
     double* val = nullptr;
     int lanes = 8;  // lanes per row used by the row-group SpMV kernels
     Sell sell;      // built for smoother operators (rav_setup); empty otherwise
+    NodeBlocked nb; // preferred over sell when the structure allows it
 };
 rav_status sell_build(Csr& A, cudaStream_t s);
 void sell_free(Sell& S);
+rav_status nb_build(Csr& A, int64_t nvel, int D, cudaStream_t s);
+void nb_free(NodeBlocked& N);
+rav_status launch_nb_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
+                              cudaStream_t s);
 // r = b - A x via the SELL copy; if part != nullptr also per-block sums of r^2 (nblk blocks)
 rav_status launch_sell_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
                                 cudaStream_t s);

@@ -117,6 +117,7 @@ static int spmv_blocks(int64_t n, int G) {
 
 rav_status launch_residual(const Csr& A, const double* x, const double* b, double* r, cudaStream_t s) {
     if (A.n_rows == 0) return RAV_OK;
+    if (A.nb.nslices > 0) return launch_nb_residual(A, x, b, r, nullptr, 0, s);
     if (A.sell.nslices > 0) return launch_sell_residual(A, x, b, r, nullptr, 0, s);
     int nb = spmv_blocks(A.n_rows, A.lanes);
     if (A.lanes == 32)
@@ -148,8 +149,9 @@ int residual_norm_blocks() { return num_sms() * 4; }
 
 rav_status launch_residual_norm2(const Csr& A, const double* x, const double* b, double* part, int nblk,
                                  double* out, cudaStream_t s) {
-    if (A.sell.nslices > 0) {
-        RAV_TRY(launch_sell_residual(A, x, b, nullptr, part, nblk, s));
+    if (A.nb.nslices > 0 || A.sell.nslices > 0) {
+        if (A.nb.nslices > 0) RAV_TRY(launch_nb_residual(A, x, b, nullptr, part, nblk, s));
+        else RAV_TRY(launch_sell_residual(A, x, b, nullptr, part, nblk, s));
         sum_parts_kernel<<<1, 256, 0, s>>>(part, nblk, out);
         count_launch();
         RAV_CHECK_LAUNCH();
@@ -232,6 +234,7 @@ rav_status csr_upload(const rav_csr* A, Csr& out, cudaStream_t s) {
 
 void csr_free(Csr& A) {
     sell_free(A.sell);
+    nb_free(A.nb);
     if (A.rp) cudaFree(A.rp);
     if (A.ci) cudaFree(A.ci);
     if (A.val) cudaFree(A.val);

@@ -1,0 +1,349 @@
+// nb.cu -- node-blocked copy of a Taylor-Hood level operator for the residual
+// r = b - L x (Eq. 10).
+//
+// For the Laplacian-form viscous term (Eq. 7) the velocity block of L is
+// I_d (x) A_s: the rows of the d components of a node carry the same columns
+// (shifted by the component) and bitwise-equal values, and they share their
+// pressure columns.  The node-blocked copy stores, per velocity NODE row j:
+//   A entries  (node k, a_jk)            one value for all components
+//   B entries  (pressure p, b_jp^c c<d)  d values per column
+// and per pressure row v:
+//   BT entries (node k, b_vk^c c<d)      d values per node
+// i.e. 12*nnz(A)/d + (4 + 8d)*nnz(B)/d*2 bytes instead of 12*nnz: -35% at c2.
+// Block rows are sorted by length in windows of 4096 and stored as SELL slices
+// of 32 rows (column-major), one thread per block row producing all d residual
+// components (x gathered as d contiguous values).  Each component sums its A
+// entries then its B entries in ascending column order -- the CSR order -- so
+// the result equals the CSR residual up to FMA contraction.
+//
+// nb_build verifies the structure (d divides n_vel, component rows with equal
+// patterns/values, no cross-component entries, pressure rows with complete
+// node groups); on failure the SELL copy is used instead.
+#include <algorithm>
+#include <cub/cub.cuh>
+
+#include "internal.cuh"
+
+namespace rav {
+
+constexpr int NB_C = 32;
+constexpr int NB_SIGMA = 4096;
+
+// per block row: (#A entries, #B entries) for node rows, (#BT entries, 0) for pressure rows
+__global__ void nb_count_kernel(int64_t nnodes, int64_t npres, int D, int64_t nvel, const int64_t* rp,
+                                const int32_t* ci, const double* val, int32_t* na, int32_t* nb,
+                                unsigned int* fail) {
+    const int64_t total = nnodes + npres;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        if (t < nnodes) {
+            const int64_t r0 = t * D;
+            const int64_t s0 = rp[r0], e0 = rp[r0 + 1];
+            int a = 0, b = 0;
+            for (int64_t k = s0; k < e0; ++k) {
+                const int c = ci[k];
+                if (c < nvel) {
+                    if (c % D != 0) atomicOr(fail, 1u);
+                    ++a;
+                } else {
+                    ++b;
+                }
+            }
+            for (int cc = 1; cc < D; ++cc) {       // rows of the other components: same pattern, same values
+                const int64_t s = rp[r0 + cc], e = rp[r0 + cc + 1];
+                if (e - s != e0 - s0) { atomicOr(fail, 1u); continue; }
+                for (int64_t k = 0; k < e - s; ++k) {
+                    const int c0 = ci[s0 + k], c1 = ci[s + k];
+                    if (c0 < nvel) {
+                        if (c1 != c0 + cc || val[s + k] != val[s0 + k]) atomicOr(fail, 1u);
+                    } else if (c1 != c0) {
+                        atomicOr(fail, 1u);
+                    }
+                }
+            }
+            na[t] = a;
+            nb[t] = b;
+        } else {
+            const int64_t row = nvel + (t - nnodes);
+            const int64_t s = rp[row], e = rp[row + 1];
+            if ((e - s) % D != 0) atomicOr(fail, 1u);
+            for (int64_t k = s; k < e; ++k)
+                if (ci[k] >= nvel || ci[k] % D != (k - s) % D || ((k - s) % D != 0 && ci[k] != ci[k - 1] + 1))
+                    atomicOr(fail, 1u);
+            na[t] = 0;                         // pressure rows: only "B-type" entries (node, d values)
+            nb[t] = (int32_t)((e - s) / D);
+        }
+    }
+}
+
+__global__ void nb_key_kernel(int64_t n, const int32_t* na, const int32_t* nb, int D, int32_t* key, int32_t* idx) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        key[t] = na[t] * 12 + nb[t] * (4 + 8 * D);   // bytes of the block row
+        idx[t] = (int32_t)t;
+    }
+}
+
+__global__ void nb_windows_kernel(int64_t n, int64_t nw, int64_t* off) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= nw; w += (int64_t)gridDim.x * blockDim.x)
+        off[w] = w * NB_SIGMA < n ? w * NB_SIGMA : n;
+}
+
+// per slice: widths (max over its 32 rows) and sizes in bytes-units
+__global__ void nb_slice_kernel(int64_t n, int64_t nslices, int D, const int32_t* perm, const int32_t* na,
+                                const int32_t* nb, int32_t* wa, int32_t* wb, int64_t* scol, int64_t* sval) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslices; s += (int64_t)gridDim.x * blockDim.x) {
+        int a = 0, b = 0;
+        for (int l = 0; l < NB_C; ++l) {
+            const int64_t t = s * NB_C + l;
+            if (t < n) {
+                a = max(a, na[perm[t]]);
+                b = max(b, nb[perm[t]]);
+            }
+        }
+        wa[s] = a;
+        wb[s] = b;
+        scol[s] = (int64_t)NB_C * (a + b);
+        sval[s] = (int64_t)NB_C * (a + (int64_t)b * D);
+    }
+}
+
+// slot t = 32 s + l; node rows: A cols/vals then B cols / D vals; pressure rows: BT cols (node dof of comp 0) / D vals
+__global__ void nb_fill_kernel(int64_t n, int64_t nnodes, int64_t nslices, int D, int64_t nvel, const int64_t* rp,
+                               const int32_t* ci, const double* val, const int32_t* perm, const int32_t* wa,
+                               const int32_t* wb, const int64_t* cptr, const int64_t* vptr, int32_t* col,
+                               double* v) {
+    const int64_t total = nslices * NB_C;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t / NB_C;
+        const int l = (int)(t % NB_C);
+        const int A = wa[s], B = wb[s];
+        int32_t* cA = col + cptr[s] + l;
+        int32_t* cB = cA + (int64_t)A * NB_C;
+        double* vA = v + vptr[s] + l;
+        double* vB = vA + (int64_t)A * NB_C;
+        if (t >= n) {
+            for (int k = 0; k < A; ++k) { cA[k * NB_C] = 0; vA[k * NB_C] = 0.0; }
+            for (int k = 0; k < B; ++k) {
+                cB[k * NB_C] = 0;
+                for (int c = 0; c < D; ++c) vB[((int64_t)k * D + c) * NB_C] = 0.0;
+            }
+            continue;
+        }
+        const int64_t br = perm[t];
+        if (br < nnodes) {
+            const int64_t r0 = br * D;
+            const int64_t s0 = rp[r0], e0 = rp[r0 + 1];
+            int a = 0, b = 0;
+            for (int64_t k = s0; k < e0; ++k) {
+                const int c = ci[k];
+                if (c < nvel) {
+                    cA[a * NB_C] = c;
+                    vA[a * NB_C] = val[k];
+                    ++a;
+                } else {
+                    cB[b * NB_C] = c;
+                    for (int cc = 0; cc < D; ++cc) vB[((int64_t)b * D + cc) * NB_C] = val[rp[r0 + cc] + (k - s0)];
+                    ++b;
+                }
+            }
+            for (; a < A; ++a) { cA[a * NB_C] = (int32_t)r0; vA[a * NB_C] = 0.0; }
+            for (; b < B; ++b) {
+                cB[b * NB_C] = (int32_t)nvel;
+                for (int cc = 0; cc < D; ++cc) vB[((int64_t)b * D + cc) * NB_C] = 0.0;
+            }
+        } else {
+            const int64_t row = nvel + (br - nnodes);
+            const int64_t s0 = rp[row], e0 = rp[row + 1];
+            for (int a = 0; a < A; ++a) { cA[a * NB_C] = 0; vA[a * NB_C] = 0.0; }
+            int q = 0;
+            for (int64_t k = s0; k < e0; k += D, ++q) {
+                cB[q * NB_C] = ci[k];   // component-0 dof of the node
+                for (int cc = 0; cc < D; ++cc) vB[((int64_t)q * D + cc) * NB_C] = val[k + cc];
+            }
+            for (; q < B; ++q) {
+                cB[q * NB_C] = 0;
+                for (int cc = 0; cc < D; ++cc) vB[((int64_t)q * D + cc) * NB_C] = 0.0;
+            }
+        }
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) nb_residual_kernel(int64_t n, int64_t nnodes, int64_t nslices, int64_t nvel,
+                                                          const int32_t* __restrict__ perm,
+                                                          const int32_t* __restrict__ wa,
+                                                          const int32_t* __restrict__ wb,
+                                                          const int64_t* __restrict__ cptr,
+                                                          const int64_t* __restrict__ vptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const double* __restrict__ v, const double* __restrict__ x,
+                                                          const double* __restrict__ b, double* __restrict__ r,
+                                                          double* __restrict__ part) {
+    __shared__ double red[8];
+    double mine = 0.0;
+    const int64_t total = nslices * NB_C;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - threadIdx.x < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        if (t >= total) continue;
+        const int64_t s = t / NB_C;
+        const int l = (int)(t % NB_C);
+        const int A = wa[s], B = wb[s];
+        const int32_t* cA = col + cptr[s] + l;
+        const int32_t* cB = cA + (int64_t)A * NB_C;
+        const double* vA = v + vptr[s] + l;
+        const double* vB = vA + (int64_t)A * NB_C;
+        const int64_t br = t < n ? perm[t] : -1;
+        if (br < 0) continue;
+        if (br < nnodes) {
+            double acc[D];
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[c] = 0.0;
+#pragma unroll 4
+            for (int k = 0; k < A; ++k) {
+                const int cc = __ldcs(cA + k * NB_C);
+                const double a = __ldcs(vA + k * NB_C);
+#pragma unroll
+                for (int c = 0; c < D; ++c) acc[c] = fma(a, __ldg(x + cc + c), acc[c]);
+            }
+#pragma unroll 2
+            for (int k = 0; k < B; ++k) {
+                const double xp = __ldg(x + __ldcs(cB + k * NB_C));
+#pragma unroll
+                for (int c = 0; c < D; ++c) acc[c] = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), xp, acc[c]);
+            }
+            const int64_t r0 = br * D;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const double rr = b[r0 + c] - acc[c];
+                if (r) r[r0 + c] = rr;
+                mine += rr * rr;
+            }
+        } else {
+            double acc = 0.0;
+#pragma unroll 4
+            for (int k = 0; k < B; ++k) {
+                const int cc = __ldcs(cB + k * NB_C);
+#pragma unroll
+                for (int c = 0; c < D; ++c) acc = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), __ldg(x + cc + c), acc);
+            }
+            const int64_t row = nvel + (br - nnodes);
+            const double rr = b[row] - acc;
+            if (r) r[row] = rr;
+            mine += rr * rr;
+        }
+    }
+    if (part) {
+        mine = warp_sum(mine);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mine;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double sum = 0.0;
+            for (int i = 0; i < 8; ++i) sum += red[i];
+            part[blockIdx.x] = sum;
+        }
+    }
+}
+
+rav_status nb_build(Csr& A, int64_t nvel, int D, cudaStream_t s) {
+    NodeBlocked& N = A.nb;
+    if (D < 2 || D > 3 || nvel <= 0 || nvel % D != 0 || A.n_rows != A.n_cols || nvel >= A.n_rows) return RAV_OK;
+    const int64_t nnodes = nvel / D, npres = A.n_rows - nvel, n = nnodes + npres;
+    int32_t *na = nullptr, *nbv = nullptr, *key = nullptr, *idx = nullptr, *skey = nullptr;
+    int64_t* woff = nullptr;
+    unsigned int* fail = nullptr;
+    RAV_CUDA(cudaMallocAsync(&na, sizeof(int32_t) * n, s));
+    RAV_CUDA(cudaMallocAsync(&nbv, sizeof(int32_t) * n, s));
+    RAV_CUDA(cudaMallocAsync(&fail, sizeof(unsigned int), s));
+    RAV_CUDA(cudaMemsetAsync(fail, 0, sizeof(unsigned int), s));
+    const int nb1 = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)num_sms() * 16));
+    nb_count_kernel<<<nb1, 256, 0, s>>>(nnodes, npres, D, nvel, A.rp, A.ci, A.val, na, nbv, fail);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    unsigned int h_fail = 0;
+    RAV_CUDA(cudaMemcpyAsync(&h_fail, fail, sizeof(h_fail), cudaMemcpyDeviceToHost, s));
+    RAV_CUDA(cudaStreamSynchronize(s));
+    cudaFreeAsync(fail, s);
+    if (h_fail) {
+        cudaFreeAsync(na, s);
+        cudaFreeAsync(nbv, s);
+        return RAV_OK;   // structure does not hold: keep the SELL residual
+    }
+    N.D = D;
+    N.nnodes = nnodes;
+    N.nblock = n;
+    N.nslices = cdiv(n, NB_C);
+    const int64_t nw = cdiv(n, NB_SIGMA);
+    RAV_CUDA(cudaMallocAsync(&key, sizeof(int32_t) * n, s));
+    RAV_CUDA(cudaMallocAsync(&skey, sizeof(int32_t) * n, s));
+    RAV_CUDA(cudaMallocAsync(&idx, sizeof(int32_t) * n, s));
+    RAV_CUDA(cudaMallocAsync(&woff, sizeof(int64_t) * (nw + 1), s));
+    RAV_CUDA(cudaMalloc(&N.perm, sizeof(int32_t) * N.nslices * NB_C));
+    RAV_CUDA(cudaMemsetAsync(N.perm, 0, sizeof(int32_t) * N.nslices * NB_C, s));
+    nb_key_kernel<<<nb1, 256, 0, s>>>(n, na, nbv, D, key, idx);
+    count_launch();
+    nb_windows_kernel<<<(int)std::max<int64_t>(1, cdiv(nw + 1, 256)), 256, 0, s>>>(n, nw, woff);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    size_t tmp = 0;
+    RAV_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(nullptr, tmp, key, skey, idx, N.perm, (int)n, (int)nw,
+                                                                woff, woff + 1, 0, 8 * sizeof(int32_t), s));
+    void* d_tmp = nullptr;
+    RAV_CUDA(cudaMallocAsync(&d_tmp, tmp + 16, s));
+    RAV_CUDA(cub::DeviceSegmentedRadixSort::SortPairsDescending(d_tmp, tmp, key, skey, idx, N.perm, (int)n, (int)nw,
+                                                                woff, woff + 1, 0, 8 * sizeof(int32_t), s));
+    int64_t *csz = nullptr, *vsz = nullptr;
+    RAV_CUDA(cudaMalloc(&N.wa, sizeof(int32_t) * N.nslices));
+    RAV_CUDA(cudaMalloc(&N.wb, sizeof(int32_t) * N.nslices));
+    RAV_CUDA(cudaMalloc(&N.cptr, sizeof(int64_t) * (N.nslices + 1)));
+    RAV_CUDA(cudaMalloc(&N.vptr, sizeof(int64_t) * (N.nslices + 1)));
+    RAV_CUDA(cudaMallocAsync(&csz, sizeof(int64_t) * N.nslices, s));
+    RAV_CUDA(cudaMallocAsync(&vsz, sizeof(int64_t) * N.nslices, s));
+    const int nbs = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(N.nslices, 256), (int64_t)num_sms() * 16));
+    nb_slice_kernel<<<nbs, 256, 0, s>>>(n, N.nslices, D, N.perm, na, nbv, N.wa, N.wb, csz, vsz);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    RAV_TRY(gen::counts_to_rowptr(csz, N.cptr, N.nslices, s));
+    RAV_TRY(gen::counts_to_rowptr(vsz, N.vptr, N.nslices, s));
+    int64_t hc = 0, hv = 0;
+    RAV_CUDA(cudaMemcpyAsync(&hc, N.cptr + N.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    RAV_CUDA(cudaMemcpyAsync(&hv, N.vptr + N.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    RAV_CUDA(cudaStreamSynchronize(s));
+    RAV_CUDA(cudaMalloc(&N.col, sizeof(int32_t) * std::max<int64_t>(1, hc)));
+    RAV_CUDA(cudaMalloc(&N.val, sizeof(double) * std::max<int64_t>(1, hv)));
+    N.bytes = 4 * hc + 8 * hv;
+    const int nbf = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(N.nslices * NB_C, 256), (int64_t)num_sms() * 16));
+    nb_fill_kernel<<<nbf, 256, 0, s>>>(n, nnodes, N.nslices, D, nvel, A.rp, A.ci, A.val, N.perm, N.wa, N.wb, N.cptr,
+                                       N.vptr, N.col, N.val);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    for (void* p : {(void*)na, (void*)nbv, (void*)key, (void*)skey, (void*)idx, (void*)woff, d_tmp, (void*)csz,
+                    (void*)vsz})
+        cudaFreeAsync(p, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    N.nvel = nvel;
+    return RAV_OK;
+}
+
+void nb_free(NodeBlocked& N) {
+    for (void* p : {(void*)N.perm, (void*)N.wa, (void*)N.wb, (void*)N.cptr, (void*)N.vptr, (void*)N.col, (void*)N.val})
+        if (p) cudaFree(p);
+    N = NodeBlocked{};
+}
+
+rav_status launch_nb_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
+                              cudaStream_t s) {
+    const NodeBlocked& N = A.nb;
+    const int64_t total = N.nslices * NB_C;
+    int blocks = (int)cdiv(total, 256);
+    if (part) blocks = nblk;
+    if (N.D == 3)
+        nb_residual_kernel<3><<<blocks, 256, 0, s>>>(N.nblock, N.nnodes, N.nslices, N.nvel, N.perm, N.wa, N.wb, N.cptr,
+                                                     N.vptr, N.col, N.val, x, b, r, part);
+    else
+        nb_residual_kernel<2><<<blocks, 256, 0, s>>>(N.nblock, N.nnodes, N.nslices, N.nvel, N.perm, N.wa, N.wb, N.cptr,
+                                                     N.vptr, N.col, N.val, x, b, r, part);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}
+
+}  // namespace rav

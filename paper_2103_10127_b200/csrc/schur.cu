@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
                                                                  const int32_t* __restrict__ NR,
                                                                  const double* __restrict__ AUX,
                                                                  const double* __restrict__ r,
-                                                                 double* __restrict__ x, double omega) {
+                                                                 double* __restrict__ x, double omega, int pf) {
     constexpr int TRI = MT * (MT + 1) / 2 + MT * D;
     constexpr int TRI_PAD = TRI + (TRI & 1);
     constexpr int RC = MT + D;   // entries per rectangular column
@@ -421,6 +421,16 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
     if (chunk >= nchunks) return;
     const double2* wp = W + chunk * pairs * 32 + lane;
     const int32_t* np_ = ND + chunk * (int64_t)NN * 32 + lane;
+    // TMA prefetch of the rectangular column blocks into L2 (no registers / smem):
+    // the first PF_AHEAD blocks now, block k + PF_AHEAD while block k is consumed
+    constexpr int PF_AHEAD = 3;
+    const char* rect0 = reinterpret_cast<const char*>(W + chunk * pairs * 32 + (TRI_PAD / 2) * 32);
+    constexpr unsigned RB = (unsigned)RC * 512u;          // bytes of one two-column block
+    const int nblocks = (NN - MT) / 2;
+    if (pf && lane == 0)
+        for (int k = 0; k < PF_AHEAD && k < nblocks; ++k)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rect0 + (size_t)k * RB), "r"(RB)
+                         : "memory");
     double acc[MT][D], rr[MT][D], gR[MT][D];
     double gacc = 0.0;
 #pragma unroll
@@ -459,6 +469,10 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
     // rectangular columns, two at a time (2 * RC entries = RC pairs)
     const double2* wq0 = wp + (TRI_PAD / 2) * 32;
     for (int j0 = MT; j0 < NN; j0 += 2) {
+        const int blk = (j0 - MT) / 2 + PF_AHEAD;
+        if (pf && lane == 0 && blk < nblocks)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rect0 + (size_t)blk * RB), "r"(RB)
+                         : "memory");
         double ra[D], rb[D];
         const int n0 = __ldcs(np_ + j0 * 32), n1 = __ldcs(np_ + (j0 + 1) * 32);
 #pragma unroll
@@ -980,22 +994,26 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
         const char* e = getenv("RAV_SCHUR_MINB");
         return e ? atoi(e) : 4;
     }();
+    static const int pf = [] {
+        const char* e = getenv("RAV_SCHUR_PF");   // L2 bulk prefetch: measured slower (127 vs 124 us), off
+        return e ? atoi(e) : 0;
+    }();
     if (minb >= 6)
         schur_sweep_thread_kernel<MT, 2, 6><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
                                                                    reinterpret_cast<const double2*>(F.facT), F.DT,
-                                                                   F.PD, F.NR, F.WT, r, x, omega);
+                                                                   F.PD, F.NR, F.WT, r, x, omega, pf);
     else if (minb == 5)
         schur_sweep_thread_kernel<MT, 2, 5><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
                                                                    reinterpret_cast<const double2*>(F.facT), F.DT,
-                                                                   F.PD, F.NR, F.WT, r, x, omega);
+                                                                   F.PD, F.NR, F.WT, r, x, omega, pf);
     else if (minb >= 4)
         schur_sweep_thread_kernel<MT, 2, 4><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
                                                                    reinterpret_cast<const double2*>(F.facT), F.DT,
-                                                                   F.PD, F.NR, F.WT, r, x, omega);
+                                                                   F.PD, F.NR, F.WT, r, x, omega, pf);
     else
         schur_sweep_thread_kernel<MT, 2, 1><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
                                                                    reinterpret_cast<const double2*>(F.facT), F.DT,
-                                                                   F.PD, F.NR, F.WT, r, x, omega);
+                                                                   F.PD, F.NR, F.WT, r, x, omega, pf);
 }
 
 rav_status launch_schur_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
