@@ -271,6 +271,47 @@ def run_vcycle_smoothers(rg, si, stream):
     return out
 
 
+def run_dist_vcycle(name, rdist, si, stream, dist, ws, rank):
+    """Slab-partitioned V-cycle to rtol on ws GPUs (strong scaling of c3 / c4):
+    partitioned fine levels with NCCL interface sums / halo refreshes, windowed
+    transfers, the coarse levels agglomerated (all-reduced rhs, solved
+    redundantly on every rank); ||r||^2 all-reduced per cycle.  Device time
+    with CUDA events around the solve, max over ranks."""
+    import torch
+    c = si.CONFIGS[name]
+    prob = si.config_problem(name)
+    t0 = time.perf_counter()
+    cyc, levels = rdist.build_gpu_cycle(prob, c["levels"], ws, rank, rdist.TorchComm())
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    x, b = levels[0]["x"], levels[0]["b"]
+    cyc.solve(x, b, pre=c["pre"], post=c["post"], omega=c["omega"], rtol=c["rtol"], maxit=2)   # warm
+    times = []
+    for _ in range(2):
+        x.zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, iters, hist = cyc.solve(x, b, pre=c["pre"], post=c["post"], omega=c["omega"], rtol=c["rtol"],
+                                   maxit=100)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    tt = torch.tensor([min(times)], device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t = float(tt.item())
+    slab = levels[0]["slab"]
+    out = {"config": VCYCLE_DESC[name] + f"; slab-partitioned over {ws} GPUs",
+           "free_dofs": slab.nvel_glob + slab.nvert_glob, "rtol": c["rtol"], "cycles": iters,
+           "converged": bool(hist[-1] <= c["rtol"] * hist[0]), "time_to_rtol_s": t,
+           "ms_per_cycle": t / max(iters, 1) * 1e3, "partitioned_levels": len(levels), "setup_s": setup_s,
+           "timing": "CUDA events around DistVCycle.solve, best of 2, max over ranks"}
+    del cyc, levels, x, b
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_gpu_dist(args):
     """N > 1 (torchrun): weak scaling of the c2 workload, one 512^2 block per GPU
     stacked along y (BASELINE config 5's layout): the finest level is
@@ -375,6 +416,16 @@ def run_gpu_dist(args):
         "gpu_launches": kernels_per_sweep * SWEEPS_PER_STEP * args.steps,
         "clocks": clk.summary(),
     }
+    if not args.no_vcycle:
+        del sw, sm, L
+        torch.cuda.empty_cache()
+        vc = {}
+        for name in ("c3", "c4"):
+            try:
+                vc[name] = run_dist_vcycle(name, rdist, si, stream, dist, ws, rank)
+            except Exception as e:  # report, keep the sweep line
+                vc[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+        line["vcycle"] = vc
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

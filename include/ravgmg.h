@@ -80,7 +80,7 @@ typedef struct {
      * only for nodes in [rnode_lo, rnode_hi] and vertices in [rvert_lo,
      * rvert_hi] (other rows are empty, b = 0); patches exist for the vertices in
      * [pvert_lo, pvert_hi].  Columns must fall inside the window (else
-     * RAV_ERR_ARG).  Transfers are not windowed. */
+     * RAV_ERR_ARG).  Transfers: see rav_gen_prolongation. */
     int32_t win;
     int32_t node_lo, node_hi, vert_lo, vert_hi;
     int32_t rnode_lo, rnode_hi, rvert_lo, rvert_hi;
@@ -115,7 +115,13 @@ rav_status rav_gen_patches(const rav_grid* g, int weights, int64_t* offs, int32_
 /* Nested prolongation P from `coarse` (ncell/2) to `fine`: Q2
  * interpolation for velocity, Q1 for pressure, Dirichlet rows/columns
  * dropped.  Rows = fine DoFs, columns = coarse DoFs, sorted.  nnz first
- * (synchronizes), then fill device buffers rp[n_fine+1], ci[nnz], val[nnz]. */
+ * (synchronizes), then fill device buffers rp[n_fine+1], ci[nnz], val[nnz].
+ * Windows (multi-rank cycles): rows are the LOCAL DoFs of the fine grid's
+ * window, and only rows inside its row window [rnode_lo, rnode_hi] /
+ * [rvert_lo, rvert_hi] are filled (the others are empty) -- a rank passes its
+ * OWNED layers there.  Columns are LOCAL DoFs of the coarse grid's window
+ * (global ids when coarse->win = 0); a row interpolating from outside the
+ * coarse window is RAV_ERR_ARG.  n_fine = the fine window's n_dofs. */
 rav_status rav_gen_prolongation_nnz(const rav_grid* fine, const rav_grid* coarse, void* stream,
                                     int64_t* nnz);
 rav_status rav_gen_prolongation(const rav_grid* fine, const rav_grid* coarse, int64_t* rp,
@@ -283,6 +289,23 @@ rav_status mg_solve(mg_ctx* ctx, double* x, const double* b, int pre, int post, 
  *                                       3 fill dst[idx[k]] = value (src unused) */
 rav_status rav_index_op(int op, const double* src, const int32_t* idx, int64_t n, double* dst, double value,
                         void* stream);
+
+/* Transfer operator of a host-driven (multi-rank) cycle (SURVEY section
+ * 8 rows a7 / e): rav_xfer_setup copies P (rav_csr, host or device, n_rows =
+ * fine DoFs, n_cols = coarse DoFs) and builds R = P^T on the device.
+ * rav_prolong: xf += alpha P xc.  rav_restrict: bc = P^T rf (bc overwritten).
+ * Device pointers, stream-ordered on the transfer's stream. */
+typedef struct rav_xfer rav_xfer;
+rav_status rav_xfer_setup(const rav_csr* P, void* stream, rav_xfer** out);
+rav_status rav_prolong(rav_xfer* t, const double* xc, double* xf, double alpha);
+rav_status rav_restrict(rav_xfer* t, const double* rf, double* bc);
+rav_status rav_xfer_set_stream(rav_xfer* t, void* stream);
+void rav_xfer_destroy(rav_xfer* t);
+
+/* *out = sum_{i<n} a[i] b[i] (accumulate = 1: *out += ...), device pointers,
+ * fixed reduction order (bitwise reproducible).  Used for the residual norm
+ * of the stopping test (R11) over a rank's owned DoFs. */
+rav_status rav_dot(const double* a, const double* b, int64_t n, double* out, int accumulate, void* stream);
 
 /* Colouring of the smoother on level `level` (1 .. n_levels-1) for
  * RAV_VARIANT_MV (same contract as rav_set_colors). */

@@ -569,3 +569,69 @@ rav_status mg_set_colors(mg_ctx* m, int level, int n_colors, const int64_t* colo
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------------------
+// transfers and reductions for host-driven (multi-rank) cycles
+// ------------------------------------------------------------------------------------
+
+struct rav_xfer {
+    Csr P, PT;
+    cudaStream_t stream = nullptr;
+    int64_t last_launches = 0;
+};
+
+extern "C" {
+
+rav_status rav_xfer_setup(const rav_csr* P, void* stream, rav_xfer** out) {
+    if (!P || !out) { set_error("rav_xfer_setup: NULL argument"); return RAV_ERR_ARG; }
+    *out = nullptr;
+    rav_xfer* t = new rav_xfer();
+    t->stream = as_stream(stream);
+    rav_status st = csr_upload(P, t->P, t->stream);
+    if (st == RAV_OK) st = csr_transpose(t->P, t->PT, t->stream);
+    if (st != RAV_OK) { rav_xfer_destroy(t); return st; }
+    *out = t;
+    return RAV_OK;
+}
+
+rav_status rav_prolong(rav_xfer* t, const double* xc, double* xf, double alpha) {
+    if (!t || !xc || !xf) { set_error("rav_prolong: NULL argument"); return RAV_ERR_ARG; }
+    g_launches = 0;
+    RAV_TRY(launch_spmv(t->P, xc, xf, alpha, 1.0, t->stream));
+    t->last_launches = g_launches;
+    return RAV_OK;
+}
+
+rav_status rav_restrict(rav_xfer* t, const double* rf, double* bc) {
+    if (!t || !rf || !bc) { set_error("rav_restrict: NULL argument"); return RAV_ERR_ARG; }
+    g_launches = 0;
+    RAV_TRY(launch_spmv(t->PT, rf, bc, 1.0, 0.0, t->stream));
+    t->last_launches = g_launches;
+    return RAV_OK;
+}
+
+rav_status rav_xfer_set_stream(rav_xfer* t, void* stream) {
+    if (!t) { set_error("NULL xfer"); return RAV_ERR_ARG; }
+    t->stream = as_stream(stream);
+    return RAV_OK;
+}
+
+void rav_xfer_destroy(rav_xfer* t) {
+    if (!t) return;
+    if (t->stream) cudaStreamSynchronize(t->stream);
+    else cudaDeviceSynchronize();
+    csr_free(t->P);
+    csr_free(t->PT);
+    delete t;
+}
+
+rav_status rav_dot(const double* a, const double* b, int64_t n, double* out, int accumulate, void* stream) {
+    if (n < 0 || !out || (n > 0 && (!a || !b))) { set_error("rav_dot: bad argument"); return RAV_ERR_ARG; }
+    g_launches = 0;
+    static thread_local double* part = nullptr;
+    const int nblk = residual_norm_blocks();
+    if (!part) RAV_CUDA(cudaMalloc(&part, sizeof(double) * nblk));
+    return launch_dot(a, b, n, part, nblk, out, accumulate, as_stream(stream));
+}
+
+}  // extern "C"

@@ -555,38 +555,39 @@ __device__ __forceinline__ int interp_q1(int bf, int* idx, double* wt) {
 }
 
 template <bool FILL>
-__global__ void prol_kernel(Grid F, Grid Cg, int64_t* cnt_or_rp, int32_t* ci, double* val) {
-    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < F.ndof;
+__global__ void prol_kernel(Grid F, Grid Cg, int64_t* cnt_or_rp, int32_t* ci, double* val, unsigned int* err) {
+    // rows: LOCAL DoFs of the fine window (rows outside its row window are empty);
+    // columns: LOCAL DoFs of the coarse window (= global ids when it is the whole grid)
+    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < F.ndof_loc;
          row += (int64_t)gridDim.x * blockDim.x) {
         int idx[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
         double wt[3][3] = {{1, 0, 0}, {1, 0, 0}, {1, 0, 0}};
         int cnt[3] = {1, 1, 1};
-        int comp = -1;
-        if (row < F.nvel) {
-            int a[3];
-            decode_vel_row(F, row, a, comp);
-            for (int k = 0; k < F.dim; ++k) cnt[k] = interp_q2(a[k], Cg.n[k], idx[k], wt[k]);
-        } else {
-            int v[3];
-            decode_vertex(F, row - F.nvel, v);
-            for (int k = 0; k < F.dim; ++k) cnt[k] = interp_q1(v[k], idx[k], wt[k]);
+        int a[3] = {0, 0, 0}, comp = 0;
+        bool vel;
+        if (!decode_local_row(F, row, a, comp, vel)) {
+            if (!FILL) cnt_or_rp[row] = 0;
+            continue;
         }
+        for (int k = 0; k < F.dim; ++k)
+            cnt[k] = vel ? interp_q2(a[k], Cg.n[k], idx[k], wt[k]) : interp_q1(a[k], idx[k], wt[k]);
         int64_t p = FILL ? cnt_or_rp[row] : 0;
         int64_t c = 0;
         for (int s2 = 0; s2 < cnt[2]; ++s2)
             for (int s1 = 0; s1 < cnt[1]; ++s1)
                 for (int s0 = 0; s0 < cnt[0]; ++s0) {
-                    int a[3] = {idx[0][s0], idx[1][s1], F.dim > 2 ? idx[2][s2] : 0};
+                    int ac[3] = {idx[0][s0], idx[1][s1], F.dim > 2 ? idx[2][s2] : 0};
                     double w = wt[0][s0] * wt[1][s1];
                     if (F.dim > 2) w *= wt[2][s2];
                     int64_t colid;
-                    if (comp >= 0) {
-                        int64_t fc = free_id(Cg, a);
+                    if (vel) {
+                        int64_t fc = free_id(Cg, ac);
                         if (fc < 0) continue;
-                        colid = fc * F.dim + comp;
+                        colid = loc_vel(Cg, fc * F.dim + comp);
                     } else {
-                        colid = Cg.nvel + vert_id(Cg, a);
+                        colid = loc_vert(Cg, vert_id(Cg, ac));
                     }
+                    if (colid < 0) { atomicOr(err, 1u); continue; }
                     if (FILL) { ci[p + c] = (int32_t)colid; val[p + c] = w; }
                     ++c;
                 }
@@ -727,48 +728,65 @@ static rav_status check_nested(const rav_grid* f, const rav_grid* c) {
     RAV_TRY(check_grid(f));
     RAV_TRY(check_grid(c));
     if (f->dim != c->dim) { set_error("prolongation: dim mismatch"); return RAV_ERR_ARG; }
-    if (f->win || c->win) { set_error("prolongation: windowed grids are not supported"); return RAV_ERR_ARG; }
     for (int k = 0; k < f->dim; ++k)
         if (f->ncell[k] != 2 * c->ncell[k]) { set_error("prolongation: fine ncell must be 2 x coarse"); return RAV_ERR_ARG; }
+    return RAV_OK;
+}
+
+// count (FILL = false into cnt) or fill the prolongation; err set when a column leaves the coarse window
+static rav_status prol_pass(const Grid& F, const Grid& Cg, int64_t* rp_or_cnt, int32_t* ci, double* val, bool fill,
+                            cudaStream_t s) {
+    unsigned int* err = nullptr;
+    RAV_CUDA(cudaMallocAsync(&err, sizeof(unsigned int), s));
+    RAV_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
+    if (fill) prol_kernel<true><<<grid_for(F.ndof_loc, 256), 256, 0, s>>>(F, Cg, rp_or_cnt, ci, val, err);
+    else prol_kernel<false><<<grid_for(F.ndof_loc, 256), 256, 0, s>>>(F, Cg, rp_or_cnt, nullptr, nullptr, err);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    unsigned int h_err = 0;
+    RAV_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(h_err), cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(err, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    if (h_err) { set_error("prolongation: a row of the fine row window interpolates from outside the coarse window"); return RAV_ERR_ARG; }
     return RAV_OK;
 }
 
 extern "C" rav_status rav_gen_prolongation_nnz(const rav_grid* fine, const rav_grid* coarse, void* stream,
                                                int64_t* nnz) {
     RAV_TRY(check_nested(fine, coarse));
+    if (!nnz) { set_error("rav_gen_prolongation_nnz: NULL nnz"); return RAV_ERR_ARG; }
     Grid F = make_grid(fine), Cg = make_grid(coarse);
     cudaStream_t s = as_stream(stream);
     int64_t *cnt = nullptr, *rp = nullptr;
-    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * F.ndof, s));
-    RAV_CUDA(cudaMallocAsync(&rp, sizeof(int64_t) * (F.ndof + 1), s));
-    prol_kernel<false><<<grid_for(F.ndof, 256), 256, 0, s>>>(F, Cg, cnt, nullptr, nullptr);
-    count_launch();
-    RAV_CHECK_LAUNCH();
-    RAV_TRY(counts_to_rowptr(cnt, rp, F.ndof, s));
+    const int64_t nr = std::max<int64_t>(1, F.ndof_loc);
+    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * nr, s));
+    RAV_CUDA(cudaMallocAsync(&rp, sizeof(int64_t) * (nr + 1), s));
+    rav_status st = prol_pass(F, Cg, cnt, nullptr, nullptr, false, s);
     int64_t h = 0;
-    RAV_CUDA(cudaMemcpyAsync(&h, rp + F.ndof, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (st == RAV_OK && F.ndof_loc > 0) {
+        st = counts_to_rowptr(cnt, rp, F.ndof_loc, s);
+        if (st == RAV_OK) RAV_CUDA(cudaMemcpyAsync(&h, rp + F.ndof_loc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    }
     cudaFreeAsync(cnt, s);
     cudaFreeAsync(rp, s);
     RAV_CUDA(cudaStreamSynchronize(s));
     *nnz = h;
-    return RAV_OK;
+    return st;
 }
 
 extern "C" rav_status rav_gen_prolongation(const rav_grid* fine, const rav_grid* coarse, int64_t* rp,
                                            int32_t* ci, double* val, void* stream) {
     RAV_TRY(check_nested(fine, coarse));
+    if (!rp) { set_error("rav_gen_prolongation: NULL buffer"); return RAV_ERR_ARG; }
     Grid F = make_grid(fine), Cg = make_grid(coarse);
     cudaStream_t s = as_stream(stream);
+    if (F.ndof_loc == 0) { RAV_CUDA(cudaMemsetAsync(rp, 0, sizeof(int64_t), s)); return RAV_OK; }
     int64_t* cnt = nullptr;
-    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * F.ndof, s));
-    prol_kernel<false><<<grid_for(F.ndof, 256), 256, 0, s>>>(F, Cg, cnt, nullptr, nullptr);
-    count_launch();
-    RAV_CHECK_LAUNCH();
-    RAV_TRY(counts_to_rowptr(cnt, rp, F.ndof, s));
-    prol_kernel<true><<<grid_for(F.ndof, 256), 256, 0, s>>>(F, Cg, rp, ci, val);
-    count_launch();
-    RAV_CHECK_LAUNCH();
+    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * F.ndof_loc, s));
+    rav_status st = prol_pass(F, Cg, cnt, nullptr, nullptr, false, s);
+    if (st == RAV_OK) st = counts_to_rowptr(cnt, rp, F.ndof_loc, s);
+    if (st == RAV_OK) st = prol_pass(F, Cg, rp, ci, val, true, s);
     cudaFreeAsync(cnt, s);
     RAV_CUDA(cudaStreamSynchronize(s));
-    return RAV_OK;
+    return st;
 }

@@ -171,6 +171,48 @@ rav_status launch_residual_norm2(const Csr& A, const double* x, const double* b,
     return RAV_OK;
 }
 
+// partial dot products per block (fixed order => deterministic)
+__global__ void __launch_bounds__(256) dot_kernel(int64_t n, const double* __restrict__ a,
+                                                  const double* __restrict__ b, double* __restrict__ part) {
+    __shared__ double red[8];
+    double t = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        t = fma(a[i], b[i], t);
+    t = warp_sum(t);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double u = 0.0;
+        for (int w = 0; w < 8; ++w) u += red[w];
+        part[blockIdx.x] = u;
+    }
+}
+
+__global__ void sum_parts_acc_kernel(const double* __restrict__ part, int nblk, double* out, int accumulate) {
+    __shared__ double red[256];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < nblk; i += blockDim.x) t += part[i];
+    red[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = accumulate ? *out + red[0] : red[0];
+}
+
+rav_status launch_dot(const double* a, const double* b, int64_t n, double* part, int nblk, double* out,
+                      int accumulate, cudaStream_t s) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(std::max<int64_t>(n, 1), 256), nblk));
+    dot_kernel<<<blocks, 256, 0, s>>>(n, a, b, part);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    sum_parts_acc_kernel<<<1, 256, 0, s>>>(part, blocks, out, accumulate);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}
+
 // pack / unpack for the slab exchanges
 __global__ void index_op_kernel(int op, const double* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
                                 double* __restrict__ dst, double value) {

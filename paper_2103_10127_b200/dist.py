@@ -48,14 +48,15 @@ def partition_layers(n_vertex_layers: int, nranks: int, min_layers: int = 3) -> 
 class Slab:
     """Geometry of rank `rank`'s window and its local <-> global DoF maps."""
 
-    def __init__(self, problem: Dict, nranks: int, rank: int):
+    def __init__(self, problem: Dict, nranks: int, rank: int, layers: Sequence[Tuple[int, int]] = None):
         self.problem = problem
         self.dim = dim = problem["dim"]
         self.nranks, self.rank = nranks, rank
         nc = [int(c) for c in problem["ncell"][:dim]]
         n = nc[-1]
         self.n_last = n
-        self.layers = partition_layers(n + 1, nranks)
+        self.layers = list(layers) if layers is not None else partition_layers(n + 1, nranks)
+        assert len(self.layers) == nranks and self.layers[0][0] == 0 and self.layers[-1][1] == n + 1
         V0, V1 = self.layers[rank]
         self.V0, self.V1 = V0, V1
         self.nlow_free = int(np.prod([2 * c - 1 for c in nc[:-1]]))
@@ -110,6 +111,24 @@ class Slab:
 
     def owned_mask(self) -> np.ndarray:
         return self.owner_of_global(self.global_ids()) == self.rank
+
+    def owned_ranges(self) -> List[Tuple[int, int]]:
+        """The owned local DoFs as two contiguous ranges [a, b): velocity, pressure."""
+        w = self.window
+        per = self.dim * self.nlow_free
+        lo, hi = self.own_node
+        vel = (per * (lo - w["node_lo"]), per * (hi - w["node_lo"] + 1))
+        pre = (self.nvel_loc + self.nlow_vert * (self.V0 - w["vert_lo"]),
+               self.nvel_loc + self.nlow_vert * (self.V1 - w["vert_lo"]))
+        return [vel, pre]
+
+    def transfer_window(self) -> Dict:
+        """This rank's window with the row window narrowed to its OWNED layers: the
+        fine-grid argument of a windowed rav_gen_prolongation (rows = owned DoFs)."""
+        w = dict(self.window)
+        w["rnode_lo"], w["rnode_hi"] = self.own_node
+        w["rvert_lo"], w["rvert_hi"] = self.V0, self.V1 - 1
+        return w
 
 
 def exchange_info(slab: Slab, written_local: np.ndarray) -> Dict:
@@ -215,6 +234,142 @@ class DistSweeper:
             self.sweep(x, b, omega)
         return x
 
+    # vector consistency outside the sweep (transfers of the distributed V-cycle)
+    def halo(self, v):
+        """Owner values -> every ghost copy (the halo refresh of the sweep)."""
+        be = self.be
+        for q, idx in self.hs.items():
+            be.gather(v, idx, self.hs_buf[q])
+        self.comm.exchange(self.hs_buf, self.hr_buf)
+        self.phase_halo(v)
+
+    def accumulate_ghosts(self, v):
+        """Partial sums held at ghost copies -> added into the owner's entry (the
+        halo exchange reversed); the ghost entries are left stale."""
+        be = self.be
+        for q, idx in self.hr.items():
+            be.gather(v, idx, self.hr_buf[q])
+        self.comm.exchange(self.hr_buf, self.hs_buf)
+        for q, idx in self.hs.items():
+            be.scatter_add(self.hs_buf[q], idx, v)
+
+
+def nested_layers(fine_layers: Sequence[Tuple[int, int]]) -> List[Tuple[int, int]]:
+    """Slab partition of the next coarser level (vertex layer 2c of the fine grid
+    is vertex layer c of the coarse grid): interior cuts V -> ceil(V / 2).  With
+    it every owned fine row interpolates from DoFs inside the rank's coarse
+    window (checked by rav_gen_prolongation)."""
+    cuts = [0] + [(b + 1) // 2 for _, b in fine_layers[:-1]] + [(fine_layers[-1][1] - 1) // 2 + 1]
+    return [(cuts[r], cuts[r + 1]) for r in range(len(fine_layers))]
+
+
+def plan_levels(problem: Dict, n_levels: int, nranks: int, min_layers: int = 3,
+                agg_layers: int = 0) -> Tuple[List[Dict], List[List[Tuple[int, int]]]]:
+    """Problems of the hierarchy (finest first) and the slab partitions of the
+    levels that stay partitioned: level k (0 = finest) is partitioned while every
+    slab has >= max(min_layers, agg_layers) vertex layers; the levels below are
+    agglomerated (every rank holds them whole).  Returns (problems, partitions)
+    with len(partitions) = number of partitioned levels (>= 1)."""
+    probs = [problem]
+    for _ in range(n_levels - 1):
+        p = dict(probs[-1])
+        p["ncell"] = [c // 2 if k < problem["dim"] else c for k, c in enumerate(p["ncell"])]
+        probs.append(p)
+    n_last = problem["ncell"][problem["dim"] - 1]
+    parts = [partition_layers(n_last + 1, nranks, min_layers)]
+    need = max(min_layers, agg_layers)
+    while len(parts) < n_levels - 1:   # the coarsest level is never partitioned
+        nxt = nested_layers(parts[-1])
+        if min(b - a for a, b in nxt) < need:
+            break
+        parts.append(nxt)
+    return probs, parts
+
+
+class DistVCycle:
+    """Slab-partitioned V-cycle (SURVEY section 8 rows a9 / e).
+
+    levels[k], k = 0 (finest) .. K-1: per rank a DistSweeper over the rank's
+    window of level k.  xfers[k] (k < K-1): the rank's windowed prolongation
+    from level k+1 to level k (rows = owned DoFs of level k, columns = level
+    k+1's window).  agg: the prolongation from the agglomerated level (global
+    numbering, held whole by every rank) to level K-1 (rows = owned DoFs).
+    coarse: the agglomerated hierarchy below (every rank runs it redundantly on
+    the same all-reduced right-hand side).
+
+    Per cycle on a partitioned level: pre-smoothing (sweeps with their
+    interface sums and halo refresh), residual on the local rows,
+    b_c = P_own^T r (partial sums of the rank's owned fine rows), partial sums
+    at coarse ghosts -> owners (accumulate_ghosts) and a coarse halo refresh, the
+    coarse cycle from x_c = 0, x += P_own x_c on owned rows, a fine halo
+    refresh, post-smoothing.  At the agglomeration level the coarse right-hand
+    side is all-reduced instead.  ||r||^2 over owned DoFs, all-reduced, for the
+    stopping test (R11).
+
+    backend (per level, see DistSweeper) additionally provides
+      restrict(xfer, r, bc), prolong(xfer, xc, x), zero(v),
+      dot_owned(r, ranges) -> partial ||r||^2 as a backend scalar buffer,
+      coarse_vcycle(xc, bc, pre, post, omega), buffer(n)
+    comm additionally: allreduce_sum(buf) (in place, identical on every rank)."""
+
+    def __init__(self, levels: Sequence[Dict], xfers: Sequence, agg, comm, n_coarse: int):
+        self.levels, self.xfers, self.agg, self.comm = list(levels), list(xfers), agg, comm
+        for lv in self.levels:
+            be = lv["be"]
+            lv.setdefault("r", be.buffer(lv["slab"].n_loc))
+        self.bc = self.levels[-1]["be"].buffer(n_coarse)
+        self.xc = self.levels[-1]["be"].buffer(n_coarse)
+
+    def _cycle(self, k: int, x, b, pre: int, post: int, omega: float):
+        lv = self.levels[k]
+        be, sw = lv["be"], lv["sweeper"]
+        sw.smooth(x, b, pre, omega)
+        be.residual(x, b, lv["r"])
+        if k + 1 < len(self.levels):
+            c = self.levels[k + 1]
+            cbe = c["be"]
+            be.restrict(self.xfers[k], lv["r"], c["b"])
+            c["sweeper"].accumulate_ghosts(c["b"])
+            c["sweeper"].halo(c["b"])
+            cbe.zero(c["x"])
+            self._cycle(k + 1, c["x"], c["b"], pre, post, omega)
+            be.prolong(self.xfers[k], c["x"], x)
+        else:
+            be.restrict(self.agg, lv["r"], self.bc)
+            self.comm.allreduce_sum(self.bc)
+            be.zero(self.xc)
+            be.coarse_vcycle(self.xc, self.bc, pre, post, omega)
+            be.prolong(self.agg, self.xc, x)
+        sw.halo(x)
+        sw.smooth(x, b, post, omega)
+
+    def vcycle(self, x, b, pre: int = 2, post: int = 2, omega: float = 0.66):
+        self._cycle(0, x, b, pre, post, omega)
+        return x
+
+    def residual_norm(self, x, b) -> float:
+        lv = self.levels[0]
+        be = lv["be"]
+        be.residual(x, b, lv["r"])
+        s = be.dot_owned(lv["r"], lv["slab"].owned_ranges())
+        self.comm.allreduce_sum(s)
+        return float(s.cpu()[0]) ** 0.5 if hasattr(s, "cpu") else float(s[0]) ** 0.5
+
+    def solve(self, x, b, pre: int = 2, post: int = 2, omega: float = 0.66, rtol: float = 1e-8,
+              maxit: int = 200):
+        """V-cycles until ||b - L x_k|| <= rtol ||b - L x_0|| (R11).  Returns (x, k, hist)."""
+        hist = [self.residual_norm(x, b)]
+        k = 0
+        while hist[0] > 0 and k < maxit:
+            self.vcycle(x, b, pre, post, omega)
+            k += 1
+            hist.append(self.residual_norm(x, b))
+            if not np.isfinite(hist[-1]):
+                raise FloatingPointError(f"distributed V-cycle diverged at cycle {k}")
+            if hist[-1] <= rtol * hist[0]:
+                break
+        return x, k, np.array(hist)
+
 
 class TorchComm:
     """torch.distributed plumbing (NCCL on GPUs, gloo on CPU)."""
@@ -229,6 +384,9 @@ class TorchComm:
         self.dist.all_gather_object(out, obj, group=self.group)
         return out
 
+    def allreduce_sum(self, buf):
+        self.dist.all_reduce(buf, op=self.dist.ReduceOp.SUM, group=self.group)
+
     def exchange(self, sends: Dict, recvs: Dict):
         dist = self.dist
         ops = [dist.P2POp(dist.isend, buf, q, group=self.group) for q, buf in sorted(sends.items())]
@@ -238,13 +396,88 @@ class TorchComm:
                 req.wait()
 
 
+class ThreadComm:
+    """In-process transport for R ranks run as threads of one process (the GPU
+    tests emulate ranks on the single available GPU this way; the CPU tests use
+    it for quick checks).  Each rank holds its own ThreadComm(hub, rank); every
+    collective is a host-side rendezvous (no kernel ever waits on another rank),
+    received data are copied after the sender's work is complete."""
+
+    class Hub:
+        def __init__(self, nranks: int):
+            import threading
+            self.n = nranks
+            self.barrier = threading.Barrier(nranks)
+            self.box: Dict = {}
+
+    def __init__(self, hub: "ThreadComm.Hub", rank: int, sync=None):
+        self.hub, self.rank = hub, rank
+        self.sync = sync or (lambda: None)   # e.g. torch.cuda.current_stream().synchronize
+
+    def all_gather_object(self, obj):
+        h = self.hub
+        h.box[("obj", self.rank)] = obj
+        h.barrier.wait()
+        out = [h.box[("obj", r)] for r in range(h.n)]
+        h.barrier.wait()
+        return out
+
+    def exchange(self, sends: Dict, recvs: Dict):
+        h = self.hub
+        self.sync()
+        for q, buf in sends.items():
+            h.box[("p2p", self.rank, q)] = buf
+        h.barrier.wait()
+        for q, buf in recvs.items():
+            buf.copy_(h.box[("p2p", q, self.rank)])
+        self.sync()
+        h.barrier.wait()
+        for q in sends:
+            del h.box[("p2p", self.rank, q)]
+
+    def allreduce_sum(self, buf):
+        h = self.hub
+        self.sync()
+        h.box[("ar", self.rank)] = buf.clone()
+        h.barrier.wait()
+        acc = h.box[("ar", 0)].clone()
+        for r in range(1, h.n):       # rank order: identical bits on every rank
+            acc += h.box[("ar", r)]
+        h.barrier.wait()
+        buf.copy_(acc)
+        self.sync()
+
+
+def run_threads(nranks: int, fn):
+    """fn(rank) on nranks threads; re-raises the first failure."""
+    import threading
+    out, err = [None] * nranks, []
+
+    def body(r):
+        try:
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+            raise
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if err:
+        raise err[0]
+    return out
+
+
 class GpuBackend:
     """Compute steps through the C-ABI (paper_2103_10127_b200.ravgmg)."""
 
-    def __init__(self, smoother, stream=None):
+    def __init__(self, smoother, stream=None, coarse=None):
         import torch
         from . import ravgmg as rg
         self.torch, self.rg, self.sm, self.stream = torch, rg, smoother, stream
+        self.coarse = coarse     # ravgmg.Multigrid of the agglomerated levels (last partitioned level)
 
     def residual(self, x, b, r):
         self.sm.residual(x, b, r)
@@ -264,6 +497,24 @@ class GpuBackend:
     def fill(self, dst, idx, value):
         self.rg.index_op(3, None, idx, dst, value=value, stream=self.stream)
 
+    def restrict(self, xfer, r, bc):
+        xfer.restrict(r, bc)
+
+    def prolong(self, xfer, xc, x):
+        xfer.prolong(xc, x)
+
+    def zero(self, v):
+        v.zero_()
+
+    def dot_owned(self, r, ranges):
+        out = self.torch.zeros(1, dtype=self.torch.float64, device="cuda")
+        for k, (a, b) in enumerate(ranges):
+            self.rg.dot(r[a:b], r[a:b], out, accumulate=k > 0, stream=self.stream)
+        return out
+
+    def coarse_vcycle(self, xc, bc, pre, post, omega):
+        self.coarse.vcycle(xc, bc, pre, post, omega)
+
     def index(self, a):
         return self.torch.tensor(np.asarray(a, dtype=np.int32), device="cuda")
 
@@ -276,3 +527,40 @@ def written_local_from_patches(P: Dict) -> np.ndarray:
     dofs = np.asarray(P["dofs"].cpu() if hasattr(P["dofs"], "cpu") else P["dofs"])
     w = np.asarray(P["w"].cpu() if hasattr(P["w"], "cpu") else P["w"])
     return np.unique(dofs[w > 0]).astype(np.int64)
+
+
+def build_gpu_cycle(problem: Dict, n_levels: int, nranks: int, rank: int, comm, weights: str = "pou",
+                    agg_layers: int = 0, kernel: int = 0) -> Tuple["DistVCycle", List[Dict]]:
+    """One rank's share of the slab-partitioned V-cycle on its GPU: every
+    partitioned level generated directly in the rank's window (rav_gen_*, win =
+    1), its smoother (rav_setup), windowed transfers (rav_gen_prolongation +
+    rav_xfer_setup) and the agglomerated coarse hierarchy (mg_setup on the whole
+    coarse grids, identical on every rank).  Returns (cycle, levels); levels[0]
+    holds the rank's fine-level rhs "b" and a zero iterate "x"."""
+    import torch
+    from . import ravgmg as rg
+    probs, parts = plan_levels(problem, n_levels, nranks, agg_layers=agg_layers)
+    K = len(parts)
+    coarse_mg, coarse_fine = rg.build_hierarchy(probs[K], n_levels - K, weights, kernel=kernel)
+    slabs = [Slab(probs[k], nranks, rank, parts[k]) for k in range(K)]
+    levels, xfers = [], []
+    for k in range(K):
+        L = rg.gen_level(slabs[k].local_problem(), weights)
+        sm = rg.Smoother(L, L, kernel=kernel)
+        be = GpuBackend(sm, coarse=coarse_mg if k == K - 1 else None)
+        sw = DistSweeper(slabs[k], be, comm, written_local_from_patches(L))
+        n = slabs[k].n_loc
+        levels.append({"slab": slabs[k], "be": be, "sweeper": sw, "smoother": sm,
+                       "b": L["b"] if k == 0 else torch.zeros(n, dtype=torch.float64, device="cuda"),
+                       "x": torch.zeros(n, dtype=torch.float64, device="cuda")})
+        del L
+    for k in range(K - 1):
+        fine = dict(probs[k], window=slabs[k].transfer_window())
+        coarse = dict(probs[k + 1], window=dict(slabs[k + 1].window))
+        xfers.append(rg.Transfer(rg.gen_prolongation(fine, coarse)))
+    fine = dict(probs[K - 1], window=slabs[K - 1].transfer_window())
+    agg = rg.Transfer(rg.gen_prolongation(fine, probs[K]))
+    cyc = DistVCycle(levels, xfers, agg, comm, coarse_fine["n"])
+    cyc.coarse_mg = coarse_mg
+    torch.cuda.empty_cache()
+    return cyc, levels

@@ -90,6 +90,11 @@ def _load():
         "mg_vcycle": [vp, vp, vp, C.c_int, C.c_int, dbl],
         "mg_solve": [vp, vp, vp, C.c_int, C.c_int, dbl, dbl, C.c_int, P(C.c_int), vp],
         "mg_set_stream": [vp, vp],
+        "rav_xfer_setup": [P(RavCsr), vp, P(vp)],
+        "rav_prolong": [vp, vp, vp, dbl],
+        "rav_restrict": [vp, vp, vp],
+        "rav_xfer_set_stream": [vp, vp],
+        "rav_dot": [vp, vp, i64, vp, C.c_int, vp],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -99,6 +104,8 @@ def _load():
     L.rav_destroy.restype = None
     L.mg_destroy.argtypes = [vp]
     L.mg_destroy.restype = None
+    L.rav_xfer_destroy.argtypes = [vp]
+    L.rav_xfer_destroy.restype = None
     L.rav_kernel_name.argtypes = [vp]
     L.rav_kernel_name.restype = C.c_char_p
     L.rav_last_error.restype = C.c_char_p
@@ -346,6 +353,46 @@ class Multigrid:
             self.close()
         except Exception:
             pass
+
+
+class Transfer:
+    """rav_xfer_setup / rav_prolong / rav_restrict: xf += alpha P xc, bc = P^T rf."""
+
+    def __init__(self, Pm: Dict, stream=None):
+        self._keep = Pm
+        ctx = C.c_void_p()
+        _check(lib.rav_xfer_setup(C.byref(csr(Pm, n_cols=Pm["nc"])), _stream(stream), C.byref(ctx)))
+        self.ctx = ctx
+        self.n, self.nc = Pm["n"], Pm["nc"]
+
+    def prolong(self, xc, xf, alpha: float = 1.0):
+        _check(lib.rav_prolong(self.ctx, _ptr(xc), _ptr(xf), float(alpha)))
+        return xf
+
+    def restrict(self, rf, bc):
+        _check(lib.rav_restrict(self.ctx, _ptr(rf), _ptr(bc)))
+        return bc
+
+    def set_stream(self, stream):
+        _check(lib.rav_xfer_set_stream(self.ctx, _stream(stream)))
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib.rav_xfer_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dot(a, b, out, accumulate: bool = False, n: Optional[int] = None, stream=None):
+    """rav_dot: out[0] (device) = sum a[i] b[i] (+ out[0] if accumulate)."""
+    n = a.numel() if n is None else int(n)
+    _check(lib.rav_dot(_ptr(a), _ptr(b), n, _ptr(out), int(bool(accumulate)), _stream(stream)))
+    return out
 
 
 def index_op(op: int, src, idx, dst, value: float = 0.0, stream=None):

@@ -61,10 +61,10 @@ class NumpyBackend:
         self.written = np.unique(np.concatenate([ld[:k] for ld, k, _ in self.patches]))
 
     def residual(self, x, b, r):
-        xv, rv = x.numpy(), r.numpy()
+        xv, rv, bv = x.numpy(), r.numpy(), b.numpy()
         for i in range(len(self.rp) - 1):
             s, e = self.rp[i], self.rp[i + 1]
-            rv[i] = self.b[i] - np.dot(self.val[s:e], xv[self.ci[s:e]])
+            rv[i] = bv[i] - np.dot(self.val[s:e], xv[self.ci[s:e]])
 
     def apply(self, r, x, omega):
         rv, xv = r.numpy(), x.numpy()
@@ -178,3 +178,143 @@ def test_partition_and_windows():
         assert owned == nglob
     with pytest.raises(ValueError):
         rdist.partition_layers(10, 4)
+
+
+# ---------------------------------------------------------------------------------------------
+# distributed V-cycle (SURVEY section 8 rows a9 / e): slab-partitioned levels with
+# windowed transfers, agglomerated coarse levels, all-reduced coarse rhs and residual norms
+# ---------------------------------------------------------------------------------------------
+
+def window_prolongation(Pg, fine_slab, coarse_slab=None):
+    """Rows = the fine slab's OWNED local DoFs (others empty); columns = the coarse
+    slab's local DoFs (global ids when coarse_slab is None), cut from the oracle's
+    global P."""
+    fg = fine_slab.global_ids()
+    own = fine_slab.owned_mask()
+    if coarse_slab is not None:
+        c2l = -np.ones(Pg["nc"], np.int64)
+        c2l[coarse_slab.global_ids()] = np.arange(coarse_slab.n_loc)
+        nc = coarse_slab.n_loc
+    else:
+        c2l = np.arange(Pg["nc"])
+        nc = Pg["nc"]
+    rows, cols, vals = [], [], []
+    for l, g in enumerate(fg):
+        if not own[l]:
+            continue
+        s, e = Pg["rp"][g], Pg["rp"][g + 1]
+        c = c2l[Pg["ci"][s:e]]
+        assert np.all(c >= 0), "owned fine row interpolates from outside the coarse window"
+        rows += [l] * (e - s)
+        cols += list(c)
+        vals += list(Pg["val"][s:e])
+    import scipy.sparse as sp
+    return sp.csr_matrix((vals, (rows, cols)), shape=(fine_slab.n_loc, nc))
+
+
+class NumpyCycleBackend(NumpyBackend):
+    def __init__(self, slab, O, P, F, coarse=None):
+        super().__init__(slab, O, P, F, None)
+        self.coarse = coarse
+
+    def restrict(self, T, r, bc):
+        bc.numpy()[:] = T.T @ r.numpy()
+
+    def prolong(self, T, xc, x):
+        x.numpy()[:] += T @ xc.numpy()
+
+    def zero(self, v):
+        v.zero_()
+
+    def dot_owned(self, r, ranges):
+        rv = r.numpy()
+        return torch.tensor([sum(float(np.dot(rv[a:b], rv[a:b])) for a, b in ranges)], dtype=torch.float64)
+
+    def coarse_vcycle(self, xc, bc, pre, post, omega):
+        xc.numpy()[:] = self.coarse.vcycle(np.zeros(len(bc)), bc.numpy(), pre, post, omega)
+
+
+def build_dist_cycle(prob, n_levels, world, rank, comm, agg_layers=0):
+    probs, parts = rdist.plan_levels(prob, n_levels, world, agg_layers=agg_layers)
+    K = len(parts)
+    coarse = oracle.Hierarchy(probs[K], n_levels - K)
+    slabs = [rdist.Slab(probs[k], world, rank, parts[k]) for k in range(K)]
+    levels, xfers = [], []
+    for k in range(K):
+        O = oracle.assemble(probs[k])
+        P = oracle.patches(probs[k], "pou")
+        F = oracle.factor(O, P, oracle.FMT_ROWS)
+        be = NumpyCycleBackend(slabs[k], O, P, F, coarse if k == K - 1 else None)
+        sw = rdist.DistSweeper(slabs[k], be, comm, be.written)
+        n = slabs[k].n_loc
+        levels.append({"slab": slabs[k], "be": be, "sweeper": sw,
+                       "b": torch.tensor(be.b) if k == 0 else torch.zeros(n, dtype=torch.float64),
+                       "x": torch.zeros(n, dtype=torch.float64)})
+        if k + 1 < K:
+            xfers.append(window_prolongation(oracle.prolongation(probs[k], probs[k + 1]), slabs[k], slabs[k + 1]))
+    agg = window_prolongation(oracle.prolongation(probs[K - 1], probs[K]), slabs[K - 1], None)
+    cyc = rdist.DistVCycle(levels, xfers, agg, comm, coarse.fine["n"])
+    return cyc, levels, K
+
+
+def _cycle_worker(rank, world, port, prob, n_levels, agg_layers, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cyc, levels, K = build_dist_cycle(prob, n_levels, world, rank, rdist.TorchComm(), agg_layers)
+        slab = levels[0]["slab"]
+        x = torch.zeros(slab.n_loc, dtype=torch.float64)
+        _, k, hist = cyc.solve(x, levels[0]["b"], rtol=1e-10, omega=0.66, maxit=60)
+        own = slab.owned_mask()
+        out_q.put((rank, slab.global_ids()[own], x.numpy()[own].copy(), k, hist, K))
+    finally:
+        dist.destroy_process_group()
+
+
+CYCLE_CASES = [
+    (si.problem(2, (16, 24), si.KIND_MMS, eta="fourier"), 4, 2, 0),
+    (si.problem(2, (24, 24), si.KIND_CAVITY, eta="fourier"), 4, 3, 0),
+    (si.problem(2, (16, 32), si.KIND_MMS, eta="fourier", box=[1.0, 2.0]), 4, 2, 8),
+    (si.problem(3, (4, 4, 8), si.KIND_CAVITY, eta="fourier", box=[1.0, 1.0, 2.0]), 2, 2, 0),
+]
+
+
+@pytest.mark.parametrize("case", CYCLE_CASES, ids=["2d-mms-w2", "2d-cavity-w3", "2d-agg8-w2", "3d-cavity-w2"])
+def test_distributed_vcycle_matches_single_domain_oracle(case):
+    prob, n_levels, world, agg = case
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cycle_worker, args=(r, world, port, prob, n_levels, agg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    H = oracle.Hierarchy(prob, n_levels)
+    xo, ko, ho = H.solve(rtol=1e-10, omega=0.66, maxit=60)
+    assert ko < 60, "the reference solve must converge"
+    xd = np.full(H.fine["n"], np.nan)
+    for _, g, v, k, hist, K in res:
+        assert k == ko, f"distributed cycles {k} != oracle {ko}"
+        assert K >= 1
+        np.testing.assert_allclose(hist, ho, rtol=1e-9, atol=1e-13 * ho[0])   # rounding floor ~ eps ||b||
+        xd[g] = v
+    assert not np.isnan(xd).any()
+    assert np.linalg.norm(xd - xo) <= 1e-10 * np.linalg.norm(xo)
+
+
+def test_level_plan_nesting():
+    prob = si.problem(2, (64, 256), si.KIND_MMS)
+    probs, parts = rdist.plan_levels(prob, 7, 4)
+    assert [p["ncell"][1] for p in probs] == [256, 128, 64, 32, 16, 8, 4]
+    for k, part in enumerate(parts):
+        n = probs[k]["ncell"][1]
+        assert part[0][0] == 0 and part[-1][1] == n + 1
+        assert all(b - a >= 3 for a, b in part)
+        assert all(part[r][1] == part[r + 1][0] for r in range(3))
+    assert len(parts) == 5      # 257, 129, 65, 33, 17 layers over 4 ranks; 9 layers -> < 3 per rank
+    _, parts8 = rdist.plan_levels(prob, 7, 4, agg_layers=8)
+    assert len(parts8) == 4
