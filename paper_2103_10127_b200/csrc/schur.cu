@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
 // ------------------------------------------------------------------------------------
 
 // one patch per thread (2D): MT restricted nodes, D components, NN nodes per patch (runtime)
-template <int MT, int D, int MINB>
+template <int MT, int D, int MINB, int NRB = 0>   // NRB > 0: compile-time number of rectangular column pairs
 __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
                                                                  const double2* __restrict__ W,
                                                                  const int32_t* __restrict__ ND,
@@ -468,7 +468,11 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
     }
     // rectangular columns, two at a time (2 * RC entries = RC pairs)
     const double2* wq0 = wp + (TRI_PAD / 2) * 32;
-    for (int j0 = MT; j0 < NN; j0 += 2) {
+    const int nrb = NRB > 0 ? NRB : (NN - MT) / 2;
+#pragma unroll
+    for (int b = 0; b < (NRB > 0 ? NRB : 1 << 20); ++b) {
+        if (NRB == 0 && b >= nrb) break;
+        const int j0 = MT + 2 * b;
         const int blk = (j0 - MT) / 2 + PF_AHEAD;
         if (pf && lane == 0 && blk < nblocks)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rect0 + (size_t)blk * RB), "r"(RB)
@@ -998,6 +1002,25 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
         const char* e = getenv("RAV_SCHUR_PF");   // L2 bulk prefetch: measured slower (127 vs 124 us), off
         return e ? atoi(e) : 0;
     }();
+    static const int nrb_env = [] {
+        const char* e = getenv("RAV_SCHUR_NRB");   // 0: runtime rectangular loop
+        return e ? atoi(e) : 1;
+    }();
+    if (nrb_env && MT == 9 && F.NN == 25) {
+        if (minb == 5)
+            schur_sweep_thread_kernel<MT, 2, 5, 8><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
+                                                                          reinterpret_cast<const double2*>(F.facT), F.DT,
+                                                                          F.PD, F.NR, F.WT, r, x, omega, pf);
+        else if (minb == 3)
+            schur_sweep_thread_kernel<MT, 2, 3, 8><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
+                                                                          reinterpret_cast<const double2*>(F.facT), F.DT,
+                                                                          F.PD, F.NR, F.WT, r, x, omega, pf);
+        else
+            schur_sweep_thread_kernel<MT, 2, 4, 8><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
+                                                                          reinterpret_cast<const double2*>(F.facT), F.DT,
+                                                                          F.PD, F.NR, F.WT, r, x, omega, pf);
+        return;
+    }
     if (minb >= 6)
         schur_sweep_thread_kernel<MT, 2, 6><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
                                                                    reinterpret_cast<const double2*>(F.facT), F.DT,
