@@ -60,7 +60,8 @@ class Desc(C.Structure):
     _fields_ = [("dim", C.c_int32), ("ncell", C.c_int32 * 3), ("len", C.c_double * 3),
                 ("kind", C.c_int32), ("eta_mode", C.c_int32), ("eta0", C.c_double),
                 ("n_modes", C.c_int32), ("amp", C.c_double * 8), ("mode", (C.c_int32 * 3) * 8),
-                ("phase", (C.c_double * 3) * 8), ("gmin", C.c_double), ("gmax", C.c_double)]
+                ("phase", (C.c_double * 3) * 8), ("gmin", C.c_double), ("gmax", C.c_double),
+                ("vel_order", C.c_int32), ("beta", C.c_double)]
 
 
 class Level(C.Structure):
@@ -150,6 +151,8 @@ def desc(problem: Dict) -> Desc:
             d.phase[m][k] = float(problem["phase"][m][k])
     d.gmin = problem["gmin"]
     d.gmax = problem["gmax"]
+    d.vel_order = int(problem.get("vel_order", 2))   # 2 Taylor-Hood Q2-Q1 (R1), 1 stabilized Q1-Q1 (R18)
+    d.beta = float(problem.get("beta", 0.0))
     if problem["dim"] == 3 and problem["kind"] == 1:
         raise ValueError("manufactured solution is 2D only (R13)")
     return d

@@ -12,7 +12,8 @@
  * follows.  Citation convention: "P:n" = PAPER.md line n, "S:n" = SPEC.md line n,
  * "R<k>" = the reading k listed in DESIGN.md / SURVEY.md section 8.
  *
- *   assembly        P:66-74 Eqs. 5-7 (Taylor-Hood Q2-Q1, C = 0: R1), Dirichlet
+ *   assembly        P:66-74 Eqs. 5-7 (Taylor-Hood Q2-Q1, C = 0: R1; or the paper's
+ *                   stabilized Q1-Q1 with C of P:78 Eq. 8: R18), Dirichlet
  *                   condensation S:207 (R8), 3-point Gauss per axis (R7)
  *   patches         P:108 (structural Bt-row support, R2), P:122 (restricted
  *                   prolongation; partition-of-unity weights R3)
@@ -48,6 +49,8 @@ typedef struct {
     int32_t mode[OR_MAXMODES][3];
     double  phase[OR_MAXMODES][3];
     double  gmin, gmax;
+    int32_t vel_order;     /* 2 (or 0): Taylor-Hood Q2-Q1 (R1); 1: stabilized Q1-Q1 (R18) */
+    double  beta;          /* Q1-Q1 stabilization constant beta_0 of R18 */
 } or_desc;
 
 /* ------------------------------------------------------------------------- */
@@ -58,10 +61,12 @@ typedef struct {
 /* ------------------------------------------------------------------------- */
 
 static int axes(const or_desc* D) { return D->dim; }
+/* velocity lattice refinement P: velocity nodes on the (P n + 1)^d lattice, vertices = nodes P a */
+static int vorder(const or_desc* D) { return D->vel_order == 1 ? 1 : 2; }
 
 int64_t or_n_free_nodes(const or_desc* D) {
     int64_t m = 1;
-    for (int k = 0; k < axes(D); ++k) m *= (int64_t)(2 * D->ncell[k] - 1);
+    for (int k = 0; k < axes(D); ++k) m *= (int64_t)(vorder(D) * D->ncell[k] - 1);
     return m;
 }
 
@@ -78,7 +83,7 @@ int64_t or_n_dofs(const or_desc* D) { return or_n_velocity(D) + or_n_vertices(D)
 static int64_t free_node(const or_desc* D, const int* a) {
     int64_t idx = 0, stride = 1;
     for (int k = 0; k < axes(D); ++k) {
-        int m = 2 * D->ncell[k];
+        int m = vorder(D) * D->ncell[k];
         if (a[k] <= 0 || a[k] >= m) return -1;
         idx += (int64_t)(a[k] - 1) * stride;
         stride *= (int64_t)(m - 1);
@@ -103,9 +108,9 @@ static int64_t pdof(const or_desc* D, const int* v) { return or_n_velocity(D) + 
 static double dirichlet_value(const or_desc* D, const int* a, int c) {
     if (D->kind != 0 || c != 0) return 0.0;
     int top = D->dim - 1;
-    if (a[top] != 2 * D->ncell[top]) return 0.0;
+    if (a[top] != vorder(D) * D->ncell[top]) return 0.0;
     for (int k = 0; k < top; ++k)
-        if (a[k] <= 0 || a[k] >= 2 * D->ncell[k]) return 0.0;
+        if (a[k] <= 0 || a[k] >= vorder(D) * D->ncell[k]) return 0.0;
     return 1.0;
 }
 
@@ -187,32 +192,45 @@ static double dq2(int i, double t) {
     return 4.0 * t - 1.0;
 }
 static double q1(int i, double t) { return i == 0 ? 1.0 - t : t; }
+static double dq1(int i, double t) { (void)t; return i == 0 ? -1.0 : 1.0; }
+/* velocity basis of order P (2: Q2, 1: Q1) */
+static double vb(int P, int i, double t) { return P == 2 ? q2(i, t) : q1(i, t); }
+static double dvb(int P, int i, double t) { return P == 2 ? dq2(i, t) : dq1(i, t); }
 
 static const double GAUSS3_T[3] = {0.5 - 0.5 * 0.77459666924148337704, 0.5,
                                    0.5 + 0.5 * 0.77459666924148337704};
 static const double GAUSS3_W[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
+/* 2-point Gauss rule on [0,1] for Q1-Q1 ("2x2 Gauss", R18) */
+static const double GAUSS2_T[2] = {0.5 - 0.5 * 0.57735026918962576451, 0.5 + 0.5 * 0.57735026918962576451};
+static const double GAUSS2_W[2] = {0.5, 0.5};
 
 static int ipow(int b, int e) { int r = 1; while (e-- > 0) r *= b; return r; }
 
-/* Element matrices of element e (Eq. 7):
+/* Element matrices of element e (Eq. 7, Eq. 8):
  *   Ae[a][b]     = int eta grad(phi_a) . grad(phi_b)          (per velocity component)
  *   Be[a][c][m]  = - int psi_m d_c phi_a                       (B := -(div v, p))
+ *   Ce[m][m']    = - beta_0 h_e^2 int (1/eta) grad psi_m . grad psi_m'   (Q1-Q1 only, R18;
+ *                  h_e = element diameter; Eq. 8 read on the pressure basis)
  *   Fe[a][c]     = int f_c phi_a
- * a, b: local Q2 nodes (3^d), m: local vertices (2^d). */
-static void element_matrices(const or_desc* D, const int* e, double* Ae, double* Be, double* Fe) {
-    const int d = D->dim, NQ = ipow(3, d), NV = ipow(2, d), NG = ipow(3, d);
-    double h[3];
-    for (int k = 0; k < d; ++k) h[k] = D->len[k] / D->ncell[k];
+ * a, b: local velocity nodes ((P+1)^d), m: local vertices (2^d).  Gauss rule with
+ * P+1 points per axis (R7 / R18). */
+static void element_matrices(const or_desc* D, const int* e, double* Ae, double* Be, double* Ce, double* Fe) {
+    const int d = D->dim, P = vorder(D), NQ = ipow(P + 1, d), NV = ipow(2, d), NP1 = P + 1, NG = ipow(NP1, d);
+    const double* GT = P == 2 ? GAUSS3_T : GAUSS2_T;
+    const double* GW = P == 2 ? GAUSS3_W : GAUSS2_W;
+    double h[3], h2 = 0.0;
+    for (int k = 0; k < d; ++k) { h[k] = D->len[k] / D->ncell[k]; h2 += h[k] * h[k]; }
     memset(Ae, 0, sizeof(double) * NQ * NQ);
     memset(Be, 0, sizeof(double) * NQ * 3 * NV);
+    memset(Ce, 0, sizeof(double) * NV * NV);
     memset(Fe, 0, sizeof(double) * NQ * 3);
-    double phi[27], grad[27][3], psi[8];
+    double phi[27], grad[27][3], psi[8], gpsi[8][3];
     for (int q = 0; q < NG; ++q) {
         double t[3], x[3], w = 1.0;
         for (int k = 0; k < d; ++k) {
-            int qk = (q / ipow(3, k)) % 3;
-            t[k] = GAUSS3_T[qk];
-            w *= GAUSS3_W[qk] * h[k];
+            int qk = (q / ipow(NP1, k)) % NP1;
+            t[k] = GT[qk];
+            w *= GW[qk] * h[k];
             x[k] = (e[k] + t[k]) * h[k];
         }
         double eta, ge[3], f[3];
@@ -220,13 +238,13 @@ static void element_matrices(const or_desc* D, const int* e, double* Ae, double*
         forcing(D, x, f);
         for (int a = 0; a < NQ; ++a) {
             int ak[3];
-            for (int k = 0; k < d; ++k) ak[k] = (a / ipow(3, k)) % 3;
+            for (int k = 0; k < d; ++k) ak[k] = (a / ipow(NP1, k)) % NP1;
             double v = 1.0;
-            for (int k = 0; k < d; ++k) v *= q2(ak[k], t[k]);
+            for (int k = 0; k < d; ++k) v *= vb(P, ak[k], t[k]);
             phi[a] = v;
             for (int k = 0; k < d; ++k) {
-                double g = dq2(ak[k], t[k]) / h[k];
-                for (int j = 0; j < d; ++j) if (j != k) g *= q2(ak[j], t[j]);
+                double g = dvb(P, ak[k], t[k]) / h[k];
+                for (int j = 0; j < d; ++j) if (j != k) g *= vb(P, ak[j], t[j]);
                 grad[a][k] = g;
             }
         }
@@ -234,6 +252,11 @@ static void element_matrices(const or_desc* D, const int* e, double* Ae, double*
             double v = 1.0;
             for (int k = 0; k < d; ++k) v *= q1((m >> k) & 1, t[k]);
             psi[m] = v;
+            for (int k = 0; k < d; ++k) {
+                double g = dq1((m >> k) & 1, t[k]) / h[k];
+                for (int j = 0; j < d; ++j) if (j != k) g *= q1((m >> j) & 1, t[j]);
+                gpsi[m][k] = g;
+            }
         }
         for (int a = 0; a < NQ; ++a) {
             for (int b = a; b < NQ; ++b) {
@@ -246,9 +269,18 @@ static void element_matrices(const or_desc* D, const int* e, double* Ae, double*
                 Fe[a * 3 + c] += w * f[c] * phi[a];
             }
         }
+        if (P == 1)
+            for (int m = 0; m < NV; ++m)
+                for (int m2 = m; m2 < NV; ++m2) {
+                    double dot = 0.0;
+                    for (int k = 0; k < d; ++k) dot += gpsi[m][k] * gpsi[m2][k];
+                    Ce[m * NV + m2] -= D->beta * h2 * (w / eta) * dot;
+                }
     }
     for (int a = 0; a < NQ; ++a)
         for (int b = 0; b < a; ++b) Ae[a * NQ + b] = Ae[b * NQ + a]; /* symmetric by definition */
+    for (int m = 0; m < NV; ++m)
+        for (int m2 = 0; m2 < m; ++m2) Ce[m * NV + m2] = Ce[m2 * NV + m];
 }
 
 /* ------------------------------------------------------------------------- */
@@ -274,9 +306,10 @@ static int64_t csr_find(const int64_t* rp, const int32_t* ci, int64_t row, int64
  * Structural (R2): entries are kept even when they evaluate to zero.
  * For a velocity row (node a, component c): same-component velocity DoFs and
  * pressure DoFs of all elements containing a.  For a pressure row (vertex v):
- * all velocity DoFs of all elements containing v.  C = 0 => no p-p entries. */
+ * all velocity DoFs of all elements containing v, plus (Q1-Q1, C != 0) the
+ * pressure DoFs of those elements.  Taylor-Hood: C = 0 => no p-p entries. */
 static int64_t row_pattern(const or_desc* D, int64_t row, int64_t* out) {
-    const int d = D->dim;
+    const int d = D->dim, P = vorder(D);
     const int64_t nu = or_n_velocity(D);
     int node[3] = {0, 0, 0}, is_vel = row < nu, comp = 0;
     int elo[3] = {0, 0, 0}, ehi[3] = {0, 0, 0};
@@ -284,13 +317,14 @@ static int64_t row_pattern(const or_desc* D, int64_t row, int64_t* out) {
         int64_t fi = row / d;
         comp = (int)(row % d);
         for (int k = 0; k < d; ++k) {
-            int m = 2 * D->ncell[k] - 1;
+            int m = P * D->ncell[k] - 1;
             node[k] = (int)(fi % m) + 1;
             fi /= m;
         }
         for (int k = 0; k < d; ++k) {
             /* elements along axis k containing lattice index node[k] */
-            if (node[k] % 2 == 0) { elo[k] = node[k] / 2 - 1; ehi[k] = node[k] / 2; }
+            if (P == 1) { elo[k] = node[k] - 1; ehi[k] = node[k]; }
+            else if (node[k] % 2 == 0) { elo[k] = node[k] / 2 - 1; ehi[k] = node[k] / 2; }
             else { elo[k] = ehi[k] = (node[k] - 1) / 2; }
             if (elo[k] < 0) elo[k] = 0;
             if (ehi[k] > D->ncell[k] - 1) ehi[k] = D->ncell[k] - 1;
@@ -305,9 +339,9 @@ static int64_t row_pattern(const or_desc* D, int64_t row, int64_t* out) {
         }
     }
     int64_t cnt = 0;
-    /* nodes of the union of those elements: lattice box [2 elo, 2 ehi + 2] */
+    /* nodes of the union of those elements: lattice box [P elo, P ehi + P] */
     int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    for (int k = 0; k < d; ++k) { lo[k] = 2 * elo[k]; hi[k] = 2 * ehi[k] + 2; }
+    for (int k = 0; k < d; ++k) { lo[k] = P * elo[k]; hi[k] = P * ehi[k] + P; }
     int b[3] = {0, 0, 0};
     int tot = 1;
     for (int k = 0; k < d; ++k) tot *= (hi[k] - lo[k] + 1);
@@ -319,7 +353,7 @@ static int64_t row_pattern(const or_desc* D, int64_t row, int64_t* out) {
         if (is_vel) out[cnt++] = fb * d + comp;
         else for (int c = 0; c < d; ++c) out[cnt++] = fb * d + c;
     }
-    if (is_vel) {
+    if (is_vel || P == 1) {   /* B entries of a velocity row; C entries of a Q1-Q1 pressure row */
         int vt = 1;
         for (int k = 0; k < d; ++k) vt *= (ehi[k] - elo[k] + 2);
         for (int t = 0; t < vt; ++t) {
@@ -345,7 +379,7 @@ int64_t or_assemble_nnz(const or_desc* D) {
  *   b_free = F_free - L_{free,D} u_D.
  * Caller allocates rp[n+1], ci[nnz], val[nnz], rhs[n]. */
 int or_assemble(const or_desc* D, int64_t* rp, int32_t* ci, double* val, double* rhs) {
-    const int d = D->dim, NQ = ipow(3, d), NV = ipow(2, d);
+    const int d = D->dim, P = vorder(D), NQ = ipow(P + 1, d), NV = ipow(2, d);
     const int64_t n = or_n_dofs(D);
     int64_t buf[512];
     rp[0] = 0;
@@ -358,6 +392,7 @@ int or_assemble(const or_desc* D, int64_t* rp, int32_t* ci, double* val, double*
     memset(rhs, 0, sizeof(double) * n);
     double* Ae = malloc(sizeof(double) * NQ * NQ);
     double* Be = malloc(sizeof(double) * NQ * 3 * NV);
+    double* Ce = malloc(sizeof(double) * NV * NV);
     double* Fe = malloc(sizeof(double) * NQ * 3);
     int64_t nel = 1;
     for (int k = 0; k < d; ++k) nel *= D->ncell[k];
@@ -365,12 +400,12 @@ int or_assemble(const or_desc* D, int64_t* rp, int32_t* ci, double* val, double*
         int e[3] = {0, 0, 0};
         int64_t r = el;
         for (int k = 0; k < d; ++k) { e[k] = (int)(r % D->ncell[k]); r /= D->ncell[k]; }
-        element_matrices(D, e, Ae, Be, Fe);
+        element_matrices(D, e, Ae, Be, Ce, Fe);
         int64_t gn[27];           /* free-node index of each local node or -1 */
         int an[27][3];
         for (int a = 0; a < NQ; ++a) {
             for (int k = 0; k < 3; ++k) an[a][k] = 0;
-            for (int k = 0; k < d; ++k) an[a][k] = 2 * e[k] + (a / ipow(3, k)) % 3;
+            for (int k = 0; k < d; ++k) an[a][k] = P * e[k] + (a / ipow(P + 1, k)) % (P + 1);
             gn[a] = free_node(D, an[a]);
         }
         int64_t gp[8];
@@ -405,8 +440,11 @@ int or_assemble(const or_desc* D, int64_t* rp, int32_t* ci, double* val, double*
                 }
             }
         }
+        if (P == 1)   /* stabilization C (Eq. 8) */
+            for (int m = 0; m < NV; ++m)
+                for (int m2 = 0; m2 < NV; ++m2) val[csr_find(rp, ci, gp[m], gp[m2])] += Ce[m * NV + m2];
     }
-    free(Ae); free(Be); free(Fe);
+    free(Ae); free(Be); free(Ce); free(Fe);
     return 0;
 }
 
@@ -445,11 +483,15 @@ void or_spmv_t(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* c
 /* weights_mode: 0 = partition-of-unity psi_v(x_j) (R3), 1 = 0/1 ownership
  * node a -> vertex floor(a/2) (the paper's 0/1 G_i extended), 2 = all ones
  * (full prolongation R^T: additive Vanka, Eq. 12). */
-static double patch_weight(int mode, int d, const int* a, const int* v) {
+static double patch_weight(int mode, int d, int P, const int* a, const int* v) {
     if (mode == 2) return 1.0;
     double w = 1.0;
     for (int k = 0; k < d; ++k) {
-        int off = a[k] - 2 * v[k];
+        int off = a[k] - P * v[k];
+        if (P == 1) {          /* Q1-Q1: the velocity DoFs on the pressure node */
+            if (off != 0) return 0.0;
+            continue;
+        }
         if (mode == 0) {
             if (off < -1 || off > 1) return 0.0;
             w *= (off == 0) ? 1.0 : 0.5;
@@ -464,11 +506,11 @@ static double patch_weight(int mode, int d, const int* a, const int* v) {
  * touching v (the structural support of row p_v of B^T) plus p_v.
  * Order: restricted DoFs (weight > 0) ascending, then the others ascending. */
 static int64_t build_patch(const or_desc* D, int mode, const int* v, int64_t* dofs, double* w) {
-    const int d = D->dim;
+    const int d = D->dim, P = vorder(D);
     int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < d; ++k) {
-        lo[k] = 2 * v[k] - 2 < 0 ? 0 : 2 * v[k] - 2;
-        hi[k] = 2 * v[k] + 2 > 2 * D->ncell[k] ? 2 * D->ncell[k] : 2 * v[k] + 2;
+        lo[k] = P * v[k] - P < 0 ? 0 : P * v[k] - P;
+        hi[k] = P * v[k] + P > P * D->ncell[k] ? P * D->ncell[k] : P * v[k] + P;
     }
     int64_t cnt_r = 0, cnt_o = 0;
     int64_t rd[1200], od[1200];
@@ -480,7 +522,7 @@ static int64_t build_patch(const or_desc* D, int mode, const int* v, int64_t* do
         for (int k = 0; k < d; ++k) { a[k] = lo[k] + r % (hi[k] - lo[k] + 1); r /= (hi[k] - lo[k] + 1); }
         int64_t fa = free_node(D, a);
         if (fa < 0) continue;
-        double wt = patch_weight(mode, d, a, v);
+        double wt = patch_weight(mode, d, P, a, v);
         for (int c = 0; c < d; ++c) {
             if (wt > 0.0) { rd[cnt_r] = fa * d + c; rw[cnt_r] = wt; cnt_r++; }
             else od[cnt_o++] = fa * d + c;
@@ -763,10 +805,10 @@ static int64_t prolong_row(const or_desc* F, const or_desc* C, int64_t row, int6
         int64_t fi = row / d;
         comp = (int)(row % d);
         for (int k = 0; k < d; ++k) {
-            int m = 2 * F->ncell[k] - 1;
+            int m = vorder(F) * F->ncell[k] - 1;
             int a = (int)(fi % m) + 1;
             fi /= m;
-            cnt[k] = interp_q2_1d(a, C->ncell[k], idx[k], wt[k]);
+            cnt[k] = vorder(F) == 2 ? interp_q2_1d(a, C->ncell[k], idx[k], wt[k]) : interp_q1_1d(a, idx[k], wt[k]);
         }
     } else {
         int64_t vi = row - nuf;
@@ -1030,9 +1072,10 @@ void or_mms_errors(const or_desc* D, const double* xsol, double* err_u, double* 
                     double w = 0.25 * G4W[q0i] * G4W[q1i] * h0 * h1;
                     double x[3] = {(e0 + t0) * h0, (e1 + t1) * h1, 0.0};
                     double uh[2] = {0, 0}, ph = 0.0;
-                    for (int a = 0; a < 9; ++a) {
-                        int an[3] = {2 * e0 + a % 3, 2 * e1 + a / 3, 0};
-                        double phi = q2(a % 3, t0) * q2(a / 3, t1);
+                    const int P = vorder(D), NP1 = P + 1;
+                    for (int a = 0; a < NP1 * NP1; ++a) {
+                        int an[3] = {P * e0 + a % NP1, P * e1 + a / NP1, 0};
+                        double phi = vb(P, a % NP1, t0) * vb(P, a / NP1, t1);
                         int64_t fn = free_node(D, an);
                         for (int c = 0; c < 2; ++c)
                             uh[c] += phi * (fn >= 0 ? xsol[fn * 2 + c] : dirichlet_value(D, an, c));

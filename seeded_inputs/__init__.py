@@ -92,11 +92,17 @@ def random_vector(n: int, seed: int) -> np.ndarray:
     return np.random.Generator(np.random.PCG64(seed)).standard_normal(n)
 
 
+ELEM_Q2Q1 = "q2q1"     # Taylor-Hood, C = 0 (R1; BASELINE configs)
+ELEM_Q1Q1 = "q1q1"     # the paper's stabilized equal-order pair (Eq. 8; R18)
+BETA0 = 0.1            # R18: beta(x) = BETA0 / eta(x) (S:209 default 0.1/eta)
+
+
 def problem(dim: int, ncell, kind: int, eta: str = "const", eta0: float = 1.0,
-            box=None, seed: int = VISC_SEED) -> Dict:
+            box=None, seed: int = VISC_SEED, elem: str = ELEM_Q2Q1, beta: float = BETA0) -> Dict:
     """A problem description dict understood by both the oracle wrapper and the
-    CUDA binding: grid cells per axis, box lengths, boundary/forcing kind and
-    the viscosity field."""
+    CUDA binding: grid cells per axis, box lengths, boundary/forcing kind, the
+    viscosity field and the element pair (vel_order 2: Q2-Q1, 1: Q1-Q1 with
+    stabilization constant beta)."""
     ncell = list(ncell) + [1] * (3 - len(ncell))
     if box is None:
         box = [1.0, 1.0, 1.0]
@@ -104,7 +110,8 @@ def problem(dim: int, ncell, kind: int, eta: str = "const", eta0: float = 1.0,
     d = {"dim": dim, "ncell": ncell[:3], "len": [float(b) for b in box[:3]], "kind": kind,
          "eta_mode": ETA_CONST, "eta0": float(eta0), "n_modes": 0,
          "amp": np.zeros(8), "mode": np.zeros((8, 3), np.int32), "phase": np.zeros((8, 3)),
-         "gmin": 0.0, "gmax": 1.0}
+         "gmin": 0.0, "gmax": 1.0,
+         "vel_order": 1 if elem == ELEM_Q1Q1 else 2, "beta": float(beta) if elem == ELEM_Q1Q1 else 0.0}
     if eta == "fourier":
         vp = viscosity_params(dim, box, seed=seed)
         d.update({"eta_mode": ETA_FOURIER, "n_modes": vp["n_modes"], "amp": vp["amp"],
