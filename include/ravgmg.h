@@ -85,6 +85,14 @@ typedef struct {
     int32_t node_lo, node_hi, vert_lo, vert_hi;
     int32_t rnode_lo, rnode_hi, rvert_lo, rvert_hi;
     int32_t pvert_lo, pvert_hi;
+    /* Element pair: vel_order 2 (or 0) = Taylor-Hood Q2-Q1, C = 0 (R1; the BASELINE
+     * configs); 1 = the paper's stabilized equal-order Q1-Q1: velocity on
+     * the vertices, C = -beta sum_e h_e^2 ((1/eta) grad q, grad p)_e (Eq. 8 read
+     * on the pressure basis with beta(x) = beta / eta(x), h_e = element diameter:
+     * reading R18), 2-point Gauss rule per axis.  beta > 0 is required for Q1-Q1.
+     * Q1-Q1 levels support the whole-grid generator and transfers (win = 0). */
+    int32_t vel_order;
+    double  beta;
 } rav_grid;
 
 /* Sizes of the generated level: n_dofs = n_vel + n_pres; nnz of L; number of

@@ -14,9 +14,6 @@
 namespace rav {
 namespace gen {
 
-// 3-point Gauss rule on [0,1] (R7)
-__constant__ double c_gt[3];
-__constant__ double c_gw[3];
 
 struct Grid {
     int dim;
@@ -39,11 +36,28 @@ struct Grid {
     int64_t nvel_loc, nvert_loc, ndof_loc;
     int rnode_lo, rnode_hi, rvert_lo, rvert_hi;
     int64_t patch_off, npatch;      // first global vertex with a patch, number of patches
+    // element pair: P = 2 Taylor-Hood Q2-Q1 (velocity nodes on the (2n+1)^d lattice, R1),
+    // P = 1 stabilized Q1-Q1 (velocity on the vertices, C of P:78 Eq. 8, R18)
+    int P, ngp;                     // velocity lattice refinement, Gauss points per axis (P + 1)
+    double gt[3], gw[3];            // Gauss rule on [0,1] (3-point for Q2-Q1 R7, 2-point for Q1-Q1 R18)
+    double beta, he2;               // stabilization beta_0 and squared element diameter
 };
 
 static Grid make_grid(const rav_grid* g) {
     Grid G{};
     G.dim = g->dim;
+    G.P = g->vel_order == 1 ? 1 : 2;
+    G.ngp = G.P + 1;
+    if (G.P == 2) {
+        const double a = 0.5 * 0.77459666924148337704;  // sqrt(3/5)/2
+        G.gt[0] = 0.5 - a; G.gt[1] = 0.5; G.gt[2] = 0.5 + a;
+        G.gw[0] = 5.0 / 18.0; G.gw[1] = 8.0 / 18.0; G.gw[2] = 5.0 / 18.0;
+    } else {
+        const double a = 0.5 * 0.57735026918962576451;  // sqrt(1/3)/2
+        G.gt[0] = 0.5 - a; G.gt[1] = 0.5 + a;
+        G.gw[0] = 0.5; G.gw[1] = 0.5;
+    }
+    G.beta = g->beta;
     G.vol = 1.0;
     G.nfree = 1;
     G.nvert = 1;
@@ -54,7 +68,8 @@ static Grid make_grid(const rav_grid* g) {
     }
     for (int k = 0; k < g->dim; ++k) {
         G.vol *= G.h[k];
-        G.nfree *= (int64_t)(2 * G.n[k] - 1);
+        G.nfree *= (int64_t)(G.P * G.n[k] - 1);
+        G.he2 += G.h[k] * G.h[k];
         G.nvert *= (int64_t)(G.n[k] + 1);
         G.nel *= G.n[k];
     }
@@ -74,14 +89,14 @@ static Grid make_grid(const rav_grid* g) {
     G.nvel = (int64_t)g->dim * G.nfree;
     G.ndof = G.nvel + G.nvert;
     G.last = g->dim - 1;
-    G.nlow_free = G.nfree / (2 * G.n[G.last] - 1);
+    G.nlow_free = G.nfree / (G.P * G.n[G.last] - 1);
     G.nlow_vert = G.nvert / (G.n[G.last] + 1);
-    int node_lo = 1, node_hi = 2 * G.n[G.last] - 1, vert_lo = 0, vert_hi = G.n[G.last];
+    int node_lo = 1, node_hi = G.P * G.n[G.last] - 1, vert_lo = 0, vert_hi = G.n[G.last];
     G.rnode_lo = node_lo; G.rnode_hi = node_hi; G.rvert_lo = vert_lo; G.rvert_hi = vert_hi;
     int pv_lo = 0, pv_hi = G.n[G.last];
     if (g->win) {
         node_lo = std::max(1, g->node_lo);
-        node_hi = std::min(2 * G.n[G.last] - 1, g->node_hi);
+        node_hi = std::min(G.P * G.n[G.last] - 1, g->node_hi);
         vert_lo = std::max(0, g->vert_lo);
         vert_hi = std::min(G.n[G.last], g->vert_hi);
         G.rnode_lo = g->rnode_lo; G.rnode_hi = g->rnode_hi;
@@ -117,6 +132,9 @@ static rav_status check_grid(const rav_grid* g) {
     if (g->kind < 0 || g->kind > 2) { set_error("rav_grid: bad kind"); return RAV_ERR_ARG; }
     if (g->n_modes < 0 || g->n_modes > 8) { set_error("rav_grid: n_modes > 8"); return RAV_ERR_ARG; }
     if (g->eta_mode == 1 && !(g->gmax > g->gmin)) { set_error("rav_grid: gmax <= gmin"); return RAV_ERR_ARG; }
+    if (g->vel_order != 0 && g->vel_order != 1 && g->vel_order != 2) { set_error("rav_grid: vel_order must be 1 or 2"); return RAV_ERR_ARG; }
+    if (g->vel_order == 1 && g->win) { set_error("rav_grid: slab windows are implemented for Q2-Q1 only"); return RAV_ERR_ARG; }
+    if (g->vel_order == 1 && !(g->beta > 0.0)) { set_error("rav_grid: Q1-Q1 needs beta > 0 (P:80)"); return RAV_ERR_ARG; }
     if (g->win && (g->node_lo > g->node_hi || g->vert_lo > g->vert_hi || g->pvert_lo > g->pvert_hi)) {
         set_error("rav_grid: empty window");
         return RAV_ERR_ARG;
@@ -124,17 +142,6 @@ static rav_status check_grid(const rav_grid* g) {
     return RAV_OK;
 }
 
-static void upload_rule(cudaStream_t s) {
-    static bool done = false;
-    if (done) return;
-    const double a = 0.5 * 0.77459666924148337704;  // sqrt(3/5)/2
-    double t[3] = {0.5 - a, 0.5, 0.5 + a};
-    double w[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
-    cudaMemcpyToSymbol(c_gt, t, sizeof(t));
-    cudaMemcpyToSymbol(c_gw, w, sizeof(w));
-    done = true;
-    (void)s;
-}
 
 // ---- 1D bases -------------------------------------------------------------------
 __device__ __forceinline__ double q2v(int l, double t) {
@@ -144,12 +151,16 @@ __device__ __forceinline__ double q2d(int l, double t) {
     return l == 0 ? 4.0 * t - 3.0 : (l == 1 ? 4.0 - 8.0 * t : 4.0 * t - 1.0);
 }
 __device__ __forceinline__ double q1v(int m, double t) { return m == 0 ? 1.0 - t : t; }
+__device__ __forceinline__ double q1d(int m, double t) { (void)t; return m == 0 ? -1.0 : 1.0; }
+// velocity basis of the element pair (P = 2: Q2, P = 1: Q1)
+__device__ __forceinline__ double vbv(int P, int l, double t) { return P == 2 ? q2v(l, t) : q1v(l, t); }
+__device__ __forceinline__ double vbd(int P, int l, double t) { return P == 2 ? q2d(l, t) : q1d(l, t); }
 
 // ---- lattice helpers --------------------------------------------------------------
 __device__ __forceinline__ int64_t free_id(const Grid& G, const int* a) {
     int64_t id = 0, s = 1;
     for (int k = 0; k < G.dim; ++k) {
-        int m = 2 * G.n[k];
+        int m = G.P * G.n[k];
         if (a[k] <= 0 || a[k] >= m) return -1;
         id += (int64_t)(a[k] - 1) * s;
         s *= (m - 1);
@@ -166,9 +177,10 @@ __device__ __forceinline__ int64_t elem_id(const Grid& G, const int* e) {
     for (int k = 0; k < G.dim; ++k) { id += (int64_t)e[k] * s; s *= G.n[k]; }
     return id;
 }
-// range of elements along one axis containing lattice node index a
-__device__ __forceinline__ void node_elems(int a, int n, int& lo, int& hi) {
-    if (a & 1) { lo = hi = (a - 1) >> 1; }
+// range of elements along one axis containing velocity lattice node index a
+__device__ __forceinline__ void node_elems(int P, int a, int n, int& lo, int& hi) {
+    if (P == 1) { lo = a - 1; hi = a; }
+    else if (a & 1) { lo = hi = (a - 1) >> 1; }
     else { lo = (a >> 1) - 1; hi = a >> 1; }
     if (lo < 0) lo = 0;
     if (hi > n - 1) hi = n - 1;
@@ -182,9 +194,9 @@ __device__ __forceinline__ void vert_elems(int v, int n, int& lo, int& hi) {
 __device__ __forceinline__ double dirichlet(const Grid& G, const int* a, int c) {
     if (G.kind != 0 || c != 0) return 0.0;
     int top = G.dim - 1;
-    if (a[top] != 2 * G.n[top]) return 0.0;
+    if (a[top] != G.P * G.n[top]) return 0.0;
     for (int k = 0; k < top; ++k)
-        if (a[k] <= 0 || a[k] >= 2 * G.n[k]) return 0.0;
+        if (a[k] <= 0 || a[k] >= G.P * G.n[k]) return 0.0;
     return 1.0;
 }
 
@@ -232,7 +244,7 @@ __device__ void mms_force(const Grid& G, const double* x, double* f) {
 
 // one thread per (element, quadrature point): eta and (MMS) f
 __global__ void coef_kernel(Grid G, double* eta_tab, double* f_tab) {
-    const int NG = G.dim == 2 ? 9 : 27;
+    const int NG = G.dim == 2 ? G.ngp * G.ngp : G.ngp * G.ngp * G.ngp;
     int64_t total = G.nel * NG;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -243,7 +255,7 @@ __global__ void coef_kernel(Grid G, double* eta_tab, double* f_tab) {
         for (int k = 0; k < G.dim; ++k) { e[k] = (int)(r % G.n[k]); r /= G.n[k]; }
         double x[3] = {0, 0, 0};
         int qq = q;
-        for (int k = 0; k < G.dim; ++k) { x[k] = (e[k] + c_gt[qq % 3]) * G.h[k]; qq /= 3; }
+        for (int k = 0; k < G.dim; ++k) { x[k] = (e[k] + G.gt[qq % G.ngp]) * G.h[k]; qq /= G.ngp; }
         double eta, ge[3];
         eta_grad(G, x, eta, ge);
         eta_tab[t] = eta;
@@ -262,29 +274,29 @@ __device__ double a_entry(const Grid& G, const double* eta_tab, const int* a, co
     int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < G.dim; ++k) {
         int la, ha, lb, hb;
-        node_elems(a[k], G.n[k], la, ha);
-        node_elems(b[k], G.n[k], lb, hb);
+        node_elems(G.P, a[k], G.n[k], la, ha);
+        node_elems(G.P, b[k], G.n[k], lb, hb);
         lo[k] = max(la, lb);
         hi[k] = min(ha, hb);
         if (lo[k] > hi[k]) return 0.0;
     }
-    const int NG = G.dim == 2 ? 9 : 27;
+    const int g = G.ngp, NG = G.dim == 2 ? g * g : g * g * g;
     double s = 0.0;
     int e[3] = {0, 0, 0};
     for (e[2] = lo[2]; e[2] <= hi[2]; ++e[2])
         for (e[1] = lo[1]; e[1] <= hi[1]; ++e[1])
             for (e[0] = lo[0]; e[0] <= hi[0]; ++e[0]) {
                 int la[3], lb[3];
-                for (int k = 0; k < 3; ++k) { la[k] = a[k] - 2 * e[k]; lb[k] = b[k] - 2 * e[k]; }
+                for (int k = 0; k < 3; ++k) { la[k] = a[k] - G.P * e[k]; lb[k] = b[k] - G.P * e[k]; }
                 const double* et = eta_tab + elem_id(G, e) * NG;
                 for (int q = 0; q < NG; ++q) {
-                    int qk[3] = {q % 3, (q / 3) % 3, q / 9};
+                    int qk[3] = {q % g, (q / g) % g, q / (g * g)};
                     double va[3], vb[3], da[3], db[3], w = G.vol;
                     for (int k = 0; k < G.dim; ++k) {
-                        double t = c_gt[qk[k]];
-                        w *= c_gw[qk[k]];
-                        va[k] = q2v(la[k], t); vb[k] = q2v(lb[k], t);
-                        da[k] = q2d(la[k], t) / G.h[k]; db[k] = q2d(lb[k], t) / G.h[k];
+                        double t = G.gt[qk[k]];
+                        w *= G.gw[qk[k]];
+                        va[k] = vbv(G.P, la[k], t); vb[k] = vbv(G.P, lb[k], t);
+                        da[k] = vbd(G.P, la[k], t) / G.h[k]; db[k] = vbd(G.P, lb[k], t) / G.h[k];
                     }
                     double dot = 0.0;
                     for (int k = 0; k < G.dim; ++k) {
@@ -303,28 +315,28 @@ __device__ double b_entry(const Grid& G, const int* b, int c, const int* v) {
     int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < G.dim; ++k) {
         int lb, hb, lv, hv;
-        node_elems(b[k], G.n[k], lb, hb);
+        node_elems(G.P, b[k], G.n[k], lb, hb);
         vert_elems(v[k], G.n[k], lv, hv);
         lo[k] = max(lb, lv);
         hi[k] = min(hb, hv);
         if (lo[k] > hi[k]) return 0.0;
     }
-    const int NG = G.dim == 2 ? 9 : 27;
+    const int g = G.ngp, NG = G.dim == 2 ? g * g : g * g * g;
     double s = 0.0;
     int e[3] = {0, 0, 0};
     for (e[2] = lo[2]; e[2] <= hi[2]; ++e[2])
         for (e[1] = lo[1]; e[1] <= hi[1]; ++e[1])
             for (e[0] = lo[0]; e[0] <= hi[0]; ++e[0]) {
                 int lb[3], lm[3];
-                for (int k = 0; k < 3; ++k) { lb[k] = b[k] - 2 * e[k]; lm[k] = v[k] - e[k]; }
+                for (int k = 0; k < 3; ++k) { lb[k] = b[k] - G.P * e[k]; lm[k] = v[k] - e[k]; }
                 for (int q = 0; q < NG; ++q) {
-                    int qk[3] = {q % 3, (q / 3) % 3, q / 9};
+                    int qk[3] = {q % g, (q / g) % g, q / (g * g)};
                     double w = G.vol, psi = 1.0, dphi = 1.0;
                     for (int k = 0; k < G.dim; ++k) {
-                        double t = c_gt[qk[k]];
-                        w *= c_gw[qk[k]];
+                        double t = G.gt[qk[k]];
+                        w *= G.gw[qk[k]];
                         psi *= q1v(lm[k], t);
-                        dphi *= (k == c) ? q2d(lb[k], t) / G.h[k] : q2v(lb[k], t);
+                        dphi *= (k == c) ? vbd(G.P, lb[k], t) / G.h[k] : vbv(G.P, lb[k], t);
                     }
                     s -= (w * psi) * dphi;
                 }
@@ -336,20 +348,62 @@ __device__ double b_entry(const Grid& G, const int* b, int c, const int* v) {
 __device__ double f_entry(const Grid& G, const double* f_tab, const int* a, int c) {
     if (G.kind != 1) return 0.0;
     int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    for (int k = 0; k < G.dim; ++k) node_elems(a[k], G.n[k], lo[k], hi[k]);
-    const int NG = 9;
+    for (int k = 0; k < G.dim; ++k) node_elems(G.P, a[k], G.n[k], lo[k], hi[k]);
+    const int g = G.ngp, NG = g * g;
     double s = 0.0;
     int e[3] = {0, 0, 0};
     for (e[1] = lo[1]; e[1] <= hi[1]; ++e[1])
         for (e[0] = lo[0]; e[0] <= hi[0]; ++e[0]) {
-            int la[2] = {a[0] - 2 * e[0], a[1] - 2 * e[1]};
+            int la[2] = {a[0] - G.P * e[0], a[1] - G.P * e[1]};
             int64_t el = elem_id(G, e);
             for (int q = 0; q < NG; ++q) {
-                double t0 = c_gt[q % 3], t1 = c_gt[q / 3];
-                double w = G.vol * c_gw[q % 3] * c_gw[q / 3];
-                s += (w * f_tab[2 * (el * NG + q) + c]) * (q2v(la[0], t0) * q2v(la[1], t1));
+                double t0 = G.gt[q % g], t1 = G.gt[q / g];
+                double w = G.vol * G.gw[q % g] * G.gw[q / g];
+                s += (w * f_tab[2 * (el * NG + q) + c]) * (vbv(G.P, la[0], t0) * vbv(G.P, la[1], t1));
             }
         }
+    return s;
+}
+
+// Q1-Q1 stabilization (Eq. 8, R18): -beta_0 h_e^2 int (1/eta) grad psi_v . grad psi_u over the
+// elements shared by vertices v and u
+__device__ double c_entry(const Grid& G, const double* eta_tab, const int* v, const int* u) {
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int k = 0; k < G.dim; ++k) {
+        int lv, hv, lu, hu;
+        vert_elems(v[k], G.n[k], lv, hv);
+        vert_elems(u[k], G.n[k], lu, hu);
+        lo[k] = max(lv, lu);
+        hi[k] = min(hv, hu);
+        if (lo[k] > hi[k]) return 0.0;
+    }
+    const int g = G.ngp, NG = G.dim == 2 ? g * g : g * g * g;
+    double s = 0.0;
+    int e[3] = {0, 0, 0};
+    for (e[2] = lo[2]; e[2] <= hi[2]; ++e[2])
+        for (e[1] = lo[1]; e[1] <= hi[1]; ++e[1])
+            for (e[0] = lo[0]; e[0] <= hi[0]; ++e[0]) {
+                int lv[3], lu[3];
+                for (int k = 0; k < 3; ++k) { lv[k] = v[k] - e[k]; lu[k] = u[k] - e[k]; }
+                const double* et = eta_tab + elem_id(G, e) * NG;
+                for (int q = 0; q < NG; ++q) {
+                    int qk[3] = {q % g, (q / g) % g, q / (g * g)};
+                    double vv[3], vu[3], dv[3], du[3], w = G.vol;
+                    for (int k = 0; k < G.dim; ++k) {
+                        double t = G.gt[qk[k]];
+                        w *= G.gw[qk[k]];
+                        vv[k] = q1v(lv[k], t); vu[k] = q1v(lu[k], t);
+                        dv[k] = q1d(lv[k], t) / G.h[k]; du[k] = q1d(lu[k], t) / G.h[k];
+                    }
+                    double dot = 0.0;
+                    for (int k = 0; k < G.dim; ++k) {
+                        double gv = dv[k], gu = du[k];
+                        for (int j = 0; j < G.dim; ++j) if (j != k) { gv *= vv[j]; gu *= vu[j]; }
+                        dot += gv * gu;
+                    }
+                    s -= G.beta * G.he2 * (w / et[q]) * dot;
+                }
+            }
     return s;
 }
 
@@ -359,7 +413,7 @@ __device__ __forceinline__ void decode_vel_row(const Grid& G, int64_t row, int* 
     c = (int)(row % G.dim);
     a[0] = a[1] = a[2] = 0;
     for (int k = 0; k < G.dim; ++k) {
-        int m = 2 * G.n[k] - 1;
+        int m = G.P * G.n[k] - 1;
         a[k] = (int)(fi % m) + 1;
         fi /= m;
     }
@@ -393,17 +447,18 @@ __global__ void op_count_kernel(Grid G, int64_t* cnt) {
         bool vel;
         if (!decode_local_row(G, row, a, c, vel)) { cnt[row] = 0; continue; }
         for (int k = 0; k < G.dim; ++k) {
-            if (vel) node_elems(a[k], G.n[k], lo[k], hi[k]);
+            if (vel) node_elems(G.P, a[k], G.n[k], lo[k], hi[k]);
             else vert_elems(a[k], G.n[k], lo[k], hi[k]);
         }
         int64_t nodes = 1, verts = 1;
         for (int k = 0; k < G.dim; ++k) {
-            // free lattice nodes in [2lo, 2hi+2] intersected with [1, 2n-1]
-            int l = max(2 * lo[k], 1), h = min(2 * hi[k] + 2, 2 * G.n[k] - 1);
+            // free lattice nodes in [P lo, P hi + P] intersected with [1, P n - 1]
+            int l = max(G.P * lo[k], 1), h = min(G.P * hi[k] + G.P, G.P * G.n[k] - 1);
             nodes *= (h - l + 1);
             verts *= (hi[k] - lo[k] + 2);
         }
-        cnt[row] = vel ? nodes + verts : nodes * G.dim;
+        // velocity row: velocity + pressure (B); pressure row: velocity (B^T) [+ pressure (C), Q1-Q1]
+        cnt[row] = vel ? nodes + verts : nodes * G.dim + (G.P == 1 ? verts : 0);
     }
 }
 
@@ -416,12 +471,12 @@ __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_ta
         bool vel;
         if (!decode_local_row(G, row, a, c, vel)) { rhs[row] = 0.0; continue; }
         for (int k = 0; k < G.dim; ++k) {
-            if (vel) node_elems(a[k], G.n[k], lo[k], hi[k]);
+            if (vel) node_elems(G.P, a[k], G.n[k], lo[k], hi[k]);
             else vert_elems(a[k], G.n[k], lo[k], hi[k]);
         }
         double lift = 0.0;
         int bl[3] = {0, 0, 0}, bh[3] = {0, 0, 0};
-        for (int k = 0; k < G.dim; ++k) { bl[k] = 2 * lo[k]; bh[k] = 2 * hi[k] + 2; }
+        for (int k = 0; k < G.dim; ++k) { bl[k] = G.P * lo[k]; bh[k] = G.P * hi[k] + G.P; }
         int b[3] = {0, 0, 0};
         for (b[2] = bl[2]; b[2] <= bh[2]; ++b[2])
             for (b[1] = bl[1]; b[1] <= bh[1]; ++b[1])
@@ -453,7 +508,7 @@ __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_ta
                         }
                     }
                 }
-        if (vel) {
+        if (vel || G.P == 1) {   // B entries of a velocity row / C entries of a Q1-Q1 pressure row
             int v[3] = {0, 0, 0};
             for (v[2] = lo[2]; v[2] <= (G.dim > 2 ? hi[2] + 1 : 0); ++v[2])
                 for (v[1] = lo[1]; v[1] <= hi[1] + 1; ++v[1])
@@ -461,22 +516,24 @@ __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_ta
                         const int64_t lc = loc_vert(G, vert_id(G, v));
                         if (lc < 0) atomicOr(err, 1u);
                         col[p] = (int32_t)lc;
-                        val[p] = b_entry(G, a, c, v);
+                        val[p] = vel ? b_entry(G, a, c, v) : c_entry(G, eta_tab, a, v);
                         ++p;
                     }
-            rhs[row] = f_entry(G, f_tab, a, c) + lift;
-        } else {
-            rhs[row] = lift;
         }
+        rhs[row] = vel ? f_entry(G, f_tab, a, c) + lift : lift;
     }
 }
 
 // ---- patches -------------------------------------------------------------------
-__device__ __forceinline__ double patch_weight(int mode, int dim, const int* a, const int* v) {
+__device__ __forceinline__ double patch_weight(int mode, int dim, int P, const int* a, const int* v) {
     if (mode == 2) return 1.0;
     double w = 1.0;
     for (int k = 0; k < dim; ++k) {
-        int off = a[k] - 2 * v[k];
+        int off = a[k] - P * v[k];
+        if (P == 1) {          // Q1-Q1: the velocity DoFs on the pressure node
+            if (off != 0) return 0.0;
+            continue;
+        }
         if (mode == 0) {
             if (off < -1 || off > 1) return 0.0;
             if (off != 0) w *= 0.5;
@@ -494,7 +551,7 @@ __global__ void patch_count_kernel(Grid G, int64_t* cnt) {
         decode_vertex(G, pi + G.patch_off, v);
         int64_t nodes = 1;
         for (int k = 0; k < G.dim; ++k) {
-            int l = max(2 * v[k] - 2, 1), h = min(2 * v[k] + 2, 2 * G.n[k] - 1);
+            int l = max(G.P * v[k] - G.P, 1), h = min(G.P * v[k] + G.P, G.P * G.n[k] - 1);
             nodes *= (h - l + 1);
         }
         cnt[pi] = nodes * G.dim + 1;
@@ -509,7 +566,7 @@ __global__ void patch_fill_kernel(Grid G, int mode, const int64_t* offs, int32_t
         int v[3];
         decode_vertex(G, vi, v);
         int l[3] = {0, 0, 0}, h[3] = {0, 0, 0};
-        for (int k = 0; k < G.dim; ++k) { l[k] = max(2 * v[k] - 2, 1); h[k] = min(2 * v[k] + 2, 2 * G.n[k] - 1); }
+        for (int k = 0; k < G.dim; ++k) { l[k] = max(G.P * v[k] - G.P, 1); h[k] = min(G.P * v[k] + G.P, G.P * G.n[k] - 1); }
         int64_t p = offs[pi];
         for (int pass = 0; pass < 2; ++pass) {
             if (pass == 1) {
@@ -523,7 +580,7 @@ __global__ void patch_fill_kernel(Grid G, int mode, const int64_t* offs, int32_t
             for (a[2] = l[2]; a[2] <= h[2]; ++a[2])
                 for (a[1] = l[1]; a[1] <= h[1]; ++a[1])
                     for (a[0] = l[0]; a[0] <= h[0]; ++a[0]) {
-                        double wt = patch_weight(mode, G.dim, a, v);
+                        double wt = patch_weight(mode, G.dim, G.P, a, v);
                         if ((pass == 0) != (wt > 0.0)) continue;
                         int64_t fa = free_id(G, a);
                         for (int c = 0; c < G.dim; ++c) {
@@ -570,7 +627,7 @@ __global__ void prol_kernel(Grid F, Grid Cg, int64_t* cnt_or_rp, int32_t* ci, do
             continue;
         }
         for (int k = 0; k < F.dim; ++k)
-            cnt[k] = vel ? interp_q2(a[k], Cg.n[k], idx[k], wt[k]) : interp_q1(a[k], idx[k], wt[k]);
+            cnt[k] = (vel && F.P == 2) ? interp_q2(a[k], Cg.n[k], idx[k], wt[k]) : interp_q1(a[k], idx[k], wt[k]);
         int64_t p = FILL ? cnt_or_rp[row] : 0;
         int64_t c = 0;
         for (int s2 = 0; s2 < cnt[2]; ++s2)
@@ -665,8 +722,7 @@ extern "C" rav_status rav_gen_operator(const rav_grid* g, int64_t* row_ptr, int3
     if (!row_ptr || !col || !val || !rhs) { set_error("rav_gen_operator: NULL buffer"); return RAV_ERR_ARG; }
     Grid G = make_grid(g);
     cudaStream_t s = as_stream(stream);
-    upload_rule(s);
-    const int NG = G.dim == 2 ? 9 : 27;
+    const int NG = G.dim == 2 ? G.ngp * G.ngp : G.ngp * G.ngp * G.ngp;
     double *eta_tab = nullptr, *f_tab = nullptr;
     int64_t* cnt = nullptr;
     unsigned int* err = nullptr;
@@ -728,6 +784,7 @@ static rav_status check_nested(const rav_grid* f, const rav_grid* c) {
     RAV_TRY(check_grid(f));
     RAV_TRY(check_grid(c));
     if (f->dim != c->dim) { set_error("prolongation: dim mismatch"); return RAV_ERR_ARG; }
+    if ((f->vel_order == 1) != (c->vel_order == 1)) { set_error("prolongation: element pair mismatch"); return RAV_ERR_ARG; }
     for (int k = 0; k < f->dim; ++k)
         if (f->ncell[k] != 2 * c->ncell[k]) { set_error("prolongation: fine ncell must be 2 x coarse"); return RAV_ERR_ARG; }
     return RAV_OK;

@@ -40,7 +40,8 @@ class RavGrid(C.Structure):
                 ("phase", (C.c_double * 3) * 8), ("gmin", C.c_double), ("gmax", C.c_double),
                 ("win", C.c_int32), ("node_lo", C.c_int32), ("node_hi", C.c_int32), ("vert_lo", C.c_int32),
                 ("vert_hi", C.c_int32), ("rnode_lo", C.c_int32), ("rnode_hi", C.c_int32),
-                ("rvert_lo", C.c_int32), ("rvert_hi", C.c_int32), ("pvert_lo", C.c_int32), ("pvert_hi", C.c_int32)]
+                ("rvert_lo", C.c_int32), ("rvert_hi", C.c_int32), ("pvert_lo", C.c_int32), ("pvert_hi", C.c_int32),
+                ("vel_order", C.c_int32), ("beta", C.c_double)]
 
 WINDOW_KEYS = ("node_lo", "node_hi", "vert_lo", "vert_hi", "rnode_lo", "rnode_hi", "rvert_lo", "rvert_hi",
                "pvert_lo", "pvert_hi")
@@ -155,6 +156,8 @@ def grid(problem: Dict) -> RavGrid:
             g.phase[m][k] = float(problem["phase"][m][k])
     g.gmin = problem["gmin"]
     g.gmax = problem["gmax"]
+    g.vel_order = int(problem.get("vel_order", 2))
+    g.beta = float(problem.get("beta", 0.0))
     win = problem.get("window")
     if win is not None:   # slab window of one rank (dist.py)
         g.win = 1
