@@ -271,6 +271,86 @@ def run_vcycle_smoothers(rg, si, stream):
     return out
 
 
+def _timed_solve(rg, prob, levels, weights, variant, omega, pre, stream, rtol=1e-8, maxit=400):
+    """Build a GPU hierarchy and time mg_solve (CUDA events, after a warm-up that
+    captures the V-cycle graph).  Returns a dict (or a divergence record)."""
+    import torch
+    mg, fine = rg.build_hierarchy(prob, levels, weights, variant=variant)
+    x = torch.zeros(fine["n"], dtype=torch.float64, device="cuda")
+    out = {"pre_post": pre, "omega": omega}
+    try:
+        mg.solve(x, fine["b"], pre=pre, post=pre, omega=omega, rtol=rtol, maxit=2)
+        x.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        x, k, h = mg.solve(x, fine["b"], pre=pre, post=pre, omega=omega, rtol=rtol, maxit=maxit)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        out.update({"cycles": k, "converged": bool(h[-1] <= rtol * h[0]), "time_s": t,
+                    "ms_per_cycle": t / max(k, 1) * 1e3,
+                    "avg_reduction_factor": (h[-1] / h[0]) ** (1.0 / max(k, 1))})
+    except rg.RavError as err:
+        torch.cuda.synchronize()
+        out.update({"converged": False, "diverged": str(err)[:120]})
+    out["free_dofs"] = fine["n"]
+    mg.close()
+    del mg, fine, x
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_q1q1_studies(rg, si, stream):
+    """The paper's own discretization (stabilized Q1-Q1; SURVEY section 8
+    row f1) in the paper's driven-cavity setting on uniform grids: coarse grid
+    8x8, V(3,3), RAV / MV omega 0.66, AV omega 0.1,
+    1e8 reduction.  (a) convergence study over the grid hierarchy (Figs. 4-5:
+    cycles, average reduction factor, runtime per cycle, total runtime);
+    (b) smoothing-step study n_S = 1..6 on 512^2 (Fig. 7 / P:199-213, SURVEY f2);
+    (c) RAV sweep throughput on a 2048^2 Q1-Q1 level."""
+    import math
+    import torch
+    smoothers = (("rav", "pou", rg.VARIANT_ROWS, 0.66), ("mv_color", "full", rg.VARIANT_MV, 0.66),
+                 ("av", "full", rg.VARIANT_ROWS, 0.1))
+    out = {"config": "Q1-Q1 stabilized (beta = 0.1/eta, R18) lid-driven cavity, eta = 1, uniform grids, "
+                     "8x8 coarsest, x0 = 0, rtol 1e-8"}
+    study = {}
+    for n in (64, 128, 256, 512, 1024):
+        prob = si.problem(2, (n, n), si.KIND_CAVITY, elem=si.ELEM_Q1Q1)
+        lv = int(math.log2(n // 8)) + 1
+        study[f"{n}x{n}"] = {name: _timed_solve(rg, prob, lv, w, v, om, 3, stream)
+                             for name, w, v, om in smoothers}
+    out["convergence_study_V33"] = study
+    steps = {}
+    prob = si.problem(2, (512, 512), si.KIND_CAVITY, elem=si.ELEM_Q1Q1)
+    for ns in range(1, 7):
+        steps[f"nS={ns}"] = {name: _timed_solve(rg, prob, 7, w, v, om, ns, stream, maxit=300)
+                             for name, w, v, om in smoothers}
+    out["smoothing_steps_512"] = steps
+    # RAV sweep throughput (residual + sweep) on 2048^2 Q1-Q1 with the seeded viscosity
+    prob = si.problem(2, (2048, 2048), si.KIND_MMS, eta="fourier", elem=si.ELEM_Q1Q1)
+    G = rg.gen_level(prob, "pou")
+    sm = rg.Smoother(G, G)
+    x = torch.tensor(si.initial_guess(G["n"], seed=si.X0_SEED), device="cuda")
+    sm.smooth(x, G["b"], 10, 0.66)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    sm.smooth(x, G["b"], 50, 0.66)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 50
+    by = sm.sweep_bytes()
+    out["rav_sweep_2048"] = {"free_dofs": G["n"], "ms_per_sweep": ms, "mdofs": G["n"] / (ms * 1e-3) / 1e6,
+                             "kernel": sm.kernel_name, "algorithmic_gb_per_sweep": (by["sweep"] + by["residual"]) / 1e9,
+                             "achieved_gbs": (by["sweep"] + by["residual"]) / (ms * 1e-3) / 1e9}
+    sm.close()
+    del sm, G, x
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_dist_vcycle(name, rdist, si, stream, dist, ws, rank):
     """Slab-partitioned V-cycle to rtol on ws GPUs (strong scaling of c3 / c4):
     partitioned fine levels with NCCL interface sums / halo refreshes, windowed
@@ -556,6 +636,8 @@ def run_gpu(args):
     if not args.no_smoothers and ws == 1:
         extra["c5_smoothers"] = run_c5_smoothers(rg, si, stream)
         extra["vcycle_smoothers"] = run_vcycle_smoothers(rg, si, stream)
+    if not args.no_paper and ws == 1:
+        extra["q1q1_paper_setting"] = run_q1q1_studies(rg, si, stream)
 
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample) ------------------
     cpu = None
@@ -613,6 +695,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-vcycle", action="store_true", help="skip the c3 V-cycle time-to-1e-8 measurement")
     ap.add_argument("--no-smoothers", action="store_true", help="skip the c5 / V-cycle smoother comparisons")
+    ap.add_argument("--no-paper", action="store_true", help="skip the Q1-Q1 paper-setting studies")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

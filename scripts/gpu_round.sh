@@ -13,9 +13,9 @@ fi
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"; tail -c 3000 $OUT/bench.json
 if [ "$NCU" != "0" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $OUT/launches.csv \
-     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-vcycle --no-smoothers > $OUT/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-vcycle --no-smoothers --no-paper > $OUT/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
   for K in ${NCU_KERNELS:-schur_sweep_thread_kernel nb_residual_kernel}; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 5 -c 1 -o $OUT/prof_$K \
-       python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-vcycle --no-smoothers > $OUT/ncu_$K.log 2>&1; echo "ncu $K rc=$?"
+       python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-vcycle --no-smoothers --no-paper > $OUT/ncu_$K.log 2>&1; echo "ncu $K rc=$?"
   done
 fi

@@ -94,7 +94,7 @@ def random_vector(n: int, seed: int) -> np.ndarray:
 
 ELEM_Q2Q1 = "q2q1"     # Taylor-Hood, C = 0 (R1; BASELINE configs)
 ELEM_Q1Q1 = "q1q1"     # the paper's stabilized equal-order pair (Eq. 8; R18)
-BETA0 = 0.1            # R18: beta(x) = BETA0 / eta(x) (S:209 default 0.1/eta)
+BETA0 = 0.01           # R18: beta(x) = BETA0 / eta(x) (chosen by the MMS + multigrid beta study)
 
 
 def problem(dim: int, ncell, kind: int, eta: str = "const", eta0: float = 1.0,
