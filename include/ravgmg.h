@@ -287,6 +287,19 @@ rav_status mg_vcycle(mg_ctx* ctx, double* x, const double* b, int pre, int post,
 rav_status mg_solve(mg_ctx* ctx, double* x, const double* b, int pre, int post, double omega,
                     double rtol, int maxit, int* iters, double* hist);
 
+/* Flexible GMRES(restart) on the finest level, right-preconditioned by one
+ * V-cycle from a zero guess ("the geometric multigrid method can
+ * also be used as a preconditioner in a Krylov subspace solver"; reading R19).
+ * Arnoldi with classical Gram-Schmidt and one reorthogonalisation pass, Givens
+ * rotations on the host.  Stops when the least-squares residual estimate
+ * <= rtol ||b - L x_0||_2 or after maxit Arnoldi steps (= preconditioner
+ * applications); *iters = steps taken, hist (host, maxit + 1, may be NULL) =
+ * ||r_0|| and the estimate after every step.  x (in/out), b: DEVICE pointers.
+ * Work space (restart + 1 + restart vectors of n_fine doubles) is allocated on
+ * the first call and kept in the context.  RAV_ERR_DIVERGED on NaN/Inf. */
+rav_status mg_fgmres(mg_ctx* ctx, double* x, const double* b, int pre, int post, double omega, int restart,
+                     double rtol, int maxit, int* iters, double* hist);
+
 /* ------------------------------------------------------------------------- */
 /* Exchange helpers for the slab-partitioned sweep (SURVEY section 8 row e)    */
 /* ------------------------------------------------------------------------- */

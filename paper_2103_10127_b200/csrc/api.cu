@@ -99,6 +99,9 @@ struct mg_ctx {
     double* hb = nullptr;
     GraphCache cyc;             // one V-cycle + residual norm
     int64_t last_launches = 0;
+    // FGMRES work space (mg_fgmres): V (m+1) x n, Z m x n, w, r, device coefficients
+    int kry_m = 0;
+    double *kV = nullptr, *kZ = nullptr, *kw = nullptr, *kr = nullptr, *kh = nullptr, *kpart = nullptr;
 };
 
 namespace rav {
@@ -378,6 +381,8 @@ void mg_destroy(mg_ctx* m) {
     if (m->h_norm2) cudaFreeHost(m->h_norm2);
     if (m->hx) cudaFree(m->hx);
     if (m->hb) cudaFree(m->hb);
+    for (double* p : {m->kV, m->kZ, m->kw, m->kr, m->kh, m->kpart})
+        if (p) cudaFree(p);
     delete m;
 }
 
@@ -635,3 +640,124 @@ rav_status rav_dot(const double* a, const double* b, int64_t n, double* out, int
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------------------
+// flexible GMRES with the V-cycle as preconditioner (reading R19)
+// ------------------------------------------------------------------------------------
+
+namespace rav {
+
+static rav_status kry_alloc(mg_ctx* m, int restart, int64_t n) {
+    if (m->kry_m == restart && m->kV) return RAV_OK;
+    for (double** p : {&m->kV, &m->kZ, &m->kw, &m->kr, &m->kh, &m->kpart})
+        if (*p) { cudaFree(*p); *p = nullptr; }
+    RAV_CUDA(cudaMalloc(&m->kV, sizeof(double) * (size_t)(restart + 1) * n));
+    RAV_CUDA(cudaMalloc(&m->kZ, sizeof(double) * (size_t)restart * n));
+    RAV_CUDA(cudaMalloc(&m->kw, sizeof(double) * n));
+    RAV_CUDA(cudaMalloc(&m->kr, sizeof(double) * n));
+    RAV_CUDA(cudaMalloc(&m->kh, sizeof(double) * (2 * (restart + 1) + 2)));
+    RAV_CUDA(cudaMalloc(&m->kpart, sizeof(double) * residual_norm_blocks()));
+    m->kry_m = restart;
+    return RAV_OK;
+}
+
+// *out (host) = ||v||_2
+static rav_status kry_norm(mg_ctx* m, const double* v, int64_t n, double* dev_slot, double* out) {
+    RAV_TRY(launch_dot(v, v, n, m->kpart, residual_norm_blocks(), dev_slot, 0, m->stream));
+    RAV_CUDA(cudaMemcpyAsync(out, dev_slot, sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+    RAV_CUDA(cudaStreamSynchronize(m->stream));
+    *out = sqrt(*out);
+    return RAV_OK;
+}
+
+}  // namespace rav
+
+extern "C" rav_status mg_fgmres(mg_ctx* m, double* x, const double* b, int pre, int post, double omega, int restart,
+                                double rtol, int maxit, int* iters, double* hist) {
+    using namespace rav;
+    if (!m || !x || !b || restart < 1 || restart > 200 || maxit < 0 || pre < 0 || post < 0) {
+        set_error("mg_fgmres: bad argument");
+        return RAV_ERR_ARG;
+    }
+    if (!is_device_ptr(x) || !is_device_ptr(b)) { set_error("mg_fgmres: x and b must be device pointers"); return RAV_ERR_ARG; }
+    g_launches = 0;
+    cudaStream_t s = m->stream;
+    mg_level& F = m->lv[m->L - 1];
+    const int64_t n = F.A.n_rows;
+    RAV_TRY(kry_alloc(m, restart, n));
+    const int M = restart;
+    double* V = m->kV;
+    double* Z = m->kZ;
+    double* hd = m->kh;                       // [0, M+1): pass-1 dots, [M+1, 2M+2): pass-2 dots, [2M+2]: norm
+    std::vector<double> H((size_t)(M + 1) * M), cs(M), sn(M), g(M + 1), hh(2 * (M + 1) + 1), y(M);
+    RAV_TRY(launch_residual(F.A, x, b, m->kr, s));
+    double beta = 0.0;
+    RAV_TRY(kry_norm(m, m->kr, n, hd + 2 * M + 2, &beta));
+    const double r0 = beta;
+    if (hist) hist[0] = r0;
+    int k = 0;
+    rav_status st = RAV_OK;
+    if (!(r0 == r0) || isinf(r0)) st = RAV_ERR_DIVERGED;
+    bool done = r0 == 0.0;
+    while (st == RAV_OK && !done && k < maxit) {
+        RAV_TRY(launch_scale(n, m->kr, 1.0 / beta, V, s));
+        std::fill(H.begin(), H.end(), 0.0);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int j = 0, jn = 0;
+        for (j = 0; j < M; ++j) {
+            double* vj = V + (size_t)j * n;
+            double* zj = Z + (size_t)j * n;
+            RAV_CUDA(cudaMemsetAsync(zj, 0, sizeof(double) * n, s));
+            if (m->L == 1) RAV_TRY(launch_coarse_solve(m->C, vj, zj, s));
+            else RAV_TRY(vcycle_launches(m, m->L - 1, zj, vj, pre, post, omega));   // z_j = M^{-1} v_j
+            RAV_TRY(launch_spmv(F.A, zj, m->kw, 1.0, 0.0, s));                        // w = L z_j
+            for (int pass = 0; pass < 2; ++pass) {                                    // CGS2
+                double* hp = hd + pass * (M + 1);
+                for (int i = 0; i <= j; ++i)
+                    RAV_TRY(launch_dot(V + (size_t)i * n, m->kw, n, m->kpart, residual_norm_blocks(), hp + i, 0, s));
+                RAV_TRY(launch_multi_axpy(n, j + 1, V, n, hp, -1.0, m->kw, s));
+            }
+            RAV_TRY(launch_dot(m->kw, m->kw, n, m->kpart, residual_norm_blocks(), hd + 2 * M + 2, 0, s));
+            RAV_CUDA(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * (2 * (M + 1) + 1), cudaMemcpyDeviceToHost, s));
+            RAV_CUDA(cudaStreamSynchronize(s));
+            for (int i = 0; i <= j; ++i) H[(size_t)i * M + j] = hh[i] + hh[M + 1 + i];
+            const double hn = sqrt(hh[2 * M + 2]);
+            H[(size_t)(j + 1) * M + j] = hn;
+            for (int i = 0; i < j; ++i) {   // previous Givens rotations
+                const double a = H[(size_t)i * M + j], c = H[(size_t)(i + 1) * M + j];
+                H[(size_t)i * M + j] = cs[i] * a + sn[i] * c;
+                H[(size_t)(i + 1) * M + j] = -sn[i] * a + cs[i] * c;
+            }
+            const double a = H[(size_t)j * M + j], c = H[(size_t)(j + 1) * M + j];
+            const double rr = hypot(a, c);
+            cs[j] = rr > 0.0 ? a / rr : 1.0;
+            sn[j] = rr > 0.0 ? c / rr : 0.0;
+            H[(size_t)j * M + j] = rr;
+            H[(size_t)(j + 1) * M + j] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            const double res = fabs(g[j + 1]);
+            ++k;
+            if (hist) hist[k] = res;
+            jn = j + 1;
+            if (!(res == res) || isinf(res)) { set_error("mg_fgmres: residual is not finite at step %d", k); st = RAV_ERR_DIVERGED; break; }
+            if (res <= rtol * r0 || k >= maxit || hn == 0.0) { done = true; break; }
+            RAV_TRY(launch_scale(n, m->kw, 1.0 / hn, V + (size_t)(j + 1) * n, s));
+        }
+        if (st != RAV_OK) break;
+        // y = H^{-1} g (upper triangular, jn x jn); x += Z y
+        for (int i = jn - 1; i >= 0; --i) {
+            double t = g[i];
+            for (int q = i + 1; q < jn; ++q) t -= H[(size_t)i * M + q] * y[q];
+            y[i] = t / H[(size_t)i * M + i];
+        }
+        RAV_CUDA(cudaMemcpyAsync(hd, y.data(), sizeof(double) * jn, cudaMemcpyHostToDevice, s));
+        RAV_TRY(launch_multi_axpy(n, jn, Z, n, hd, 1.0, x, s));
+        RAV_TRY(launch_residual(F.A, x, b, m->kr, s));
+        RAV_TRY(kry_norm(m, m->kr, n, hd + 2 * M + 2, &beta));
+    }
+    if (iters) *iters = k;
+    m->last_launches = g_launches;
+    return st;
+}

@@ -68,6 +68,10 @@ int residual_norm_blocks();
 // *out (device) = sum_i a[i] b[i] (+ *out if accumulate), deterministic (part: >= nblk doubles)
 rav_status launch_dot(const double* a, const double* b, int64_t n, double* part, int nblk, double* out,
                       int accumulate, cudaStream_t s);
+// w += alpha * sum_i coef[i] V[i * ld + .] (coef: device, nv entries); dst = s * src
+rav_status launch_multi_axpy(int64_t n, int nv, const double* V, int64_t ld, const double* coef, double alpha,
+                             double* w, cudaStream_t s);
+rav_status launch_scale(int64_t n, const double* src, double sc, double* dst, cudaStream_t s);
 
 // ---- setup.cu -------------------------------------------------------------------------
 struct PatchSet {

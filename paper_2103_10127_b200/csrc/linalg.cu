@@ -213,6 +213,41 @@ rav_status launch_dot(const double* a, const double* b, int64_t n, double* part,
     return RAV_OK;
 }
 
+// w[k] += alpha * sum_{i < nv} coef[i] * V[i * ld + k]   (coef on the device; Krylov updates)
+__global__ void __launch_bounds__(256) multi_axpy_kernel(int64_t n, int nv, const double* __restrict__ V, int64_t ld,
+                                                         const double* __restrict__ coef, double alpha,
+                                                         double* __restrict__ w) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int i = 0; i < nv; ++i) s = fma(coef[i], V[i * ld + k], s);
+        w[k] = fma(alpha, s, w[k]);
+    }
+}
+
+__global__ void scale_kernel(int64_t n, const double* __restrict__ src, double s, double* __restrict__ dst) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        dst[k] = s * src[k];
+}
+
+rav_status launch_multi_axpy(int64_t n, int nv, const double* V, int64_t ld, const double* coef, double alpha,
+                             double* w, cudaStream_t s) {
+    if (n == 0 || nv == 0) return RAV_OK;
+    const int blocks = (int)std::min<int64_t>(cdiv(n, 256), (int64_t)num_sms() * 8);
+    multi_axpy_kernel<<<blocks, 256, 0, s>>>(n, nv, V, ld, coef, alpha, w);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}
+
+rav_status launch_scale(int64_t n, const double* src, double sc, double* dst, cudaStream_t s) {
+    if (n == 0) return RAV_OK;
+    const int blocks = (int)std::min<int64_t>(cdiv(n, 256), (int64_t)num_sms() * 8);
+    scale_kernel<<<blocks, 256, 0, s>>>(n, src, sc, dst);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}
+
 // pack / unpack for the slab exchanges
 __global__ void index_op_kernel(int op, const double* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
                                 double* __restrict__ dst, double value) {

@@ -96,6 +96,7 @@ def _load():
         "rav_restrict": [vp, vp, vp],
         "rav_xfer_set_stream": [vp, vp],
         "rav_dot": [vp, vp, i64, vp, C.c_int, vp],
+        "mg_fgmres": [vp, vp, vp, C.c_int, C.c_int, dbl, C.c_int, dbl, C.c_int, P(C.c_int), vp],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -340,6 +341,14 @@ class Multigrid:
         st = lib.mg_solve(self.ctx, _ptr(x), _ptr(b), int(pre), int(post), float(omega), float(rtol), int(maxit),
                           C.byref(it), hist.ctypes.data)
         _check(st)
+        return x, it.value, hist[:it.value + 1]
+
+    def fgmres(self, x, b, pre=2, post=2, omega=0.66, restart=30, rtol=1e-8, maxit=200):
+        """mg_fgmres: FGMRES(restart) preconditioned by one V-cycle (R19)."""
+        hist = np.zeros(maxit + 1)
+        it = C.c_int(0)
+        _check(lib.mg_fgmres(self.ctx, _ptr(x), _ptr(b), int(pre), int(post), float(omega), int(restart),
+                             float(rtol), int(maxit), C.byref(it), hist.ctypes.data))
         return x, it.value, hist[:it.value + 1]
 
     @property
