@@ -167,7 +167,11 @@ __global__ void nb_fill_kernel(int64_t n, int64_t nnodes, int64_t nslices, int D
     }
 }
 
-template <int D>
+// G lanes per block row (G = 1: one thread per row; G > 1 for the long rows of 3D): a warp
+// covers 32/G consecutive slots of one slice, lane q of a group takes entries q, q+G, ...
+// of its row (for a fixed k the 32/G rows of the warp are contiguous, so every 32-byte
+// sector is fully used), then the group sums by shuffles.
+template <int D, int G, int UA>
 __global__ void __launch_bounds__(256) nb_residual_kernel(int64_t n, int64_t nnodes, int64_t nslices, int64_t nvel,
                                                           const int32_t* __restrict__ perm,
                                                           const int32_t* __restrict__ wa,
@@ -180,55 +184,109 @@ __global__ void __launch_bounds__(256) nb_residual_kernel(int64_t n, int64_t nno
                                                           double* __restrict__ part) {
     __shared__ double red[8];
     double mine = 0.0;
-    const int64_t total = nslices * NB_C;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - threadIdx.x < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        if (t >= total) continue;
+    const int64_t total = nslices * NB_C * G;
+    const int q = threadIdx.x % G;
+    for (int64_t tt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; tt - threadIdx.x < total;
+         tt += (int64_t)gridDim.x * blockDim.x) {
+        const bool live = tt < total;
+        const int64_t t = live ? tt / G : 0;       // slot
         const int64_t s = t / NB_C;
         const int l = (int)(t % NB_C);
-        const int A = wa[s], B = wb[s];
-        const int32_t* cA = col + cptr[s] + l;
+        const int A = live ? wa[s] : 0, B = live ? wb[s] : 0;
+        const int32_t* cA = col + (live ? cptr[s] : 0) + l;
         const int32_t* cB = cA + (int64_t)A * NB_C;
-        const double* vA = v + vptr[s] + l;
+        const double* vA = v + (live ? vptr[s] : 0) + l;
         const double* vB = vA + (int64_t)A * NB_C;
-        const int64_t br = t < n ? perm[t] : -1;
-        if (br < 0) continue;
-        if (br < nnodes) {
-            double acc[D];
+        const int64_t br = (live && t < n) ? perm[t] : -1;
+        if constexpr (G == 1) {   // one thread per row: per-branch accumulation (no shuffles)
+            if (br < 0) continue;
+            if (br < nnodes) {
+                double acc[D];
 #pragma unroll
-            for (int c = 0; c < D; ++c) acc[c] = 0.0;
-#pragma unroll 4
-            for (int k = 0; k < A; ++k) {
+                for (int c = 0; c < D; ++c) acc[c] = 0.0;
+#pragma unroll UA
+                for (int k = 0; k < A; ++k) {
+                    const int cc = __ldcs(cA + k * NB_C);
+                    const double a = __ldcs(vA + k * NB_C);
+#pragma unroll
+                    for (int c = 0; c < D; ++c) acc[c] = fma(a, __ldg(x + cc + c), acc[c]);
+                }
+#pragma unroll 2
+                for (int k = 0; k < B; ++k) {
+                    const double xp = __ldg(x + __ldcs(cB + k * NB_C));
+#pragma unroll
+                    for (int c = 0; c < D; ++c) acc[c] = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), xp, acc[c]);
+                }
+                const int64_t r0 = br * D;
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    const double rr = b[r0 + c] - acc[c];
+                    if (r) r[r0 + c] = rr;
+                    mine += rr * rr;
+                }
+            } else {
+                double acc = 0.0;
+#pragma unroll UA
+                for (int k = 0; k < B; ++k) {
+                    const int cc = __ldcs(cB + k * NB_C);
+#pragma unroll
+                    for (int c = 0; c < D; ++c) acc = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), __ldg(x + cc + c), acc);
+                }
+                const int64_t row = nvel + (br - nnodes);
+                const double rr = b[row] - acc;
+                if (r) r[row] = rr;
+                mine += rr * rr;
+            }
+            continue;
+        }
+        // the lanes of a group share the row, but a warp may hold node and pressure rows: the group
+        // sums run outside the branches with every lane converged (full-mask shuffles)
+        double acc[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc[c] = 0.0;
+        if (br >= 0 && br < nnodes) {
+#pragma unroll UA
+            for (int k = q; k < A; k += G) {
                 const int cc = __ldcs(cA + k * NB_C);
                 const double a = __ldcs(vA + k * NB_C);
 #pragma unroll
                 for (int c = 0; c < D; ++c) acc[c] = fma(a, __ldg(x + cc + c), acc[c]);
             }
 #pragma unroll 2
-            for (int k = 0; k < B; ++k) {
+            for (int k = q; k < B; k += G) {
                 const double xp = __ldg(x + __ldcs(cB + k * NB_C));
 #pragma unroll
                 for (int c = 0; c < D; ++c) acc[c] = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), xp, acc[c]);
             }
-            const int64_t r0 = br * D;
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-                const double rr = b[r0 + c] - acc[c];
-                if (r) r[r0 + c] = rr;
-                mine += rr * rr;
-            }
-        } else {
-            double acc = 0.0;
-#pragma unroll 4
-            for (int k = 0; k < B; ++k) {
+        } else if (br >= 0) {
+#pragma unroll UA
+            for (int k = q; k < B; k += G) {
                 const int cc = __ldcs(cB + k * NB_C);
 #pragma unroll
-                for (int c = 0; c < D; ++c) acc = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), __ldg(x + cc + c), acc);
+                for (int c = 0; c < D; ++c)
+                    acc[0] = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), __ldg(x + cc + c), acc[0]);
             }
-            const int64_t row = nvel + (br - nnodes);
-            const double rr = b[row] - acc;
-            if (r) r[row] = rr;
-            mine += rr * rr;
+        }
+        if (G > 1) {
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[c] = group_sum<G>(acc[c]);
+        }
+        if (q == 0 && br >= 0) {
+            if (br < nnodes) {
+                const int64_t r0 = br * D;
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    const double rr = b[r0 + c] - acc[c];
+                    if (r) r[r0 + c] = rr;
+                    mine += rr * rr;
+                }
+            } else {
+                const int64_t row = nvel + (br - nnodes);
+                const double rr = b[row] - acc[0];
+                if (r) r[row] = rr;
+                mine += rr * rr;
+            }
         }
     }
     if (part) {
@@ -329,18 +387,34 @@ void nb_free(NodeBlocked& N) {
     N = NodeBlocked{};
 }
 
+template <int D, int G, int UA>
+static void nb_launch(const NodeBlocked& N, const double* x, const double* b, double* r, double* part, int nblk,
+                      cudaStream_t s) {
+    const int64_t total = N.nslices * NB_C * G;
+    int blocks = (int)cdiv(total, 256);
+    if (part) blocks = nblk;
+    nb_residual_kernel<D, G, UA><<<blocks, 256, 0, s>>>(N.nblock, N.nnodes, N.nslices, N.nvel, N.perm, N.wa, N.wb,
+                                                        N.cptr, N.vptr, N.col, N.val, x, b, r, part);
+}
+
 rav_status launch_nb_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
                               cudaStream_t s) {
     const NodeBlocked& N = A.nb;
-    const int64_t total = N.nslices * NB_C;
-    int blocks = (int)cdiv(total, 256);
-    if (part) blocks = nblk;
-    if (N.D == 3)
-        nb_residual_kernel<3><<<blocks, 256, 0, s>>>(N.nblock, N.nnodes, N.nslices, N.nvel, N.perm, N.wa, N.wb, N.cptr,
-                                                     N.vptr, N.col, N.val, x, b, r, part);
-    else
-        nb_residual_kernel<2><<<blocks, 256, 0, s>>>(N.nblock, N.nnodes, N.nslices, N.nvel, N.perm, N.wa, N.wb, N.cptr,
-                                                     N.vptr, N.col, N.val, x, b, r, part);
+    static const int genv = [] {
+        const char* e = getenv("RAV_NB_LANES");   // lanes per block row (0: by dimension)
+        return e ? atoi(e) : 0;
+    }();
+    const int G = genv > 0 ? genv : (N.D == 3 ? 2 : 1);   // measured: 3D c4 98 us (G=2) vs 110 (G=1), 111 (G=4)
+    if (N.D == 3) {
+        if (G >= 8) nb_launch<3, 8, 4>(N, x, b, r, part, nblk, s);
+        else if (G >= 4) nb_launch<3, 4, 4>(N, x, b, r, part, nblk, s);
+        else if (G >= 2) nb_launch<3, 2, 4>(N, x, b, r, part, nblk, s);
+        else nb_launch<3, 1, 8>(N, x, b, r, part, nblk, s);
+    } else {
+        if (G >= 4) nb_launch<2, 4, 4>(N, x, b, r, part, nblk, s);
+        else if (G >= 2) nb_launch<2, 2, 4>(N, x, b, r, part, nblk, s);
+        else nb_launch<2, 1, 4>(N, x, b, r, part, nblk, s);
+    }
     count_launch();
     RAV_CHECK_LAUNCH();
     return RAV_OK;
