@@ -410,6 +410,65 @@ def run_dist_vcycle(name, rdist, si, stream, dist, ws, rank):
     return out
 
 
+def run_dist_c5(rdist, rg, si, stream, dist, ws, rank):
+    """BASELINE config 5 at N GPUs (weak scaling): 2048^2 Q2-Q1 per GPU stacked in
+    y, slab-partitioned; 50 sweeps each of RAV (omega 0.66), diagonal Vanka
+    (omega 0.1) and multicoloured MV (omega 0.66) from the seeded N(0,1) guess,
+    every sweep with its interface exchanges over NCCL (MV: one exchange pair per
+    colour).  Device time (CUDA events), max over ranks; MDoF/s over all GPUs."""
+    import torch
+    prob = si.config_problem("c5", scale_y=ws)
+    out = {"config": f"c5 weak scaling: 2048 x {2048 * ws} Q2-Q1 MMS on [0,1]x[0,{ws}], seeded eta, "
+                     f"slab-partitioned over {ws} GPUs, 50 sweeps from seeded N(0,1)"}
+    comm = rdist.TorchComm()
+    for name, weights, variant, omega in (("rav", "pou", rg.VARIANT_ROWS, 0.66),
+                                          ("diag_vanka", "full", rg.VARIANT_DIAG, 0.1),
+                                          ("mv_color", "full", rg.VARIANT_MV, 0.66)):
+        try:
+            slab = rdist.Slab(prob, ws, rank)
+            L = rg.gen_level(slab.local_problem(), weights)
+            sm = rg.Smoother(L, L, variant=variant)
+            be = rdist.GpuBackend(sm, stream)
+            written = rdist.written_local_from_patches(L)
+            if variant == rg.VARIANT_MV:
+                offs, ids = rdist.local_colors(slab)
+                sm.set_colors(offs, ids)
+                sw = rdist.DistMVSweeper(slab, be, comm, written, len(offs) - 1)
+            else:
+                sw = rdist.DistSweeper(slab, be, comm, written)
+            nglob = slab.nvel_glob + slab.nvert_glob
+            x0 = torch.tensor(si.initial_guess(nglob, seed=si.X0_SEED)[slab.global_ids()], device="cuda")
+            b = L["b"]
+
+            def rnorm(xv):
+                r = sm.residual(xv, b)
+                s = be.dot_owned(r, slab.owned_ranges())
+                dist.all_reduce(s)
+                return float(s.item()) ** 0.5
+            r0 = rnorm(x0)
+            x = x0.clone()
+            sw.smooth(x, b, 2, omega)      # warm
+            x = x0.clone()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sw.smooth(x, b, 50, omega)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / 50], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            out[name] = {"ms_per_sweep": ms, "mdofs": nglob / (ms * 1e-3) / 1e6, "omega": omega,
+                         "residual_reduction_50": rnorm(x) / r0, "kernel": sm.kernel_name}
+            sm.close()
+            del sm, L, sw, be, x, x0, b
+            torch.cuda.empty_cache()
+        except Exception as err:  # report, keep the line
+            out[name] = {"error": f"{type(err).__name__}: {err}"[:200]}
+    return out
+
+
 def run_gpu_dist(args):
     """N > 1 (torchrun): weak scaling of the c2 workload, one 512^2 block per GPU
     stacked along y (BASELINE config 5's layout): the finest level is
@@ -514,9 +573,11 @@ def run_gpu_dist(args):
         "gpu_launches": kernels_per_sweep * SWEEPS_PER_STEP * args.steps,
         "clocks": clk.summary(),
     }
+    del sw, sm, L
+    torch.cuda.empty_cache()
+    if not args.no_smoothers:
+        line["c5_smoothers"] = run_dist_c5(rdist, rg, si, stream, dist, ws, rank)
     if not args.no_vcycle:
-        del sw, sm, L
-        torch.cuda.empty_cache()
         vc = {}
         for name in ("c3", "c4"):
             try:

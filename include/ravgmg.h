@@ -247,6 +247,13 @@ rav_status rav_sweep_bytes(const rav_ctx* ctx, double* bytes_sweep, double* byte
  * 1, ...; patch_ids must be a permutation of 0..n_patches-1.  Copied. */
 rav_status rav_set_colors(rav_ctx* ctx, int n_colors, const int64_t* color_offs, const int32_t* patch_ids);
 
+/* One colour of multiplicative Vanka (RAV_VARIANT_MV after rav_set_colors): every
+ * patch of colour `color` relaxes concurrently with a fresh local residual
+ * (Eq. 15) and x += omega L_i^{-1} r_i on all its DoFs (Eq. 11).  Device
+ * pointers.  rav_smooth runs all colours in order; this entry point lets a
+ * multi-rank driver exchange interface values between colours. */
+rav_status rav_apply_color(rav_ctx* ctx, int color, double* x, const double* b, double omega);
+
 /* Name of the sweep kernel / factor format chosen by rav_setup (static string). */
 const char* rav_kernel_name(const rav_ctx* ctx);
 
@@ -307,7 +314,8 @@ rav_status mg_fgmres(mg_ctx* ctx, double* x, const double* b, int pre, int post,
  *                                       1 scatter dst[idx[k]] = src[k]
  *                                       2 scatter-add dst[idx[k]] += src[k]
  *                                         (indices unique within one call)
- *                                       3 fill dst[idx[k]] = value (src unused) */
+ *                                       3 fill dst[idx[k]] = value (src unused)
+ *                                       4 gather-difference dst[k] = src[idx[k]] - dst[k] */
 rav_status rav_index_op(int op, const double* src, const int32_t* idx, int64_t n, double* dst, double value,
                         void* stream);
 

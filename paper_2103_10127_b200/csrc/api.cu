@@ -228,6 +228,20 @@ rav_status rav_set_colors(rav_ctx* c, int n_colors, const int64_t* color_offs, c
     return RAV_OK;
 }
 
+rav_status rav_apply_color(rav_ctx* c, int color, double* x, const double* b, double omega) {
+    if (!c || !x || !b) { set_error("rav_apply_color: NULL argument"); return RAV_ERR_ARG; }
+    if (c->variant != RAV_VARIANT_MV || c->coffs.empty()) {
+        set_error("rav_apply_color: needs RAV_VARIANT_MV and rav_set_colors");
+        return RAV_ERR_ARG;
+    }
+    if (color < 0 || color + 1 >= (int)c->coffs.size()) { set_error("rav_apply_color: bad colour"); return RAV_ERR_ARG; }
+    g_launches = 0;
+    RAV_TRY(launch_mv_color(c->A, c->F, c->coffs[color + 1] - c->coffs[color], c->plist + c->coffs[color], b, x, omega,
+                            c->stream));
+    c->last_launches = g_launches;
+    return RAV_OK;
+}
+
 rav_status rav_set_stream(rav_ctx* c, void* stream) {
     if (!c) { set_error("NULL ctx"); return RAV_ERR_ARG; }
     if (c->stream != as_stream(stream)) c->graph.reset();

@@ -256,6 +256,7 @@ __global__ void index_op_kernel(int op, const double* __restrict__ src, const in
         if (op == 0) dst[k] = src[i];
         else if (op == 1) dst[i] = src[k];
         else if (op == 2) dst[i] += src[k];
+        else if (op == 4) dst[k] = src[i] - dst[k];
         else dst[i] = value;
     }
 }
@@ -389,7 +390,7 @@ rav_status csr_transpose(const Csr& A, Csr& At, cudaStream_t s) {
 extern "C" rav_status rav_index_op(int op, const double* src, const int32_t* idx, int64_t n, double* dst,
                                    double value, void* stream) {
     using namespace rav;
-    if (op < 0 || op > 3 || n < 0 || (n > 0 && (!idx || !dst || (op != 3 && !src)))) {
+    if (op < 0 || op > 4 || n < 0 || (n > 0 && (!idx || !dst || (op != 3 && !src)))) {
         set_error("rav_index_op: bad argument");
         return RAV_ERR_ARG;
     }

@@ -254,6 +254,59 @@ class DistSweeper:
             be.scatter_add(self.hs_buf[q], idx, v)
 
 
+def local_colors(slab: Slab) -> Tuple[np.ndarray, np.ndarray]:
+    """4^d colouring (R10) of this rank's patches by GLOBAL vertex coordinates,
+    so every rank relaxes the same colour at the same time: colour (i mod 4) +
+    4 (j mod 4) [+ 16 (k mod 4)], local patches ascending inside each colour.
+    Returns (offs[4^d + 1], local patch ids)."""
+    dim = slab.dim
+    nc = [int(c) for c in slab.problem["ncell"][:dim]]
+    nv = [c + 1 for c in nc]
+    gid = slab.nlow_vert * slab.V0 + np.arange(slab.n_patches)
+    color = np.zeros(slab.n_patches, np.int64)
+    r, mult = gid.copy(), 1
+    for k in range(dim):
+        color += (r % nv[k]) % 4 * mult
+        r //= nv[k]
+        mult *= 4
+    ids = np.argsort(color, kind="stable").astype(np.int32)
+    offs = np.zeros(4 ** dim + 1, np.int64)
+    offs[1:] = np.cumsum(np.bincount(color, minlength=4 ** dim))
+    return offs, ids
+
+
+class DistMVSweeper(DistSweeper):
+    """Slab-partitioned multiplicative Vanka in colours (Eq. 11, R10).
+
+    Per colour every rank relaxes its patches of that colour (fresh local
+    residuals, Eq. 15, full prolongation).  Same-colour patches share no
+    DoF and are not coupled through L (vertex spacing >= 4), also across ranks,
+    so a DoF is changed by at most one patch per colour: the rank that changed
+    a ghost DoF sends its change (new - old) to the owner, which adds it; then
+    a halo refresh makes the next colour see current values.  The result equals
+    the sequential MV sweep in colour-major order (single-domain oracle).
+
+    backend additionally: apply_color(c, x, b, omega), gather_diff(src, idx, buf)
+    (buf[k] = src[idx[k]] - buf[k])."""
+
+    def __init__(self, slab: Slab, backend, comm, written_local: np.ndarray, n_colors: int, all_infos=None):
+        super().__init__(slab, backend, comm, written_local, all_infos)
+        self.n_colors = n_colors
+
+    def sweep(self, x, b, omega: float):
+        be = self.be
+        for c in range(self.n_colors):
+            for q, idx in self.cs.items():
+                be.gather(x, idx, self.cs_buf[q])          # old values of ghost-written DoFs
+            be.apply_color(c, x, b, omega)
+            for q, idx in self.cs.items():
+                be.gather_diff(x, idx, self.cs_buf[q])     # their changes in this colour
+            self.comm.exchange(self.cs_buf, self.cr_buf)
+            for q, idx in self.cr.items():
+                be.scatter_add(self.cr_buf[q], idx, x)
+            self.halo(x)
+
+
 def nested_layers(fine_layers: Sequence[Tuple[int, int]]) -> List[Tuple[int, int]]:
     """Slab partition of the next coarser level (vertex layer 2c of the fine grid
     is vertex layer c of the coarse grid): interior cuts V -> ceil(V / 2).  With
@@ -496,6 +549,12 @@ class GpuBackend:
 
     def fill(self, dst, idx, value):
         self.rg.index_op(3, None, idx, dst, value=value, stream=self.stream)
+
+    def apply_color(self, c, x, b, omega):
+        self.sm.apply_color(c, x, b, omega)
+
+    def gather_diff(self, src, idx, buf):
+        self.rg.index_op(4, src, idx, buf, stream=self.stream)
 
     def restrict(self, xfer, r, bc):
         xfer.restrict(r, bc)

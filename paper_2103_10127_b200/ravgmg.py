@@ -84,6 +84,7 @@ def _load():
         "rav_sweep_bytes": [vp, P(dbl), P(dbl), P(dbl)],
         "rav_set_stream": [vp, vp],
         "rav_set_colors": [vp, C.c_int, vp, vp],
+        "rav_apply_color": [vp, C.c_int, vp, vp, dbl],
         "mg_set_colors": [vp, C.c_int, C.c_int, vp, vp],
         "rav_index_op": [C.c_int, vp, vp, i64, vp, dbl, vp],
         "mg_setup": [C.c_int, P(RavCsr), P(RavPatches), P(RavCsr), P(i64), i64, P(RavOpts), P(vp), P(C.c_int),
@@ -284,6 +285,11 @@ class Smoother:
         self._colors = (offs, ids)
         _check(lib.rav_set_colors(self.ctx, len(offs) - 1, offs.ctypes.data, ids.ctypes.data))
 
+    def apply_color(self, color: int, x, b, omega: float):
+        """One colour of multiplicative Vanka (rav_apply_color)."""
+        _check(lib.rav_apply_color(self.ctx, int(color), _ptr(x), _ptr(b), float(omega)))
+        return x
+
     def set_stream(self, stream):
         _check(lib.rav_set_stream(self.ctx, _stream(stream)))
 
@@ -409,7 +415,8 @@ def dot(a, b, out, accumulate: bool = False, n: Optional[int] = None, stream=Non
 
 def index_op(op: int, src, idx, dst, value: float = 0.0, stream=None):
     """rav_index_op: 0 gather dst[k] = src[idx[k]], 1 scatter dst[idx[k]] = src[k],
-    2 scatter-add, 3 fill dst[idx[k]] = value (device tensors)."""
+    2 scatter-add, 3 fill dst[idx[k]] = value, 4 gather-difference
+    dst[k] = src[idx[k]] - dst[k] (device tensors)."""
     n = idx.numel()
     _check(lib.rav_index_op(int(op), _ptr(src) if src is not None else None, _ptr(idx), int(n), _ptr(dst),
                             float(value), _stream(stream)))

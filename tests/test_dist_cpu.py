@@ -318,3 +318,111 @@ def test_level_plan_nesting():
     assert len(parts) == 5      # 257, 129, 65, 33, 17 layers over 4 ranks; 9 layers -> < 3 per rank
     _, parts8 = rdist.plan_levels(prob, 7, 4, agg_layers=8)
     assert len(parts8) == 4
+
+
+# ---------------------------------------------------------------------------------------------
+# comparison smoothers across ranks: multicoloured MV with
+# per-colour interface exchanges, additive diagonal Vanka through the additive protocol
+# ---------------------------------------------------------------------------------------------
+
+class NumpySmootherBackend(NumpyBackend):
+    """Local MV colours / diagonal-Vanka corrections from dense local systems of the
+    slab's local rows (plain numpy, written from Eqs. 11 / 12 and R17)."""
+
+    def __init__(self, slab, O, P, F, mode):
+        super().__init__(slab, O, P, F, None)
+        import scipy.sparse as sp
+        self.mode = mode
+        self.colors = rdist.local_colors(slab)
+        n = len(self.rp) - 1
+        self.Lloc = sp.csr_matrix((self.val, self.ci, self.rp), shape=(n, n))
+        is_vel = np.arange(n) < slab.nvel_loc
+        self.inv = []
+        for ld, _, _ in self.patches:
+            Li = self.Lloc[ld][:, ld].toarray()          # L_i = R_i L R_i^T (P:114)
+            if mode == "diag":                           # R17: velocity block -> its diagonal
+                v = is_vel[ld]
+                Li[np.ix_(v, v)] = np.diag(np.diag(Li)[v])
+            self.inv.append(np.linalg.inv(Li))
+
+    def apply_color(self, c, x, b, omega):
+        offs, ids = self.colors
+        xv, bv = x.numpy(), b.numpy()
+        for p in ids[offs[c]:offs[c + 1]]:
+            ld = self.patches[p][0]
+            r = bv[ld] - self.Lloc[ld] @ xv             # fresh local residual (P:221 Eq. 15)
+            xv[ld] += omega * (self.inv[p] @ r)
+
+    def gather_diff(self, src, idx, buf):
+        buf.numpy()[:] = src.numpy()[idx] - buf.numpy()
+
+    def apply(self, r, x, omega):       # additive diagonal Vanka, full prolongation (Eq. 12 with R17)
+        rv, xv = r.numpy(), x.numpy()
+        delta = np.zeros_like(xv)
+        for (ld, _, _), Mi in zip(self.patches, self.inv):
+            delta[ld] += Mi @ rv[ld]
+        xv += omega * delta
+
+
+def _smoother_worker(rank, world, port, prob, mode, nu, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        O = oracle.assemble(prob)
+        P = oracle.patches(prob, "full")
+        F = oracle.factor(O, P, oracle.FMT_ROWS)
+        slab = rdist.Slab(prob, world, rank)
+        be = NumpySmootherBackend(slab, O, P, F, mode)
+        comm = rdist.TorchComm()
+        if mode == "mv":
+            sw = rdist.DistMVSweeper(slab, be, comm, be.written, len(be.colors[0]) - 1)
+        else:
+            sw = rdist.DistSweeper(slab, be, comm, be.written)
+        x0 = si.initial_guess(O["n"], seed=23)
+        gids = slab.global_ids()
+        x = torch.tensor(x0[gids])
+        b = torch.tensor(be.b)
+        sw.smooth(x, b, nu, 0.66 if mode == "mv" else 0.1)
+        own = slab.owned_mask()
+        out_q.put((rank, gids[own], x.numpy()[own].copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+SMOOTHER_CASES = [
+    (si.problem(2, (10, 14), si.KIND_MMS, eta="fourier"), "mv", 2),
+    (si.problem(2, (9, 17), si.KIND_CAVITY, eta="fourier"), "mv", 3),
+    (si.problem(2, (8, 12), si.KIND_MMS, eta="fourier"), "diag", 2),
+    (si.problem(3, (3, 3, 8), si.KIND_CAVITY, eta="fourier"), "mv", 2),
+]
+
+
+@pytest.mark.parametrize("case", SMOOTHER_CASES, ids=["mv-w2", "mv-w3", "diag-w2", "mv-3d-w2"])
+def test_distributed_comparison_smoothers_match_oracle(case):
+    prob, mode, world = case
+    nu = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_smoother_worker, args=(r, world, port, prob, mode, nu, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    O = oracle.assemble(prob)
+    P = oracle.patches(prob, "full")
+    x0 = si.initial_guess(O["n"], seed=23)
+    if mode == "mv":
+        F = oracle.factor(O, P, oracle.FMT_LU)
+        xo = oracle.mv_sweeps(O, P, F, x0, O["b"], 0.66, nu, order=oracle.multicolor_order(prob))
+    else:
+        F = oracle.factor(O, P, oracle.FMT_DIAG)
+        xo = oracle.additive_sweeps(O, P, F, x0, O["b"], 0.1, nu)
+    xd = np.full(O["n"], np.nan)
+    for _, g, v in res:
+        xd[g] = v
+    assert not np.isnan(xd).any()
+    assert np.linalg.norm(xd - xo) <= 1e-12 * np.linalg.norm(xo)
