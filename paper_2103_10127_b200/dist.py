@@ -284,7 +284,7 @@ class DistMVSweeper(DistSweeper):
     so a DoF is changed by at most one patch per colour: the rank that changed
     a ghost DoF sends its change (new - old) to the owner, which adds it; then
     a halo refresh makes the next colour see current values.  The result equals
-    the sequential MV sweep in colour-major order (single-domain oracle).
+    the sequential single-domain MV sweep in colour-major order.
 
     backend additionally: apply_color(c, x, b, omega), gather_diff(src, idx, buf)
     (buf[k] = src[idx[k]] - buf[k])."""
