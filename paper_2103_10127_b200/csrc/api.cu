@@ -106,7 +106,10 @@ struct mg_ctx {
 
 namespace rav {
 
-static rav_status smooth_launches(rav_ctx* c, double* x, const double* b, int nu, double omega) {
+// r_ready: c->r already holds b - L x for the incoming x (the stopping test of mg_solve
+// computed it), so the first sweep skips its residual pass
+static rav_status smooth_launches(rav_ctx* c, double* x, const double* b, int nu, double omega,
+                                  bool r_ready = false) {
     for (int k = 0; k < nu; ++k) {
         if (c->variant == RAV_VARIANT_MV) {   // colour by colour, fresh local residuals (Eq. 11, 15)
             for (size_t q = 0; q + 1 < c->coffs.size(); ++q)
@@ -114,7 +117,7 @@ static rav_status smooth_launches(rav_ctx* c, double* x, const double* b, int nu
                                         omega, c->stream));
             continue;
         }
-        RAV_TRY(launch_residual(c->A, x, b, c->r, c->stream));
+        if (!(r_ready && k == 0)) RAV_TRY(launch_residual(c->A, x, b, c->r, c->stream));
         RAV_TRY(launch_sweep(c->P, c->F, c->r, x, omega, c->stream));
     }
     return RAV_OK;
@@ -483,13 +486,15 @@ rav_status mg_set_stream(mg_ctx* m, void* stream) {
 namespace rav {
 
 // V-cycle on level l (Fig. 1): x and b are the level's iterate / rhs
-static rav_status vcycle_launches(mg_ctx* m, int l, double* x, const double* b, int pre, int post, double omega) {
+static rav_status vcycle_launches(mg_ctx* m, int l, double* x, const double* b, int pre, int post, double omega,
+                                  bool r_ready = false) {
     cudaStream_t s = m->stream;
     if (l == 0) return launch_coarse_solve(m->C, b, x, s);
     mg_level& L = m->lv[l];
     mg_level& Lc = m->lv[l - 1];
-    RAV_TRY(smooth_launches(L.sm, x, b, pre, omega));
-    RAV_TRY(launch_residual(L.A, x, b, L.r, s));
+    RAV_TRY(smooth_launches(L.sm, x, b, pre, omega, r_ready));
+    if (pre == 0 && r_ready) RAV_CUDA(cudaMemcpyAsync(L.r, L.sm->r, sizeof(double) * L.A.n_rows, cudaMemcpyDeviceToDevice, s));
+    else RAV_TRY(launch_residual(L.A, x, b, L.r, s));
     RAV_TRY(launch_spmv(L.PT, L.r, Lc.b, 1.0, 0.0, s));       // b_{l-1} = P^T r_l
     if (l - 1 > 0) RAV_CUDA(cudaMemsetAsync(Lc.x, 0, sizeof(double) * Lc.A.n_rows, s));
     RAV_TRY(vcycle_launches(m, l - 1, Lc.x, Lc.b, pre, post, omega));
@@ -498,10 +503,16 @@ static rav_status vcycle_launches(mg_ctx* m, int l, double* x, const double* b, 
     return RAV_OK;
 }
 
+// one cycle whose first smoothing sweep reuses the residual of the previous stopping test,
+// then the stopping test's residual (kept in the smoother's r for the next cycle) + its norm
 static rav_status cycle_and_norm(mg_ctx* m, double* x, const double* b, int pre, int post, double omega) {
-    RAV_TRY(vcycle_launches(m, m->L - 1, x, b, pre, post, omega));
     mg_level& F = m->lv[m->L - 1];
-    RAV_TRY(launch_residual_norm2(F.A, x, b, m->part, residual_norm_blocks(), m->norm2, m->stream));
+    const bool reuse = F.sm && F.sm->variant != RAV_VARIANT_MV;
+    RAV_TRY(vcycle_launches(m, m->L - 1, x, b, pre, post, omega, reuse));
+    if (reuse)
+        RAV_TRY(launch_residual_and_norm2(F.A, x, b, F.sm->r, m->part, residual_norm_blocks(), m->norm2, m->stream));
+    else
+        RAV_TRY(launch_residual_norm2(F.A, x, b, m->part, residual_norm_blocks(), m->norm2, m->stream));
     RAV_CUDA(cudaMemcpyAsync(m->h_norm2, m->norm2, sizeof(double), cudaMemcpyDeviceToHost, m->stream));
     return RAV_OK;
 }
@@ -545,7 +556,10 @@ rav_status mg_solve(mg_ctx* m, double* x, const double* b, int pre, int post, do
         X = m->hx;
         B = m->hb;
     }
-    RAV_TRY(launch_residual_norm2(F.A, X, B, m->part, residual_norm_blocks(), m->norm2, s));
+    if (m->L > 1 && F.sm->variant != RAV_VARIANT_MV)   // r0 stays in the smoother's r for the first sweep
+        RAV_TRY(launch_residual_and_norm2(F.A, X, B, F.sm->r, m->part, residual_norm_blocks(), m->norm2, s));
+    else
+        RAV_TRY(launch_residual_norm2(F.A, X, B, m->part, residual_norm_blocks(), m->norm2, s));
     RAV_CUDA(cudaMemcpyAsync(m->h_norm2, m->norm2, sizeof(double), cudaMemcpyDeviceToHost, s));
     RAV_CUDA(cudaStreamSynchronize(s));
     total += g_launches;

@@ -65,6 +65,9 @@ rav_status launch_spmv(const Csr& A, const double* x, double* y, double alpha, d
 rav_status launch_residual_norm2(const Csr& A, const double* x, const double* b, double* part, int nblk,
                                  double* out, cudaStream_t s);
 int residual_norm_blocks();
+// r = b - A x and *out = ||r||^2 (one pass over A when the node-blocked / SELL copy exists)
+rav_status launch_residual_and_norm2(const Csr& A, const double* x, const double* b, double* r, double* part,
+                                     int nblk, double* out, cudaStream_t s);
 // *out (device) = sum_i a[i] b[i] (+ *out if accumulate), deterministic (part: >= nblk doubles)
 rav_status launch_dot(const double* a, const double* b, int64_t n, double* part, int nblk, double* out,
                       int accumulate, cudaStream_t s);

@@ -147,6 +147,21 @@ rav_status launch_spmv(const Csr& A, const double* x, double* y, double alpha, d
 
 int residual_norm_blocks() { return num_sms() * 4; }
 
+// r = b - A x and *out = ||r||^2 in one pass over A when a fused kernel exists (node-blocked / SELL)
+rav_status launch_residual_and_norm2(const Csr& A, const double* x, const double* b, double* r, double* part,
+                                     int nblk, double* out, cudaStream_t s) {
+    if (A.nb.nslices > 0 || A.sell.nslices > 0) {
+        if (A.nb.nslices > 0) RAV_TRY(launch_nb_residual(A, x, b, r, part, nblk, s));
+        else RAV_TRY(launch_sell_residual(A, x, b, r, part, nblk, s));
+        sum_parts_kernel<<<1, 256, 0, s>>>(part, nblk, out);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+        return RAV_OK;
+    }
+    RAV_TRY(launch_residual(A, x, b, r, s));
+    return launch_dot(r, r, A.n_rows, part, nblk, out, 0, s);
+}
+
 rav_status launch_residual_norm2(const Csr& A, const double* x, const double* b, double* part, int nblk,
                                  double* out, cudaStream_t s) {
     if (A.nb.nslices > 0 || A.sell.nslices > 0) {
