@@ -93,6 +93,7 @@ struct mg_ctx {
     CoarseLU C;
     cudaStream_t stream = nullptr;
     double* part = nullptr;     // residual-norm partials
+    int part_cap = 0;           // their number (full grid of the finest fused residual kernel)
     double* norm2 = nullptr;    // device scalar
     double* h_norm2 = nullptr;  // pinned host scalar
     double* hx = nullptr;
@@ -454,7 +455,10 @@ rav_status mg_setup(int n_levels, const rav_csr* A, const rav_patches* patches, 
         if (e != cudaSuccess) { set_error("mg_setup: %s", cudaGetErrorString(e)); st = RAV_ERR_OOM; }
     }
     if (st == RAV_OK) {
-        cudaError_t e = cudaMalloc(&m->part, sizeof(double) * residual_norm_blocks());
+        int64_t cap = residual_norm_blocks();
+        for (auto& L : m->lv) cap = std::max(cap, residual_part_capacity(L.A));
+        m->part_cap = (int)cap;
+        cudaError_t e = cudaMalloc(&m->part, sizeof(double) * cap);
         if (e == cudaSuccess) e = cudaMalloc(&m->norm2, sizeof(double));
         if (e == cudaSuccess) e = cudaMallocHost(&m->h_norm2, sizeof(double));
         if (e != cudaSuccess) { set_error("mg_setup: %s", cudaGetErrorString(e)); st = RAV_ERR_OOM; }
@@ -510,9 +514,9 @@ static rav_status cycle_and_norm(mg_ctx* m, double* x, const double* b, int pre,
     const bool reuse = F.sm && F.sm->variant != RAV_VARIANT_MV;
     RAV_TRY(vcycle_launches(m, m->L - 1, x, b, pre, post, omega, reuse));
     if (reuse)
-        RAV_TRY(launch_residual_and_norm2(F.A, x, b, F.sm->r, m->part, residual_norm_blocks(), m->norm2, m->stream));
+        RAV_TRY(launch_residual_and_norm2(F.A, x, b, F.sm->r, m->part, m->part_cap, m->norm2, m->stream));
     else
-        RAV_TRY(launch_residual_norm2(F.A, x, b, m->part, residual_norm_blocks(), m->norm2, m->stream));
+        RAV_TRY(launch_residual_norm2(F.A, x, b, m->part, m->part_cap, m->norm2, m->stream));
     RAV_CUDA(cudaMemcpyAsync(m->h_norm2, m->norm2, sizeof(double), cudaMemcpyDeviceToHost, m->stream));
     return RAV_OK;
 }
@@ -557,9 +561,9 @@ rav_status mg_solve(mg_ctx* m, double* x, const double* b, int pre, int post, do
         B = m->hb;
     }
     if (m->L > 1 && F.sm->variant != RAV_VARIANT_MV)   // r0 stays in the smoother's r for the first sweep
-        RAV_TRY(launch_residual_and_norm2(F.A, X, B, F.sm->r, m->part, residual_norm_blocks(), m->norm2, s));
+        RAV_TRY(launch_residual_and_norm2(F.A, X, B, F.sm->r, m->part, m->part_cap, m->norm2, s));
     else
-        RAV_TRY(launch_residual_norm2(F.A, X, B, m->part, residual_norm_blocks(), m->norm2, s));
+        RAV_TRY(launch_residual_norm2(F.A, X, B, m->part, m->part_cap, m->norm2, s));
     RAV_CUDA(cudaMemcpyAsync(m->h_norm2, m->norm2, sizeof(double), cudaMemcpyDeviceToHost, s));
     RAV_CUDA(cudaStreamSynchronize(s));
     total += g_launches;

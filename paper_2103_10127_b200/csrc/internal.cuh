@@ -47,11 +47,16 @@ rav_status sell_build(Csr& A, cudaStream_t s);
 void sell_free(Sell& S);
 rav_status nb_build(Csr& A, int64_t nvel, int D, cudaStream_t s);
 void nb_free(NodeBlocked& N);
+// r = b - A x via the node-blocked / SELL copy (r may be null); if part != nullptr also one partial sum
+// of r^2 per block, with min(full grid, nblk) blocks (*used = blocks launched)
 rav_status launch_nb_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
-                              cudaStream_t s);
-// r = b - A x via the SELL copy; if part != nullptr also per-block sums of r^2 (nblk blocks)
+                              cudaStream_t s, int* used = nullptr);
 rav_status launch_sell_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
-                                cudaStream_t s);
+                                cudaStream_t s, int* used = nullptr);
+int64_t nb_full_blocks(const NodeBlocked& N);
+int64_t sell_full_blocks(const Sell& S);
+// partial-sum capacity for which the fused residual-norm kernels run on their full grid
+int64_t residual_part_capacity(const Csr& A);
 
 rav_status csr_upload(const rav_csr* A, Csr& out, cudaStream_t s);
 void csr_free(Csr& A);

@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int64_t* __r
         double acc = 0.0;
         if (row < n) {
             const int64_t s = rp[row], e = rp[row + 1];
-            for (int64_t k = s + lane; k < e; k += G) acc += val[k] * __ldg(x + ci[k]);
+            for (int64_t k = s + lane; k < e; k += G) acc += ld_stream(val + k) * __ldg(x + ld_stream_i(ci + k));
         }
         acc = group_sum<G>(acc);
         if (lane == 0 && row < n) y[row] = (beta == 0.0 ? 0.0 : beta * y[row]) + alpha * acc;
@@ -133,13 +133,19 @@ rav_status launch_residual(const Csr& A, const double* x, const double* b, doubl
 
 rav_status launch_spmv(const Csr& A, const double* x, double* y, double alpha, double beta, cudaStream_t s) {
     if (A.n_rows == 0) return RAV_OK;
-    int nb = spmv_blocks(A.n_rows, A.lanes);
-    if (A.lanes == 32)
+    // transfers (P: 1-9 entries per row, R = P^T: up to ~25) are short-row matrices: lanes per row
+    // from the mean row length, one pass of the whole grid (no grid-stride cap)
+    const double mean = (double)A.nnz / (double)A.n_rows;
+    const int G = mean > 48.0 ? 32 : (mean > 12.0 ? 8 : (mean > 5.0 ? 4 : 2));
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(A.n_rows * G, 256), (int64_t)1 << 30));
+    if (G == 32)
         spmv_kernel<32><<<nb, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, y, alpha, beta);
-    else if (A.lanes == 16)
-        spmv_kernel<16><<<nb, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, y, alpha, beta);
-    else
+    else if (G == 8)
         spmv_kernel<8><<<nb, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, y, alpha, beta);
+    else if (G == 4)
+        spmv_kernel<4><<<nb, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, y, alpha, beta);
+    else
+        spmv_kernel<2><<<nb, 256, 0, s>>>(A.n_rows, A.rp, A.ci, A.val, x, y, alpha, beta);
     count_launch();
     RAV_CHECK_LAUNCH();
     return RAV_OK;
@@ -148,12 +154,20 @@ rav_status launch_spmv(const Csr& A, const double* x, double* y, double alpha, d
 int residual_norm_blocks() { return num_sms() * 4; }
 
 // r = b - A x and *out = ||r||^2 in one pass over A when a fused kernel exists (node-blocked / SELL)
+int64_t residual_part_capacity(const Csr& A) {
+    int64_t c = residual_norm_blocks();
+    if (A.nb.nslices > 0) c = std::max(c, nb_full_blocks(A.nb));
+    if (A.sell.nslices > 0) c = std::max(c, sell_full_blocks(A.sell));
+    return c;
+}
+
 rav_status launch_residual_and_norm2(const Csr& A, const double* x, const double* b, double* r, double* part,
                                      int nblk, double* out, cudaStream_t s) {
     if (A.nb.nslices > 0 || A.sell.nslices > 0) {
-        if (A.nb.nslices > 0) RAV_TRY(launch_nb_residual(A, x, b, r, part, nblk, s));
-        else RAV_TRY(launch_sell_residual(A, x, b, r, part, nblk, s));
-        sum_parts_kernel<<<1, 256, 0, s>>>(part, nblk, out);
+        int used = nblk;
+        if (A.nb.nslices > 0) RAV_TRY(launch_nb_residual(A, x, b, r, part, nblk, s, &used));
+        else RAV_TRY(launch_sell_residual(A, x, b, r, part, nblk, s, &used));
+        sum_parts_kernel<<<1, 256, 0, s>>>(part, used, out);
         count_launch();
         RAV_CHECK_LAUNCH();
         return RAV_OK;
@@ -165,9 +179,10 @@ rav_status launch_residual_and_norm2(const Csr& A, const double* x, const double
 rav_status launch_residual_norm2(const Csr& A, const double* x, const double* b, double* part, int nblk,
                                  double* out, cudaStream_t s) {
     if (A.nb.nslices > 0 || A.sell.nslices > 0) {
-        if (A.nb.nslices > 0) RAV_TRY(launch_nb_residual(A, x, b, nullptr, part, nblk, s));
-        else RAV_TRY(launch_sell_residual(A, x, b, nullptr, part, nblk, s));
-        sum_parts_kernel<<<1, 256, 0, s>>>(part, nblk, out);
+        int used = nblk;
+        if (A.nb.nslices > 0) RAV_TRY(launch_nb_residual(A, x, b, nullptr, part, nblk, s, &used));
+        else RAV_TRY(launch_sell_residual(A, x, b, nullptr, part, nblk, s, &used));
+        sum_parts_kernel<<<1, 256, 0, s>>>(part, used, out);
         count_launch();
         RAV_CHECK_LAUNCH();
         return RAV_OK;

@@ -389,31 +389,40 @@ void nb_free(NodeBlocked& N) {
 
 template <int D, int G, int UA>
 static void nb_launch(const NodeBlocked& N, const double* x, const double* b, double* r, double* part, int nblk,
-                      cudaStream_t s) {
-    const int64_t total = N.nslices * NB_C * G;
-    int blocks = (int)cdiv(total, 256);
-    if (part) blocks = nblk;
+                      cudaStream_t s, int* used) {
+    const int64_t full = cdiv(N.nslices * NB_C * G, 256);
+    // with partial norms: one partial per block, the full grid when the caller's buffer holds it
+    const int blocks = (int)(part ? std::min<int64_t>(full, nblk) : full);
+    if (used) *used = blocks;
     nb_residual_kernel<D, G, UA><<<blocks, 256, 0, s>>>(N.nblock, N.nnodes, N.nslices, N.nvel, N.perm, N.wa, N.wb,
                                                         N.cptr, N.vptr, N.col, N.val, x, b, r, part);
 }
 
-rav_status launch_nb_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
-                              cudaStream_t s) {
-    const NodeBlocked& N = A.nb;
+static int nb_lanes(const NodeBlocked& N) {
     static const int genv = [] {
         const char* e = getenv("RAV_NB_LANES");   // lanes per block row (0: by dimension)
         return e ? atoi(e) : 0;
     }();
-    const int G = genv > 0 ? genv : (N.D == 3 ? 2 : 1);   // measured: 3D c4 98 us (G=2) vs 110 (G=1), 111 (G=4)
+    // measured: 3D c4 98 us (G=2) vs 110 (G=1), 111 (G=4); 2D c2 G=1 best
+    const int G = genv > 0 ? genv : (N.D == 3 ? 2 : 1);
+    return G >= 8 ? 8 : (G >= 4 ? 4 : (G >= 2 ? 2 : 1));
+}
+
+int64_t nb_full_blocks(const NodeBlocked& N) { return cdiv(N.nslices * NB_C * nb_lanes(N), 256); }
+
+rav_status launch_nb_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
+                              cudaStream_t s, int* used) {
+    const NodeBlocked& N = A.nb;
+    const int G = nb_lanes(N);
     if (N.D == 3) {
-        if (G >= 8) nb_launch<3, 8, 4>(N, x, b, r, part, nblk, s);
-        else if (G >= 4) nb_launch<3, 4, 4>(N, x, b, r, part, nblk, s);
-        else if (G >= 2) nb_launch<3, 2, 4>(N, x, b, r, part, nblk, s);
-        else nb_launch<3, 1, 8>(N, x, b, r, part, nblk, s);
+        if (G == 8) nb_launch<3, 8, 4>(N, x, b, r, part, nblk, s, used);
+        else if (G == 4) nb_launch<3, 4, 4>(N, x, b, r, part, nblk, s, used);
+        else if (G == 2) nb_launch<3, 2, 4>(N, x, b, r, part, nblk, s, used);
+        else nb_launch<3, 1, 8>(N, x, b, r, part, nblk, s, used);
     } else {
-        if (G >= 4) nb_launch<2, 4, 4>(N, x, b, r, part, nblk, s);
-        else if (G >= 2) nb_launch<2, 2, 4>(N, x, b, r, part, nblk, s);
-        else nb_launch<2, 1, 4>(N, x, b, r, part, nblk, s);
+        if (G >= 4) nb_launch<2, 4, 4>(N, x, b, r, part, nblk, s, used);
+        else if (G == 2) nb_launch<2, 2, 4>(N, x, b, r, part, nblk, s, used);
+        else nb_launch<2, 1, 4>(N, x, b, r, part, nblk, s, used);
     }
     count_launch();
     RAV_CHECK_LAUNCH();

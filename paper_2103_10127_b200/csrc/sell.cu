@@ -179,12 +179,14 @@ void sell_free(Sell& S) {
     S = Sell{};
 }
 
+int64_t sell_full_blocks(const Sell& S) { return cdiv(S.nslices * SELL_C, SELL_THREADS); }
+
 rav_status launch_sell_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
-                                cudaStream_t s) {
+                                cudaStream_t s, int* used) {
     const Sell& S = A.sell;
-    const int64_t total = S.nslices * SELL_C;
-    int blocks = (int)cdiv(total, SELL_THREADS);
-    if (part) blocks = nblk;   // grid-stride with a fixed number of partial sums
+    const int64_t full = sell_full_blocks(S);
+    const int blocks = (int)(part ? std::min<int64_t>(full, nblk) : full);   // one partial norm per block
+    if (used) *used = blocks;
     sell_residual_kernel<<<blocks, SELL_THREADS, 0, s>>>(A.n_rows, S.nslices, S.sptr, S.col, S.val, S.perm, x, b, r,
                                                          part);
     count_launch();
