@@ -2,8 +2,10 @@
 // use LU factorization to solve the coarse system to machine accuracy").
 // The coarsest operator (<= a few hundred DoFs) is densified with DoF `pin`
 // removed (R4: the pressure null space is fixed only here), factored once by
-// Gaussian elimination with partial pivoting in one CTA, and every V-cycle
-// applies the row swaps and the two triangular solves in one warp.
+// Gaussian elimination with partial pivoting in one CTA; the inverse is formed
+// from the factors at setup (one warp per column) and every V-cycle applies it
+// as one dense mat-vec in one CTA (fallback above 2048 unknowns: the row swaps
+// and two triangular solves in one warp).
 #include <algorithm>
 
 #include "internal.cuh"
@@ -119,6 +121,56 @@ __global__ void coarse_solve_kernel(int64_t n, int64_t pin, int m, const double*
     }
 }
 
+// column w of A^{-1} from the LU factors (one warp per column; setup only)
+__global__ void coarse_inverse_kernel(int m, const double* __restrict__ LU, const int32_t* __restrict__ piv,
+                                      double* __restrict__ inv) {
+    extern __shared__ double ysh[];
+    const int w = blockIdx.x, lane = threadIdx.x;
+    double* y = ysh;
+    for (int i = lane; i < m; i += 32) y[i] = (i == w) ? 1.0 : 0.0;
+    __syncwarp();
+    if (lane == 0)
+        for (int k = 0; k < m; ++k) {
+            int p = piv[k];
+            if (p != k) { double u = y[k]; y[k] = y[p]; y[p] = u; }
+        }
+    __syncwarp();
+    for (int i = 0; i < m; ++i) {
+        double t = 0.0;
+        for (int j = lane; j < i; j += 32) t += LU[(size_t)i * m + j] * y[j];
+        t = warp_sum(t);
+        if (lane == 0) y[i] -= t;
+        __syncwarp();
+    }
+    for (int i = m - 1; i >= 0; --i) {
+        double t = 0.0;
+        for (int j = i + 1 + lane; j < m; j += 32) t += LU[(size_t)i * m + j] * y[j];
+        t = warp_sum(t);
+        if (lane == 0) y[i] = (y[i] - t) / LU[(size_t)i * m + i];
+        __syncwarp();
+    }
+    for (int i = lane; i < m; i += 32) inv[(size_t)i * m + w] = y[i];
+}
+
+// x = A^{-1} b with the precomputed inverse: one CTA, a warp per row, pinned DoF set to 0
+__global__ void __launch_bounds__(512) coarse_apply_kernel(int64_t n, int64_t pin, int m, const double* __restrict__ inv,
+                                                           const double* __restrict__ b, double* __restrict__ x) {
+    extern __shared__ double yb[];
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        if (i == pin) continue;
+        yb[(pin >= 0 && i > pin) ? i - 1 : i] = b[i];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int r = warp; r < m; r += nw) {
+        double t = 0.0;
+        for (int j = lane; j < m; j += 32) t = fma(inv[(size_t)r * m + j], yb[j], t);
+        t = warp_sum(t);
+        if (lane == 0) x[(pin >= 0 && r >= pin) ? r + 1 : r] = t;
+    }
+    if (pin >= 0 && threadIdx.x == 0) x[pin] = 0.0;
+}
+
 rav_status coarse_factor(const Csr& A, int64_t pin, CoarseLU& C, cudaStream_t s) {
     C.n = A.n_rows;
     C.pin = pin;
@@ -143,11 +195,21 @@ rav_status coarse_factor(const Csr& A, int64_t pin, CoarseLU& C, cudaStream_t s)
         set_error("singular coarsest system (column %d)", h_fail - 1);
         return RAV_ERR_SINGULAR_COARSE;
     }
+    // explicit inverse from the LU factors: every V-cycle's coarse solve becomes one dense
+    // mat-vec in one CTA (the per-cycle triangular solves were 2m dependent warp steps)
+    if (C.m <= 2048) {
+        RAV_CUDA(cudaMalloc(&C.inv, sizeof(double) * (size_t)C.m * C.m));
+        coarse_inverse_kernel<<<C.m, 32, sizeof(double) * C.m, s>>>(C.m, C.lu, C.piv, C.inv);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+        RAV_CUDA(cudaStreamSynchronize(s));
+    }
     return RAV_OK;
 }
 
 rav_status launch_coarse_solve(const CoarseLU& C, const double* b, double* x, cudaStream_t s) {
-    coarse_solve_kernel<<<1, 32, sizeof(double) * C.m, s>>>(C.n, C.pin, C.m, C.lu, C.piv, b, x);
+    if (C.inv) coarse_apply_kernel<<<1, 512, sizeof(double) * C.m, s>>>(C.n, C.pin, C.m, C.inv, b, x);
+    else coarse_solve_kernel<<<1, 32, sizeof(double) * C.m, s>>>(C.n, C.pin, C.m, C.lu, C.piv, b, x);
     count_launch();
     RAV_CHECK_LAUNCH();
     return RAV_OK;
@@ -156,6 +218,7 @@ rav_status launch_coarse_solve(const CoarseLU& C, const double* b, double* x, cu
 void coarse_free(CoarseLU& C) {
     if (C.lu) cudaFree(C.lu);
     if (C.piv) cudaFree(C.piv);
+    if (C.inv) cudaFree(C.inv);
     C = CoarseLU{};
 }
 

@@ -150,6 +150,7 @@ struct CoarseLU {
     int m = 0;
     double* lu = nullptr;      // m x m
     int32_t* piv = nullptr;
+    double* inv = nullptr;     // m x m explicit inverse (m <= 2048), row-major
 };
 rav_status coarse_factor(const Csr& A, int64_t pin, CoarseLU& C, cudaStream_t s);
 rav_status launch_coarse_solve(const CoarseLU& C, const double* b, double* x, cudaStream_t s);
