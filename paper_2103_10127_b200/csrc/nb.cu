@@ -403,9 +403,13 @@ static int nb_lanes(const NodeBlocked& N) {
         const char* e = getenv("RAV_NB_LANES");   // lanes per block row (0: by dimension)
         return e ? atoi(e) : 0;
     }();
-    // measured: 3D c4 98 us (G=2) vs 110 (G=1), 111 (G=4); 2D c2 G=1 best
-    const int G = genv > 0 ? genv : (N.D == 3 ? 2 : 1);
-    return G >= 8 ? 8 : (G >= 4 ? 4 : (G >= 2 ? 2 : 1));
+    // measured: 3D c4 98 us (G=2) vs 110 (G=1), 111 (G=4); 2D c2 G=1 best.  Small (coarse) levels
+    // cannot fill the GPU with one short group per row: their long rows get a full warp (latency)
+    const int G = genv > 0 ? genv
+                           : N.nblock < 8192 ? (N.D == 3 ? 32 : 8)
+                           : N.nblock < 131072 ? (N.D == 3 ? 8 : 2)
+                           : (N.D == 3 ? 2 : 1);
+    return G >= 32 ? 32 : (G >= 8 ? 8 : (G >= 4 ? 4 : (G >= 2 ? 2 : 1)));
 }
 
 int64_t nb_full_blocks(const NodeBlocked& N) { return cdiv(N.nslices * NB_C * nb_lanes(N), 256); }
@@ -415,12 +419,15 @@ rav_status launch_nb_residual(const Csr& A, const double* x, const double* b, do
     const NodeBlocked& N = A.nb;
     const int G = nb_lanes(N);
     if (N.D == 3) {
-        if (G == 8) nb_launch<3, 8, 4>(N, x, b, r, part, nblk, s, used);
+        if (G == 32) nb_launch<3, 32, 2>(N, x, b, r, part, nblk, s, used);
+        else if (G == 8) nb_launch<3, 8, 4>(N, x, b, r, part, nblk, s, used);
         else if (G == 4) nb_launch<3, 4, 4>(N, x, b, r, part, nblk, s, used);
         else if (G == 2) nb_launch<3, 2, 4>(N, x, b, r, part, nblk, s, used);
         else nb_launch<3, 1, 8>(N, x, b, r, part, nblk, s, used);
     } else {
-        if (G >= 4) nb_launch<2, 4, 4>(N, x, b, r, part, nblk, s, used);
+        if (G == 32) nb_launch<2, 32, 2>(N, x, b, r, part, nblk, s, used);
+        else if (G == 8) nb_launch<2, 8, 4>(N, x, b, r, part, nblk, s, used);
+        else if (G >= 4) nb_launch<2, 4, 4>(N, x, b, r, part, nblk, s, used);
         else if (G == 2) nb_launch<2, 2, 4>(N, x, b, r, part, nblk, s, used);
         else nb_launch<2, 1, 4>(N, x, b, r, part, nblk, s, used);
     }
