@@ -21,6 +21,14 @@ void set_error(const char* fmt, ...) {
 }
 const char* get_error() { return g_err; }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("RAV_PDL");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 int num_sms() {
     static int n = 0;
     if (n == 0) {

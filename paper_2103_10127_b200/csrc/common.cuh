@@ -4,6 +4,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string>
+#include <utility>
 
 #include "../../include/ravgmg.h"
 
@@ -42,6 +43,33 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // launch counter (kernels issued by the current API call; graph replays count their nodes)
 extern thread_local int64_t g_launches;
 inline void count_launch(int64_t k = 1) { g_launches += k; }
+
+// ---- programmatic dependent launch (PDL) ------------------------------------------
+// The hot-loop kernels (residual, RAV sweep) let their successor launch while their last
+// CTAs drain (griddepcontrol.launch_dependents at entry); the successor prefetches the
+// stream data that does not depend on its predecessor into L2, then waits
+// (griddepcontrol.wait: the predecessor has completed and its writes are visible).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_maybe_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---- device helpers -----------------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {

@@ -186,6 +186,18 @@ __global__ void __launch_bounds__(256) nb_residual_kernel(int64_t n, int64_t nno
     double mine = 0.0;
     const int64_t total = nslices * NB_C * G;
     const int q = threadIdx.x % G;
+    pdl_trigger();
+    if (G == 1) {   // before x exists: this warp's first slice lines (values, columns) into L2
+        const int64_t s0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / NB_C;
+        const int lane = threadIdx.x & 31;
+        if (s0 < nslices) {
+            const char* vb = reinterpret_cast<const char*>(v + vptr[s0]);
+            const char* cb = reinterpret_cast<const char*>(col + cptr[s0]);
+            if (lane < 16) prefetch_l2(vb + (size_t)lane * 128);
+            else prefetch_l2(cb + (size_t)(lane - 16) * 128);
+        }
+    }
+    pdl_wait();
     for (int64_t tt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; tt - threadIdx.x < total;
          tt += (int64_t)gridDim.x * blockDim.x) {
         const bool live = tt < total;
@@ -394,8 +406,10 @@ static void nb_launch(const NodeBlocked& N, const double* x, const double* b, do
     // with partial norms: one partial per block, the full grid when the caller's buffer holds it
     const int blocks = (int)(part ? std::min<int64_t>(full, nblk) : full);
     if (used) *used = blocks;
-    nb_residual_kernel<D, G, UA><<<blocks, 256, 0, s>>>(N.nblock, N.nnodes, N.nslices, N.nvel, N.perm, N.wa, N.wb,
-                                                        N.cptr, N.vptr, N.col, N.val, x, b, r, part);
+    launch_maybe_pdl(nb_residual_kernel<D, G, UA>, dim3(blocks), dim3(256), 0, s, N.nblock, N.nnodes, N.nslices,
+                     N.nvel, (const int32_t*)N.perm, (const int32_t*)N.wa, (const int32_t*)N.wb,
+                     (const int64_t*)N.cptr, (const int64_t*)N.vptr, (const int32_t*)N.col, (const double*)N.val, x, b,
+                     r, part);
 }
 
 static int nb_lanes(const NodeBlocked& N) {

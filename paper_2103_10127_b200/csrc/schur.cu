@@ -418,9 +418,18 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t chunk = i >> 5;
     const int lane = threadIdx.x & 31;
+    pdl_trigger();
     if (chunk >= nchunks) return;
     const double2* wp = W + chunk * pairs * 32 + lane;
     const int32_t* np_ = ND + chunk * (int64_t)NN * 32 + lane;
+    {   // before r exists: the chunk's node indices and first factor lines into L2
+        const char* wc = reinterpret_cast<const char*>(W + chunk * pairs * 32);
+        const char* nc = reinterpret_cast<const char*>(ND + chunk * (int64_t)NN * 32);
+        for (int ln = lane; ln < NN; ln += 32) prefetch_l2(nc + (size_t)ln * 128);
+        const int lines = (int)(pairs * 4 < 128 ? pairs * 4 : 128);
+        for (int ln = lane; ln < lines; ln += 32) prefetch_l2(wc + (size_t)ln * 128);
+    }
+    pdl_wait();
     // TMA prefetch of the rectangular column blocks into L2 (no registers / smem):
     // the first PF_AHEAD blocks now, block k + PF_AHEAD while block k is consumed
     constexpr int PF_AHEAD = 3;
@@ -1078,9 +1087,9 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
                                                                           reinterpret_cast<const double2*>(F.facT), F.DT,
                                                                           F.PD, F.NR, F.WT, r, x, omega, pf);
         else
-            schur_sweep_thread_kernel<MT, 2, 4, 8><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
-                                                                          reinterpret_cast<const double2*>(F.facT), F.DT,
-                                                                          F.PD, F.NR, F.WT, r, x, omega, pf);
+            launch_maybe_pdl(schur_sweep_thread_kernel<MT, 2, 4, 8>, dim3(blocks), dim3(128), 0, s, np, F.nchunks,
+                             F.NN, F.pairs, reinterpret_cast<const double2*>(F.facT), (const int32_t*)F.DT,
+                             (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, pf);
         return;
     }
     if (minb >= 6)
