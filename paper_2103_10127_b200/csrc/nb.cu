@@ -171,8 +171,8 @@ __global__ void nb_fill_kernel(int64_t n, int64_t nnodes, int64_t nslices, int D
 // covers 32/G consecutive slots of one slice, lane q of a group takes entries q, q+G, ...
 // of its row (for a fixed k the 32/G rows of the warp are contiguous, so every 32-byte
 // sector is fully used), then the group sums by shuffles.
-template <int D, int G, int UA>
-__global__ void __launch_bounds__(256) nb_residual_kernel(int64_t n, int64_t nnodes, int64_t nslices, int64_t nvel,
+template <int D, int G, int UA, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64_t nnodes, int64_t nslices, int64_t nvel,
                                                           const int32_t* __restrict__ perm,
                                                           const int32_t* __restrict__ wa,
                                                           const int32_t* __restrict__ wb,
@@ -406,7 +406,15 @@ static void nb_launch(const NodeBlocked& N, const double* x, const double* b, do
     // with partial norms: one partial per block, the full grid when the caller's buffer holds it
     const int blocks = (int)(part ? std::min<int64_t>(full, nblk) : full);
     if (used) *used = blocks;
-    launch_maybe_pdl(nb_residual_kernel<D, G, UA>, dim3(blocks), dim3(256), 0, s, N.nblock, N.nnodes, N.nslices,
+    static const int minb = [] {   // register cap of the one-thread-per-row variant (measured: 6 best, 102 vs 105 us)
+        const char* e = getenv("RAV_NB_MINB");
+        return e ? atoi(e) : 6;
+    }();
+    auto kern = (minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8>
+              : (minb == 7 && G == 1) ? nb_residual_kernel<D, G, UA, 7>
+              : (minb == 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6>
+              : (minb == 5 && G == 1) ? nb_residual_kernel<D, G, UA, 5> : nb_residual_kernel<D, G, UA, 1>;
+    launch_maybe_pdl(kern, dim3(blocks), dim3(256), 0, s, N.nblock, N.nnodes, N.nslices,
                      N.nvel, (const int32_t*)N.perm, (const int32_t*)N.wa, (const int32_t*)N.wb,
                      (const int64_t*)N.cptr, (const int64_t*)N.vptr, (const int32_t*)N.col, (const double*)N.val, x, b,
                      r, part);
