@@ -478,8 +478,15 @@ def run_gpu_dist(args):
     import torch
     import torch.distributed as dist
     ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # RAV_DIST_BACKEND=gloo + RAV_SINGLE_DEVICE=1: every rank on cuda:0 with host-staged exchanges --
+    # a functional check of this path on a one-GPU box, never a timed configuration
+    dev = 0 if os.environ.get("RAV_SINGLE_DEVICE") else local
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("RAV_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group(backend)
     from paper_2103_10127_b200 import dist as rdist
     from paper_2103_10127_b200 import ravgmg as rg
     import seeded_inputs as si
@@ -507,7 +514,7 @@ def run_gpu_dist(args):
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             sw.smooth(x, b, SWEEPS_PER_STEP, OMEGA)

@@ -425,12 +425,16 @@ class DistVCycle:
 
 
 class TorchComm:
-    """torch.distributed plumbing (NCCL on GPUs, gloo on CPU)."""
+    """torch.distributed plumbing (NCCL on GPUs, gloo on CPU).  Under gloo, device
+    buffers of the point-to-point exchanges are staged through host memory (gloo
+    has no CUDA send/recv); this is the debug path that lets several ranks share
+    one GPU, never a timed configuration."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
+        self.stage = dist.get_backend(group) == "gloo"
 
     def all_gather_object(self, obj):
         out = [None] * self.dist.get_world_size(self.group)
@@ -442,11 +446,18 @@ class TorchComm:
 
     def exchange(self, sends: Dict, recvs: Dict):
         dist = self.dist
+        staged = {}
+        if self.stage:
+            sends = {q: (b.cpu() if b.is_cuda else b) for q, b in sends.items()}
+            staged = {q: b for q, b in recvs.items() if b.is_cuda}
+            recvs = {q: (b.cpu() if b.is_cuda else b) for q, b in recvs.items()}
         ops = [dist.P2POp(dist.isend, buf, q, group=self.group) for q, buf in sorted(sends.items())]
         ops += [dist.P2POp(dist.irecv, buf, q, group=self.group) for q, buf in sorted(recvs.items())]
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        for q, dev in staged.items():
+            dev.copy_(recvs[q])
 
 
 class ThreadComm:
