@@ -696,6 +696,25 @@ def run_gpu(args):
         except Exception:
             traffic = None
 
+    # ---- deterministic scatter mode (R16): same sweeps, slot writes + ordered per-DoF sums ----
+    det = None
+    try:
+        smd = rg.Smoother(G, G, deterministic=True)
+        xd = x0.clone()
+        smd.smooth(xd, b, SWEEPS_PER_STEP, OMEGA)       # warm (graph)
+        xd = x0.clone()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        smd.smooth(xd, b, SWEEPS_PER_STEP, OMEGA)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dms = e0.elapsed_time(e1) / SWEEPS_PER_STEP
+        det = {"ms_per_sweep": dms, "mdofs": n / (dms * 1e-3) / 1e6, "kernel": smd.kernel_name + " + det_gather_kernel"}
+        smd.close()
+        del smd, xd
+    except Exception as err:  # report, keep the line
+        det = {"error": f"{type(err).__name__}: {err}"[:200]}
+
     # ---- end to end through the C-ABI with host buffers ----------------------------
     xh = x0.cpu().pin_memory()
     bh = b.cpu().pin_memory()
@@ -762,6 +781,8 @@ def run_gpu(args):
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if det is not None:
+        line["deterministic_mode"] = det
     if vcyc is not None:
         line["vcycle"] = vcyc
     line.update(extra)

@@ -193,7 +193,10 @@ enum {
 typedef struct {
     int32_t variant;            /* RAV_VARIANT_* */
     int32_t kernel;             /* RAV_KERNEL_* */
-    int32_t deterministic;      /* 1: run-to-run bitwise reproducible scatter (two-phase) */
+    int32_t deterministic;      /* 1: run-to-run bitwise reproducible scatter (R16): the sweep writes
+                                   every correction to its own slot and a second kernel adds them
+                                   to x per DoF in ascending patch order (no atomics).  Schur formats
+                                   only (RAV_ERR_ARG otherwise); MV is deterministic by construction */
     int64_t n_vel;              /* DoFs < n_vel are velocity (needed by DIAG and SCHUR) */
     void*   stream;             /* cudaStream_t */
     int32_t block_dim;          /* velocity components interleaved as dof = block_dim * node + c

@@ -181,7 +181,6 @@ rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opt
         set_error("rav_setup: bad variant");
         return RAV_ERR_ARG;
     }
-    if (o.deterministic) { set_error("rav_setup: deterministic scatter not available in this build"); return RAV_ERR_ARG; }
     if (A->n_rows != A->n_cols) { set_error("rav_setup: L must be square"); return RAV_ERR_ARG; }
     rav_ctx* c = new rav_ctx();
     c->stream = as_stream(o.stream);
@@ -209,6 +208,14 @@ rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opt
             st = RAV_ERR_ARG;
         } else {
             st = factorize(c->A, c->P, o.variant, o.n_vel, o.kernel, c->F, bad_patch, c->stream);
+        }
+    }
+    if (st == RAV_OK && o.deterministic && o.variant != RAV_VARIANT_MV) {
+        if (c->F.layout == 4 || c->F.layout == 5) {
+            st = schur_det_setup(c->P, c->F, c->stream);
+        } else {
+            set_error("rav_setup: deterministic scatter needs the Schur format (block_dim > 0, Vanka-shaped patches)");
+            st = RAV_ERR_ARG;
         }
     }
     if (st == RAV_OK) {

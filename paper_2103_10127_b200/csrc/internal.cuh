@@ -115,7 +115,17 @@ struct Factors {
     int32_t* DT = nullptr;     // nchunks * NMAX * 32
     int32_t* NR = nullptr;     // nchunks * 32 restricted counts (0 for padding)
     int64_t bytes = 0;
+    // deterministic scatter (rav_opts.deterministic, Schur formats): per-patch correction slots and,
+    // per written DoF, its slots in ascending patch order
+    double* cbuf = nullptr;
+    int64_t det_n = 0;          // number of written DoFs
+    int32_t* det_dof = nullptr;
+    int64_t* det_off = nullptr; // det_n + 1
+    int32_t* det_slot = nullptr;
 };
+
+// build the deterministic-scatter tables of a Schur format (layouts 4 / 5)
+rav_status schur_det_setup(const PatchSet& P, Factors& F, cudaStream_t s);
 
 rav_status patches_upload(const rav_patches* P, int64_t n_dofs, PatchSet& out, cudaStream_t s);
 void patches_free(PatchSet& P);

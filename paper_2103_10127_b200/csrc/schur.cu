@@ -23,7 +23,10 @@
 // Gaussian elimination with partial pivoting in shared memory (one CTA per
 // patch; 2D nn = 25, 3D nn = 125).
 #include <algorithm>
+#include <climits>
 #include <vector>
+
+#include <cub/cub.cuh>
 
 #include "internal.cuh"
 
@@ -403,7 +406,9 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
 // ------------------------------------------------------------------------------------
 
 // one patch per thread (2D): MT restricted nodes, D components, NN nodes per patch (runtime)
-template <int MT, int D, int MINB, int NRB = 0>   // NRB > 0: compile-time number of rectangular column pairs
+// DET: the corrections go to per-patch slots cbuf[i (MT D + 1) + k D + c] (pressure: slot MT D)
+// instead of atomics; det_gather_kernel adds them to x in ascending patch order (rav_opts.deterministic)
+template <int MT, int D, int MINB, int NRB = 0, bool DET = false>   // NRB > 0: compile-time rectangular column pairs
 __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
                                                                  const double2* __restrict__ W,
                                                                  const int32_t* __restrict__ ND,
@@ -411,7 +416,8 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
                                                                  const int32_t* __restrict__ NR,
                                                                  const double* __restrict__ AUX,
                                                                  const double* __restrict__ r,
-                                                                 double* __restrict__ x, double omega, int pf) {
+                                                                 double* __restrict__ x, double omega,
+                                                                 double* __restrict__ cbuf) {
     constexpr int TRI = MT * (MT + 1) / 2 + MT * D;
     constexpr int TRI_PAD = TRI + (TRI & 1);
     constexpr int RC = MT + D;   // entries per rectangular column
@@ -430,16 +436,6 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
         for (int ln = lane; ln < lines; ln += 32) prefetch_l2(wc + (size_t)ln * 128);
     }
     pdl_wait();
-    // TMA prefetch of the rectangular column blocks into L2 (no registers / smem):
-    // the first PF_AHEAD blocks now, block k + PF_AHEAD while block k is consumed
-    constexpr int PF_AHEAD = 3;
-    const char* rect0 = reinterpret_cast<const char*>(W + chunk * pairs * 32 + (TRI_PAD / 2) * 32);
-    constexpr unsigned RB = (unsigned)RC * 512u;          // bytes of one two-column block
-    const int nblocks = (NN - MT) / 2;
-    if (pf && lane == 0)
-        for (int k = 0; k < PF_AHEAD && k < nblocks; ++k)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rect0 + (size_t)k * RB), "r"(RB)
-                         : "memory");
     double acc[MT][D], rr[MT][D], gR[MT][D];
     double gacc = 0.0;
 #pragma unroll
@@ -482,10 +478,6 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
     for (int b = 0; b < (NRB > 0 ? NRB : 1 << 20); ++b) {
         if (NRB == 0 && b >= nrb) break;
         const int j0 = MT + 2 * b;
-        const int blk = (j0 - MT) / 2 + PF_AHEAD;
-        if (pf && lane == 0 && blk < nblocks)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rect0 + (size_t)blk * RB), "r"(RB)
-                         : "memory");
         double ra[D], rb[D];
         const int n0 = __ldcs(np_ + j0 * 32), n1 = __ldcs(np_ + (j0 + 1) * 32);
 #pragma unroll
@@ -517,21 +509,29 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
     const double t = aux[(MT + 1) * 32] * (gacc - __ldg(r + pd));
     if (i >= np) return;   // padding slots of the last chunk
     const int m = NR[i];
+    double* cb = DET ? cbuf + i * (MT * D + 1) : nullptr;
 #pragma unroll
     for (int k = 0; k < MT; ++k) {
         if (k < m) {
             const double wk = omega * aux[k * 32];
             const int nd = np_[k * 32];
 #pragma unroll
-            for (int c = 0; c < D; ++c) atomicAdd(x + nd + c, wk * fma(gR[k][c], t, acc[k][c]));
+            for (int c = 0; c < D; ++c) {
+                const double v = wk * fma(gR[k][c], t, acc[k][c]);
+                if (DET) cb[k * D + c] = v;
+                else atomicAdd(x + nd + c, v);
+            }
         }
     }
     const double wpr = aux[MT * 32];
-    if (wpr != 0.0) atomicAdd(x + pd, omega * wpr * (-t));
+    if (wpr != 0.0) {
+        if (DET) cb[MT * D] = omega * wpr * (-t);
+        else atomicAdd(x + pd, omega * wpr * (-t));
+    }
 }
 
 // one patch per warp (3D and large patches): lane k owns restricted node k
-template <int D>
+template <int D, bool DET = false>
 __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int MT, int nnmax,
                                                                const int64_t* __restrict__ foffs,
                                                                const int64_t* __restrict__ nodeoffs,
@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int M
                                                                const int32_t* __restrict__ nresn,
                                                                const double* __restrict__ fac,
                                                                const double* __restrict__ r, double* __restrict__ x,
-                                                               double omega) {
+                                                               double omega, double* __restrict__ cbuf) {
     extern __shared__ double sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* rl = sm + (size_t)warp * nnmax * D;
@@ -566,13 +566,21 @@ __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int M
         for (int t = lane; t < nn * D; t += 32) gs = fma(__ldcs(g + t), rl[t], gs);
         gs = warp_sum(gs);
         const double t = aux[MT + 1] * (gs - __ldg(r + pdof[i]));
+        double* cb = DET ? cbuf + i * ((int64_t)MT * D + 1) : nullptr;
         if (lane < nresn[i]) {
             const double wk = omega * aux[lane];
             const int nd = nodes[no + lane];
 #pragma unroll
-            for (int c = 0; c < D; ++c) atomicAdd(x + nd + c, wk * fma(g[lane * D + c], t, acc[c]));
+            for (int c = 0; c < D; ++c) {
+                const double v = wk * fma(g[lane * D + c], t, acc[c]);
+                if (DET) cb[lane * D + c] = v;
+                else atomicAdd(x + nd + c, v);
+            }
         }
-        if (lane == 0) atomicAdd(x + pdof[i], omega * aux[MT] * (-t));
+        if (lane == 0) {
+            if (DET) cb[MT * D] = omega * aux[MT] * (-t);
+            else atomicAdd(x + pdof[i], omega * aux[MT] * (-t));
+        }
         __syncwarp();
     }
 }
@@ -580,7 +588,7 @@ __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int M
 // coarse levels (few patches): one CTA of 8 warps per patch, warp w takes the columns j = w
 // (mod 8) of A_s^{-1} and of g, the partial sums meet in shared memory -- 8x less serial latency
 // per patch than schur_sweep_warp_kernel when the grid cannot fill the GPU anyway
-template <int D>
+template <int D, bool DET = false>
 __global__ void __launch_bounds__(256) schur_sweep_cta_kernel(int64_t np, int MT, int nnmax,
                                                               const int64_t* __restrict__ foffs,
                                                               const int64_t* __restrict__ nodeoffs,
@@ -589,7 +597,7 @@ __global__ void __launch_bounds__(256) schur_sweep_cta_kernel(int64_t np, int MT
                                                               const int32_t* __restrict__ nresn,
                                                               const double* __restrict__ fac,
                                                               const double* __restrict__ r, double* __restrict__ x,
-                                                              double omega) {
+                                                              double omega, double* __restrict__ cbuf) {
     extern __shared__ double sm[];
     double* rl = sm;                                  // nnmax * D
     double* part = rl + (size_t)nnmax * D;            // 8 warps x 32 lanes x D
@@ -623,6 +631,7 @@ __global__ void __launch_bounds__(256) schur_sweep_cta_kernel(int64_t np, int MT
             double gt = 0.0;
             for (int w = 0; w < 8; ++w) gt += gpart[w];
             const double t = aux[MT + 1] * (gt - __ldg(r + pdof[i]));
+            double* cb = DET ? cbuf + i * ((int64_t)MT * D + 1) : nullptr;
             if (lane < nresn[i]) {
                 const double wk = omega * aux[lane];
                 const int nd = nodes[no + lane];
@@ -630,10 +639,15 @@ __global__ void __launch_bounds__(256) schur_sweep_cta_kernel(int64_t np, int MT
                 for (int c = 0; c < D; ++c) {
                     double a = 0.0;
                     for (int w = 0; w < 8; ++w) a += part[(w * 32 + lane) * D + c];
-                    atomicAdd(x + nd + c, wk * fma(g[lane * D + c], t, a));
+                    const double v = wk * fma(g[lane * D + c], t, a);
+                    if (DET) cb[lane * D + c] = v;
+                    else atomicAdd(x + nd + c, v);
                 }
             }
-            if (lane == 0) atomicAdd(x + pdof[i], omega * aux[MT] * (-t));
+            if (lane == 0) {
+                if (DET) cb[MT * D] = omega * aux[MT] * (-t);
+                else atomicAdd(x + pdof[i], omega * aux[MT] * (-t));
+            }
         }
         __syncthreads();
     }
@@ -1061,92 +1075,185 @@ rav_status launch_mv_color(const Csr& A, const Factors& F, int64_t ncol, const i
     return RAV_OK;
 }
 
-template <int MT>
+template <int MT, bool DET>
 static void launch_schur_thread(int64_t np, const Factors& F, const double* r, double* x, double omega,
                                 cudaStream_t s) {
     const int blocks = (int)cdiv(F.nchunks * 32, 128);
-    static const int minb = [] {
-        const char* e = getenv("RAV_SCHUR_MINB");
-        return e ? atoi(e) : 4;
-    }();
-    static const int pf = [] {
-        const char* e = getenv("RAV_SCHUR_PF");   // L2 bulk prefetch: measured slower (127 vs 124 us), off
-        return e ? atoi(e) : 0;
-    }();
-    static const int nrb_env = [] {
-        const char* e = getenv("RAV_SCHUR_NRB");   // 0: runtime rectangular loop
-        return e ? atoi(e) : 1;
-    }();
-    if (nrb_env && MT == 9 && F.NN == 25) {
-        if (minb == 5)
-            schur_sweep_thread_kernel<MT, 2, 5, 8><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
-                                                                          reinterpret_cast<const double2*>(F.facT), F.DT,
-                                                                          F.PD, F.NR, F.WT, r, x, omega, pf);
-        else if (minb == 3)
-            schur_sweep_thread_kernel<MT, 2, 3, 8><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
-                                                                          reinterpret_cast<const double2*>(F.facT), F.DT,
-                                                                          F.PD, F.NR, F.WT, r, x, omega, pf);
-        else
-            launch_maybe_pdl(schur_sweep_thread_kernel<MT, 2, 4, 8>, dim3(blocks), dim3(128), 0, s, np, F.nchunks,
-                             F.NN, F.pairs, reinterpret_cast<const double2*>(F.facT), (const int32_t*)F.DT,
-                             (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, pf);
-        return;
-    }
-    if (minb >= 6)
-        schur_sweep_thread_kernel<MT, 2, 6><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
-                                                                   reinterpret_cast<const double2*>(F.facT), F.DT,
-                                                                   F.PD, F.NR, F.WT, r, x, omega, pf);
-    else if (minb == 5)
-        schur_sweep_thread_kernel<MT, 2, 5><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
-                                                                   reinterpret_cast<const double2*>(F.facT), F.DT,
-                                                                   F.PD, F.NR, F.WT, r, x, omega, pf);
-    else if (minb >= 4)
-        schur_sweep_thread_kernel<MT, 2, 4><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
-                                                                   reinterpret_cast<const double2*>(F.facT), F.DT,
-                                                                   F.PD, F.NR, F.WT, r, x, omega, pf);
+    const double2* W = reinterpret_cast<const double2*>(F.facT);
+    // 2D PoU interior shape (25 nodes, 9 restricted): compile-time rectangular loop (122 -> 113 us at c2)
+    if (MT == 9 && F.NN == 25)
+        launch_maybe_pdl(schur_sweep_thread_kernel<MT, 2, 4, 8, DET>, dim3(blocks), dim3(128), 0, s, np, F.nchunks,
+                         F.NN, F.pairs, W, (const int32_t*)F.DT, (const int32_t*)F.PD, (const int32_t*)F.NR,
+                         (const double*)F.WT, r, x, omega, F.cbuf);
     else
-        schur_sweep_thread_kernel<MT, 2, 1><<<blocks, 128, 0, s>>>(np, F.nchunks, F.NN, F.pairs,
-                                                                   reinterpret_cast<const double2*>(F.facT), F.DT,
-                                                                   F.PD, F.NR, F.WT, r, x, omega, pf);
+        launch_maybe_pdl(schur_sweep_thread_kernel<MT, 2, 4, 0, DET>, dim3(blocks), dim3(128), 0, s, np, F.nchunks,
+                         F.NN, F.pairs, W, (const int32_t*)F.DT, (const int32_t*)F.PD, (const int32_t*)F.NR,
+                         (const double*)F.WT, r, x, omega, F.cbuf);
+}
+
+template <int D, bool DET>
+static void launch_schur_perpatch(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
+                                  cudaStream_t s) {
+    if (P.n_patches < 2048 && F.MT <= 32) {   // coarse levels: a CTA per patch (latency)
+        const size_t shmem = sizeof(double) * ((size_t)F.NN * D + 8 * 32 * (size_t)D);
+        schur_sweep_cta_kernel<D, DET><<<(int)std::max<int64_t>(1, P.n_patches), 256, shmem, s>>>(
+            P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD, F.NR, F.fac, r, x, omega, F.cbuf);
+    } else {
+        const size_t shmem = sizeof(double) * (size_t)F.NN * D * 8;
+        const int blocks = (int)std::min<int64_t>(cdiv(P.n_patches, 8), (int64_t)num_sms() * 16);
+        schur_sweep_warp_kernel<D, DET><<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs,
+                                                                   F.nodes, F.PD, F.NR, F.fac, r, x, omega, F.cbuf);
+    }
+}
+
+// deterministic mode, phase 2: x[dof_u] += (sum of its slots in ascending patch order)
+__global__ void det_gather_kernel(int64_t nu, const int32_t* __restrict__ dof, const int64_t* __restrict__ off,
+                                  const int32_t* __restrict__ slot, const double* __restrict__ cbuf,
+                                  double* __restrict__ x) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x) {
+        double t = 0.0;
+        for (int64_t e = off[u]; e < off[u + 1]; ++e) t += cbuf[slot[e]];
+        x[dof[u]] += t;
+    }
 }
 
 rav_status launch_schur_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
                               cudaStream_t s) {
+    const bool det = F.cbuf != nullptr;
     if (F.layout == 4) {
-        switch (F.MT) {
-            case 1: launch_schur_thread<1>(P.n_patches, F, r, x, omega, s); break;
-            case 2: launch_schur_thread<2>(P.n_patches, F, r, x, omega, s); break;
-            case 4: launch_schur_thread<4>(P.n_patches, F, r, x, omega, s); break;
-            case 9: launch_schur_thread<9>(P.n_patches, F, r, x, omega, s); break;
+        switch (F.MT * 2 + (det ? 1 : 0)) {
+            case 2: launch_schur_thread<1, false>(P.n_patches, F, r, x, omega, s); break;
+            case 3: launch_schur_thread<1, true>(P.n_patches, F, r, x, omega, s); break;
+            case 4: launch_schur_thread<2, false>(P.n_patches, F, r, x, omega, s); break;
+            case 5: launch_schur_thread<2, true>(P.n_patches, F, r, x, omega, s); break;
+            case 8: launch_schur_thread<4, false>(P.n_patches, F, r, x, omega, s); break;
+            case 9: launch_schur_thread<4, true>(P.n_patches, F, r, x, omega, s); break;
+            case 18: launch_schur_thread<9, false>(P.n_patches, F, r, x, omega, s); break;
+            case 19: launch_schur_thread<9, true>(P.n_patches, F, r, x, omega, s); break;
             default: set_error("schur thread kernel: unsupported MT %d", F.MT); return RAV_ERR_ARG;
         }
-    } else if (P.n_patches < 2048 && F.MT <= 32) {   // coarse levels: a CTA per patch (latency)
-        const size_t shmem = sizeof(double) * ((size_t)F.NN * F.D + 8 * 32 * (size_t)F.D);
-        const int blocks = (int)std::max<int64_t>(1, P.n_patches);
-        if (F.D == 3)
-            schur_sweep_cta_kernel<3><<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs,
-                                                                 F.nodes, F.PD, F.NR, F.fac, r, x, omega);
-        else if (F.D == 2)
-            schur_sweep_cta_kernel<2><<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs,
-                                                                 F.nodes, F.PD, F.NR, F.fac, r, x, omega);
-        else
-            schur_sweep_cta_kernel<1><<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs,
-                                                                 F.nodes, F.PD, F.NR, F.fac, r, x, omega);
+    } else if (F.D == 3) {
+        if (det) launch_schur_perpatch<3, true>(P, F, r, x, omega, s);
+        else launch_schur_perpatch<3, false>(P, F, r, x, omega, s);
+    } else if (F.D == 2) {
+        if (det) launch_schur_perpatch<2, true>(P, F, r, x, omega, s);
+        else launch_schur_perpatch<2, false>(P, F, r, x, omega, s);
     } else {
-        const size_t shmem = sizeof(double) * (size_t)F.NN * F.D * 8;
-        const int blocks = (int)std::min<int64_t>(cdiv(P.n_patches, 8), (int64_t)num_sms() * 16);
-        if (F.D == 3)
-            schur_sweep_warp_kernel<3><<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs,
-                                                                  F.nodes, F.PD, F.NR, F.fac, r, x, omega);
-        else if (F.D == 2)
-            schur_sweep_warp_kernel<2><<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs,
-                                                                  F.nodes, F.PD, F.NR, F.fac, r, x, omega);
-        else
-            schur_sweep_warp_kernel<1><<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs,
-                                                                  F.nodes, F.PD, F.NR, F.fac, r, x, omega);
+        if (det) launch_schur_perpatch<1, true>(P, F, r, x, omega, s);
+        else launch_schur_perpatch<1, false>(P, F, r, x, omega, s);
     }
     count_launch();
     RAV_CHECK_LAUNCH();
+    if (det) {
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(F.det_n, 256), (int64_t)num_sms() * 16));
+        det_gather_kernel<<<blocks, 256, 0, s>>>(F.det_n, F.det_dof, F.det_off, F.det_slot, F.cbuf, x);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+    }
+    return RAV_OK;
+}
+
+
+// ---- deterministic scatter tables ------------------------------------------------------------
+// (dof, slot) pairs of every written correction: restricted node k < m_i, component c -> slot
+// i (MT D + 1) + k D + c; the pressure DoF (weight != 0) -> slot i (MT D + 1) + MT D.  Unused
+// slots get key INT_MAX and sort to the end.
+__global__ void det_pairs_kernel(int64_t np, int layout, int MT, int D, int NN, const int32_t* __restrict__ ND,
+                                 const int32_t* __restrict__ NR, const int32_t* __restrict__ PD,
+                                 const double* __restrict__ AUX, const int64_t* __restrict__ foffs,
+                                 const int64_t* __restrict__ nodeoffs, const int32_t* __restrict__ nodes,
+                                 const double* __restrict__ fac, int32_t* __restrict__ key, int32_t* __restrict__ val) {
+    const int spp = MT * D + 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x) {
+        const int m = NR[i];
+        double wp;
+        if (layout == 4) {
+            const int64_t chunk = i >> 5;
+            const int lane = (int)(i & 31);
+            wp = AUX[(chunk * (MT + 2) + MT) * 32 + lane];
+            for (int k = 0; k < MT; ++k)
+                for (int cc = 0; cc < D; ++cc) {
+                    const int64_t sl = i * spp + k * D + cc;
+                    key[sl] = k < m ? ND[(chunk * NN + k) * 32 + lane] + cc : INT_MAX;
+                    val[sl] = (int32_t)sl;
+                }
+        } else {
+            const int64_t no = nodeoffs[i];
+            const int nn = (int)(nodeoffs[i + 1] - no);
+            wp = fac[foffs[i] + (int64_t)MT * nn + (int64_t)nn * D + MT];
+            for (int k = 0; k < MT; ++k)
+                for (int cc = 0; cc < D; ++cc) {
+                    const int64_t sl = i * spp + k * D + cc;
+                    key[sl] = k < m ? nodes[no + k] + cc : INT_MAX;
+                    val[sl] = (int32_t)sl;
+                }
+        }
+        const int64_t sp = i * spp + MT * D;
+        key[sp] = wp != 0.0 ? PD[i] : INT_MAX;
+        val[sp] = (int32_t)sp;
+    }
+}
+
+rav_status schur_det_setup(const PatchSet& P, Factors& F, cudaStream_t s) {
+    if (F.layout != 4 && F.layout != 5) {
+        set_error("rav_setup: deterministic scatter is implemented for the Schur formats only");
+        return RAV_ERR_ARG;
+    }
+    const int64_t spp = (int64_t)F.MT * F.D + 1;
+    const int64_t ns = P.n_patches * spp;
+    if (ns >= INT32_MAX) { set_error("rav_setup: too many correction slots for deterministic mode"); return RAV_ERR_ARG; }
+    RAV_CUDA(cudaMalloc(&F.cbuf, sizeof(double) * std::max<int64_t>(1, ns)));
+    int32_t *key = nullptr, *val = nullptr, *skey = nullptr, *uniq = nullptr, *cnt32 = nullptr;
+    int64_t *cnt = nullptr, *nrun = nullptr;
+    RAV_CUDA(cudaMallocAsync(&key, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&val, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&skey, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMalloc(&F.det_slot, sizeof(int32_t) * ns));
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(P.n_patches, 128), (int64_t)num_sms() * 16));
+    det_pairs_kernel<<<blocks, 128, 0, s>>>(P.n_patches, F.layout, F.MT, F.D, F.NN, F.DT, F.NR, F.PD, F.WT, F.foffs,
+                                            F.nodeoffs, F.nodes, F.fac, key, val);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    size_t tmp = 0;
+    RAV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, skey, val, F.det_slot, (int)ns, 0, 32, s));
+    void* d_tmp = nullptr;
+    RAV_CUDA(cudaMallocAsync(&d_tmp, tmp + 16, s));
+    // LSD radix sort is stable: equal DoFs keep ascending slots = ascending patches
+    RAV_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp, key, skey, val, F.det_slot, (int)ns, 0, 32, s));
+    RAV_CUDA(cudaMallocAsync(&uniq, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&cnt32, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&nrun, sizeof(int64_t), s));
+    size_t tmp2 = 0;
+    RAV_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp2, skey, uniq, cnt32, nrun, (int)ns, s));
+    void* d_tmp2 = nullptr;
+    RAV_CUDA(cudaMallocAsync(&d_tmp2, tmp2 + 16, s));
+    RAV_CUDA(cub::DeviceRunLengthEncode::Encode(d_tmp2, tmp2, skey, uniq, cnt32, nrun, (int)ns, s));
+    int64_t h_nrun = 0;
+    RAV_CUDA(cudaMemcpyAsync(&h_nrun, nrun, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    RAV_CUDA(cudaStreamSynchronize(s));
+    int32_t last = 0;
+    if (h_nrun > 0) RAV_CUDA(cudaMemcpy(&last, uniq + h_nrun - 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    const int64_t nu = (h_nrun > 0 && last == INT_MAX) ? h_nrun - 1 : h_nrun;   // drop the unused-slot run
+    F.det_n = nu;
+    RAV_CUDA(cudaMalloc(&F.det_dof, sizeof(int32_t) * std::max<int64_t>(1, nu)));
+    RAV_CUDA(cudaMalloc(&F.det_off, sizeof(int64_t) * (nu + 1)));
+    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * std::max<int64_t>(1, nu), s));
+    if (nu > 0) {
+        RAV_CUDA(cudaMemcpyAsync(F.det_dof, uniq, sizeof(int32_t) * nu, cudaMemcpyDeviceToDevice, s));
+        // widen the counts and scan them into offsets
+        std::vector<int32_t> hc(nu);
+        RAV_CUDA(cudaMemcpyAsync(hc.data(), cnt32, sizeof(int32_t) * nu, cudaMemcpyDeviceToHost, s));
+        RAV_CUDA(cudaStreamSynchronize(s));
+        std::vector<int64_t> ho(nu + 1, 0);
+        for (int64_t u = 0; u < nu; ++u) ho[u + 1] = ho[u] + hc[u];
+        RAV_CUDA(cudaMemcpy(F.det_off, ho.data(), sizeof(int64_t) * (nu + 1), cudaMemcpyHostToDevice));
+    } else {
+        RAV_CUDA(cudaMemsetAsync(F.det_off, 0, sizeof(int64_t), s));
+    }
+    for (void* p : {(void*)key, (void*)val, (void*)skey, (void*)uniq, (void*)cnt32, (void*)cnt, (void*)nrun, d_tmp,
+                    d_tmp2})
+        cudaFreeAsync(p, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
     return RAV_OK;
 }
 

@@ -231,12 +231,12 @@ class Smoother:
     """rav_setup / rav_smooth / rav_destroy (Eq. 13)."""
 
     def __init__(self, A: Dict, P: Dict, variant: int = VARIANT_ROWS, kernel: int = KERNEL_AUTO,
-                 stream=None, block_dim: Optional[int] = None):
+                 stream=None, block_dim: Optional[int] = None, deterministic: bool = False):
         self.n = A["n"]
         self._keep = (A, P)
         if block_dim is None:   # the generator's interleaved velocity numbering (R9)
             block_dim = A["problem"]["dim"] if "problem" in A else 0
-        opts = RavOpts(variant, kernel, 0, A.get("nvel", 0), _stream(stream), int(block_dim))
+        opts = RavOpts(variant, kernel, int(bool(deterministic)), A.get("nvel", 0), _stream(stream), int(block_dim))
         ctx = C.c_void_p()
         bad = C.c_int64(-1)
         st = lib.rav_setup(C.byref(csr(A)), C.byref(patches_struct(P)), C.byref(opts), C.byref(ctx), C.byref(bad))
@@ -310,7 +310,7 @@ class Multigrid:
 
     def __init__(self, levels: Sequence[Dict], prolongations: Sequence[Optional[Dict]], coarse_pin: int,
                  variant: int = VARIANT_ROWS, kernel: int = KERNEL_AUTO, stream=None,
-                 block_dim: Optional[int] = None):
+                 block_dim: Optional[int] = None, deterministic: bool = False):
         L = len(levels)
         self.L = L
         self.n = levels[-1]["n"]
@@ -322,7 +322,8 @@ class Multigrid:
             Pr[l] = csr(prolongations[l], n_cols=prolongations[l]["nc"])
         if block_dim is None:
             block_dim = levels[-1]["problem"]["dim"] if "problem" in levels[-1] else 0
-        opts = RavOpts(variant, kernel, 0, levels[-1].get("nvel", 0), _stream(stream), int(block_dim))
+        opts = RavOpts(variant, kernel, int(bool(deterministic)), levels[-1].get("nvel", 0), _stream(stream),
+                       int(block_dim))
         nvel = (C.c_int64 * L)(*[int(A.get("nvel", 0)) for A in levels])
         self._keep = (levels, prolongations, nvel)
         ctx = C.c_void_p()
@@ -448,7 +449,7 @@ def coarsen_problem(problem: Dict) -> Dict:
 
 
 def build_hierarchy(problem: Dict, n_levels: int, weights: str = "pou", variant: int = VARIANT_ROWS,
-                    kernel: int = KERNEL_AUTO, free_inputs: bool = True):
+                    kernel: int = KERNEL_AUTO, free_inputs: bool = True, deterministic: bool = False):
     """Generate every level on the GPU (rediscretized operators) and
     build the multigrid context.  Returns (mg, fine_level_dict)."""
     probs = [problem]
@@ -462,7 +463,7 @@ def build_hierarchy(problem: Dict, n_levels: int, weights: str = "pou", variant:
         if l > 0:
             prols.append(gen_prolongation(p, probs[l - 1]))
     pin = levels[0]["nvel"]       # pressure DoF of vertex 0 (R4)
-    mg = Multigrid(levels, prols, pin, variant=variant, kernel=kernel)
+    mg = Multigrid(levels, prols, pin, variant=variant, kernel=kernel, deterministic=deterministic)
     if variant == VARIANT_MV:     # colour every smoothed level (R10)
         for l in range(1, len(probs)):
             mg.set_colors(l, *multicolor(probs[l]))
