@@ -120,6 +120,7 @@ def lib():
             "or_rav_sweep_sampled": (i64, [i64, vp, vp, vp, i64, vp, vp, vp, vp, vp, dbl, vp, vp]),
             "or_mms_errors": (None, [pd, vp, C.POINTER(dbl), C.POINTER(dbl)]),
             "or_eta": (dbl, [pd, dbl, dbl, dbl]),
+            "or_element_matrices": (C.c_int, [pd, vp, vp, vp, vp, vp, vp]),
             "or_num_threads": (C.c_int, []),
         }
         for name, (res, args) in sig.items():

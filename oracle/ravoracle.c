@@ -214,12 +214,29 @@ static int ipow(int b, int e) { int r = 1; while (e-- > 0) r *= b; return r; }
  *   Fe[a][c]     = int f_c phi_a
  * a, b: local velocity nodes ((P+1)^d), m: local vertices (2^d).  Gauss rule with
  * P+1 points per axis (R7 / R18). */
+static void element_matrices_at(const or_desc* D, const double* org, const double* hin, double* Ae, double* Be,
+                                double* Ce, double* Fe);
+
 static void element_matrices(const or_desc* D, const int* e, double* Ae, double* Be, double* Ce, double* Fe) {
+    double h[3] = {1.0, 1.0, 1.0}, org[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < D->dim; ++k) { h[k] = D->len[k] / D->ncell[k]; org[k] = e[k] * h[k]; }
+    element_matrices_at(D, org, h, Ae, Be, Ce, Fe);
+}
+
+/* the same element matrices for the cell [org, org + h] (adaptive meshes, R20) */
+int or_element_matrices(const or_desc* D, const double* org, const double* h, double* Ae, double* Be, double* Ce,
+                        double* Fe) {
+    element_matrices_at(D, org, h, Ae, Be, Ce, Fe);
+    return 0;
+}
+
+static void element_matrices_at(const or_desc* D, const double* org, const double* hin, double* Ae, double* Be,
+                                double* Ce, double* Fe) {
     const int d = D->dim, P = vorder(D), NQ = ipow(P + 1, d), NV = ipow(2, d), NP1 = P + 1, NG = ipow(NP1, d);
     const double* GT = P == 2 ? GAUSS3_T : GAUSS2_T;
     const double* GW = P == 2 ? GAUSS3_W : GAUSS2_W;
     double h[3], h2 = 0.0;
-    for (int k = 0; k < d; ++k) { h[k] = D->len[k] / D->ncell[k]; h2 += h[k] * h[k]; }
+    for (int k = 0; k < d; ++k) { h[k] = hin[k]; h2 += h[k] * h[k]; }
     memset(Ae, 0, sizeof(double) * NQ * NQ);
     memset(Be, 0, sizeof(double) * NQ * 3 * NV);
     memset(Ce, 0, sizeof(double) * NV * NV);
@@ -231,7 +248,7 @@ static void element_matrices(const or_desc* D, const int* e, double* Ae, double*
             int qk = (q / ipow(NP1, k)) % NP1;
             t[k] = GT[qk];
             w *= GW[qk] * h[k];
-            x[k] = (e[k] + t[k]) * h[k];
+            x[k] = org[k] + t[k] * h[k];
         }
         double eta, ge[3], f[3];
         eta_and_grad(D, x, &eta, ge);
