@@ -136,6 +136,42 @@ rav_status rav_gen_prolongation(const rav_grid* fine, const rav_grid* coarse, in
                                 int32_t* ci, double* val, void* stream);
 
 /* ------------------------------------------------------------------------- */
+/* Adaptive quadtree hierarchies with hanging nodes */
+/* ------------------------------------------------------------------------- */
+
+/* The paper's grid hierarchies (Table 1; reading R20): base is the
+ * problem on an n0 x n0 coarse grid of the unit square (ncell[0] = ncell[1] = n0,
+ * len = 1, 2D, stabilized Q1-Q1: vel_order 1, beta > 0, win = 0).  Level 0 (the
+ * coarsest) is that grid; level k+1 splits every leaf of level k closer to the
+ * boundary than bands[k] cells of the current finest size (bands[k] <= 0: the R20
+ * default (2, 3, 5, 8, 13, 19), which reproduces Table 1), then restores 2:1 edge
+ * balance.  uniform = 1 splits every leaf instead (the structured grids).  Hanging
+ * vertices (edge midpoints of coarser neighbours) are constrained to the mean of the
+ * edge's end points and eliminated.  Numbering: non-hanging vertices by
+ * (y, x); velocity DoFs 2 * free_vertex + c, then one pressure DoF per non-hanging
+ * vertex.  Per level: the operator (CSR, sorted columns, structural pattern), the
+ * right-hand side, the Vanka patches (restricted = velocity on the pressure node,
+ * P:122; order: restricted, p, others) and for levels >= 1 the prolongation from
+ * level - 1.  The mesh logic runs on the host at creation (setup); the
+ * element matrices on the device.  Outputs go to caller buffers, host or device. */
+typedef struct {
+    rav_grid base;
+    int32_t n_levels;           /* >= 1 */
+    int32_t bands[16];          /* per refinement step, in finest cells (<= 0: default) */
+    int32_t uniform;
+} rav_adaptive_desc;
+
+typedef struct rav_adaptive rav_adaptive;
+rav_status rav_adaptive_create(const rav_adaptive_desc* desc, rav_adaptive** out);
+rav_status rav_adaptive_sizes(const rav_adaptive* a, int level, int64_t* n_dofs, int64_t* n_vel, int64_t* nnz,
+                              int64_t* n_patches, int64_t* patch_entries, int64_t* prol_nnz, int64_t* n_cells);
+/* rp[n+1], ci[nnz], val[nnz], rhs[n], poffs[n_patches+1], pdofs/pw[patch_entries],
+ * prp[n+1], pci/pval[prol_nnz] (prolongation ignored on level 0); NULL skips a buffer. */
+rav_status rav_adaptive_fill(const rav_adaptive* a, int level, int64_t* rp, int32_t* ci, double* val, double* rhs,
+                             int64_t* poffs, int32_t* pdofs, double* pw, int64_t* prp, int32_t* pci, double* pval);
+void rav_adaptive_destroy(rav_adaptive* a);
+
+/* ------------------------------------------------------------------------- */
 /* Smoother: RAV (Eq. 13) and its additive relatives                    */
 /* ------------------------------------------------------------------------- */
 

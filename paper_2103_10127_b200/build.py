@@ -20,7 +20,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + INCLUDE, "-Xptxas", "-v"]
 
-SOURCES = ["api.cu", "gen.cu", "linalg.cu", "sell.cu", "nb.cu", "setup.cu", "schur.cu", "sweep.cu", "coarse.cu"]
+SOURCES = ["api.cu", "gen.cu", "linalg.cu", "sell.cu", "nb.cu", "setup.cu", "schur.cu", "sweep.cu", "coarse.cu",
+           "adaptive.cu"]
 
 
 def _deps_mtime() -> float:

@@ -671,6 +671,74 @@ static int grid_for(int64_t n, int bs) {
     return (int)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
+// ---- Q1-Q1 element matrices of arbitrary square cells (adaptive meshes, R20) ----------------------
+// cell c: origin (cx[c], cy[c]), side hc[c].  out[c * Q1_CELL_DOUBLES + ...]:
+//   A[a][b] (16): int eta grad phi_a . grad phi_b          a, b: corners (x fastest)
+//   B[a][k][m] (32): -int psi_m d_k phi_a
+//   C[m][m'] (16): -beta h_e^2 int (1/eta) grad psi_m . grad psi_m'     (Eq. 8, R18)
+//   F[a][k] (8): int f_k phi_a
+__global__ void q1_cell_kernel(Grid G, int64_t ncell, const double* __restrict__ cx, const double* __restrict__ cy,
+                               const double* __restrict__ hc, double* __restrict__ out) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncell; c += (int64_t)gridDim.x * blockDim.x) {
+        const double h = hc[c], he2 = 2.0 * h * h;
+        double A[16] = {0}, B[32] = {0}, Cm[16] = {0}, F[8] = {0};
+        for (int q = 0; q < 4; ++q) {
+            const double t0 = G.gt[q & 1], t1 = G.gt[q >> 1];
+            const double w = G.gw[q & 1] * G.gw[q >> 1] * h * h;
+            double x[3] = {cx[c] + t0 * h, cy[c] + t1 * h, 0.0};
+            double eta, ge[3], f[3] = {0.0, 0.0, 0.0};
+            eta_grad(G, x, eta, ge);
+            if (G.kind == 1) mms_force(G, x, f);
+            double phi[4], gx[4], gy[4];
+            for (int a = 0; a < 4; ++a) {
+                const int ax = a & 1, ay = a >> 1;
+                phi[a] = q1v(ax, t0) * q1v(ay, t1);
+                gx[a] = q1d(ax, t0) / h * q1v(ay, t1);
+                gy[a] = q1v(ax, t0) * q1d(ay, t1) / h;
+            }
+            for (int a = 0; a < 4; ++a) {
+                for (int b = 0; b < 4; ++b) {
+                    const double dot = gx[a] * gx[b] + gy[a] * gy[b];
+                    A[a * 4 + b] += (w * eta) * dot;
+                    Cm[a * 4 + b] -= G.beta * he2 * (w / eta) * dot;
+                }
+                for (int m = 0; m < 4; ++m) {
+                    B[(a * 2 + 0) * 4 + m] -= (w * phi[m]) * gx[a];
+                    B[(a * 2 + 1) * 4 + m] -= (w * phi[m]) * gy[a];
+                }
+                F[a * 2 + 0] += (w * f[0]) * phi[a];
+                F[a * 2 + 1] += (w * f[1]) * phi[a];
+            }
+        }
+        double* o = out + c * 72;
+        for (int i = 0; i < 16; ++i) o[i] = A[i];
+        for (int i = 0; i < 32; ++i) o[16 + i] = B[i];
+        for (int i = 0; i < 16; ++i) o[48 + i] = Cm[i];
+        for (int i = 0; i < 8; ++i) o[64 + i] = F[i];
+    }
+}
+
+rav_status q1_cell_matrices(const rav_grid* g, int64_t ncell, const double* cx, const double* cy, const double* hc,
+                            double* out) {
+    RAV_TRY(check_grid(g));
+    Grid G = make_grid(g);
+    if (G.P != 1 || G.dim != 2) { set_error("q1_cell_matrices: 2D Q1-Q1 only"); return RAV_ERR_ARG; }
+    double *d_in = nullptr, *d_out = nullptr;
+    RAV_CUDA(cudaMalloc(&d_in, sizeof(double) * 3 * std::max<int64_t>(1, ncell)));
+    RAV_CUDA(cudaMalloc(&d_out, sizeof(double) * 72 * std::max<int64_t>(1, ncell)));
+    RAV_CUDA(cudaMemcpy(d_in, cx, sizeof(double) * ncell, cudaMemcpyHostToDevice));
+    RAV_CUDA(cudaMemcpy(d_in + ncell, cy, sizeof(double) * ncell, cudaMemcpyHostToDevice));
+    RAV_CUDA(cudaMemcpy(d_in + 2 * ncell, hc, sizeof(double) * ncell, cudaMemcpyHostToDevice));
+    q1_cell_kernel<<<grid_for(std::max<int64_t>(1, ncell), 128), 128>>>(G, ncell, d_in, d_in + ncell, d_in + 2 * ncell,
+                                                                        d_out);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    RAV_CUDA(cudaMemcpy(out, d_out, sizeof(double) * 72 * ncell, cudaMemcpyDeviceToHost));
+    cudaFree(d_in);
+    cudaFree(d_out);
+    return RAV_OK;
+}
+
 }  // namespace gen
 }  // namespace rav
 

@@ -6,6 +6,10 @@ namespace rav {
 
 namespace gen {
 rav_status counts_to_rowptr(const int64_t* cnt, int64_t* rp, int64_t n, cudaStream_t s);
+// Q1-Q1 element matrices (A 16, B 32, C 16, F 8 doubles per cell, see gen.cu) of square cells
+// (host arrays in and out; runs on the device) -- the adaptive generator's assembly input
+rav_status q1_cell_matrices(const rav_grid* g, int64_t ncell, const double* cx, const double* cy, const double* hc,
+                            double* out);
 }
 
 // ---- linalg.cu ------------------------------------------------------------------------

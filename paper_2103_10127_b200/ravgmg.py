@@ -47,6 +47,10 @@ WINDOW_KEYS = ("node_lo", "node_hi", "vert_lo", "vert_hi", "rnode_lo", "rnode_hi
                "pvert_lo", "pvert_hi")
 
 
+class RavAdaptiveDesc(C.Structure):
+    _fields_ = [("base", RavGrid), ("n_levels", C.c_int32), ("bands", C.c_int32 * 16), ("uniform", C.c_int32)]
+
+
 class RavCsr(C.Structure):
     _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("row_ptr", C.c_void_p),
                 ("col", C.c_void_p), ("val", C.c_void_p), ("on_device", C.c_int32)]
@@ -98,6 +102,9 @@ def _load():
         "rav_xfer_set_stream": [vp, vp],
         "rav_dot": [vp, vp, i64, vp, C.c_int, vp],
         "mg_fgmres": [vp, vp, vp, C.c_int, C.c_int, dbl, C.c_int, dbl, C.c_int, P(C.c_int), vp],
+        "rav_adaptive_create": [P(RavAdaptiveDesc), P(vp)],
+        "rav_adaptive_sizes": [vp, C.c_int, P(i64), P(i64), P(i64), P(i64), P(i64), P(i64), P(i64)],
+        "rav_adaptive_fill": [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -109,6 +116,8 @@ def _load():
     L.mg_destroy.restype = None
     L.rav_xfer_destroy.argtypes = [vp]
     L.rav_xfer_destroy.restype = None
+    L.rav_adaptive_destroy.argtypes = [vp]
+    L.rav_adaptive_destroy.restype = None
     L.rav_kernel_name.argtypes = [vp]
     L.rav_kernel_name.restype = C.c_char_p
     L.rav_last_error.restype = C.c_char_p
@@ -472,4 +481,54 @@ def build_hierarchy(problem: Dict, n_levels: int, weights: str = "pou", variant:
         fine = {k: v for k, v in fine.items() if k in ("n", "nvel", "nnz", "b", "problem")}
         del levels, prols
         torch.cuda.empty_cache()
+    return mg, fine
+
+
+def gen_adaptive(problem: Dict, n_levels: int, bands: Optional[Sequence[int]] = None, uniform: bool = False,
+                 device="cuda") -> List[Dict]:
+    """rav_adaptive_*: the paper's adaptive hierarchy (R20) -- per level
+    (coarsest first) the operator, rhs, patches, and the prolongation from the level
+    below ("prol", levels >= 1).  problem: 2D Q1-Q1 on an n0 x n0 grid."""
+    d = RavAdaptiveDesc()
+    d.base = grid(problem)
+    d.n_levels = int(n_levels)
+    for k, bk in enumerate(bands or []):
+        d.bands[k] = int(bk)
+    d.uniform = int(bool(uniform))
+    h = C.c_void_p()
+    _check(lib.rav_adaptive_create(C.byref(d), C.byref(h)))
+    out = []
+    try:
+        for l in range(n_levels):
+            sz = [C.c_int64() for _ in range(7)]
+            _check(lib.rav_adaptive_sizes(h, l, *[C.byref(s) for s in sz]))
+            n, nvel, nnz, npatch, pe, pnnz, ncell = [s.value for s in sz]
+            t = lambda k, dt: torch.empty(max(k, 1), dtype=dt, device=device)
+            rp, ci, val, b = t(n + 1, torch.int64), t(nnz, torch.int32), t(nnz, torch.float64), t(n, torch.float64)
+            offs, dofs, w = t(npatch + 1, torch.int64), t(pe, torch.int32), t(pe, torch.float64)
+            prp, pci, pval = t(n + 1, torch.int64), t(pnnz, torch.int32), t(pnnz, torch.float64)
+            _check(lib.rav_adaptive_fill(h, l, _ptr(rp), _ptr(ci), _ptr(val), _ptr(b), _ptr(offs), _ptr(dofs),
+                                         _ptr(w), _ptr(prp), _ptr(pci), _ptr(pval)))
+            lev = {"n": n, "nvel": nvel, "nnz": nnz, "rp": rp, "ci": ci[:nnz], "val": val[:nnz], "b": b[:n],
+                   "offs": offs, "dofs": dofs[:pe], "w": w[:pe], "n_cells": ncell, "problem": problem}
+            if l > 0:
+                lev["prol"] = {"n": n, "nc": out[-1]["n"], "rp": prp, "ci": pci[:pnnz], "val": pval[:pnnz]}
+            out.append(lev)
+    finally:
+        lib.rav_adaptive_destroy(h)
+    return out
+
+
+def build_adaptive_hierarchy(problem: Dict, n_levels: int, weights: str = "own", variant: int = VARIANT_ROWS,
+                             kernel: int = KERNEL_AUTO, deterministic: bool = False):
+    """mg_setup on the adaptive hierarchy.  weights: "own" = the paper's restricted
+    prolongation, "full" = additive Vanka (Eq. 12)."""
+    levels = gen_adaptive(problem, n_levels)
+    if weights == "full":
+        for lev in levels:
+            lev["w"].fill_(1.0)
+    prols = [None] + [lev["prol"] for lev in levels[1:]]
+    pin = levels[0]["nvel"]       # pressure DoF of vertex (0, 0) (R4)
+    mg = Multigrid(levels, prols, pin, variant=variant, kernel=kernel, deterministic=deterministic)
+    fine = {k: v for k, v in levels[-1].items() if k in ("n", "nvel", "nnz", "b", "problem", "n_cells")}
     return mg, fine
