@@ -293,6 +293,16 @@ rav_status rav_set_colors(rav_ctx* ctx, int n_colors, const int64_t* color_offs,
  * multi-rank driver exchange interface values between colours. */
 rav_status rav_apply_color(rav_ctx* ctx, int color, double* x, const double* b, double omega);
 
+/* Greedy multicolouring of arbitrary patches for RAV_VARIANT_MV (R10 / R20):
+ * patches i and j conflict when j holds a DoF of patch i or a DoF coupled to it
+ * through L; patches are coloured in ascending order with the smallest free colour,
+ * so same-colour patches may relax concurrently and the colour-major sweep is a
+ * sequential MV sweep.  A, P: host or device.  Outputs (host): *n_colors,
+ * color_offs[n_patches + 1] (capacity; n_colors + 1 used), patch_ids[n_patches]
+ * (colour-major, ascending inside a colour) -- the rav_set_colors layout. */
+rav_status rav_color_patches(const rav_csr* A, const rav_patches* P, int64_t* n_colors, int64_t* color_offs,
+                             int32_t* patch_ids);
+
 /* Name of the sweep kernel / factor format chosen by rav_setup (static string). */
 const char* rav_kernel_name(const rav_ctx* ctx);
 

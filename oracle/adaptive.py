@@ -255,12 +255,37 @@ def prolongation(fine: Mesh, coarse: Mesh) -> Dict:
     return {"n": fine.n, "nc": coarse.n, "rp": rp, "ci": ci, "val": val}
 
 
+def greedy_colors(A: Dict, P: Dict) -> np.ndarray:
+    """Greedy multicolouring (R10 / R20), written plainly: patch j conflicts with patch i
+    when j holds a DoF of patch i or a DoF coupled to one through L; patches in
+    ascending order take the smallest colour no conflicting earlier patch has.
+    Returns the colour-major order (ascending inside a colour)."""
+    npatch = len(P["offs"]) - 1
+    holders: Dict[int, List[int]] = {}
+    for i in range(npatch):
+        for d in P["dofs"][P["offs"][i]:P["offs"][i + 1]]:
+            holders.setdefault(int(d), []).append(i)
+    color = [-1] * npatch
+    for i in range(npatch):
+        touched = set()
+        for d in P["dofs"][P["offs"][i]:P["offs"][i + 1]]:
+            touched.add(int(d))
+            touched |= set(int(c) for c in A["ci"][A["rp"][d]:A["rp"][d + 1]])
+        taken = {color[j] for d in touched for j in holders.get(d, []) if j < i}
+        c = 0
+        while c in taken:
+            c += 1
+        color[i] = c
+    return np.array(sorted(range(npatch), key=lambda i: (color[i], i)), np.int32)
+
+
 class AdaptiveHierarchy(Hierarchy):
     """The oracle V-cycle on the adaptive hierarchy: level operators,
     RAV / AV / MV patch data and transfers from this module, the C oracle's
     factorizations, sweeps, coarse LU (pin: pressure of vertex (0, 0), R4)."""
 
-    def __init__(self, problem: Dict, n_levels: int, smoother: str = "rav", uniform: bool = False, n0: int = 8):
+    def __init__(self, problem: Dict, n_levels: int, smoother: str = "rav", uniform: bool = False, n0: int = 8,
+                 mv_order: str = "ascending"):
         from . import FMT_DIAG, FMT_LU
         self.problem = problem
         self.smoother = smoother
@@ -271,8 +296,8 @@ class AdaptiveHierarchy(Hierarchy):
         for l, m in enumerate(self.meshes):
             A = assemble(problem, m)
             self.A.append(A)
-            self.order.append(None)
             if l == 0:
+                self.order.append(None)
                 self.P.append(None)
                 self.F.append(None)
                 self.T.append(None)
@@ -281,6 +306,7 @@ class AdaptiveHierarchy(Hierarchy):
             if smoother in ("av", "mv", "diag"):
                 Pt = dict(Pt, w=np.ones_like(Pt["w"]))
             fmt = {"rav": FMT_ROWS, "av": FMT_ROWS, "mv": FMT_LU, "diag": FMT_DIAG}[smoother]
+            self.order.append(greedy_colors(A, Pt) if (smoother == "mv" and mv_order == "color") else None)
             self.P.append(Pt)
             self.F.append(factor(A, Pt, fmt))
             self.T.append(prolongation(m, self.meshes[l - 1]))

@@ -87,7 +87,6 @@ struct Level {
     int N = 0;
     std::vector<Cell> cells;
     std::vector<int> sizes;                                  // distinct leaf sizes, descending
-    std::unordered_set<uint64_t> leafset;                    // key(x0, y0) * 64 + log2 s encoded below
     std::unordered_map<uint64_t, std::pair<uint64_t, uint64_t>> hang;   // vertex -> coarse edge end points
     std::vector<uint64_t> regular;                           // non-hanging vertices by (y, x)
     std::unordered_map<uint64_t, int> vel_id, p_id;
@@ -114,10 +113,6 @@ static const Cell* find_leaf(const Level& L, int px, int py, const std::vector<C
     }
     return nullptr;
 }
-
-struct Expansion {
-    std::vector<std::pair<uint64_t, double>> terms;
-};
 
 static void expand(const Level& L, uint64_t v, double w, std::map<uint64_t, double>& acc) {
     auto it = L.hang.find(v);
@@ -424,3 +419,74 @@ rav_status rav_adaptive_fill(const rav_adaptive* A, int level, int64_t* rp, int3
 void rav_adaptive_destroy(rav_adaptive* A) { delete A; }
 
 }  // extern "C"
+
+// ---- greedy multicolouring of arbitrary Vanka patches (multiplicative Vanka, R10 / R20) -------
+// Patches i and j conflict when j holds a DoF of patch i or a DoF coupled to patch i through L
+// (then relaxing them concurrently is not the sequential sweep).  Greedy in ascending patch
+// order, smallest free colour.  Host algorithm (setup); inputs host or device.
+namespace {
+
+template <class Tv>
+static rav_status to_host(std::vector<Tv>& dst, const Tv* src, int64_t n) {
+    dst.resize(std::max<int64_t>(n, 0));
+    if (n > 0) RAV_CUDA(cudaMemcpy(dst.data(), src, sizeof(Tv) * n, cudaMemcpyDefault));
+    return RAV_OK;
+}
+
+}  // namespace
+
+extern "C" rav_status rav_color_patches(const rav_csr* A, const rav_patches* P, int64_t* n_colors,
+                                        int64_t* color_offs, int32_t* patch_ids) {
+    if (!A || !P || !n_colors || !color_offs || !patch_ids || A->n_rows < 0 || P->n_patches < 0) {
+        set_error("rav_color_patches: bad argument");
+        return RAV_ERR_ARG;
+    }
+    const int64_t n = A->n_rows, np = P->n_patches;
+    std::vector<int64_t> rp, po;
+    std::vector<int32_t> ci, pd;
+    RAV_TRY(to_host(rp, A->row_ptr, n + 1));
+    RAV_TRY(to_host(ci, A->col, rp.empty() ? 0 : rp[n]));
+    RAV_TRY(to_host(po, P->offs, np + 1));
+    RAV_TRY(to_host(pd, P->dofs, po.empty() ? 0 : po[np]));
+    // DoF -> patches holding it
+    std::vector<int64_t> dp(n + 1, 0);
+    for (int32_t d : pd) dp[d + 1]++;
+    for (int64_t i = 0; i < n; ++i) dp[i + 1] += dp[i];
+    std::vector<int32_t> dl(pd.size());
+    {
+        std::vector<int64_t> cur(dp.begin(), dp.end() - 1);
+        for (int64_t i = 0; i < np; ++i)
+            for (int64_t k = po[i]; k < po[i + 1]; ++k) dl[cur[pd[k]]++] = (int32_t)i;
+    }
+    std::vector<int32_t> color(np, -1);
+    std::vector<int64_t> seen(np, -1);   // last patch that marked j as a neighbour
+    std::vector<int64_t> used;           // colour -> last patch that found it taken
+    int32_t ncol = 0;
+    for (int64_t i = 0; i < np; ++i) {
+        auto visit = [&](int32_t d) {
+            for (int64_t q = dp[d]; q < dp[d + 1]; ++q) {
+                const int32_t j = dl[q];
+                if (j >= i || seen[j] == i) continue;
+                seen[j] = i;
+                used[color[j]] = i;
+            }
+        };
+        for (int64_t k = po[i]; k < po[i + 1]; ++k) {
+            const int32_t d = pd[k];
+            visit(d);
+            for (int64_t e = rp[d]; e < rp[d + 1]; ++e) visit(ci[e]);
+        }
+        int32_t c = 0;
+        while (c < ncol && used[c] == i) ++c;
+        if (c == ncol) { ++ncol; used.push_back(-1); }
+        color[i] = c;
+    }
+    std::vector<int64_t> cnt(ncol + 1, 0);
+    for (int32_t c : color) cnt[c + 1]++;
+    for (int c = 0; c < ncol; ++c) cnt[c + 1] += cnt[c];
+    for (int c = 0; c <= ncol; ++c) color_offs[c] = cnt[c];
+    std::vector<int64_t> cur(cnt.begin(), cnt.end() - 1);
+    for (int64_t i = 0; i < np; ++i) patch_ids[cur[color[i]]++] = (int32_t)i;
+    *n_colors = ncol;
+    return RAV_OK;
+}

@@ -103,6 +103,7 @@ def _load():
         "rav_dot": [vp, vp, i64, vp, C.c_int, vp],
         "mg_fgmres": [vp, vp, vp, C.c_int, C.c_int, dbl, C.c_int, dbl, C.c_int, P(C.c_int), vp],
         "rav_adaptive_create": [P(RavAdaptiveDesc), P(vp)],
+        "rav_color_patches": [P(RavCsr), P(RavPatches), P(i64), vp, vp],
         "rav_adaptive_sizes": [vp, C.c_int, P(i64), P(i64), P(i64), P(i64), P(i64), P(i64), P(i64)],
         "rav_adaptive_fill": [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
     }
@@ -519,6 +520,18 @@ def gen_adaptive(problem: Dict, n_levels: int, bands: Optional[Sequence[int]] = 
     return out
 
 
+def color_patches(A: Dict, P: Dict):
+    """rav_color_patches: greedy multicolouring for multiplicative Vanka on any patches.
+    Returns (offs, ids) for rav_set_colors."""
+    npatch = len(P["offs"]) - 1
+    offs = np.zeros(npatch + 1, np.int64)
+    ids = np.zeros(max(npatch, 1), np.int32)
+    nc = C.c_int64()
+    _check(lib.rav_color_patches(C.byref(csr(A)), C.byref(patches_struct(P)), C.byref(nc), offs.ctypes.data,
+                                 ids.ctypes.data))
+    return offs[:nc.value + 1].copy(), ids[:npatch].copy()
+
+
 def build_adaptive_hierarchy(problem: Dict, n_levels: int, weights: str = "own", variant: int = VARIANT_ROWS,
                              kernel: int = KERNEL_AUTO, deterministic: bool = False):
     """mg_setup on the adaptive hierarchy.  weights: "own" = the paper's restricted
@@ -530,5 +543,8 @@ def build_adaptive_hierarchy(problem: Dict, n_levels: int, weights: str = "own",
     prols = [None] + [lev["prol"] for lev in levels[1:]]
     pin = levels[0]["nvel"]       # pressure DoF of vertex (0, 0) (R4)
     mg = Multigrid(levels, prols, pin, variant=variant, kernel=kernel, deterministic=deterministic)
+    if variant == VARIANT_MV:     # greedy colouring of every smoothed level (R10 / R20)
+        for l in range(1, n_levels):
+            mg.set_colors(l, *color_patches(levels[l], levels[l]))
     fine = {k: v for k, v in levels[-1].items() if k in ("n", "nvel", "nnz", "b", "problem", "n_cells")}
     return mg, fine

@@ -80,3 +80,24 @@ def test_adaptive_vcycle_counts_match_oracle(rg, smoother, weights, omega):
     _, kg, _ = mg.solve(x, fine["b"], pre=3, post=3, omega=omega, rtol=1e-8, maxit=300)
     assert kg == ko, (kg, ko)
     assert np.linalg.norm(np_(x) - xo) <= 1e-9 * np.linalg.norm(xo)
+
+
+def test_greedy_colors_match_oracle_and_mv_vcycle(rg):
+    prob = si.problem(2, (8, 8), si.KIND_CAVITY, elem=si.ELEM_Q1Q1)
+    levels = rg.gen_adaptive(prob, 3)
+    cells, N = ad.hierarchy_cells(3)
+    for l in (1, 2):
+        m = ad.Mesh(cells[l], N)
+        A = ad.assemble(prob, m)
+        P = dict(ad.patches(A, m))
+        P["w"] = np.ones_like(P["w"])
+        order = ad.greedy_colors(A, P)
+        offs, ids = rg.color_patches(levels[l], levels[l])
+        assert np.array_equal(ids, order)
+    H = ad.AdaptiveHierarchy(prob, 3, "mv", mv_order="color")
+    xo, ko, _ = H.solve(rtol=1e-8, omega=0.66, pre=3, post=3, maxit=300)
+    mg, fine = rg.build_adaptive_hierarchy(prob, 3, "full", variant=rg.VARIANT_MV)
+    x = torch.zeros(fine["n"], dtype=torch.float64, device="cuda")
+    _, kg, _ = mg.solve(x, fine["b"], pre=3, post=3, omega=0.66, rtol=1e-8, maxit=300)
+    assert kg == ko, (kg, ko)
+    assert np.linalg.norm(np_(x) - xo) <= 1e-9 * np.linalg.norm(xo)
