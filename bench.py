@@ -369,6 +369,50 @@ def run_q1q1_studies(rg, si, stream):
     return out
 
 
+def run_adaptive_study(rg, si, stream, max_levels=7):
+    """The paper's driven-cavity convergence study (Figs. 4-5) on its own grid
+    hierarchy: stabilized Q1-Q1 on the adaptive grids of Table 1 (reading R20: level
+    counts reproduced exactly), M^2 .. M^7 with the 8x8 grid as the coarse grid,
+    V(3,3), RAV / multicoloured MV omega 0.66, AV omega 0.1, 1e8 reduction."""
+    import torch
+    prob = si.problem(2, (8, 8), si.KIND_CAVITY, elem=si.ELEM_Q1Q1)
+    out = {"config": "driven cavity, stabilized Q1-Q1 (beta_0 = 0.01, R18), eta = 1, adaptive hierarchy of "
+                     "Table 1 (R20), V(3,3), x0 = 0, rtol 1e-8"}
+    for L in range(2, max_levels + 1):
+        row = {}
+        for name, w, v, om in (("rav", "own", rg.VARIANT_ROWS, 0.66), ("mv_color", "full", rg.VARIANT_MV, 0.66),
+                               ("av", "full", rg.VARIANT_ROWS, 0.1)):
+            t0 = time.perf_counter()
+            mg, fine = rg.build_adaptive_hierarchy(prob, L, w, variant=v)
+            torch.cuda.synchronize()
+            setup = time.perf_counter() - t0
+            x = torch.zeros(fine["n"], dtype=torch.float64, device="cuda")
+            r = {"setup_s": setup}
+            try:
+                mg.solve(x, fine["b"], pre=3, post=3, omega=om, rtol=1e-8, maxit=2)
+                x.zero_()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                x, k, h = mg.solve(x, fine["b"], pre=3, post=3, omega=om, rtol=1e-8, maxit=400)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1) / 1e3
+                r.update({"cycles": k, "converged": bool(h[-1] <= 1e-8 * h[0]), "time_s": t,
+                          "ms_per_cycle": t / max(k, 1) * 1e3,
+                          "avg_reduction_factor": (h[-1] / h[0]) ** (1.0 / max(k, 1))})
+            except rg.RavError as err:
+                r.update({"converged": False, "diverged": str(err)[:120]})
+            row[name] = r
+            mg.close()
+            del mg, x
+            torch.cuda.empty_cache()
+        row["elements"] = fine["n_cells"]
+        row["dofs"] = fine["n"]
+        out[f"M{L}"] = row
+    return out
+
+
 def run_dist_vcycle(name, rdist, si, stream, dist, ws, rank):
     """Slab-partitioned V-cycle to rtol on ws GPUs (strong scaling of c3 / c4):
     partitioned fine levels with NCCL interface sums / halo refreshes, windowed
@@ -743,6 +787,7 @@ def run_gpu(args):
         extra["vcycle_smoothers"] = run_vcycle_smoothers(rg, si, stream)
     if not args.no_paper and ws == 1:
         extra["q1q1_paper_setting"] = run_q1q1_studies(rg, si, stream)
+        extra["adaptive_cavity_table1"] = run_adaptive_study(rg, si, stream)
 
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample) ------------------
     cpu = None

@@ -17,7 +17,7 @@ stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 t0 = time.time()
 fn = {"q1q1": bench.run_q1q1_studies, "vcycle_smoothers": bench.run_vcycle_smoothers,
-      "c5": bench.run_c5_smoothers}[sys.argv[1]]
+      "c5": bench.run_c5_smoothers, "adaptive": bench.run_adaptive_study}[sys.argv[1]]
 out = fn(rg, si, stream)
 print(json.dumps(out, indent=1))
 print("wall", time.time() - t0, file=sys.stderr)
