@@ -85,6 +85,19 @@ __device__ __forceinline__ double group_sum(double v) {
     return v;
 }
 
+// the D components of a node (dof = D * node + c): one 16-byte load when D = 2 and aligned
+template <int D>
+__device__ __forceinline__ void ld_node(const double* __restrict__ p, double* out) {
+    if (D == 2 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+        out[0] = v.x;
+        out[D - 1] = v.y;
+    } else {
+#pragma unroll
+        for (int c = 0; c < D; ++c) out[c] = __ldg(p + c);
+    }
+}
+
 // streaming (evict-first) loads for data read exactly once per sweep
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ double2 ld_stream2(const double2* p) { return __ldcs(p); }

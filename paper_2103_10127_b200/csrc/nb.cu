@@ -220,8 +220,10 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                 for (int k = 0; k < A; ++k) {
                     const int cc = __ldcs(cA + k * NB_C);
                     const double a = __ldcs(vA + k * NB_C);
+                    double xv[D];
+                    ld_node<D>(x + cc, xv);
 #pragma unroll
-                    for (int c = 0; c < D; ++c) acc[c] = fma(a, __ldg(x + cc + c), acc[c]);
+                    for (int c = 0; c < D; ++c) acc[c] = fma(a, xv[c], acc[c]);
                 }
 #pragma unroll 2
                 for (int k = 0; k < B; ++k) {
@@ -261,8 +263,10 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
             for (int k = q; k < A; k += G) {
                 const int cc = __ldcs(cA + k * NB_C);
                 const double a = __ldcs(vA + k * NB_C);
+                double xv[D];
+                ld_node<D>(x + cc, xv);
 #pragma unroll
-                for (int c = 0; c < D; ++c) acc[c] = fma(a, __ldg(x + cc + c), acc[c]);
+                for (int c = 0; c < D; ++c) acc[c] = fma(a, xv[c], acc[c]);
             }
 #pragma unroll 2
             for (int k = q; k < B; k += G) {

@@ -441,11 +441,9 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
 #pragma unroll
     for (int k = 0; k < MT; ++k) {
         const int nd = __ldcs(np_ + k * 32);
+        ld_node<D>(r + nd, rr[k]);
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-            acc[k][c] = 0.0;
-            rr[k][c] = __ldg(r + nd + c);
-        }
+        for (int c = 0; c < D; ++c) acc[k][c] = 0.0;
     }
     double2 pv = make_double2(0.0, 0.0);
 #pragma unroll
@@ -480,11 +478,8 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
         const int j0 = MT + 2 * b;
         double ra[D], rb[D];
         const int n0 = __ldcs(np_ + j0 * 32), n1 = __ldcs(np_ + (j0 + 1) * 32);
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-            ra[c] = __ldg(r + n0 + c);
-            rb[c] = __ldg(r + n1 + c);
-        }
+        ld_node<D>(r + n0, ra);
+        ld_node<D>(r + n1, rb);
         const double2* wq = wq0 + (int64_t)((j0 - MT) / 2) * RC * 32;
 #pragma unroll
         for (int p = 0; p < RC; ++p) {
