@@ -116,8 +116,21 @@ def cpu_oracle_rate(prob, steps, warmup, sweeps_per_step=1):
     dt = time.perf_counter() - t0
     rate = O["n"] * sweeps_per_step * steps / dt / 1e6
     sample = (f"c2 (512^2, {O['n']} DoFs) oracle RAV sweeps, {steps} x {sweeps_per_step} sweep(s) "
-              f"after untimed setup; {dt:.2f} s")
+              f"after untimed setup; {dt:.2f} s; single-threaded sweep on {host_cpu()}")
     return rate, 1, sample, dt
+
+
+def host_cpu() -> str:
+    """CPU model and logical core count of this host (context for the oracle timing)."""
+    model = "unknown CPU"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{model}, {os.cpu_count()} logical cores"
 
 
 def run_reference(args):
