@@ -975,6 +975,52 @@ __global__ void __launch_bounds__(256) diag_sweep_kernel(int64_t np, const int64
     }
 }
 
+// the same with GL lanes per patch (32 / GL patches per warp): short patches keep all lanes busy
+template <int D, int GL>
+__global__ void __launch_bounds__(256) diag_sweep_group_kernel(int64_t np, const int64_t* __restrict__ foffs,
+                                                               const int64_t* __restrict__ nodeoffs,
+                                                               const int32_t* __restrict__ nodes,
+                                                               const int32_t* __restrict__ pdof,
+                                                               const double* __restrict__ fac,
+                                                               const double* __restrict__ r, double* __restrict__ x,
+                                                               double omega) {
+    const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / GL;
+    const int q = threadIdx.x % GL;
+    const int64_t ngroups = (int64_t)gridDim.x * blockDim.x / GL;
+    // warp-uniform trip count: every lane reaches the group shuffles
+    for (int64_t base = gid - (threadIdx.x % 32) / GL; base < np; base += ngroups) {
+        const int64_t i = base + (threadIdx.x % 32) / GL;
+        const bool live = i < np;
+        int64_t no = 0;
+        int nn = 0;
+        const double *dinv = fac, *g = fac, *aux = fac;
+        if (live) {
+            no = nodeoffs[i];
+            nn = (int)(nodeoffs[i + 1] - no);
+            dinv = fac + foffs[i];
+            g = dinv + nn;
+            aux = g + (size_t)nn * D;
+        }
+        double gs = 0.0;
+        for (int t = q; t < nn * D; t += GL) gs = fma(__ldcs(g + t), __ldg(r + nodes[no + t / D] + t % D), gs);
+        gs = group_sum<GL>(gs);
+        if (!live) continue;
+        const int pd = pdof[i];
+        const double t = aux[nn + 1] * (gs - __ldg(r + pd));
+        for (int j = q; j < nn; j += GL) {
+            const double wj = aux[j];
+            if (wj == 0.0) continue;
+            const int nd = nodes[no + j];
+            const double dj = __ldcs(dinv + j);
+            double rv[D];
+            ld_node<D>(r + nd, rv);
+#pragma unroll
+            for (int c = 0; c < D; ++c) atomicAdd(x + nd + c, omega * wj * fma(g[j * D + c], t, dj * rv[c]));
+        }
+        if (q == 0 && aux[nn] != 0.0) atomicAdd(x + pd, omega * aux[nn] * (-t));
+    }
+}
+
 // ---- multicoloured multiplicative Vanka (Eq. 11, R10): one colour per launch --------
 // Patches of one colour share no DoF and are not coupled through L, so they are
 // relaxed concurrently; each computes a fresh local residual on its own rows
@@ -1042,7 +1088,11 @@ rav_status launch_diag_sweep(const PatchSet& P, const Factors& F, const double* 
     const int blocks = (int)std::min<int64_t>(cdiv(P.n_patches, 8), (int64_t)num_sms() * 16);
     if (F.D == 3)
         diag_sweep_kernel<3><<<blocks, 256, 0, s>>>(P.n_patches, F.foffs, F.nodeoffs, F.nodes, F.PD, F.fac, r, x, omega);
-    else if (F.D == 2)
+    else if (F.D == 2 && F.NN <= 32) {   // 2D: 8 lanes per patch (measured in bench c5)
+        const int gb = (int)std::max<int64_t>(1, cdiv(P.n_patches * 8, 256));
+        diag_sweep_group_kernel<2, 8><<<gb, 256, 0, s>>>(P.n_patches, F.foffs, F.nodeoffs, F.nodes, F.PD, F.fac, r, x,
+                                                         omega);
+    } else if (F.D == 2)
         diag_sweep_kernel<2><<<blocks, 256, 0, s>>>(P.n_patches, F.foffs, F.nodeoffs, F.nodes, F.PD, F.fac, r, x, omega);
     else
         diag_sweep_kernel<1><<<blocks, 256, 0, s>>>(P.n_patches, F.foffs, F.nodeoffs, F.nodes, F.PD, F.fac, r, x, omega);
