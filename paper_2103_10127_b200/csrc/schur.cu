@@ -1045,12 +1045,17 @@ __global__ void __launch_bounds__(256) mv_color_kernel(int64_t ncol, const int32
         const int64_t no = nodeoffs[i];
         const int nn = (int)(nodeoffs[i + 1] - no);
         const int pd = pdof[i];
-        // fresh local residual on the patch rows (Eq. 15)
-        for (int t = lane; t <= nn * D; t += 32) {
-            const int row = t < nn * D ? nodes[no + t / D] + t % D : pd;
+        // fresh local residual on the patch rows (Eq. 15): 4 lanes per row, 8 rows per pass
+        for (int t0 = 0; t0 <= nn * D; t0 += 8) {
+            const int t = t0 + (lane >> 2), q = lane & 3;
             double s = 0.0;
-            for (int64_t k = rp[row]; k < rp[row + 1]; ++k) s = fma(val[k], x[ci[k]], s);
-            rl[t] = b[row] - s;
+            int row = 0;
+            if (t <= nn * D) {
+                row = t < nn * D ? nodes[no + t / D] + t % D : pd;
+                for (int64_t k = rp[row] + q; k < rp[row + 1]; k += 4) s = fma(val[k], x[ci[k]], s);
+            }
+            s = group_sum<4>(s);
+            if (q == 0 && t <= nn * D) rl[t] = b[row] - s;
         }
         __syncwarp();
         const double* Y = fac + foffs[i];
