@@ -175,7 +175,9 @@ void rav_adaptive_destroy(rav_adaptive* a);
 /* Smoother: RAV (Eq. 13) and its additive relatives                    */
 /* ------------------------------------------------------------------------- */
 
-/* A sparse matrix in CSR.  Columns sorted ascending within each row. */
+/* A sparse matrix in CSR.  Columns sorted ascending within each row.  Setup calls
+ * validate it (row_ptr[0] = 0 and non-decreasing, 0 <= col < n_cols, strictly
+ * increasing columns per row) and return RAV_ERR_ARG otherwise. */
 typedef struct {
     int64_t n_rows, n_cols;
     const int64_t* row_ptr;     /* n_rows + 1 */

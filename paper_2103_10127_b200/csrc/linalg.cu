@@ -309,6 +309,21 @@ __global__ void row_len_max_kernel(int64_t n, const int64_t* rp, unsigned long l
     (void)t;
 }
 
+// input validation of a CSR (include/ravgmg.h: "columns sorted ascending within each row"):
+// bit 0: row_ptr not monotone / not starting at 0, bit 1: column out of range, bit 2: columns
+// not strictly increasing within a row
+__global__ void csr_check_kernel(int64_t n, int64_t ncols, const int64_t* rp, const int32_t* ci, unsigned int* err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = rp[i], b = rp[i + 1];
+        if ((i == 0 && a != 0) || b < a) { atomicOr(err, 1u); continue; }
+        for (int64_t k = a; k < b; ++k) {
+            const int32_t c = ci[k];
+            if (c < 0 || c >= ncols) atomicOr(err, 2u);
+            if (k > a && c <= ci[k - 1]) atomicOr(err, 4u);
+        }
+    }
+}
+
 rav_status csr_upload(const rav_csr* A, Csr& out, cudaStream_t s) {
     if (!A || A->n_rows < 0 || !A->row_ptr) { set_error("rav_csr: NULL or negative size"); return RAV_ERR_ARG; }
     out.n_rows = A->n_rows;
@@ -331,6 +346,26 @@ rav_status csr_upload(const rav_csr* A, Csr& out, cudaStream_t s) {
     if (nnz > 0) {
         RAV_CUDA(cudaMemcpyAsync(out.ci, A->col, sizeof(int32_t) * nnz, kind, s));
         RAV_CUDA(cudaMemcpyAsync(out.val, A->val, sizeof(double) * nnz, kind, s));
+    }
+    if (out.n_rows > 0) {
+        unsigned int* err = nullptr;
+        RAV_CUDA(cudaMallocAsync(&err, sizeof(unsigned int), s));
+        RAV_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
+        const int nb = (int)std::min<int64_t>(cdiv(out.n_rows, 256), (int64_t)num_sms() * 16);
+        csr_check_kernel<<<nb, 256, 0, s>>>(out.n_rows, out.n_cols, out.rp, out.ci, err);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+        unsigned int h_err = 0;
+        RAV_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(h_err), cudaMemcpyDeviceToHost, s));
+        cudaFreeAsync(err, s);
+        RAV_CUDA(cudaStreamSynchronize(s));
+        if (h_err) {
+            set_error("rav_csr: %s", (h_err & 1) ? "row_ptr must start at 0 and be non-decreasing"
+                                     : (h_err & 2) ? "column index out of range"
+                                                   : "columns must be strictly increasing within a row");
+            csr_free(out);
+            return RAV_ERR_ARG;
+        }
     }
     // lanes per row from the mean row length
     double mean = out.n_rows > 0 ? (double)nnz / (double)out.n_rows : 0.0;

@@ -91,3 +91,18 @@ def test_device_side_errors():
     with pytest.raises(rg.RavError) as ei:
         mg.solve(xs, b, rtol=1e-8, maxit=5)
     assert ei.value.status == RAV_ERR_DIVERGED
+
+
+@pytest.mark.gpu
+def test_malformed_csr_is_rejected():
+    import torch
+    from paper_2103_10127_b200 import ravgmg as rg
+    G = rg.gen_level(si.problem(2, (4, 4), si.KIND_CAVITY), "pou")
+    bad_col = dict(G, ci=G["ci"].clone())
+    bad_col["ci"][5] = G["n"] + 3                       # out of range
+    unsorted = dict(G, ci=G["ci"].clone())
+    unsorted["ci"][0], unsorted["ci"][1] = G["ci"][1].item(), G["ci"][0].item()
+    for A in (bad_col, unsorted):
+        with pytest.raises(rg.RavError) as ei:
+            rg.Smoother(A, G)
+        assert ei.value.status == RAV_ERR_ARG
