@@ -78,7 +78,18 @@ class Coarse(C.Structure):
 
 
 def build(force: bool = False) -> str:
-    """Compile liboracle.so with gcc (plain -O2, OpenMP over patches)."""
+    """Compile liboracle.so with gcc (plain -O2, OpenMP over patches).  With
+    ORACLE_SANITIZE=1 a separate AddressSanitizer + UBSan build is used instead
+    (scripts/oracle_sanitize.sh; the process needs libasan preloaded)."""
+    global _LIB
+    if os.environ.get("ORACLE_SANITIZE") == "1":
+        _LIB = os.path.join(_HERE, "liboracle_asan.so")
+        with _lock:
+            if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+                subprocess.check_call(["gcc", "-O1", "-g", "-fsanitize=address,undefined", "-fno-sanitize-recover=all",
+                                       "-fno-omit-frame-pointer", "-fopenmp", "-shared", "-fPIC", "-std=c11",
+                                       "-D_GNU_SOURCE", "-o", _LIB, _SRC, "-lm"])
+        return _LIB
     with _lock:
         if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
             tmp = _LIB + f".tmp{os.getpid()}"
