@@ -338,6 +338,7 @@ static rav_status copy_out(Tv* dst, const std::vector<Tv>& src) {
 extern "C" {
 
 rav_status rav_adaptive_create(const rav_adaptive_desc* d, rav_adaptive** out) {
+    NvtxRange nvtx_range("rav_adaptive_create");
     if (!d || !out) { set_error("rav_adaptive_create: NULL argument"); return RAV_ERR_ARG; }
     *out = nullptr;
     const rav_grid& g = d->base;

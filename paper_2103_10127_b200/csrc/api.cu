@@ -172,6 +172,7 @@ const char* rav_version(void) { return "ravgmg 0.1 (sm_100a)"; }
 
 rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opts, rav_ctx** out,
                      int64_t* bad_patch) {
+    NvtxRange nvtx_range("rav_setup");
     if (!out || !A || !P) { set_error("rav_setup: NULL argument"); return RAV_ERR_ARG; }
     *out = nullptr;
     if (bad_patch) *bad_patch = -1;
@@ -269,6 +270,7 @@ rav_status rav_set_stream(rav_ctx* c, void* stream) {
 }
 
 rav_status rav_smooth(rav_ctx* c, double* x, const double* b, int nu, double omega) {
+    NvtxRange nvtx_range("rav_smooth");
     if (!c || !x || !b || nu < 0) { set_error("rav_smooth: bad argument"); return RAV_ERR_ARG; }
     g_launches = 0;
     if (nu == 0) { c->last_launches = 0; return RAV_OK; }
@@ -302,6 +304,7 @@ rav_status rav_smooth(rav_ctx* c, double* x, const double* b, int nu, double ome
 }
 
 rav_status rav_residual(rav_ctx* c, const double* x, const double* b, double* r) {
+    NvtxRange nvtx_range("rav_residual");
     if (!c || !x || !b || !r) { set_error("rav_residual: NULL argument"); return RAV_ERR_ARG; }
     g_launches = 0;
     RAV_TRY(launch_residual(c->A, x, b, r, c->stream));
@@ -310,6 +313,7 @@ rav_status rav_residual(rav_ctx* c, const double* x, const double* b, double* r)
 }
 
 rav_status rav_apply(rav_ctx* c, const double* r, double* x, double omega) {
+    NvtxRange nvtx_range("rav_apply");
     if (!c || !x || !r) { set_error("rav_apply: NULL argument"); return RAV_ERR_ARG; }
     g_launches = 0;
     RAV_TRY(launch_sweep(c->P, c->F, r, x, omega, c->stream));
@@ -422,6 +426,7 @@ void mg_destroy(mg_ctx* m) {
 rav_status mg_setup(int n_levels, const rav_csr* A, const rav_patches* patches, const rav_csr* P,
                     const int64_t* n_vel, int64_t coarse_pin, const rav_opts* opts, mg_ctx** out, int* bad_level,
                     int64_t* bad_patch) {
+    NvtxRange nvtx_range("mg_setup");
     if (!out || !A || n_levels < 1 || (n_levels > 1 && (!patches || !P))) {
         set_error("mg_setup: bad argument");
         return RAV_ERR_ARG;
@@ -541,6 +546,7 @@ static rav_status cycle_and_norm(mg_ctx* m, double* x, const double* b, int pre,
 extern "C" {
 
 rav_status mg_vcycle(mg_ctx* m, double* x, const double* b, int pre, int post, double omega) {
+    NvtxRange nvtx_range("mg_vcycle");
     if (!m || !x || !b || pre < 0 || post < 0) { set_error("mg_vcycle: bad argument"); return RAV_ERR_ARG; }
     g_launches = 0;
     if (m->L == 1) {
@@ -555,6 +561,7 @@ rav_status mg_vcycle(mg_ctx* m, double* x, const double* b, int pre, int post, d
 
 rav_status mg_solve(mg_ctx* m, double* x, const double* b, int pre, int post, double omega, double rtol, int maxit,
                     int* iters, double* hist) {
+    NvtxRange nvtx_range("mg_solve");
     if (!m || !x || !b || maxit < 0 || pre < 0 || post < 0) { set_error("mg_solve: bad argument"); return RAV_ERR_ARG; }
     g_launches = 0;
     int64_t total = 0;
@@ -721,6 +728,7 @@ static rav_status kry_norm(mg_ctx* m, const double* v, int64_t n, double* dev_sl
 
 extern "C" rav_status mg_fgmres(mg_ctx* m, double* x, const double* b, int pre, int post, double omega, int restart,
                                 double rtol, int maxit, int* iters, double* hist) {
+    rav::NvtxRange nvtx_range("mg_fgmres");
     using namespace rav;
     if (!m || !x || !b || restart < 1 || restart > 200 || maxit < 0 || pre < 0 || post < 0) {
         set_error("mg_fgmres: bad argument");

@@ -6,6 +6,8 @@
 #include <string>
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/ravgmg.h"
 
 namespace rav {
@@ -33,6 +35,12 @@ const char* get_error();
     } while (0)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// NVTX range around a C-ABI call (setup / smooth / cycle phases in nsys / ncu timelines)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 int num_sms();
 
