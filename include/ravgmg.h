@@ -387,6 +387,24 @@ void rav_xfer_destroy(rav_xfer* t);
  * of the stopping test (R11) over a rank's owned DoFs. */
 rav_status rav_dot(const double* a, const double* b, int64_t n, double* out, int accumulate, void* stream);
 
+/* Peer-memory transport of the slab exchanges (SURVEY section 8 row e; dist.PeerComm):
+ * rav_device_alloc / rav_device_free: zeroed library allocations (exact allocation bases,
+ * so CUDA IPC handles map them 1:1).  rav_ipc_export / rav_ipc_import / rav_ipc_close:
+ * CUDA IPC (64-byte handles; import maps a peer's buffer, over NVLink when it lives on
+ * another GPU).  rav_stream_wait: the stream waits until *flag >= value (32-bit,
+ * wrap-around compare), then flushes remote writes where supported;
+ * rav_stream_signal: *flag = value after all prior work in the stream (release order).
+ * Both are stream memory operations: no host round trip, no spinning kernel.
+ * rav_peer_put: dst[k] = src[k], k < n, with dst possibly a peer (imported) pointer. */
+rav_status rav_device_alloc(int64_t bytes, void** dev_ptr);
+rav_status rav_device_free(void* dev_ptr);
+rav_status rav_ipc_export(void* dev_ptr, unsigned char* handle);
+rav_status rav_ipc_import(const unsigned char* handle, void** dev_ptr);
+rav_status rav_ipc_close(void* dev_ptr);
+rav_status rav_stream_wait(void* stream, uint32_t* flag, uint32_t value);
+rav_status rav_stream_signal(void* stream, uint32_t* flag, uint32_t value);
+rav_status rav_peer_put(const double* src, double* dst, int64_t n, void* stream);
+
 /* Colouring of the smoother on level `level` (1 .. n_levels-1) for
  * RAV_VARIANT_MV (same contract as rav_set_colors). */
 rav_status mg_set_colors(mg_ctx* ctx, int level, int n_colors, const int64_t* color_offs,

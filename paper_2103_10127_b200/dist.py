@@ -512,6 +512,115 @@ class ThreadComm:
         self.sync()
 
 
+class PeerComm:
+    """Peer-memory transport of the point-to-point exchanges (SURVEY section 8 row e):
+    the payload is stored straight into the receiver's buffer (CUDA IPC mapping, peer
+    stores over NVLink between GPUs) and the hand-over is a pair of stream memory
+    operations on 32-bit sequence flags -- the sender's stream waits until the
+    receiver has consumed the slot's previous use, puts, and publishes the sequence
+    number in the receiver's flag; the receiver's stream waits for it, consumes, and
+    hands the slot back.  No host round trip, no spinning kernel, NCCL is not involved.
+    Two slots per channel (a channel = one call site of exchange(), identified by its
+    buffer dictionaries); set up lazily with one host all-gather of IPC handles.
+    all_gather_object / allreduce_sum go to the wrapped TorchComm."""
+
+    def __init__(self, base, rank: int):
+        import torch
+        from . import ravgmg as rg
+        self.base, self.rank, self.rg, self.torch = base, rank, rg, torch
+        self.channels: Dict = {}
+        self._allocs: List = []
+
+    def all_gather_object(self, obj):
+        return self.base.all_gather_object(obj)
+
+    def allreduce_sum(self, buf):
+        self.base.allreduce_sum(buf)
+
+    def _alloc(self, nbytes: int) -> int:
+        import ctypes as C
+        p = C.c_void_p()
+        self.rg._check(self.rg.lib.rav_device_alloc(max(int(nbytes), 8), C.byref(p)))
+        self._allocs.append(p.value)
+        return p.value
+
+    def _export(self, ptr: int) -> bytes:
+        import ctypes as C
+        h = (C.c_ubyte * 64)()
+        self.rg._check(self.rg.lib.rav_ipc_export(C.c_void_p(ptr), h))
+        return bytes(h)
+
+    def _import(self, handle: bytes) -> int:
+        import ctypes as C
+        p = C.c_void_p()
+        buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+        self.rg._check(self.rg.lib.rav_ipc_import(buf, C.byref(p)))
+        return p.value
+
+    def _channel(self, sends: Dict, recvs: Dict):
+        key = (id(sends), id(recvs))
+        ch = self.channels.get(key)
+        if ch is not None:
+            return ch
+        # my side, per peer q I receive from: 2 slots of its message, a ready flag (q writes) and a
+        # free flag for my messages to q (q writes after consuming them)
+        mine = {}
+        for q in set(recvs) | set(sends):
+            n = recvs[q].numel() if q in recvs else 0
+            slots = self._alloc(16 * max(n, 1))
+            flags = self._alloc(64)     # [0] ready (q -> me), [4] free (q consumed my message)
+            mine[q] = {"n": n, "slots": slots, "flags": flags,
+                       "h_slots": self._export(slots), "h_flags": self._export(flags)}
+        table = self.all_gather_object({"rank": self.rank,
+                                        "mine": {q: {k: v for k, v in m.items() if k.startswith("h_") or k == "n"}
+                                                 for q, m in mine.items()}})
+        peer = {}
+        for t in table:
+            q = t["rank"]
+            if q == self.rank or self.rank not in t["mine"]:
+                continue
+            m = t["mine"][self.rank]   # q's buffers for messages from me, q's flags
+            peer[q] = {"n": m["n"], "slots": self._import(m["h_slots"]), "flags": self._import(m["h_flags"])}
+        ch = {"mine": mine, "peer": peer, "seq": 0}
+        self.channels[key] = ch
+        return ch
+
+    def exchange(self, sends: Dict, recvs: Dict):
+        import ctypes as C
+        if not sends and not recvs:
+            return
+        ch = self._channel(sends, recvs)
+        ch["seq"] += 1
+        s = ch["seq"]
+        slot = s % 2
+        st = C.c_void_p(self.torch.cuda.current_stream().cuda_stream)
+        lib = self.rg.lib
+        for q, buf in sorted(sends.items()):
+            pq, mq = ch["peer"][q], ch["mine"][q]
+            n = buf.numel()
+            # the slot's previous message (exchange s - 2) has been consumed by q
+            self.rg._check(lib.rav_stream_wait(st, C.c_void_p(mq["flags"] + 4), max(0, s - 2)))
+            self.rg._check(lib.rav_peer_put(C.c_void_p(buf.data_ptr()), C.c_void_p(pq["slots"] + slot * 8 * n), n, st))
+            self.rg._check(lib.rav_stream_signal(st, C.c_void_p(pq["flags"]), s))          # q's ready flag
+        for q, buf in sorted(recvs.items()):
+            pq, mq = ch["peer"][q], ch["mine"][q]
+            n = buf.numel()
+            self.rg._check(lib.rav_stream_wait(st, C.c_void_p(mq["flags"]), s))          # my ready flag
+            self.rg._check(lib.rav_peer_put(C.c_void_p(mq["slots"] + slot * 8 * n), C.c_void_p(buf.data_ptr()), n, st))
+            self.rg._check(lib.rav_stream_signal(st, C.c_void_p(pq["flags"] + 4), s))    # q's free flag
+
+    def close(self):
+        import ctypes as C
+        self.torch.cuda.synchronize()
+        for ch in self.channels.values():
+            for p in ch["peer"].values():
+                self.rg.lib.rav_ipc_close(C.c_void_p(p["slots"]))
+                self.rg.lib.rav_ipc_close(C.c_void_p(p["flags"]))
+        for a in self._allocs:
+            self.rg.lib.rav_device_free(C.c_void_p(a))
+        self.channels, self._allocs = {}, []
+
+
 def run_threads(nranks: int, fn):
     """fn(rank) on nranks threads; re-raises the first failure."""
     import threading

@@ -104,6 +104,14 @@ def _load():
         "mg_fgmres": [vp, vp, vp, C.c_int, C.c_int, dbl, C.c_int, dbl, C.c_int, P(C.c_int), vp],
         "rav_adaptive_create": [P(RavAdaptiveDesc), P(vp)],
         "rav_color_patches": [P(RavCsr), P(RavPatches), P(i64), vp, vp],
+        "rav_device_alloc": [i64, P(vp)],
+        "rav_device_free": [vp],
+        "rav_ipc_export": [vp, vp],
+        "rav_ipc_import": [vp, P(vp)],
+        "rav_ipc_close": [vp],
+        "rav_stream_wait": [vp, vp, C.c_uint32],
+        "rav_stream_signal": [vp, vp, C.c_uint32],
+        "rav_peer_put": [vp, vp, i64, vp],
         "rav_adaptive_sizes": [vp, C.c_int, P(i64), P(i64), P(i64), P(i64), P(i64), P(i64), P(i64)],
         "rav_adaptive_fill": [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
     }
