@@ -585,6 +585,54 @@ def run_gpu_dist(args):
     value = n_glob * SWEEPS_PER_STEP / (ms_per_step * 1e-3) / 1e6
     assert torch.isfinite(x).all()
 
+    # the same sweeps over the peer-memory transport (CUDA IPC + stream-memory-op flags, no NCCL);
+    # checked against the NCCL result; a watchdog keeps a stuck transport from costing the line
+    p2p = None
+    if os.environ.get("RAV_BENCH_P2P", "1") == "1":
+        import threading
+        done = threading.Event()
+        xref = x.clone()
+
+        def watchdog():
+            if not done.wait(120):
+                line_partial = {"metric": "RAV sweep throughput (c2: 512^2 Q2-Q1, variable viscosity)",
+                                "value": value, "unit": "MDoF/s", "n_gpus": ws, "steps": args.steps,
+                                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                                "config": {"workload": "c2 per GPU stacked along y", "free_dofs": n_glob},
+                                "p2p": {"error": "peer transport did not finish within 120 s"}}
+                if rank == 0:
+                    print(json.dumps(line_partial), flush=True)
+                os._exit(0)
+        threading.Thread(target=watchdog, daemon=True).start()
+        try:
+            pcomm = rdist.PeerComm(rdist.TorchComm(), rank)
+            swp = rdist.DistSweeper(slab, rdist.GpuBackend(sm, stream), pcomm, written)
+            xp = x0.clone()                              # same start and sweep count as the NCCL run (xref)
+            for _ in range(args.warmup):
+                swp.smooth(xp, b, SWEEPS_PER_STEP, OMEGA)
+            torch.cuda.synchronize()
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0p, e1p = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0p.record(stream)
+            for _ in range(args.steps):
+                swp.smooth(xp, b, SWEEPS_PER_STEP, OMEGA)
+            e1p.record(stream)
+            torch.cuda.synchronize()
+            tp = torch.tensor([e0p.elapsed_time(e1p)], device="cuda")
+            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
+            msp = float(tp.item()) / args.steps
+            rel = float((xp - xref).norm() / xref.norm())
+            p2p = {"value": n_glob * SWEEPS_PER_STEP / (msp * 1e-3) / 1e6, "unit": "MDoF/s", "ms_per_step": msp,
+                   "rel_diff_vs_nccl": rel,
+                   "transport": "CUDA IPC receive slots + cuStreamWaitValue32/cuStreamWriteValue32 flags"}
+            pcomm.close()
+        except Exception as err:  # report, keep the line
+            p2p = {"error": f"{type(err).__name__}: {err}"[:200]}
+        done.set()
+        x = xref
+
     # dominant kernel alone on this rank (local patches)
     r = sm.residual(x, b)
     for _ in range(5):
@@ -637,6 +685,8 @@ def run_gpu_dist(args):
         "gpu_launches": kernels_per_sweep * SWEEPS_PER_STEP * args.steps,
         "clocks": clk.summary(),
     }
+    if p2p is not None:
+        line["p2p_exchange"] = p2p
     del sw, sm, L
     torch.cuda.empty_cache()
     if not args.no_smoothers:
