@@ -588,7 +588,7 @@ def run_gpu_dist(args):
     # the same sweeps over the peer-memory transport (CUDA IPC + stream-memory-op flags, no NCCL);
     # checked against the NCCL result; a watchdog keeps a stuck transport from costing the line
     p2p = None
-    if os.environ.get("RAV_BENCH_P2P", "1") == "1":
+    if os.environ.get("RAV_BENCH_P2P", "1") == "1" and not os.environ.get("RAV_SINGLE_DEVICE"):
         import threading
         done = threading.Event()
         xref = x.clone()
