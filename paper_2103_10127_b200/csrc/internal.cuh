@@ -36,6 +36,10 @@ struct NodeBlocked {
     int32_t* col = nullptr;
     double* val = nullptr;
     int64_t bytes = 0;
+    // stencil-compressed columns (structured operators): slot t's columns are base + the offsets
+    // of its pattern pid[t] (tbl[pid * W + k]; A entries first, then B); col is then freed
+    int32_t *pid = nullptr, *baseA = nullptr, *baseB = nullptr, *tbl = nullptr;
+    int W = 0, npat = 0;
 };
 
 struct Csr {

@@ -20,6 +20,7 @@
 // patterns/values, no cross-component entries, pressure rows with complete
 // node groups); on failure the SELL copy is used instead.
 #include <algorithm>
+#include <vector>
 #include <cub/cub.cuh>
 
 #include "internal.cuh"
@@ -171,17 +172,28 @@ __global__ void nb_fill_kernel(int64_t n, int64_t nnodes, int64_t nslices, int D
 // covers 32/G consecutive slots of one slice, lane q of a group takes entries q, q+G, ...
 // of its row (for a fixed k the 32/G rows of the warp are contiguous, so every 32-byte
 // sector is fully used), then the group sums by shuffles.
-template <int D, int G, int UA, int MINB = 1>
+// column access: explicit (SELL column array) or stencil-compressed (base + pattern offset)
+struct NbCols {
+    const int32_t* __restrict__ col;      // explicit
+    const int32_t* __restrict__ pid;      // compressed
+    const int32_t* __restrict__ baseA;
+    const int32_t* __restrict__ baseB;
+    const int32_t* __restrict__ tbl;
+    int W;
+};
+
+template <int D, int G, int UA, int MINB = 1, bool PAT = false>
 __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64_t nnodes, int64_t nslices, int64_t nvel,
                                                           const int32_t* __restrict__ perm,
                                                           const int32_t* __restrict__ wa,
                                                           const int32_t* __restrict__ wb,
                                                           const int64_t* __restrict__ cptr,
                                                           const int64_t* __restrict__ vptr,
-                                                          const int32_t* __restrict__ col,
+                                                          NbCols cols,
                                                           const double* __restrict__ v, const double* __restrict__ x,
                                                           const double* __restrict__ b, double* __restrict__ r,
                                                           double* __restrict__ part) {
+    const int32_t* __restrict__ col = cols.col;
     __shared__ double red[8];
     double mine = 0.0;
     const int64_t total = nslices * NB_C * G;
@@ -192,9 +204,9 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
         const int lane = threadIdx.x & 31;
         if (s0 < nslices) {
             const char* vb = reinterpret_cast<const char*>(v + vptr[s0]);
-            const char* cb = reinterpret_cast<const char*>(col + cptr[s0]);
-            if (lane < 16) prefetch_l2(vb + (size_t)lane * 128);
-            else prefetch_l2(cb + (size_t)(lane - 16) * 128);
+            if (PAT) prefetch_l2(vb + (size_t)lane * 128);
+            else if (lane < 16) prefetch_l2(vb + (size_t)lane * 128);
+            else prefetch_l2(reinterpret_cast<const char*>(col + cptr[s0]) + (size_t)(lane - 16) * 128);
         }
     }
     pdl_wait();
@@ -205,8 +217,13 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
         const int64_t s = t / NB_C;
         const int l = (int)(t % NB_C);
         const int A = live ? wa[s] : 0, B = live ? wb[s] : 0;
-        const int32_t* cA = col + (live ? cptr[s] : 0) + l;
-        const int32_t* cB = cA + (int64_t)A * NB_C;
+        const int32_t* cA = PAT ? nullptr : col + (live ? cptr[s] : 0) + l;
+        const int32_t* cB = PAT ? nullptr : cA + (int64_t)A * NB_C;
+        // PAT: column of entry k = base + tbl[pid * W + k] (the pattern table is L1-resident)
+        const int32_t* tp = PAT ? cols.tbl + (int64_t)(live ? cols.pid[t] : 0) * cols.W : nullptr;
+        const int32_t bA = PAT && live ? cols.baseA[t] : 0, bB = PAT && live ? cols.baseB[t] : 0;
+#define NB_COLA(k) (PAT ? bA + __ldg(tp + (k)) : __ldcs(cA + (k) * NB_C))
+#define NB_COLB(k) (PAT ? bB + __ldg(tp + A + (k)) : __ldcs(cB + (k) * NB_C))
         const double* vA = v + (live ? vptr[s] : 0) + l;
         const double* vB = vA + (int64_t)A * NB_C;
         const int64_t br = (live && t < n) ? perm[t] : -1;
@@ -218,7 +235,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                 for (int c = 0; c < D; ++c) acc[c] = 0.0;
 #pragma unroll UA
                 for (int k = 0; k < A; ++k) {
-                    const int cc = __ldcs(cA + k * NB_C);
+                    const int cc = NB_COLA(k);
                     const double a = __ldcs(vA + k * NB_C);
                     double xv[D];
                     ld_node<D>(x + cc, xv);
@@ -227,7 +244,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                 }
 #pragma unroll 2
                 for (int k = 0; k < B; ++k) {
-                    const double xp = __ldg(x + __ldcs(cB + k * NB_C));
+                    const double xp = __ldg(x + NB_COLB(k));
 #pragma unroll
                     for (int c = 0; c < D; ++c) acc[c] = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), xp, acc[c]);
                 }
@@ -242,7 +259,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                 double acc = 0.0;
 #pragma unroll UA
                 for (int k = 0; k < B; ++k) {
-                    const int cc = __ldcs(cB + k * NB_C);
+                    const int cc = NB_COLB(k);
 #pragma unroll
                     for (int c = 0; c < D; ++c) acc = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), __ldg(x + cc + c), acc);
                 }
@@ -261,7 +278,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
         if (br >= 0 && br < nnodes) {
 #pragma unroll UA
             for (int k = q; k < A; k += G) {
-                const int cc = __ldcs(cA + k * NB_C);
+                const int cc = NB_COLA(k);
                 const double a = __ldcs(vA + k * NB_C);
                 double xv[D];
                 ld_node<D>(x + cc, xv);
@@ -270,14 +287,14 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
             }
 #pragma unroll 2
             for (int k = q; k < B; k += G) {
-                const double xp = __ldg(x + __ldcs(cB + k * NB_C));
+                const double xp = __ldg(x + NB_COLB(k));
 #pragma unroll
                 for (int c = 0; c < D; ++c) acc[c] = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), xp, acc[c]);
             }
         } else if (br >= 0) {
 #pragma unroll UA
             for (int k = q; k < B; k += G) {
-                const int cc = __ldcs(cB + k * NB_C);
+                const int cc = NB_COLB(k);
 #pragma unroll
                 for (int c = 0; c < D; ++c)
                     acc[0] = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), __ldg(x + cc + c), acc[0]);
@@ -305,6 +322,8 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
             }
         }
     }
+#undef NB_COLA
+#undef NB_COLB
     if (part) {
         mine = warp_sum(mine);
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mine;
@@ -315,6 +334,167 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
             part[blockIdx.x] = sum;
         }
     }
+}
+
+// ---- stencil compression of the column arrays (structured operators) ------------------------
+// A slot's column list = (A node columns, B pressure columns); its pattern = (A, B, offsets of
+// the A columns from the first A column, offsets of the B columns from the first B column).
+// Structured grids have a few hundred distinct patterns, so the 4-byte column indices (a
+// quarter of the residual's bytes) become a per-slot pattern id and two bases.
+__device__ __forceinline__ uint64_t fnv(uint64_t h, uint32_t v) {
+    for (int k = 0; k < 4; ++k) { h ^= (v >> (8 * k)) & 0xffu; h *= 1099511628211ull; }
+    return h;
+}
+
+__global__ void nb_hash_kernel(int64_t nslots, const int32_t* wa, const int32_t* wb, const int64_t* cptr,
+                               const int32_t* col, uint64_t* key, int32_t* idx, int32_t* bA, int32_t* bB) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nslots; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t / NB_C;
+        const int l = (int)(t % NB_C);
+        const int A = wa[s], B = wb[s];
+        const int32_t* cA = col + cptr[s] + l;
+        const int32_t* cB = cA + (int64_t)A * NB_C;
+        const int32_t a0 = A > 0 ? cA[0] : 0, b0 = B > 0 ? cB[0] : 0;
+        uint64_t h = 1469598103934665603ull;
+        h = fnv(h, (uint32_t)A);
+        h = fnv(h, (uint32_t)B);
+        for (int k = 0; k < A; ++k) h = fnv(h, (uint32_t)(cA[k * NB_C] - a0));
+        for (int k = 0; k < B; ++k) h = fnv(h, (uint32_t)(cB[k * NB_C] - b0));
+        key[t] = h;
+        idx[t] = (int32_t)t;
+        bA[t] = a0;
+        bB[t] = b0;
+    }
+}
+
+__global__ void nb_segment_kernel(int64_t nslots, const uint64_t* skey, int32_t* flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nslots; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = (i == 0 || skey[i] != skey[i - 1]) ? 1 : 0;
+}
+
+__global__ void nb_pid_kernel(int64_t nslots, const int32_t* sidx, const int32_t* flag, const int32_t* seg,
+                              int32_t* pid, int32_t* rep) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nslots; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t p = seg[i] - 1;
+        pid[sidx[i]] = p;
+        if (flag[i]) rep[p] = sidx[i];
+    }
+}
+
+__global__ void nb_table_kernel(int npat, int W, const int32_t* rep, const int32_t* wa, const int32_t* wb,
+                                const int64_t* cptr, const int32_t* col, int32_t* tbl, int32_t* tw) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npat; p += gridDim.x * blockDim.x) {
+        const int64_t t = rep[p], s = t / NB_C;
+        const int l = (int)(t % NB_C);
+        const int A = wa[s], B = wb[s];
+        const int32_t* cA = col + cptr[s] + l;
+        const int32_t* cB = cA + (int64_t)A * NB_C;
+        const int32_t a0 = A > 0 ? cA[0] : 0, b0 = B > 0 ? cB[0] : 0;
+        for (int k = 0; k < A; ++k) tbl[(int64_t)p * W + k] = cA[k * NB_C] - a0;
+        for (int k = 0; k < B; ++k) tbl[(int64_t)p * W + A + k] = cB[k * NB_C] - b0;
+        tw[2 * p] = A;
+        tw[2 * p + 1] = B;
+    }
+}
+
+__global__ void nb_verify_kernel(int64_t nslots, int W, const int32_t* wa, const int32_t* wb, const int64_t* cptr,
+                                 const int32_t* col, const int32_t* pid, const int32_t* bA, const int32_t* bB,
+                                 const int32_t* tbl, const int32_t* tw, unsigned int* err) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nslots; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t / NB_C;
+        const int l = (int)(t % NB_C);
+        const int A = wa[s], B = wb[s], p = pid[t];
+        if (tw[2 * p] != A || tw[2 * p + 1] != B) { atomicOr(err, 1u); continue; }
+        const int32_t* cA = col + cptr[s] + l;
+        const int32_t* cB = cA + (int64_t)A * NB_C;
+        for (int k = 0; k < A; ++k)
+            if (cA[k * NB_C] != bA[t] + tbl[(int64_t)p * W + k]) atomicOr(err, 1u);
+        for (int k = 0; k < B; ++k)
+            if (cB[k * NB_C] != bB[t] + tbl[(int64_t)p * W + A + k]) atomicOr(err, 1u);
+    }
+}
+
+// replace N.col by (pattern id, bases, table) when the patterns are few and verified
+static rav_status nb_compress(NodeBlocked& N, cudaStream_t s) {
+    const int64_t ns = N.nslices * NB_C;
+    std::vector<int32_t> hwa(N.nslices), hwb(N.nslices);
+    RAV_CUDA(cudaMemcpy(hwa.data(), N.wa, sizeof(int32_t) * N.nslices, cudaMemcpyDeviceToHost));
+    RAV_CUDA(cudaMemcpy(hwb.data(), N.wb, sizeof(int32_t) * N.nslices, cudaMemcpyDeviceToHost));
+    int W = 1;
+    for (int64_t k = 0; k < N.nslices; ++k) W = std::max(W, hwa[k] + hwb[k]);
+    uint64_t *key = nullptr, *skey = nullptr;
+    int32_t *idx = nullptr, *sidx = nullptr, *flag = nullptr, *seg = nullptr, *rep = nullptr, *tw = nullptr;
+    int32_t *pid = nullptr, *bA = nullptr, *bB = nullptr, *tbl = nullptr;
+    unsigned int* err = nullptr;
+    RAV_CUDA(cudaMallocAsync(&key, sizeof(uint64_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&skey, sizeof(uint64_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&idx, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&sidx, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&flag, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&seg, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMalloc(&pid, sizeof(int32_t) * ns));
+    RAV_CUDA(cudaMalloc(&bA, sizeof(int32_t) * ns));
+    RAV_CUDA(cudaMalloc(&bB, sizeof(int32_t) * ns));
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(ns, 256), (int64_t)num_sms() * 16));
+    nb_hash_kernel<<<nb, 256, 0, s>>>(ns, N.wa, N.wb, N.cptr, N.col, key, idx, bA, bB);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    size_t tmp = 0;
+    RAV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, skey, idx, sidx, (int)ns, 0, 64, s));
+    void* d_tmp = nullptr;
+    RAV_CUDA(cudaMallocAsync(&d_tmp, tmp + 16, s));
+    RAV_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp, key, skey, idx, sidx, (int)ns, 0, 64, s));
+    nb_segment_kernel<<<nb, 256, 0, s>>>(ns, skey, flag);
+    count_launch();
+    size_t tmp2 = 0;
+    RAV_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp2, flag, seg, (int)ns, s));
+    void* d_tmp2 = nullptr;
+    RAV_CUDA(cudaMallocAsync(&d_tmp2, tmp2 + 16, s));
+    RAV_CUDA(cub::DeviceScan::InclusiveSum(d_tmp2, tmp2, flag, seg, (int)ns, s));
+    int32_t npat = 0;
+    RAV_CUDA(cudaMemcpyAsync(&npat, seg + ns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    RAV_CUDA(cudaStreamSynchronize(s));
+    bool ok = npat > 0 && (int64_t)npat * W * 4 <= (16 << 20);   // table must stay cache-sized
+    if (ok) {
+        RAV_CUDA(cudaMallocAsync(&rep, sizeof(int32_t) * npat, s));
+        RAV_CUDA(cudaMallocAsync(&tw, sizeof(int32_t) * 2 * npat, s));
+        RAV_CUDA(cudaMalloc(&tbl, sizeof(int32_t) * (int64_t)npat * W));
+        RAV_CUDA(cudaMallocAsync(&err, sizeof(unsigned int), s));
+        RAV_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
+        nb_pid_kernel<<<nb, 256, 0, s>>>(ns, sidx, flag, seg, pid, rep);
+        count_launch();
+        nb_table_kernel<<<(int)cdiv(npat, 128), 128, 0, s>>>(npat, W, rep, N.wa, N.wb, N.cptr, N.col, tbl, tw);
+        count_launch();
+        nb_verify_kernel<<<nb, 256, 0, s>>>(ns, W, N.wa, N.wb, N.cptr, N.col, pid, bA, bB, tbl, tw, err);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+        unsigned int h_err = 0;
+        RAV_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(h_err), cudaMemcpyDeviceToHost, s));
+        RAV_CUDA(cudaStreamSynchronize(s));
+        ok = h_err == 0;   // a hash collision keeps the explicit columns
+    }
+    for (void* p : {(void*)key, (void*)skey, (void*)idx, (void*)sidx, (void*)flag, (void*)seg, (void*)rep, (void*)tw,
+                    (void*)err, d_tmp, d_tmp2})
+        if (p) cudaFreeAsync(p, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    if (!ok) {
+        for (void* p : {(void*)pid, (void*)bA, (void*)bB, (void*)tbl})
+            if (p) cudaFree(p);
+        return RAV_OK;
+    }
+    int64_t hc = 0;
+    RAV_CUDA(cudaMemcpy(&hc, N.cptr + N.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    cudaFree(N.col);
+    N.col = nullptr;
+    N.pid = pid;
+    N.baseA = bA;
+    N.baseB = bB;
+    N.tbl = tbl;
+    N.W = W;
+    N.npat = npat;
+    // streamed bytes: values + per-slot (pid, two bases); the table is cache-resident
+    N.bytes = N.bytes - 4 * hc + 12 * ns;
+    return RAV_OK;
 }
 
 rav_status nb_build(Csr& A, int64_t nvel, int D, cudaStream_t s) {
@@ -394,11 +574,17 @@ rav_status nb_build(Csr& A, int64_t nvel, int D, cudaStream_t s) {
         cudaFreeAsync(p, s);
     RAV_CUDA(cudaStreamSynchronize(s));
     N.nvel = nvel;
+    static const bool compress = [] {
+        const char* e = getenv("RAV_NB_COMPRESS");
+        return !(e && atoi(e) == 0);
+    }();
+    if (compress) RAV_TRY(nb_compress(N, s));
     return RAV_OK;
 }
 
 void nb_free(NodeBlocked& N) {
-    for (void* p : {(void*)N.perm, (void*)N.wa, (void*)N.wb, (void*)N.cptr, (void*)N.vptr, (void*)N.col, (void*)N.val})
+    for (void* p : {(void*)N.perm, (void*)N.wa, (void*)N.wb, (void*)N.cptr, (void*)N.vptr, (void*)N.col, (void*)N.val,
+                    (void*)N.pid, (void*)N.baseA, (void*)N.baseB, (void*)N.tbl})
         if (p) cudaFree(p);
     N = NodeBlocked{};
 }
@@ -406,6 +592,7 @@ void nb_free(NodeBlocked& N) {
 template <int D, int G, int UA>
 static void nb_launch(const NodeBlocked& N, const double* x, const double* b, double* r, double* part, int nblk,
                       cudaStream_t s, int* used) {
+    const NbCols cols{N.col, N.pid, N.baseA, N.baseB, N.tbl, N.W};
     const int64_t full = cdiv(N.nslices * NB_C * G, 256);
     // with partial norms: one partial per block, the full grid when the caller's buffer holds it
     const int blocks = (int)(part ? std::min<int64_t>(full, nblk) : full);
@@ -414,13 +601,14 @@ static void nb_launch(const NodeBlocked& N, const double* x, const double* b, do
         const char* e = getenv("RAV_NB_MINB");
         return e ? atoi(e) : 6;
     }();
-    auto kern = (minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8>
+    auto kern = N.tbl ? ((minb >= 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6, true> : nb_residual_kernel<D, G, UA, 1, true>)
+              : (minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8>
               : (minb == 7 && G == 1) ? nb_residual_kernel<D, G, UA, 7>
               : (minb == 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6>
               : (minb == 5 && G == 1) ? nb_residual_kernel<D, G, UA, 5> : nb_residual_kernel<D, G, UA, 1>;
     launch_maybe_pdl(kern, dim3(blocks), dim3(256), 0, s, N.nblock, N.nnodes, N.nslices,
                      N.nvel, (const int32_t*)N.perm, (const int32_t*)N.wa, (const int32_t*)N.wb,
-                     (const int64_t*)N.cptr, (const int64_t*)N.vptr, (const int32_t*)N.col, (const double*)N.val, x, b,
+                     (const int64_t*)N.cptr, (const int64_t*)N.vptr, cols, (const double*)N.val, x, b,
                      r, part);
 }
 
