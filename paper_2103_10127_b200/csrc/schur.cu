@@ -417,15 +417,18 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
                                                                  const double* __restrict__ AUX,
                                                                  const double* __restrict__ r,
                                                                  double* __restrict__ x, double omega,
-                                                                 double* __restrict__ cbuf) {
+                                                                 double* __restrict__ cbuf, int64_t chunk0, int half) {
     constexpr int TRI = MT * (MT + 1) / 2 + MT * D;
     constexpr int TRI_PAD = TRI + (TRI & 1);
     constexpr int RC = MT + D;   // entries per rectangular column
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t chunk = i >> 5;
-    const int lane = threadIdx.x & 31;
+    // half = 0: warp w -> chunk chunk0 + w; half = 1 (the last, partial wave): two warps per chunk,
+    // 16 active lanes each -- the tail's patches spread over twice as many warps
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t chunk = chunk0 + (half ? gw >> 1 : gw);
+    const int lane = half ? (int)((gw & 1) << 4) + (threadIdx.x & 15) : (threadIdx.x & 31);
+    const int64_t i = chunk * 32 + lane;
     pdl_trigger();
-    if (chunk >= nchunks) return;
+    if (chunk >= nchunks || (half && (threadIdx.x & 31) >= 16)) return;
     const double2* wp = W + chunk * pairs * 32 + lane;
     const int32_t* np_ = ND + chunk * (int64_t)NN * 32 + lane;
     {   // before r exists: the chunk's node indices and first factor lines into L2
@@ -1128,17 +1131,34 @@ rav_status launch_mv_color(const Csr& A, const Factors& F, int64_t ncol, const i
 template <int MT, bool DET>
 static void launch_schur_thread(int64_t np, const Factors& F, const double* r, double* x, double omega,
                                 cudaStream_t s) {
-    const int blocks = (int)cdiv(F.nchunks * 32, 128);
     const double2* W = reinterpret_cast<const double2*>(F.facT);
     // 2D PoU interior shape (25 nodes, 9 restricted): compile-time rectangular loop (122 -> 113 us at c2)
-    if (MT == 9 && F.NN == 25)
-        launch_maybe_pdl(schur_sweep_thread_kernel<MT, 2, 4, 8, DET>, dim3(blocks), dim3(128), 0, s, np, F.nchunks,
-                         F.NN, F.pairs, W, (const int32_t*)F.DT, (const int32_t*)F.PD, (const int32_t*)F.NR,
-                         (const double*)F.WT, r, x, omega, F.cbuf);
-    else
-        launch_maybe_pdl(schur_sweep_thread_kernel<MT, 2, 4, 0, DET>, dim3(blocks), dim3(128), 0, s, np, F.nchunks,
-                         F.NN, F.pairs, W, (const int32_t*)F.DT, (const int32_t*)F.PD, (const int32_t*)F.NR,
-                         (const double*)F.WT, r, x, omega, F.cbuf);
+    auto kern = (MT == 9 && F.NN == 25) ? schur_sweep_thread_kernel<MT, 2, 4, 8, DET>
+                                        : schur_sweep_thread_kernel<MT, 2, 4, 0, DET>;
+    // wave split: full waves of one warp per chunk, then the partial last wave with two half-warps
+    // per chunk (its chunks finish in about half the time of a full-chunk warp)
+    static int conc = 0;
+    if (!conc) {
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0) != cudaSuccess) per_sm = 0;
+        cudaGetLastError();
+        conc = std::max(1, per_sm) * 4 * num_sms();   // resident warps (4 per block)
+    }
+    static const bool split = [] {   // measured at c2: 119.5 us split vs 114.0 us single launch -> off
+        const char* e = getenv("RAV_SCHUR_TAIL");
+        return e && atoi(e) == 1;
+    }();
+    const int64_t full = split && F.nchunks > conc ? F.nchunks / conc * conc : F.nchunks;
+    const int64_t rem = F.nchunks - full;
+    launch_maybe_pdl(kern, dim3((unsigned)cdiv(full * 32, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
+                     (const int32_t*)F.DT, (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x,
+                     omega, F.cbuf, (int64_t)0, 0);
+    if (rem > 0) {
+        count_launch();
+        launch_maybe_pdl(kern, dim3((unsigned)cdiv(rem * 64, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
+                         (const int32_t*)F.DT, (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x,
+                         omega, F.cbuf, full, 1);
+    }
 }
 
 template <int D, bool DET>
