@@ -123,6 +123,9 @@ struct Factors {
     int32_t* DT = nullptr;     // nchunks * NMAX * 32
     int32_t* NR = nullptr;     // nchunks * 32 restricted counts (0 for padding)
     int64_t bytes = 0;
+    // layout 4 node-index compression: node j of slot i = nbase[i] + ntbl[npid[i] * NN + j] (DT freed)
+    int32_t *npid = nullptr, *nbase = nullptr, *ntbl = nullptr;
+    int nnpat = 0;
     // deterministic scatter (rav_opts.deterministic, Schur formats): per-patch correction slots and,
     // per written DoF, its slots in ascending patch order
     double* cbuf = nullptr;

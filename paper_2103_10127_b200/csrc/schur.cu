@@ -408,10 +408,14 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
 // one patch per thread (2D): MT restricted nodes, D components, NN nodes per patch (runtime)
 // DET: the corrections go to per-patch slots cbuf[i (MT D + 1) + k D + c] (pressure: slot MT D)
 // instead of atomics; det_gather_kernel adds them to x in ascending patch order (rav_opts.deterministic)
-template <int MT, int D, int MINB, int NRB = 0, bool DET = false>   // NRB > 0: compile-time rectangular column pairs
+// NDP: node indices from (nbase[i], pattern table ntbl[npid[i] * NN + j]) instead of the ND array
+template <int MT, int D, int MINB, int NRB = 0, bool DET = false, bool NDP = false>   // NRB > 0: compile-time rect pairs
 __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
                                                                  const double2* __restrict__ W,
                                                                  const int32_t* __restrict__ ND,
+                                                                 const int32_t* __restrict__ npid,
+                                                                 const int32_t* __restrict__ nbase,
+                                                                 const int32_t* __restrict__ ntbl,
                                                                  const int32_t* __restrict__ PD,
                                                                  const int32_t* __restrict__ NR,
                                                                  const double* __restrict__ AUX,
@@ -430,11 +434,16 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
     pdl_trigger();
     if (chunk >= nchunks || (half && (threadIdx.x & 31) >= 16)) return;
     const double2* wp = W + chunk * pairs * 32 + lane;
-    const int32_t* np_ = ND + chunk * (int64_t)NN * 32 + lane;
+    const int32_t* np_ = NDP ? nullptr : ND + chunk * (int64_t)NN * 32 + lane;
+    const int32_t* ntp = NDP ? ntbl + (int64_t)npid[i] * NN : nullptr;   // L1-resident pattern row
+    const int32_t nb0 = NDP ? nbase[i] : 0;
+#define ND_AT(j) (NDP ? nb0 + __ldg(ntp + (j)) : __ldcs(np_ + (j) * 32))
     {   // before r exists: the chunk's node indices and first factor lines into L2
         const char* wc = reinterpret_cast<const char*>(W + chunk * pairs * 32);
-        const char* nc = reinterpret_cast<const char*>(ND + chunk * (int64_t)NN * 32);
-        for (int ln = lane; ln < NN; ln += 32) prefetch_l2(nc + (size_t)ln * 128);
+        if (!NDP) {
+            const char* nc = reinterpret_cast<const char*>(ND + chunk * (int64_t)NN * 32);
+            for (int ln = lane; ln < NN; ln += 32) prefetch_l2(nc + (size_t)ln * 128);
+        }
         const int lines = (int)(pairs * 4 < 128 ? pairs * 4 : 128);
         for (int ln = lane; ln < lines; ln += 32) prefetch_l2(wc + (size_t)ln * 128);
     }
@@ -443,7 +452,7 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
     double gacc = 0.0;
 #pragma unroll
     for (int k = 0; k < MT; ++k) {
-        const int nd = __ldcs(np_ + k * 32);
+        const int nd = ND_AT(k);
         ld_node<D>(r + nd, rr[k]);
 #pragma unroll
         for (int c = 0; c < D; ++c) acc[k][c] = 0.0;
@@ -480,7 +489,7 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
         if (NRB == 0 && b >= nrb) break;
         const int j0 = MT + 2 * b;
         double ra[D], rb[D];
-        const int n0 = __ldcs(np_ + j0 * 32), n1 = __ldcs(np_ + (j0 + 1) * 32);
+        const int n0 = ND_AT(j0), n1 = ND_AT(j0 + 1);
         ld_node<D>(r + n0, ra);
         ld_node<D>(r + n1, rb);
         const double2* wq = wq0 + (int64_t)((j0 - MT) / 2) * RC * 32;
@@ -512,7 +521,7 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
     for (int k = 0; k < MT; ++k) {
         if (k < m) {
             const double wk = omega * aux[k * 32];
-            const int nd = np_[k * 32];
+            const int nd = ND_AT(k);
 #pragma unroll
             for (int c = 0; c < D; ++c) {
                 const double v = wk * fma(gR[k][c], t, acc[k][c]);
@@ -527,6 +536,8 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
         else atomicAdd(x + pd, omega * wpr * (-t));
     }
 }
+
+#undef ND_AT
 
 // one patch per warp (3D and large patches): lane k owns restricted node k
 template <int D, bool DET = false>
@@ -660,6 +671,123 @@ static int pick_MT(int mnmax) {
     for (int c : cand)
         if (c >= mnmax) return c;
     return -1;
+}
+
+// ---- node-index patterns of the thread layout (structured patches) ----------------------------
+// slot i's node list ND[(chunk NN + j) 32 + lane] = base + pattern offsets; few distinct patterns
+__device__ __forceinline__ uint64_t nd_fnv(uint64_t h, uint32_t v) {
+    for (int k = 0; k < 4; ++k) { h ^= (v >> (8 * k)) & 0xffu; h *= 1099511628211ull; }
+    return h;
+}
+
+__global__ void nd_hash_kernel(int64_t nslots, int NN, const int32_t* ND, uint64_t* key, int32_t* idx, int32_t* base) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nslots; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t chunk = t >> 5;
+        const int lane = (int)(t & 31);
+        const int32_t* p = ND + chunk * (int64_t)NN * 32 + lane;
+        const int32_t b0 = p[0];
+        uint64_t h = 1469598103934665603ull;
+        for (int j = 0; j < NN; ++j) h = nd_fnv(h, (uint32_t)(p[j * 32] - b0));
+        key[t] = h;
+        idx[t] = (int32_t)t;
+        base[t] = b0;
+    }
+}
+
+__global__ void nd_flag_kernel(int64_t n, const uint64_t* skey, int32_t* flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = (i == 0 || skey[i] != skey[i - 1]) ? 1 : 0;
+}
+
+__global__ void nd_pid_kernel(int64_t n, const int32_t* sidx, const int32_t* flag, const int32_t* seg, int32_t* pid,
+                              int32_t* rep) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        pid[sidx[i]] = seg[i] - 1;
+        if (flag[i]) rep[seg[i] - 1] = sidx[i];
+    }
+}
+
+__global__ void nd_table_kernel(int npat, int NN, const int32_t* rep, const int32_t* ND, int32_t* tbl) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npat; p += gridDim.x * blockDim.x) {
+        const int64_t t = rep[p];
+        const int32_t* q = ND + (t >> 5) * (int64_t)NN * 32 + (t & 31);
+        for (int j = 0; j < NN; ++j) tbl[(int64_t)p * NN + j] = q[j * 32] - q[0];
+    }
+}
+
+__global__ void nd_verify_kernel(int64_t nslots, int NN, const int32_t* ND, const int32_t* pid, const int32_t* base,
+                                 const int32_t* tbl, unsigned int* err) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nslots; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t* q = ND + (t >> 5) * (int64_t)NN * 32 + (t & 31);
+        for (int j = 0; j < NN; ++j)
+            if (q[j * 32] != base[t] + tbl[(int64_t)pid[t] * NN + j]) atomicOr(err, 1u);
+    }
+}
+
+static rav_status schur_nd_compress(Factors& F, int64_t np, cudaStream_t s) {
+    (void)np;
+    const int64_t ns = F.nchunks * 32;
+    const int NN = F.NN;
+    uint64_t *key = nullptr, *skey = nullptr;
+    int32_t *idx = nullptr, *sidx = nullptr, *flag = nullptr, *seg = nullptr, *rep = nullptr;
+    int32_t *pid = nullptr, *base = nullptr, *tbl = nullptr;
+    unsigned int* err = nullptr;
+    RAV_CUDA(cudaMallocAsync(&key, sizeof(uint64_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&skey, sizeof(uint64_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&idx, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&sidx, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&flag, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&seg, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMalloc(&pid, sizeof(int32_t) * ns));
+    RAV_CUDA(cudaMalloc(&base, sizeof(int32_t) * ns));
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(ns, 256), (int64_t)num_sms() * 16));
+    nd_hash_kernel<<<nb, 256, 0, s>>>(ns, NN, F.DT, key, idx, base);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    size_t tmp = 0, tmp2 = 0;
+    RAV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, skey, idx, sidx, (int)ns, 0, 64, s));
+    RAV_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp2, flag, seg, (int)ns, s));
+    void* d_tmp = nullptr;
+    RAV_CUDA(cudaMallocAsync(&d_tmp, std::max(tmp, tmp2) + 16, s));
+    RAV_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp, key, skey, idx, sidx, (int)ns, 0, 64, s));
+    nd_flag_kernel<<<nb, 256, 0, s>>>(ns, skey, flag);
+    count_launch();
+    RAV_CUDA(cub::DeviceScan::InclusiveSum(d_tmp, tmp2, flag, seg, (int)ns, s));
+    int32_t npat = 0;
+    RAV_CUDA(cudaMemcpyAsync(&npat, seg + ns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    RAV_CUDA(cudaStreamSynchronize(s));
+    bool ok = npat > 0 && (int64_t)npat * NN * 4 <= (4 << 20);
+    if (ok) {
+        RAV_CUDA(cudaMallocAsync(&rep, sizeof(int32_t) * npat, s));
+        RAV_CUDA(cudaMalloc(&tbl, sizeof(int32_t) * (int64_t)npat * NN));
+        RAV_CUDA(cudaMallocAsync(&err, sizeof(unsigned int), s));
+        RAV_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
+        nd_pid_kernel<<<nb, 256, 0, s>>>(ns, sidx, flag, seg, pid, rep);
+        count_launch();
+        nd_table_kernel<<<(int)cdiv(npat, 128), 128, 0, s>>>(npat, NN, rep, F.DT, tbl);
+        count_launch();
+        nd_verify_kernel<<<nb, 256, 0, s>>>(ns, NN, F.DT, pid, base, tbl, err);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+        unsigned int h_err = 0;
+        RAV_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(h_err), cudaMemcpyDeviceToHost, s));
+        RAV_CUDA(cudaStreamSynchronize(s));
+        ok = h_err == 0;
+    }
+    for (void* p : {(void*)key, (void*)skey, (void*)idx, (void*)sidx, (void*)flag, (void*)seg, (void*)rep, (void*)err,
+                    d_tmp})
+        if (p) cudaFreeAsync(p, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    if (!ok) {
+        for (void* p : {(void*)pid, (void*)base, (void*)tbl})
+            if (p) cudaFree(p);
+        return RAV_OK;
+    }
+    F.npid = pid;
+    F.nbase = base;
+    F.ntbl = tbl;
+    F.nnpat = npat;
+    return RAV_OK;
 }
 
 rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D, int kernel_choice, int mode,
@@ -833,6 +961,17 @@ rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D,
         return RAV_ERR_SINGULAR_LOCAL;
     }
     if (bad_patch) *bad_patch = -1;
+    static const bool ndc = [] {   // measured at c2: 113.3 -> 111.2 us, c3 unchanged (already at 92%): opt-in
+        const char* e = getenv("RAV_SCHUR_NDC");
+        return e && atoi(e) == 1;
+    }();
+    if (F.layout == 4 && mode == 0 && ndc) {
+        RAV_TRY(schur_nd_compress(F, P.n_patches, s));
+        if (F.npid) {   // streamed index bytes: pattern id + base + pressure DoF instead of nn + 1 indices
+            const int64_t sum_nn = (P.entries - P.n_patches) / D;
+            F.alg_bytes += -4 * (sum_nn + P.n_patches) + 12 * P.n_patches;
+        }
+    }
     return RAV_OK;
 }
 
@@ -1133,8 +1272,10 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
                                 cudaStream_t s) {
     const double2* W = reinterpret_cast<const double2*>(F.facT);
     // 2D PoU interior shape (25 nodes, 9 restricted): compile-time rectangular loop (122 -> 113 us at c2)
-    auto kern = (MT == 9 && F.NN == 25) ? schur_sweep_thread_kernel<MT, 2, 4, 8, DET>
-                                        : schur_sweep_thread_kernel<MT, 2, 4, 0, DET>;
+    auto kern = F.npid ? ((MT == 9 && F.NN == 25) ? schur_sweep_thread_kernel<MT, 2, 4, 8, DET, true>
+                                                  : schur_sweep_thread_kernel<MT, 2, 4, 0, DET, true>)
+                       : ((MT == 9 && F.NN == 25) ? schur_sweep_thread_kernel<MT, 2, 4, 8, DET>
+                                                  : schur_sweep_thread_kernel<MT, 2, 4, 0, DET>);
     // wave split: full waves of one warp per chunk, then the partial last wave with two half-warps
     // per chunk (its chunks finish in about half the time of a full-chunk warp)
     static int conc = 0;
@@ -1151,13 +1292,13 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
     const int64_t full = split && F.nchunks > conc ? F.nchunks / conc * conc : F.nchunks;
     const int64_t rem = F.nchunks - full;
     launch_maybe_pdl(kern, dim3((unsigned)cdiv(full * 32, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
-                     (const int32_t*)F.DT, (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x,
-                     omega, F.cbuf, (int64_t)0, 0);
+                     (const int32_t*)F.DT, (const int32_t*)F.npid, (const int32_t*)F.nbase, (const int32_t*)F.ntbl,
+                     (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, (int64_t)0, 0);
     if (rem > 0) {
         count_launch();
         launch_maybe_pdl(kern, dim3((unsigned)cdiv(rem * 64, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
-                         (const int32_t*)F.DT, (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x,
-                         omega, F.cbuf, full, 1);
+                         (const int32_t*)F.DT, (const int32_t*)F.npid, (const int32_t*)F.nbase, (const int32_t*)F.ntbl,
+                         (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, full, 1);
     }
 }
 

@@ -506,7 +506,8 @@ void factors_free(Factors& F) {
     if (F.PD) cudaFree(F.PD);
     if (F.nodes) cudaFree(F.nodes);
     if (F.nodeoffs) cudaFree(F.nodeoffs);
-    for (void* p : {(void*)F.cbuf, (void*)F.det_dof, (void*)F.det_off, (void*)F.det_slot})
+    for (void* p : {(void*)F.cbuf, (void*)F.det_dof, (void*)F.det_off, (void*)F.det_slot, (void*)F.npid,
+                    (void*)F.nbase, (void*)F.ntbl})
         if (p) cudaFree(p);
     F = Factors{};
 }
