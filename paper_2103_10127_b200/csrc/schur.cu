@@ -817,7 +817,14 @@ rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D,
     if ((a.ld & 15) == 0) a.ld += 1;
     a.MT = MT;
     if (mode == 1) a.mnmax = nnmax;   // diagonal Vanka: any number of weighted nodes
-    const bool thread = mode == 0 && kernel_choice != RAV_KERNEL_WARP && D == 2 && MT <= 9 && nnmax <= 32;
+    // small levels (few patches: latency-bound) take the per-patch layout, whose CTA / warp kernels
+    // spread one patch over many lanes; the thread-per-patch SoA layout needs many patches to fill the GPU
+    static const int64_t small = [] {
+        const char* e = getenv("RAV_SCHUR_SMALL");
+        return e ? atoll(e) : 4096;
+    }();
+    const bool thread = mode == 0 && kernel_choice != RAV_KERNEL_WARP && D == 2 && MT <= 9 && nnmax <= 32 &&
+                        (P.n_patches >= small || kernel_choice == RAV_KERNEL_SCHUR);
     F.nchunks = cdiv(P.n_patches, 32);
     F.mode = mode;
     if (mode == 1) {
