@@ -423,6 +423,34 @@ def run_adaptive_study(rg, si, stream, max_levels=7):
         row["elements"] = fine["n_cells"]
         row["dofs"] = fine["n"]
         out[f"M{L}"] = row
+    # smoothing-step study on M6 (Fig. 7 / P:199-213, here on the cavity's own adaptive grids)
+    steps = {}
+    for ns in range(1, 7):
+        row = {}
+        for name, w, v, om in (("rav", "own", rg.VARIANT_ROWS, 0.66), ("mv_color", "full", rg.VARIANT_MV, 0.66),
+                               ("av", "full", rg.VARIANT_ROWS, 0.1)):
+            mg, fine = rg.build_adaptive_hierarchy(prob, 6, w, variant=v)
+            x = torch.zeros(fine["n"], dtype=torch.float64, device="cuda")
+            r = {}
+            try:
+                mg.solve(x, fine["b"], pre=ns, post=ns, omega=om, rtol=1e-8, maxit=2)
+                x.zero_()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                x, k, h = mg.solve(x, fine["b"], pre=ns, post=ns, omega=om, rtol=1e-8, maxit=300)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                r = {"cycles": k, "converged": bool(h[-1] <= 1e-8 * h[0]), "time_s": e0.elapsed_time(e1) / 1e3,
+                     "avg_reduction_factor": (h[-1] / h[0]) ** (1.0 / max(k, 1))}
+            except rg.RavError as err:
+                r = {"converged": False, "diverged": str(err)[:120]}
+            row[name] = r
+            mg.close()
+            del mg, x
+            torch.cuda.empty_cache()
+        steps[f"nS={ns}"] = row
+    out["smoothing_steps_M6"] = steps
     return out
 
 
