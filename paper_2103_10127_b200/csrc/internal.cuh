@@ -35,6 +35,7 @@ struct NodeBlocked {
     int64_t *cptr = nullptr, *vptr = nullptr;
     int32_t* col = nullptr;
     double* val = nullptr;
+    int pair = 0;              // D = 2: values stored as 16-byte pairs (nb.cu, slot layout)
     int64_t bytes = 0;
     // stencil-compressed columns (structured operators): slot t's columns are base + the offsets
     // of its pattern pid[t] (tbl[pid * W + k]; A entries first, then B); col is then freed

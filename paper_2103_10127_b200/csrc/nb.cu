@@ -12,7 +12,9 @@
 // i.e. 12*nnz(A)/d + (4 + 8d)*nnz(B)/d*2 bytes instead of 12*nnz: -35% at c2.
 // Block rows are sorted by length in windows of 4096 and stored as SELL slices
 // of 32 rows (column-major), one thread per block row producing all d residual
-// components (x gathered as d contiguous values).  Each component sums its A
+// components (x gathered as d contiguous values).  For d = 2 the values are
+// stored as 16-byte pairs per slot (two consecutive A entries; the two
+// components of a B / BT entry), so a warp-wide load moves 512 contiguous bytes.  Each component sums its A
 // entries then its B entries in ascending column order -- the CSR order -- so
 // the result equals the CSR residual up to FMA contraction.
 //
@@ -107,11 +109,26 @@ __global__ void nb_slice_kernel(int64_t n, int64_t nslices, int D, const int32_t
     }
 }
 
+// value layout of a slice of width (A, B), lane l, relative to the slice's first value:
+//   plain: A entry k at k*32 + l; B entry (k, c) at A*32 + (k*D + c)*32 + l
+//   pair (D = 2): A entries (2p, 2p+1) at (p*32 + l)*2 + {0,1}, an odd last A entry at
+//                 (A & ~1)*32 + l; B entry (k, c) at A*32 + (k*32 + l)*2 + c
+// Both occupy 32*(A + D*B) values; the pair layout keeps every 16-byte slot pair contiguous.
+__device__ __forceinline__ int64_t nb_ia(bool pair, int A, int k, int l) {
+    if (!pair) return (int64_t)k * NB_C + l;
+    const int A2 = A & ~1;
+    return k < A2 ? ((int64_t)(k >> 1) * NB_C + l) * 2 + (k & 1) : (int64_t)A2 * NB_C + l;
+}
+__device__ __forceinline__ int64_t nb_ib(bool pair, int D, int A, int k, int c, int l) {
+    return (int64_t)A * NB_C + (pair ? ((int64_t)k * NB_C + l) * 2 + c : ((int64_t)k * D + c) * NB_C + l);
+}
+
 // slot t = 32 s + l; node rows: A cols/vals then B cols / D vals; pressure rows: BT cols (node dof of comp 0) / D vals
 __global__ void nb_fill_kernel(int64_t n, int64_t nnodes, int64_t nslices, int D, int64_t nvel, const int64_t* rp,
                                const int32_t* ci, const double* val, const int32_t* perm, const int32_t* wa,
                                const int32_t* wb, const int64_t* cptr, const int64_t* vptr, int32_t* col,
-                               double* v) {
+                               double* v, int pair_i) {
+    const bool pair = pair_i != 0;
     const int64_t total = nslices * NB_C;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = t / NB_C;
@@ -119,13 +136,14 @@ __global__ void nb_fill_kernel(int64_t n, int64_t nnodes, int64_t nslices, int D
         const int A = wa[s], B = wb[s];
         int32_t* cA = col + cptr[s] + l;
         int32_t* cB = cA + (int64_t)A * NB_C;
-        double* vA = v + vptr[s] + l;
-        double* vB = vA + (int64_t)A * NB_C;
+        double* vs = v + vptr[s];
+#define NB_VA(k) vs[nb_ia(pair, A, (k), l)]
+#define NB_VB(k, c) vs[nb_ib(pair, D, A, (k), (c), l)]
         if (t >= n) {
-            for (int k = 0; k < A; ++k) { cA[k * NB_C] = 0; vA[k * NB_C] = 0.0; }
+            for (int k = 0; k < A; ++k) { cA[k * NB_C] = 0; NB_VA(k) = 0.0; }
             for (int k = 0; k < B; ++k) {
                 cB[k * NB_C] = 0;
-                for (int c = 0; c < D; ++c) vB[((int64_t)k * D + c) * NB_C] = 0.0;
+                for (int c = 0; c < D; ++c) NB_VB(k, c) = 0.0;
             }
             continue;
         }
@@ -138,33 +156,35 @@ __global__ void nb_fill_kernel(int64_t n, int64_t nnodes, int64_t nslices, int D
                 const int c = ci[k];
                 if (c < nvel) {
                     cA[a * NB_C] = c;
-                    vA[a * NB_C] = val[k];
+                    NB_VA(a) = val[k];
                     ++a;
                 } else {
                     cB[b * NB_C] = c;
-                    for (int cc = 0; cc < D; ++cc) vB[((int64_t)b * D + cc) * NB_C] = val[rp[r0 + cc] + (k - s0)];
+                    for (int cc = 0; cc < D; ++cc) NB_VB(b, cc) = val[rp[r0 + cc] + (k - s0)];
                     ++b;
                 }
             }
-            for (; a < A; ++a) { cA[a * NB_C] = (int32_t)r0; vA[a * NB_C] = 0.0; }
+            for (; a < A; ++a) { cA[a * NB_C] = (int32_t)r0; NB_VA(a) = 0.0; }
             for (; b < B; ++b) {
                 cB[b * NB_C] = (int32_t)nvel;
-                for (int cc = 0; cc < D; ++cc) vB[((int64_t)b * D + cc) * NB_C] = 0.0;
+                for (int cc = 0; cc < D; ++cc) NB_VB(b, cc) = 0.0;
             }
         } else {
             const int64_t row = nvel + (br - nnodes);
             const int64_t s0 = rp[row], e0 = rp[row + 1];
-            for (int a = 0; a < A; ++a) { cA[a * NB_C] = 0; vA[a * NB_C] = 0.0; }
+            for (int a = 0; a < A; ++a) { cA[a * NB_C] = 0; NB_VA(a) = 0.0; }
             int q = 0;
             for (int64_t k = s0; k < e0; k += D, ++q) {
                 cB[q * NB_C] = ci[k];   // component-0 dof of the node
-                for (int cc = 0; cc < D; ++cc) vB[((int64_t)q * D + cc) * NB_C] = val[k + cc];
+                for (int cc = 0; cc < D; ++cc) NB_VB(q, cc) = val[k + cc];
             }
             for (; q < B; ++q) {
                 cB[q * NB_C] = 0;
-                for (int cc = 0; cc < D; ++cc) vB[((int64_t)q * D + cc) * NB_C] = 0.0;
+                for (int cc = 0; cc < D; ++cc) NB_VB(q, cc) = 0.0;
             }
         }
+#undef NB_VA
+#undef NB_VB
     }
 }
 
@@ -182,7 +202,7 @@ struct NbCols {
     int W;
 };
 
-template <int D, int G, int UA, int MINB = 1, bool PAT = false>
+template <int D, int G, int UA, int MINB = 1, bool PAT = false, bool PR = false>
 __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64_t nnodes, int64_t nslices, int64_t nvel,
                                                           const int32_t* __restrict__ perm,
                                                           const int32_t* __restrict__ wa,
@@ -193,11 +213,14 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                                                           const double* __restrict__ v, const double* __restrict__ x,
                                                           const double* __restrict__ b, double* __restrict__ r,
                                                           double* __restrict__ part) {
+    static_assert(!PR || D == 2, "pair layout is 2D only");
     const int32_t* __restrict__ col = cols.col;
     __shared__ double red[8];
     double mine = 0.0;
     const int64_t total = nslices * NB_C * G;
     const int q = threadIdx.x % G;
+    // 16-byte vector access to b / r for the d = 2 node rows (uniform: depends on the pointers only)
+    const bool v2 = PR && ((reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(r)) & 15) == 0;
     pdl_trigger();
     if (G == 1) {   // before x exists: this warp's first slice lines (values, columns) into L2
         const int64_t s0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / NB_C;
@@ -224,8 +247,11 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
         const int32_t bA = PAT && live ? cols.baseA[t] : 0, bB = PAT && live ? cols.baseB[t] : 0;
 #define NB_COLA(k) (PAT ? bA + __ldg(tp + (k)) : __ldcs(cA + (k) * NB_C))
 #define NB_COLB(k) (PAT ? bB + __ldg(tp + A + (k)) : __ldcs(cB + (k) * NB_C))
-        const double* vA = v + (live ? vptr[s] : 0) + l;
+        const double* vs = v + (live ? vptr[s] : 0);   // the slice's values (layout: nb_ia / nb_ib)
+        const double* vA = vs + l;                     // plain layout
         const double* vB = vA + (int64_t)A * NB_C;
+        const double2* pA = reinterpret_cast<const double2*>(vs) + l;                      // pair layout
+        const double2* pB = reinterpret_cast<const double2*>(vs + (int64_t)A * NB_C) + l;
         const int64_t br = (live && t < n) ? perm[t] : -1;
         if constexpr (G == 1) {   // one thread per row: per-branch accumulation (no shuffles)
             if (br < 0) continue;
@@ -233,35 +259,84 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                 double acc[D];
 #pragma unroll
                 for (int c = 0; c < D; ++c) acc[c] = 0.0;
-#pragma unroll UA
-                for (int k = 0; k < A; ++k) {
-                    const int cc = NB_COLA(k);
-                    const double a = __ldcs(vA + k * NB_C);
-                    double xv[D];
-                    ld_node<D>(x + cc, xv);
-#pragma unroll
-                    for (int c = 0; c < D; ++c) acc[c] = fma(a, xv[c], acc[c]);
-                }
+                if constexpr (PR) {
+                    const int A2 = A >> 1;
+                    // two entries per iteration; a second iteration in flight only with the 48-register cap
+#pragma unroll (MINB <= 5 ? 2 : 1)
+                    for (int p = 0; p < A2; ++p) {
+                        const double2 a = __ldcs(pA + (int64_t)p * NB_C);
+                        double x0[2], x1[2];
+                        ld_node<2>(x + NB_COLA(2 * p), x0);
+                        ld_node<2>(x + NB_COLA(2 * p + 1), x1);
+                        acc[0] = fma(a.x, x0[0], acc[0]);
+                        acc[1] = fma(a.x, x0[1], acc[1]);
+                        acc[0] = fma(a.y, x1[0], acc[0]);
+                        acc[1] = fma(a.y, x1[1], acc[1]);
+                    }
+                    if (A & 1) {
+                        const double a = __ldcs(vs + (int64_t)(2 * A2) * NB_C + l);
+                        double x0[2];
+                        ld_node<2>(x + NB_COLA(A - 1), x0);
+                        acc[0] = fma(a, x0[0], acc[0]);
+                        acc[1] = fma(a, x0[1], acc[1]);
+                    }
 #pragma unroll 2
-                for (int k = 0; k < B; ++k) {
-                    const double xp = __ldg(x + NB_COLB(k));
+                    for (int k = 0; k < B; ++k) {
+                        const double xp = __ldg(x + NB_COLB(k));
+                        const double2 bv = __ldcs(pB + (int64_t)k * NB_C);
+                        acc[0] = fma(bv.x, xp, acc[0]);
+                        acc[1] = fma(bv.y, xp, acc[1]);
+                    }
+                } else {
+#pragma unroll UA
+                    for (int k = 0; k < A; ++k) {
+                        const int cc = NB_COLA(k);
+                        const double a = __ldcs(vA + k * NB_C);
+                        double xv[D];
+                        ld_node<D>(x + cc, xv);
 #pragma unroll
-                    for (int c = 0; c < D; ++c) acc[c] = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), xp, acc[c]);
+                        for (int c = 0; c < D; ++c) acc[c] = fma(a, xv[c], acc[c]);
+                    }
+#pragma unroll 2
+                    for (int k = 0; k < B; ++k) {
+                        const double xp = __ldg(x + NB_COLB(k));
+#pragma unroll
+                        for (int c = 0; c < D; ++c) acc[c] = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), xp, acc[c]);
+                    }
                 }
                 const int64_t r0 = br * D;
+                if (PR && v2) {
+                    const double2 bb = __ldg(reinterpret_cast<const double2*>(b + r0));
+                    const double2 rr = make_double2(bb.x - acc[0], bb.y - acc[D - 1]);
+                    if (r) *reinterpret_cast<double2*>(r + r0) = rr;
+                    mine += rr.x * rr.x;
+                    mine += rr.y * rr.y;
+                } else {
 #pragma unroll
-                for (int c = 0; c < D; ++c) {
-                    const double rr = b[r0 + c] - acc[c];
-                    if (r) r[r0 + c] = rr;
-                    mine += rr * rr;
+                    for (int c = 0; c < D; ++c) {
+                        const double rr = b[r0 + c] - acc[c];
+                        if (r) r[r0 + c] = rr;
+                        mine += rr * rr;
+                    }
                 }
             } else {
                 double acc = 0.0;
+                if constexpr (PR) {
 #pragma unroll UA
-                for (int k = 0; k < B; ++k) {
-                    const int cc = NB_COLB(k);
+                    for (int k = 0; k < B; ++k) {
+                        double xv[2];
+                        ld_node<2>(x + NB_COLB(k), xv);
+                        const double2 bv = __ldcs(pB + (int64_t)k * NB_C);
+                        acc = fma(bv.x, xv[0], acc);
+                        acc = fma(bv.y, xv[1], acc);
+                    }
+                } else {
+#pragma unroll UA
+                    for (int k = 0; k < B; ++k) {
+                        const int cc = NB_COLB(k);
 #pragma unroll
-                    for (int c = 0; c < D; ++c) acc = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), __ldg(x + cc + c), acc);
+                        for (int c = 0; c < D; ++c) acc = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), __ldg(x + cc + c), acc);
+                    }
                 }
                 const int64_t row = nvel + (br - nnodes);
                 const double rr = b[row] - acc;
@@ -279,7 +354,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
 #pragma unroll UA
             for (int k = q; k < A; k += G) {
                 const int cc = NB_COLA(k);
-                const double a = __ldcs(vA + k * NB_C);
+                const double a = __ldcs(vs + nb_ia(PR, A, k, l));
                 double xv[D];
                 ld_node<D>(x + cc, xv);
 #pragma unroll
@@ -289,7 +364,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
             for (int k = q; k < B; k += G) {
                 const double xp = __ldg(x + NB_COLB(k));
 #pragma unroll
-                for (int c = 0; c < D; ++c) acc[c] = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), xp, acc[c]);
+                for (int c = 0; c < D; ++c) acc[c] = fma(__ldcs(vs + nb_ib(PR, D, A, k, c, l)), xp, acc[c]);
             }
         } else if (br >= 0) {
 #pragma unroll UA
@@ -297,7 +372,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                 const int cc = NB_COLB(k);
 #pragma unroll
                 for (int c = 0; c < D; ++c)
-                    acc[0] = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), __ldg(x + cc + c), acc[0]);
+                    acc[0] = fma(__ldcs(vs + nb_ib(PR, D, A, k, c, l)), __ldg(x + cc + c), acc[0]);
             }
         }
         if (G > 1) {
@@ -564,9 +639,14 @@ rav_status nb_build(Csr& A, int64_t nvel, int D, cudaStream_t s) {
     RAV_CUDA(cudaMalloc(&N.col, sizeof(int32_t) * std::max<int64_t>(1, hc)));
     RAV_CUDA(cudaMalloc(&N.val, sizeof(double) * std::max<int64_t>(1, hv)));
     N.bytes = 4 * hc + 8 * hv;
+    static const bool pair_env = [] {
+        const char* e = getenv("RAV_NB_PAIR");   // 16-byte value pairs for d = 2 (default on)
+        return !(e && atoi(e) == 0);
+    }();
+    N.pair = (D == 2 && pair_env) ? 1 : 0;
     const int nbf = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(N.nslices * NB_C, 256), (int64_t)num_sms() * 16));
     nb_fill_kernel<<<nbf, 256, 0, s>>>(n, nnodes, N.nslices, D, nvel, A.rp, A.ci, A.val, N.perm, N.wa, N.wb, N.cptr,
-                                       N.vptr, N.col, N.val);
+                                       N.vptr, N.col, N.val, N.pair);
     count_launch();
     RAV_CHECK_LAUNCH();
     for (void* p : {(void*)na, (void*)nbv, (void*)key, (void*)skey, (void*)idx, (void*)woff, d_tmp, (void*)csz,
@@ -589,7 +669,7 @@ void nb_free(NodeBlocked& N) {
     N = NodeBlocked{};
 }
 
-template <int D, int G, int UA>
+template <int D, int G, int UA, bool PR = false>
 static void nb_launch(const NodeBlocked& N, const double* x, const double* b, double* r, double* part, int nblk,
                       cudaStream_t s, int* used) {
     const NbCols cols{N.col, N.pid, N.baseA, N.baseB, N.tbl, N.W};
@@ -601,11 +681,13 @@ static void nb_launch(const NodeBlocked& N, const double* x, const double* b, do
         const char* e = getenv("RAV_NB_MINB");
         return e ? atoi(e) : 6;
     }();
-    auto kern = N.tbl ? ((minb >= 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6, true> : nb_residual_kernel<D, G, UA, 1, true>)
-              : (minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8>
-              : (minb == 7 && G == 1) ? nb_residual_kernel<D, G, UA, 7>
-              : (minb == 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6>
-              : (minb == 5 && G == 1) ? nb_residual_kernel<D, G, UA, 5> : nb_residual_kernel<D, G, UA, 1>;
+    auto kern = N.tbl ? ((minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8, true, PR>
+                         : (minb >= 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6, true, PR>
+                         : (minb == 5 && G == 1) ? nb_residual_kernel<D, G, UA, 5, true, PR>
+                                                 : nb_residual_kernel<D, G, UA, 1, true, PR>)
+              : (minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8, false, PR>
+              : (minb >= 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6, false, PR>
+                                      : nb_residual_kernel<D, G, UA, 1, false, PR>;
     launch_maybe_pdl(kern, dim3(blocks), dim3(256), 0, s, N.nblock, N.nnodes, N.nslices,
                      N.nvel, (const int32_t*)N.perm, (const int32_t*)N.wa, (const int32_t*)N.wb,
                      (const int64_t*)N.cptr, (const int64_t*)N.vptr, cols, (const double*)N.val, x, b,
@@ -639,11 +721,19 @@ rav_status launch_nb_residual(const Csr& A, const double* x, const double* b, do
         else if (G == 2) nb_launch<3, 2, 4>(N, x, b, r, part, nblk, s, used);
         else nb_launch<3, 1, 8>(N, x, b, r, part, nblk, s, used);
     } else {
-        if (G == 32) nb_launch<2, 32, 2>(N, x, b, r, part, nblk, s, used);
-        else if (G == 8) nb_launch<2, 8, 4>(N, x, b, r, part, nblk, s, used);
-        else if (G >= 4) nb_launch<2, 4, 4>(N, x, b, r, part, nblk, s, used);
-        else if (G == 2) nb_launch<2, 2, 4>(N, x, b, r, part, nblk, s, used);
-        else nb_launch<2, 1, 4>(N, x, b, r, part, nblk, s, used);
+        if (N.pair) {
+            if (G == 32) nb_launch<2, 32, 2, true>(N, x, b, r, part, nblk, s, used);
+            else if (G == 8) nb_launch<2, 8, 4, true>(N, x, b, r, part, nblk, s, used);
+            else if (G >= 4) nb_launch<2, 4, 4, true>(N, x, b, r, part, nblk, s, used);
+            else if (G == 2) nb_launch<2, 2, 4, true>(N, x, b, r, part, nblk, s, used);
+            else nb_launch<2, 1, 4, true>(N, x, b, r, part, nblk, s, used);
+        } else {
+            if (G == 32) nb_launch<2, 32, 2>(N, x, b, r, part, nblk, s, used);
+            else if (G == 8) nb_launch<2, 8, 4>(N, x, b, r, part, nblk, s, used);
+            else if (G >= 4) nb_launch<2, 4, 4>(N, x, b, r, part, nblk, s, used);
+            else if (G == 2) nb_launch<2, 2, 4>(N, x, b, r, part, nblk, s, used);
+            else nb_launch<2, 1, 4>(N, x, b, r, part, nblk, s, used);
+        }
     }
     count_launch();
     RAV_CHECK_LAUNCH();
