@@ -421,7 +421,8 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
                                                                  const double* __restrict__ AUX,
                                                                  const double* __restrict__ r,
                                                                  double* __restrict__ x, double omega,
-                                                                 double* __restrict__ cbuf, int64_t chunk0, int half) {
+                                                                 double* __restrict__ cbuf, int64_t chunk0, int half,
+                                                                 int pf) {
     constexpr int TRI = MT * (MT + 1) / 2 + MT * D;
     constexpr int TRI_PAD = TRI + (TRI & 1);
     constexpr int RC = MT + D;   // entries per rectangular column
@@ -446,6 +447,9 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
         }
         const int lines = (int)(pairs * 4 < 128 ? pairs * 4 : 128);
         for (int ln = lane; ln < lines; ln += 32) prefetch_l2(wc + (size_t)ln * 128);
+        // NRB > 0: the first pf rectangular blocks by one bulk prefetch (the rest rolls inside the loop)
+        if (NRB > 0 && pf > 0 && !half && lane == 0)
+            bulk_prefetch_l2(wc + (size_t)(TRI_PAD / 2) * 512, (uint32_t)(min(pf, NRB) * RC * 512));
     }
     pdl_wait();
     double acc[MT][D], rr[MT][D], gR[MT][D];
@@ -488,6 +492,8 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
     for (int b = 0; b < (NRB > 0 ? NRB : 1 << 20); ++b) {
         if (NRB == 0 && b >= nrb) break;
         const int j0 = MT + 2 * b;
+        if (NRB > 0 && pf > 0 && !half && lane == 0 && b + pf < NRB)   // rolling: block b + pf into L2
+            bulk_prefetch_l2(W + chunk * pairs * 32 + (int64_t)(TRI_PAD / 2 + (b + pf) * RC) * 32, (uint32_t)(RC * 512));
         double ra[D], rb[D];
         const int n0 = ND_AT(j0), n1 = ND_AT(j0 + 1);
         ld_node<D>(r + n0, ra);
@@ -1292,6 +1298,12 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
         cudaGetLastError();
         conc = std::max(1, per_sm) * 4 * num_sms();   // resident warps (4 per block)
     }
+    // rectangular blocks prefetched ahead by the bulk-copy unit (0: off).  Measured (rav_apply alone):
+    // c2 115.0 / 109.7 / 108.9 / 110.3 / 117.0 us for 0 / 1 / 2 / 3 / 5; c3 1606 -> 1474 us at 2
+    static const int pf = [] {
+        const char* e = getenv("RAV_SCHUR_PF");
+        return e ? atoi(e) : 2;
+    }();
     static const bool split = [] {   // measured at c2: 119.5 us split vs 114.0 us single launch -> off
         const char* e = getenv("RAV_SCHUR_TAIL");
         return e && atoi(e) == 1;
@@ -1300,12 +1312,12 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
     const int64_t rem = F.nchunks - full;
     launch_maybe_pdl(kern, dim3((unsigned)cdiv(full * 32, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
                      (const int32_t*)F.DT, (const int32_t*)F.npid, (const int32_t*)F.nbase, (const int32_t*)F.ntbl,
-                     (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, (int64_t)0, 0);
+                     (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, (int64_t)0, 0, pf);
     if (rem > 0) {
         count_launch();
         launch_maybe_pdl(kern, dim3((unsigned)cdiv(rem * 64, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
                          (const int32_t*)F.DT, (const int32_t*)F.npid, (const int32_t*)F.nbase, (const int32_t*)F.ntbl,
-                         (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, full, 1);
+                         (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, full, 1, pf);
     }
 }
 
