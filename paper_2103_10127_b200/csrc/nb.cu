@@ -223,6 +223,12 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
     // 16-byte vector access to b / r for the d = 2 node rows (uniform: depends on the pointers only)
     const bool v2 = PR && ((reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(r)) & 15) == 0;
     pdl_trigger();
+    if (G > 1 && cols.bulk) {   // the first warp of each slice prefetches the whole slice
+        const int64_t t0 = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) / G;
+        const int64_t s0 = t0 / NB_C;
+        if (s0 < nslices && t0 % NB_C == 0 && (threadIdx.x & 31) == 0)
+            bulk_prefetch_l2(v + vptr[s0], (uint32_t)((vptr[s0 + 1] - vptr[s0]) * 8));
+    }
     if (G == 1) {   // before x exists: this warp's first slice lines (values, columns) into L2
         const int64_t s0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / NB_C;
         const int lane = threadIdx.x & 31;

@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
                                                                  const double* __restrict__ r,
                                                                  double* __restrict__ x, double omega,
                                                                  double* __restrict__ cbuf, int64_t chunk0, int half,
-                                                                 int pf) {
+                                                                 int pf, int64_t tail0) {
     constexpr int TRI = MT * (MT + 1) / 2 + MT * D;
     constexpr int TRI_PAD = TRI + (TRI & 1);
     constexpr int RC = MT + D;   // entries per rectangular column
@@ -447,9 +447,11 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
         }
         const int lines = (int)(pairs * 4 < 128 ? pairs * 4 : 128);
         for (int ln = lane; ln < lines; ln += 32) prefetch_l2(wc + (size_t)ln * 128);
-        // NRB > 0: the first pf rectangular blocks by one bulk prefetch (the rest rolls inside the loop)
+        // NRB > 0: the first pf rectangular blocks by one bulk prefetch (the rest rolls inside the loop);
+        // chunks of the last partial wave (chunk >= tail0, L2 no longer shared with full waves): all of them
         if (NRB > 0 && pf > 0 && !half && lane == 0)
-            bulk_prefetch_l2(wc + (size_t)(TRI_PAD / 2) * 512, (uint32_t)(min(pf, NRB) * RC * 512));
+            bulk_prefetch_l2(wc + (size_t)(TRI_PAD / 2) * 512, (uint32_t)((chunk >= tail0 ? NRB : min(pf, NRB)) * RC * 512));
+        if (chunk >= tail0) pf = 0;
     }
     pdl_wait();
     double acc[MT][D], rr[MT][D], gR[MT][D];
@@ -555,14 +557,37 @@ __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int M
                                                                const int32_t* __restrict__ nresn,
                                                                const double* __restrict__ fac,
                                                                const double* __restrict__ r, double* __restrict__ x,
-                                                               double omega, double* __restrict__ cbuf) {
+                                                               double omega, double* __restrict__ cbuf, int wpf) {
     extern __shared__ double sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* rl = sm + (size_t)warp * nnmax * D;
     for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < np; i += (int64_t)gridDim.x * 8) {
+        if (lane == 0 && wpf > 0) {   // this patch's (and with wpf = 2 the next one's) factor block into L2
+            const int64_t last = wpf > 1 ? min(i + (int64_t)gridDim.x * 8, np - 1) : i;
+            for (int64_t k = i; k <= last; k += (int64_t)gridDim.x * 8) {
+                const uintptr_t a0 = reinterpret_cast<uintptr_t>(fac + foffs[k]) & ~(uintptr_t)15;
+                const uintptr_t a1 = (reinterpret_cast<uintptr_t>(fac + foffs[k + 1]) + 15) & ~(uintptr_t)15;
+                bulk_prefetch_l2(reinterpret_cast<const void*>(a0), (uint32_t)(a1 - a0));
+            }
+        }
         const int64_t no = nodeoffs[i];
         const int nn = (int)(nodeoffs[i + 1] - no);
-        for (int t = lane; t < nn * D; t += 32) rl[t] = __ldg(r + nodes[no + t / D] + (t % D));
+        {   // gather r of the patch's nodes: lane takes nodes lane + 32u (independent index loads first)
+            int nd[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) nd[u] = lane + 32 * u < nn ? __ldg(nodes + no + lane + 32 * u) : -1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (nd[u] >= 0) {
+#pragma unroll
+                    for (int c = 0; c < D; ++c) rl[(lane + 32 * u) * D + c] = __ldg(r + nd[u] + c);
+                }
+            for (int j = lane + 128; j < nn; j += 32) {
+                const int n1 = __ldg(nodes + no + j);
+#pragma unroll
+                for (int c = 0; c < D; ++c) rl[j * D + c] = __ldg(r + n1 + c);
+            }
+        }
         __syncwarp();
         const double* Y = fac + foffs[i];
         const double* g = Y + (size_t)MT * nn;
@@ -571,7 +596,18 @@ __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int M
 #pragma unroll
         for (int c = 0; c < D; ++c) acc[c] = 0.0;
         if (lane < MT) {
-            for (int j = 0; j < nn; ++j) {
+            // batches of 8 independent column loads in flight per lane (the loop is latency-bound otherwise)
+            int j = 0;
+            for (; j + 8 <= nn; j += 8) {
+                double y[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) y[u] = __ldcs(Y + (size_t)(j + u) * MT + lane);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                    for (int c = 0; c < D; ++c) acc[c] = fma(y[u], rl[(j + u) * D + c], acc[c]);
+            }
+            for (; j < nn; ++j) {
                 const double y = __ldcs(Y + (size_t)j * MT + lane);
 #pragma unroll
                 for (int c = 0; c < D; ++c) acc[c] = fma(y, rl[j * D + c], acc[c]);
@@ -1308,16 +1344,21 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
         const char* e = getenv("RAV_SCHUR_TAIL");
         return e && atoi(e) == 1;
     }();
+    static const int tailpf = [] {   // whole-chunk prefetch for the last partial wave (c2: 111.2 vs 109.2 us -> off)
+        const char* e = getenv("RAV_SCHUR_TAILPF");
+        return e ? atoi(e) : 0;
+    }();
+    const int64_t tail0 = tailpf ? F.nchunks / conc * conc : F.nchunks;
     const int64_t full = split && F.nchunks > conc ? F.nchunks / conc * conc : F.nchunks;
     const int64_t rem = F.nchunks - full;
     launch_maybe_pdl(kern, dim3((unsigned)cdiv(full * 32, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
                      (const int32_t*)F.DT, (const int32_t*)F.npid, (const int32_t*)F.nbase, (const int32_t*)F.ntbl,
-                     (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, (int64_t)0, 0, pf);
+                     (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, (int64_t)0, 0, pf, tail0);
     if (rem > 0) {
         count_launch();
         launch_maybe_pdl(kern, dim3((unsigned)cdiv(rem * 64, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
                          (const int32_t*)F.DT, (const int32_t*)F.npid, (const int32_t*)F.nbase, (const int32_t*)F.ntbl,
-                         (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, full, 1, pf);
+                         (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, full, 1, pf, tail0);
     }
 }
 
@@ -1331,8 +1372,13 @@ static void launch_schur_perpatch(const PatchSet& P, const Factors& F, const dou
     } else {
         const size_t shmem = sizeof(double) * (size_t)F.NN * D * 8;
         const int blocks = (int)std::min<int64_t>(cdiv(P.n_patches, 8), (int64_t)num_sms() * 16);
+        static const int wpf = [] {   // per-patch bulk prefetch (c4, batched loads: 188.4 us off, 194.9 on)
+            const char* e = getenv("RAV_SCHUR_WPF");
+            return e ? atoi(e) : 0;
+        }();
         schur_sweep_warp_kernel<D, DET><<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs,
-                                                                   F.nodes, F.PD, F.NR, F.fac, r, x, omega, F.cbuf);
+                                                                   F.nodes, F.PD, F.NR, F.fac, r, x, omega, F.cbuf,
+                                                                   wpf);
     }
 }
 
