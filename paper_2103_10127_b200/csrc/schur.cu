@@ -454,7 +454,11 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
         if (chunk >= tail0) pf = 0;
     }
     pdl_wait();
-    double acc[MT][D], rr[MT][D], gR[MT][D];
+    // MINB > 4: g_R lives in shared memory (one column per thread, conflict-free), which frees 2 MT D
+    // registers for a higher residency
+    constexpr bool SG = MINB > 4;
+    __shared__ double sgR[SG ? MT * D : 1][SG ? 128 : 1];
+    double acc[MT][D], rr[MT][D], gR[SG ? 1 : MT][SG ? 1 : D];
     double gacc = 0.0;
 #pragma unroll
     for (int k = 0; k < MT; ++k) {
@@ -482,7 +486,8 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
                 }
             } else {
                 const int c = q - j - 1;
-                gR[j][c] = v;
+                if constexpr (SG) sgR[j * D + c][threadIdx.x] = v;
+                else gR[j][c] = v;
                 gacc = fma(v, rr[j][c], gacc);
             }
         }
@@ -532,7 +537,8 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
             const int nd = ND_AT(k);
 #pragma unroll
             for (int c = 0; c < D; ++c) {
-                const double v = wk * fma(gR[k][c], t, acc[k][c]);
+                const double gk = SG ? sgR[k * D + c][threadIdx.x] : gR[SG ? 0 : k][SG ? 0 : c];
+                const double v = wk * fma(gk, t, acc[k][c]);
                 if (DET) cb[k * D + c] = v;
                 else atomicAdd(x + nd + c, v);
             }
@@ -1321,10 +1327,16 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
                                 cudaStream_t s) {
     const double2* W = reinterpret_cast<const double2*>(F.facT);
     // 2D PoU interior shape (25 nodes, 9 restricted): compile-time rectangular loop (122 -> 113 us at c2)
+    static const int minb = [] {   // residency: 4 blocks of 128 (g_R in registers) or 5 (g_R in smem)
+        const char* e = getenv("RAV_SCHUR_MINB");
+        return e ? atoi(e) : 4;
+    }();
     auto kern = F.npid ? ((MT == 9 && F.NN == 25) ? schur_sweep_thread_kernel<MT, 2, 4, 8, DET, true>
                                                   : schur_sweep_thread_kernel<MT, 2, 4, 0, DET, true>)
-                       : ((MT == 9 && F.NN == 25) ? schur_sweep_thread_kernel<MT, 2, 4, 8, DET>
-                                                  : schur_sweep_thread_kernel<MT, 2, 4, 0, DET>);
+              : (MT == 9 && F.NN == 25) ? (minb >= 6 ? schur_sweep_thread_kernel<MT, 2, 6, 8, DET>
+                                           : minb == 5 ? schur_sweep_thread_kernel<MT, 2, 5, 8, DET>
+                                                       : schur_sweep_thread_kernel<MT, 2, 4, 8, DET>)
+                                        : schur_sweep_thread_kernel<MT, 2, 4, 0, DET>;
     // wave split: full waves of one warp per chunk, then the partial last wave with two half-warps
     // per chunk (its chunks finish in about half the time of a full-chunk warp)
     static int conc = 0;
