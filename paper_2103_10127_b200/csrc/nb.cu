@@ -164,9 +164,13 @@ __global__ void nb_fill_kernel(int64_t n, int64_t nnodes, int64_t nslices, int D
                     ++b;
                 }
             }
-            for (; a < A; ++a) { cA[a * NB_C] = (int32_t)r0; NB_VA(a) = 0.0; }
+            // padding entries (value 0) repeat the row's first column: offset 0 from the pattern base,
+            // so padded rows add few stencil patterns (a per-row column here made the pattern count
+            // grow with the number of windows and disabled the compression at c3)
+            const int32_t padA = a > 0 ? cA[0] : (int32_t)r0, padB = b > 0 ? cB[0] : (int32_t)nvel;
+            for (; a < A; ++a) { cA[a * NB_C] = padA; NB_VA(a) = 0.0; }
             for (; b < B; ++b) {
-                cB[b * NB_C] = (int32_t)nvel;
+                cB[b * NB_C] = padB;
                 for (int cc = 0; cc < D; ++cc) NB_VB(b, cc) = 0.0;
             }
         } else {
@@ -178,8 +182,9 @@ __global__ void nb_fill_kernel(int64_t n, int64_t nnodes, int64_t nslices, int D
                 cB[q * NB_C] = ci[k];   // component-0 dof of the node
                 for (int cc = 0; cc < D; ++cc) NB_VB(q, cc) = val[k + cc];
             }
+            const int32_t padB = q > 0 ? cB[0] : 0;
             for (; q < B; ++q) {
-                cB[q * NB_C] = 0;
+                cB[q * NB_C] = padB;
                 for (int cc = 0; cc < D; ++cc) NB_VB(q, cc) = 0.0;
             }
         }
