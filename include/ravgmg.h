@@ -380,6 +380,15 @@ rav_status rav_xfer_setup(const rav_csr* P, void* stream, rav_xfer** out);
 rav_status rav_prolong(rav_xfer* t, const double* xc, double* xf, double alpha);
 rav_status rav_restrict(rav_xfer* t, const double* rf, double* bc);
 rav_status rav_xfer_set_stream(rav_xfer* t, void* stream);
+/* Switch the transfer to its stencil form (P:88 -- the nested interpolation of
+ * a uniformly refined tensor-product grid: Q2 1D weights 1 / (3/8, 3/4, -1/8),
+ * Q1 weights 1 / (1/2, 1/2), Dirichlet nodes dropped; R = P^T): the kernels
+ * read the input and write the output vector, no matrix.  fine / coarse: the
+ * rav_grid descriptors of the two levels (whole grids, fine ncell = 2 coarse
+ * ncell, same element pair).  Before switching, both forms are applied to
+ * seeded vectors and must agree to 1e-13 relative; otherwise RAV_ERR_ARG and
+ * the CSR form stays.  Synchronizes the transfer's stream. */
+rav_status rav_xfer_set_structured(rav_xfer* t, const rav_grid* fine, const rav_grid* coarse);
 void rav_xfer_destroy(rav_xfer* t);
 
 /* *out = sum_{i<n} a[i] b[i] (accumulate = 1: *out += ...), device pointers,
@@ -409,6 +418,13 @@ rav_status rav_peer_put(const double* src, double* dst, int64_t n, void* stream)
  * RAV_VARIANT_MV (same contract as rav_set_colors). */
 rav_status mg_set_colors(mg_ctx* ctx, int level, int n_colors, const int64_t* color_offs,
                          const int32_t* patch_ids);
+
+/* Stencil-form transfers for every level (see rav_xfer_set_structured):
+ * grids[0 .. n_levels-1] are the levels' rav_grid descriptors, coarsest first,
+ * each the uniform refinement of the one before.  Every level is verified
+ * against its CSR P before any is switched; on RAV_ERR_ARG nothing changes.
+ * Synchronizes the context's stream. */
+rav_status mg_set_structured_transfers(mg_ctx* ctx, const rav_grid* grids);
 
 /* Number of GPU kernel launches issued by the most recent rav_smooth,
  * mg_vcycle or mg_solve call on this context (graph nodes included). */

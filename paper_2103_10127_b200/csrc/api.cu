@@ -90,6 +90,7 @@ struct mg_level {
     rav_ctx* sm = nullptr;  // smoother (levels >= 1)
     Csr A;                  // level operator (owned by sm for l >= 1; own copy at l = 0)
     Csr P, PT;              // prolongation from l-1 and its transpose (restriction)
+    XStruct xs;             // stencil form of P (mg_set_structured_transfers), used when xs.on
     double* x = nullptr;    // level iterate (l < L-1)
     double* b = nullptr;    // level right-hand side (l < L-1)
     double* r = nullptr;    // level residual
@@ -496,6 +497,19 @@ rav_status mg_setup(int n_levels, const rav_csr* A, const rav_patches* patches, 
     return RAV_OK;
 }
 
+rav_status mg_set_structured_transfers(mg_ctx* m, const rav_grid* grids) {
+    if (!m || !grids) { set_error("mg_set_structured_transfers: NULL argument"); return RAV_ERR_ARG; }
+    std::vector<XStruct> xs(m->L);
+    for (int l = 1; l < m->L; ++l) {
+        mg_level& L = m->lv[l];
+        RAV_TRY(xs_build(&grids[l], &grids[l - 1], L.P.n_rows, L.P.n_cols, xs[l]));
+        RAV_TRY(xs_verify(xs[l], L.P, L.PT, m->stream));
+    }
+    for (int l = 1; l < m->L; ++l) m->lv[l].xs = xs[l];
+    m->cyc.reset();   // the captured cycle used the CSR transfers
+    return RAV_OK;
+}
+
 rav_status mg_set_stream(mg_ctx* m, void* stream) {
     if (!m) { set_error("NULL ctx"); return RAV_ERR_ARG; }
     if (m->stream != as_stream(stream)) m->cyc.reset();
@@ -519,10 +533,12 @@ static rav_status vcycle_launches(mg_ctx* m, int l, double* x, const double* b, 
     RAV_TRY(smooth_launches(L.sm, x, b, pre, omega, r_ready));
     if (pre == 0 && r_ready) RAV_CUDA(cudaMemcpyAsync(L.r, L.sm->r, sizeof(double) * L.A.n_rows, cudaMemcpyDeviceToDevice, s));
     else RAV_TRY(launch_residual(L.A, x, b, L.r, s));
-    RAV_TRY(launch_spmv(L.PT, L.r, Lc.b, 1.0, 0.0, s));       // b_{l-1} = P^T r_l
+    if (L.xs.on) RAV_TRY(launch_xs_restrict(L.xs, L.r, Lc.b, s));   // b_{l-1} = P^T r_l
+    else RAV_TRY(launch_spmv(L.PT, L.r, Lc.b, 1.0, 0.0, s));
     if (l - 1 > 0) RAV_CUDA(cudaMemsetAsync(Lc.x, 0, sizeof(double) * Lc.A.n_rows, s));
     RAV_TRY(vcycle_launches(m, l - 1, Lc.x, Lc.b, pre, post, omega));
-    RAV_TRY(launch_spmv(L.P, Lc.x, x, 1.0, 1.0, s));          // x_l += P x_{l-1}
+    if (L.xs.on) RAV_TRY(launch_xs_prolong(L.xs, Lc.x, x, 1.0, 1.0, s));   // x_l += P x_{l-1}
+    else RAV_TRY(launch_spmv(L.P, Lc.x, x, 1.0, 1.0, s));
     RAV_TRY(smooth_launches(L.sm, x, b, post, omega));
     return RAV_OK;
 }
@@ -635,6 +651,7 @@ rav_status mg_set_colors(mg_ctx* m, int level, int n_colors, const int64_t* colo
 
 struct rav_xfer {
     Csr P, PT;
+    XStruct xs;
     cudaStream_t stream = nullptr;
     int64_t last_launches = 0;
 };
@@ -656,7 +673,8 @@ rav_status rav_xfer_setup(const rav_csr* P, void* stream, rav_xfer** out) {
 rav_status rav_prolong(rav_xfer* t, const double* xc, double* xf, double alpha) {
     if (!t || !xc || !xf) { set_error("rav_prolong: NULL argument"); return RAV_ERR_ARG; }
     g_launches = 0;
-    RAV_TRY(launch_spmv(t->P, xc, xf, alpha, 1.0, t->stream));
+    if (t->xs.on) RAV_TRY(launch_xs_prolong(t->xs, xc, xf, alpha, 1.0, t->stream));
+    else RAV_TRY(launch_spmv(t->P, xc, xf, alpha, 1.0, t->stream));
     t->last_launches = g_launches;
     return RAV_OK;
 }
@@ -664,8 +682,18 @@ rav_status rav_prolong(rav_xfer* t, const double* xc, double* xf, double alpha) 
 rav_status rav_restrict(rav_xfer* t, const double* rf, double* bc) {
     if (!t || !rf || !bc) { set_error("rav_restrict: NULL argument"); return RAV_ERR_ARG; }
     g_launches = 0;
-    RAV_TRY(launch_spmv(t->PT, rf, bc, 1.0, 0.0, t->stream));
+    if (t->xs.on) RAV_TRY(launch_xs_restrict(t->xs, rf, bc, t->stream));
+    else RAV_TRY(launch_spmv(t->PT, rf, bc, 1.0, 0.0, t->stream));
     t->last_launches = g_launches;
+    return RAV_OK;
+}
+
+rav_status rav_xfer_set_structured(rav_xfer* t, const rav_grid* fine, const rav_grid* coarse) {
+    if (!t || !fine || !coarse) { set_error("rav_xfer_set_structured: NULL argument"); return RAV_ERR_ARG; }
+    XStruct S;
+    RAV_TRY(xs_build(fine, coarse, t->P.n_rows, t->P.n_cols, S));
+    RAV_TRY(xs_verify(S, t->P, t->PT, t->stream));
+    t->xs = S;
     return RAV_OK;
 }
 

@@ -167,6 +167,19 @@ rav_status launch_sweep(const PatchSet& P, const Factors& F, const double* r, do
                         cudaStream_t s);
 
 // ---- coarse.cu ------------------------------------------------------------------------
+// ---- xfer.cu: stencil form of the nested transfers of uniformly refined structured grids -----
+struct XStruct {
+    int on = 0;
+    int dim = 0, P = 2;    // P: velocity lattice refinement (2: Q2-Q1, 1: Q1-Q1)
+    int nc[3] = {1, 1, 1}; // coarse cells per axis
+    int64_t n_fine = 0, n_coarse = 0;
+};
+rav_status xs_build(const rav_grid* fine, const rav_grid* coarse, int64_t n_fine, int64_t n_coarse, XStruct& S);
+rav_status xs_verify(const XStruct& S, const Csr& P, const Csr& PT, cudaStream_t s);
+rav_status launch_xs_prolong(const XStruct& S, const double* xc, double* yf, double alpha, double beta,
+                             cudaStream_t s);
+rav_status launch_xs_restrict(const XStruct& S, const double* rf, double* bc, cudaStream_t s);
+
 struct CoarseLU {
     int64_t n = 0, pin = -1;
     int m = 0;

@@ -100,6 +100,8 @@ def _load():
         "rav_prolong": [vp, vp, vp, dbl],
         "rav_restrict": [vp, vp, vp],
         "rav_xfer_set_stream": [vp, vp],
+        "rav_xfer_set_structured": [vp, P(RavGrid), P(RavGrid)],
+        "mg_set_structured_transfers": [vp, vp],
         "rav_dot": [vp, vp, i64, vp, C.c_int, vp],
         "mg_fgmres": [vp, vp, vp, C.c_int, C.c_int, dbl, C.c_int, dbl, C.c_int, P(C.c_int), vp],
         "rav_adaptive_create": [P(RavAdaptiveDesc), P(vp)],
@@ -356,6 +358,12 @@ class Multigrid:
         ids = np.ascontiguousarray(ids, dtype=np.int32)
         _check(lib.mg_set_colors(self.ctx, int(level), len(offs) - 1, offs.ctypes.data, ids.ctypes.data))
 
+    def set_structured_transfers(self, problems: Sequence[Dict]):
+        """mg_set_structured_transfers: stencil-form P / P^T on every level (problems coarsest
+        first, each the uniform refinement of the previous; verified against the CSR P)."""
+        gs = (RavGrid * self.L)(*[grid(p) for p in problems])
+        _check(lib.mg_set_structured_transfers(self.ctx, gs))
+
     def vcycle(self, x, b, pre=2, post=2, omega=0.66):
         _check(lib.mg_vcycle(self.ctx, _ptr(x), _ptr(b), int(pre), int(post), float(omega)))
         return x
@@ -413,6 +421,11 @@ class Transfer:
     def set_stream(self, stream):
         _check(lib.rav_xfer_set_stream(self.ctx, _stream(stream)))
 
+    def set_structured(self, fine_problem: Dict, coarse_problem: Dict):
+        """rav_xfer_set_structured: stencil-form transfer (verified against the CSR P)."""
+        gf, gc = grid(fine_problem), grid(coarse_problem)
+        _check(lib.rav_xfer_set_structured(self.ctx, C.byref(gf), C.byref(gc)))
+
     def close(self):
         if getattr(self, "ctx", None):
             lib.rav_xfer_destroy(self.ctx)
@@ -467,9 +480,12 @@ def coarsen_problem(problem: Dict) -> Dict:
 
 
 def build_hierarchy(problem: Dict, n_levels: int, weights: str = "pou", variant: int = VARIANT_ROWS,
-                    kernel: int = KERNEL_AUTO, free_inputs: bool = True, deterministic: bool = False):
+                    kernel: int = KERNEL_AUTO, free_inputs: bool = True, deterministic: bool = False,
+                    structured_transfers: bool = True):
     """Generate every level on the GPU (rediscretized operators) and
-    build the multigrid context.  Returns (mg, fine_level_dict)."""
+    build the multigrid context.  Returns (mg, fine_level_dict).  With
+    structured_transfers the V-cycle applies P / P^T in stencil form
+    (mg_set_structured_transfers) instead of streaming their CSR."""
     probs = [problem]
     for _ in range(n_levels - 1):
         probs.append(coarsen_problem(probs[-1]))
@@ -485,6 +501,10 @@ def build_hierarchy(problem: Dict, n_levels: int, weights: str = "pou", variant:
     if variant == VARIANT_MV:     # colour every smoothed level (R10)
         for l in range(1, len(probs)):
             mg.set_colors(l, *multicolor(probs[l]))
+    nested = all(probs[l]["ncell"][k] == 2 * probs[l - 1]["ncell"][k]
+                 for l in range(1, len(probs)) for k in range(problem["dim"]))
+    if structured_transfers and nested and len(probs) > 1:
+        mg.set_structured_transfers(probs)
     fine = levels[-1]
     if free_inputs:   # the library copied everything it needs
         fine = {k: v for k, v in fine.items() if k in ("n", "nvel", "nnz", "b", "problem")}
