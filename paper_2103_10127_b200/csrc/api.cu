@@ -533,7 +533,7 @@ static rav_status vcycle_launches(mg_ctx* m, int l, double* x, const double* b, 
     RAV_TRY(smooth_launches(L.sm, x, b, pre, omega, r_ready));
     if (pre == 0 && r_ready) RAV_CUDA(cudaMemcpyAsync(L.r, L.sm->r, sizeof(double) * L.A.n_rows, cudaMemcpyDeviceToDevice, s));
     else RAV_TRY(launch_residual(L.A, x, b, L.r, s));
-    if (L.xs.on) RAV_TRY(launch_xs_restrict(L.xs, L.r, Lc.b, s));   // b_{l-1} = P^T r_l
+    if (L.xs.on && L.xs.dim == 2) RAV_TRY(launch_xs_restrict(L.xs, L.r, Lc.b, s));   // b_{l-1} = P^T r_l
     else RAV_TRY(launch_spmv(L.PT, L.r, Lc.b, 1.0, 0.0, s));
     if (l - 1 > 0) RAV_CUDA(cudaMemsetAsync(Lc.x, 0, sizeof(double) * Lc.A.n_rows, s));
     RAV_TRY(vcycle_launches(m, l - 1, Lc.x, Lc.b, pre, post, omega));
@@ -682,7 +682,7 @@ rav_status rav_prolong(rav_xfer* t, const double* xc, double* xf, double alpha) 
 rav_status rav_restrict(rav_xfer* t, const double* rf, double* bc) {
     if (!t || !rf || !bc) { set_error("rav_restrict: NULL argument"); return RAV_ERR_ARG; }
     g_launches = 0;
-    if (t->xs.on) RAV_TRY(launch_xs_restrict(t->xs, rf, bc, t->stream));
+    if (t->xs.on && t->xs.dim == 2) RAV_TRY(launch_xs_restrict(t->xs, rf, bc, t->stream));
     else RAV_TRY(launch_spmv(t->PT, rf, bc, 1.0, 0.0, t->stream));
     t->last_launches = g_launches;
     return RAV_OK;

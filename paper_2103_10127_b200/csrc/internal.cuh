@@ -168,6 +168,8 @@ rav_status launch_sweep(const PatchSet& P, const Factors& F, const double* r, do
 
 // ---- coarse.cu ------------------------------------------------------------------------
 // ---- xfer.cu: stencil form of the nested transfers of uniformly refined structured grids -----
+// (3D restriction stays on the CSR P^T: its 125-point gather per coarse node is latency-bound,
+// measured 34 vs 19 us at the c4 fine level; the 3D prolongation uses the stencil, 15 vs 22 us)
 struct XStruct {
     int on = 0;
     int dim = 0, P = 2;    // P: velocity lattice refinement (2: Q2-Q1, 1: Q1-Q1)

@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
 #undef ND_AT
 
 // one patch per warp (3D and large patches): lane k owns restricted node k
-template <int D, bool DET = false>
+template <int D, bool DET = false, int WB = 8>
 __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int MT, int nnmax,
                                                                const int64_t* __restrict__ foffs,
                                                                const int64_t* __restrict__ nodeoffs,
@@ -602,14 +602,14 @@ __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int M
 #pragma unroll
         for (int c = 0; c < D; ++c) acc[c] = 0.0;
         if (lane < MT) {
-            // batches of 8 independent column loads in flight per lane (the loop is latency-bound otherwise)
+            // batches of WB independent column loads in flight per lane (the loop is latency-bound otherwise)
             int j = 0;
-            for (; j + 8 <= nn; j += 8) {
-                double y[8];
+            for (; j + WB <= nn; j += WB) {
+                double y[WB];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) y[u] = __ldcs(Y + (size_t)(j + u) * MT + lane);
+                for (int u = 0; u < WB; ++u) y[u] = __ldcs(Y + (size_t)(j + u) * MT + lane);
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
+                for (int u = 0; u < WB; ++u)
 #pragma unroll
                     for (int c = 0; c < D; ++c) acc[c] = fma(y[u], rl[(j + u) * D + c], acc[c]);
             }
@@ -1383,14 +1383,25 @@ static void launch_schur_perpatch(const PatchSet& P, const Factors& F, const dou
             P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD, F.NR, F.fac, r, x, omega, F.cbuf);
     } else {
         const size_t shmem = sizeof(double) * (size_t)F.NN * D * 8;
-        const int blocks = (int)std::min<int64_t>(cdiv(P.n_patches, 8), (int64_t)num_sms() * 16);
+        // grid cap in blocks per SM.  c4 (WB 8): 218 us at 8 (one persistent wave), 189 at 16, 185 at 32
+        // (one patch per warp); WB 16 / 24 within 2%
+        static const int bps = [] {
+            const char* e = getenv("RAV_SCHUR_WBPS");
+            return e ? atoi(e) : 32;
+        }();
+        const int blocks = (int)std::min<int64_t>(cdiv(P.n_patches, 8), (int64_t)num_sms() * bps);
         static const int wpf = [] {   // per-patch bulk prefetch (c4, batched loads: 188.4 us off, 194.9 on)
             const char* e = getenv("RAV_SCHUR_WPF");
             return e ? atoi(e) : 0;
         }();
-        schur_sweep_warp_kernel<D, DET><<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs,
-                                                                   F.nodes, F.PD, F.NR, F.fac, r, x, omega, F.cbuf,
-                                                                   wpf);
+        static const int wb = [] {    // column loads in flight per lane
+            const char* e = getenv("RAV_SCHUR_WB");
+            return e ? atoi(e) : 8;
+        }();
+        auto kern = wb >= 24 ? schur_sweep_warp_kernel<D, DET, 24>
+                  : wb >= 16 ? schur_sweep_warp_kernel<D, DET, 16> : schur_sweep_warp_kernel<D, DET, 8>;
+        kern<<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD, F.NR, F.fac, r, x,
+                                        omega, F.cbuf, wpf);
     }
 }
 
