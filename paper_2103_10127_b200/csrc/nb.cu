@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
         __syncthreads();
         if (threadIdx.x == 0) {
             double sum = 0.0;
-            for (int i = 0; i < 8; ++i) sum += red[i];
+            for (int i = 0; i < (int)(blockDim.x >> 5); ++i) sum += red[i];
             part[blockIdx.x] = sum;
         }
     }
@@ -687,6 +687,16 @@ void nb_free(NodeBlocked& N) {
     N = NodeBlocked{};
 }
 
+// threads per block of the residual kernel (128 or 256; the kernel is compiled for <= 256)
+static int nb_block_threads() {
+    static const int bs = [] {
+        const char* e = getenv("RAV_NB_BS");
+        const int v = e ? atoi(e) : 256;
+        return v == 128 ? 128 : 256;
+    }();
+    return bs;
+}
+
 template <int D, int G, int UA, bool PR = false>
 static void nb_launch(const NodeBlocked& N, const double* x, const double* b, double* r, double* part, int nblk,
                       cudaStream_t s, int* used) {
@@ -695,7 +705,8 @@ static void nb_launch(const NodeBlocked& N, const double* x, const double* b, do
         return e ? atoi(e) : 1;
     }();
     const NbCols cols{N.col, N.pid, N.baseA, N.baseB, N.tbl, N.W, bulk};
-    const int64_t full = cdiv(N.nslices * NB_C * G, 256);
+    const int bs = nb_block_threads();
+    const int64_t full = cdiv(N.nslices * NB_C * G, bs);
     // with partial norms: one partial per block, the full grid when the caller's buffer holds it
     const int blocks = (int)(part ? std::min<int64_t>(full, nblk) : full);
     if (used) *used = blocks;
@@ -710,7 +721,7 @@ static void nb_launch(const NodeBlocked& N, const double* x, const double* b, do
               : (minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8, false, PR>
               : (minb >= 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6, false, PR>
                                       : nb_residual_kernel<D, G, UA, 1, false, PR>;
-    launch_maybe_pdl(kern, dim3(blocks), dim3(256), 0, s, N.nblock, N.nnodes, N.nslices,
+    launch_maybe_pdl(kern, dim3(blocks), dim3(bs), 0, s, N.nblock, N.nnodes, N.nslices,
                      N.nvel, (const int32_t*)N.perm, (const int32_t*)N.wa, (const int32_t*)N.wb,
                      (const int64_t*)N.cptr, (const int64_t*)N.vptr, cols, (const double*)N.val, x, b,
                      r, part);
@@ -730,7 +741,7 @@ static int nb_lanes(const NodeBlocked& N) {
     return G >= 32 ? 32 : (G >= 8 ? 8 : (G >= 4 ? 4 : (G >= 2 ? 2 : 1)));
 }
 
-int64_t nb_full_blocks(const NodeBlocked& N) { return cdiv(N.nslices * NB_C * nb_lanes(N), 256); }
+int64_t nb_full_blocks(const NodeBlocked& N) { return cdiv(N.nslices * NB_C * nb_lanes(N), nb_block_threads()); }
 
 rav_status launch_nb_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
                               cudaStream_t s, int* used) {
