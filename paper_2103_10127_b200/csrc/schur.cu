@@ -553,6 +553,148 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
 
 #undef ND_AT
 
+// 2D PoU interior shape, one chunk (32 patches, one per lane) per CTA of 4 warps that split the
+// chunk's factor bytes: warp 0 reads the triangular block (+ g) and warps 1-3 the rectangular
+// column pairs (blocks [ (w-1) B1, min(NRB, w B1) )).  The rectangular partial sums meet in
+// shared memory; warp 0 adds them in fixed order (w = 1, 2, 3: deterministic) and scatters.  A
+// chunk then takes about a quarter of the time it takes one warp, so the partial last wave of
+// a small grid (c2: 3.5 waves of one-warp chunks) is a quarter as long.
+template <int MT, int D, int NRB, bool DET>
+__global__ void __launch_bounds__(128, 4) schur_sweep_cta4_kernel(int64_t np, int64_t nchunks, int64_t pairs,
+                                                                  const double2* __restrict__ W,
+                                                                  const int32_t* __restrict__ ND,
+                                                                  const int32_t* __restrict__ PD,
+                                                                  const int32_t* __restrict__ NR,
+                                                                  const double* __restrict__ AUX,
+                                                                  const double* __restrict__ r,
+                                                                  double* __restrict__ x, double omega,
+                                                                  double* __restrict__ cbuf) {
+    constexpr int TRI = MT * (MT + 1) / 2 + MT * D;
+    constexpr int TRI_PAD = TRI + (TRI & 1);
+    constexpr int RC = MT + D;
+    constexpr int NN = MT + 2 * NRB;
+    constexpr int B1 = (NRB + 2) / 3;
+    __shared__ double part[3][MT * D + 1][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t chunk = blockIdx.x;
+    const int64_t i = chunk * 32 + lane;
+    pdl_trigger();
+    const double2* wc = W + chunk * pairs * 32;
+    const int32_t* np_ = ND + chunk * (int64_t)NN * 32 + lane;
+    const int b0 = warp == 0 ? 0 : (warp - 1) * B1;
+    const int b1 = warp == 0 ? 0 : min(NRB, warp * B1);
+    {   // before r exists: this warp's factor segment (one bulk prefetch) and the node-index lines
+        if (lane == 0) {
+            if (warp == 0) bulk_prefetch_l2(wc, (uint32_t)(TRI_PAD / 2 * 512));
+            else if (b1 > b0) bulk_prefetch_l2(wc + (int64_t)(TRI_PAD / 2 + b0 * RC) * 32, (uint32_t)((b1 - b0) * RC * 512));
+        }
+        if (warp == 0 && lane < NN) prefetch_l2(ND + (chunk * (int64_t)NN + lane) * 32);
+    }
+    pdl_wait();
+    double acc[MT][D], gR[MT][D];
+    double gacc = 0.0;
+#pragma unroll
+    for (int k = 0; k < MT; ++k)
+#pragma unroll
+        for (int c = 0; c < D; ++c) { acc[k][c] = 0.0; gR[k][c] = 0.0; }
+    if (warp == 0) {   // triangular block of the restricted rows of A_s^{-1}, and g_R (as the thread kernel)
+        const double2* wp = wc + lane;
+        double rr[MT][D];
+#pragma unroll
+        for (int k = 0; k < MT; ++k) ld_node<D>(r + __ldcs(np_ + k * 32), rr[k]);
+        double2 pv = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < MT; ++j) {
+#pragma unroll
+            for (int q = 0; q <= j + D; ++q) {
+                const int e = j * (j + 1) / 2 + j * D + q;
+                if ((e & 1) == 0) pv = __ldcs(wp + (e >> 1) * 32);
+                const double v = (e & 1) ? pv.y : pv.x;
+                if (q <= j) {
+#pragma unroll
+                    for (int c = 0; c < D; ++c) {
+                        acc[q][c] = fma(v, rr[j][c], acc[q][c]);
+                        if (q != j) acc[j][c] = fma(v, rr[q][c], acc[j][c]);
+                    }
+                } else {
+                    const int c = q - j - 1;
+                    gR[j][c] = v;
+                    gacc = fma(v, rr[j][c], gacc);
+                }
+            }
+        }
+    } else {           // rectangular column pairs b0 .. b1-1
+        const double2* wq0 = wc + (TRI_PAD / 2) * 32 + lane;
+#pragma unroll
+        for (int bb = 0; bb < B1; ++bb) {
+            const int b = b0 + bb;
+            if (b < b1) {
+                const int j0 = MT + 2 * b;
+                double ra[D], rb[D];
+                ld_node<D>(r + __ldcs(np_ + j0 * 32), ra);
+                ld_node<D>(r + __ldcs(np_ + (j0 + 1) * 32), rb);
+                const double2* wq = wq0 + (int64_t)b * RC * 32;
+#pragma unroll
+                for (int p = 0; p < RC; ++p) {
+                    const double2 v2 = __ldcs(wq + p * 32);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int e = 2 * p + h;
+                        const double v = h ? v2.y : v2.x;
+                        const bool second = e >= RC;
+                        const int q = second ? e - RC : e;
+                        if (q < MT) {
+#pragma unroll
+                            for (int c = 0; c < D; ++c) acc[q][c] = fma(v, second ? rb[c] : ra[c], acc[q][c]);
+                        } else {
+                            gacc = fma(v, second ? rb[q - MT] : ra[q - MT], gacc);
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < MT; ++k)
+#pragma unroll
+            for (int c = 0; c < D; ++c) part[warp - 1][k * D + c][lane] = acc[k][c];
+        part[warp - 1][MT * D][lane] = gacc;
+    }
+    __syncthreads();
+    if (warp != 0) return;
+#pragma unroll
+    for (int w = 0; w < 3; ++w) {
+#pragma unroll
+        for (int k = 0; k < MT; ++k)
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[k][c] += part[w][k * D + c][lane];
+        gacc += part[w][MT * D][lane];
+    }
+    const double* aux = AUX + chunk * (MT + 2) * 32 + lane;
+    const int pd = PD[i];
+    const double t = aux[(MT + 1) * 32] * (gacc - __ldg(r + pd));
+    if (i >= np) return;   // padding slots of the last chunk
+    const int m = NR[i];
+    double* cb = DET ? cbuf + i * (MT * D + 1) : nullptr;
+#pragma unroll
+    for (int k = 0; k < MT; ++k) {
+        if (k < m) {
+            const double wk = omega * aux[k * 32];
+            const int nd = __ldcs(np_ + k * 32);
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const double v = wk * fma(gR[k][c], t, acc[k][c]);
+                if (DET) cb[k * D + c] = v;
+                else atomicAdd(x + nd + c, v);
+            }
+        }
+    }
+    const double wpr = aux[MT * 32];
+    if (wpr != 0.0) {
+        if (DET) cb[MT * D] = omega * wpr * (-t);
+        else atomicAdd(x + pd, omega * wpr * (-t));
+    }
+}
+
 // one patch per warp (3D and large patches): lane k owns restricted node k
 template <int D, bool DET = false, int WB = 8>
 __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int MT, int nnmax,
@@ -1360,6 +1502,18 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
         const char* e = getenv("RAV_SCHUR_TAILPF");
         return e ? atoi(e) : 0;
     }();
+    static const int cta4 = [] {   // one chunk per 4-warp CTA (schur_sweep_cta4_kernel)
+        const char* e = getenv("RAV_SCHUR_CTA4");
+        return e ? atoi(e) : 0;
+    }();
+    if constexpr (MT == 9) {
+        if (cta4 && F.NN == 25 && !F.npid && F.nchunks > 0) {
+            launch_maybe_pdl(schur_sweep_cta4_kernel<MT, 2, 8, DET>, dim3((unsigned)F.nchunks), dim3(128), 0, s, np,
+                             F.nchunks, F.pairs, W, (const int32_t*)F.DT, (const int32_t*)F.PD, (const int32_t*)F.NR,
+                             (const double*)F.WT, r, x, omega, F.cbuf);
+            return;
+        }
+    }
     const int64_t tail0 = tailpf ? F.nchunks / conc * conc : F.nchunks;
     const int64_t full = split && F.nchunks > conc ? F.nchunks / conc * conc : F.nchunks;
     const int64_t rem = F.nchunks - full;
