@@ -439,7 +439,8 @@ rav_status wave_build(const Csr& A, const Factors& F, int64_t n_patches, int nb_
     wave_free(V);
     const NodeBlocked& N = A.nb;
     if (!(N.nslices > 0 && N.D == 2 && N.pair && N.tbl && nb_lanes_used == 1)) return RAV_OK;
-    if (!(F.layout == 4 && F.MT == 9 && F.NN == 25 && F.D == 2 && !F.npid && !F.cbuf && F.DT)) return RAV_OK;
+    // (the node-index compression keeps F.DT, which the pipelined sweep reads)
+    if (!(F.layout == 4 && F.MT == 9 && F.NN == 25 && F.D == 2 && !F.cbuf && F.DT)) return RAV_OK;
     const int64_t n = A.n_rows;
     const int64_t nslots = N.nslices * W_NBC;
     const int64_t nres = cdiv(nslots, W_RES_BS);              // residual CTAs
