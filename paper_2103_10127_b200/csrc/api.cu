@@ -79,7 +79,11 @@ struct rav_ctx {
     double* r = nullptr;        // residual work vector
     double* hx = nullptr;       // staging for host x / b
     double* hb = nullptr;
-    GraphCache graph;
+    // captured sweep chains for the two most recent (x, b, nu, omega) keys: a caller that alternates
+    // between two buffer pairs (double-buffered host transfers) replays without re-capturing
+    GraphCache graph[2];
+    int graph_next = 0;         // entry to replace on a miss
+    void graphs_reset() { graph[0].reset(); graph[1].reset(); }
     int64_t last_launches = 0;
     // multicoloured MV (RAV_VARIANT_MV): colour c = patches plist[coffs[c] .. coffs[c+1])
     std::vector<int64_t> coffs;
@@ -259,7 +263,7 @@ rav_status rav_set_colors(rav_ctx* c, int n_colors, const int64_t* color_offs, c
     if (c->plist) cudaFree(c->plist);
     RAV_CUDA(cudaMalloc(&c->plist, sizeof(int32_t) * c->P.n_patches));
     RAV_CUDA(cudaMemcpy(c->plist, patch_ids, sizeof(int32_t) * c->P.n_patches, cudaMemcpyHostToDevice));
-    c->graph.reset();
+    c->graphs_reset();
     return RAV_OK;
 }
 
@@ -279,7 +283,7 @@ rav_status rav_apply_color(rav_ctx* c, int color, double* x, const double* b, do
 
 rav_status rav_set_stream(rav_ctx* c, void* stream) {
     if (!c) { set_error("NULL ctx"); return RAV_ERR_ARG; }
-    if (c->stream != as_stream(stream)) c->graph.reset();
+    if (c->stream != as_stream(stream)) c->graphs_reset();
     c->stream = as_stream(stream);
     return RAV_OK;
 }
@@ -309,7 +313,12 @@ rav_status rav_smooth(rav_ctx* c, double* x, const double* b, int nu, double ome
         return RAV_ERR_ARG;
     }
     bool use_graph = c->stream != nullptr && (nu >= 2 || c->variant == RAV_VARIANT_MV);
-    RAV_TRY(run_graph(c->graph, c->stream, use_graph, X, B, nu, 0, 0, omega, c->last_launches,
+    int gi = c->graph[0].match(X, B, nu, 0, 0, omega) ? 0 : (c->graph[1].match(X, B, nu, 0, 0, omega) ? 1 : -1);
+    if (gi < 0) {
+        gi = c->graph_next;
+        c->graph_next ^= 1;
+    }
+    RAV_TRY(run_graph(c->graph[gi], c->stream, use_graph, X, B, nu, 0, 0, omega, c->last_launches,
                       [&]() { return smooth_launches(c, X, B, nu, omega); }));
     if (!dx) {
         RAV_CUDA(cudaMemcpyAsync(x, c->hx, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
@@ -397,7 +406,7 @@ void rav_destroy(rav_ctx* c) {
     if (!c) return;
     if (c->stream) cudaStreamSynchronize(c->stream);
     else cudaDeviceSynchronize();
-    c->graph.reset();
+    c->graphs_reset();
     csr_free(c->A);
     patches_free(c->P);
     factors_free(c->F);
