@@ -39,7 +39,7 @@ constexpr int W_RES_BS = 256;
 // change during the kernel's lifetime).  The waiting thread's acquire fence invalidates the SM's
 // L1 (CCTL.IVALL), so a line cached afterwards already holds every write the CTA waited for.
 #ifndef RAV_WAVE_LOAD
-#define RAV_WAVE_LOAD 3   // 0: ld.relaxed.gpu; 1: ld.global.cg; 2: non-coherent (timing only); 3: weak ld.global
+#define RAV_WAVE_LOAD 3   // 0: ld.relaxed.gpu; 1: ld.global.cg; 3: weak ld.global (measured equal, fewest constraints)
 #endif
 __device__ __forceinline__ void ld2_strong(const double* p, double* out) {
 #if RAV_WAVE_LOAD == 0
@@ -49,11 +49,8 @@ __device__ __forceinline__ void ld2_strong(const double* p, double* out) {
     // path), ordered by the compiler after the wait's barrier, free to be scheduled for ILP
     const double2 v = *reinterpret_cast<const double2*>(p);
     out[0] = v.x; out[1] = v.y;
-#elif RAV_WAVE_LOAD == 1
-    const double2 v = __ldcg(reinterpret_cast<const double2*>(p));
-    out[0] = v.x; out[1] = v.y;
 #else
-    const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(p));
     out[0] = v.x; out[1] = v.y;
 #endif
 }
@@ -64,10 +61,8 @@ __device__ __forceinline__ double ld_strong(const double* p) {
     return v;
 #elif RAV_WAVE_LOAD == 3
     return *p;
-#elif RAV_WAVE_LOAD == 1
-    return __ldcg(p);
 #else
-    return __ldg(p);
+    return __ldcg(p);
 #endif
 }
 __device__ __forceinline__ void red_release(unsigned* p, unsigned v) {
@@ -81,10 +76,9 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
 // The CTA waits until done[b] >= mult * cnt[b] for every band b of up to three ranges.  Thread k
 // polls the k-th band of the concatenated ranges (all polls in flight at once: one L2 round trip
 // when the producers are done), with relaxed loads, then issues its own acquire fence; the
-// barrier orders the CTA's later loads after every polling thread's fence.  nofence (timing
-// experiments only) skips the fences.
+// barrier orders the CTA's later loads after every polling thread's fence.
 __device__ __forceinline__ void wait_ranges(const unsigned* done, const int32_t* cnt, const int32_t* lo,
-                                            const int32_t* hi, int nr, unsigned mult, int nofence) {
+                                            const int32_t* hi, int nr, unsigned mult) {
     int k = threadIdx.x, b = -1;
     for (int q = 0; q < nr && b < 0; ++q) {
         const int w = hi[q] >= lo[q] ? hi[q] - lo[q] + 1 : 0;
@@ -98,7 +92,7 @@ __device__ __forceinline__ void wait_ranges(const unsigned* done, const int32_t*
             __nanosleep(64);
             if (++it > (1ll << 24)) __trap();
         }
-        if (!nofence) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
 }
@@ -235,7 +229,6 @@ struct WRes {
     const int32_t *alo, *ahi, *cntA;
     const unsigned* doneA;
     unsigned* doneR;
-    int nofence;
 };
 
 __global__ void __launch_bounds__(256, 6) wave_residual_kernel(WRes R, const double* x,
@@ -248,7 +241,7 @@ __global__ void __launch_bounds__(256, 6) wave_residual_kernel(WRes R, const dou
     const int lane = threadIdx.x & 31;
     if (s < R.nslices && lane == 0) bulk_prefetch_l2(R.v + R.vptr[s], (uint32_t)((R.vptr[s + 1] - R.vptr[s]) * 8));
     if (first) pdl_wait();
-    else if (R.ahi[blockIdx.x] >= 0) wait_ranges(R.doneA, R.cntA, R.alo + blockIdx.x, R.ahi + blockIdx.x, 1, sweep, R.nofence);
+    else if (R.ahi[blockIdx.x] >= 0) wait_ranges(R.doneA, R.cntA, R.alo + blockIdx.x, R.ahi + blockIdx.x, 1, sweep);
     const int64_t br = t < R.n ? R.perm[t] : -1;
     if (br >= 0) {
         const int A = R.wa[s], B = R.wb[s];
@@ -314,7 +307,6 @@ struct WSw {
     const int32_t *rlo, *rhi, *cntR;
     const unsigned* doneR;
     unsigned* doneA;
-    int nofence;
 };
 
 __global__ void __launch_bounds__(128, 4) wave_sweep_kernel(WSw S, const double* r,
@@ -339,7 +331,7 @@ __global__ void __launch_bounds__(128, 4) wave_sweep_kernel(WSw S, const double*
         if (lane == 0) bulk_prefetch_l2(wc, (uint32_t)((TRI_PAD / 2 + PF * RC) * 512));
     }
     if (first) pdl_wait();
-    else wait_ranges(S.doneR, S.cntR, S.rlo + 3 * band, S.rhi + 3 * band, 3, sweep, S.nofence);
+    else wait_ranges(S.doneR, S.cntR, S.rlo + 3 * band, S.rhi + 3 * band, 3, sweep);
     if (live) {
         double acc[MT][D], rr[MT][D], gR[MT][D];
         double gacc = 0.0;
@@ -536,14 +528,10 @@ rav_status wave_smooth(const Csr& A, const Factors& F, int64_t n_patches, const 
     RAV_CUDA(cudaMemsetAsync(V.done, 0, sizeof(unsigned) * (V.nA + V.nR), s));
     unsigned* doneA = V.done;
     unsigned* doneR = V.done + V.nA;
-    static const int nofence = [] {   // timing experiments only: unsafe
-        const char* e = getenv("RAV_WAVE_NOFENCE");
-        return e ? atoi(e) : 0;
-    }();
     const WRes R{N.nblock, N.nnodes, N.nslices, N.nvel, N.perm, N.wa, N.wb, N.pid, N.baseA, N.baseB, N.tbl,
-                 N.vptr, N.W, N.val, V.alo, V.ahi, V.cntA, doneA, doneR, nofence};
+                 N.vptr, N.W, N.val, V.alo, V.ahi, V.cntA, doneA, doneR};
     const WSw S{n_patches, F.nchunks, F.pairs, reinterpret_cast<const double2*>(F.facT), F.DT, F.PD, F.NR, F.WT,
-                V.rlo, V.rhi, V.cntR, doneR, doneA, nofence};
+                V.rlo, V.rhi, V.cntR, doneR, doneA};
     int nres_done = 0;   // residual kernels issued so far in this chain
     for (int k = 0; k < nu; ++k) {
         const bool skip_r = r_ready && k == 0;
