@@ -259,6 +259,23 @@ def run_c5_smoothers(rg, si, stream):
         out[name] = {"ms_per_sweep": ms, "mdofs": G["n"] / (ms * 1e-3) / 1e6, "omega": omega,
                      "residual_reduction_50": r50 / r0, "setup_s": setup_s, "kernel": sm.kernel_name,
                      "factor_bytes_per_sweep": sm.sweep_bytes()["sweep"]}
+        if name == "rav":   # the two kernels of the sweep alone at this size (roofline, DESIGN 5.1)
+            peak = load_peaks()[0]
+            r = sm.residual(x0, b)
+            for kname, fn, nbytes in (("sweep_kernel", lambda: sm.apply(r, x, omega), sm.sweep_bytes()["sweep"]),
+                                      ("residual_kernel", lambda: sm.residual(x, b, r), sm.sweep_bytes()["residual"])):
+                for _ in range(3):
+                    fn()
+                torch.cuda.synchronize()
+                e0.record(stream)
+                for _ in range(20):
+                    fn()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                kms = e0.elapsed_time(e1) / 20
+                out[name][kname] = {"ms": kms, "algorithmic_bytes": nbytes,
+                                    "achieved_gbs": nbytes / (kms * 1e-3) / 1e9,
+                                    "frac_of_measured_peak": nbytes / (kms * 1e-3) / 1e9 / peak}
         sm.close()
         del sm, G, x, b
         torch.cuda.empty_cache()
