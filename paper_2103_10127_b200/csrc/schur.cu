@@ -1533,7 +1533,11 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
 template <int D, bool DET>
 static void launch_schur_perpatch(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
                                   cudaStream_t s) {
-    if (P.n_patches < 2048 && F.MT <= 32) {   // coarse levels: a CTA per patch (latency)
+    static const int64_t cta_max = [] {   // patch count below which a CTA (8 warps) takes one patch
+        const char* e = getenv("RAV_SCHUR_CTA_MAX");
+        return e ? atoll(e) : 2048;
+    }();
+    if (P.n_patches < cta_max && F.MT <= 32) {   // coarse levels: a CTA per patch (latency)
         const size_t shmem = sizeof(double) * ((size_t)F.NN * D + 8 * 32 * (size_t)D);
         schur_sweep_cta_kernel<D, DET><<<(int)std::max<int64_t>(1, P.n_patches), 256, shmem, s>>>(
             P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD, F.NR, F.fac, r, x, omega, F.cbuf);
