@@ -387,7 +387,9 @@ rav_status rav_xfer_set_stream(rav_xfer* t, void* stream);
  * rav_grid descriptors of the two levels (whole grids, fine ncell = 2 coarse
  * ncell, same element pair).  Before switching, both forms are applied to
  * seeded vectors and must agree to 1e-13 relative; otherwise RAV_ERR_ARG and
- * the CSR form stays.  Synchronizes the transfer's stream. */
+ * the CSR form stays.  In 3D only the prolongation switches (the 125-point
+ * restriction gather measured slower than the CSR P^T).  Synchronizes the
+ * transfer's stream. */
 rav_status rav_xfer_set_structured(rav_xfer* t, const rav_grid* fine, const rav_grid* coarse);
 void rav_xfer_destroy(rav_xfer* t);
 
