@@ -696,7 +696,9 @@ __global__ void __launch_bounds__(128, 4) schur_sweep_cta4_kernel(int64_t np, in
 }
 
 // one patch per warp (3D and large patches): lane k owns restricted node k
-template <int D, bool DET = false, int WB = 8>
+// MTC > 0: compile-time number of restricted nodes (27 for the 3D PoU interior shape): the column
+// loads then use immediate offsets from a running pointer instead of 64-bit index arithmetic
+template <int D, bool DET = false, int WB = 8, int MTC = 0>
 __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int MT, int nnmax,
                                                                const int64_t* __restrict__ foffs,
                                                                const int64_t* __restrict__ nodeoffs,
@@ -743,7 +745,27 @@ __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int M
         double acc[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) acc[c] = 0.0;
-        if (lane < MT) {
+        if constexpr (MTC > 0) {
+            if (lane < MTC) {
+                const double* yp = Y + lane;
+                const double* rp = rl;
+                int j = 0;
+                for (; j + WB <= nn; j += WB, yp += WB * MTC, rp += WB * D) {
+                    double y[WB];
+#pragma unroll
+                    for (int u = 0; u < WB; ++u) y[u] = __ldcs(yp + u * MTC);
+#pragma unroll
+                    for (int u = 0; u < WB; ++u)
+#pragma unroll
+                        for (int c = 0; c < D; ++c) acc[c] = fma(y[u], rp[u * D + c], acc[c]);
+                }
+                for (; j < nn; ++j, yp += MTC, rp += D) {
+                    const double y = __ldcs(yp);
+#pragma unroll
+                    for (int c = 0; c < D; ++c) acc[c] = fma(y, rp[c], acc[c]);
+                }
+            }
+        } else if (lane < MT) {
             // batches of WB independent column loads in flight per lane (the loop is latency-bound otherwise)
             int j = 0;
             for (; j + WB <= nn; j += WB) {
@@ -1558,7 +1580,13 @@ static void launch_schur_perpatch(const PatchSet& P, const Factors& F, const dou
             const char* e = getenv("RAV_SCHUR_WB");
             return e ? atoi(e) : 8;
         }();
-        auto kern = wb >= 24 ? schur_sweep_warp_kernel<D, DET, 24>
+        static const int mtc = [] {   // compile-time restricted-node count for the 3D PoU shape
+            const char* e = getenv("RAV_SCHUR_MTC");
+            return e ? atoi(e) : 1;
+        }();
+        auto kern = (mtc && D == 3 && F.MT == 27) ? (wb >= 16 ? schur_sweep_warp_kernel<D, DET, 16, 27>
+                                                              : schur_sweep_warp_kernel<D, DET, 8, 27>)
+                  : wb >= 24 ? schur_sweep_warp_kernel<D, DET, 24>
                   : wb >= 16 ? schur_sweep_warp_kernel<D, DET, 16> : schur_sweep_warp_kernel<D, DET, 8>;
         kern<<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD, F.NR, F.fac, r, x,
                                         omega, F.cbuf, wpf);
