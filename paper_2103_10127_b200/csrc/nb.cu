@@ -222,7 +222,9 @@ struct NbCols {
     int bulk;   // prologue: the warp's whole slice into L2 by one bulk prefetch
 };
 
-template <int D, int G, int UA, int MINB = 1, bool PAT = false, bool PR = false>
+// XA: x is 16-byte aligned (checked once at launch), so the node gathers of the pair layout are
+// single 16-byte loads without the per-load alignment test of ld_node
+template <int D, int G, int UA, int MINB = 1, bool PAT = false, bool PR = false, bool XA = false>
 __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64_t nnodes, int64_t nslices, int64_t nvel,
                                                           const int32_t* __restrict__ perm,
                                                           const int32_t* __restrict__ wa,
@@ -234,6 +236,15 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                                                           const double* __restrict__ b, double* __restrict__ r,
                                                           double* __restrict__ part) {
     static_assert(!PR || D == 2, "pair layout is 2D only");
+    auto ldx2 = [&](const double* p, double* out) {
+        if constexpr (XA) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+            out[0] = v.x;
+            out[1] = v.y;
+        } else {
+            ld_node<2>(p, out);
+        }
+    };
     const int32_t* __restrict__ col = cols.col;
     __shared__ double red[8];
     double mine = 0.0;
@@ -298,8 +309,8 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                     for (int p = 0; p < A2; ++p) {
                         const double2 a = __ldcs(pA + (int64_t)p * NB_C);
                         double x0[2], x1[2];
-                        ld_node<2>(x + NB_COLA(2 * p), x0);
-                        ld_node<2>(x + NB_COLA(2 * p + 1), x1);
+                        ldx2(x + NB_COLA(2 * p), x0);
+                        ldx2(x + NB_COLA(2 * p + 1), x1);
                         acc[0] = fma(a.x, x0[0], acc[0]);
                         acc[1] = fma(a.x, x0[1], acc[1]);
                         acc[0] = fma(a.y, x1[0], acc[0]);
@@ -308,7 +319,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                     if (A & 1) {
                         const double a = __ldcs(vs + (int64_t)(2 * A2) * NB_C + l);
                         double x0[2];
-                        ld_node<2>(x + NB_COLA(A - 1), x0);
+                        ldx2(x + NB_COLA(A - 1), x0);
                         acc[0] = fma(a, x0[0], acc[0]);
                         acc[1] = fma(a, x0[1], acc[1]);
                     }
@@ -357,7 +368,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
 #pragma unroll UA
                     for (int k = 0; k < B; ++k) {
                         double xv[2];
-                        ld_node<2>(x + NB_COLB(k), xv);
+                        ldx2(x + NB_COLB(k), xv);
                         const double2 bv = __ldcs(pB + (int64_t)k * NB_C);
                         acc = fma(bv.x, xv[0], acc);
                         acc = fma(bv.y, xv[1], acc);
@@ -733,7 +744,7 @@ static int nb_block_threads() {
     return bs;
 }
 
-template <int D, int G, int UA, bool PR = false>
+template <int D, int G, int UA, bool PR = false, bool XA = false>
 static void nb_launch(const NodeBlocked& N, const double* x, const double* b, double* r, double* part, int nblk,
                       cudaStream_t s, int* used) {
     static const int bulk = [] {   // measured: c2 85.2 -> 81.1 us, c3 1549 -> 1426 us
@@ -750,10 +761,10 @@ static void nb_launch(const NodeBlocked& N, const double* x, const double* b, do
         const char* e = getenv("RAV_NB_MINB");
         return e ? atoi(e) : 6;
     }();
-    auto kern = N.tbl ? ((minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8, true, PR>
-                         : (minb >= 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6, true, PR>
-                         : (minb == 5 && G == 1) ? nb_residual_kernel<D, G, UA, 5, true, PR>
-                                                 : nb_residual_kernel<D, G, UA, 1, true, PR>)
+    auto kern = N.tbl ? ((minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8, true, PR, XA>
+                         : (minb >= 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6, true, PR, XA>
+                         : (minb == 5 && G == 1) ? nb_residual_kernel<D, G, UA, 5, true, PR, XA>
+                                                 : nb_residual_kernel<D, G, UA, 1, true, PR, XA>)
               : (minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8, false, PR>
               : (minb >= 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6, false, PR>
                                       : nb_residual_kernel<D, G, UA, 1, false, PR>;
@@ -792,7 +803,9 @@ rav_status launch_nb_residual(const Csr& A, const double* x, const double* b, do
         else if (G == 2) nb_launch<3, 2, 4>(N, x, b, r, part, nblk, s, used);
         else nb_launch<3, 1, 8>(N, x, b, r, part, nblk, s, used);
     } else {
-        if (N.pair) {
+        if (N.pair && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && G == 1) {
+            nb_launch<2, 1, 4, true, true>(N, x, b, r, part, nblk, s, used);
+        } else if (N.pair) {
             if (G == 32) nb_launch<2, 32, 2, true>(N, x, b, r, part, nblk, s, used);
             else if (G == 8) nb_launch<2, 8, 4, true>(N, x, b, r, part, nblk, s, used);
             else if (G >= 4) nb_launch<2, 4, 4, true>(N, x, b, r, part, nblk, s, used);
