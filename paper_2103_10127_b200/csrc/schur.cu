@@ -409,7 +409,8 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
 // DET: the corrections go to per-patch slots cbuf[i (MT D + 1) + k D + c] (pressure: slot MT D)
 // instead of atomics; det_gather_kernel adds them to x in ascending patch order (rav_opts.deterministic)
 // NDP: node indices from (nbase[i], pattern table ntbl[npid[i] * NN + j]) instead of the ND array
-template <int MT, int D, int MINB, int NRB = 0, bool DET = false, bool NDP = false>   // NRB > 0: compile-time rect pairs
+// RA: r is 16-byte aligned (checked at launch): node gathers without the per-load alignment test
+template <int MT, int D, int MINB, int NRB = 0, bool DET = false, bool NDP = false, bool RA = false>   // NRB > 0: compile-time rect pairs
 __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
                                                                  const double2* __restrict__ W,
                                                                  const int32_t* __restrict__ ND,
@@ -454,6 +455,15 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
         if (chunk >= tail0) pf = 0;
     }
     pdl_wait();
+    auto ldr = [&](const double* p, double* out) {
+        if constexpr (RA && D == 2) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+            out[0] = v.x;
+            out[D - 1] = v.y;
+        } else {
+            ld_node<D>(p, out);
+        }
+    };
     // MINB > 4: g_R lives in shared memory (one column per thread, conflict-free), which frees 2 MT D
     // registers for a higher residency
     constexpr bool SG = MINB > 4;
@@ -463,7 +473,7 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
 #pragma unroll
     for (int k = 0; k < MT; ++k) {
         const int nd = ND_AT(k);
-        ld_node<D>(r + nd, rr[k]);
+        ldr(r + nd, rr[k]);
 #pragma unroll
         for (int c = 0; c < D; ++c) acc[k][c] = 0.0;
     }
@@ -503,8 +513,8 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
             bulk_prefetch_l2(W + chunk * pairs * 32 + (int64_t)(TRI_PAD / 2 + (b + pf) * RC) * 32, (uint32_t)(RC * 512));
         double ra[D], rb[D];
         const int n0 = ND_AT(j0), n1 = ND_AT(j0 + 1);
-        ld_node<D>(r + n0, ra);
-        ld_node<D>(r + n1, rb);
+        ldr(r + n0, ra);
+        ldr(r + n1, rb);
         const double2* wq = wq0 + (int64_t)((j0 - MT) / 2) * RC * 32;
 #pragma unroll
         for (int p = 0; p < RC; ++p) {
@@ -1497,7 +1507,9 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
         const char* e = getenv("RAV_SCHUR_MINB");
         return e ? atoi(e) : 4;
     }();
-    auto kern = F.npid ? ((MT == 9 && F.NN == 25) ? schur_sweep_thread_kernel<MT, 2, 4, 8, DET, true>
+    const bool ra = (reinterpret_cast<uintptr_t>(r) & 15) == 0;
+    auto kern = F.npid ? ((MT == 9 && F.NN == 25) ? (ra ? schur_sweep_thread_kernel<MT, 2, 4, 8, DET, true, true>
+                                                        : schur_sweep_thread_kernel<MT, 2, 4, 8, DET, true>)
                                                   : schur_sweep_thread_kernel<MT, 2, 4, 0, DET, true>)
               : (MT == 9 && F.NN == 25) ? (minb >= 6 ? schur_sweep_thread_kernel<MT, 2, 6, 8, DET>
                                            : minb == 5 ? schur_sweep_thread_kernel<MT, 2, 5, 8, DET>
