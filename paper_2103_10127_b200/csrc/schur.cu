@@ -66,6 +66,8 @@ struct SchurArgs {
     unsigned int* fail;          // bit 0: structure does not hold; bit 1: singular
     unsigned long long* bad;     // smallest singular patch
     unsigned long long* alg;     // sum of algorithmic bytes of the stored data
+    int comp_verified;           // the node-blocked build verified equal component blocks and no
+                                 // cross-component entries for the whole operator (nb.cu)
 };
 
 __device__ __forceinline__ int64_t tri_col_start(int j, int D) { return (int64_t)j * (j + 1) / 2 + (int64_t)j * D; }
@@ -149,8 +151,24 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
             sperm[rank] = t;
         }
         __syncthreads();
-        // gather A_s (component 0 rows), the B column, and verify components 1..D-1
-        for (int t = tid; t < nn * D; t += ST) {
+        // gather A_s (component 0 rows), the B column, and verify components 1..D-1.  With the
+        // component structure verified for the whole operator (nb.cu), the component-0 rows of A_s
+        // are gathered by a merge of the sorted row with the sorted node list and nothing else is
+        // re-checked
+        for (int t = tid; t < nn * D && a.comp_verified; t += ST) {
+            const int j = t / D, c = t % D;
+            const int row = ndof[j] + c;
+            int p = 0;
+            for (int64_t k = a.rp[row]; k < a.rp[row + 1]; ++k) {
+                const int col = a.ci[k];
+                if (col == pd) { bcol[j * D + c] = a.val[k]; continue; }
+                if (c != 0 || col >= a.nvel) continue;
+                const int cn = col / D;
+                while (p < nn && snode[p] < cn) ++p;
+                if (p < nn && snode[p] == cn) M[(size_t)j * ld + sperm[p]] = a.val[k];
+            }
+        }
+        for (int t = tid; t < nn * D && !a.comp_verified; t += ST) {
             const int j = t / D, c = t % D;
             const int row = ndof[j] + c;
             for (int64_t k = a.rp[row]; k < a.rp[row + 1]; ++k) {
@@ -175,7 +193,7 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
             }
         }
         __syncthreads();
-        for (int t = tid; t < nn * (D - 1); t += ST) {
+        for (int t = tid; t < nn * (D - 1) && !a.comp_verified; t += ST) {
             const int j = t / (D - 1), c = 1 + t % (D - 1);
             const int row = ndof[j] + c;
             for (int64_t k = a.rp[row]; k < a.rp[row + 1]; ++k) {
@@ -297,9 +315,18 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
             __syncthreads();
             const double inv = 1.0 / M[(size_t)c * ld + c];
             const int nr = nn - c - 1, ncol = W - c - 1;
-            for (int t = tid; t < nr * ncol; t += ST) {
-                const int r = c + 1 + t / ncol, col = c + 1 + t % ncol;
-                M[(size_t)r * ld + col] -= (M[(size_t)r * ld + c] * inv) * M[(size_t)c * ld + col];
+            if (nr > 0 && ncol > 0) {
+                // flattened (row, column) walk with incremental indices: one division per thread and
+                // pivot instead of a division and a remainder per updated entry
+                const int dq = ST / ncol, dr = ST % ncol;
+                int rr = tid / ncol, cc = tid % ncol;
+                for (int t = tid; t < nr * ncol; t += ST) {
+                    const int r = c + 1 + rr, col = c + 1 + cc;
+                    M[(size_t)r * ld + col] -= (M[(size_t)r * ld + c] * inv) * M[(size_t)c * ld + col];
+                    rr += dq;
+                    cc += dr;
+                    if (cc >= ncol) { cc -= ncol; ++rr; }
+                }
             }
             __syncthreads();
         }
@@ -311,9 +338,15 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
         for (int c = nn - 1; c >= 0; --c) {
             for (int t = tid; t < nrhs; t += ST) M[(size_t)c * ld + nn + t] /= M[(size_t)c * ld + c];
             __syncthreads();
-            for (int t = tid; t < c * nrhs; t += ST) {
-                const int r = t / nrhs, k = t % nrhs;
-                M[(size_t)r * ld + nn + k] -= M[(size_t)r * ld + c] * M[(size_t)c * ld + nn + k];
+            {
+                const int dq = ST / nrhs, dr = ST % nrhs;
+                int r = tid / nrhs, k = tid % nrhs;
+                for (int t = tid; t < c * nrhs; t += ST) {
+                    M[(size_t)r * ld + nn + k] -= M[(size_t)r * ld + c] * M[(size_t)c * ld + nn + k];
+                    r += dq;
+                    k += dr;
+                    if (k >= nrhs) { k -= nrhs; ++r; }
+                }
             }
             __syncthreads();
         }
@@ -1152,6 +1185,7 @@ rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D,
     RAV_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
     RAV_CUDA(cudaMemsetAsync(alg, 0, sizeof(unsigned long long), s));
     a.fail = fail;
+    a.comp_verified = (A.nb.nslices > 0 && A.nb.D == D) ? 1 : 0;
     a.bad = bad;
     a.alg = alg;
     const size_t shmem = sizeof(double) * ((size_t)a.nnmax * a.ld + a.nnmax + (size_t)a.nnmax * D + a.nnmax) +
