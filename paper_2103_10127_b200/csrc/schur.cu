@@ -72,7 +72,10 @@ struct SchurArgs {
 
 __device__ __forceinline__ int64_t tri_col_start(int j, int D) { return (int64_t)j * (j + 1) / 2 + (int64_t)j * D; }
 
-__global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
+// NT threads per CTA: 128 for the small 2D patches (several CTAs per SM), 512 for the
+// 3D patches whose ~150 KB of shared memory allow one CTA per SM
+template <int NT>
+__global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
     extern __shared__ double smem[];
     const int tid = threadIdx.x;
     const int D = a.D;
@@ -141,9 +144,9 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
         }
         const int nn = s_nn, mn = s_mn, pd = s_pd;
         const int W = nn + D + mn, ld = a.ld;
-        for (int t = tid; t < nn * ld; t += ST) M[t] = 0.0;
-        for (int t = tid; t < nn * D; t += ST) bcol[t] = 0.0;
-        for (int t = tid; t < nn; t += ST) {
+        for (int t = tid; t < nn * ld; t += NT) M[t] = 0.0;
+        for (int t = tid; t < nn * D; t += NT) bcol[t] = 0.0;
+        for (int t = tid; t < nn; t += NT) {
             const int nd = ndof[t] / D;
             int rank = 0;
             for (int u = 0; u < nn; ++u) rank += (ndof[u] / D < nd);
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
         // component structure verified for the whole operator (nb.cu), the component-0 rows of A_s
         // are gathered by a merge of the sorted row with the sorted node list and nothing else is
         // re-checked
-        for (int t = tid; t < nn * D && a.comp_verified; t += ST) {
+        for (int t = tid; t < nn * D && a.comp_verified; t += NT) {
             const int j = t / D, c = t % D;
             const int row = ndof[j] + c;
             int p = 0;
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
                 if (p < nn && snode[p] == cn) M[(size_t)j * ld + sperm[p]] = a.val[k];
             }
         }
-        for (int t = tid; t < nn * D && !a.comp_verified; t += ST) {
+        for (int t = tid; t < nn * D && !a.comp_verified; t += NT) {
             const int j = t / D, c = t % D;
             const int row = ndof[j] + c;
             for (int64_t k = a.rp[row]; k < a.rp[row + 1]; ++k) {
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
             }
         }
         __syncthreads();
-        for (int t = tid; t < nn * (D - 1) && !a.comp_verified; t += ST) {
+        for (int t = tid; t < nn * (D - 1) && !a.comp_verified; t += NT) {
             const int j = t / (D - 1), c = 1 + t % (D - 1);
             const int row = ndof[j] + c;
             for (int64_t k = a.rp[row]; k < a.rp[row + 1]; ++k) {
@@ -238,14 +241,14 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
             double* base = a.fac + a.foffs[i];
             double* g = base + nn;
             double* aux = g + (size_t)nn * D;
-            for (int t = tid; t < nn; t += ST) {
+            for (int t = tid; t < nn; t += NT) {
                 const double dj = M[(size_t)t * ld + t];
                 base[t] = 1.0 / dj;
                 if (!(fabs(dj) > 0.0)) atomicOr((unsigned int*)&s_fail, 2u);
                 aux[t] = wnode[t];
             }
-            for (int t = tid; t < nn * D; t += ST) g[t] = bcol[t] / M[(size_t)(t / D) * ld + (t / D)];
-            for (int j = tid; j < nn; j += ST) a.nodes[a.nodeoffs[i] + j] = ndof[j];
+            for (int t = tid; t < nn * D; t += NT) g[t] = bcol[t] / M[(size_t)(t / D) * ld + (t / D)];
+            for (int j = tid; j < nn; j += NT) a.nodes[a.nodeoffs[i] + j] = ndof[j];
             __syncthreads();
             if (tid < 32) {
                 double sacc = 0.0, sa = 0.0;
@@ -273,9 +276,9 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
             continue;
         }
         // right-hand sides: B columns, then e_k for the restricted nodes
-        for (int t = tid; t < nn * D; t += ST) M[(size_t)(t / D) * ld + nn + (t % D)] = bcol[t];
-        for (int k = tid; k < mn; k += ST) M[(size_t)k * ld + nn + D + k] = 1.0;
-        for (int r = tid; r < nn; r += ST) {
+        for (int t = tid; t < nn * D; t += NT) M[(size_t)(t / D) * ld + nn + (t % D)] = bcol[t];
+        for (int k = tid; k < mn; k += NT) M[(size_t)k * ld + nn + D + k] = 1.0;
+        for (int r = tid; r < nn; r += NT) {
             double mx = 0.0;
             for (int c = 0; c < nn; ++c) mx = fmax(mx, fabs(M[(size_t)r * ld + c]));
             rn[r] = mx;
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
             if (s_fail) break;
             const int p = s_piv;
             if (p != c) {
-                for (int t = c + tid; t < W; t += ST) {
+                for (int t = c + tid; t < W; t += NT) {
                     double u = M[(size_t)c * ld + t];
                     M[(size_t)c * ld + t] = M[(size_t)p * ld + t];
                     M[(size_t)p * ld + t] = u;
@@ -318,9 +321,9 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
             if (nr > 0 && ncol > 0) {
                 // flattened (row, column) walk with incremental indices: one division per thread and
                 // pivot instead of a division and a remainder per updated entry
-                const int dq = ST / ncol, dr = ST % ncol;
+                const int dq = NT / ncol, dr = NT % ncol;
                 int rr = tid / ncol, cc = tid % ncol;
-                for (int t = tid; t < nr * ncol; t += ST) {
+                for (int t = tid; t < nr * ncol; t += NT) {
                     const int r = c + 1 + rr, col = c + 1 + cc;
                     M[(size_t)r * ld + col] -= (M[(size_t)r * ld + c] * inv) * M[(size_t)c * ld + col];
                     rr += dq;
@@ -336,12 +339,12 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
         }
         const int nrhs = D + mn;
         for (int c = nn - 1; c >= 0; --c) {
-            for (int t = tid; t < nrhs; t += ST) M[(size_t)c * ld + nn + t] /= M[(size_t)c * ld + c];
+            for (int t = tid; t < nrhs; t += NT) M[(size_t)c * ld + nn + t] /= M[(size_t)c * ld + c];
             __syncthreads();
             {
-                const int dq = ST / nrhs, dr = ST % nrhs;
+                const int dq = NT / nrhs, dr = NT % nrhs;
                 int r = tid / nrhs, k = tid % nrhs;
-                for (int t = tid; t < c * nrhs; t += ST) {
+                for (int t = tid; t < c * nrhs; t += NT) {
                     M[(size_t)r * ld + nn + k] -= M[(size_t)r * ld + c] * M[(size_t)c * ld + nn + k];
                     r += dq;
                     k += dr;
@@ -386,7 +389,7 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
             const int64_t tri = tri_col_start(MT, D);
             const int64_t tri_pad = tri + (tri & 1);
             // entries: column j < MT: Y[0..j][j], g[j][0..D-1]; column j >= MT: Y[0..MT-1][j], g[j][.]
-            for (int t = tid; t < nn * (MT + D); t += ST) {
+            for (int t = tid; t < nn * (MT + D); t += NT) {
                 const int j = t / (MT + D), q = t % (MT + D);
                 int64_t e;
                 double v;
@@ -402,9 +405,9 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
                 }
                 base[((e >> 1) * 32 + lane) * 2 + (e & 1)] = v;
             }
-            for (int j = tid; j < a.NN; j += ST)
+            for (int j = tid; j < a.NN; j += NT)
                 a.ND[(chunk * a.NN + j) * 32 + lane] = j < nn ? ndof[j] : ndof[0];
-            for (int k = tid; k < MT; k += ST)
+            for (int k = tid; k < MT; k += NT)
                 a.AUX[(chunk * (MT + 2) + k) * 32 + lane] = k < mn ? wnode[k] : 0.0;
             if (tid == 0) {
                 a.AUX[(chunk * (MT + 2) + MT) * 32 + lane] = s_wp;
@@ -417,13 +420,13 @@ __global__ void __launch_bounds__(ST) schur_factor_kernel(SchurArgs a) {
             double* Y = a.fac + a.foffs[i];            // MT x nn, column-major (stride MT)
             double* g = Y + (size_t)MT * nn;           // nn * D
             double* aux = g + (size_t)nn * D;          // MT weights, w_p, 1/S
-            for (int t = tid; t < nn * MT; t += ST) {
+            for (int t = tid; t < nn * MT; t += NT) {
                 const int j = t / MT, k = t % MT;
                 Y[t] = k < mn ? M[(size_t)j * ld + nn + D + k] : 0.0;
             }
-            for (int t = tid; t < nn * D; t += ST) g[t] = M[(size_t)(t / D) * ld + nn + (t % D)];
-            for (int k = tid; k < MT; k += ST) aux[k] = k < mn ? wnode[k] : 0.0;
-            for (int j = tid; j < nn; j += ST) a.nodes[a.nodeoffs[i] + j] = ndof[j];
+            for (int t = tid; t < nn * D; t += NT) g[t] = M[(size_t)(t / D) * ld + nn + (t % D)];
+            for (int k = tid; k < MT; k += NT) aux[k] = k < mn ? wnode[k] : 0.0;
+            for (int j = tid; j < nn; j += NT) a.nodes[a.nodeoffs[i] + j] = ndof[j];
             if (tid == 0) {
                 aux[MT] = s_wp;
                 aux[MT + 1] = Sinv;
@@ -1196,11 +1199,15 @@ rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D,
         cudaFreeAsync(bad, s);
         return RAV_OK;
     }
-    if (shmem > 48 * 1024)
-        RAV_CUDA(cudaFuncSetAttribute(schur_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
+    if (shmem > 48 * 1024) {
+        RAV_CUDA(cudaFuncSetAttribute(schur_factor_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
+        RAV_CUDA(cudaFuncSetAttribute(schur_factor_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
+    }
     const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(16, (220 * 1024) / shmem));
     const int grid = (int)std::min<int64_t>(P.n_patches, (int64_t)num_sms() * per_sm);
-    schur_factor_kernel<<<grid, ST, shmem, s>>>(a);
+    // one or two CTAs per SM (3D): 512 threads, measured c4 factor 260 -> see DESIGN; else 128
+    if (per_sm <= 2) schur_factor_kernel<512><<<grid, 512, shmem, s>>>(a);
+    else schur_factor_kernel<128><<<grid, 128, shmem, s>>>(a);
     count_launch();
     RAV_CHECK_LAUNCH();
     unsigned int h_fail = 0;

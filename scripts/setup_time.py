@@ -12,7 +12,7 @@ from paper_2103_10127_b200 import ravgmg as rg
 name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 c = si.CONFIGS[name]
 best = None
-for _ in range(2):
+for _ in range(int(os.environ.get("RAV_SETUP_REPS", "2"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     mg, fine = rg.build_hierarchy(si.config_problem(name), c["levels"], "pou")
