@@ -269,8 +269,36 @@ __global__ void coef_kernel(Grid G, double* eta_tab, double* f_tab) {
 }
 
 // ---- entry formulas -------------------------------------------------------------------
+// Basis values at the quadrature points of the reference element, formed once per CTA (the same
+// expressions the entry formulas evaluated inline before, so the entries do not change): velocity
+// basis v[l][q] and derivative / h_k d[k][l][q]; Q1 (pressure) basis pv[m][q], pd[k][m][q].
+// Removes the per-entry basis polynomials and FP64 divisions from the row-gather assembly.
+struct BasisTab {
+    double v[3][3];
+    double d[3][3][3];
+    double pv[2][3];
+    double pd[3][2][3];
+};
+__device__ void basis_tab_init(const Grid& G, BasisTab& T) {
+    for (int idx = threadIdx.x; idx < 9 + 27 + 6 + 18; idx += blockDim.x) {
+        if (idx < 9) {
+            const int l = idx / 3, q = idx % 3;
+            T.v[l][q] = (q < G.ngp && l <= G.P) ? vbv(G.P, l, G.gt[q]) : 0.0;
+        } else if (idx < 36) {
+            const int t = idx - 9, k = t / 9, l = (t / 3) % 3, q = t % 3;
+            T.d[k][l][q] = (q < G.ngp && l <= G.P) ? vbd(G.P, l, G.gt[q]) / G.h[k] : 0.0;
+        } else if (idx < 42) {
+            const int t = idx - 36, m = t / 3, q = t % 3;
+            T.pv[m][q] = q < G.ngp ? q1v(m, G.gt[q]) : 0.0;
+        } else {
+            const int t = idx - 42, k = t / 6, m = (t / 3) % 2, q = t % 3;
+            T.pd[k][m][q] = q < G.ngp ? q1d(m, G.gt[q]) / G.h[k] : 0.0;
+        }
+    }
+}
+
 // int_e eta grad phi_a . grad phi_b over the elements shared by nodes a and b
-__device__ double a_entry(const Grid& G, const double* eta_tab, const int* a, const int* b) {
+__device__ double a_entry(const Grid& G, const BasisTab& T, const double* eta_tab, const int* a, const int* b) {
     int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < G.dim; ++k) {
         int la, ha, lb, hb;
@@ -293,10 +321,9 @@ __device__ double a_entry(const Grid& G, const double* eta_tab, const int* a, co
                     int qk[3] = {q % g, (q / g) % g, q / (g * g)};
                     double va[3], vb[3], da[3], db[3], w = G.vol;
                     for (int k = 0; k < G.dim; ++k) {
-                        double t = G.gt[qk[k]];
                         w *= G.gw[qk[k]];
-                        va[k] = vbv(G.P, la[k], t); vb[k] = vbv(G.P, lb[k], t);
-                        da[k] = vbd(G.P, la[k], t) / G.h[k]; db[k] = vbd(G.P, lb[k], t) / G.h[k];
+                        va[k] = T.v[la[k]][qk[k]]; vb[k] = T.v[lb[k]][qk[k]];
+                        da[k] = T.d[k][la[k]][qk[k]]; db[k] = T.d[k][lb[k]][qk[k]];
                     }
                     double dot = 0.0;
                     for (int k = 0; k < G.dim; ++k) {
@@ -311,7 +338,7 @@ __device__ double a_entry(const Grid& G, const double* eta_tab, const int* a, co
 }
 
 // -int_e psi_v d_c phi_b over the elements shared by node b and vertex v
-__device__ double b_entry(const Grid& G, const int* b, int c, const int* v) {
+__device__ double b_entry(const Grid& G, const BasisTab& T, const int* b, int c, const int* v) {
     int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < G.dim; ++k) {
         int lb, hb, lv, hv;
@@ -333,10 +360,9 @@ __device__ double b_entry(const Grid& G, const int* b, int c, const int* v) {
                     int qk[3] = {q % g, (q / g) % g, q / (g * g)};
                     double w = G.vol, psi = 1.0, dphi = 1.0;
                     for (int k = 0; k < G.dim; ++k) {
-                        double t = G.gt[qk[k]];
                         w *= G.gw[qk[k]];
-                        psi *= q1v(lm[k], t);
-                        dphi *= (k == c) ? vbd(G.P, lb[k], t) / G.h[k] : vbv(G.P, lb[k], t);
+                        psi *= T.pv[lm[k]][qk[k]];
+                        dphi *= (k == c) ? T.d[k][lb[k]][qk[k]] : T.v[lb[k]][qk[k]];
                     }
                     s -= (w * psi) * dphi;
                 }
@@ -345,7 +371,7 @@ __device__ double b_entry(const Grid& G, const int* b, int c, const int* v) {
 }
 
 // int f_c phi_a over the elements containing node a (2D manufactured forcing)
-__device__ double f_entry(const Grid& G, const double* f_tab, const int* a, int c) {
+__device__ double f_entry(const Grid& G, const BasisTab& T, const double* f_tab, const int* a, int c) {
     if (G.kind != 1) return 0.0;
     int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < G.dim; ++k) node_elems(G.P, a[k], G.n[k], lo[k], hi[k]);
@@ -357,9 +383,8 @@ __device__ double f_entry(const Grid& G, const double* f_tab, const int* a, int 
             int la[2] = {a[0] - G.P * e[0], a[1] - G.P * e[1]};
             int64_t el = elem_id(G, e);
             for (int q = 0; q < NG; ++q) {
-                double t0 = G.gt[q % g], t1 = G.gt[q / g];
                 double w = G.vol * G.gw[q % g] * G.gw[q / g];
-                s += (w * f_tab[2 * (el * NG + q) + c]) * (vbv(G.P, la[0], t0) * vbv(G.P, la[1], t1));
+                s += (w * f_tab[2 * (el * NG + q) + c]) * (T.v[la[0]][q % g] * T.v[la[1]][q / g]);
             }
         }
     return s;
@@ -367,7 +392,7 @@ __device__ double f_entry(const Grid& G, const double* f_tab, const int* a, int 
 
 // Q1-Q1 stabilization (Eq. 8, R18): -beta_0 h_e^2 int (1/eta) grad psi_v . grad psi_u over the
 // elements shared by vertices v and u
-__device__ double c_entry(const Grid& G, const double* eta_tab, const int* v, const int* u) {
+__device__ double c_entry(const Grid& G, const BasisTab& T, const double* eta_tab, const int* v, const int* u) {
     int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < G.dim; ++k) {
         int lv, hv, lu, hu;
@@ -390,10 +415,9 @@ __device__ double c_entry(const Grid& G, const double* eta_tab, const int* v, co
                     int qk[3] = {q % g, (q / g) % g, q / (g * g)};
                     double vv[3], vu[3], dv[3], du[3], w = G.vol;
                     for (int k = 0; k < G.dim; ++k) {
-                        double t = G.gt[qk[k]];
                         w *= G.gw[qk[k]];
-                        vv[k] = q1v(lv[k], t); vu[k] = q1v(lu[k], t);
-                        dv[k] = q1d(lv[k], t) / G.h[k]; du[k] = q1d(lu[k], t) / G.h[k];
+                        vv[k] = T.pv[lv[k]][qk[k]]; vu[k] = T.pv[lu[k]][qk[k]];
+                        dv[k] = T.pd[k][lv[k]][qk[k]]; du[k] = T.pd[k][lu[k]][qk[k]];
                     }
                     double dot = 0.0;
                     for (int k = 0; k < G.dim; ++k) {
@@ -464,6 +488,9 @@ __global__ void op_count_kernel(Grid G, int64_t* cnt) {
 
 __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_tab, const int64_t* rp,
                                int32_t* col, double* val, double* rhs, unsigned int* err) {
+    __shared__ BasisTab T;
+    basis_tab_init(G, T);
+    __syncthreads();
     for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < G.ndof_loc;
          row += (int64_t)gridDim.x * blockDim.x) {
         int64_t p = rp[row];
@@ -487,11 +514,11 @@ __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_ta
                             const int64_t lc = loc_vel(G, fb * G.dim + c);
                             if (lc < 0) atomicOr(err, 1u);
                             col[p] = (int32_t)lc;
-                            val[p] = a_entry(G, eta_tab, a, b);
+                            val[p] = a_entry(G, T, eta_tab, a, b);
                             ++p;
                         } else {
                             double ud = dirichlet(G, b, c);
-                            if (ud != 0.0) lift -= a_entry(G, eta_tab, a, b) * ud;
+                            if (ud != 0.0) lift -= a_entry(G, T, eta_tab, a, b) * ud;
                         }
                     } else {
                         for (int cc = 0; cc < G.dim; ++cc) {
@@ -499,11 +526,11 @@ __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_ta
                                 const int64_t lc = loc_vel(G, fb * G.dim + cc);
                                 if (lc < 0) atomicOr(err, 1u);
                                 col[p] = (int32_t)lc;
-                                val[p] = b_entry(G, b, cc, a);
+                                val[p] = b_entry(G, T, b, cc, a);
                                 ++p;
                             } else {
                                 double ud = dirichlet(G, b, cc);
-                                if (ud != 0.0) lift -= b_entry(G, b, cc, a) * ud;
+                                if (ud != 0.0) lift -= b_entry(G, T, b, cc, a) * ud;
                             }
                         }
                     }
@@ -516,11 +543,11 @@ __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_ta
                         const int64_t lc = loc_vert(G, vert_id(G, v));
                         if (lc < 0) atomicOr(err, 1u);
                         col[p] = (int32_t)lc;
-                        val[p] = vel ? b_entry(G, a, c, v) : c_entry(G, eta_tab, a, v);
+                        val[p] = vel ? b_entry(G, T, a, c, v) : c_entry(G, T, eta_tab, a, v);
                         ++p;
                     }
         }
-        rhs[row] = vel ? f_entry(G, f_tab, a, c) + lift : lift;
+        rhs[row] = vel ? f_entry(G, T, f_tab, a, c) + lift : lift;
     }
 }
 
