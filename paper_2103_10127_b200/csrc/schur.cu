@@ -86,12 +86,23 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
     int32_t* ndof = (int32_t*)(wnode + a.nnmax);              // nnmax: dof of component 0
     int32_t* snode = ndof + a.nnmax;                          // sorted node ids (dof / D)
     int32_t* sperm = snode + a.nnmax;                         // local index of sorted entry
-    __shared__ int s_nn, s_mn, s_pd, s_fail, s_piv;
+    __shared__ int s_nn, s_mn, s_pd, s_fail, s_piv, s_sym;
     __shared__ double s_wp, s_cpp;
 
     for (int64_t i = blockIdx.x; i < a.np; i += gridDim.x) {
         const int64_t off = a.poffs[i];
         const int n = (int)(a.poffs[i + 1] - off);
+        __syncthreads();
+        // the patch's DoF list and weights into shared memory by all threads (M is free here and
+        // holds nnmax * ld >= n doubles + ints), then the sequential scan reads shared memory only
+        double* stw = M;
+        int32_t* std_ = reinterpret_cast<int32_t*>(M + n);
+        const bool staged = (size_t)n * 12 + 8 <= (size_t)a.nnmax * a.ld * 8;
+        if (staged)
+            for (int t = tid; t < n; t += NT) {
+                std_[t] = a.pdofs[off + t];
+                stw[t] = a.pw[off + t];
+            }
         __syncthreads();
         if (tid == 0) {
             // node table + structure checks (sequential: n <= a few hundred)
@@ -99,8 +110,8 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
             double wcur = 0.0, wp = 0.0;
             bool in_rest = true;
             for (int t = 0; t < n && !fail; ++t) {
-                const int dof = a.pdofs[off + t];
-                const double w = a.pw[off + t];
+                const int dof = staged ? std_[t] : a.pdofs[off + t];
+                const double w = staged ? stw[t] : a.pw[off + t];
                 if (dof >= a.nvel) {
                     if (pd >= 0) fail = 1;
                     pd = dof;
@@ -213,22 +224,21 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
                 if (M[(size_t)j * ld + sperm[pos]] != a.val[k]) atomicOr((unsigned int*)&s_fail, 1u);
             }
         }
-        // pressure row: symmetric B and C_pp
-        if (tid == 0) {
-            for (int64_t k = a.rp[pd]; k < a.rp[pd + 1]; ++k) {
-                const int col = a.ci[k];
-                if (col == pd) { s_cpp = a.val[k]; continue; }
-                if (col >= a.nvel) continue;
-                const int cn = col / D, cc = col % D;
-                int lo = 0, hi = nn - 1, pos = -1;
-                while (lo <= hi) {
-                    int mid = (lo + hi) >> 1;
-                    if (snode[mid] == cn) { pos = mid; break; }
-                    if (snode[mid] < cn) lo = mid + 1; else hi = mid - 1;
-                }
-                if (pos < 0) continue;
-                if (bcol[sperm[pos] * D + cc] != a.val[k]) s_fail = 1;
+        // pressure row: symmetric B and C_pp (entries in parallel: one thread walking a 3D pressure
+        // row of 375 entries with dependent global loads kept the other warps at the barrier)
+        for (int64_t k = a.rp[pd] + tid; k < a.rp[pd + 1]; k += NT) {
+            const int col = a.ci[k];
+            if (col == pd) { s_cpp = a.val[k]; continue; }
+            if (col >= a.nvel) continue;
+            const int cn = col / D, cc = col % D;
+            int lo = 0, hi = nn - 1, pos = -1;
+            while (lo <= hi) {
+                int mid = (lo + hi) >> 1;
+                if (snode[mid] == cn) { pos = mid; break; }
+                if (snode[mid] < cn) lo = mid + 1; else hi = mid - 1;
             }
+            if (pos < 0) continue;
+            if (bcol[sperm[pos] * D + cc] != a.val[k]) atomicOr((unsigned int*)&s_fail, 1u);
         }
         __syncthreads();
         if (s_fail) {
@@ -283,9 +293,38 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
             for (int c = 0; c < nn; ++c) mx = fmax(mx, fabs(M[(size_t)r * ld + c]));
             rn[r] = mx;
         }
+        // symmetric A_s (every generated operator: the principal block of the SPD viscous operator)
+        // is eliminated without pivoting -- one barrier per column instead of three; an unsymmetric
+        // block keeps partial pivoting
+        if (tid == 0) s_sym = 1;
         __syncthreads();
+        for (int t = tid; t < nn * nn; t += NT) {
+            const int r = t / nn, c = t % nn;
+            if (c > r && M[(size_t)r * ld + c] != M[(size_t)c * ld + r]) s_sym = 0;
+        }
+        __syncthreads();
+        const bool nopiv = s_sym != 0;
         // Gaussian elimination with partial pivoting (A_s symmetric: A_s^T = A_s)
         for (int c = 0; c < nn; ++c) {
+            if (nopiv) {
+                const double piv = M[(size_t)c * ld + c];
+                if (tid == 0 && !(fabs(piv) > 1e-14 * rn[c])) s_fail = 2;
+                const double inv = 1.0 / piv;
+                const int nr = nn - c - 1, ncol = W - c - 1;
+                if (nr > 0 && ncol > 0) {
+                    const int dq = NT / ncol, dr = NT % ncol;
+                    int rr = tid / ncol, cc = tid % ncol;
+                    for (int t = tid; t < nr * ncol; t += NT) {
+                        const int r = c + 1 + rr, col = c + 1 + cc;
+                        M[(size_t)r * ld + col] -= (M[(size_t)r * ld + c] * inv) * M[(size_t)c * ld + col];
+                        rr += dq;
+                        cc += dr;
+                        if (cc >= ncol) { cc -= ncol; ++rr; }
+                    }
+                }
+                __syncthreads();
+                continue;
+            }
             if (tid < 32) {
                 double best = -1.0;
                 int bi = c;
