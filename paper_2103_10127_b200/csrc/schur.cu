@@ -169,17 +169,32 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
         // component structure verified for the whole operator (nb.cu), the component-0 rows of A_s
         // are gathered by a merge of the sorted row with the sorted node list and nothing else is
         // re-checked
-        for (int t = tid; t < nn * D && a.comp_verified; t += NT) {
-            const int j = t / D, c = t % D;
-            const int row = ndof[j] + c;
-            int p = 0;
-            for (int64_t k = a.rp[row]; k < a.rp[row + 1]; ++k) {
-                const int col = a.ci[k];
-                if (col == pd) { bcol[j * D + c] = a.val[k]; continue; }
-                if (c != 0 || col >= a.nvel) continue;
-                const int cn = col / D;
-                while (p < nn && snode[p] < cn) ++p;
-                if (p < nn && snode[p] == cn) M[(size_t)j * ld + sperm[p]] = a.val[k];
+        if (a.comp_verified) {
+            // one warp per component-0 row, its lanes over the row's entries (independent loads; a
+            // thread per row walked ~34 entries with dependent global loads in 2D); the lane that
+            // meets the patch's pressure column also takes the other components' B entries, at the
+            // same offset of their rows (verified identical structure)
+            const int warp = tid >> 5, lane = tid & 31;
+            for (int j = warp; j < nn; j += NT / 32) {
+                const int row = ndof[j];
+                const int64_t k0 = a.rp[row], k1 = a.rp[row + 1];
+                for (int64_t k = k0 + lane; k < k1; k += 32) {
+                    const int col = a.ci[k];
+                    if (col == pd) {
+                        bcol[j * D] = a.val[k];
+                        for (int c = 1; c < D; ++c) bcol[j * D + c] = a.val[a.rp[row + c] + (k - k0)];
+                        continue;
+                    }
+                    if (col >= a.nvel) continue;
+                    const int cn = col / D;
+                    int lo = 0, hi = nn - 1, pos = -1;
+                    while (lo <= hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (snode[mid] == cn) { pos = mid; break; }
+                        if (snode[mid] < cn) lo = mid + 1; else hi = mid - 1;
+                    }
+                    if (pos >= 0) M[(size_t)j * ld + sperm[pos]] = a.val[k];
+                }
             }
         }
         for (int t = tid; t < nn * D && !a.comp_verified; t += NT) {
