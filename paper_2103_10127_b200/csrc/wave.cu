@@ -13,10 +13,12 @@
 //     entries it reads, or read the r rows it overwrites, are done;
 //   * A-band b of sweep s waits until the R-bands of sweep s that write the r entries it
 //     reads, or read the x entries it updates, are done.
-// The dependency ranges come from the operator and the patch lists at setup (wave_build).
-// Completion is counted per band (release add after a fence by every thread); waits are
-// acquire loads by one thread followed by a CTA barrier.  x and r are read with strong
-// (L1-bypassing, .relaxed.gpu) loads, because the producing kernel may still be running.
+// The dependency ranges come from the operator and the patch lists at setup (wave_build);
+// an A-band waits on up to three R-band ranges (node rows, pressure rows, the one band that
+// holds both).  Completion is counted per band: the CTA barrier, then one release add.  A
+// wait: one thread per band polls with relaxed loads and issues an acquire fence, then the
+// CTA barrier.  x and r are then read with weak L1-cacheable loads (the fence invalidated
+// the SM's L1).  Measured: correct, but no faster than the plain chain (DESIGN 7).
 //
 // Progress: a kernel of the chain is launched only after every CTA of its predecessor has
 // started (the trigger is the first instruction), so every CTA a waiter depends on is
