@@ -297,8 +297,82 @@ __device__ void basis_tab_init(const Grid& G, BasisTab& T) {
     }
 }
 
+// Element matrices (row a1).  A_e[i][j] = int_e eta grad phi_i . grad phi_j (i <= j, local node
+// index i = l_x + (P+1) l_y [+ (P+1)^2 l_z]) is formed once per element by elem_a_kernel with the
+// quadrature of the former per-entry loop; an entry then sums A_e over the elements its two nodes
+// share, in the same element order.  The B block is the same for every element of a uniform
+// level: B_e[i][m][c] = -int_e psi_m d_c phi_i, formed once per CTA in shared memory.
+__device__ __forceinline__ int pair_index(int NL, int i, int j) {   // i <= j
+    return i * NL - i * (i - 1) / 2 + (j - i);
+}
+
+__global__ void elem_a_kernel(Grid G, const double* __restrict__ eta_tab, double* __restrict__ Ae) {
+    __shared__ BasisTab T;
+    basis_tab_init(G, T);
+    __syncthreads();
+    const int P1 = G.P + 1;
+    const int NL = G.dim == 2 ? P1 * P1 : P1 * P1 * P1;
+    const int NPAIR = NL * (NL + 1) / 2;
+    const int g = G.ngp, NG = G.dim == 2 ? g * g : g * g * g;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < G.nel * NPAIR;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t el = t / NPAIR;
+        int pr = (int)(t % NPAIR), i = 0;
+        while (pr >= NL - i) { pr -= NL - i; ++i; }
+        const int j = i + pr;
+        int la[3] = {0, 0, 0}, lb[3] = {0, 0, 0};
+        for (int k = 0, ii = i, jj = j; k < G.dim; ++k) { la[k] = ii % P1; ii /= P1; lb[k] = jj % P1; jj /= P1; }
+        const double* et = eta_tab + el * NG;
+        double s = 0.0;
+        for (int q = 0; q < NG; ++q) {
+            int qk[3] = {q % g, (q / g) % g, q / (g * g)};
+            double va[3], vb[3], da[3], db[3], w = G.vol;
+            for (int k = 0; k < G.dim; ++k) {
+                w *= G.gw[qk[k]];
+                va[k] = T.v[la[k]][qk[k]]; vb[k] = T.v[lb[k]][qk[k]];
+                da[k] = T.d[k][la[k]][qk[k]]; db[k] = T.d[k][lb[k]][qk[k]];
+            }
+            double dot = 0.0;
+            for (int k = 0; k < G.dim; ++k) {
+                double ga = da[k], gb = db[k];
+                for (int m = 0; m < G.dim; ++m) if (m != k) { ga *= va[m]; gb *= vb[m]; }
+                dot += ga * gb;
+            }
+            s += (w * et[q]) * dot;
+        }
+        Ae[t] = s;
+    }
+}
+
+struct ElemB {
+    double b[27][8][3];
+};
+__device__ void elem_b_init(const Grid& G, const BasisTab& T, ElemB& E) {
+    const int P1 = G.P + 1;
+    const int NL = G.dim == 2 ? P1 * P1 : P1 * P1 * P1;
+    const int NV = G.dim == 2 ? 4 : 8;
+    const int g = G.ngp, NG = G.dim == 2 ? g * g : g * g * g;
+    for (int idx = threadIdx.x; idx < NL * NV * G.dim; idx += blockDim.x) {
+        const int c = idx % G.dim, m = (idx / G.dim) % NV, i = idx / (G.dim * NV);
+        int lb[3] = {0, 0, 0}, lm[3] = {0, 0, 0};
+        for (int k = 0, ii = i, mm = m; k < G.dim; ++k) { lb[k] = ii % P1; ii /= P1; lm[k] = mm % 2; mm /= 2; }
+        double s = 0.0;
+        for (int q = 0; q < NG; ++q) {
+            int qk[3] = {q % g, (q / g) % g, q / (g * g)};
+            double w = G.vol, psi = 1.0, dphi = 1.0;
+            for (int k = 0; k < G.dim; ++k) {
+                w *= G.gw[qk[k]];
+                psi *= T.pv[lm[k]][qk[k]];
+                dphi *= (k == c) ? T.d[k][lb[k]][qk[k]] : T.v[lb[k]][qk[k]];
+            }
+            s -= (w * psi) * dphi;
+        }
+        E.b[i][m][c] = s;
+    }
+}
+
 // int_e eta grad phi_a . grad phi_b over the elements shared by nodes a and b
-__device__ double a_entry(const Grid& G, const BasisTab& T, const double* eta_tab, const int* a, const int* b) {
+__device__ double a_entry(const Grid& G, const double* __restrict__ Ae, const int* a, const int* b) {
     int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < G.dim; ++k) {
         int la, ha, lb, hb;
@@ -308,37 +382,26 @@ __device__ double a_entry(const Grid& G, const BasisTab& T, const double* eta_ta
         hi[k] = min(ha, hb);
         if (lo[k] > hi[k]) return 0.0;
     }
-    const int g = G.ngp, NG = G.dim == 2 ? g * g : g * g * g;
+    const int P1 = G.P + 1;
+    const int NL = G.dim == 2 ? P1 * P1 : P1 * P1 * P1;
+    const int NPAIR = NL * (NL + 1) / 2;
     double s = 0.0;
     int e[3] = {0, 0, 0};
     for (e[2] = lo[2]; e[2] <= hi[2]; ++e[2])
         for (e[1] = lo[1]; e[1] <= hi[1]; ++e[1])
             for (e[0] = lo[0]; e[0] <= hi[0]; ++e[0]) {
-                int la[3], lb[3];
-                for (int k = 0; k < 3; ++k) { la[k] = a[k] - G.P * e[k]; lb[k] = b[k] - G.P * e[k]; }
-                const double* et = eta_tab + elem_id(G, e) * NG;
-                for (int q = 0; q < NG; ++q) {
-                    int qk[3] = {q % g, (q / g) % g, q / (g * g)};
-                    double va[3], vb[3], da[3], db[3], w = G.vol;
-                    for (int k = 0; k < G.dim; ++k) {
-                        w *= G.gw[qk[k]];
-                        va[k] = T.v[la[k]][qk[k]]; vb[k] = T.v[lb[k]][qk[k]];
-                        da[k] = T.d[k][la[k]][qk[k]]; db[k] = T.d[k][lb[k]][qk[k]];
-                    }
-                    double dot = 0.0;
-                    for (int k = 0; k < G.dim; ++k) {
-                        double ga = da[k], gb = db[k];
-                        for (int j = 0; j < G.dim; ++j) if (j != k) { ga *= va[j]; gb *= vb[j]; }
-                        dot += ga * gb;
-                    }
-                    s += (w * et[q]) * dot;
+                int ia = 0, ib = 0;
+                for (int k = G.dim - 1; k >= 0; --k) {
+                    ia = ia * P1 + (a[k] - G.P * e[k]);
+                    ib = ib * P1 + (b[k] - G.P * e[k]);
                 }
+                s += __ldg(Ae + elem_id(G, e) * NPAIR + pair_index(NL, min(ia, ib), max(ia, ib)));
             }
     return s;
 }
 
 // -int_e psi_v d_c phi_b over the elements shared by node b and vertex v
-__device__ double b_entry(const Grid& G, const BasisTab& T, const int* b, int c, const int* v) {
+__device__ double b_entry(const Grid& G, const ElemB& E, const int* b, int c, const int* v) {
     int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (int k = 0; k < G.dim; ++k) {
         int lb, hb, lv, hv;
@@ -348,24 +411,18 @@ __device__ double b_entry(const Grid& G, const BasisTab& T, const int* b, int c,
         hi[k] = min(hb, hv);
         if (lo[k] > hi[k]) return 0.0;
     }
-    const int g = G.ngp, NG = G.dim == 2 ? g * g : g * g * g;
+    const int P1 = G.P + 1;
     double s = 0.0;
     int e[3] = {0, 0, 0};
     for (e[2] = lo[2]; e[2] <= hi[2]; ++e[2])
         for (e[1] = lo[1]; e[1] <= hi[1]; ++e[1])
             for (e[0] = lo[0]; e[0] <= hi[0]; ++e[0]) {
-                int lb[3], lm[3];
-                for (int k = 0; k < 3; ++k) { lb[k] = b[k] - G.P * e[k]; lm[k] = v[k] - e[k]; }
-                for (int q = 0; q < NG; ++q) {
-                    int qk[3] = {q % g, (q / g) % g, q / (g * g)};
-                    double w = G.vol, psi = 1.0, dphi = 1.0;
-                    for (int k = 0; k < G.dim; ++k) {
-                        w *= G.gw[qk[k]];
-                        psi *= T.pv[lm[k]][qk[k]];
-                        dphi *= (k == c) ? T.d[k][lb[k]][qk[k]] : T.v[lb[k]][qk[k]];
-                    }
-                    s -= (w * psi) * dphi;
+                int ib = 0, im = 0;
+                for (int k = G.dim - 1; k >= 0; --k) {
+                    ib = ib * P1 + (b[k] - G.P * e[k]);
+                    im = im * 2 + (v[k] - e[k]);
                 }
+                s += E.b[ib][im][c];
             }
     return s;
 }
@@ -486,10 +543,13 @@ __global__ void op_count_kernel(Grid G, int64_t* cnt) {
     }
 }
 
-__global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_tab, const int64_t* rp,
-                               int32_t* col, double* val, double* rhs, unsigned int* err) {
+__global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* __restrict__ Ae, const double* f_tab,
+                               const int64_t* rp, int32_t* col, double* val, double* rhs, unsigned int* err) {
     __shared__ BasisTab T;
+    __shared__ ElemB E;
     basis_tab_init(G, T);
+    __syncthreads();
+    elem_b_init(G, T, E);
     __syncthreads();
     for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < G.ndof_loc;
          row += (int64_t)gridDim.x * blockDim.x) {
@@ -514,11 +574,11 @@ __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_ta
                             const int64_t lc = loc_vel(G, fb * G.dim + c);
                             if (lc < 0) atomicOr(err, 1u);
                             col[p] = (int32_t)lc;
-                            val[p] = a_entry(G, T, eta_tab, a, b);
+                            val[p] = a_entry(G, Ae, a, b);
                             ++p;
                         } else {
                             double ud = dirichlet(G, b, c);
-                            if (ud != 0.0) lift -= a_entry(G, T, eta_tab, a, b) * ud;
+                            if (ud != 0.0) lift -= a_entry(G, Ae, a, b) * ud;
                         }
                     } else {
                         for (int cc = 0; cc < G.dim; ++cc) {
@@ -526,11 +586,11 @@ __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_ta
                                 const int64_t lc = loc_vel(G, fb * G.dim + cc);
                                 if (lc < 0) atomicOr(err, 1u);
                                 col[p] = (int32_t)lc;
-                                val[p] = b_entry(G, T, b, cc, a);
+                                val[p] = b_entry(G, E, b, cc, a);
                                 ++p;
                             } else {
                                 double ud = dirichlet(G, b, cc);
-                                if (ud != 0.0) lift -= b_entry(G, T, b, cc, a) * ud;
+                                if (ud != 0.0) lift -= b_entry(G, E, b, cc, a) * ud;
                             }
                         }
                     }
@@ -543,7 +603,7 @@ __global__ void op_fill_kernel(Grid G, const double* eta_tab, const double* f_ta
                         const int64_t lc = loc_vert(G, vert_id(G, v));
                         if (lc < 0) atomicOr(err, 1u);
                         col[p] = (int32_t)lc;
-                        val[p] = vel ? b_entry(G, T, a, c, v) : c_entry(G, T, eta_tab, a, v);
+                        val[p] = vel ? b_entry(G, E, a, c, v) : c_entry(G, T, eta_tab, a, v);
                         ++p;
                     }
         }
@@ -829,15 +889,23 @@ extern "C" rav_status rav_gen_operator(const rav_grid* g, int64_t* row_ptr, int3
     coef_kernel<<<grid_for(G.nel * NG, 256), 256, 0, s>>>(G, eta_tab, f_tab);
     count_launch();
     RAV_CHECK_LAUNCH();
+    const int P1 = G.P + 1, NL = G.dim == 2 ? P1 * P1 : P1 * P1 * P1;
+    const int64_t npair = (int64_t)NL * (NL + 1) / 2;
+    double* Ae = nullptr;
+    RAV_CUDA(cudaMallocAsync(&Ae, sizeof(double) * std::max<int64_t>(1, G.nel * npair), s));
+    elem_a_kernel<<<grid_for(G.nel * npair, 256), 256, 0, s>>>(G, eta_tab, Ae);
+    count_launch();
+    RAV_CHECK_LAUNCH();
     op_count_kernel<<<grid_for(G.ndof_loc, 256), 256, 0, s>>>(G, cnt);
     count_launch();
     RAV_CHECK_LAUNCH();
     RAV_TRY(counts_to_rowptr(cnt, row_ptr, G.ndof_loc, s));
-    op_fill_kernel<<<grid_for(G.ndof_loc, 128), 128, 0, s>>>(G, eta_tab, f_tab, row_ptr, col, val, rhs, err);
+    op_fill_kernel<<<grid_for(G.ndof_loc, 128), 128, 0, s>>>(G, eta_tab, Ae, f_tab, row_ptr, col, val, rhs, err);
     count_launch();
     RAV_CHECK_LAUNCH();
     unsigned int h_err = 0;
     RAV_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(h_err), cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(Ae, s);
     cudaFreeAsync(eta_tab, s);
     if (f_tab) cudaFreeAsync(f_tab, s);
     cudaFreeAsync(cnt, s);
