@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
     int32_t* ndof = (int32_t*)(wnode + a.nnmax);              // nnmax: dof of component 0
     int32_t* snode = ndof + a.nnmax;                          // sorted node ids (dof / D)
     int32_t* sperm = snode + a.nnmax;                         // local index of sorted entry
-    __shared__ int s_nn, s_mn, s_pd, s_fail, s_piv, s_sym;
+    __shared__ int s_nn, s_mn, s_pd, s_fail, s_piv, s_sym, s_np, s_pidx;
     __shared__ double s_wp, s_cpp;
 
     for (int64_t i = blockIdx.x; i < a.np; i += gridDim.x) {
@@ -104,49 +104,104 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
                 stw[t] = a.pw[off + t];
             }
         __syncthreads();
-        if (tid == 0) {
-            // node table + structure checks (sequential: n <= a few hundred)
-            int nn = 0, mn = 0, pd = -1, fail = 0, cnt = 0, cur = -1;
-            double wcur = 0.0, wp = 0.0;
-            bool in_rest = true;
-            for (int t = 0; t < n && !fail; ++t) {
-                const int dof = staged ? std_[t] : a.pdofs[off + t];
-                const double w = staged ? stw[t] : a.pw[off + t];
-                if (dof >= a.nvel) {
-                    if (pd >= 0) fail = 1;
-                    pd = dof;
-                    wp = w;
-                    continue;
+        // node table + structure checks, in parallel over the staged DoF list (a single thread
+        // scanning it held the other warps at the barrier).  The list must be: node groups of D
+        // consecutive entries (dof = node D + c, c = 0 .. D-1, one weight per group, no node twice
+        // in a row), restricted (w > 0) groups first, and exactly one pressure DoF anywhere.
+        if (staged) {
+            if (tid == 0) { s_np = 0; s_pidx = -1; s_fail = 0; s_cpp = 0.0; s_mn = 0; }
+            __syncthreads();
+            for (int t = tid; t < n; t += NT)
+                if (std_[t] >= a.nvel) {
+                    atomicAdd(&s_np, 1);
+                    s_pidx = t;
                 }
-                const int node = dof / D, c = dof % D;
-                if (node != cur) {
-                    if (cur >= 0 && cnt != D) fail = 1;
-                    if (c != 0 || nn >= a.nnmax) { fail = 1; break; }
-                    cur = node;
-                    cnt = 1;
-                    wcur = w;
-                    ndof[nn] = dof;
-                    wnode[nn] = w;
-                    if (w > 0.0) {
-                        if (!in_rest) fail = 1;   // restricted nodes must come first
-                        ++mn;
+            __syncthreads();
+            const int nvent = n - s_np;     // velocity entries
+            const int pidx = s_pidx;
+            if (tid == 0 && (s_np != 1 || nvent % D != 0 || nvent / D < 1 || nvent / D > a.nnmax)) s_fail = 1;
+            __syncthreads();
+            if (!s_fail) {
+                for (int t = tid; t < n; t += NT) {
+                    if (t == pidx) continue;
+                    const int v = t - (t > pidx ? 1 : 0);          // index among the velocity entries
+                    const int dof = std_[t];
+                    const double w = stw[t];
+                    const int c = dof % D;
+                    if (v % D == 0) {
+                        if (c != 0) atomicOr((unsigned int*)&s_fail, 1u);
+                        const int j = v / D;
+                        ndof[j] = dof;
+                        wnode[j] = w;
                     } else {
-                        in_rest = false;
+                        const int tp = (t - 1 == pidx) ? t - 2 : t - 1;   // previous velocity entry
+                        if (dof != std_[tp] + 1 || c == 0 || w != stw[tp]) atomicOr((unsigned int*)&s_fail, 1u);
                     }
-                    ++nn;
-                } else {
-                    if (c != cnt || w != wcur) fail = 1;
-                    ++cnt;
                 }
             }
-            if (cur >= 0 && cnt != D) fail = 1;
-            if (pd < 0 || nn < 1 || mn > a.mnmax) fail = 1;
-            s_nn = nn;
-            s_mn = mn;
-            s_pd = pd;
-            s_wp = wp;
-            s_cpp = 0.0;
-            s_fail = fail;
+            __syncthreads();
+            if (!s_fail) {
+                const int nn = nvent / D;
+                for (int j = tid; j < nn; j += NT) {
+                    if (wnode[j] > 0.0) {
+                        atomicAdd(&s_mn, 1);
+                        if (j > 0 && !(wnode[j - 1] > 0.0)) atomicOr((unsigned int*)&s_fail, 1u);   // restricted first
+                    }
+                    if (j > 0 && ndof[j] == ndof[j - 1]) atomicOr((unsigned int*)&s_fail, 1u);
+                }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                s_nn = nvent / D;
+                s_pd = pidx >= 0 ? std_[pidx] : -1;
+                s_wp = pidx >= 0 ? stw[pidx] : 0.0;
+                if (s_mn > a.mnmax) s_fail = 1;
+            }
+        } else {   // DoF list larger than the staging space: the sequential scan from global memory
+            if (tid == 0) {
+                // node table + structure checks (sequential: n <= a few hundred)
+                int nn = 0, mn = 0, pd = -1, fail = 0, cnt = 0, cur = -1;
+                double wcur = 0.0, wp = 0.0;
+                bool in_rest = true;
+                for (int t = 0; t < n && !fail; ++t) {
+                    const int dof = staged ? std_[t] : a.pdofs[off + t];
+                    const double w = staged ? stw[t] : a.pw[off + t];
+                    if (dof >= a.nvel) {
+                        if (pd >= 0) fail = 1;
+                        pd = dof;
+                        wp = w;
+                        continue;
+                    }
+                    const int node = dof / D, c = dof % D;
+                    if (node != cur) {
+                        if (cur >= 0 && cnt != D) fail = 1;
+                        if (c != 0 || nn >= a.nnmax) { fail = 1; break; }
+                        cur = node;
+                        cnt = 1;
+                        wcur = w;
+                        ndof[nn] = dof;
+                        wnode[nn] = w;
+                        if (w > 0.0) {
+                            if (!in_rest) fail = 1;   // restricted nodes must come first
+                            ++mn;
+                        } else {
+                            in_rest = false;
+                        }
+                        ++nn;
+                    } else {
+                        if (c != cnt || w != wcur) fail = 1;
+                        ++cnt;
+                    }
+                }
+                if (cur >= 0 && cnt != D) fail = 1;
+                if (pd < 0 || nn < 1 || mn > a.mnmax) fail = 1;
+                s_nn = nn;
+                s_mn = mn;
+                s_pd = pd;
+                s_wp = wp;
+                s_cpp = 0.0;
+                s_fail = fail;
+            }
         }
         __syncthreads();
         if (s_fail) {
