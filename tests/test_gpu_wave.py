@@ -19,11 +19,14 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(args, wave, tmp_path, tag):
+def _run(args, wave, tmp_path, tag, spatial=False):
     env = dict(os.environ)
     env.pop("RAV_WAVE", None)
+    env.pop("RAV_WAVE_SPATIAL", None)
     if wave:
         env["RAV_WAVE"] = "1"
+    if spatial:
+        env["RAV_WAVE_SPATIAL"] = "1"
     out = str(tmp_path / f"{tag}.npy")
     res = subprocess.run([sys.executable] + args + [out], cwd=ROOT, env=env, capture_output=True, text=True,
                          timeout=300)
@@ -31,9 +34,10 @@ def _run(args, wave, tmp_path, tag):
     return np.load(out), res.stdout
 
 
-def test_wave_sweeps_match_default_chain(tmp_path):
+@pytest.mark.parametrize("spatial", [False, True], ids=["slot_order", "spatial_order"])
+def test_wave_sweeps_match_default_chain(tmp_path, spatial):
     a, _ = _run(["scripts/wave_check.py", "512", "20"], False, tmp_path, "ref")
-    b, _ = _run(["scripts/wave_check.py", "512", "20"], True, tmp_path, "wave")
+    b, _ = _run(["scripts/wave_check.py", "512", "20"], True, tmp_path, "wave", spatial=spatial)
     assert np.linalg.norm(a - b) <= 1e-13 * np.linalg.norm(a)
 
 
