@@ -117,6 +117,7 @@ struct mg_ctx {
     // FGMRES work space (mg_fgmres): V (m+1) x n, Z m x n, w, r, device coefficients
     int kry_m = 0;
     double *kV = nullptr, *kZ = nullptr, *kw = nullptr, *kr = nullptr, *kh = nullptr, *kpart = nullptr;
+    double *kzero = nullptr, *kmd = nullptr;   // zero right-hand side (w = L z via the residual), multi-dot partials
 };
 
 namespace rav {
@@ -443,7 +444,7 @@ void mg_destroy(mg_ctx* m) {
     if (m->h_norm2) cudaFreeHost(m->h_norm2);
     if (m->hx) cudaFree(m->hx);
     if (m->hb) cudaFree(m->hb);
-    for (double* p : {m->kV, m->kZ, m->kw, m->kr, m->kh, m->kpart})
+    for (double* p : {m->kV, m->kZ, m->kw, m->kr, m->kh, m->kpart, m->kzero, m->kmd})
         if (p) cudaFree(p);
     delete m;
 }
@@ -755,7 +756,7 @@ namespace rav {
 
 static rav_status kry_alloc(mg_ctx* m, int restart, int64_t n) {
     if (m->kry_m == restart && m->kV) return RAV_OK;
-    for (double** p : {&m->kV, &m->kZ, &m->kw, &m->kr, &m->kh, &m->kpart})
+    for (double** p : {&m->kV, &m->kZ, &m->kw, &m->kr, &m->kh, &m->kpart, &m->kzero, &m->kmd})
         if (*p) { cudaFree(*p); *p = nullptr; }
     RAV_CUDA(cudaMalloc(&m->kV, sizeof(double) * (size_t)(restart + 1) * n));
     RAV_CUDA(cudaMalloc(&m->kZ, sizeof(double) * (size_t)restart * n));
@@ -763,6 +764,9 @@ static rav_status kry_alloc(mg_ctx* m, int restart, int64_t n) {
     RAV_CUDA(cudaMalloc(&m->kr, sizeof(double) * n));
     RAV_CUDA(cudaMalloc(&m->kh, sizeof(double) * (2 * (restart + 1) + 2)));
     RAV_CUDA(cudaMalloc(&m->kpart, sizeof(double) * residual_norm_blocks()));
+    RAV_CUDA(cudaMalloc(&m->kzero, sizeof(double) * n));
+    RAV_CUDA(cudaMemset(m->kzero, 0, sizeof(double) * n));
+    RAV_CUDA(cudaMalloc(&m->kmd, sizeof(double) * (size_t)multi_dot_blocks() * multi_dot_max()));
     m->kry_m = restart;
     return RAV_OK;
 }
@@ -818,11 +822,18 @@ extern "C" rav_status mg_fgmres(mg_ctx* m, double* x, const double* b, int pre, 
             RAV_CUDA(cudaMemsetAsync(zj, 0, sizeof(double) * n, s));
             if (m->L == 1) RAV_TRY(launch_coarse_solve(m->C, vj, zj, s));
             else RAV_TRY(vcycle_launches(m, m->L - 1, zj, vj, pre, post, omega));   // z_j = M^{-1} v_j
-            RAV_TRY(launch_spmv(F.A, zj, m->kw, 1.0, 0.0, s));                        // w = L z_j
+            // w = L z_j through the level's residual kernel (node-blocked, ~half the CSR bytes) with a zero
+            // right-hand side, r = -L z_j, then negated
+            RAV_TRY(launch_residual(F.A, zj, m->kzero, m->kw, s));
+            RAV_TRY(launch_scale(n, m->kw, -1.0, m->kw, s));
             for (int pass = 0; pass < 2; ++pass) {                                    // CGS2
                 double* hp = hd + pass * (M + 1);
-                for (int i = 0; i <= j; ++i)
-                    RAV_TRY(launch_dot(V + (size_t)i * n, m->kw, n, m->kpart, residual_norm_blocks(), hp + i, 0, s));
+                if (j + 1 <= multi_dot_max()) {   // all projections in one pass over w
+                    RAV_TRY(launch_multi_dot(n, j + 1, V, n, m->kw, m->kmd, hp, s));
+                } else {
+                    for (int i = 0; i <= j; ++i)
+                        RAV_TRY(launch_dot(V + (size_t)i * n, m->kw, n, m->kpart, residual_norm_blocks(), hp + i, 0, s));
+                }
                 RAV_TRY(launch_multi_axpy(n, j + 1, V, n, hp, -1.0, m->kw, s));
             }
             RAV_TRY(launch_dot(m->kw, m->kw, n, m->kpart, residual_norm_blocks(), hd + 2 * M + 2, 0, s));

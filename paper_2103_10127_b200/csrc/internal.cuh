@@ -86,6 +86,11 @@ rav_status launch_residual_and_norm2(const Csr& A, const double* x, const double
 rav_status launch_dot(const double* a, const double* b, int64_t n, double* part, int nblk, double* out,
                       int accumulate, cudaStream_t s);
 // w += alpha * sum_i coef[i] V[i * ld + .] (coef: device, nv entries); dst = s * src
+// out[i] = V_i . w for i < nv <= multi_dot_max() (part: multi_dot_blocks() * multi_dot_max() doubles)
+int multi_dot_max();
+int multi_dot_blocks();
+rav_status launch_multi_dot(int64_t n, int nv, const double* V, int64_t ld, const double* w, double* part, double* out,
+                            cudaStream_t s);
 rav_status launch_multi_axpy(int64_t n, int nv, const double* V, int64_t ld, const double* coef, double alpha,
                              double* w, cudaStream_t s);
 rav_status launch_scale(int64_t n, const double* src, double sc, double* dst, cudaStream_t s);

@@ -263,6 +263,61 @@ __global__ void __launch_bounds__(256) multi_axpy_kernel(int64_t n, int nv, cons
     }
 }
 
+// out[i] = sum_k V[i ld + k] w[k] for i < nv <= MD_NV in one pass over w and the nv vectors
+// (Gram-Schmidt of FGMRES); per-block partials part[b MD_NV + i], summed in fixed block order
+constexpr int MD_NV = 32;
+__global__ void __launch_bounds__(256, 2) multi_dot_kernel(int64_t n, int nv, const double* __restrict__ V, int64_t ld,
+                                                        const double* __restrict__ w, double* __restrict__ part) {
+    double acc[MD_NV];
+#pragma unroll
+    for (int i = 0; i < MD_NV; ++i) acc[i] = 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const double wk = w[k];
+#pragma unroll
+        for (int i = 0; i < MD_NV; ++i)
+            if (i < nv) acc[i] = fma(V[i * ld + k], wk, acc[i]);
+    }
+    __shared__ double red[8][MD_NV];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < MD_NV; ++i) {
+        if (i < nv) {
+            const double v = warp_sum(acc[i]);
+            if (lane == 0) red[warp][i] = v;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < nv) {
+        double t = 0.0;
+        for (int q = 0; q < 8; ++q) t += red[q][threadIdx.x];
+        part[(int64_t)blockIdx.x * MD_NV + threadIdx.x] = t;
+    }
+}
+
+__global__ void multi_dot_sum_kernel(int nblk, int nv, const double* __restrict__ part, double* __restrict__ out) {
+    if (threadIdx.x < nv) {
+        double t = 0.0;
+        for (int b = 0; b < nblk; ++b) t += part[(int64_t)b * MD_NV + threadIdx.x];
+        out[threadIdx.x] = t;
+    }
+}
+
+int multi_dot_max() { return MD_NV; }
+int multi_dot_blocks() { return num_sms() * 4; }
+
+rav_status launch_multi_dot(int64_t n, int nv, const double* V, int64_t ld, const double* w, double* part, double* out,
+                            cudaStream_t s) {
+    if (nv <= 0) return RAV_OK;
+    if (nv > MD_NV) { set_error("multi_dot: at most %d vectors", MD_NV); return RAV_ERR_ARG; }
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(std::max<int64_t>(n, 1), 256), multi_dot_blocks()));
+    multi_dot_kernel<<<blocks, 256, 0, s>>>(n, nv, V, ld, w, part);
+    count_launch();
+    multi_dot_sum_kernel<<<1, 32, 0, s>>>(blocks, nv, part, out);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}
+
 __global__ void scale_kernel(int64_t n, const double* __restrict__ src, double s, double* __restrict__ dst) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
         dst[k] = s * src[k];
