@@ -124,20 +124,31 @@ namespace rav {
 
 // r_ready: c->r already holds b - L x for the incoming x (the stopping test of mg_solve
 // computed it), so the first sweep skips its residual pass
+// x_zero: x is zero on entry (coarse-level corrections, FGMRES preconditioner applications), so the
+// first sweep's residual is b itself and is read from b instead of being computed
 static rav_status smooth_launches(rav_ctx* c, double* x, const double* b, int nu, double omega,
-                                  bool r_ready = false) {
+                                  bool r_ready = false, bool x_zero = false) {
     static const bool wave_use = [] {   // RAV_WAVE_USE=0: keep the wave layout, run the plain chain
         const char* e = getenv("RAV_WAVE_USE");
         return !(e && atoi(e) == 0);
     }();
     const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
-    if (wave_use && aligned && c->wave.on && c->variant != RAV_VARIANT_MV && nu > 0)
+    if (wave_use && aligned && c->wave.on && c->variant != RAV_VARIANT_MV && nu > 0) {
+        if (x_zero && !r_ready) {
+            RAV_CUDA(cudaMemcpyAsync(c->r, b, sizeof(double) * c->A.n_rows, cudaMemcpyDeviceToDevice, c->stream));
+            r_ready = true;
+        }
         return wave_smooth(c->A, c->F, c->P.n_patches, c->wave, x, b, c->r, nu, omega, r_ready, c->stream);
+    }
     for (int k = 0; k < nu; ++k) {
         if (c->variant == RAV_VARIANT_MV) {   // colour by colour, fresh local residuals (Eq. 11, 15)
             for (size_t q = 0; q + 1 < c->coffs.size(); ++q)
                 RAV_TRY(launch_mv_color(c->A, c->F, c->coffs[q + 1] - c->coffs[q], c->plist + c->coffs[q], b, x,
                                         omega, c->stream));
+            continue;
+        }
+        if (k == 0 && x_zero && !r_ready) {   // r = b - L 0 = b
+            RAV_TRY(launch_sweep(c->P, c->F, b, x, omega, c->stream));
             continue;
         }
         if (!(r_ready && k == 0)) RAV_TRY(launch_residual(c->A, x, b, c->r, c->stream));
@@ -549,19 +560,20 @@ rav_status mg_set_stream(mg_ctx* m, void* stream) {
 namespace rav {
 
 // V-cycle on level l (Fig. 1): x and b are the level's iterate / rhs
+// x_zero: x is zero on entry (every level below the finest; FGMRES's z_j), see smooth_launches
 static rav_status vcycle_launches(mg_ctx* m, int l, double* x, const double* b, int pre, int post, double omega,
-                                  bool r_ready = false) {
+                                  bool r_ready = false, bool x_zero = false) {
     cudaStream_t s = m->stream;
     if (l == 0) return launch_coarse_solve(m->C, b, x, s);
     mg_level& L = m->lv[l];
     mg_level& Lc = m->lv[l - 1];
-    RAV_TRY(smooth_launches(L.sm, x, b, pre, omega, r_ready));
+    RAV_TRY(smooth_launches(L.sm, x, b, pre, omega, r_ready, x_zero));
     if (pre == 0 && r_ready) RAV_CUDA(cudaMemcpyAsync(L.r, L.sm->r, sizeof(double) * L.A.n_rows, cudaMemcpyDeviceToDevice, s));
     else RAV_TRY(launch_residual(L.A, x, b, L.r, s));
     if (L.xs.on && L.xs.dim == 2) RAV_TRY(launch_xs_restrict(L.xs, L.r, Lc.b, s));   // b_{l-1} = P^T r_l
     else RAV_TRY(launch_spmv(L.PT, L.r, Lc.b, 1.0, 0.0, s));
     if (l - 1 > 0) RAV_CUDA(cudaMemsetAsync(Lc.x, 0, sizeof(double) * Lc.A.n_rows, s));
-    RAV_TRY(vcycle_launches(m, l - 1, Lc.x, Lc.b, pre, post, omega));
+    RAV_TRY(vcycle_launches(m, l - 1, Lc.x, Lc.b, pre, post, omega, false, l - 1 > 0));
     if (L.xs.on) RAV_TRY(launch_xs_prolong(L.xs, Lc.x, x, 1.0, 1.0, s));   // x_l += P x_{l-1}
     else RAV_TRY(launch_spmv(L.P, Lc.x, x, 1.0, 1.0, s));
     RAV_TRY(smooth_launches(L.sm, x, b, post, omega));
@@ -821,7 +833,7 @@ extern "C" rav_status mg_fgmres(mg_ctx* m, double* x, const double* b, int pre, 
             double* zj = Z + (size_t)j * n;
             RAV_CUDA(cudaMemsetAsync(zj, 0, sizeof(double) * n, s));
             if (m->L == 1) RAV_TRY(launch_coarse_solve(m->C, vj, zj, s));
-            else RAV_TRY(vcycle_launches(m, m->L - 1, zj, vj, pre, post, omega));   // z_j = M^{-1} v_j
+            else RAV_TRY(vcycle_launches(m, m->L - 1, zj, vj, pre, post, omega, false, true));   // z_j = M^{-1} v_j
             // w = L z_j through the level's residual kernel (node-blocked, ~half the CSR bytes) with a zero
             // right-hand side, r = -L z_j, then negated
             RAV_TRY(launch_residual(F.A, zj, m->kzero, m->kw, s));
