@@ -10,8 +10,14 @@ N(0,1) guess.  value = free DoFs x sweeps / second (MDoF/s), device-timed.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
 --impl reference times the CPU oracle (oracle/, plain C) on the same workload
-(bounded: one sweep per step).  Under torchrun (N > 1) every rank runs its own
-c2 replica (weak scaling, no data-path collective yet).
+(bounded: one sweep per step).  Under torchrun (N > 1) the c2 workload is
+stacked along y, one 512^2 block per GPU, and slab-partitioned: every sweep runs
+the interface-correction sum and the halo refresh between neighbouring ranks
+(weak scaling).
+
+The JSON line ends with the V-cycle metric ("vcycle": c3 / c4 time to 1e-8);
+the paper-setting studies (Q1-Q1, adaptive hierarchy, V-cycle smoother
+comparison) run only with --studies FILE and go to FILE.
 """
 from __future__ import annotations
 
@@ -98,26 +104,88 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_oracle_rate(prob, steps, warmup, sweeps_per_step=1):
+def cpu_oracle_rate(prob, steps, warmup, sweeps_per_step=1, threads=None):
     """The oracle (as it stands) timed on this host: setup untimed, then
-    `sweeps_per_step` RAV sweeps per step.  Returns (MDoF/s, cores, sample)."""
-    import numpy as np
+    `sweeps_per_step` RAV sweeps per step on `threads` OpenMP threads (None: all;
+    the oracle's parallel loops give the same bits at any count).
+    Returns (MDoF/s, threads used, sample, seconds)."""
     import oracle
     import seeded_inputs as si
     O = oracle.assemble(prob)
     P = oracle.patches(prob, "pou")
     F = oracle.factor(O, P, oracle.FMT_ROWS)
     x = si.initial_guess(O["n"], seed=si.X0_SEED)
-    for _ in range(warmup):
-        x = oracle.additive_sweeps(O, P, F, x, O["b"], OMEGA, sweeps_per_step)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        x = oracle.additive_sweeps(O, P, F, x, O["b"], OMEGA, sweeps_per_step)
-    dt = time.perf_counter() - t0
+    prev = oracle.set_num_threads(threads or (os.cpu_count() or 1))
+    used = oracle.lib().or_num_threads()
+    try:
+        for _ in range(warmup):
+            x = oracle.additive_sweeps(O, P, F, x, O["b"], OMEGA, sweeps_per_step)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            x = oracle.additive_sweeps(O, P, F, x, O["b"], OMEGA, sweeps_per_step)
+        dt = time.perf_counter() - t0
+    finally:
+        oracle.set_num_threads(prev)
     rate = O["n"] * sweeps_per_step * steps / dt / 1e6
     sample = (f"c2 (512^2, {O['n']} DoFs) oracle RAV sweeps, {steps} x {sweeps_per_step} sweep(s) "
-              f"after untimed setup; {dt:.2f} s; single-threaded sweep on {host_cpu()}")
-    return rate, 1, sample, dt
+              f"after untimed setup; {dt:.2f} s on {used} thread(s) of {host_cpu()}")
+    return rate, used, sample, dt
+
+
+def oracle_sweep_samples(si, threads):
+    """Per-sweep oracle times for c3 / c4 / c5 from bounded samples at the configs' mesh
+    spacing (SURVEY row d): a strip 2048 x 128 cells of the 2048^2
+    grid (1/16 of c3 / c5) and a slab 32 x 32 x 4 cells of c4 (5 of its 33 vertex layers);
+    per-sweep time scaled to the full config by the patch count.  RAV (Eq. 13), and
+    for c5 also diagonal Vanka (R17) and multiplicative Vanka (Eq. 11, sequential)."""
+    import oracle
+    out = {}
+    prev = oracle.set_num_threads(threads)
+    used = oracle.lib().or_num_threads()
+    try:
+        strip = si.problem(2, (2048, 128), si.KIND_MMS, eta="fourier", box=(1.0, 1.0 / 16))
+        full_patches = 2049 * 2049
+        O = oracle.assemble(strip)
+        for name, w, fmt, om in (("rav", "pou", oracle.FMT_ROWS, OMEGA), ("diag_vanka", "full", oracle.FMT_DIAG, 0.1),
+                                 ("mv", "full", oracle.FMT_LU, OMEGA)):
+            P = oracle.patches(strip, w)
+            F = oracle.factor(O, P, fmt)
+            x = si.initial_guess(O["n"], seed=si.X0_SEED)
+            t0 = time.perf_counter()
+            if name == "mv":
+                oracle.mv_sweeps(O, P, F, x, O["b"], om, 1)
+            else:
+                oracle.additive_sweeps(O, P, F, x, O["b"], om, 1)
+            dt = time.perf_counter() - t0
+            out[f"c3_c5_{name}_s_per_sweep"] = dt * full_patches / (len(P["offs"]) - 1)
+            del P, F
+        out["c3_c5_sample"] = "2048 x 128 cells (h = 1/2048), 1 sweep, scaled x 2049^2 / 2049*129 patches"
+        slab = si.problem(3, (32, 32, 4), si.KIND_CAVITY, eta="fourier", box=(1.0, 1.0, 0.125))
+        O = oracle.assemble(slab)
+        P = oracle.patches(slab, "pou")
+        F = oracle.factor(O, P, oracle.FMT_ROWS)
+        x = si.initial_guess(O["n"], seed=si.X0_SEED)
+        t0 = time.perf_counter()
+        oracle.additive_sweeps(O, P, F, x, O["b"], OMEGA, 1)
+        dt = time.perf_counter() - t0
+        out["c4_rav_s_per_sweep"] = dt * 33 ** 3 / (len(P["offs"]) - 1)
+        out["c4_sample"] = "32 x 32 x 4 cells (h = 1/32), 1 sweep, scaled x 33^3 / 33*33*5 patches"
+    finally:
+        oracle.set_num_threads(prev)
+    out["threads"] = used
+    return out
+
+
+def host_info() -> dict:
+    """nproc, CPU model and memory of this host (context for the oracle timings)."""
+    mem = None
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                mem = round(int(line.split()[1]) / 2 ** 20, 1)
+    except OSError:
+        pass
+    return {"cpu": host_cpu(), "nproc": os.cpu_count(), "mem_gib": mem}
 
 
 def host_cpu() -> str:
@@ -220,6 +288,23 @@ def run_vcycle(name, rg, si, stream, dist):
     del mg, fine, x, b
     torch.cuda.empty_cache()
     return out
+
+
+def run_c1(rg, si):
+    """BASELINE config 1 (correctness config, launch-bound): 8x8 cavity, 3 levels, V(2,2)-RAV to
+    1e-10, then the pressure normalised so p(vertex 0) = 0 (row a10, R4)."""
+    import torch
+    c = si.CONFIGS["c1"]
+    prob = si.problem(2, c["ncell"], c["kind"], eta=c["eta"])
+    mg, fine = rg.build_hierarchy(prob, c["levels"], "pou")
+    x = torch.zeros(fine["n"], dtype=torch.float64, device="cuda")
+    x, k, h = mg.solve(x, fine["b"], pre=c["pre"], post=c["post"], omega=c["omega"], rtol=c["rtol"])
+    mg.normalize_pressure(x, mode=0)
+    p0 = float(x[fine["nvel"]].item())
+    mg.close()
+    return {"config": "c1: 8x8 Q2-Q1 cavity, eta = 1, 3 levels, V(2,2)-RAV omega 0.66, rtol 1e-10",
+            "free_dofs": fine["n"], "cycles": k, "converged": bool(h[-1] <= c["rtol"] * h[0]),
+            "pressure_normalized": "p(vertex 0) = 0 (mg_normalize_pressure)", "p_vertex0": p0}
 
 
 def run_c5_smoothers(rg, si, stream):
@@ -361,7 +446,7 @@ def run_q1q1_studies(rg, si, stream):
     import torch
     smoothers = (("rav", "pou", rg.VARIANT_ROWS, 0.66), ("mv_color", "full", rg.VARIANT_MV, 0.66),
                  ("av", "full", rg.VARIANT_ROWS, 0.1))
-    out = {"config": "Q1-Q1 stabilized (beta = 0.1/eta, R18) lid-driven cavity, eta = 1, uniform grids, "
+    out = {"config": "Q1-Q1 stabilized (beta = 0.01/eta, R18) lid-driven cavity, eta = 1, uniform grids, "
                      "8x8 coarsest, x0 = 0, rtol 1e-8"}
     study = {}
     for n in (64, 128, 256, 512, 1024):
@@ -883,25 +968,35 @@ def run_gpu(args):
         e2e_s = float(t.item())
     e2e_value = ws * n * SWEEPS_PER_STEP * args.steps / e2e_s / 1e6
 
-    # ---- V-cycle time to 1e-8 on c3 (2048^2, 10 levels), BASELINE metric part 2 ------
-    vcyc = None
-    if not args.no_vcycle:
-        del sm, G
-        torch.cuda.empty_cache()
-        vcyc = {name: run_vcycle(name, rg, si, stream, dist) for name in ("c3", "c4")}
+    # ---- V-cycle time to 1e-8 on c3 (2048^2, 10 levels) and c4, BASELINE metric part 2 ----
+    del sm, G
+    torch.cuda.empty_cache()
     extra = {}
     if not args.no_smoothers and ws == 1:
         extra["c5_smoothers"] = run_c5_smoothers(rg, si, stream)
-        extra["vcycle_smoothers"] = run_vcycle_smoothers(rg, si, stream)
-    if not args.no_paper and ws == 1:
-        extra["q1q1_paper_setting"] = run_q1q1_studies(rg, si, stream)
-        extra["adaptive_cavity_table1"] = run_adaptive_study(rg, si, stream)
+    vcyc = None
+    if not args.no_vcycle:
+        vcyc = {"c1": run_c1(rg, si)}
+        vcyc.update({name: run_vcycle(name, rg, si, stream, dist) for name in ("c3", "c4")})
+    if args.studies and ws == 1:   # the paper-setting studies (rows f1, f2, f4), to their own file
+        studies = {"vcycle_smoothers": run_vcycle_smoothers(rg, si, stream),
+                   "q1q1_paper_setting": run_q1q1_studies(rg, si, stream),
+                   "adaptive_cavity_table1": run_adaptive_study(rg, si, stream)}
+        with open(args.studies, "w") as f:
+            json.dump(studies, f)
 
     # ---- CPU oracle baseline (rank 0, N = 1 only; bounded sample) ------------------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rate, cores, sample, _ = cpu_oracle_rate(prob, steps=3, warmup=0)
-        cpu = {"value": rate, "unit": "MDoF/s", "cores": cores, "kind": "oracle", "sample": sample}
+        rate, cores, sample, _ = cpu_oracle_rate(prob, steps=3, warmup=1)
+        rate1, _, sample1, _ = cpu_oracle_rate(prob, steps=2, warmup=0, threads=1)
+        cpu = {"value": rate, "unit": "MDoF/s", "cores": cores, "kind": "oracle", "sample": sample,
+               "single_thread": {"value": rate1, "unit": "MDoF/s", "cores": 1, "sample": sample1},
+               "host": host_info()}
+        try:
+            cpu["per_sweep"] = oracle_sweep_samples(si, os.cpu_count() or 1)
+        except Exception as err:  # report, keep the line
+            cpu["per_sweep"] = {"error": f"{type(err).__name__}: {err}"[:200]}
 
     clocks = clk.summary()
     line = {
@@ -913,8 +1008,9 @@ def run_gpu(args):
                                "step = 100 RAV sweeps (residual SpMV + RAV sweep) from seeded N(0,1)",
                    "free_dofs": n, "nnz": nnz_c2, "patches": npatch_c2,
                    "sweeps_per_step": SWEEPS_PER_STEP, "omega": OMEGA, "weights": "partition of unity (R3)",
-                   "l2": "inputs larger than L2 (factor rows 2.0 GB + CSR 0.73 GB streamed per sweep; "
-                         "x, r, b vectors 19 MB each stay L2-resident by design)",
+                   "l2": "inputs larger than L2 (per sweep the factored Schur rows, 0.58 GB, and the node-blocked "
+                         "operator, 0.42 GB, stream from HBM; x, r, b vectors, 19 MB each, stay L2-resident "
+                         "by design)",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
@@ -936,9 +1032,9 @@ def run_gpu(args):
         line["cpu_baseline"] = cpu
     if det is not None:
         line["deterministic_mode"] = det
-    if vcyc is not None:
-        line["vcycle"] = vcyc
     line.update(extra)
+    if vcyc is not None:
+        line["vcycle"] = vcyc          # last: the record keeps the tail of the line
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -955,7 +1051,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-vcycle", action="store_true", help="skip the c3 V-cycle time-to-1e-8 measurement")
     ap.add_argument("--no-smoothers", action="store_true", help="skip the c5 / V-cycle smoother comparisons")
-    ap.add_argument("--no-paper", action="store_true", help="skip the Q1-Q1 paper-setting studies")
+    ap.add_argument("--studies", default="", help="also run the paper-setting studies (V-cycle smoother "
+                    "comparison, Q1-Q1, adaptive hierarchy) and write them to this JSON file")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -135,6 +135,15 @@ rav_status rav_gen_prolongation_nnz(const rav_grid* fine, const rav_grid* coarse
 rav_status rav_gen_prolongation(const rav_grid* fine, const rav_grid* coarse, int64_t* rp,
                                 int32_t* ci, double* val, void* stream);
 
+/* Multicolouring of the generated patches for RAV_VARIANT_MV (Eq. 11; reading
+ * R10): the patch of vertex (i, j[, k]) gets colour (i mod 4) + 4 (j mod 4)
+ * [+ 16 (k mod 4)] from its GLOBAL vertex coordinates (a slab window colours its
+ * patches as the whole grid does); patches ascending inside each colour.  Same-colour
+ * patches are >= 4 vertices apart, so they share no DoF and are not coupled through L.
+ * Host outputs in the rav_set_colors layout: color_offs[4^dim + 1] and
+ * patch_ids[n_patches] (local patch ids of the window).  Integer host work, no stream. */
+rav_status rav_gen_colors(const rav_grid* g, int64_t* color_offs, int32_t* patch_ids);
+
 /* ------------------------------------------------------------------------- */
 /* Adaptive quadtree hierarchies with hanging nodes */
 /* ------------------------------------------------------------------------- */
@@ -213,7 +222,9 @@ enum {
 };
 
 enum {
-    RAV_KERNEL_AUTO = 0,        /* RAV_KERNEL_SYM when the patch shape allows, else WARP */
+    RAV_KERNEL_AUTO = 0,        /* RAV_KERNEL_SCHUR when block_dim > 0 and every patch has the Schur
+                                   structure; otherwise RAV_KERNEL_SYM when the patch shape allows,
+                                   else WARP */
     RAV_KERNEL_WARP = 1,        /* general warp-per-patch kernel (any n_i, nres_i), rows row-major */
     RAV_KERNEL_THREAD = 2,      /* thread-per-patch kernel, full weighted rows (nres <= 32, n <= 64) */
     RAV_KERNEL_SYM = 3,         /* thread-per-patch kernel storing the symmetric restricted block of
@@ -244,9 +255,13 @@ typedef struct {
 typedef struct rav_ctx rav_ctx;
 
 /* Build the smoother for L x = b: for every patch gather
- * L_i = R_i L R_i^T from the CSR, factor it (Gaussian elimination with partial
- * pivoting on L_i^T, pivot tolerance 1e-14 * ||row||_inf) and store the
- * restricted rows W_i = diag(w_i) L_i^{-1}[restricted, :].
+ * L_i = R_i L R_i^T from the CSR and store what the sweep needs of L_i^{-1}
+ * (P:225-227).  Default for Vanka-shaped patches (block_dim > 0, see
+ * RAV_KERNEL_SCHUR): the exact block form -- A_s is eliminated per patch and the
+ * restricted rows of A_s^{-1}, g = A_s^{-1} b and 1/S are stored.  Other
+ * patches: Gaussian elimination with partial pivoting on L_i^T (pivot tolerance
+ * 1e-14 * ||row||_inf) and the restricted rows
+ * W_i = diag(w_i) L_i^{-1}[restricted, :].
  * On RAV_ERR_SINGULAR_LOCAL, *bad_patch (if non-NULL) holds the smallest
  * failing patch id.  Empty patches are RAV_ERR_ARG. */
 rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opts,
@@ -349,10 +364,13 @@ rav_status mg_solve(mg_ctx* ctx, double* x, const double* b, int pre, int post, 
  * V-cycle from a zero guess ("the geometric multigrid method can
  * also be used as a preconditioner in a Krylov subspace solver"; reading R19).
  * Arnoldi with classical Gram-Schmidt and one reorthogonalisation pass, Givens
- * rotations on the host.  Stops when the least-squares residual estimate
- * <= rtol ||b - L x_0||_2 or after maxit Arnoldi steps (= preconditioner
- * applications); *iters = steps taken, hist (host, maxit + 1, may be NULL) =
- * ||r_0|| and the estimate after every step.  x (in/out), b: DEVICE pointers.
+ * rotations on the host.  A restart cycle ends when the least-squares residual
+ * estimate <= rtol ||b - L x_0||_2, after `restart` steps, or after maxit
+ * Arnoldi steps (= preconditioner applications); x is then updated and the TRUE
+ * residual ||b - L x||_2 is computed: the solve stops only when it meets rtol
+ * (else it restarts).  *iters = steps taken; hist (host, maxit + 1, may be NULL)
+ * = ||r_0||, the estimate after every step, with the entry of each cycle's last
+ * step replaced by the true residual (so hist[*iters] is always ||b - L x||).  x (in/out), b: DEVICE pointers.
  * Work space (restart + 1 + restart vectors of n_fine doubles) is allocated on
  * the first call and kept in the context.  RAV_ERR_DIVERGED on NaN/Inf. */
 rav_status mg_fgmres(mg_ctx* ctx, double* x, const double* b, int pre, int post, double omega, int restart,
@@ -431,7 +449,24 @@ rav_status mg_set_structured_transfers(mg_ctx* ctx, const rav_grid* grids);
 /* Number of GPU kernel launches issued by the most recent rav_smooth,
  * mg_vcycle or mg_solve call on this context (graph nodes included). */
 int64_t rav_last_launches(const rav_ctx* ctx);
+
+/* Pressure normalisation (reading R4).  The
+ * pressure of the enclosed-flow Stokes system is defined only up to a constant: the
+ * operators keep every pressure DoF and the constant is fixed only inside the
+ * coarsest solve (mg_setup coarse_pin), so the fine-level pressure of an iterate
+ * carries whatever constant the cycles leave.  This call fixes it after a solve:
+ * mode 0: p <- p - p[pin] (config c1's "pressure pinned at one corner vertex": with the
+ *         generator's numbering (R9) pin = n_vel is vertex 0, the corner (0, 0[, 0]));
+ * mode 1: p <- p - mean(p) (arithmetic mean of the n - n_vel pressure DoFs, summed in
+ *         a fixed order: bitwise reproducible).
+ * x: device pointer of length n, DoFs [n_vel, n) are pressure.  Stream-ordered.
+ * RAV_ERR_ARG for n_vel > n, mode not 0/1, pin outside [n_vel, n) in mode 0. */
+rav_status rav_pressure_normalize(double* x, int64_t n_vel, int64_t n, int mode, int64_t pin, void* stream);
 int64_t mg_last_launches(const mg_ctx* ctx);
+/* rav_pressure_normalize on the finest level of the hierarchy (its n_vel from
+ * mg_setup; mode 0 pins the first pressure DoF, i.e. vertex 0 in the generator's
+ * numbering).  x: device pointer, stream-ordered on the context stream. */
+rav_status mg_normalize_pressure(mg_ctx* ctx, double* x, int mode);
 rav_status mg_set_stream(mg_ctx* ctx, void* stream);
 void mg_destroy(mg_ctx* ctx);
 

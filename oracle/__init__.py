@@ -128,11 +128,12 @@ def lib():
                                  C.c_int, C.c_int, dbl]),
             "or_mg_solve": (C.c_int, [C.POINTER(Level), C.POINTER(Coarse), C.c_int, C.c_int, vp, vp,
                                       C.c_int, C.c_int, dbl, dbl, C.c_int, vp]),
-            "or_rav_sweep_sampled": (i64, [i64, vp, vp, vp, i64, vp, vp, vp, vp, vp, dbl, vp, vp]),
+            "or_rav_sweep_sampled": (i64, [i64, vp, vp, vp, i64, vp, vp, vp, vp, vp, dbl, vp, vp, vp]),
             "or_mms_errors": (None, [pd, vp, C.POINTER(dbl), C.POINTER(dbl)]),
             "or_eta": (dbl, [pd, dbl, dbl, dbl]),
             "or_element_matrices": (C.c_int, [pd, vp, vp, vp, vp, vp, vp]),
             "or_num_threads": (C.c_int, []),
+            "or_set_num_threads": (None, [C.c_int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -140,6 +141,15 @@ def lib():
             f.argtypes = args
         _lib = L
     return _lib
+
+
+def set_num_threads(t: int) -> int:
+    """OpenMP threads of the oracle (row-independent loops only; results do not depend
+    on it).  Returns the previous value."""
+    L = lib()
+    prev = L.or_num_threads()
+    L.or_set_num_threads(int(t))
+    return prev
 
 
 def _p(a: Optional[np.ndarray]):
@@ -418,17 +428,20 @@ class Hierarchy:
 
 
 def rav_sweep_sampled(A: Dict, P: Dict, x: np.ndarray, b: np.ndarray, omega: float,
-                      sample: np.ndarray) -> np.ndarray:
-    """One RAV sweep evaluated only at the sampled DoFs (full-size parity)."""
+                      sample: np.ndarray, with_magnitude: bool = False):
+    """One RAV sweep evaluated only at the sampled DoFs (full-size parity).  With
+    with_magnitude also the per-entry rounding scale |x_j| + omega sum |w L_i^{-T} e_k|
+    (|b| + |L||x| + |r|) of the sampled entries (for element-wise bounds)."""
     mask = np.zeros(A["n"], np.uint8)
     mask[sample] = 1
     xnew = np.full(A["n"], np.nan)
+    mag = np.full(A["n"], np.nan) if with_magnitude else None
     bad = lib().or_rav_sweep_sampled(A["n"], _p(A["rp"]), _p(A["ci"]), _p(A["val"]), len(P["offs"]) - 1,
                                      _p(P["offs"]), _p(P["dofs"]), _p(P["w"]), _p(x), _p(b), float(omega),
-                                     _p(mask), _p(xnew))
+                                     _p(mask), _p(xnew), _p(mag))
     if bad >= 0:
         raise SingularLocalSystem(int(bad))
-    return xnew[sample]
+    return (xnew[sample], mag[sample]) if with_magnitude else xnew[sample]
 
 
 def mms_errors(problem: Dict, x: np.ndarray):

@@ -465,9 +465,12 @@ int or_assemble(const or_desc* D, int64_t* rp, int32_t* ci, double* val, double*
     return 0;
 }
 
-/* y = b - L x  (Eq. 10, the residual) */
+/* y = b - L x  (Eq. 10, the residual).  Rows are independent; each row is
+ * summed in column order by one thread, so the result does not depend on the
+ * thread count. */
 void or_residual(int64_t n, const int64_t* rp, const int32_t* ci, const double* val,
                  const double* x, const double* b, double* r) {
+#pragma omp parallel for schedule(static, 4096)
     for (int64_t i = 0; i < n; ++i) {
         double s = 0.0;
         for (int64_t k = rp[i]; k < rp[i + 1]; ++k) s += val[k] * x[ci[k]];
@@ -478,6 +481,7 @@ void or_residual(int64_t n, const int64_t* rp, const int32_t* ci, const double* 
 /* y = M x for a general CSR (transfers) */
 void or_spmv(int64_t nrows, const int64_t* rp, const int32_t* ci, const double* val,
              const double* x, double* y) {
+#pragma omp parallel for schedule(static, 4096)
     for (int64_t i = 0; i < nrows; ++i) {
         double s = 0.0;
         for (int64_t k = rp[i]; k < rp[i + 1]; ++k) s += val[k] * x[ci[k]];
@@ -707,53 +711,78 @@ int64_t or_factor(int64_t n, int64_t nvel, const int64_t* rp, const int32_t* ci,
 
 /* Additive sweep with precomputed weighted rows (RAV P:124 Eq. 13 with PoU or
  * ownership weights; AV P:118 Eq. 12 with unit weights):
- *   r = b - L x ;  Delta = sum_i R_i^T (W_i R_i r)  (ascending i) ;  x += omega Delta */
+ *   r = b - L x ;  Delta = sum_i R_i^T (W_i R_i r)  (ascending i) ;  x += omega Delta
+ * The patch products c_ik = (W_i R_i r)_k are independent (computed in parallel
+ * over patches into their own slots, foffs-aligned per restricted row); the sum
+ * into Delta runs serially in ascending patch order, so every thread count gives
+ * the same bits. */
 void or_additive_sweeps(int64_t n, const int64_t* rp, const int32_t* ci, const double* val,
                         int64_t npatch, const int64_t* poffs, const int32_t* pdofs, const double* pw,
                         const int64_t* foffs, const double* fac,
                         double* x, const double* b, double omega, int nu) {
     double* r = malloc(sizeof(double) * n);
     double* delta = malloc(sizeof(double) * n);
+    /* slot of restricted row k of patch i: coffs[i] + (its rank among the restricted entries) */
+    int64_t* coffs = malloc(sizeof(int64_t) * (npatch + 1));
+    coffs[0] = 0;
+    for (int64_t i = 0; i < npatch; ++i) {
+        int64_t m = 0;
+        for (int64_t k = poffs[i]; k < poffs[i + 1]; ++k) m += pw[k] > 0.0;
+        coffs[i + 1] = coffs[i] + m;
+    }
+    double* c = malloc(sizeof(double) * (coffs[npatch] > 0 ? coffs[npatch] : 1));
     for (int s = 0; s < nu; ++s) {
         or_residual(n, rp, ci, val, x, b, r);
-        memset(delta, 0, sizeof(double) * n);
+#pragma omp parallel for schedule(dynamic, 256)
         for (int64_t i = 0; i < npatch; ++i) {
             int ni = (int)(poffs[i + 1] - poffs[i]);
             const int32_t* dofs = pdofs + poffs[i];
             const double* w = pw + poffs[i];
             const double* row = fac + foffs[i];
+            int64_t q = coffs[i];
             for (int k = 0; k < ni; ++k) {
                 if (!(w[k] > 0.0)) continue;
-                double c = 0.0;
-                for (int j = 0; j < ni; ++j) c += row[j] * r[dofs[j]];
-                delta[dofs[k]] += c;
+                double t = 0.0;
+                for (int j = 0; j < ni; ++j) t += row[j] * r[dofs[j]];
+                c[q++] = t;
                 row += ni;
             }
         }
+        memset(delta, 0, sizeof(double) * n);
+        for (int64_t i = 0; i < npatch; ++i) {
+            int64_t q = coffs[i];
+            for (int64_t k = poffs[i]; k < poffs[i + 1]; ++k)
+                if (pw[k] > 0.0) delta[pdofs[k]] += c[q++];
+        }
         for (int64_t j = 0; j < n; ++j) x[j] += omega * delta[j];
     }
-    free(r); free(delta);
+    free(r); free(delta); free(coffs); free(c);
 }
 
 /* Additive sweep with full local LU solves (diagonal Vanka, R17; also usable
- * for AV with fmt LU): r = b - L x; Delta = sum_i R_i^T (w_i o L_i^{-1} R_i r). */
+ * for AV with fmt LU): r = b - L x; Delta = sum_i R_i^T (w_i o L_i^{-1} R_i r).
+ * Local solves in parallel into per-patch slots (poffs-aligned), the sum into
+ * Delta serially in ascending patch order (thread-count independent bits). */
 void or_additive_lu_sweeps(int64_t n, const int64_t* rp, const int32_t* ci, const double* val,
                            int64_t npatch, const int64_t* poffs, const int32_t* pdofs, const double* pw,
                            const int64_t* foffs, const double* fac, const int32_t* piv_all,
                            const int64_t* pivoffs, double* x, const double* b, double omega, int nu) {
     double* r = malloc(sizeof(double) * n);
     double* delta = malloc(sizeof(double) * n);
-    double* loc = malloc(sizeof(double) * 1200);
+    double* loc = malloc(sizeof(double) * (poffs[npatch] > 0 ? poffs[npatch] : 1));
     for (int s = 0; s < nu; ++s) {
         or_residual(n, rp, ci, val, x, b, r);
-        memset(delta, 0, sizeof(double) * n);
+#pragma omp parallel for schedule(dynamic, 256)
         for (int64_t i = 0; i < npatch; ++i) {
             int ni = (int)(poffs[i + 1] - poffs[i]);
             const int32_t* dofs = pdofs + poffs[i];
-            for (int j = 0; j < ni; ++j) loc[j] = r[dofs[j]];
-            or_lu_solve(ni, fac + foffs[i], piv_all + pivoffs[i], loc);
-            for (int j = 0; j < ni; ++j) delta[dofs[j]] += pw[poffs[i] + j] * loc[j];
+            double* li = loc + poffs[i];
+            for (int j = 0; j < ni; ++j) li[j] = r[dofs[j]];
+            or_lu_solve(ni, fac + foffs[i], piv_all + pivoffs[i], li);
         }
+        memset(delta, 0, sizeof(double) * n);
+        for (int64_t i = 0; i < npatch; ++i)
+            for (int64_t k = poffs[i]; k < poffs[i + 1]; ++k) delta[pdofs[k]] += pw[k] * loc[k];
         for (int64_t j = 0; j < n; ++j) x[j] += omega * delta[j];
     }
     free(r); free(delta); free(loc);
@@ -1012,8 +1041,13 @@ int or_mg_solve(const or_level* levels, const or_coarse* C, int nlev, int smooth
 int64_t or_rav_sweep_sampled(int64_t n, const int64_t* rp, const int32_t* ci, const double* val,
                              int64_t npatch, const int64_t* poffs, const int32_t* pdofs, const double* pw,
                              const double* x, const double* b, double omega, const uint8_t* mask,
-                             double* xnew /* length n; only sampled entries written */) {
+                             double* xnew /* length n; only sampled entries written */,
+                             double* mag /* NULL or length n: rounding scale at sampled entries */) {
+    /* mag[j] = |x_j| + omega sum over patches |w_k (L_i^{-T} e_k)_a| (|b_a| + sum |L_a.| |x| + |r_a|):
+     * the magnitude of the terms that make up x_new[j] (a scale for element-wise parity bounds,
+     * not part of the method) */
     double* delta = calloc((size_t)n, sizeof(double));
+    double* dmag = mag ? calloc((size_t)n, sizeof(double)) : NULL;
     int64_t bad = -1;
     for (int64_t i = 0; i < npatch; ++i) {
         int ni = (int)(poffs[i + 1] - poffs[i]);
@@ -1025,29 +1059,43 @@ int64_t or_rav_sweep_sampled(int64_t n, const int64_t* rp, const int32_t* ci, co
         double* Li = malloc(sizeof(double) * ni * ni);
         int32_t* piv = malloc(sizeof(int32_t) * ni);
         double* ri = malloc(sizeof(double) * ni);
+        double* ra = malloc(sizeof(double) * ni);
         double* y = malloc(sizeof(double) * ni);
         extract_local(rp, ci, val, ni, dofs, Li);
         if (or_lu_factor(ni, Li, piv) != 0) { if (bad < 0) bad = i; }
         else {
             for (int a = 0; a < ni; ++a) {
                 int64_t row = dofs[a];
-                double s = 0.0;
-                for (int64_t k = rp[row]; k < rp[row + 1]; ++k) s += val[k] * x[ci[k]];
+                double s = 0.0, sa = 0.0;
+                for (int64_t k = rp[row]; k < rp[row + 1]; ++k) {
+                    s += val[k] * x[ci[k]];
+                    sa += fabs(val[k] * x[ci[k]]);
+                }
                 ri[a] = b[row] - s;
+                ra[a] = fabs(b[row]) + sa + fabs(ri[a]);
             }
             for (int k = 0; k < ni; ++k) {
                 if (!(w[k] > 0.0) || !mask[dofs[k]]) continue;
                 for (int j = 0; j < ni; ++j) y[j] = (j == k) ? 1.0 : 0.0;
                 or_lu_solve_t(ni, Li, piv, y);
-                double c = 0.0;
-                for (int j = 0; j < ni; ++j) c += w[k] * y[j] * ri[j];
+                double c = 0.0, ca = 0.0;
+                for (int j = 0; j < ni; ++j) {
+                    c += w[k] * y[j] * ri[j];
+                    ca += fabs(w[k] * y[j]) * ra[j];
+                }
                 delta[dofs[k]] += c;
+                if (dmag) dmag[dofs[k]] += ca;
             }
         }
-        free(Li); free(piv); free(ri); free(y);
+        free(Li); free(piv); free(ri); free(ra); free(y);
     }
-    for (int64_t j = 0; j < n; ++j) if (mask[j]) xnew[j] = x[j] + omega * delta[j];
+    for (int64_t j = 0; j < n; ++j)
+        if (mask[j]) {
+            xnew[j] = x[j] + omega * delta[j];
+            if (mag) mag[j] = fabs(x[j]) + omega * dmag[j];
+        }
     free(delta);
+    free(dmag);
     return bad;
 }
 
@@ -1115,6 +1163,14 @@ double or_eta(const or_desc* D, double x, double y, double z) {
     double p[3] = {x, y, z}, e, g[3];
     eta_and_grad(D, p, &e, g);
     return e;
+}
+
+void or_set_num_threads(int t) {
+#ifdef _OPENMP
+    if (t > 0) omp_set_num_threads(t);
+#else
+    (void)t;
+#endif
 }
 
 int or_num_threads(void) {

@@ -99,6 +99,7 @@ struct mg_level {
     double* x = nullptr;    // level iterate (l < L-1)
     double* b = nullptr;    // level right-hand side (l < L-1)
     double* r = nullptr;    // level residual
+    int64_t nvel = 0;       // DoFs < nvel are velocity
 };
 
 struct mg_ctx {
@@ -481,6 +482,7 @@ rav_status mg_setup(int n_levels, const rav_csr* A, const rav_patches* patches, 
     for (int l = 0; l < n_levels && st == RAV_OK; ++l) {
         mg_level& L = m->lv[l];
         if (l == 0) {
+            L.nvel = n_vel ? n_vel[0] : o.n_vel;
             st = csr_upload(&A[0], L.A, m->stream);
             if (st == RAV_OK) st = coarse_factor(L.A, coarse_pin, m->C, m->stream);
         } else {
@@ -492,6 +494,7 @@ rav_status mg_setup(int n_levels, const rav_csr* A, const rav_patches* patches, 
             int64_t bp = -1;
             rav_opts ol = o;
             if (n_vel) ol.n_vel = n_vel[l];
+            L.nvel = ol.n_vel;
             st = rav_setup(&A[l], &patches[l], &ol, &L.sm, &bp);
             if (st == RAV_ERR_SINGULAR_LOCAL) {
                 if (bad_level) *bad_level = l;
@@ -673,6 +676,20 @@ rav_status mg_solve(mg_ctx* m, double* x, const double* b, int pre, int post, do
 
 int64_t mg_last_launches(const mg_ctx* m) { return m ? m->last_launches : 0; }
 
+rav_status mg_normalize_pressure(mg_ctx* m, double* x, int mode) {
+    if (!m || !x || (mode != 0 && mode != 1)) { set_error("mg_normalize_pressure: bad argument"); return RAV_ERR_ARG; }
+    if (!is_device_ptr(x)) { set_error("mg_normalize_pressure: x must be a device pointer"); return RAV_ERR_ARG; }
+    mg_level& F = m->lv[m->L - 1];
+    if (F.nvel <= 0 || F.nvel >= F.A.n_rows) {
+        set_error("mg_normalize_pressure: the finest level has no pressure block (n_vel not given at mg_setup)");
+        return RAV_ERR_ARG;
+    }
+    g_launches = 0;
+    RAV_TRY(launch_pressure_normalize(x, F.nvel, F.A.n_rows, mode, F.nvel, m->norm2, m->part, m->stream));
+    m->last_launches = g_launches;
+    return RAV_OK;
+}
+
 rav_status mg_set_colors(mg_ctx* m, int level, int n_colors, const int64_t* color_offs, const int32_t* patch_ids) {
     if (!m || level < 1 || level >= m->L) { set_error("mg_set_colors: bad level"); return RAV_ERR_ARG; }
     RAV_TRY(rav_set_colors(m->lv[level].sm, n_colors, color_offs, patch_ids));
@@ -834,10 +851,10 @@ extern "C" rav_status mg_fgmres(mg_ctx* m, double* x, const double* b, int pre, 
             RAV_CUDA(cudaMemsetAsync(zj, 0, sizeof(double) * n, s));
             if (m->L == 1) RAV_TRY(launch_coarse_solve(m->C, vj, zj, s));
             else RAV_TRY(vcycle_launches(m, m->L - 1, zj, vj, pre, post, omega, false, true));   // z_j = M^{-1} v_j
-            // w = L z_j through the level's residual kernel (node-blocked, ~half the CSR bytes) with a zero
-            // right-hand side, r = -L z_j, then negated
+            // w' = -L z_j through the level's residual kernel (node-blocked, ~half the CSR bytes) with a zero
+            // right-hand side.  The sign is not flipped back: CGS on w' gives h'_i = -h_i and leaves -w, so
+            // the Hessenberg column takes -(h'_1 + h'_2) and v_{j+1} = w' / (-||w'||).
             RAV_TRY(launch_residual(F.A, zj, m->kzero, m->kw, s));
-            RAV_TRY(launch_scale(n, m->kw, -1.0, m->kw, s));
             for (int pass = 0; pass < 2; ++pass) {                                    // CGS2
                 double* hp = hd + pass * (M + 1);
                 if (j + 1 <= multi_dot_max()) {   // all projections in one pass over w
@@ -851,7 +868,7 @@ extern "C" rav_status mg_fgmres(mg_ctx* m, double* x, const double* b, int pre, 
             RAV_TRY(launch_dot(m->kw, m->kw, n, m->kpart, residual_norm_blocks(), hd + 2 * M + 2, 0, s));
             RAV_CUDA(cudaMemcpyAsync(hh.data(), hd, sizeof(double) * (2 * (M + 1) + 1), cudaMemcpyDeviceToHost, s));
             RAV_CUDA(cudaStreamSynchronize(s));
-            for (int i = 0; i <= j; ++i) H[(size_t)i * M + j] = hh[i] + hh[M + 1 + i];
+            for (int i = 0; i <= j; ++i) H[(size_t)i * M + j] = -(hh[i] + hh[M + 1 + i]);
             const double hn = sqrt(hh[2 * M + 2]);
             H[(size_t)(j + 1) * M + j] = hn;
             for (int i = 0; i < j; ++i) {   // previous Givens rotations
@@ -873,7 +890,7 @@ extern "C" rav_status mg_fgmres(mg_ctx* m, double* x, const double* b, int pre, 
             jn = j + 1;
             if (!(res == res) || isinf(res)) { set_error("mg_fgmres: residual is not finite at step %d", k); st = RAV_ERR_DIVERGED; break; }
             if (res <= rtol * r0 || k >= maxit || hn == 0.0) { done = true; break; }
-            RAV_TRY(launch_scale(n, m->kw, 1.0 / hn, V + (size_t)(j + 1) * n, s));
+            RAV_TRY(launch_scale(n, m->kw, -1.0 / hn, V + (size_t)(j + 1) * n, s));
         }
         if (st != RAV_OK) break;
         // y = H^{-1} g (upper triangular, jn x jn); x += Z y
@@ -886,6 +903,12 @@ extern "C" rav_status mg_fgmres(mg_ctx* m, double* x, const double* b, int pre, 
         RAV_TRY(launch_multi_axpy(n, jn, Z, n, hd, 1.0, x, s));
         RAV_TRY(launch_residual(F.A, x, b, m->kr, s));
         RAV_TRY(kry_norm(m, m->kr, n, hd + 2 * M + 2, &beta));
+        // the stopping test and the reported history use the TRUE residual ||b - L x|| after the update,
+        // not only the least-squares estimate: an estimate that met rtol while the true residual did
+        // not triggers a restart
+        if (hist) hist[k] = beta;
+        if (!(beta == beta) || isinf(beta)) { set_error("mg_fgmres: residual is not finite at step %d", k); st = RAV_ERR_DIVERGED; break; }
+        if (done && beta > rtol * r0 && k < maxit) done = false;
     }
     if (iters) *iters = k;
     m->last_launches = g_launches;

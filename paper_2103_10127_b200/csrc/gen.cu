@@ -8,6 +8,8 @@
 #include <cub/cub.cuh>
 #include <math_constants.h>
 
+#include <vector>
+
 #include "common.cuh"
 #include "internal.cuh"
 
@@ -1009,4 +1011,33 @@ extern "C" rav_status rav_gen_prolongation(const rav_grid* fine, const rav_grid*
     cudaFreeAsync(cnt, s);
     RAV_CUDA(cudaStreamSynchronize(s));
     return st;
+}
+
+// 4^d multicolouring of the generated patches (R10): patch of vertex (i, j[, k]) gets colour
+// (i mod 4) + 4 (j mod 4) [+ 16 (k mod 4)] by GLOBAL vertex coordinates (a slab window colours its
+// patches like the whole grid, so every rank relaxes the same colour at the same time); patches
+// ascending inside each colour.  Host outputs in the rav_set_colors layout.
+extern "C" rav_status rav_gen_colors(const rav_grid* g, int64_t* color_offs, int32_t* patch_ids) {
+    RAV_TRY(check_grid(g));
+    if (!color_offs || !patch_ids) { set_error("rav_gen_colors: NULL buffer"); return RAV_ERR_ARG; }
+    const Grid G = make_grid(g);
+    const int nc = g->dim == 2 ? 16 : 64;
+    int64_t nv[3] = {1, 1, 1};
+    for (int k = 0; k < g->dim; ++k) nv[k] = (int64_t)G.n[k] + 1;
+    std::vector<int> col(G.npatch);
+    std::vector<int64_t> cnt(nc + 1, 0);
+    for (int64_t q = 0; q < G.npatch; ++q) {
+        int64_t v = G.patch_off + q, c = 0, mult = 1;
+        for (int k = 0; k < g->dim; ++k) {
+            c += (v % nv[k]) % 4 * mult;
+            v /= nv[k];
+            mult *= 4;
+        }
+        col[q] = (int)c;
+        cnt[c + 1]++;
+    }
+    for (int c = 0; c < nc; ++c) cnt[c + 1] += cnt[c];
+    for (int c = 0; c <= nc; ++c) color_offs[c] = cnt[c];
+    for (int64_t q = 0; q < G.npatch; ++q) patch_ids[cnt[col[q]]++] = (int32_t)q;
+    return RAV_OK;
 }

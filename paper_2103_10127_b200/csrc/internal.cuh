@@ -94,6 +94,10 @@ rav_status launch_multi_dot(int64_t n, int nv, const double* V, int64_t ld, cons
 rav_status launch_multi_axpy(int64_t n, int nv, const double* V, int64_t ld, const double* coef, double alpha,
                              double* w, cudaStream_t s);
 rav_status launch_scale(int64_t n, const double* src, double sc, double* dst, cudaStream_t s);
+// a10 / R4: mode 0 p -= p[pin], mode 1 p -= mean(p) over x[n_vel .. n); shift: 1 device double,
+// part: >= residual_norm_blocks() device doubles
+rav_status launch_pressure_normalize(double* x, int64_t n_vel, int64_t n, int mode, int64_t pin, double* shift,
+                                     double* part, cudaStream_t s);
 
 // ---- setup.cu -------------------------------------------------------------------------
 struct PatchSet {

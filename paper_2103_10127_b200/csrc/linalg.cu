@@ -531,3 +531,74 @@ extern "C" rav_status rav_index_op(int op, const double* src, const int32_t* idx
     RAV_CHECK_LAUNCH();
     return RAV_OK;
 }
+
+// ------------------------------------------------------------------------------------
+// pressure normalisation (reading R4)
+// ------------------------------------------------------------------------------------
+namespace rav {
+
+// s[0] = the shift: mode 0 x[pin], mode 1 the mean of x[n_vel .. n) (partials summed in fixed
+// block order, so the result is bitwise reproducible)
+__global__ void pressure_shift_kernel(int64_t np, double* __restrict__ xp, const double* __restrict__ s,
+                                      double scale) {
+    const double sh = s[0] * scale;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < np; k += (int64_t)gridDim.x * blockDim.x)
+        xp[k] -= sh;
+}
+
+__global__ void __launch_bounds__(256) sum_kernel(int64_t n, const double* __restrict__ a, double* __restrict__ part) {
+    __shared__ double red[8];
+    double t = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        t += a[i];
+    t = warp_sum(t);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double u = 0.0;
+        for (int w = 0; w < 8; ++w) u += red[w];
+        part[blockIdx.x] = u;
+    }
+}
+
+// shift: one device double; part: >= residual_norm_blocks() doubles of device scratch
+rav_status launch_pressure_normalize(double* x, int64_t n_vel, int64_t n, int mode, int64_t pin, double* shift,
+                                     double* part, cudaStream_t s) {
+    const int64_t np = n - n_vel;
+    if (np <= 0) return RAV_OK;
+    double scale = 1.0;
+    if (mode == 0) {
+        RAV_CUDA(cudaMemcpyAsync(shift, x + pin, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    } else {
+        const int nblk = residual_norm_blocks();
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(np, 256), nblk));
+        sum_kernel<<<blocks, 256, 0, s>>>(np, x + n_vel, part);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+        sum_parts_acc_kernel<<<1, 256, 0, s>>>(part, blocks, shift, 0);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+        scale = 1.0 / (double)np;
+    }
+    const int blocks = (int)std::min<int64_t>(cdiv(np, 256), (int64_t)num_sms() * 8);
+    pressure_shift_kernel<<<blocks, 256, 0, s>>>(np, x + n_vel, shift, scale);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}
+
+}  // namespace rav
+
+extern "C" rav_status rav_pressure_normalize(double* x, int64_t n_vel, int64_t n, int mode, int64_t pin,
+                                             void* stream) {
+    using namespace rav;
+    if (!x || n_vel < 0 || n < n_vel || (mode != 0 && mode != 1) || (mode == 0 && (pin < n_vel || pin >= n))) {
+        set_error("rav_pressure_normalize: bad argument (need 0 <= n_vel <= n, mode 0/1, n_vel <= pin < n for mode 0)");
+        return RAV_ERR_ARG;
+    }
+    if (!is_device_ptr(x)) { set_error("rav_pressure_normalize: x must be a device pointer"); return RAV_ERR_ARG; }
+    g_launches = 0;
+    static thread_local double* work = nullptr;
+    if (!work) RAV_CUDA(cudaMalloc(&work, sizeof(double) * (residual_norm_blocks() + 1)));
+    return launch_pressure_normalize(x, n_vel, n, mode, pin, work, work + 1, as_stream(stream));
+}

@@ -256,23 +256,10 @@ class DistSweeper:
 
 def local_colors(slab: Slab) -> Tuple[np.ndarray, np.ndarray]:
     """4^d colouring (R10) of this rank's patches by GLOBAL vertex coordinates,
-    so every rank relaxes the same colour at the same time: colour (i mod 4) +
-    4 (j mod 4) [+ 16 (k mod 4)], local patches ascending inside each colour.
-    Returns (offs[4^d + 1], local patch ids)."""
-    dim = slab.dim
-    nc = [int(c) for c in slab.problem["ncell"][:dim]]
-    nv = [c + 1 for c in nc]
-    gid = slab.nlow_vert * slab.V0 + np.arange(slab.n_patches)
-    color = np.zeros(slab.n_patches, np.int64)
-    r, mult = gid.copy(), 1
-    for k in range(dim):
-        color += (r % nv[k]) % 4 * mult
-        r //= nv[k]
-        mult *= 4
-    ids = np.argsort(color, kind="stable").astype(np.int32)
-    offs = np.zeros(4 ** dim + 1, np.int64)
-    offs[1:] = np.cumsum(np.bincount(color, minlength=4 ** dim))
-    return offs, ids
+    so every rank relaxes the same colour at the same time: the library's
+    rav_gen_colors on the rank's window.  Returns (offs[4^d + 1], local patch ids)."""
+    from . import ravgmg as rg
+    return rg.multicolor(slab.local_problem())
 
 
 class DistMVSweeper(DistSweeper):

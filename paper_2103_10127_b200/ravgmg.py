@@ -114,6 +114,9 @@ def _load():
         "rav_stream_wait": [vp, vp, C.c_uint32],
         "rav_stream_signal": [vp, vp, C.c_uint32],
         "rav_peer_put": [vp, vp, i64, vp],
+        "rav_gen_colors": [P(RavGrid), vp, vp],
+        "rav_pressure_normalize": [vp, i64, i64, C.c_int, i64, vp],
+        "mg_normalize_pressure": [vp, vp, C.c_int],
         "rav_adaptive_sizes": [vp, C.c_int, P(i64), P(i64), P(i64), P(i64), P(i64), P(i64), P(i64)],
         "rav_adaptive_fill": [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
     }
@@ -384,6 +387,11 @@ class Multigrid:
                              float(rtol), int(maxit), C.byref(it), hist.ctypes.data))
         return x, it.value, hist[:it.value + 1]
 
+    def normalize_pressure(self, x, mode: int = 0):
+        """mg_normalize_pressure (row a10, R4): mode 0 p -= p(vertex 0), mode 1 p -= mean(p)."""
+        _check(lib.mg_normalize_pressure(self.ctx, _ptr(x), int(mode)))
+        return x
+
     @property
     def last_launches(self) -> int:
         return int(lib.mg_last_launches(self.ctx))
@@ -445,6 +453,14 @@ def dot(a, b, out, accumulate: bool = False, n: Optional[int] = None, stream=Non
     return out
 
 
+def pressure_normalize(x, n_vel: int, mode: int = 0, pin: Optional[int] = None, stream=None):
+    """rav_pressure_normalize (row a10, R4): mode 0 p -= p[pin] (default pin = n_vel, vertex 0),
+    mode 1 p -= mean(p), over x[n_vel:] (device tensor, in place)."""
+    pin = int(n_vel) if pin is None else int(pin)
+    _check(lib.rav_pressure_normalize(_ptr(x), int(n_vel), x.numel(), int(mode), pin, _stream(stream)))
+    return x
+
+
 def index_op(op: int, src, idx, dst, value: float = 0.0, stream=None):
     """rav_index_op: 0 gather dst[k] = src[idx[k]], 1 scatter dst[idx[k]] = src[k],
     2 scatter-add, 3 fill dst[idx[k]] = value, 4 gather-difference
@@ -456,21 +472,23 @@ def index_op(op: int, src, idx, dst, value: float = 0.0, stream=None):
 
 
 def multicolor(problem: Dict):
-    """4^d colouring of the vertex patches (R10): colour (i mod 4) + 4 (j mod 4)
-    [+ 16 (k mod 4)], patches ascending inside each colour.  Returns (offs, ids)."""
-    dim = problem["dim"]
-    nv = [problem["ncell"][k] + 1 for k in range(dim)]
-    idx = np.arange(int(np.prod(nv)))
-    color = np.zeros_like(idx)
-    r, mult = idx.copy(), 1
-    for k in range(dim):
-        color += (r % nv[k]) % 4 * mult
-        r //= nv[k]
-        mult *= 4
-    ids = np.argsort(color, kind="stable").astype(np.int32)
-    offs = np.zeros(4 ** dim + 1, np.int64)
-    offs[1:] = np.cumsum(np.bincount(color, minlength=4 ** dim))
-    return offs, ids
+    """rav_gen_colors: 4^d colouring of the generated vertex patches (R10) by global
+    vertex coordinates (a slab window colours its patches like the whole grid),
+    patches ascending inside each colour.  Returns (offs, ids) for rav_set_colors."""
+    g = grid(problem)
+    sz = rav_gen_sizes(problem) if "window" not in problem else None
+    npatch = sz["npatch"] if sz is not None else _window_patches(problem)
+    offs = np.zeros(4 ** problem["dim"] + 1, np.int64)
+    ids = np.zeros(max(npatch, 1), np.int32)
+    _check(lib.rav_gen_colors(C.byref(g), offs.ctypes.data, ids.ctypes.data))
+    return offs, ids[:npatch]
+
+
+def _window_patches(problem: Dict) -> int:
+    """Patches of a slab window (vertex layers [pvert_lo, pvert_hi] of the last axis), host arithmetic."""
+    dim, w = problem["dim"], problem["window"]
+    low = int(np.prod([int(problem["ncell"][k]) + 1 for k in range(dim - 1)]))
+    return low * (int(w["pvert_hi"]) - int(w["pvert_lo"]) + 1)
 
 
 def coarsen_problem(problem: Dict) -> Dict:

@@ -47,6 +47,8 @@ def main(argv=None) -> int:
     ap.add_argument("--max-iters", type=int, default=200)
     ap.add_argument("--fgmres", action="store_true", help="FGMRES(30) with the V-cycle as preconditioner (R19)")
     ap.add_argument("--deterministic", action="store_true", help="bitwise reproducible scatter (R16)")
+    ap.add_argument("--pressure", default="pin", choices=["pin", "mean", "none"],
+                    help="normalise the solution's pressure (row a10, R4): p(vertex 0) = 0, zero mean, or as is")
     a = ap.parse_args(argv)
 
     import torch
@@ -89,11 +91,13 @@ def main(argv=None) -> int:
     else:
         x, k, hist = mg.solve(x, fine["b"], pre=a.pre, post=a.post, omega=omega, rtol=a.tol, maxit=a.max_iters)
     e1.record(stream)
+    if a.pressure != "none":
+        mg.normalize_pressure(x, mode=0 if a.pressure == "pin" else 1)
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / 1e3
     rho = float((hist[-1] / hist[0]) ** (1.0 / max(k, 1))) if hist[0] > 0 else 0.0
     print(json.dumps({"problem": desc, "smoother": a.smoother, "omega": omega, "pre": a.pre, "post": a.post,
-                      "krylov": "fgmres(30)" if a.fgmres else None, "free_dofs": fine["n"], "iterations": k,
+                      "krylov": "fgmres(30)" if a.fgmres else None, "pressure": a.pressure, "free_dofs": fine["n"], "iterations": k,
                       "converged": bool(hist[-1] <= a.tol * hist[0]), "avg_reduction_factor": rho,
                       "setup_s": setup, "solve_s": t, "ms_per_iteration": t / max(k, 1) * 1e3,
                       "residual_history": [float(h) for h in hist]}))

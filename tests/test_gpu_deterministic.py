@@ -9,6 +9,7 @@ import torch
 
 import oracle
 import seeded_inputs as si
+from _parity import SweepChecker
 
 pytestmark = pytest.mark.gpu
 
@@ -38,16 +39,20 @@ def test_deterministic_sweeps_are_bitwise_reproducible_and_match_oracle(rg, prob
         runs.append(x.cpu().numpy())
     for r in runs[1:]:
         assert np.array_equal(r, runs[0])
-    if prob["ncell"][0] <= 12 or prob["dim"] == 2:
-        O = oracle.assemble(prob)
-        P = oracle.patches(prob, "pou")
-        F = oracle.factor(O, P, oracle.FMT_ROWS)
-        xo = oracle.additive_sweeps(O, P, F, x0, O["b"], 0.66, 4)
-        assert np.linalg.norm(runs[0] - xo) <= 1e-12 * np.linalg.norm(xo)
+    O = oracle.assemble(prob)
+    P = oracle.patches(prob, "pou")
+    F = oracle.factor(O, P, oracle.FMT_ROWS)
+    xd = torch.tensor(x0, device="cuda")
+
+    def gpu(k):
+        sm.smooth(xd, G["b"], k, 0.66)
+        return xd.cpu().numpy()
+
+    SweepChecker(O, P, F, O["b"], 0.66).run(x0, gpu, (1, 4), what="deterministic " + sm.kernel_name)
     sa = rg.Smoother(G, G)
     xa = torch.tensor(x0, device="cuda")
     sa.smooth(xa, G["b"], 4, 0.66)
-    assert np.linalg.norm(xa.cpu().numpy() - runs[0]) <= 1e-13 * np.linalg.norm(runs[0])
+    assert np.abs(xa.cpu().numpy() - runs[0]).max() <= 1e-13 * np.abs(runs[0]).max()
 
 
 def test_deterministic_vcycle_same_counts(rg):

@@ -211,3 +211,22 @@ def test_lu_pivoting_and_transposed_solve():
         np.testing.assert_allclose(oracle.lu_solve(LU, piv, e, trans=True), inv[j], rtol=1e-10, atol=1e-12)
     with pytest.raises(oracle.SingularLocalSystem):
         oracle.lu_factor(np.array([[1.0, 2.0], [2.0, 4.0]]))
+
+
+def test_oracle_sweeps_are_thread_count_independent():
+    """The oracle's parallel loops (residual rows, per-patch products / local solves) write
+    disjoint slots and the corrections are summed serially in ascending patch order, so 1
+    and all threads give the same bits (AV/RAV rows and the LU-based diagonal Vanka)."""
+    prob = si.problem(2, (12, 10), si.KIND_MMS, eta="fourier")
+    A = oracle.assemble(prob)
+    x0 = si.initial_guess(A["n"], seed=5)
+    out = {}
+    for t in (1, 4):
+        prev = oracle.set_num_threads(t)
+        for w, fmt, om in (("pou", oracle.FMT_ROWS, 0.66), ("full", oracle.FMT_DIAG, 0.1)):
+            P = oracle.patches(prob, w)
+            F = oracle.factor(A, P, fmt)
+            out[(t, w)] = oracle.additive_sweeps(A, P, F, x0, A["b"], om, 3)
+        oracle.set_num_threads(prev)
+    for w in ("pou", "full"):
+        assert np.array_equal(out[(1, w)], out[(4, w)]), w
