@@ -556,100 +556,93 @@ def run_adaptive_study(rg, si, stream, max_levels=7):
     return out
 
 
-def run_dist_vcycle(name, rdist, si, stream, dist, ws, rank):
-    """Slab-partitioned V-cycle to rtol on ws GPUs (strong scaling of c3 / c4):
-    partitioned fine levels with NCCL interface sums / halo refreshes, windowed
-    transfers, the coarse levels agglomerated (all-reduced rhs, solved
-    redundantly on every rank); ||r||^2 all-reduced per cycle.  Device time
-    with CUDA events around the solve, max over ranks."""
+def _dist_build(rdist, rg, prob, levels, ws, rank, comm, gather, stream, **kw):
+    """One rank's share of the library-driven slab-partitioned hierarchy (mgd_setup)."""
+    return rdist.build_lib_dist(prob, levels, ws, [rank], list(range(ws)), comm, gather=gather, stream=stream, **kw)
+
+
+def run_dist_vcycle(name, rdist, rg, si, stream, dist, ws, rank, comm, gather):
+    """Slab-partitioned V-cycle to rtol on ws GPUs (strong scaling of c3 / c4) inside the library
+    (mgd_solve): partitioned fine levels with NCCL interface sums / halo refreshes, windowed
+    transfers, the coarse levels agglomerated (all-gathered rhs summed in subdomain order, solved
+    redundantly on every rank); ||r||^2 all-gathered per cycle; every cycle one CUDA graph.
+    Device time with CUDA events around the solve, max over ranks."""
     import torch
     c = si.CONFIGS[name]
     prob = si.config_problem(name)
     t0 = time.perf_counter()
-    cyc, levels = rdist.build_gpu_cycle(prob, c["levels"], ws, rank, rdist.TorchComm())
+    mgd, info = _dist_build(rdist, rg, prob, c["levels"], ws, rank, comm, gather, stream)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
-    x, b = levels[0]["x"], levels[0]["b"]
-    cyc.solve(x, b, pre=c["pre"], post=c["post"], omega=c["omega"], rtol=c["rtol"], maxit=2)   # warm
+    xs, bs = info["x"], info["b"]
+    mgd.solve(xs, bs, pre=c["pre"], post=c["post"], omega=c["omega"], rtol=c["rtol"], maxit=2)   # warm (capture)
     times = []
     for _ in range(2):
-        x.zero_()
+        for x in xs:
+            x.zero_()
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        _, iters, hist = cyc.solve(x, b, pre=c["pre"], post=c["post"], omega=c["omega"], rtol=c["rtol"],
-                                   maxit=100)
+        _, iters, hist = mgd.solve(xs, bs, pre=c["pre"], post=c["post"], omega=c["omega"], rtol=c["rtol"], maxit=100)
         e1.record(stream)
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) / 1e3)
+    enq, wait, ncyc = mgd.host_time()
     tt = torch.tensor([min(times)], device="cuda")
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t = float(tt.item())
-    slab = levels[0]["slab"]
-    out = {"config": VCYCLE_DESC[name] + f"; slab-partitioned over {ws} GPUs",
+    slab = info["slabs"][0][0]
+    out = {"config": VCYCLE_DESC[name] + f"; slab-partitioned over {ws} GPUs (library mgd_solve, NCCL)",
            "free_dofs": slab.nvel_glob + slab.nvert_glob, "rtol": c["rtol"], "cycles": iters,
            "converged": bool(hist[-1] <= c["rtol"] * hist[0]), "time_to_rtol_s": t,
-           "ms_per_cycle": t / max(iters, 1) * 1e3, "partitioned_levels": len(levels), "setup_s": setup_s,
-           "timing": "CUDA events around DistVCycle.solve, best of 2, max over ranks"}
-    del cyc, levels, x, b
+           "ms_per_cycle": t / max(iters, 1) * 1e3, "partitioned_levels": info["K"],
+           "partition": [list(p) for p in info["parts"][0]], "setup_s": setup_s,
+           "host_enqueue_ms_per_cycle": enq / max(ncyc, 1) * 1e3, "gpu_launches": mgd.last_launches,
+           "timing": "CUDA events around mgd_solve, best of 2, max over ranks"}
+    mgd.close()
+    del mgd, info, xs, bs
     torch.cuda.empty_cache()
     return out
 
 
-def run_dist_c5(rdist, rg, si, stream, dist, ws, rank):
-    """BASELINE config 5 at N GPUs (weak scaling): 2048^2 Q2-Q1 per GPU stacked in
-    y, slab-partitioned; 50 sweeps each of RAV (omega 0.66), diagonal Vanka
-    (omega 0.1) and multicoloured MV (omega 0.66) from the seeded N(0,1) guess,
-    every sweep with its interface exchanges over NCCL (MV: one exchange pair per
-    colour).  Device time (CUDA events), max over ranks; MDoF/s over all GPUs."""
+def run_dist_c5(rdist, rg, si, stream, dist, ws, rank, comm, gather):
+    """BASELINE config 5 at N GPUs (weak scaling): 2048^2 Q2-Q1 per GPU stacked in y, slab-
+    partitioned; 50 sweeps each of RAV (omega 0.66), diagonal Vanka (omega 0.1) and multicoloured
+    MV (omega 0.66) from the seeded N(0,1) guess through mgd_smooth (every sweep with its interface
+    exchanges over NCCL; MV: one exchange pair per colour).  Device time, max over ranks."""
     import torch
     prob = si.config_problem("c5", scale_y=ws)
     out = {"config": f"c5 weak scaling: 2048 x {2048 * ws} Q2-Q1 MMS on [0,1]x[0,{ws}], seeded eta, "
                      f"slab-partitioned over {ws} GPUs, 50 sweeps from seeded N(0,1)"}
-    comm = rdist.TorchComm()
     for name, weights, variant, omega in (("rav", "pou", rg.VARIANT_ROWS, 0.66),
                                           ("diag_vanka", "full", rg.VARIANT_DIAG, 0.1),
                                           ("mv_color", "full", rg.VARIANT_MV, 0.66)):
         try:
-            slab = rdist.Slab(prob, ws, rank)
-            L = rg.gen_level(slab.local_problem(), weights)
-            sm = rg.Smoother(L, L, variant=variant)
-            be = rdist.GpuBackend(sm, stream)
-            written = rdist.written_local_from_patches(L)
-            if variant == rg.VARIANT_MV:
-                offs, ids = rdist.local_colors(slab)
-                sm.set_colors(offs, ids)
-                sw = rdist.DistMVSweeper(slab, be, comm, written, len(offs) - 1)
-            else:
-                sw = rdist.DistSweeper(slab, be, comm, written)
+            mgd, info = _dist_build(rdist, rg, prob, 1, ws, rank, comm, gather, stream, weights=weights,
+                                    variant=variant, smooth_only=True)
+            slab = info["slabs"][0][0]
             nglob = slab.nvel_glob + slab.nvert_glob
             x0 = torch.tensor(si.initial_guess(nglob, seed=si.X0_SEED)[slab.global_ids()], device="cuda")
-            b = L["b"]
-
-            def rnorm(xv):
-                r = sm.residual(xv, b)
-                s = be.dot_owned(r, slab.owned_ranges())
-                dist.all_reduce(s)
-                return float(s.item()) ** 0.5
-            r0 = rnorm(x0)
+            b = info["b"][0]
+            r0 = mgd.residual_norm([x0], [b])
             x = x0.clone()
-            sw.smooth(x, b, 2, omega)      # warm
-            x = x0.clone()
+            mgd.smooth([x], [b], 50, omega)      # warm (capture)
+            x.copy_(x0)
             torch.cuda.synchronize()
             dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            sw.smooth(x, b, 50, omega)
+            mgd.smooth([x], [b], 50, omega)
             e1.record(stream)
             torch.cuda.synchronize()
             t = torch.tensor([e0.elapsed_time(e1) / 50], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
             out[name] = {"ms_per_sweep": ms, "mdofs": nglob / (ms * 1e-3) / 1e6, "omega": omega,
-                         "residual_reduction_50": rnorm(x) / r0, "kernel": sm.kernel_name}
-            sm.close()
-            del sm, L, sw, be, x, x0, b
+                         "residual_reduction_50": mgd.residual_norm([x], [b]) / r0}
+            mgd.close()
+            del mgd, info, x, x0, b
             torch.cuda.empty_cache()
         except Exception as err:  # report, keep the line
             out[name] = {"error": f"{type(err).__name__}: {err}"[:200]}
@@ -657,54 +650,52 @@ def run_dist_c5(rdist, rg, si, stream, dist, ws, rank):
 
 
 def run_gpu_dist(args):
-    """N > 1 (torchrun): weak scaling of the c2 workload, one 512^2 block per GPU
-    stacked along y (BASELINE config 5's layout): the finest level is
-    slab-partitioned and every sweep runs the interface-correction sum and the
-    halo refresh over NCCL (paper_2103_10127_b200/dist.py)."""
-    import numpy as np
+    """N > 1 (torchrun): weak scaling of the c2 workload, one 512^2 block per GPU stacked along y
+    (BASELINE config 5's layout), slab-partitioned inside the library: every sweep runs the
+    interface-correction sum and the halo refresh over NCCL (mgd_smooth, one CUDA graph per step).
+    torch.distributed (NCCL) is the plumbing: the library communicator's NCCL id, the host
+    all-gather of the exchange plans, barriers and the max-over-ranks timing."""
     import torch
     import torch.distributed as dist
     ws, rank, local = dist_env()
-    # RAV_DIST_BACKEND=gloo + RAV_SINGLE_DEVICE=1: every rank on cuda:0 with host-staged exchanges --
-    # a functional check of this path on a one-GPU box, never a timed configuration
-    dev = 0 if os.environ.get("RAV_SINGLE_DEVICE") else local
-    torch.cuda.set_device(dev)
-    backend = os.environ.get("RAV_DIST_BACKEND", "nccl")
-    if backend == "nccl":
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-    else:
-        dist.init_process_group(backend)
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2103_10127_b200 import dist as rdist
     from paper_2103_10127_b200 import ravgmg as rg
     import seeded_inputs as si
 
+    obj = [rg.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = rg.Comm(ws, rank, obj[0])
+
+    def gather(o):
+        out = [None] * ws
+        dist.all_gather_object(out, o)
+        return out
+
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     prob = si.config_problem("c2", scale_y=ws)
-    slab = rdist.Slab(prob, ws, rank)
     t0 = time.perf_counter()
-    L = rg.gen_level(slab.local_problem(), "pou")
-    sm = rg.Smoother(L, L)
+    mgd, info = _dist_build(rdist, rg, prob, 1, ws, rank, comm, gather, stream, smooth_only=True)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
-    written = rdist.written_local_from_patches(L)
-    sw = rdist.DistSweeper(slab, rdist.GpuBackend(sm, stream), rdist.TorchComm(), written)
+    slab = info["slabs"][0][0]
     n_glob = slab.nvel_glob + slab.nvert_glob
-    gids = slab.global_ids()
-    x0 = torch.tensor(si.initial_guess(n_glob, seed=si.X0_SEED)[gids], device="cuda")
-    x, b = x0.clone(), L["b"]
-    kernels_per_sweep = 3 + len(sw.cs) + len(sw.cr) + len(sw.hs) + len(sw.hr)
+    x0 = torch.tensor(si.initial_guess(n_glob, seed=si.X0_SEED)[slab.global_ids()], device="cuda")
+    x, b = x0.clone(), info["b"][0]
 
     for _ in range(args.warmup):
-        sw.smooth(x, b, SWEEPS_PER_STEP, OMEGA)
+        mgd.smooth([x], [b], SWEEPS_PER_STEP, OMEGA)
+    launches_per_step = mgd.last_launches
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
+    with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            sw.smooth(x, b, SWEEPS_PER_STEP, OMEGA)
+            mgd.smooth([x], [b], SWEEPS_PER_STEP, OMEGA)
         e1.record(stream)
         torch.cuda.synchronize()
     dist.barrier()
@@ -715,55 +706,9 @@ def run_gpu_dist(args):
     value = n_glob * SWEEPS_PER_STEP / (ms_per_step * 1e-3) / 1e6
     assert torch.isfinite(x).all()
 
-    # the same sweeps over the peer-memory transport (CUDA IPC + stream-memory-op flags, no NCCL);
-    # checked against the NCCL result; a watchdog keeps a stuck transport from costing the line
-    p2p = None
-    if os.environ.get("RAV_BENCH_P2P", "1") == "1" and not os.environ.get("RAV_SINGLE_DEVICE"):
-        import threading
-        done = threading.Event()
-        xref = x.clone()
-
-        def watchdog():
-            if not done.wait(120):
-                line_partial = {"metric": "RAV sweep throughput (c2: 512^2 Q2-Q1, variable viscosity)",
-                                "value": value, "unit": "MDoF/s", "n_gpus": ws, "steps": args.steps,
-                                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                                "config": {"workload": "c2 per GPU stacked along y", "free_dofs": n_glob},
-                                "p2p": {"error": "peer transport did not finish within 120 s"}}
-                if rank == 0:
-                    print(json.dumps(line_partial), flush=True)
-                os._exit(0)
-        threading.Thread(target=watchdog, daemon=True).start()
-        try:
-            pcomm = rdist.PeerComm(rdist.TorchComm(), rank)
-            swp = rdist.DistSweeper(slab, rdist.GpuBackend(sm, stream), pcomm, written)
-            xp = x0.clone()                              # same start and sweep count as the NCCL run (xref)
-            for _ in range(args.warmup):
-                swp.smooth(xp, b, SWEEPS_PER_STEP, OMEGA)
-            torch.cuda.synchronize()
-            dist.barrier()
-            torch.cuda.synchronize()
-            e0p, e1p = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0p.record(stream)
-            for _ in range(args.steps):
-                swp.smooth(xp, b, SWEEPS_PER_STEP, OMEGA)
-            e1p.record(stream)
-            torch.cuda.synchronize()
-            tp = torch.tensor([e0p.elapsed_time(e1p)], device="cuda")
-            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
-            msp = float(tp.item()) / args.steps
-            rel = float((xp - xref).norm() / xref.norm())
-            p2p = {"value": n_glob * SWEEPS_PER_STEP / (msp * 1e-3) / 1e6, "unit": "MDoF/s", "ms_per_step": msp,
-                   "rel_diff_vs_nccl": rel,
-                   "transport": "CUDA IPC receive slots + cuStreamWaitValue32/cuStreamWriteValue32 flags"}
-            pcomm.close()
-        except Exception as err:  # report, keep the line
-            p2p = {"error": f"{type(err).__name__}: {err}"[:200]}
-        done.set()
-        x = xref
-
-    # dominant kernel alone on this rank (local patches)
+    # dominant kernel alone on this rank (its window's patches), through a single-domain smoother
+    L = mgd._keep[0][0][0]["level"]
+    sm = rg.Smoother(L, L)
     r = sm.residual(x, b)
     for _ in range(5):
         sm.apply(r, x, OMEGA)
@@ -777,8 +722,11 @@ def run_gpu_dist(args):
     bytes_info = sm.sweep_bytes()
     peak, peak_kind = load_peaks()
     achieved = bytes_info["sweep"] / (sweep_ms * 1e-3) / 1e9
+    kname = sm.kernel_name
+    sm.close()
+    del sm
 
-    # end to end: pinned host x/b in, result out, every step
+    # end to end: pinned host x / b in, the iterate out, every step
     xh = x0.cpu().pin_memory()
     bh = b.cpu().pin_memory()
     dist.barrier()
@@ -787,7 +735,7 @@ def run_gpu_dist(args):
     for _ in range(args.steps):
         x.copy_(xh, non_blocking=True)
         b.copy_(bh, non_blocking=True)
-        sw.smooth(x, b, SWEEPS_PER_STEP, OMEGA)
+        mgd.smooth([x], [b], SWEEPS_PER_STEP, OMEGA)
         xh.copy_(x, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -801,36 +749,37 @@ def run_gpu_dist(args):
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"c2 per GPU stacked along y: 512 x {512 * ws} Q2-Q1 cells on [0,1]x[0,{ws}], "
-                               "MMS forcing, seeded eta; step = 100 slab-partitioned RAV sweeps (residual, "
-                               "RAV sweep, NCCL interface-correction sum + halo refresh)",
+                               "MMS forcing, seeded eta; step = 100 slab-partitioned RAV sweeps inside the library "
+                               "(residual, RAV sweep, NCCL interface-correction sum + halo refresh; one CUDA graph)",
                    "free_dofs": n_glob, "sweeps_per_step": SWEEPS_PER_STEP, "omega": OMEGA,
-                   "parallelism": f"slab partition x{ws} (NCCL point-to-point)",
-                   "l2": "inputs larger than L2 (factor rows + CSR stream from HBM every sweep)"},
+                   "parallelism": f"slab partition x{ws} (mgd_smooth, NCCL point-to-point)",
+                   "partition": [list(p) for p in info["parts"][0]],
+                   "l2": "inputs larger than L2 (factor rows + node-blocked operator stream from HBM every sweep)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_kind": peak_kind, "kernel": sm.kernel_name + " via rav_apply (rank 0)",
+                     "traffic": None, "peak_kind": peak_kind, "kernel": kname + " via rav_apply (rank 0's window)",
                      "kernel_ms": sweep_ms, "algorithmic_bytes_per_launch": bytes_info["sweep"]},
         "setup_s": setup_s,
         "e2e": {"value": e2e_value, "unit": "MDoF/s", "h2d_bytes_per_step": 16 * slab.n_loc * ws,
                 "d2h_bytes_per_step": 8 * slab.n_loc * ws},
-        "gpu_launches": kernels_per_sweep * SWEEPS_PER_STEP * args.steps,
+        "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }
-    if p2p is not None:
-        line["p2p_exchange"] = p2p
-    del sw, sm, L
+    mgd.close()
+    del mgd, info, x, x0, b
     torch.cuda.empty_cache()
     if not args.no_smoothers:
-        line["c5_smoothers"] = run_dist_c5(rdist, rg, si, stream, dist, ws, rank)
+        line["c5_smoothers"] = run_dist_c5(rdist, rg, si, stream, dist, ws, rank, comm, gather)
     if not args.no_vcycle:
         vc = {}
         for name in ("c3", "c4"):
             try:
-                vc[name] = run_dist_vcycle(name, rdist, si, stream, dist, ws, rank)
+                vc[name] = run_dist_vcycle(name, rdist, rg, si, stream, dist, ws, rank, comm, gather)
             except Exception as e:  # report, keep the sweep line
                 vc[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
         line["vcycle"] = vc
     if rank == 0:
         print(json.dumps(line), flush=True)
+    comm.close()
     dist.destroy_process_group()
     return 0
 

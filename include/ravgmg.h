@@ -416,23 +416,124 @@ void rav_xfer_destroy(rav_xfer* t);
  * of the stopping test (R11) over a rank's owned DoFs. */
 rav_status rav_dot(const double* a, const double* b, int64_t n, double* out, int accumulate, void* stream);
 
-/* Peer-memory transport of the slab exchanges (SURVEY section 8 row e; dist.PeerComm):
- * rav_device_alloc / rav_device_free: zeroed library allocations (exact allocation bases,
- * so CUDA IPC handles map them 1:1).  rav_ipc_export / rav_ipc_import / rav_ipc_close:
- * CUDA IPC (64-byte handles; import maps a peer's buffer, over NVLink when it lives on
- * another GPU).  rav_stream_wait: the stream waits until *flag >= value (32-bit,
- * wrap-around compare), then flushes remote writes where supported;
- * rav_stream_signal: *flag = value after all prior work in the stream (release order).
- * Both are stream memory operations: no host round trip, no spinning kernel.
- * rav_peer_put: dst[k] = src[k], k < n, with dst possibly a peer (imported) pointer. */
-rav_status rav_device_alloc(int64_t bytes, void** dev_ptr);
-rav_status rav_device_free(void* dev_ptr);
-rav_status rav_ipc_export(void* dev_ptr, unsigned char* handle);
-rav_status rav_ipc_import(const unsigned char* handle, void** dev_ptr);
-rav_status rav_ipc_close(void* dev_ptr);
-rav_status rav_stream_wait(void* stream, uint32_t* flag, uint32_t value);
-rav_status rav_stream_signal(void* stream, uint32_t* flag, uint32_t value);
-rav_status rav_peer_put(const double* src, double* dst, int64_t n, void* stream);
+
+/* ------------------------------------------------------------------------- */
+/* Slab-partitioned (multi-GPU) smoother and V-cycle in the library           */
+/* (SURVEY section 8 rows a11 / b / e; within a sweep every       */
+/* patch is independent, so RAV shards by patches with one interface exchange  */
+/* per sweep)                                                                  */
+/* ------------------------------------------------------------------------- */
+/* The finest levels are cut into subdomains (slabs of patches); global
+ * subdomain ids are 0 .. n_sub_total-1 and subdomain g lives on process
+ * sub_proc[g].  A process drives one or more subdomains (n_local >= 1) on its
+ * current device: one per GPU in production; several on one GPU to emulate a
+ * multi-GPU run with one process (the exchanges between subdomains of the same
+ * process are then plain device reads of the neighbour's buffers -- no kernel
+ * ever waits on another).  Per sweep on a partitioned level, for every local
+ * subdomain: r = b - L x on its rows; x := 0 on its ghost-written DoFs; the RAV
+ * sweep of its patches (Eq. 13); then (1) the partial corrections on
+ * ghost-written DoFs go to their owners, which add them (interface-correction
+ * sum), (2) the owners' values refresh every ghost copy (halo refresh).  The
+ * V-cycle restricts / prolongs with each subdomain's windowed
+ * transfer, sums coarse partials at the owners, and below the partitioned
+ * levels runs an agglomerated multigrid context (mg_setup, identical on every
+ * process) on the sum of all subdomains' restricted residuals.  Collectives
+ * between processes are NCCL point-to-point sends / receives and all-gathers
+ * on the context stream (loaded at run time from the process's libnccl.so.2);
+ * sums over subdomains run in ascending subdomain order, so every process sees
+ * bitwise-identical coarse right-hand sides and norms, and a run emulated on one
+ * GPU reproduces the multi-GPU bits.  Everything a cycle launches (NCCL
+ * included) is captured once as a CUDA graph per argument set. */
+
+typedef struct rav_comm rav_comm;
+
+/* A new NCCL unique id (process 0 calls it; the caller broadcasts the 128
+ * bytes to the other processes, e.g. with torch.distributed). */
+rav_status rav_comm_unique_id(unsigned char id[128]);
+
+/* Communicator of process `proc` of `nprocs` on the current device.  nccl_id =
+ * NULL: no NCCL (only valid for nprocs = 1; every subdomain is local).  With an
+ * id, ncclCommInitRank(nprocs, id, proc) -- collective over the processes; with
+ * nprocs = 1 this gives a one-rank communicator whose self sends / receives can
+ * carry the local exchanges (mgd_setup flag via_comm) to verify the NCCL path on
+ * one GPU.  RAV_ERR_COMM when libnccl.so.2 cannot be loaded or NCCL fails. */
+rav_status rav_comm_create(int nprocs, int proc, const unsigned char* nccl_id, rav_comm** out);
+void rav_comm_destroy(rav_comm* c);
+
+/* One neighbour of a subdomain on one level (host arrays of LOCAL DoF ids of
+ * the subdomain's window, order agreed with the neighbour's lists):
+ * corr_send  ghost-written DoFs owned by `peer` whose partial corrections go to it;
+ * corr_recv  owned DoFs receiving `peer`'s partial corrections (same order as its corr_send);
+ * halo_send  owned DoFs `peer` holds as ghosts (its halo_recv, same order);
+ * halo_recv  ghost DoFs owned by `peer`, refreshed from its halo_send. */
+typedef struct {
+    int32_t peer;                       /* global subdomain id */
+    int64_t n_corr_send, n_corr_recv, n_halo_send, n_halo_recv;
+    const int32_t* corr_send;
+    const int32_t* corr_recv;
+    const int32_t* halo_send;
+    const int32_t* halo_recv;
+} rav_neighbor;
+
+/* One subdomain's share of one partitioned level (copied at setup). */
+typedef struct {
+    rav_csr A;                          /* the subdomain's window of the level operator (rows assembled
+                                           for the DoFs its patches read) */
+    rav_patches P;                      /* its patches (only they write corrections) */
+    int64_t n_vel;                      /* window DoFs < n_vel are velocity */
+    int32_t n_neighbors;
+    const rav_neighbor* neighbors;
+    int64_t n_ghost_written;            /* ghost DoFs its patches write (zeroed before each sweep) */
+    const int32_t* ghost_written;
+    int64_t owned[4];                   /* owned DoFs: [owned[0], owned[1]) and [owned[2], owned[3]) */
+    rav_csr P_coarse;                   /* prolongation from the next level: rows = this window's DoFs
+                                           (owned rows filled), columns = the next partitioned level's
+                                           window of the same subdomain, or -- on the last partitioned
+                                           level -- the agglomerated level's global DoFs */
+    int32_t n_colors;                   /* RAV_VARIANT_MV: colouring of the patches (rav_set_colors */
+    const int64_t* color_offs;          /*   layout; the same colour index on every subdomain) */
+    const int32_t* color_ids;
+} rav_subdomain;
+
+typedef struct mgd_ctx mgd_ctx;
+
+/* Build the partitioned hierarchy: subs[k * n_local + i] = local subdomain i
+ * (global id local_ids[i], ascending) on partitioned level k = 0 (finest) ..
+ * n_levels-1.  coarse: the agglomerated hierarchy below (mg_setup on the whole
+ * grids; caller-owned, must outlive the context; its stream is set to
+ * opts->stream), or NULL for smoothing only (mgd_smooth).  via_comm = 1 routes
+ * the exchanges between local subdomains through the communicator's NCCL
+ * self sends too (verification on one GPU).  Every message size is checked
+ * against the peer's list (RAV_ERR_ARG on a mismatch).  opts as for rav_setup. */
+rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, int n_local,
+                     const int32_t* local_ids, int n_levels, const rav_subdomain* subs, mg_ctx* coarse,
+                     const rav_opts* opts, int via_comm, mgd_ctx** out);
+
+/* nu slab-partitioned sweeps on the finest partitioned level: x[i], b[i] are
+ * device vectors of local subdomain i's window (x in/out; ghost copies are
+ * current on return).  RAV / AV / diagonal Vanka: one interface-correction sum
+ * and one halo refresh per sweep; RAV_VARIANT_MV: per colour (Eq. 11). */
+rav_status mgd_smooth(mgd_ctx* ctx, double* const* x, const double* const* b, int nu, double omega);
+
+/* One distributed V-cycle (x in/out, ghosts current on return). */
+rav_status mgd_vcycle(mgd_ctx* ctx, double* const* x, const double* const* b, int pre, int post, double omega);
+
+/* V-cycles until ||b - L x_k|| <= rtol ||b - L x_0|| over the OWNED DoFs of all
+ * subdomains (R11) or maxit; *iters, hist (host, maxit + 1) as in mg_solve.
+ * Host work per cycle: one graph launch and one 8-byte read of the norm. */
+rav_status mgd_solve(mgd_ctx* ctx, double* const* x, const double* const* b, int pre, int post, double omega,
+                     double rtol, int maxit, int* iters, double* hist);
+
+/* ||b - L x||_2 over the owned DoFs of all subdomains (host result, synchronizes). */
+rav_status mgd_residual_norm(mgd_ctx* ctx, double* const* x, const double* const* b, double* norm);
+
+/* Kernel launches (graph nodes) of the last mgd_* call. */
+int64_t mgd_last_launches(const mgd_ctx* ctx);
+/* Host time of the last mgd_solve: seconds spent enqueueing the cycles (graph launches,
+ * the first call's capture included) and waiting for each cycle's norm, and the cycle count. */
+rav_status mgd_host_time(const mgd_ctx* ctx, double* enqueue_s, double* wait_s, int* cycles);
+rav_status mgd_set_stream(mgd_ctx* ctx, void* stream);
+void mgd_destroy(mgd_ctx* ctx);
 
 /* Colouring of the smoother on level `level` (1 .. n_levels-1) for
  * RAV_VARIANT_MV (same contract as rav_set_colors). */

@@ -20,8 +20,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + INCLUDE, "-Xptxas", "-v"]
 
-SOURCES = ["api.cu", "gen.cu", "linalg.cu", "sell.cu", "nb.cu", "setup.cu", "schur.cu", "sweep.cu", "coarse.cu",
-           "adaptive.cu", "p2p.cu", "xfer.cu", "wave.cu"]
+SOURCES = ["api.cu", "dist.cu", "gen.cu", "linalg.cu", "sell.cu", "nb.cu", "setup.cu", "schur.cu", "sweep.cu", "coarse.cu",
+           "adaptive.cu", "xfer.cu", "wave.cu"]
 
 
 def _deps_mtime() -> float:

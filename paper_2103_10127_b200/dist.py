@@ -499,115 +499,6 @@ class ThreadComm:
         self.sync()
 
 
-class PeerComm:
-    """Peer-memory transport of the point-to-point exchanges (SURVEY section 8 row e):
-    the payload is stored straight into the receiver's buffer (CUDA IPC mapping, peer
-    stores over NVLink between GPUs) and the hand-over is a pair of stream memory
-    operations on 32-bit sequence flags -- the sender's stream waits until the
-    receiver has consumed the slot's previous use, puts, and publishes the sequence
-    number in the receiver's flag; the receiver's stream waits for it, consumes, and
-    hands the slot back.  No host round trip, no spinning kernel, NCCL is not involved.
-    Two slots per channel (a channel = one call site of exchange(), identified by its
-    buffer dictionaries); set up lazily with one host all-gather of IPC handles.
-    all_gather_object / allreduce_sum go to the wrapped TorchComm."""
-
-    def __init__(self, base, rank: int):
-        import torch
-        from . import ravgmg as rg
-        self.base, self.rank, self.rg, self.torch = base, rank, rg, torch
-        self.channels: Dict = {}
-        self._allocs: List = []
-
-    def all_gather_object(self, obj):
-        return self.base.all_gather_object(obj)
-
-    def allreduce_sum(self, buf):
-        self.base.allreduce_sum(buf)
-
-    def _alloc(self, nbytes: int) -> int:
-        import ctypes as C
-        p = C.c_void_p()
-        self.rg._check(self.rg.lib.rav_device_alloc(max(int(nbytes), 8), C.byref(p)))
-        self._allocs.append(p.value)
-        return p.value
-
-    def _export(self, ptr: int) -> bytes:
-        import ctypes as C
-        h = (C.c_ubyte * 64)()
-        self.rg._check(self.rg.lib.rav_ipc_export(C.c_void_p(ptr), h))
-        return bytes(h)
-
-    def _import(self, handle: bytes) -> int:
-        import ctypes as C
-        p = C.c_void_p()
-        buf = (C.c_ubyte * 64).from_buffer_copy(handle)
-        self.rg._check(self.rg.lib.rav_ipc_import(buf, C.byref(p)))
-        return p.value
-
-    def _channel(self, sends: Dict, recvs: Dict):
-        key = (id(sends), id(recvs))
-        ch = self.channels.get(key)
-        if ch is not None:
-            return ch
-        # my side, per peer q I receive from: 2 slots of its message, a ready flag (q writes) and a
-        # free flag for my messages to q (q writes after consuming them)
-        mine = {}
-        for q in set(recvs) | set(sends):
-            n = recvs[q].numel() if q in recvs else 0
-            slots = self._alloc(16 * max(n, 1))
-            flags = self._alloc(64)     # [0] ready (q -> me), [4] free (q consumed my message)
-            mine[q] = {"n": n, "slots": slots, "flags": flags,
-                       "h_slots": self._export(slots), "h_flags": self._export(flags)}
-        table = self.all_gather_object({"rank": self.rank,
-                                        "mine": {q: {k: v for k, v in m.items() if k.startswith("h_") or k == "n"}
-                                                 for q, m in mine.items()}})
-        peer = {}
-        for t in table:
-            q = t["rank"]
-            if q == self.rank or self.rank not in t["mine"]:
-                continue
-            m = t["mine"][self.rank]   # q's buffers for messages from me, q's flags
-            peer[q] = {"n": m["n"], "slots": self._import(m["h_slots"]), "flags": self._import(m["h_flags"])}
-        ch = {"mine": mine, "peer": peer, "seq": 0}
-        self.channels[key] = ch
-        return ch
-
-    def exchange(self, sends: Dict, recvs: Dict):
-        import ctypes as C
-        if not sends and not recvs:
-            return
-        ch = self._channel(sends, recvs)
-        ch["seq"] += 1
-        s = ch["seq"]
-        slot = s % 2
-        st = C.c_void_p(self.torch.cuda.current_stream().cuda_stream)
-        lib = self.rg.lib
-        for q, buf in sorted(sends.items()):
-            pq, mq = ch["peer"][q], ch["mine"][q]
-            n = buf.numel()
-            # the slot's previous message (exchange s - 2) has been consumed by q
-            self.rg._check(lib.rav_stream_wait(st, C.c_void_p(mq["flags"] + 4), max(0, s - 2)))
-            self.rg._check(lib.rav_peer_put(C.c_void_p(buf.data_ptr()), C.c_void_p(pq["slots"] + slot * 8 * n), n, st))
-            self.rg._check(lib.rav_stream_signal(st, C.c_void_p(pq["flags"]), s))          # q's ready flag
-        for q, buf in sorted(recvs.items()):
-            pq, mq = ch["peer"][q], ch["mine"][q]
-            n = buf.numel()
-            self.rg._check(lib.rav_stream_wait(st, C.c_void_p(mq["flags"]), s))          # my ready flag
-            self.rg._check(lib.rav_peer_put(C.c_void_p(mq["slots"] + slot * 8 * n), C.c_void_p(buf.data_ptr()), n, st))
-            self.rg._check(lib.rav_stream_signal(st, C.c_void_p(pq["flags"] + 4), s))    # q's free flag
-
-    def close(self):
-        import ctypes as C
-        self.torch.cuda.synchronize()
-        for ch in self.channels.values():
-            for p in ch["peer"].values():
-                self.rg.lib.rav_ipc_close(C.c_void_p(p["slots"]))
-                self.rg.lib.rav_ipc_close(C.c_void_p(p["flags"]))
-        for a in self._allocs:
-            self.rg.lib.rav_device_free(C.c_void_p(a))
-        self.channels, self._allocs = {}, []
-
-
 def run_threads(nranks: int, fn):
     """fn(rank) on nranks threads; re-raises the first failure."""
     import threading
@@ -730,3 +621,163 @@ def build_gpu_cycle(problem: Dict, n_levels: int, nranks: int, rank: int, comm, 
     cyc.coarse_mg = coarse_mg
     torch.cuda.empty_cache()
     return cyc, levels
+
+
+# ---------------------------------------------------------------------------------------------
+# planning for the library-driven distributed cycle (mgd_* in csrc/dist.cu): this module only
+# computes the partition, the windows and the index lists; every compute step and exchange of
+# the sweep and the V-cycle runs inside the library, captured as CUDA graphs
+# ---------------------------------------------------------------------------------------------
+
+def layer_weights(problem: Dict, weights: str = "pou") -> np.ndarray:
+    """Factor bytes of each vertex layer along the last axis, proportional to sum_i n~_i n_i over
+    the layer's patches (SURVEY section 8 row e: "balance by sum n~_i n_i bytes, not whole
+    layers"): n_i = d prod_k a_k + 1, n~_i = d prod_k t_k + 1 with a_k / t_k the free / restricted
+    Q2 node counts of the patch along axis k (host arithmetic on the structured grid, R2 / R3)."""
+    dim = problem["dim"]
+    nc = [int(c) for c in problem["ncell"][:dim]]
+    per_axis = []
+    for n in nc:
+        v = np.arange(n + 1)
+        lo, hi = np.maximum(2 * v - 2, 1), np.minimum(2 * v + 2, 2 * n - 1)     # free nodes of the patch
+        a = hi - lo + 1
+        if weights == "own":
+            t = ((2 * v >= 1) & (2 * v <= 2 * n - 1)).astype(int) + ((2 * v + 1) <= 2 * n - 1).astype(int)
+        else:
+            rlo, rhi = np.maximum(2 * v - 1, 1), np.minimum(2 * v + 1, 2 * n - 1)
+            t = rhi - rlo + 1
+        if weights == "full":
+            t = a
+        per_axis.append((a, t))
+    # sum over the other axes of (d prod a + 1)(d prod t + 1), per layer of the last axis
+    A = np.ones(1)
+    T = np.ones(1)
+    for a, t in per_axis[:-1]:
+        A = np.outer(A, a).ravel()
+        T = np.outer(T, t).ravel()
+    a_l, t_l = per_axis[-1]
+    n_i = dim * np.outer(A, a_l) + 1
+    nt_i = dim * np.outer(T, t_l) + 1
+    return (n_i * nt_i).sum(axis=0).astype(np.float64)
+
+
+def partition_balanced(problem: Dict, nranks: int, min_layers: int = 3, weights: str = "pou") -> List[Tuple[int, int]]:
+    """Contiguous vertex-layer slabs [V0, V1) of >= min_layers layers minimising the largest slab's
+    factor bytes (layer_weights): bisection on the bottleneck with a greedy feasibility test, then
+    the cuts of the smallest feasible bottleneck (whole layers, so the bound is one layer's weight)."""
+    w = layer_weights(problem, weights)
+    nv = len(w)
+    if nv < nranks * min_layers:
+        raise ValueError(f"{nv} vertex layers cannot give {nranks} slabs of >= {min_layers} layers")
+
+    def cuts_for(cap):
+        cuts, acc, cnt = [0], 0.0, 0
+        for v in range(nv):
+            left_layers = nv - v
+            need = (nranks - len(cuts)) * min_layers       # layers the later slabs still need
+            if cnt >= min_layers and (acc + w[v] > cap or left_layers <= need) and len(cuts) < nranks:
+                cuts.append(v)
+                acc, cnt = 0.0, 0
+            acc += w[v]
+            cnt += 1
+            if acc > cap and cnt > min_layers:
+                return None
+        if len(cuts) != nranks or acc > cap or cnt < min_layers:
+            return None
+        return cuts + [nv]
+
+    lo, hi = float(w.max()), float(w.sum())
+    best = None
+    for _ in range(100):
+        mid = 0.5 * (lo + hi)
+        c = cuts_for(mid)
+        if c is not None:
+            best, hi = c, mid
+        else:
+            lo = mid
+        if hi - lo <= 1e-9 * hi:
+            break
+    if best is None:
+        return partition_layers(nv, nranks, min_layers)
+    return [(best[r], best[r + 1]) for r in range(nranks)]
+
+
+def plan_levels_balanced(problem: Dict, n_levels: int, nranks: int, min_layers: int = 3, agg_layers: int = 0,
+                         weights: str = "pou"):
+    """plan_levels with the finest partition balanced by factor bytes (partition_balanced)."""
+    probs, _ = plan_levels(problem, n_levels, 1, min_layers=1)
+    parts = [partition_balanced(problem, nranks, min_layers, weights)]
+    need = max(min_layers, agg_layers)
+    while len(parts) < n_levels - 1:
+        nxt = nested_layers(parts[-1])
+        if min(b - a for a, b in nxt) < need:
+            break
+        parts.append(nxt)
+    return probs, parts
+
+
+def neighbor_plan(slab: "Slab", written: np.ndarray, all_infos: Sequence[Dict]) -> Dict:
+    """One subdomain's exchange plan for mgd_setup: {peer: (corr_send, corr_recv, halo_send,
+    halo_recv)} local index lists, its ghost-written DoFs and owned ranges (from the exchange_info
+    of every subdomain)."""
+    lists = _exchange_lists(slab, written, all_infos)
+    peers = set(lists["corr_send"]) | set(lists["corr_recv"]) | set(lists["halo_send"]) | set(lists["halo_recv"])
+    e = np.zeros(0, np.int64)
+    nb = {q: (lists["corr_send"].get(q, e), lists["corr_recv"].get(q, e), lists["halo_send"].get(q, e),
+              lists["halo_recv"].get(q, e)) for q in peers}
+    return {"neighbors": nb, "ghost_written": lists["ghost_written"], "owned": slab.owned_ranges()}
+
+
+def build_lib_dist(problem: Dict, n_levels: int, nsub: int, local_ids: Sequence[int], sub_proc: Sequence[int],
+                   comm, gather=None, weights: str = "pou", variant: int = 0, agg_layers: int = 0,
+                   smooth_only: bool = False, via_comm: bool = False, balanced: bool = True, stream=None,
+                   deterministic: bool = False):
+    """One process's share of the library-driven slab-partitioned hierarchy (mgd_setup).
+
+    nsub subdomains in all; this process drives local_ids (global ids, ascending) on its current
+    GPU; sub_proc[g] = process of subdomain g.  gather(obj) -> list over ALL processes of obj (the
+    host all-gather of the exchange plans; None when every subdomain is local).  smooth_only: the
+    finest level alone, no coarse hierarchy (mgd_smooth).  Returns (DistMultigrid, info) with
+    info["b"] / info["x"]: per local subdomain the window's rhs and a zero iterate, and
+    info["slabs"]: per level, per local subdomain, its Slab."""
+    import torch
+    from . import ravgmg as rg
+    if smooth_only:
+        probs = [problem]
+        parts = [partition_balanced(problem, nsub) if balanced else partition_layers(problem["ncell"][problem["dim"] - 1] + 1, nsub)]
+    elif balanced:
+        probs, parts = plan_levels_balanced(problem, n_levels, nsub, agg_layers=agg_layers, weights=weights)
+    else:
+        probs, parts = plan_levels(problem, n_levels, nsub, agg_layers=agg_layers)
+    K = len(parts)
+    coarse = None
+    if not smooth_only:
+        coarse, _ = rg.build_hierarchy(probs[K], n_levels - K, weights, variant=variant, deterministic=deterministic)
+    subs, slabs = [], []
+    for k in range(K):
+        lev_slabs = [Slab(probs[k], nsub, g, parts[k]) for g in local_ids]
+        levels = [rg.gen_level(s.local_problem(), weights) for s in lev_slabs]
+        written = [written_local_from_patches(L) for L in levels]
+        infos = [exchange_info(s, w) for s, w in zip(lev_slabs, written)]
+        if gather is not None:
+            infos = [i for part in gather(infos) for i in part]
+        row = []
+        for s, L, w in zip(lev_slabs, levels, written):
+            d = neighbor_plan(s, w, infos)
+            d.update({"level": L, "prol": None, "colors": local_colors(s) if variant == 2 else None})
+            row.append(d)
+        subs.append(row)
+        slabs.append(lev_slabs)
+    if not smooth_only:
+        for k in range(K):
+            for i, g in enumerate(local_ids):
+                fine = dict(probs[k], window=slabs[k][i].transfer_window())
+                crs = dict(probs[k + 1], window=dict(slabs[k + 1][i].window)) if k + 1 < K else probs[K]
+                subs[k][i]["prol"] = rg.gen_prolongation(fine, crs)
+    mgd = rg.DistMultigrid(comm, sub_proc, local_ids, subs, coarse=coarse, variant=variant, stream=stream,
+                           via_comm=via_comm, deterministic=deterministic)
+    mgd._keep = (subs, coarse)
+    info = {"b": [d["level"]["b"] for d in subs[0]],
+            "x": [torch.zeros(d["level"]["n"], dtype=torch.float64, device="cuda") for d in subs[0]],
+            "slabs": slabs, "parts": parts, "K": K}
+    return mgd, info

@@ -61,6 +61,19 @@ class RavPatches(C.Structure):
                 ("weight", C.c_void_p), ("on_device", C.c_int32)]
 
 
+class RavNeighbor(C.Structure):
+    _fields_ = [("peer", C.c_int32), ("n_corr_send", C.c_int64), ("n_corr_recv", C.c_int64),
+                ("n_halo_send", C.c_int64), ("n_halo_recv", C.c_int64), ("corr_send", C.c_void_p),
+                ("corr_recv", C.c_void_p), ("halo_send", C.c_void_p), ("halo_recv", C.c_void_p)]
+
+
+class RavSubdomain(C.Structure):
+    _fields_ = [("A", RavCsr), ("P", RavPatches), ("n_vel", C.c_int64), ("n_neighbors", C.c_int32),
+                ("neighbors", C.c_void_p), ("n_ghost_written", C.c_int64), ("ghost_written", C.c_void_p),
+                ("owned", C.c_int64 * 4), ("P_coarse", RavCsr), ("n_colors", C.c_int32),
+                ("color_offs", C.c_void_p), ("color_ids", C.c_void_p)]
+
+
 class RavOpts(C.Structure):
     _fields_ = [("variant", C.c_int32), ("kernel", C.c_int32), ("deterministic", C.c_int32),
                 ("n_vel", C.c_int64), ("stream", C.c_void_p), ("block_dim", C.c_int32)]
@@ -106,15 +119,16 @@ def _load():
         "mg_fgmres": [vp, vp, vp, C.c_int, C.c_int, dbl, C.c_int, dbl, C.c_int, P(C.c_int), vp],
         "rav_adaptive_create": [P(RavAdaptiveDesc), P(vp)],
         "rav_color_patches": [P(RavCsr), P(RavPatches), P(i64), vp, vp],
-        "rav_device_alloc": [i64, P(vp)],
-        "rav_device_free": [vp],
-        "rav_ipc_export": [vp, vp],
-        "rav_ipc_import": [vp, P(vp)],
-        "rav_ipc_close": [vp],
-        "rav_stream_wait": [vp, vp, C.c_uint32],
-        "rav_stream_signal": [vp, vp, C.c_uint32],
-        "rav_peer_put": [vp, vp, i64, vp],
         "rav_gen_colors": [P(RavGrid), vp, vp],
+        "rav_comm_unique_id": [vp],
+        "rav_comm_create": [C.c_int, C.c_int, vp, P(vp)],
+        "mgd_setup": [vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, P(RavOpts), C.c_int, P(vp)],
+        "mgd_smooth": [vp, vp, vp, C.c_int, dbl],
+        "mgd_vcycle": [vp, vp, vp, C.c_int, C.c_int, dbl],
+        "mgd_solve": [vp, vp, vp, C.c_int, C.c_int, dbl, dbl, C.c_int, P(C.c_int), vp],
+        "mgd_residual_norm": [vp, vp, vp, P(dbl)],
+        "mgd_set_stream": [vp, vp],
+        "mgd_host_time": [vp, P(dbl), P(dbl), P(C.c_int)],
         "rav_pressure_normalize": [vp, i64, i64, C.c_int, i64, vp],
         "mg_normalize_pressure": [vp, vp, C.c_int],
         "rav_adaptive_sizes": [vp, C.c_int, P(i64), P(i64), P(i64), P(i64), P(i64), P(i64), P(i64)],
@@ -140,6 +154,12 @@ def _load():
     L.rav_last_launches.restype = i64
     L.mg_last_launches.argtypes = [vp]
     L.mg_last_launches.restype = i64
+    L.mgd_last_launches.argtypes = [vp]
+    L.mgd_last_launches.restype = i64
+    L.mgd_destroy.argtypes = [vp]
+    L.mgd_destroy.restype = None
+    L.rav_comm_destroy.argtypes = [vp]
+    L.rav_comm_destroy.restype = None
     return L
 
 
@@ -594,3 +614,150 @@ def build_adaptive_hierarchy(problem: Dict, n_levels: int, weights: str = "own",
             mg.set_colors(l, *color_patches(levels[l], levels[l]))
     fine = {k: v for k, v in levels[-1].items() if k in ("n", "nvel", "nnz", "b", "problem", "n_cells")}
     return mg, fine
+
+
+# ---------------------------------------------------------------------------------------------
+# slab-partitioned smoother / V-cycle in the library (mgd_*; include/ravgmg.h)
+# ---------------------------------------------------------------------------------------------
+
+class Comm:
+    """rav_comm_create: the library's communicator (NCCL between processes, loaded at run time).
+    nccl_id: 128 bytes from unique_id() on process 0, broadcast by the caller; None = no NCCL
+    (one process, every subdomain local)."""
+
+    def __init__(self, nprocs: int = 1, proc: int = 0, nccl_id: Optional[bytes] = None):
+        h = C.c_void_p()
+        idb = None if nccl_id is None else (C.c_ubyte * 128).from_buffer_copy(nccl_id)
+        _check(lib.rav_comm_create(int(nprocs), int(proc), idb, C.byref(h)))
+        self.ctx, self.nprocs, self.proc = h, nprocs, proc
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        _check(lib.rav_comm_unique_id(buf))
+        return bytes(buf)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib.rav_comm_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64).astype(np.int32))
+
+
+class DistMultigrid:
+    """mgd_setup / mgd_smooth / mgd_vcycle / mgd_solve.  subs[k][i]: dict of partitioned level k,
+    local subdomain i with keys level (gen_level dict of the window), neighbors {peer: (corr_send,
+    corr_recv, halo_send, halo_recv)}, ghost_written, owned (2 ranges), prol (gen_prolongation dict
+    or None), colors ((offs, ids) or None).  Argument marshalling only."""
+
+    def __init__(self, comm: "Comm", sub_proc: Sequence[int], local_ids: Sequence[int], subs, coarse=None,
+                 variant: int = VARIANT_ROWS, kernel: int = KERNEL_AUTO, stream=None, via_comm: bool = False,
+                 deterministic: bool = False):
+        K, nl = len(subs), len(local_ids)
+        keep = []
+        arr = (RavSubdomain * (K * nl))()
+        for k in range(K):
+            for i in range(nl):
+                d = subs[k][i]
+                L = d["level"]
+                sd = arr[k * nl + i]
+                sd.A = csr(L)
+                sd.P = patches_struct(L)
+                sd.n_vel = int(L["nvel"])
+                peers = sorted(d["neighbors"])
+                nbs = (RavNeighbor * max(1, len(peers)))()
+                for j, q in enumerate(peers):
+                    lists = [_i32(v) for v in d["neighbors"][q]]
+                    keep.append(lists)
+                    nb = nbs[j]
+                    nb.peer = int(q)
+                    nb.n_corr_send, nb.n_corr_recv, nb.n_halo_send, nb.n_halo_recv = [len(v) for v in lists]
+                    nb.corr_send, nb.corr_recv, nb.halo_send, nb.halo_recv = [v.ctypes.data for v in lists]
+                keep.append(nbs)
+                sd.n_neighbors = len(peers)
+                sd.neighbors = C.cast(nbs, C.c_void_p)
+                gw = _i32(d["ghost_written"])
+                keep.append(gw)
+                sd.n_ghost_written = len(gw)
+                sd.ghost_written = gw.ctypes.data
+                (a0, b0), (a1, b1) = d["owned"]
+                sd.owned[0], sd.owned[1], sd.owned[2], sd.owned[3] = int(a0), int(b0), int(a1), int(b1)
+                if d.get("prol") is not None:
+                    sd.P_coarse = csr(d["prol"], n_cols=d["prol"]["nc"])
+                if d.get("colors") is not None:
+                    offs = np.ascontiguousarray(d["colors"][0], dtype=np.int64)
+                    ids = np.ascontiguousarray(d["colors"][1], dtype=np.int32)
+                    keep.append((offs, ids))
+                    sd.n_colors = len(offs) - 1
+                    sd.color_offs, sd.color_ids = offs.ctypes.data, ids.ctypes.data
+        sp = _i32(sub_proc)
+        li = _i32(local_ids)
+        dim = subs[0][0]["level"]["problem"]["dim"] if "problem" in subs[0][0]["level"] else 0
+        opts = RavOpts(variant, kernel, int(bool(deterministic)), 0, _stream(stream), int(dim))
+        h = C.c_void_p()
+        _check(lib.mgd_setup(comm.ctx, len(sp), sp.ctypes.data, nl, li.ctypes.data, K, arr,
+                             coarse.ctx if coarse is not None else None, C.byref(opts), int(bool(via_comm)),
+                             C.byref(h)))
+        self.ctx, self.nl, self.comm, self.coarse = h, nl, comm, coarse
+
+    def _vecs(self, xs, bs):
+        X = (C.c_void_p * self.nl)(*[_ptr(x) for x in xs])
+        B = (C.c_void_p * self.nl)(*[_ptr(b) for b in bs])
+        return X, B
+
+    def smooth(self, xs, bs, nu: int, omega: float):
+        X, B = self._vecs(xs, bs)
+        _check(lib.mgd_smooth(self.ctx, X, B, int(nu), float(omega)))
+        return xs
+
+    def vcycle(self, xs, bs, pre=2, post=2, omega=0.66):
+        X, B = self._vecs(xs, bs)
+        _check(lib.mgd_vcycle(self.ctx, X, B, int(pre), int(post), float(omega)))
+        return xs
+
+    def solve(self, xs, bs, pre=2, post=2, omega=0.66, rtol=1e-8, maxit=200):
+        X, B = self._vecs(xs, bs)
+        hist = np.zeros(maxit + 1)
+        it = C.c_int(0)
+        _check(lib.mgd_solve(self.ctx, X, B, int(pre), int(post), float(omega), float(rtol), int(maxit), C.byref(it),
+                             hist.ctypes.data))
+        return xs, it.value, hist[:it.value + 1]
+
+    def residual_norm(self, xs, bs) -> float:
+        X, B = self._vecs(xs, bs)
+        out = C.c_double()
+        _check(lib.mgd_residual_norm(self.ctx, X, B, C.byref(out)))
+        return out.value
+
+    def set_stream(self, stream):
+        _check(lib.mgd_set_stream(self.ctx, _stream(stream)))
+
+    def host_time(self):
+        """(enqueue seconds, wait seconds, cycles) of the last solve (mgd_host_time)."""
+        a, b, c = C.c_double(), C.c_double(), C.c_int()
+        _check(lib.mgd_host_time(self.ctx, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    @property
+    def last_launches(self) -> int:
+        return int(lib.mgd_last_launches(self.ctx))
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib.mgd_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

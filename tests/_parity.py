@@ -94,3 +94,11 @@ class SweepChecker:
             assert_entrywise(xg, xo, scale, what=f"{what} after {t} sweeps")
             worst = max(worst, float(np.max(np.abs(xg - xo) / (TOL * np.asarray(scale) + 1e-300))))
         return xo, worst
+
+
+def iterate_tol(ncell_per_axis: int) -> float:
+    """Entry-wise bar for a converged V-cycle iterate relative to max |x|: the two paths follow the
+    same cycles and differ by rounding of each cycle's residual, ~eps |L| |x|, which the solve maps
+    to ~eps cond(L) |x| in x; cond(L) grows like h^-2 = N^2 for the Stokes operator (N cells per
+    axis).  20 eps N^2, at least 1e-10 (the coarse-grid cases)."""
+    return max(1e-10, 20 * 2.22e-16 * float(ncell_per_axis) ** 2)

@@ -426,3 +426,59 @@ def test_distributed_comparison_smoothers_match_oracle(case):
         xd[g] = v
     assert not np.isnan(xd).any()
     assert np.linalg.norm(xd - xo) <= 1e-12 * np.linalg.norm(xo)
+
+
+def _lib_plan_worker(rank, world, port, nsub, q):
+    """Planning of the library-driven cycle (dist.neighbor_plan) across processes: 2 processes
+    driving nsub // 2 subdomains each, exchange_info all-gathered over gloo."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        prob = si.problem(2, (20, 26), si.KIND_MMS, eta="fourier")
+        P = oracle.patches(prob, "pou")
+        per = nsub // world
+        local = list(range(rank * per, (rank + 1) * per))
+        parts = rdist.partition_balanced(prob, nsub)
+        slabs = [rdist.Slab(prob, nsub, g, parts) for g in local]
+        written = []
+        for s in slabs:
+            gids = s.global_ids()
+            g2l = -np.ones(int(gids.max()) + 1 + 10 ** 7, np.int64)
+            g2l[gids] = np.arange(len(gids))
+            p0, p1 = s.nlow_vert * s.V0, s.nlow_vert * s.V1
+            wr = [g2l[P["dofs"][P["offs"][i]:P["offs"][i + 1]][P["w"][P["offs"][i]:P["offs"][i + 1]] > 0]]
+                  for i in range(p0, p1)]
+            written.append(np.unique(np.concatenate(wr)))
+        infos = [rdist.exchange_info(s, w) for s, w in zip(slabs, written)]
+        out = [None] * world
+        dist.all_gather_object(out, infos)
+        infos_all = [i for part in out for i in part]
+        plans = {g: rdist.neighbor_plan(s, w, infos_all) for g, s, w in zip(local, slabs, written)}
+        sizes = {g: {p: tuple(len(v) for v in lists) for p, lists in pl["neighbors"].items()} for g, pl in plans.items()}
+        allsizes = [None] * world
+        dist.all_gather_object(allsizes, sizes)
+        q.put((rank, {k: v for d in allsizes for k, v in d.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nsub", [2, 4])
+def test_lib_plan_lists_match_across_processes(nsub):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lib_plan_worker, args=(r, 2, port, nsub, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sizes = res[0]
+    assert res[0] == res[1] and sorted(sizes) == list(range(nsub))
+    for g, nbs in sizes.items():
+        for p, (cs, cr, hs, hr) in nbs.items():
+            pcs, pcr, phs, phr = sizes[p][g]      # the peer's lists for me
+            assert (cs, cr, hs, hr) == (pcr, pcs, phr, phs), (g, p)
+            assert cs + cr > 0 and hs + hr > 0
