@@ -21,7 +21,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-I" + INCLUDE, "-Xptxas", "-v"]
 
 SOURCES = ["api.cu", "dist.cu", "gen.cu", "linalg.cu", "sell.cu", "nb.cu", "setup.cu", "schur.cu", "sweep.cu", "coarse.cu",
-           "adaptive.cu", "xfer.cu", "wave.cu"]
+           "adaptive.cu", "xfer.cu"]
 
 
 def _deps_mtime() -> float:

@@ -57,18 +57,6 @@ namespace rav {
 // first sweep's residual is b itself and is read from b instead of being computed
 rav_status smooth_launches(rav_ctx* c, double* x, const double* b, int nu, double omega, bool r_ready,
                            bool x_zero) {
-    static const bool wave_use = [] {   // RAV_WAVE_USE=0: keep the wave layout, run the plain chain
-        const char* e = getenv("RAV_WAVE_USE");
-        return !(e && atoi(e) == 0);
-    }();
-    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
-    if (wave_use && aligned && c->wave.on && c->variant != RAV_VARIANT_MV && nu > 0) {
-        if (x_zero && !r_ready) {
-            RAV_CUDA(cudaMemcpyAsync(c->r, b, sizeof(double) * c->A.n_rows, cudaMemcpyDeviceToDevice, c->stream));
-            r_ready = true;
-        }
-        return wave_smooth(c->A, c->F, c->P.n_patches, c->wave, x, b, c->r, nu, omega, r_ready, c->stream);
-    }
     for (int k = 0; k < nu; ++k) {
         if (c->variant == RAV_VARIANT_MV) {   // colour by colour, fresh local residuals (Eq. 11, 15)
             for (size_t q = 0; q + 1 < c->coffs.size(); ++q)
@@ -146,12 +134,6 @@ rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opt
         cudaError_t e = cudaMalloc(&c->r, sizeof(double) * std::max<int64_t>(1, c->A.n_rows));
         if (e != cudaSuccess) { set_error("rav_setup: %s", cudaGetErrorString(e)); st = RAV_ERR_OOM; }
     }
-    static const bool wave_env = [] {
-        const char* e = getenv("RAV_WAVE");
-        return e && atoi(e) == 1;
-    }();
-    if (st == RAV_OK && wave_env && o.variant != RAV_VARIANT_MV && c->A.nb.nslices > 0)
-        st = wave_build(c->A, c->F, c->P.n_patches, nb_lanes_of(c->A.nb), c->wave, c->stream);
     if (st != RAV_OK) { rav_destroy(c); return st; }
     *out = c;
     return RAV_OK;
@@ -320,7 +302,6 @@ void rav_destroy(rav_ctx* c) {
     csr_free(c->A);
     patches_free(c->P);
     factors_free(c->F);
-    wave_free(c->wave);
     if (c->r) cudaFree(c->r);
     if (c->hx) cudaFree(c->hx);
     if (c->hb) cudaFree(c->hb);

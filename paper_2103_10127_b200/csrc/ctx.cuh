@@ -51,7 +51,6 @@ struct rav_ctx {
     // multicoloured MV (RAV_VARIANT_MV): colour c = patches plist[coffs[c] .. coffs[c+1])
     std::vector<int64_t> coffs;
     int32_t* plist = nullptr;
-    Wave wave;                  // band-pipelined sweeps (RAV_WAVE=1, wave.cu)
 };
 
 struct mg_level {

@@ -191,23 +191,6 @@ rav_status launch_xs_prolong(const XStruct& S, const double* xc, double* yf, dou
                              cudaStream_t s);
 rav_status launch_xs_restrict(const XStruct& S, const double* rf, double* bc, cudaStream_t s);
 
-// ---- wave.cu: band-pipelined sweeps (RAV_WAVE=1) ---------------------------------------------
-struct Wave {
-    int on = 0;
-    int nA = 0, nR = 0;              // A-bands (sweep chunk groups), R-bands (residual CTA groups)
-    int64_t nres = 0, nsw = 0;       // residual / sweep CTAs
-    int maxA = 0, maxR = 0;          // widest dependency ranges (diagnostics)
-    int32_t *alo = nullptr, *ahi = nullptr;   // per residual CTA: A-bands it waits for
-    int32_t *rlo = nullptr, *rhi = nullptr;   // per A-band: R-bands it waits for
-    int32_t *cntA = nullptr, *cntR = nullptr; // CTAs per band
-    unsigned* done = nullptr;                 // nA + nR completion counters
-};
-int nb_lanes_of(const NodeBlocked& N);
-rav_status wave_build(const Csr& A, const Factors& F, int64_t n_patches, int nb_lanes_used, Wave& V, cudaStream_t s);
-void wave_free(Wave& V);
-rav_status wave_smooth(const Csr& A, const Factors& F, int64_t n_patches, const Wave& V, double* x, const double* b,
-                       double* r, int nu, double omega, bool r_ready, cudaStream_t s);
-
 struct CoarseLU {
     int64_t n = 0, pin = -1;
     int m = 0;

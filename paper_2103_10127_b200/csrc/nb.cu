@@ -78,26 +78,15 @@ __global__ void nb_count_kernel(int64_t nnodes, int64_t npres, int D, int64_t nv
     }
 }
 
-__global__ void nb_key_kernel(int64_t n, const int32_t* na, const int32_t* nb, int D, const int32_t* order,
+__global__ void nb_key_kernel(int64_t n, const int32_t* na, const int32_t* nb, int D,
                               int32_t* key, int32_t* idx) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t br = order ? order[t] : (int32_t)t;
+        const int32_t br = (int32_t)t;
         key[t] = na[br] * 12 + nb[br] * (4 + 8 * D);   // bytes of the block row
         idx[t] = br;
     }
 }
 
-// spatial key of a block row (RAV_WAVE): node rows their node index, pressure rows the node index
-// of their first velocity column -- so the windows hold the node and pressure rows of one strip
-__global__ void nb_spatial_kernel(int64_t nnodes, int64_t npres, int D, int64_t nvel, const int64_t* rp,
-                                  const int32_t* ci, int32_t* key, int32_t* idx) {
-    const int64_t total = nnodes + npres;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = t < nnodes ? t * D : nvel + (t - nnodes);
-        key[t] = t < nnodes ? (int32_t)t : (rp[row + 1] > rp[row] ? ci[rp[row]] / D : 0);
-        idx[t] = (int32_t)t;
-    }
-}
 
 __global__ void nb_windows_kernel(int64_t n, int64_t nw, int64_t* off) {
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w <= nw; w += (int64_t)gridDim.x * blockDim.x)
@@ -650,30 +639,8 @@ rav_status nb_build(Csr& A, int64_t nvel, int D, cudaStream_t s) {
     RAV_CUDA(cudaMallocAsync(&woff, sizeof(int64_t) * (nw + 1), s));
     RAV_CUDA(cudaMalloc(&N.perm, sizeof(int32_t) * N.nslices * NB_C));
     RAV_CUDA(cudaMemsetAsync(N.perm, 0, sizeof(int32_t) * N.nslices * NB_C, s));
-    static const bool spatial = [] {   // the band-pipelined sweeps (wave.cu) want strips of rows per window
-        const char* e = getenv("RAV_WAVE");
-        const char* f = getenv("RAV_WAVE_SPATIAL");
-        return e && atoi(e) == 1 && f && atoi(f) == 1;   // measured: residual 78.3 -> 86.2 us at c2, off
-    }();
-    int32_t* order = nullptr;
-    if (spatial) {
-        int32_t *skey = nullptr, *sidx = nullptr, *okey = nullptr;
-        RAV_CUDA(cudaMallocAsync(&skey, sizeof(int32_t) * n, s));
-        RAV_CUDA(cudaMallocAsync(&sidx, sizeof(int32_t) * n, s));
-        RAV_CUDA(cudaMallocAsync(&okey, sizeof(int32_t) * n, s));
-        RAV_CUDA(cudaMallocAsync(&order, sizeof(int32_t) * n, s));
-        nb_spatial_kernel<<<nb1, 256, 0, s>>>(nnodes, npres, D, nvel, A.rp, A.ci, skey, sidx);
-        count_launch();
-        size_t t0 = 0;
-        RAV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t0, skey, okey, sidx, order, (int)n, 0, 32, s));
-        void* d_t0 = nullptr;
-        RAV_CUDA(cudaMallocAsync(&d_t0, t0 + 16, s));
-        RAV_CUDA(cub::DeviceRadixSort::SortPairs(d_t0, t0, skey, okey, sidx, order, (int)n, 0, 32, s));
-        for (void* p : {(void*)skey, (void*)sidx, (void*)okey, d_t0}) cudaFreeAsync(p, s);
-    }
-    nb_key_kernel<<<nb1, 256, 0, s>>>(n, na, nbv, D, order, key, idx);
+    nb_key_kernel<<<nb1, 256, 0, s>>>(n, na, nbv, D, key, idx);
     count_launch();
-    if (order) cudaFreeAsync(order, s);
     nb_windows_kernel<<<(int)std::max<int64_t>(1, cdiv(nw + 1, 256)), 256, 0, s>>>(n, nw, woff);
     count_launch();
     RAV_CHECK_LAUNCH();
@@ -788,7 +755,6 @@ static int nb_lanes(const NodeBlocked& N) {
     return G >= 32 ? 32 : (G >= 8 ? 8 : (G >= 4 ? 4 : (G >= 2 ? 2 : 1)));
 }
 
-int nb_lanes_of(const NodeBlocked& N) { return nb_lanes(N); }
 
 int64_t nb_full_blocks(const NodeBlocked& N) { return cdiv(N.nslices * NB_C * nb_lanes(N), nb_block_threads()); }
 

@@ -555,8 +555,8 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
 // instead of atomics; det_gather_kernel adds them to x in ascending patch order (rav_opts.deterministic)
 // NDP: node indices from (nbase[i], pattern table ntbl[npid[i] * NN + j]) instead of the ND array
 // RA: r is 16-byte aligned (checked at launch): node gathers without the per-load alignment test
-template <int MT, int D, int MINB, int NRB = 0, bool DET = false, bool NDP = false, bool RA = false>   // NRB > 0: compile-time rect pairs
-__global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
+template <int MT, int D, int NRB = 0, bool DET = false, bool NDP = false, bool RA = false>   // NRB > 0: compile-time rect pairs
+__global__ void __launch_bounds__(128, 4) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
                                                                  const double2* __restrict__ W,
                                                                  const int32_t* __restrict__ ND,
                                                                  const int32_t* __restrict__ npid,
@@ -567,19 +567,15 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
                                                                  const double* __restrict__ AUX,
                                                                  const double* __restrict__ r,
                                                                  double* __restrict__ x, double omega,
-                                                                 double* __restrict__ cbuf, int64_t chunk0, int half,
-                                                                 int pf, int64_t tail0) {
+                                                                 double* __restrict__ cbuf, int pf) {
     constexpr int TRI = MT * (MT + 1) / 2 + MT * D;
     constexpr int TRI_PAD = TRI + (TRI & 1);
     constexpr int RC = MT + D;   // entries per rectangular column
-    // half = 0: warp w -> chunk chunk0 + w; half = 1 (the last, partial wave): two warps per chunk,
-    // 16 active lanes each -- the tail's patches spread over twice as many warps
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t chunk = chunk0 + (half ? gw >> 1 : gw);
-    const int lane = half ? (int)((gw & 1) << 4) + (threadIdx.x & 15) : (threadIdx.x & 31);
+    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;   // warp -> chunk
+    const int lane = threadIdx.x & 31;
     const int64_t i = chunk * 32 + lane;
     pdl_trigger();
-    if (chunk >= nchunks || (half && (threadIdx.x & 31) >= 16)) return;
+    if (chunk >= nchunks) return;
     const double2* wp = W + chunk * pairs * 32 + lane;
     const int32_t* np_ = NDP ? nullptr : ND + chunk * (int64_t)NN * 32 + lane;
     const int32_t* ntp = NDP ? ntbl + (int64_t)npid[i] * NN : nullptr;   // L1-resident pattern row
@@ -593,11 +589,9 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
         }
         const int lines = (int)(pairs * 4 < 128 ? pairs * 4 : 128);
         for (int ln = lane; ln < lines; ln += 32) prefetch_l2(wc + (size_t)ln * 128);
-        // NRB > 0: the first pf rectangular blocks by one bulk prefetch (the rest rolls inside the loop);
-        // chunks of the last partial wave (chunk >= tail0, L2 no longer shared with full waves): all of them
-        if (NRB > 0 && pf > 0 && !half && lane == 0)
-            bulk_prefetch_l2(wc + (size_t)(TRI_PAD / 2) * 512, (uint32_t)((chunk >= tail0 ? NRB : min(pf, NRB)) * RC * 512));
-        if (chunk >= tail0) pf = 0;
+        // NRB > 0: the first pf rectangular blocks by one bulk prefetch (the rest rolls inside the loop)
+        if (NRB > 0 && pf > 0 && lane == 0)
+            bulk_prefetch_l2(wc + (size_t)(TRI_PAD / 2) * 512, (uint32_t)(min(pf, NRB) * RC * 512));
     }
     pdl_wait();
     auto ldr = [&](const double* p, double* out) {
@@ -609,11 +603,7 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
             ld_node<D>(p, out);
         }
     };
-    // MINB > 4: g_R lives in shared memory (one column per thread, conflict-free), which frees 2 MT D
-    // registers for a higher residency
-    constexpr bool SG = MINB > 4;
-    __shared__ double sgR[SG ? MT * D : 1][SG ? 128 : 1];
-    double acc[MT][D], rr[MT][D], gR[SG ? 1 : MT][SG ? 1 : D];
+    double acc[MT][D], rr[MT][D], gR[MT][D];
     double gacc = 0.0;
 #pragma unroll
     for (int k = 0; k < MT; ++k) {
@@ -641,8 +631,7 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
                 }
             } else {
                 const int c = q - j - 1;
-                if constexpr (SG) sgR[j * D + c][threadIdx.x] = v;
-                else gR[j][c] = v;
+                gR[j][c] = v;
                 gacc = fma(v, rr[j][c], gacc);
             }
         }
@@ -654,7 +643,7 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
     for (int b = 0; b < (NRB > 0 ? NRB : 1 << 20); ++b) {
         if (NRB == 0 && b >= nrb) break;
         const int j0 = MT + 2 * b;
-        if (NRB > 0 && pf > 0 && !half && lane == 0 && b + pf < NRB)   // rolling: block b + pf into L2
+        if (NRB > 0 && pf > 0 && lane == 0 && b + pf < NRB)   // rolling: block b + pf into L2
             bulk_prefetch_l2(W + chunk * pairs * 32 + (int64_t)(TRI_PAD / 2 + (b + pf) * RC) * 32, (uint32_t)(RC * 512));
         double ra[D], rb[D];
         const int n0 = ND_AT(j0), n1 = ND_AT(j0 + 1);
@@ -692,7 +681,7 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
             const int nd = ND_AT(k);
 #pragma unroll
             for (int c = 0; c < D; ++c) {
-                const double gk = SG ? sgR[k * D + c][threadIdx.x] : gR[SG ? 0 : k][SG ? 0 : c];
+                const double gk = gR[k][c];
                 const double v = wk * fma(gk, t, acc[k][c]);
                 if (DET) cb[k * D + c] = v;
                 else atomicAdd(x + nd + c, v);
@@ -707,148 +696,6 @@ __global__ void __launch_bounds__(128, MINB) schur_sweep_thread_kernel(int64_t n
 }
 
 #undef ND_AT
-
-// 2D PoU interior shape, one chunk (32 patches, one per lane) per CTA of 4 warps that split the
-// chunk's factor bytes: warp 0 reads the triangular block (+ g) and warps 1-3 the rectangular
-// column pairs (blocks [ (w-1) B1, min(NRB, w B1) )).  The rectangular partial sums meet in
-// shared memory; warp 0 adds them in fixed order (w = 1, 2, 3: deterministic) and scatters.  A
-// chunk then takes about a quarter of the time it takes one warp, so the partial last wave of
-// a small grid (c2: 3.5 waves of one-warp chunks) is a quarter as long.
-template <int MT, int D, int NRB, bool DET>
-__global__ void __launch_bounds__(128, 4) schur_sweep_cta4_kernel(int64_t np, int64_t nchunks, int64_t pairs,
-                                                                  const double2* __restrict__ W,
-                                                                  const int32_t* __restrict__ ND,
-                                                                  const int32_t* __restrict__ PD,
-                                                                  const int32_t* __restrict__ NR,
-                                                                  const double* __restrict__ AUX,
-                                                                  const double* __restrict__ r,
-                                                                  double* __restrict__ x, double omega,
-                                                                  double* __restrict__ cbuf) {
-    constexpr int TRI = MT * (MT + 1) / 2 + MT * D;
-    constexpr int TRI_PAD = TRI + (TRI & 1);
-    constexpr int RC = MT + D;
-    constexpr int NN = MT + 2 * NRB;
-    constexpr int B1 = (NRB + 2) / 3;
-    __shared__ double part[3][MT * D + 1][32];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t chunk = blockIdx.x;
-    const int64_t i = chunk * 32 + lane;
-    pdl_trigger();
-    const double2* wc = W + chunk * pairs * 32;
-    const int32_t* np_ = ND + chunk * (int64_t)NN * 32 + lane;
-    const int b0 = warp == 0 ? 0 : (warp - 1) * B1;
-    const int b1 = warp == 0 ? 0 : min(NRB, warp * B1);
-    {   // before r exists: this warp's factor segment (one bulk prefetch) and the node-index lines
-        if (lane == 0) {
-            if (warp == 0) bulk_prefetch_l2(wc, (uint32_t)(TRI_PAD / 2 * 512));
-            else if (b1 > b0) bulk_prefetch_l2(wc + (int64_t)(TRI_PAD / 2 + b0 * RC) * 32, (uint32_t)((b1 - b0) * RC * 512));
-        }
-        if (warp == 0 && lane < NN) prefetch_l2(ND + (chunk * (int64_t)NN + lane) * 32);
-    }
-    pdl_wait();
-    double acc[MT][D], gR[MT][D];
-    double gacc = 0.0;
-#pragma unroll
-    for (int k = 0; k < MT; ++k)
-#pragma unroll
-        for (int c = 0; c < D; ++c) { acc[k][c] = 0.0; gR[k][c] = 0.0; }
-    if (warp == 0) {   // triangular block of the restricted rows of A_s^{-1}, and g_R (as the thread kernel)
-        const double2* wp = wc + lane;
-        double rr[MT][D];
-#pragma unroll
-        for (int k = 0; k < MT; ++k) ld_node<D>(r + __ldcs(np_ + k * 32), rr[k]);
-        double2 pv = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int j = 0; j < MT; ++j) {
-#pragma unroll
-            for (int q = 0; q <= j + D; ++q) {
-                const int e = j * (j + 1) / 2 + j * D + q;
-                if ((e & 1) == 0) pv = __ldcs(wp + (e >> 1) * 32);
-                const double v = (e & 1) ? pv.y : pv.x;
-                if (q <= j) {
-#pragma unroll
-                    for (int c = 0; c < D; ++c) {
-                        acc[q][c] = fma(v, rr[j][c], acc[q][c]);
-                        if (q != j) acc[j][c] = fma(v, rr[q][c], acc[j][c]);
-                    }
-                } else {
-                    const int c = q - j - 1;
-                    gR[j][c] = v;
-                    gacc = fma(v, rr[j][c], gacc);
-                }
-            }
-        }
-    } else {           // rectangular column pairs b0 .. b1-1
-        const double2* wq0 = wc + (TRI_PAD / 2) * 32 + lane;
-#pragma unroll
-        for (int bb = 0; bb < B1; ++bb) {
-            const int b = b0 + bb;
-            if (b < b1) {
-                const int j0 = MT + 2 * b;
-                double ra[D], rb[D];
-                ld_node<D>(r + __ldcs(np_ + j0 * 32), ra);
-                ld_node<D>(r + __ldcs(np_ + (j0 + 1) * 32), rb);
-                const double2* wq = wq0 + (int64_t)b * RC * 32;
-#pragma unroll
-                for (int p = 0; p < RC; ++p) {
-                    const double2 v2 = __ldcs(wq + p * 32);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int e = 2 * p + h;
-                        const double v = h ? v2.y : v2.x;
-                        const bool second = e >= RC;
-                        const int q = second ? e - RC : e;
-                        if (q < MT) {
-#pragma unroll
-                            for (int c = 0; c < D; ++c) acc[q][c] = fma(v, second ? rb[c] : ra[c], acc[q][c]);
-                        } else {
-                            gacc = fma(v, second ? rb[q - MT] : ra[q - MT], gacc);
-                        }
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < MT; ++k)
-#pragma unroll
-            for (int c = 0; c < D; ++c) part[warp - 1][k * D + c][lane] = acc[k][c];
-        part[warp - 1][MT * D][lane] = gacc;
-    }
-    __syncthreads();
-    if (warp != 0) return;
-#pragma unroll
-    for (int w = 0; w < 3; ++w) {
-#pragma unroll
-        for (int k = 0; k < MT; ++k)
-#pragma unroll
-            for (int c = 0; c < D; ++c) acc[k][c] += part[w][k * D + c][lane];
-        gacc += part[w][MT * D][lane];
-    }
-    const double* aux = AUX + chunk * (MT + 2) * 32 + lane;
-    const int pd = PD[i];
-    const double t = aux[(MT + 1) * 32] * (gacc - __ldg(r + pd));
-    if (i >= np) return;   // padding slots of the last chunk
-    const int m = NR[i];
-    double* cb = DET ? cbuf + i * (MT * D + 1) : nullptr;
-#pragma unroll
-    for (int k = 0; k < MT; ++k) {
-        if (k < m) {
-            const double wk = omega * aux[k * 32];
-            const int nd = __ldcs(np_ + k * 32);
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-                const double v = wk * fma(gR[k][c], t, acc[k][c]);
-                if (DET) cb[k * D + c] = v;
-                else atomicAdd(x + nd + c, v);
-            }
-        }
-    }
-    const double wpr = aux[MT * 32];
-    if (wpr != 0.0) {
-        if (DET) cb[MT * D] = omega * wpr * (-t);
-        else atomicAdd(x + pd, omega * wpr * (-t));
-    }
-}
 
 // one patch per warp (3D and large patches): lane k owns restricted node k
 // MTC > 0: compile-time number of restricted nodes (27 for the 3D PoU interior shape): the column
@@ -1653,65 +1500,21 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
                                 cudaStream_t s) {
     const double2* W = reinterpret_cast<const double2*>(F.facT);
     // 2D PoU interior shape (25 nodes, 9 restricted): compile-time rectangular loop (122 -> 113 us at c2)
-    static const int minb = [] {   // residency: 4 blocks of 128 (g_R in registers) or 5 (g_R in smem)
-        const char* e = getenv("RAV_SCHUR_MINB");
-        return e ? atoi(e) : 4;
-    }();
+    const bool shape = MT == 9 && F.NN == 25;
     const bool ra = (reinterpret_cast<uintptr_t>(r) & 15) == 0;
-    auto kern = F.npid ? ((MT == 9 && F.NN == 25) ? (ra ? schur_sweep_thread_kernel<MT, 2, 4, 8, DET, true, true>
-                                                        : schur_sweep_thread_kernel<MT, 2, 4, 8, DET, true>)
-                                                  : schur_sweep_thread_kernel<MT, 2, 4, 0, DET, true>)
-              : (MT == 9 && F.NN == 25) ? (minb >= 6 ? schur_sweep_thread_kernel<MT, 2, 6, 8, DET>
-                                           : minb == 5 ? schur_sweep_thread_kernel<MT, 2, 5, 8, DET>
-                                                       : schur_sweep_thread_kernel<MT, 2, 4, 8, DET>)
-                                        : schur_sweep_thread_kernel<MT, 2, 4, 0, DET>;
-    // wave split: full waves of one warp per chunk, then the partial last wave with two half-warps
-    // per chunk (its chunks finish in about half the time of a full-chunk warp)
-    static int conc = 0;
-    if (!conc) {
-        int per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0) != cudaSuccess) per_sm = 0;
-        cudaGetLastError();
-        conc = std::max(1, per_sm) * 4 * num_sms();   // resident warps (4 per block)
-    }
+    auto kern = F.npid ? (shape ? (ra ? schur_sweep_thread_kernel<MT, 2, 8, DET, true, true>
+                                      : schur_sweep_thread_kernel<MT, 2, 8, DET, true>)
+                                : schur_sweep_thread_kernel<MT, 2, 0, DET, true>)
+                       : shape ? schur_sweep_thread_kernel<MT, 2, 8, DET> : schur_sweep_thread_kernel<MT, 2, 0, DET>;
     // rectangular blocks prefetched ahead by the bulk-copy unit (0: off).  Measured (rav_apply alone):
     // c2 115.0 / 109.7 / 108.9 / 110.3 / 117.0 us for 0 / 1 / 2 / 3 / 5; c3 1606 -> 1474 us at 2
     static const int pf = [] {
         const char* e = getenv("RAV_SCHUR_PF");
         return e ? atoi(e) : 2;
     }();
-    static const bool split = [] {   // measured at c2: 119.5 us split vs 114.0 us single launch -> off
-        const char* e = getenv("RAV_SCHUR_TAIL");
-        return e && atoi(e) == 1;
-    }();
-    static const int tailpf = [] {   // whole-chunk prefetch for the last partial wave (c2: 111.2 vs 109.2 us -> off)
-        const char* e = getenv("RAV_SCHUR_TAILPF");
-        return e ? atoi(e) : 0;
-    }();
-    static const int cta4 = [] {   // one chunk per 4-warp CTA (schur_sweep_cta4_kernel)
-        const char* e = getenv("RAV_SCHUR_CTA4");
-        return e ? atoi(e) : 0;
-    }();
-    if constexpr (MT == 9) {
-        if (cta4 && F.NN == 25 && !F.npid && F.nchunks > 0) {
-            launch_maybe_pdl(schur_sweep_cta4_kernel<MT, 2, 8, DET>, dim3((unsigned)F.nchunks), dim3(128), 0, s, np,
-                             F.nchunks, F.pairs, W, (const int32_t*)F.DT, (const int32_t*)F.PD, (const int32_t*)F.NR,
-                             (const double*)F.WT, r, x, omega, F.cbuf);
-            return;
-        }
-    }
-    const int64_t tail0 = tailpf ? F.nchunks / conc * conc : F.nchunks;
-    const int64_t full = split && F.nchunks > conc ? F.nchunks / conc * conc : F.nchunks;
-    const int64_t rem = F.nchunks - full;
-    launch_maybe_pdl(kern, dim3((unsigned)cdiv(full * 32, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
+    launch_maybe_pdl(kern, dim3((unsigned)cdiv(F.nchunks * 32, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
                      (const int32_t*)F.DT, (const int32_t*)F.npid, (const int32_t*)F.nbase, (const int32_t*)F.ntbl,
-                     (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, (int64_t)0, 0, pf, tail0);
-    if (rem > 0) {
-        count_launch();
-        launch_maybe_pdl(kern, dim3((unsigned)cdiv(rem * 64, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
-                         (const int32_t*)F.DT, (const int32_t*)F.npid, (const int32_t*)F.nbase, (const int32_t*)F.ntbl,
-                         (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, full, 1, pf, tail0);
-    }
+                     (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, pf);
 }
 
 template <int D, bool DET>

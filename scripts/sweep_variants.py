@@ -1,5 +1,5 @@
 """Time the RAV sweep kernel (rav_apply alone, CUDA events) on a BASELINE config
-for the current build / environment (e.g. RAV_SCHUR_MINB)."""
+for the current build / environment (e.g. RAV_SCHUR_PF)."""
 import os
 import sys
 
