@@ -455,6 +455,15 @@ def run_q1q1_studies(rg, si, stream):
         study[f"{n}x{n}"] = {name: _timed_solve(rg, prob, lv, w, v, om, 3, stream)
                              for name, w, v, om in smoothers}
     out["convergence_study_V33"] = study
+    # the same at SPEC's beta = 0.1 / eta beside the beta_0 = 0.01 of R18, which was
+    # chosen by a beta study (DESIGN R18): f1 reported at both values
+    study = {}
+    for n in (64, 256, 1024):
+        prob = si.problem(2, (n, n), si.KIND_CAVITY, elem=si.ELEM_Q1Q1, beta=0.1)
+        lv = int(math.log2(n // 8)) + 1
+        study[f"{n}x{n}"] = {name: _timed_solve(rg, prob, lv, w, v, om, 3, stream, maxit=200)
+                             for name, w, v, om in smoothers}
+    out["convergence_study_V33_beta0_0.1"] = study
     steps = {}
     prob = si.problem(2, (512, 512), si.KIND_CAVITY, elem=si.ELEM_Q1Q1)
     for ns in range(1, 7):

@@ -68,9 +68,192 @@ struct SchurArgs {
     unsigned long long* alg;     // sum of algorithmic bytes of the stored data
     int comp_verified;           // the node-blocked build verified equal component blocks and no
                                  // cross-component entries for the whole operator (nb.cu)
+    int gj;                      // 3D: blocked Gauss-Jordan on the FP64 tensor cores (gj_dmma)
+    int hbits;                   // node hash table of 2^hbits slots (>= 2 nnmax) in shared memory
 };
 
 __device__ __forceinline__ int64_t tri_col_start(int j, int D) { return (int64_t)j * (j + 1) / 2 + (int64_t)j * D; }
+
+// ---- 3D local solves on the FP64 tensor cores --------------------------------------------------
+// D = C + A B for 8x8 (C, D) / 8x4 (A) / 4x8 (B) f64 tiles: one DMMA (mma.sync m8n8k4 f64; sm_100a
+// has no tcgen05 kind for f64).  Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
+// c = C[lane/4][2 (lane%4) + {0,1}].
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+constexpr int GJ_NB = 16;    // 8-wide block rows / columns of A_s (nn <= 128)
+constexpr int GJ_NJ = 20;    // + 4 block columns of right-hand sides (D + mn <= 32)
+constexpr int GJ_LDP = 168;  // stride of a published block row (B-fragment reads: 2 wavefronts)
+constexpr int GJ_BUF = 8 * GJ_LDP + 3 * 64;   // published block row, Dinv, and the next diagonal helper tiles
+
+// In-place inverse of an 8 x 8 tile held in accumulator layout (thread (g, t) = lane (4g + t) holds
+// D[g][2t], D[g][2t + 1]): Gauss-Jordan, 8 pivots, rows and columns by shuffles.  Pivot row
+// 8K + p below 1e-14 ||row||_inf (S:268's tolerance) sets *s_fail = 2.
+__device__ __forceinline__ void gj_inv8(double& d0, double& d1, int g, int t, int K, int nn, const double* rn,
+                                        int* s_fail) {
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+        const double f0 = __shfl_sync(0xffffffffu, d0, 4 * g + (p >> 1));
+        const double f1 = __shfl_sync(0xffffffffu, d1, 4 * g + (p >> 1));
+        const double r0 = __shfl_sync(0xffffffffu, d0, 4 * p + t);
+        const double r1 = __shfl_sync(0xffffffffu, d1, 4 * p + t);
+        const double f = (p & 1) ? f1 : f0;                       // D[g][p]
+        const double piv = __shfl_sync(0xffffffffu, f, 4 * p);   // D[p][p]
+        const int pr = 8 * K + p;
+        if (g == 0 && t == 0 && pr < nn && !(fabs(piv) > 1e-14 * rn[pr])) *s_fail = 2;
+        const double inv = 1.0 / piv;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int col = 2 * t + h;
+            const double rp = (h ? r1 : r0) * inv;
+            double& d = h ? d1 : d0;
+            d = g == p ? (col == p ? inv : rp) : (col == p ? -f * inv : fma(-f, rp, d));
+        }
+    }
+}
+
+// A-operand fragments (row g, columns 4 kk + t, kk = 0, 1) of an 8 x 8 tile held in accumulator
+// layout: held by lane 4g + 2kk + t/2, slot t & 1
+__device__ __forceinline__ void gj_afrag(double d0, double d1, int g, int t, double& A0, double& A1) {
+    const double x00 = __shfl_sync(0xffffffffu, d0, 4 * g + (t >> 1));
+    const double x01 = __shfl_sync(0xffffffffu, d1, 4 * g + (t >> 1));
+    const double x10 = __shfl_sync(0xffffffffu, d0, 4 * g + 2 + (t >> 1));
+    const double x11 = __shfl_sync(0xffffffffu, d1, 4 * g + 2 + (t >> 1));
+    A0 = (t & 1) ? x01 : x00;
+    A1 = (t & 1) ? x11 : x10;
+}
+
+// X = A_s^{-1} [b_0 .. b_{D-1} | e_k (k < mn)] (g and the restricted columns of A_s^{-1}, which are
+// its restricted rows: A_s is symmetric) for a symmetric positive definite A_s, nn <= 128,
+// D + mn <= 32: block Gauss-Jordan elimination without pivoting in 8 x 8 blocks, 16 warps, the
+// block updates on the FP64 tensor cores.  Warp I owns block row I of the augmented matrix
+// [A_s | R] (rows 8I .. 8I+7, 160 columns) as 20 m8n8k4 accumulator tiles in registers.  The pivot
+// rows are never scaled: at step K the buffer K & 1 holds block row K (published by warp K) and
+// Dinv_K, the inverse of its diagonal block; every other warp I forms its multiplier
+// L = M_IK Dinv_K (two DMMA) and subtracts L M_KJ from its tiles J > K (two DMMA per tile).  At
+// the end block row I holds [.. M_II .. | R_I] and X_I = Dinv_I R_I.  The serial part -- the next
+// diagonal block's update and 8 x 8 inversion -- is done at step K by warp K, whose own row has
+// nothing to update at that step, from the tiles (K+1, K) and (K+1, K+1) that warp K+1 published
+// after step K-1: Dinv_{K+1} = (M_{K+1,K+1} - M_{K+1,K} Dinv_K M_{K,K+1})^{-1}.  So it overlaps
+// the other warps' tensor-core updates instead of following them.  One barrier per step (double
+// buffered).  Rows and columns nn .. 127 are an identity block.  On return (after a barrier) rows
+// j < nn of X are in M[j ld + nn + q], q < D + mn, where the elimination path leaves them.
+__device__ void gj_dmma(double* M, int ld, int nn, int D, int mn, const double* bcol, const double* rn,
+                        int* s_fail) {
+    const int tid = threadIdx.x, I = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int row = 8 * I + g;
+    double c[GJ_NJ][2];
+#pragma unroll
+    for (int J = 0; J < GJ_NJ; ++J)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int col = 8 * J + 2 * t + h;
+            double v;
+            if (J < GJ_NB) {
+                v = (row < nn && col < nn) ? M[(size_t)row * ld + col] : (row == col ? 1.0 : 0.0);
+            } else {
+                const int q = col - 8 * GJ_NB;
+                v = row >= nn ? 0.0 : q < D ? bcol[row * D + q] : (q - D < mn && row == q - D) ? 1.0 : 0.0;
+            }
+            c[J][h] = v;
+        }
+    __syncthreads();   // M is free: from here on it holds the two publication buffers
+    // buffer layout: block row [8][GJ_LDP] | Dinv [8][8] | tile (K+1, K) [8][8] | tile (K+1, K+1) [8][8]
+    auto put = [&](double* T, double v0, double v1) {
+        *reinterpret_cast<double2*>(T + g * 8 + 2 * t) = make_double2(v0, v1);
+    };
+    double di0 = 0.0, di1 = 0.0;   // Dinv_I (accumulator layout)
+    if (I == 0) {
+        di0 = c[0][0];
+        di1 = c[0][1];
+        gj_inv8(di0, di1, g, t, 0, nn, rn, s_fail);
+#pragma unroll
+        for (int J = 1; J < GJ_NJ; ++J)
+            *reinterpret_cast<double2*>(M + g * GJ_LDP + 8 * J + 2 * t) = make_double2(c[J][0], c[J][1]);
+        put(M + 8 * GJ_LDP, di0, di1);
+    } else if (I == 1) {
+        put(M + 8 * GJ_LDP + 64, c[0][0], c[0][1]);
+        put(M + 8 * GJ_LDP + 128, c[1][0], c[1][1]);
+    }
+#pragma unroll   // compile-time K: every tile index below is static (a runtime K made the selects dynamic indexing)
+    for (int K = 0; K < GJ_NB; ++K) {
+        __syncthreads();
+        const double* P = M + (K & 1) * GJ_BUF;    // block row K
+        const double* Dv = P + 8 * GJ_LDP;         // Dinv_K
+        double* Q = M + ((K + 1) & 1) * GJ_BUF;    // publications for step K + 1
+        if (I == K) {   // helper: Dinv_{K+1}
+            if (K > 0) {
+                di0 = Dv[g * 8 + 2 * t];
+                di1 = Dv[g * 8 + 2 * t + 1];
+            }
+            if (K + 1 < GJ_NB) {
+                const double* T1 = Dv + 64;
+                const double* T2 = Dv + 128;
+                double L[2] = {0.0, 0.0}, A0, A1;
+                dmma884(L, T1[g * 8 + t], Dv[t * 8 + g]);             // L = M_{K+1,K} Dinv_K
+                dmma884(L, T1[g * 8 + 4 + t], Dv[(4 + t) * 8 + g]);
+                gj_afrag(L[0], L[1], g, t, A0, A1);
+                double X[2] = {T2[g * 8 + 2 * t], T2[g * 8 + 2 * t + 1]};
+                dmma884(X, -A0, P[t * GJ_LDP + 8 * (K + 1) + g]);     // - L M_{K,K+1}
+                dmma884(X, -A1, P[(4 + t) * GJ_LDP + 8 * (K + 1) + g]);
+                gj_inv8(X[0], X[1], g, t, K + 1, nn, rn, s_fail);
+                put(Q + 8 * GJ_LDP, X[0], X[1]);
+            }
+        } else {
+            double A0, A1, L[2] = {0.0, 0.0};
+            gj_afrag(c[K][0], c[K][1], g, t, A0, A1);
+            dmma884(L, A0, Dv[t * 8 + g]);           // L = M_IK Dinv_K
+            dmma884(L, A1, Dv[(4 + t) * 8 + g]);
+            gj_afrag(L[0], L[1], g, t, A0, A1);
+            A0 = -A0;
+            A1 = -A1;
+#pragma unroll
+            for (int J = K + 1; J < GJ_NJ; ++J) {
+                if (J == K + 1 && I == K + 1) continue;   // its diagonal tile: only Dinv is used
+                dmma884(c[J], A0, P[t * GJ_LDP + 8 * J + g]);
+                dmma884(c[J], A1, P[(4 + t) * GJ_LDP + 8 * J + g]);
+            }
+            if (K + 1 < GJ_NB && I == K + 1) {
+#pragma unroll
+                for (int J = K + 2; J < GJ_NJ; ++J)
+                    *reinterpret_cast<double2*>(Q + g * GJ_LDP + 8 * J + 2 * t) = make_double2(c[J][0], c[J][1]);
+            }
+            if (K + 2 < GJ_NB && I == K + 2) {
+                put(Q + 8 * GJ_LDP + 64, c[K + 1][0], c[K + 1][1]);
+                put(Q + 8 * GJ_LDP + 128, c[K + 2][0], c[K + 2][1]);
+            }
+        }
+    }
+    __syncthreads();
+    // X_I = Dinv_I R_I: R_I through a per-warp shared-memory tile into B-fragment layout
+    double* R = M + 2 * GJ_BUF + I * (8 * 34);
+#pragma unroll
+    for (int J = GJ_NB; J < GJ_NJ; ++J)
+        *reinterpret_cast<double2*>(R + g * 34 + 8 * (J - GJ_NB) + 2 * t) = make_double2(c[J][0], c[J][1]);
+    __syncwarp();
+    double A0, A1;
+    gj_afrag(di0, di1, g, t, A0, A1);
+#pragma unroll
+    for (int J = GJ_NB; J < GJ_NJ; ++J) {
+        double x[2] = {0.0, 0.0};
+        dmma884(x, A0, R[t * 34 + 8 * (J - GJ_NB) + g]);
+        dmma884(x, A1, R[(4 + t) * 34 + 8 * (J - GJ_NB) + g]);
+        c[J][0] = x[0];
+        c[J][1] = x[1];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int J = GJ_NB; J < GJ_NJ; ++J)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int q = 8 * (J - GJ_NB) + 2 * t + h;
+            if (row < nn && q < D + mn) M[(size_t)row * ld + nn + q] = c[J][h];
+        }
+    __syncthreads();
+}
 
 // NT threads per CTA: 128 for the small 2D patches (several CTAs per SM), 512 for the
 // 3D patches whose ~150 KB of shared memory allow one CTA per SM
@@ -84,8 +267,17 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
     double* bcol = rn + a.nnmax;                              // nnmax * D (B column of L_i)
     double* wnode = bcol + (size_t)a.nnmax * D;               // nnmax weights (per node)
     int32_t* ndof = (int32_t*)(wnode + a.nnmax);              // nnmax: dof of component 0
-    int32_t* snode = ndof + a.nnmax;                          // sorted node ids (dof / D)
-    int32_t* sperm = snode + a.nnmax;                         // local index of sorted entry
+    int32_t* hkey = ndof + a.nnmax;                           // node id (dof / D) -> local index:
+    int32_t* hval = hkey + (1 << a.hbits);                    // open addressing, linear probing
+    const unsigned hmask = (1u << a.hbits) - 1;
+    auto hslot = [&](int nd) { return ((unsigned)nd * 2654435761u) >> (32 - a.hbits); };
+    auto hfind = [&](int nd) {   // local index of node nd in the patch, or -1
+        for (unsigned h = hslot(nd);; h = (h + 1) & hmask) {
+            const int k = hkey[h];
+            if (k == nd) return (int)hval[h];
+            if (k < 0) return -1;
+        }
+    };
     __shared__ int s_nn, s_mn, s_pd, s_fail, s_piv, s_sym, s_np, s_pidx;
     __shared__ double s_wp, s_cpp;
 
@@ -212,12 +404,15 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
         const int W = nn + D + mn, ld = a.ld;
         for (int t = tid; t < nn * ld; t += NT) M[t] = 0.0;
         for (int t = tid; t < nn * D; t += NT) bcol[t] = 0.0;
-        for (int t = tid; t < nn; t += NT) {
+        for (int t = tid; t <= (int)hmask; t += NT) hkey[t] = -1;
+        __syncthreads();
+        for (int t = tid; t < nn; t += NT) {   // the patch's nodes into the hash table
             const int nd = ndof[t] / D;
-            int rank = 0;
-            for (int u = 0; u < nn; ++u) rank += (ndof[u] / D < nd);
-            snode[rank] = nd;
-            sperm[rank] = t;
+            for (unsigned h = hslot(nd);; h = (h + 1) & hmask) {
+                const int old = atomicCAS(&hkey[h], -1, nd);
+                if (old == -1) { hval[h] = t; break; }
+                if (old == nd) { atomicOr((unsigned int*)&s_fail, 1u); break; }   // a node twice
+            }
         }
         __syncthreads();
         // gather A_s (component 0 rows), the B column, and verify components 1..D-1.  With the
@@ -225,30 +420,68 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
         // are gathered by a merge of the sorted row with the sorted node list and nothing else is
         // re-checked
         if (a.comp_verified) {
-            // one warp per component-0 row, its lanes over the row's entries (independent loads; a
-            // thread per row walked ~34 entries with dependent global loads in 2D); the lane that
-            // meets the patch's pressure column also takes the other components' B entries, at the
-            // same offset of their rows (verified identical structure)
+            // one warp per component-0 row, its lanes over the row's entries; the lane that meets the
+            // patch's pressure column also takes the other components' B entries, at the same offset of
+            // their rows (verified identical structure).  The loads are issued ahead of their use:
+            // lane m first loads the row starts of the warp's m-th row and of the next D - 1 component
+            // rows, then two rows at a time every lane loads all its (column, value) pairs
+            // (GATHER_U per row) before the searches and stores -- the dependent global round trips
+            // of a serial walk held the CTA (one per SM in 3D) most of the kernel's time.
+            constexpr int NW = NT / 32, GATHER_U = 5;
             const int warp = tid >> 5, lane = tid & 31;
-            for (int j = warp; j < nn; j += NT / 32) {
-                const int row = ndof[j];
-                const int64_t k0 = a.rp[row], k1 = a.rp[row + 1];
-                for (int64_t k = k0 + lane; k < k1; k += 32) {
-                    const int col = a.ci[k];
-                    if (col == pd) {
-                        bcol[j * D] = a.val[k];
-                        for (int c = 1; c < D; ++c) bcol[j * D + c] = a.val[a.rp[row + c] + (k - k0)];
-                        continue;
+            const int nrw = nn > warp ? (nn - warp + NW - 1) / NW : 0;   // rows j = warp + NW m
+            int64_t rs[4] = {0, 0, 0, 0};                               // rp[row + c], c <= D (D <= 3)
+            for (int m0 = 0; m0 < nrw; m0 += 32) {
+                if (m0 + lane < nrw) {
+                    const int row = ndof[warp + NW * (m0 + lane)];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (c <= D) rs[c] = __ldg(a.rp + row + c);
+                }
+                const int mend = min(nrw, m0 + 32);
+                for (int m = m0; m < mend; m += 2) {
+                    int64_t k0[2], k1[2];
+                    int col[2][GATHER_U];
+                    double vv[2][GATHER_U];
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const int src = min(m + r, mend - 1) - m0;
+                        k0[r] = __shfl_sync(0xffffffffu, rs[0], src);
+                        k1[r] = m + r < mend ? __shfl_sync(0xffffffffu, rs[1], src) : k0[r];
+#pragma unroll
+                        for (int u = 0; u < GATHER_U; ++u) {
+                            const int64_t k = k0[r] + lane + 32 * u;
+                            const bool ok = k < k1[r];
+                            col[r][u] = ok ? __ldg(a.ci + k) : -1;
+                            vv[r][u] = ok ? __ldg(a.val + k) : 0.0;
+                        }
                     }
-                    if (col >= a.nvel) continue;
-                    const int cn = col / D;
-                    int lo = 0, hi = nn - 1, pos = -1;
-                    while (lo <= hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (snode[mid] == cn) { pos = mid; break; }
-                        if (snode[mid] < cn) lo = mid + 1; else hi = mid - 1;
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        if (m + r >= mend) break;
+                        const int j = warp + NW * (m + r);
+                        const int src = m + r - m0;
+                        int64_t kc[3];
+#pragma unroll
+                        for (int c = 1; c < 3; ++c) kc[c] = __shfl_sync(0xffffffffu, rs[c], src);
+                        auto put = [&](int cl, double v, int64_t k) {
+                            if (cl < 0) return;
+                            if (cl == pd) {
+                                bcol[j * D] = v;
+#pragma unroll
+                                for (int c = 1; c < 3; ++c)
+                                    if (c < D) bcol[j * D + c] = __ldg(a.val + kc[c] + (k - k0[r]));
+                                return;
+                            }
+                            if (cl >= a.nvel) return;
+                            const int l = hfind(cl / D);
+                            if (l >= 0) M[(size_t)j * ld + l] = v;
+                        };
+#pragma unroll
+                        for (int u = 0; u < GATHER_U; ++u) put(col[r][u], vv[r][u], k0[r] + lane + 32 * u);
+                        for (int64_t k = k0[r] + 32 * GATHER_U + lane; k < k1[r]; k += 32)   // long rows
+                            put(__ldg(a.ci + k), __ldg(a.val + k), k);
                     }
-                    if (pos >= 0) M[(size_t)j * ld + sperm[pos]] = a.val[k];
                 }
             }
         }
@@ -260,15 +493,9 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
                 const double v = a.val[k];
                 if (col == pd) { bcol[j * D + c] = v; continue; }
                 if (col >= a.nvel) continue;    // other pressure DoFs are outside the patch
-                const int cn = col / D, cc = col % D;
-                int lo = 0, hi = nn - 1, pos = -1;
-                while (lo <= hi) {
-                    int mid = (lo + hi) >> 1;
-                    if (snode[mid] == cn) { pos = mid; break; }
-                    if (snode[mid] < cn) lo = mid + 1; else hi = mid - 1;
-                }
-                if (pos < 0) continue;
-                const int l = sperm[pos];
+                const int cc = col % D;
+                const int l = hfind(col / D);
+                if (l < 0) continue;
                 if (cc != c) {
                     if (v != 0.0) atomicOr((unsigned int*)&s_fail, 1u);
                     continue;
@@ -283,15 +510,9 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
             for (int64_t k = a.rp[row]; k < a.rp[row + 1]; ++k) {
                 const int col = a.ci[k];
                 if (col >= a.nvel || col % D != c) continue;
-                const int cn = col / D;
-                int lo = 0, hi = nn - 1, pos = -1;
-                while (lo <= hi) {
-                    int mid = (lo + hi) >> 1;
-                    if (snode[mid] == cn) { pos = mid; break; }
-                    if (snode[mid] < cn) lo = mid + 1; else hi = mid - 1;
-                }
-                if (pos < 0) continue;
-                if (M[(size_t)j * ld + sperm[pos]] != a.val[k]) atomicOr((unsigned int*)&s_fail, 1u);
+                const int l = hfind(col / D);
+                if (l < 0) continue;
+                if (M[(size_t)j * ld + l] != a.val[k]) atomicOr((unsigned int*)&s_fail, 1u);
             }
         }
         // pressure row: symmetric B and C_pp (entries in parallel: one thread walking a 3D pressure
@@ -300,15 +521,9 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
             const int col = a.ci[k];
             if (col == pd) { s_cpp = a.val[k]; continue; }
             if (col >= a.nvel) continue;
-            const int cn = col / D, cc = col % D;
-            int lo = 0, hi = nn - 1, pos = -1;
-            while (lo <= hi) {
-                int mid = (lo + hi) >> 1;
-                if (snode[mid] == cn) { pos = mid; break; }
-                if (snode[mid] < cn) lo = mid + 1; else hi = mid - 1;
-            }
-            if (pos < 0) continue;
-            if (bcol[sperm[pos] * D + cc] != a.val[k]) atomicOr((unsigned int*)&s_fail, 1u);
+            const int l = hfind(col / D);
+            if (l < 0) continue;
+            if (bcol[l * D + col % D] != a.val[k]) atomicOr((unsigned int*)&s_fail, 1u);
         }
         __syncthreads();
         if (s_fail) {
@@ -358,24 +573,36 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
         // right-hand sides: B columns, then e_k for the restricted nodes
         for (int t = tid; t < nn * D; t += NT) M[(size_t)(t / D) * ld + nn + (t % D)] = bcol[t];
         for (int k = tid; k < mn; k += NT) M[(size_t)k * ld + nn + D + k] = 1.0;
-        for (int r = tid; r < nn; r += NT) {
-            double mx = 0.0;
-            for (int c = 0; c < nn; ++c) mx = fmax(mx, fabs(M[(size_t)r * ld + c]));
-            rn[r] = mx;
-        }
-        // symmetric A_s (every generated operator: the principal block of the SPD viscous operator)
-        // is eliminated without pivoting -- one barrier per column instead of three; an unsymmetric
-        // block keeps partial pivoting
+        // row norms ||row||_inf (pivot tolerance) and the symmetry test of A_s: one warp per row, its
+        // lanes over the columns.  A symmetric A_s (every generated operator: the principal block of
+        // the SPD viscous operator) is eliminated without pivoting; an unsymmetric block keeps
+        // partial pivoting
         if (tid == 0) s_sym = 1;
         __syncthreads();
-        for (int t = tid; t < nn * nn; t += NT) {
-            const int r = t / nn, c = t % nn;
-            if (c > r && M[(size_t)r * ld + c] != M[(size_t)c * ld + r]) s_sym = 0;
+        for (int r = tid >> 5; r < nn; r += NT / 32) {
+            double mx = 0.0;
+            bool sym = true;
+            for (int c = tid & 31; c < nn; c += 32) {
+                const double v = M[(size_t)r * ld + c];
+                mx = fmax(mx, fabs(v));
+                if (c > r && v != M[(size_t)c * ld + r]) sym = false;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if ((tid & 31) == 0) rn[r] = mx;
+            if (!sym) s_sym = 0;
         }
         __syncthreads();
         const bool nopiv = s_sym != 0;
+        bool gj = false;   // solved on the tensor cores (gj_dmma): no elimination / back substitution
+        if constexpr (NT == 512) {
+            if (a.gj && nopiv && D == 3 && nn <= 8 * GJ_NB && D + mn <= 8 * (GJ_NJ - GJ_NB)) {
+                gj_dmma(M, ld, nn, D, mn, bcol, rn, &s_fail);
+                gj = true;
+            }
+        }
         // Gaussian elimination with partial pivoting (A_s symmetric: A_s^T = A_s)
-        for (int c = 0; c < nn; ++c) {
+        for (int c = 0; c < nn && !gj; ++c) {
             if (nopiv) {
                 const double piv = M[(size_t)c * ld + c];
                 if (tid == 0 && !(fabs(piv) > 1e-14 * rn[c])) s_fail = 2;
@@ -447,7 +674,7 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
             continue;
         }
         const int nrhs = D + mn;
-        for (int c = nn - 1; c >= 0; --c) {
+        for (int c = nn - 1; c >= 0 && !gj; --c) {
             for (int t = tid; t < nrhs; t += NT) M[(size_t)c * ld + nn + t] /= M[(size_t)c * ld + c];
             __syncthreads();
             {
@@ -1145,10 +1372,17 @@ rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D,
     RAV_CUDA(cudaMemsetAsync(alg, 0, sizeof(unsigned long long), s));
     a.fail = fail;
     a.comp_verified = (A.nb.nslices > 0 && A.nb.D == D) ? 1 : 0;
+    static const int gj = [] {   // 3D local solves by the tensor-core Gauss-Jordan (gj_dmma)
+        const char* e = getenv("RAV_SCHUR_GJ");
+        return e ? atoi(e) : 1;
+    }();
+    a.gj = gj;
     a.bad = bad;
     a.alg = alg;
+    a.hbits = 4;
+    while ((1 << a.hbits) < 2 * a.nnmax) ++a.hbits;
     const size_t shmem = sizeof(double) * ((size_t)a.nnmax * a.ld + a.nnmax + (size_t)a.nnmax * D + a.nnmax) +
-                         sizeof(int32_t) * 3 * a.nnmax + 64;
+                         sizeof(int32_t) * (a.nnmax + 2 * ((size_t)1 << a.hbits)) + 64;
     if (shmem > 220 * 1024) {
         factors_free(F);
         cudaFreeAsync(fail, s);
