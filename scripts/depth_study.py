@@ -1,10 +1,12 @@
 """Depth versus resolution on the c3 family (VERDICT r01 "what's weak" 4): V(2,2)-RAV cycle
 counts to 1e-8 (P:132 stopping rule, R11) for 64^2 ... 2048^2 with
   (a) the c3 hierarchy shape: 4^2 coarsest grid, so the depth grows with the resolution;
-  (b) a fixed depth of 5 levels: the coarsest grid is n/16 and grows with the resolution;
-both with the seeded variable viscosity (R12) and with eta = 1.  GPU (mg_solve) for every
-case; the oracle's count beside it where the oracle finishes in seconds to minutes
-(n <= 256, and 512 for the fixed depth).  Writes one JSON file (argv[1]).
+  (b) a 16^2 coarsest grid (two levels fewer at every resolution);
+  (c) fixed resolution (256^2, 1024^2), depth varied: coarsest 16^2, 8^2, 4^2
+(the direct coarse solve takes at most 6000 DoFs, i.e. 16^2 at most, so a fixed depth over the
+whole family is not possible); all with the seeded variable viscosity (R12) and with eta = 1.
+GPU (mg_solve) for every case; the oracle's count beside it where it finishes in seconds
+(n <= 256).  Writes one JSON file (argv[1]).
 
     python scripts/depth_study.py profiles/r02_depth_study.json
 """
@@ -33,7 +35,7 @@ def gpu(prob, levels):
     mg.close()
     del mg, x
     torch.cuda.empty_cache()
-    return k, float((h[-1] / h[0]) ** (1.0 / max(k, 1)))
+    return k, float((h[-1] / h[0]) ** (1.0 / max(k, 1))), [float(v / h[0]) for v in h]
 
 
 def ora(prob, levels):
@@ -42,15 +44,18 @@ def ora(prob, levels):
     return k
 
 
+cases = [(n, c) for n in (64, 128, 256, 512, 1024, 2048) for c in (4, 16)] + [(256, 8), (1024, 8)]
 for eta in ("fourier", "const"):
-    for n in (64, 128, 256, 512, 1024, 2048):
-        for shape in ("coarsest 4^2", "5 levels"):
-            levels = int(np.log2(n // 4)) + 1 if shape == "coarsest 4^2" else 5
+    for n, coarse in cases:
+        for _ in (0,):
+            levels = int(np.log2(n // coarse)) + 1
+            shape = f"coarsest {coarse}^2"
             prob = si.problem(2, (n, n), si.KIND_MMS, eta=eta)
-            k, rho = gpu(prob, levels)
+            k, rho, hist = gpu(prob, levels)
             row = {"eta": eta, "n": n, "shape": shape, "levels": levels, "coarsest": n >> (levels - 1),
-                   "gpu_cycles": k, "gpu_rho": rho}
-            if n <= 256 or (n == 512 and shape == "5 levels"):
+                   "gpu_cycles": k, "gpu_rho": rho, "gpu_rho_first5": hist[min(5, k)] ** (1.0 / min(5, k)),
+                   "gpu_rel_hist": hist}
+            if n <= 256:
                 t0 = time.perf_counter()
                 row["oracle_cycles"] = ora(prob, levels)
                 row["oracle_s"] = time.perf_counter() - t0
