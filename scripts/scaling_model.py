@@ -2,7 +2,9 @@
 round" 6; SURVEY section 8 row e).  Only one GPU is available to this build, so the N-GPU time of
 one rank is assembled from pieces measured on it:
 
-  T_N = (T_emul(N) - T_coarse) / N + T_coarse + T_nccl(N) + T_link(N)
+  strong (c3, c4 V-cycles):  T_N = (T_emul(N) - T_coarse) / N + T_coarse + T_nccl + T_link(N)
+                             (+ (1 - 1/N) T_phase in the conservative form)
+  weak (c2, c5 sweeps):      T_N = T_1 + (T_emul(N) - N T_1) + T_nccl + T_link(N)
 
 * T_emul(N): the library's slab-partitioned driver (mgd_vcycle / mgd_smooth, csrc/dist.cu) with
   all N subdomains on the one GPU and the exchanges between them as device reads (via_comm = 0).
@@ -10,11 +12,20 @@ one rank is assembled from pieces measured on it:
   would on its own GPU -- so T_emul(N) / N is one rank's compute (balanced slabs).
 * T_coarse: the agglomerated coarse levels, which every rank runs whole (not divided by N):
   mg_vcycle of that sub-hierarchy alone.
-* T_nccl(N): T_emul(N, via_comm = 1) - T_emul(N, via_comm = 0): the same run with every exchange
-  phase as an NCCL group of self sends / receives (one group per phase, as each rank posts one
-  group per phase) -- NCCL's launch and copy cost per phase on this GPU.
+* T_nccl: T_emul(2, via_comm = 1) - T_emul(2, via_comm = 0): the same 2-subdomain run with every
+  exchange phase as an NCCL group of self sends / receives.  With two subdomains one group holds
+  2 sends + 2 receives, what an interior rank posts per phase (two neighbours); with N
+  subdomains the emulated group holds all 2(N - 1) pairs, more than any rank posts, so the
+  N = 2 difference is the per-rank estimate (the N > 2 differences are reported too).  NCCL's
+  self send is its on-device copy path: NVLink adds its latency (a few us per phase) -- T_link.
+* T_phase (strong, conservative): the exchange-phase kernels (zero / pack / add / unpack) run once
+  per phase for ALL local subdomains in the emulation but once per rank on N GPUs; counted from
+  the graph's launch count (mgd_last_launches for N = 2 and 4) at 3 us per launch.
+* weak: T_emul(N) - N T_1 is everything the partitioned run adds to N single-GPU sweeps (ghost
+  rows, phase kernels); it is charged to every rank in full.
 * T_link(N): one rank's message bytes per cycle (largest interface lists) / 400 GB/s (NVLink 5,
-  900 GB/s per direction nominal; half of it assumed achieved for ~100 KB messages).
+  900 GB/s per direction nominal; half of it assumed achieved for ~100 KB messages) + 3 us of
+  NVLink latency per exchange phase.
 
 Strong scaling (c3, c4 V-cycles): E = T_1 / (N T_N).  Weak scaling (c5 smoothers, c2 sweeps per
 GPU): E = T_1 / T_N.  Writes one JSON file (argv[1]).
@@ -35,6 +46,8 @@ OUT = sys.argv[1] if len(sys.argv) > 1 else "scaling_model.json"
 STREAM = torch.cuda.Stream()
 torch.cuda.set_stream(STREAM)
 LINK_GBS = 400.0
+LINK_LAT_S = 3e-6
+LAUNCH_S = 3e-6
 
 
 def timed(fn, reps):
@@ -87,27 +100,41 @@ def vcycle_case(name, Ns):
             row["T_emul_nccl_s" if via else "T_emul_s"] = t
             if not via:
                 subs, coarse = mgd._keep
+                row["launches_per_cycle"] = mgd.last_launches
                 row["partitioned_levels"] = info["K"]
                 row["coarse_levels"] = c["levels"] - info["K"]
                 row["link_bytes_per_cycle"] = link_bytes(subs, pre + post + 2)
+                row["phases_per_cycle"] = 2 * (pre + post) * info["K"] + 4 * info["K"]
                 row["T_coarse_s"] = 0.0
+                row["coarse_launches_per_cycle"] = 0
                 if coarse is not None:
                     xc = torch.zeros(coarse.n, dtype=torch.float64, device="cuda")
                     bc = torch.randn(coarse.n, dtype=torch.float64, device="cuda")
                     row["T_coarse_s"] = timed(lambda: coarse.vcycle(xc, bc, pre, post, om), 10)
+                    row["coarse_launches_per_cycle"] = coarse.last_launches
+                    del xc, bc
+                del subs, coarse
             mgd.close()
             del mgd, info, xs
             torch.cuda.empty_cache()
-        tc = row.get("T_coarse_s") or 0.0
-        row["T_nccl_s"] = max(0.0, row["T_emul_nccl_s"] - row["T_emul_s"])
-        row["T_link_s"] = row["link_bytes_per_cycle"] / (LINK_GBS * 1e9)
-        TN = (row["T_emul_s"] - tc) / N + tc + row["T_nccl_s"] + row["T_link_s"]
-        row["T_N_model_s"] = TN
-        row["efficiency_strong"] = t1 / (N * TN)
+        row["T_nccl_s_emulated_group"] = max(0.0, row["T_emul_nccl_s"] - row["T_emul_s"])
         out["N"][N] = row
         print(name, N, json.dumps(row), flush=True)
     comm0.close()
     comm1.close()
+    # per-subdomain and shared (phase) launches from N = 2 and N = 4: L(N) = N L_sub + L_phase + L_coarse
+    r2, r4 = out["N"][2], out["N"][4]
+    l_sub = (r4["launches_per_cycle"] - r2["launches_per_cycle"]) / 2
+    l_phase = max(0.0, r2["launches_per_cycle"] - 2 * l_sub - r2["coarse_launches_per_cycle"])
+    t_nccl = r2["T_nccl_s_emulated_group"]
+    out["per_rank"] = {"launches_per_subdomain": l_sub, "phase_launches": l_phase, "T_nccl_s": t_nccl}
+    for N, row in out["N"].items():
+        tc = row["T_coarse_s"]
+        t_link = row["link_bytes_per_cycle"] / (LINK_GBS * 1e9) + row["phases_per_cycle"] * LINK_LAT_S
+        TN = (row["T_emul_s"] - tc) / N + tc + t_nccl + t_link
+        TNc = TN + (1 - 1 / N) * l_phase * LAUNCH_S
+        row.update({"T_link_s": t_link, "T_N_model_s": TN, "T_N_model_conservative_s": TNc,
+                    "efficiency_strong": t1 / (N * TN), "efficiency_strong_conservative": t1 / (N * TNc)})
     return out
 
 
@@ -137,18 +164,22 @@ def smooth_case(name, Ns, sweeps):
             if not via:
                 subs, _ = mgd._keep
                 row["link_bytes_per_sweep"] = link_bytes(subs, 1)
+                del subs
             mgd.close()
             del mgd, info, xs
             torch.cuda.empty_cache()
-        row["T_nccl_s"] = max(0.0, row["T_emul_nccl_s"] - row["T_emul_s"])
-        row["T_link_s"] = row["link_bytes_per_sweep"] / (LINK_GBS * 1e9)
-        TN = row["T_emul_s"] / N + row["T_nccl_s"] + row["T_link_s"]
-        row["T_N_model_s"] = TN
-        row["efficiency_weak"] = t1 / TN
+        row["T_nccl_s_emulated_group"] = max(0.0, row["T_emul_nccl_s"] - row["T_emul_s"])
         out["N"][N] = row
         print(name, N, json.dumps(row), flush=True)
     comm0.close()
     comm1.close()
+    t_nccl = out["N"][Ns[0]]["T_nccl_s_emulated_group"]   # N = 2: one interior rank's group
+    for N, row in out["N"].items():
+        t_link = row["link_bytes_per_sweep"] / (LINK_GBS * 1e9) + 2 * LINK_LAT_S
+        extra = max(0.0, row["T_emul_s"] - N * t1)
+        TN = t1 + extra + t_nccl + t_link
+        row.update({"T_extra_s": extra, "T_nccl_s": t_nccl, "T_link_s": t_link, "T_N_model_s": TN,
+                    "efficiency_weak": t1 / TN})
     return out
 
 
