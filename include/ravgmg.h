@@ -290,11 +290,14 @@ rav_status rav_rows_size(const rav_ctx* ctx, int64_t* total);
 rav_status rav_export_rows(const rav_ctx* ctx, double* rows);
 
 /* Algorithmic roofline bytes of one application (SURVEY section 8 row d):
- * bytes_sweep = factor bytes of the stored format (RAV_KERNEL_SYM: the
- * symmetric restricted block once + one weight per restricted row; other
- * kernels: 8 sum nres_i n_i) + 4 sum n_i (patch DoF lists) + vectors (r read,
- * x read + write); bytes_residual = 12 nnz + 8 (n+1) + 32 n (CSR, x, b, r);
- * flops = 2 sum nres_i n_i + 2 nnz. */
+ * bytes_sweep = the bytes the stored format must move: Schur formats (default)
+ * the factored rows (restricted rows of A_s^{-1}, g, weights, 1/S) + node
+ * indices as counted at setup; RAV_KERNEL_SYM the symmetric restricted block
+ * once + one weight per restricted row; other kernels 8 sum nres_i n_i + 4
+ * sum n_i (patch DoF lists); plus r read, x read + write.  bytes_residual =
+ * the node-blocked copy's bytes (values, pattern ids / bases or columns) +
+ * its row permutation and slice headers + x, b, r (24 n) when it exists,
+ * else the CSR's 12 nnz + 8 (n+1) + 24 n.  flops = 2 sum nres_i n_i + 2 nnz. */
 rav_status rav_sweep_bytes(const rav_ctx* ctx, double* bytes_sweep, double* bytes_residual,
                            double* flops);
 
@@ -402,8 +405,8 @@ rav_status rav_xfer_set_stream(rav_xfer* t, void* stream);
  * a uniformly refined tensor-product grid: Q2 1D weights 1 / (3/8, 3/4, -1/8),
  * Q1 weights 1 / (1/2, 1/2), Dirichlet nodes dropped; R = P^T): the kernels
  * read the input and write the output vector, no matrix.  fine / coarse: the
- * rav_grid descriptors of the two levels (whole grids, fine ncell = 2 coarse
- * ncell, same element pair).  Before switching, both forms are applied to
+ * rav_grid descriptors of the two levels (fine ncell = 2 coarse ncell, same
+ * element pair; slab windows as in rav_gen_prolongation).  Before switching, both forms are applied to
  * seeded vectors and must agree to 1e-13 relative; otherwise RAV_ERR_ARG and
  * the CSR form stays.  In 3D only the prolongation switches (the 125-point
  * restriction gather measured slower than the CSR P^T).  Synchronizes the
@@ -493,6 +496,15 @@ typedef struct {
     int32_t n_colors;                   /* RAV_VARIANT_MV: colouring of the patches (rav_set_colors */
     const int64_t* color_offs;          /*   layout; the same colour index on every subdomain) */
     const int32_t* color_ids;
+    /* Optional (NULL = the CSR P_coarse is applied): the rav_grid descriptors P_coarse was generated
+     * from -- this level's window with its row window on the OWNED layers (as passed to
+     * rav_gen_prolongation) and the next partitioned level's window, or the agglomerated level's
+     * whole grid.  With both, mgd_setup switches the transfer to its stencil form (rav_xfer_set_
+     * structured's contract, slab windows included: the prolongation fills the owned rows only,
+     * the restriction gathers from them) after checking it against P_coarse on seeded vectors
+     * (1e-13); a mismatch keeps the CSR form. */
+    const rav_grid* grid_fine;
+    const rav_grid* grid_coarse;
 } rav_subdomain;
 
 typedef struct mgd_ctx mgd_ctx;

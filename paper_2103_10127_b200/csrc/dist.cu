@@ -167,6 +167,7 @@ struct DSub {                     // one local subdomain on one partitioned leve
     int64_t ngw = 0;
     int64_t own[4] = {0, 0, 0, 0};
     Csr P, PT;                    // prolongation from the next level / the agglomerated level
+    XStruct xs;                   // its stencil form (rav_subdomain grids), used when xs.on
     double *x = nullptr, *b = nullptr, *r = nullptr;   // x, b: levels > 0 (level 0: caller's)
     bool add_atomic_c = false, add_atomic_r = false;   // corr_recv / halo_send lists overlap
 };
@@ -307,8 +308,11 @@ VecTab vt_of(const std::vector<double*>& v) {
 }
 
 // ---- the distributed sweep on partitioned level k (x[i], b[i]: local subdomain vectors) ----
+// x_zero: every x[i] is zero on entry (the partitioned coarse levels: the correction starts from
+// 0, ghosts included), so the first sweep's residual b - L 0 is b itself and is read from b (the
+// window's b is complete: owners accumulated, ghosts refreshed), and there is nothing to zero
 rav_status dist_sweeps(mgd_ctx* m, int k, const std::vector<double*>& x, const std::vector<const double*>& b, int nu,
-                       double omega) {
+                       double omega, bool x_zero = false) {
     cudaStream_t s = m->stream;
     auto& L = m->lv[k];
     auto& P = m->ph[k];
@@ -331,9 +335,13 @@ rav_status dist_sweeps(mgd_ctx* m, int k, const std::vector<double*>& x, const s
             }
             continue;
         }
-        for (int i = 0; i < m->nl; ++i) RAV_TRY(launch_residual(L[i].sm->A, x[i], b[i], L[i].sm->r, s));
-        RAV_TRY(run_phase(P.zero_gw, vx, s));
-        for (int i = 0; i < m->nl; ++i) RAV_TRY(launch_sweep(L[i].sm->P, L[i].sm->F, L[i].sm->r, x[i], omega, s));
+        const bool from_b = x_zero && it == 0;
+        if (!from_b) {
+            for (int i = 0; i < m->nl; ++i) RAV_TRY(launch_residual(L[i].sm->A, x[i], b[i], L[i].sm->r, s));
+            RAV_TRY(run_phase(P.zero_gw, vx, s));
+        }
+        for (int i = 0; i < m->nl; ++i)
+            RAV_TRY(launch_sweep(L[i].sm->P, L[i].sm->F, from_b ? b[i] : L[i].sm->r, x[i], omega, s));
         RAV_TRY(run_phase(P.pack_c, vx, s));
         RAV_TRY(run_msgs(m, P.m_corr, s));
         RAV_TRY(run_phase(P.add_c, vx, s));
@@ -367,10 +375,10 @@ rav_status coarse_cycle(mg_ctx* c, double* x, const double* b, int pre, int post
 
 // V-cycle from partitioned level k (dist.DistVCycle._cycle, in the library)
 rav_status dist_cycle(mgd_ctx* m, int k, const std::vector<double*>& x, const std::vector<const double*>& b, int pre,
-                      int post, double omega) {
+                      int post, double omega, bool x_zero = false) {
     cudaStream_t s = m->stream;
     auto& L = m->lv[k];
-    RAV_TRY(dist_sweeps(m, k, x, b, pre, omega));
+    RAV_TRY(dist_sweeps(m, k, x, b, pre, omega, x_zero));
     for (int i = 0; i < m->nl; ++i) RAV_TRY(launch_residual(L[i].sm->A, x[i], b[i], L[i].r, s));
     if (k + 1 < m->K) {
         auto& C = m->lv[k + 1];
@@ -380,20 +388,30 @@ rav_status dist_cycle(mgd_ctx* m, int k, const std::vector<double*>& x, const st
             cb[i] = C[i].b;
             cx[i] = C[i].x;
             cbc[i] = C[i].b;
-            RAV_TRY(launch_spmv(L[i].PT, L[i].r, C[i].b, 1.0, 0.0, s));   // b_c = P_own^T r (window partials)
+            if (L[i].xs.on && L[i].xs.dim == 2) RAV_TRY(launch_xs_restrict(L[i].xs, L[i].r, C[i].b, s));
+            else RAV_TRY(launch_spmv(L[i].PT, L[i].r, C[i].b, 1.0, 0.0, s));   // b_c = P_own^T r (window partials)
         }
         RAV_TRY(dist_accumulate(m, k + 1, cb));
         RAV_TRY(dist_halo(m, k + 1, cb));
         for (int i = 0; i < m->nl; ++i) RAV_CUDA(cudaMemsetAsync(C[i].x, 0, sizeof(double) * C[i].n, s));
-        RAV_TRY(dist_cycle(m, k + 1, cx, cbc, pre, post, omega));
-        for (int i = 0; i < m->nl; ++i) RAV_TRY(launch_spmv(L[i].P, C[i].x, x[i], 1.0, 1.0, s));
+        RAV_TRY(dist_cycle(m, k + 1, cx, cbc, pre, post, omega, true));
+        for (int i = 0; i < m->nl; ++i) {
+            if (L[i].xs.on) RAV_TRY(launch_xs_prolong(L[i].xs, C[i].x, x[i], 1.0, 1.0, s));
+            else RAV_TRY(launch_spmv(L[i].P, C[i].x, x[i], 1.0, 1.0, s));
+        }
     } else {
-        for (int i = 0; i < m->nl; ++i)
-            RAV_TRY(launch_spmv(L[i].PT, L[i].r, m->bc_part + (size_t)i * m->nc, 1.0, 0.0, s));
+        for (int i = 0; i < m->nl; ++i) {
+            double* bp = m->bc_part + (size_t)i * m->nc;
+            if (L[i].xs.on && L[i].xs.dim == 2) RAV_TRY(launch_xs_restrict(L[i].xs, L[i].r, bp, s));
+            else RAV_TRY(launch_spmv(L[i].PT, L[i].r, bp, 1.0, 0.0, s));
+        }
         RAV_TRY(ordered_allsum(m, m->bc_part, m->nc, m->nc, m->bc_loc, m->bc_all, m->bc, s));
         RAV_CUDA(cudaMemsetAsync(m->xc, 0, sizeof(double) * m->nc, s));
         RAV_TRY(coarse_cycle(m->coarse, m->xc, m->bc, pre, post, omega));
-        for (int i = 0; i < m->nl; ++i) RAV_TRY(launch_spmv(L[i].P, m->xc, x[i], 1.0, 1.0, s));
+        for (int i = 0; i < m->nl; ++i) {
+            if (L[i].xs.on) RAV_TRY(launch_xs_prolong(L[i].xs, m->xc, x[i], 1.0, 1.0, s));
+            else RAV_TRY(launch_spmv(L[i].P, m->xc, x[i], 1.0, 1.0, s));
+        }
     }
     RAV_TRY(dist_halo(m, k, x));
     return dist_sweeps(m, k, x, b, post, omega);
@@ -646,6 +664,13 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
                 }
                 st = csr_upload(&D.P_coarse, S.P, m->stream);
                 if (st == RAV_OK) st = csr_transpose(S.P, S.PT, m->stream);
+                if (st == RAV_OK && D.grid_fine && D.grid_coarse) {   // stencil form, verified against P
+                    XStruct X;
+                    if (xs_build(D.grid_fine, D.grid_coarse, S.P.n_rows, S.P.n_cols, X) == RAV_OK &&
+                        xs_verify(X, S.P, S.PT, m->stream) == RAV_OK)
+                        S.xs = X;
+                    set_error("");
+                }
             } else if (k + 1 < n_levels || coarse) {
                 set_error("mgd_setup: level %d subdomain %d needs P_coarse", k, S.gid);
                 st = RAV_ERR_ARG;

@@ -184,6 +184,11 @@ struct XStruct {
     int dim = 0, P = 2;    // P: velocity lattice refinement (2: Q2-Q1, 1: Q1-Q1)
     int nc[3] = {1, 1, 1}; // coarse cells per axis
     int64_t n_fine = 0, n_coarse = 0;
+    // slab windows along the last axis (global lattice layers, inclusive; whole grids: everything):
+    // fine window node / vertex layers, the fine rows P fills (owned layers), coarse window layers
+    int fn_lo = 0, fn_hi = -1, fv_lo = 0, fv_hi = -1;
+    int rn_lo = 0, rn_hi = -1, rv_lo = 0, rv_hi = -1;
+    int cn_lo = 0, cn_hi = -1, cv_lo = 0, cv_hi = -1;
 };
 rav_status xs_build(const rav_grid* fine, const rav_grid* coarse, int64_t n_fine, int64_t n_coarse, XStruct& S);
 rav_status xs_verify(const XStruct& S, const Csr& P, const Csr& PT, cudaStream_t s);

@@ -15,6 +15,10 @@
 //     Q1: fine 2c-1, 2c, 2c+1 with (1/2, 1, 1/2).
 // Sums run over the stencil in ascending DoF order.  xs_verify checks the stencil form against
 // the level's own CSR P / P^T on seeded vectors before it is used.
+// Slab windows (multi-GPU levels, rav_grid win = 1): the vectors are windows of layers along the
+// last axis; the prolongation fills only the fine rows of the owned layers (the others keep their
+// value: rav_gen_prolongation leaves those rows empty) and the restriction gathers only from them
+// (P_own^T r), writing every coarse window entry.
 #include "internal.cuh"
 
 namespace rav {
@@ -23,9 +27,11 @@ namespace {
 struct XArgs {
     int dim, P;                 // P: velocity lattice refinement (2: Q2, 1: Q1)
     int nc[3];                  // coarse cells per axis (fine: 2 nc)
-    int64_t nfree_f, nfree_c;   // free velocity nodes
-    int64_t nvert_f, nvert_c;   // vertices (pressure DoFs)
+    int64_t nfree_f, nfree_c;   // free velocity nodes (of the windows)
+    int64_t nvert_f, nvert_c;   // vertices (pressure DoFs, of the windows)
     int64_t nvel_f, nvel_c;     // dim * nfree
+    // last-axis windows (global lattice layers, inclusive): see XStruct
+    int fn_lo, fn_hi, fv_lo, fv_hi, rn_lo, rn_hi, rv_lo, rv_hi, cn_lo, cn_hi, cv_lo, cv_hi;
 };
 
 // Per-axis stencils as fixed-length candidate lists (weight 0 = absent), so that every loop
@@ -91,8 +97,9 @@ __global__ void __launch_bounds__(256) xs_prolong_kernel(XArgs X, const double* 
 #pragma unroll
         for (int k = 0; k < DIM; ++k) {
             const int m = 2 * X.P * X.nc[k] - 1;
-            const int a = (int)(r % m) + 1;
-            r /= m;
+            const int a = k < DIM - 1 ? (int)(r % m) + 1 : (int)r + X.fn_lo;   // last axis: the window's layers
+            if (k < DIM - 1) r /= m;
+            else if (a < X.rn_lo || a > X.rn_hi) return;                      // not an owned row
             if (X.P == 2) q2_interp(a, X.nc[k], idx[k], wt[k]);
             else q1_interp(a, idx[k], wt[k]);
         }
@@ -113,8 +120,8 @@ __global__ void __launch_bounds__(256) xs_prolong_kernel(XArgs X, const double* 
                     for (int k = 0; k < DIM; ++k) {
                         const int ak = k == 0 ? idx[0][s0] : (k == 1 ? idx[1][s1] : idx[2][s2]);
                         const int m = X.P * X.nc[k];
-                        free_ = free_ && ak > 0 && ak < m;
-                        id += (int64_t)(ak - 1) * st;
+                        free_ = free_ && ak > 0 && ak < m && (k < DIM - 1 || (ak >= X.cn_lo && ak <= X.cn_hi));
+                        id += (int64_t)(k < DIM - 1 ? ak - 1 : ak - X.cn_lo) * st;
                         st *= m - 1;
                     }
                     if (!free_) continue;
@@ -138,8 +145,9 @@ __global__ void __launch_bounds__(256) xs_prolong_kernel(XArgs X, const double* 
 #pragma unroll
         for (int k = 0; k < DIM; ++k) {
             const int m = 2 * X.nc[k] + 1;
-            const int v = (int)(r % m);
-            r /= m;
+            const int v = k < DIM - 1 ? (int)(r % m) : (int)r + X.fv_lo;
+            if (k < DIM - 1) r /= m;
+            else if (v < X.rv_lo || v > X.rv_hi) return;
             q1_interp(v, idx[k], wt[k]);
         }
         double acc = 0.0;
@@ -153,12 +161,15 @@ __global__ void __launch_bounds__(256) xs_prolong_kernel(XArgs X, const double* 
                     if (DIM > 2) w *= wt[2][s2];
                     if (w == 0.0) continue;
                     int64_t id = 0, st = 1;
+                    bool in = true;
 #pragma unroll
                     for (int k = 0; k < DIM; ++k) {
                         const int ak = k == 0 ? idx[0][s0] : (k == 1 ? idx[1][s1] : idx[2][s2]);
-                        id += (int64_t)ak * st;
+                        in = in && (k < DIM - 1 || (ak >= X.cv_lo && ak <= X.cv_hi));
+                        id += (int64_t)(k < DIM - 1 ? ak : ak - X.cv_lo) * st;
                         st *= X.nc[k] + 1;
                     }
+                    if (!in) continue;
                     acc = fma(w, __ldg(xc + X.nvel_c + id), acc);
                 }
         double* yp = yf + X.nvel_f + (t - X.nfree_f);
@@ -181,11 +192,11 @@ __global__ void __launch_bounds__(256) xs_restrict_kernel(XArgs X, const double*
 #pragma unroll
         for (int k = 0; k < DIM; ++k) {
             const int m = X.P * X.nc[k] - 1;
-            const int c = (int)(r % m) + 1;
-            r /= m;
-            const int hi = 2 * X.P * X.nc[k] - 1;
-            if (X.P == 2) q2_gather(c, 1, hi, idx[k], wt[k]);
-            else q1_gather(c, 1, hi, idx[k], wt[k]);
+            const int c = k < DIM - 1 ? (int)(r % m) + 1 : (int)r + X.cn_lo;
+            if (k < DIM - 1) r /= m;
+            const int lo = k < DIM - 1 ? 1 : X.rn_lo, hi = k < DIM - 1 ? 2 * X.P * X.nc[k] - 1 : X.rn_hi;
+            if (X.P == 2) q2_gather(c, lo, hi, idx[k], wt[k]);
+            else q1_gather(c, lo, hi, idx[k], wt[k]);
         }
         double acc[DIM];
 #pragma unroll
@@ -203,7 +214,7 @@ __global__ void __launch_bounds__(256) xs_restrict_kernel(XArgs X, const double*
 #pragma unroll
                     for (int k = 0; k < DIM; ++k) {
                         const int ak = k == 0 ? idx[0][s0] : (k == 1 ? idx[1][s1] : idx[2][s2]);
-                        id += (int64_t)(ak - 1) * st;
+                        id += (int64_t)(k < DIM - 1 ? ak - 1 : ak - X.fn_lo) * st;
                         st *= 2 * X.P * X.nc[k] - 1;
                     }
                     double rv[DIM];
@@ -223,9 +234,9 @@ __global__ void __launch_bounds__(256) xs_restrict_kernel(XArgs X, const double*
 #pragma unroll
         for (int k = 0; k < DIM; ++k) {
             const int m = X.nc[k] + 1;
-            const int c = (int)(r % m);
-            r /= m;
-            q1_gather(c, 0, 2 * X.nc[k], idx[k], wt[k]);
+            const int c = k < DIM - 1 ? (int)(r % m) : (int)r + X.cv_lo;
+            if (k < DIM - 1) r /= m;
+            q1_gather(c, k < DIM - 1 ? 0 : X.rv_lo, k < DIM - 1 ? 2 * X.nc[k] : X.rv_hi, idx[k], wt[k]);
         }
         double acc = 0.0;
 #pragma unroll
@@ -241,7 +252,7 @@ __global__ void __launch_bounds__(256) xs_restrict_kernel(XArgs X, const double*
 #pragma unroll
                     for (int k = 0; k < DIM; ++k) {
                         const int ak = k == 0 ? idx[0][s0] : (k == 1 ? idx[1][s1] : idx[2][s2]);
-                        id += (int64_t)ak * st;
+                        id += (int64_t)(k < DIM - 1 ? ak : ak - X.fv_lo) * st;
                         st *= 2 * X.nc[k] + 1;
                     }
                     acc = fma(w, __ldg(rf + X.nvel_f + id), acc);
@@ -280,12 +291,16 @@ XArgs make_args(const XStruct& S) {
     X.dim = S.dim;
     X.P = S.P;
     for (int k = 0; k < 3; ++k) X.nc[k] = k < S.dim ? S.nc[k] : 1;
+    X.fn_lo = S.fn_lo; X.fn_hi = S.fn_hi; X.fv_lo = S.fv_lo; X.fv_hi = S.fv_hi;
+    X.rn_lo = S.rn_lo; X.rn_hi = S.rn_hi; X.rv_lo = S.rv_lo; X.rv_hi = S.rv_hi;
+    X.cn_lo = S.cn_lo; X.cn_hi = S.cn_hi; X.cv_lo = S.cv_lo; X.cv_hi = S.cv_hi;
     X.nfree_f = X.nfree_c = X.nvert_f = X.nvert_c = 1;
-    for (int k = 0; k < S.dim; ++k) {
-        X.nfree_f *= (int64_t)(2 * S.P * X.nc[k] - 1);
-        X.nfree_c *= (int64_t)(S.P * X.nc[k] - 1);
-        X.nvert_f *= (int64_t)(2 * X.nc[k] + 1);
-        X.nvert_c *= (int64_t)(X.nc[k] + 1);
+    for (int k = 0; k < S.dim; ++k) {   // last axis: the window's layers
+        const bool last = k == S.dim - 1;
+        X.nfree_f *= last ? (int64_t)(S.fn_hi - S.fn_lo + 1) : (int64_t)(2 * S.P * X.nc[k] - 1);
+        X.nfree_c *= last ? (int64_t)(S.cn_hi - S.cn_lo + 1) : (int64_t)(S.P * X.nc[k] - 1);
+        X.nvert_f *= last ? (int64_t)(S.fv_hi - S.fv_lo + 1) : (int64_t)(2 * X.nc[k] + 1);
+        X.nvert_c *= last ? (int64_t)(S.cv_hi - S.cv_lo + 1) : (int64_t)(X.nc[k] + 1);
     }
     X.nvel_f = S.dim * X.nfree_f;
     X.nvel_c = S.dim * X.nfree_c;
@@ -300,7 +315,6 @@ rav_status xs_build(const rav_grid* f, const rav_grid* c, int64_t n_fine, int64_
     if (f->dim != c->dim || (f->dim != 2 && f->dim != 3)) { set_error("structured transfer: dim mismatch"); return RAV_ERR_ARG; }
     const int Pf = f->vel_order == 1 ? 1 : 2, Pc = c->vel_order == 1 ? 1 : 2;
     if (Pf != Pc) { set_error("structured transfer: element pairs differ"); return RAV_ERR_ARG; }
-    if (f->win || c->win) { set_error("structured transfer: slab windows keep the CSR transfer"); return RAV_ERR_ARG; }
     for (int k = 0; k < f->dim; ++k)
         if (c->ncell[k] < 1 || f->ncell[k] != 2 * c->ncell[k]) {
             set_error("structured transfer: the fine grid must be the uniform refinement of the coarse one");
@@ -309,6 +323,27 @@ rav_status xs_build(const rav_grid* f, const rav_grid* c, int64_t n_fine, int64_
     S.dim = f->dim;
     S.P = Pf;
     for (int k = 0; k < 3; ++k) S.nc[k] = k < f->dim ? c->ncell[k] : 1;
+    // last-axis windows: whole grids take every free node layer / vertex layer
+    const int L = f->dim - 1;
+    const int fnm = Pf * f->ncell[L] - 1, cnm = Pf * c->ncell[L] - 1;   // free node layers 1 .. m
+    if (f->win) {
+        S.fn_lo = f->node_lo; S.fn_hi = f->node_hi; S.fv_lo = f->vert_lo; S.fv_hi = f->vert_hi;
+        S.rn_lo = f->rnode_lo; S.rn_hi = f->rnode_hi; S.rv_lo = f->rvert_lo; S.rv_hi = f->rvert_hi;
+    } else {
+        S.fn_lo = S.rn_lo = 1; S.fn_hi = S.rn_hi = fnm;
+        S.fv_lo = S.rv_lo = 0; S.fv_hi = S.rv_hi = f->ncell[L];
+    }
+    if (c->win) {
+        S.cn_lo = c->node_lo; S.cn_hi = c->node_hi; S.cv_lo = c->vert_lo; S.cv_hi = c->vert_hi;
+    } else {
+        S.cn_lo = 1; S.cn_hi = cnm; S.cv_lo = 0; S.cv_hi = c->ncell[L];
+    }
+    if (S.fn_lo < 1 || S.fn_hi > fnm || S.fn_lo > S.fn_hi || S.cn_lo < 1 || S.cn_hi > cnm || S.cn_lo > S.cn_hi ||
+        S.fv_lo < 0 || S.fv_hi > f->ncell[L] || S.cv_lo < 0 || S.cv_hi > c->ncell[L] ||
+        S.rn_lo < S.fn_lo || S.rn_hi > S.fn_hi || S.rv_lo < S.fv_lo || S.rv_hi > S.fv_hi) {
+        set_error("structured transfer: inconsistent slab windows");
+        return RAV_ERR_ARG;
+    }
     const XArgs X = make_args(S);
     if (X.nvel_f + X.nvert_f != n_fine || X.nvel_c + X.nvert_c != n_coarse) {
         set_error("structured transfer: grid sizes (%lld x %lld) do not match P (%lld x %lld)",

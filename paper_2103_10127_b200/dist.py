@@ -774,6 +774,7 @@ def build_lib_dist(problem: Dict, n_levels: int, nsub: int, local_ids: Sequence[
                 fine = dict(probs[k], window=slabs[k][i].transfer_window())
                 crs = dict(probs[k + 1], window=dict(slabs[k + 1][i].window)) if k + 1 < K else probs[K]
                 subs[k][i]["prol"] = rg.gen_prolongation(fine, crs)
+                subs[k][i]["prol_grids"] = (fine, crs)   # -> the stencil form (mgd_setup verifies it)
     mgd = rg.DistMultigrid(comm, sub_proc, local_ids, subs, coarse=coarse, variant=variant, stream=stream,
                            via_comm=via_comm, deterministic=deterministic)
     mgd._keep = (subs, coarse)

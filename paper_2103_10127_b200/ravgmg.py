@@ -71,7 +71,8 @@ class RavSubdomain(C.Structure):
     _fields_ = [("A", RavCsr), ("P", RavPatches), ("n_vel", C.c_int64), ("n_neighbors", C.c_int32),
                 ("neighbors", C.c_void_p), ("n_ghost_written", C.c_int64), ("ghost_written", C.c_void_p),
                 ("owned", C.c_int64 * 4), ("P_coarse", RavCsr), ("n_colors", C.c_int32),
-                ("color_offs", C.c_void_p), ("color_ids", C.c_void_p)]
+                ("color_offs", C.c_void_p), ("color_ids", C.c_void_p),
+                ("grid_fine", C.c_void_p), ("grid_coarse", C.c_void_p)]
 
 
 class RavOpts(C.Structure):
@@ -693,6 +694,10 @@ class DistMultigrid:
                 sd.owned[0], sd.owned[1], sd.owned[2], sd.owned[3] = int(a0), int(b0), int(a1), int(b1)
                 if d.get("prol") is not None:
                     sd.P_coarse = csr(d["prol"], n_cols=d["prol"]["nc"])
+                if d.get("prol_grids") is not None:
+                    gf, gc = grid(d["prol_grids"][0]), grid(d["prol_grids"][1])
+                    keep.append((gf, gc))
+                    sd.grid_fine, sd.grid_coarse = C.addressof(gf), C.addressof(gc)
                 if d.get("colors") is not None:
                     offs = np.ascontiguousarray(d["colors"][0], dtype=np.int64)
                     ids = np.ascontiguousarray(d["colors"][1], dtype=np.int32)

@@ -5,6 +5,8 @@ the library's NVTX range "mg_vcycle".
     ncu --nvtx --nvtx-include "mg_vcycle/" --metrics gpu__time_duration.sum --clock-control none \
         --csv --log-file out.csv python scripts/cycle_breakdown.py c3
     python scripts/cycle_breakdown.py --summarize out.csv
+    (python scripts/cycle_breakdown.py c3 N: the slab-partitioned cycle, N subdomains on this GPU,
+     NVTX range "mgd_vcycle")
 """
 import csv
 import os
@@ -28,9 +30,9 @@ if len(sys.argv) > 2 and sys.argv[1] == "--summarize":
         per[key][0] += 1
         per[key][1] += v
         tot += v
-    print(f"total {tot / 1e3 / 3:.3f} ms per cycle (3 cycles profiled), {sum(c for c, _ in per.values()) // 3} launches per cycle")
+    print(f"total {tot / 3e6:.3f} ms per cycle (3 cycles profiled), {sum(c for c, _ in per.values()) // 3} launches per cycle")
     for (k, g), (c, v) in sorted(per.items(), key=lambda kv: -kv[1][1])[:40]:
-        print(f"{v / 3e3:9.3f} ms  {c // 3:4d}x  {k:40s} grid {g}")
+        print(f"{v / 3e3:9.1f} us  {c // 3:4d}x  {k:40s} grid {g}")
     sys.exit(0)
 
 import torch
@@ -40,6 +42,16 @@ from paper_2103_10127_b200 import ravgmg as rg
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 c = si.CONFIGS[name]
+if len(sys.argv) > 2:   # the slab-partitioned cycle with N subdomains on this GPU (NVTX range "mgd_vcycle")
+    from paper_2103_10127_b200 import dist as rdist
+    N = int(sys.argv[2])
+    comm = rg.Comm(1, 0, None)
+    mgd, info = rdist.build_lib_dist(si.config_problem(name), c["levels"], N, list(range(N)), [0] * N, comm)
+    xs = [torch.zeros_like(v) for v in info["x"]]
+    for _ in range(3):
+        mgd.vcycle(xs, info["b"], c["pre"], c["post"], c["omega"])
+    torch.cuda.synchronize()
+    sys.exit(0)
 mg, fine = rg.build_hierarchy(si.config_problem(name), c["levels"], "pou")
 x = torch.zeros(fine["n"], dtype=torch.float64, device="cuda")
 mg.vcycle(x, fine["b"], c["pre"], c["post"], c["omega"])

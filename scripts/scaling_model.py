@@ -76,7 +76,7 @@ def link_bytes(subs, sweeps_per_level):
     return worst
 
 
-def vcycle_case(name, Ns):
+def vcycle_case(name, Ns, agg_layers=0):
     c = si.CONFIGS[name]
     prob = si.config_problem(name)
     pre, post, om = c["pre"], c["post"], c["omega"]
@@ -87,14 +87,14 @@ def vcycle_case(name, Ns):
     mg.close()
     del mg, x, fine
     torch.cuda.empty_cache()
-    out = {"config": name, "T1_s_per_cycle": t1, "N": {}}
+    out = {"config": name, "agg_layers": agg_layers, "T1_s_per_cycle": t1, "N": {}}
     comm0 = rg.Comm(1, 0, None)
     comm1 = rg.Comm(1, 0, rg.Comm.unique_id())
     for N in Ns:
         row = {}
         for via, comm in ((False, comm0), (True, comm1)):
             mgd, info = rdist.build_lib_dist(prob, c["levels"], N, list(range(N)), [0] * N, comm, via_comm=via,
-                                             stream=STREAM)
+                                             stream=STREAM, agg_layers=agg_layers)
             xs = [torch.zeros_like(v) for v in info["x"]]
             t = timed(lambda: mgd.vcycle(xs, info["b"], pre, post, om), 5)
             row["T_emul_nccl_s" if via else "T_emul_s"] = t
@@ -184,9 +184,16 @@ def smooth_case(name, Ns, sweeps):
 
 
 res = {"model": __doc__.strip(), "gpu": torch.cuda.get_device_name(0)}
-res["c2_weak_sweeps"] = smooth_case("c2", (2, 4, 8), 20)
-res["c5_weak_sweeps"] = smooth_case("c5", (2, 4), 10)
-res["c4_vcycle"] = vcycle_case("c4", (2, 4, 8))
-res["c3_vcycle"] = vcycle_case("c3", (2, 4, 8))
+which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["c2", "c5", "c4", "c3"]
+if "c2" in which:
+    res["c2_weak_sweeps"] = smooth_case("c2", (2, 4, 8), 20)
+if "c5" in which:
+    res["c5_weak_sweeps"] = smooth_case("c5", (2, 4), 10)
+if "c4" in which:
+    res["c4_vcycle"] = vcycle_case("c4", (2, 4, 8))
+if "c3" in which:
+    res["c3_vcycle"] = vcycle_case("c3", (2, 4, 8))
+for agg in [int(a) for a in (sys.argv[3].split(",") if len(sys.argv) > 3 else [])]:
+    res[f"c3_vcycle_agg{agg}"] = vcycle_case("c3", (2, 4, 8), agg_layers=agg)
 with open(OUT, "w") as f:
     json.dump(res, f, indent=1)
