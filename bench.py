@@ -280,8 +280,15 @@ def run_vcycle(name, rg, si, stream, dist):
               "time_to_rtol_s": ft, "restart": 30}
     except Exception as err:  # report, keep the line
         fg = {"error": f"{type(err).__name__}: {err}"[:200]}
+    # HBM roofline of the whole cycle: mg_cycle_bytes (algorithmic bytes of every kernel of a cycle
+    # + the stopping test's residual) / the measured time per cycle
+    cyc_bytes = mg.cycle_bytes(c["pre"], c["post"])
+    peak, peak_kind = load_peaks()
+    ach = cyc_bytes / (t / max(iters, 1)) / 1e9
     out = {"config": VCYCLE_DESC[name], "free_dofs": fine["n"], "rtol": c["rtol"], "cycles": iters, "converged": bool(hist[-1] <= c["rtol"] * hist[0]),
            "time_to_rtol_s": t, "ms_per_cycle": t / max(iters, 1) * 1e3, "avg_reduction_factor": rho,
+           "roofline": {"bound": "hbm", "algorithmic_gb_per_cycle": cyc_bytes / 1e9, "achieved": ach,
+                        "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": ach / peak},
            "setup_s": setup_s, "gpu_launches": launches, "timing": "CUDA events around mg_solve, best of 3",
            "fgmres": fg}
     mg.close()

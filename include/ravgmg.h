@@ -576,6 +576,12 @@ int64_t rav_last_launches(const rav_ctx* ctx);
  * RAV_ERR_ARG for n_vel > n, mode not 0/1, pin outside [n_vel, n) in mode 0. */
 rav_status rav_pressure_normalize(double* x, int64_t n_vel, int64_t n, int mode, int64_t pin, void* stream);
 int64_t mg_last_launches(const mg_ctx* ctx);
+/* Algorithmic HBM bytes of one V(pre, post) cycle of mg_solve (the roofline of the V-cycle
+ * metric): per smoothed level, (pre + post) sweeps of the sweep kernel and one residual launch per
+ * sweep (below the finest level the first sweep's residual is b itself) + the restriction's
+ * residual on the finest level, each at rav_sweep_bytes' figures; the transfers' vector traffic
+ * (stencil form) or CSR bytes; the coarse solve's explicit inverse. */
+rav_status mg_cycle_bytes(const mg_ctx* ctx, int pre, int post, double* bytes);
 /* rav_pressure_normalize on the finest level of the hierarchy (its n_vel from
  * mg_setup; mode 0 pins the first pressure DoF, i.e. vertex 0 in the generator's
  * numbering).  x: device pointer, stream-ordered on the context stream. */

@@ -554,6 +554,28 @@ rav_status mg_solve(mg_ctx* m, double* x, const double* b, int pre, int post, do
 
 int64_t mg_last_launches(const mg_ctx* m) { return m ? m->last_launches : 0; }
 
+rav_status mg_cycle_bytes(const mg_ctx* m, int pre, int post, double* bytes) {
+    if (!m || !bytes || pre < 0 || post < 0) { set_error("mg_cycle_bytes: bad arguments"); return RAV_ERR_ARG; }
+    double tot = 0.0;
+    for (int l = 1; l < m->L; ++l) {
+        const mg_level& L = m->lv[l];
+        const double nf = (double)L.A.n_rows, nc = (double)m->lv[l - 1].A.n_rows;
+        double bs = 0.0, br = 0.0;
+        RAV_TRY(rav_sweep_bytes(L.sm, &bs, &br, nullptr));
+        // residual launches: one per sweep but the first below the finest level (x = 0: it reads b),
+        // + the restriction's; the finest level's first sweep reuses the stopping test's residual,
+        // which mg_solve adds (same count)
+        const int nres = pre + post + (l == m->L - 1 ? 1 : 0);
+        tot += (pre + post) * bs + nres * br;
+        if (L.xs.on) tot += 8.0 * (nc + 2.0 * nf) + (L.xs.dim == 2 ? 8.0 * (nf + nc) : 12.0 * L.PT.nnz + 8.0 * (nf + 2.0 * nc));
+        else tot += 2.0 * (12.0 * (double)L.P.nnz) + 8.0 * (3.0 * nf + 2.0 * nc);
+        if (l - 1 > 0) tot += 8.0 * nc;   // zeroing the coarse correction
+    }
+    tot += 8.0 * (double)m->C.m * (double)m->C.m;   // the coarse solve's explicit inverse
+    *bytes = tot;
+    return RAV_OK;
+}
+
 rav_status mg_normalize_pressure(mg_ctx* m, double* x, int mode) {
     if (!m || !x || (mode != 0 && mode != 1)) { set_error("mg_normalize_pressure: bad argument"); return RAV_ERR_ARG; }
     if (!is_device_ptr(x)) { set_error("mg_normalize_pressure: x must be a device pointer"); return RAV_ERR_ARG; }

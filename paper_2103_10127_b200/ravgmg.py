@@ -132,6 +132,7 @@ def _load():
         "mgd_host_time": [vp, P(dbl), P(dbl), P(C.c_int)],
         "rav_pressure_normalize": [vp, i64, i64, C.c_int, i64, vp],
         "mg_normalize_pressure": [vp, vp, C.c_int],
+        "mg_cycle_bytes": [vp, C.c_int, C.c_int, P(dbl)],
         "rav_adaptive_sizes": [vp, C.c_int, P(i64), P(i64), P(i64), P(i64), P(i64), P(i64), P(i64)],
         "rav_adaptive_fill": [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
     }
@@ -412,6 +413,12 @@ class Multigrid:
         """mg_normalize_pressure (row a10, R4): mode 0 p -= p(vertex 0), mode 1 p -= mean(p)."""
         _check(lib.mg_normalize_pressure(self.ctx, _ptr(x), int(mode)))
         return x
+
+    def cycle_bytes(self, pre=2, post=2) -> float:
+        """mg_cycle_bytes: algorithmic HBM bytes of one V(pre, post) cycle."""
+        out = C.c_double()
+        _check(lib.mg_cycle_bytes(self.ctx, int(pre), int(post), C.byref(out)))
+        return out.value
 
     @property
     def last_launches(self) -> int:
