@@ -572,8 +572,16 @@ def run_adaptive_study(rg, si, stream, max_levels=7):
     return out
 
 
+def _transport():
+    """RAV_MGD_TRANSPORT=peer: the peer-memory transport (mgd_setup via_comm = 2: pack kernels store
+    into the neighbour's receive buffer over NVLink and release its flag); default nccl."""
+    return "peer" if os.environ.get("RAV_MGD_TRANSPORT", "nccl") == "peer" else "nccl"
+
+
 def _dist_build(rdist, rg, prob, levels, ws, rank, comm, gather, stream, **kw):
     """One rank's share of the library-driven slab-partitioned hierarchy (mgd_setup)."""
+    if _transport() == "peer" and kw.get("variant", 0) != 2:
+        kw.setdefault("via_comm", 2)
     return rdist.build_lib_dist(prob, levels, ws, [rank], list(range(ws)), comm, gather=gather, stream=stream, **kw)
 
 
@@ -768,7 +776,9 @@ def run_gpu_dist(args):
                                "MMS forcing, seeded eta; step = 100 slab-partitioned RAV sweeps inside the library "
                                "(residual, RAV sweep, NCCL interface-correction sum + halo refresh; one CUDA graph)",
                    "free_dofs": n_glob, "sweeps_per_step": SWEEPS_PER_STEP, "omega": OMEGA,
-                   "parallelism": f"slab partition x{ws} (mgd_smooth, NCCL point-to-point)",
+                   "parallelism": f"slab partition x{ws} (mgd_smooth, "
+                                  + ("peer-memory transport over NVLink)" if _transport() == "peer"
+                                     else "NCCL point-to-point)"),
                    "partition": [list(p) for p in info["parts"][0]],
                    "l2": "inputs larger than L2 (factor rows + node-blocked operator stream from HBM every sweep)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

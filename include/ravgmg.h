@@ -513,10 +513,20 @@ typedef struct mgd_ctx mgd_ctx;
  * (global id local_ids[i], ascending) on partitioned level k = 0 (finest) ..
  * n_levels-1.  coarse: the agglomerated hierarchy below (mg_setup on the whole
  * grids; caller-owned, must outlive the context; its stream is set to
- * opts->stream), or NULL for smoothing only (mgd_smooth).  via_comm = 1 routes
- * the exchanges between local subdomains through the communicator's NCCL
- * self sends too (verification on one GPU).  Every message size is checked
- * against the peer's list (RAV_ERR_ARG on a mismatch).  opts as for rav_setup. */
+ * opts->stream), or NULL for smoothing only (mgd_smooth).  Transport (via_comm):
+ * 0 = messages to other processes through NCCL, between local subdomains the
+ * receiver reads the sender's packed buffer; 1 = every message through NCCL
+ * (the local ones by self sends: verification on one GPU); 2 = the peer-memory
+ * transport: the pack kernel stores each message straight into the consumer's
+ * receive buffer (CUDA IPC mapping of the other process's block over NVLink, a
+ * plain pointer for a local subdomain) and releases the consumer's flag; the
+ * consumer's unpack kernel acquires it and releases the producer's ack; no
+ * NCCL call on the data path (NCCL only carries the setup's handle exchange
+ * and the per-cycle coarse-rhs / norm all-gathers between processes).  Waits
+ * are bounded (~4 s): a timeout is reported as RAV_ERR_COMM by the next
+ * mgd_solve / mgd_residual_norm.  RAV / AV / diagonal Vanka only (MV: RAV_ERR_ARG).
+ * Every message size is checked against the peer's list (RAV_ERR_ARG on a
+ * mismatch).  opts as for rav_setup. */
 rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, int n_local,
                      const int32_t* local_ids, int n_levels, const rav_subdomain* subs, mg_ctx* coarse,
                      const rav_opts* opts, int via_comm, mgd_ctx** out);

@@ -94,20 +94,67 @@ bool is_dev(const void* p) {
 enum { OP_GATHER = 0, OP_SCATTER = 1, OP_ADD = 2, OP_ZERO = 3, OP_DIFF = 4, OP_ADD_ATOMIC = 5 };
 constexpr int MAX_VEC = 64;
 
+// Peer-memory transport (mgd_setup via_comm = 2): a message is written by the producer's pack
+// step straight into the consumer's receive buffer (a peer-mapped allocation over NVLink when the
+// consumer is another process / GPU), then the producer's last CTA sets the consumer's flag to the
+// message's sequence number (release, system scope).  The consumer's step waits for the flag
+// (acquire), applies the message and sets the producer's ack (so the producer does not overwrite
+// a buffer that has not been consumed: it waits for ack >= its previous sequence number).  No
+// NCCL call, no host involvement: the exchange is the pack / unpack kernels themselves, captured
+// in the cycle's CUDA graph (the sequence counters live in device memory).  Every wait is bounded
+// (~4 s): on a timeout the kernel records it in g_peer_timeout and goes on, so a broken peer can
+// give wrong numbers but never a hung GPU; mgd_* return RAV_ERR_COMM when it is set.
+enum { ROLE_NONE = 0, ROLE_PRODUCER = 1, ROLE_CONSUMER = 2 };
+
 struct Step {
     int op;
     int vec;                 // index into the launch's vector table
     const int32_t* idx;      // device
     int64_t n;
-    double* buf;             // device message buffer (own, or the local sender's)
+    double* buf;             // device message buffer (own, the local sender's, or the peer's receive buffer)
+    int role;                // ROLE_*: peer-transport synchronisation of this step
+    unsigned long long* sig; // producer: the consumer's flag (remote); consumer: its own flag
+    unsigned long long* ack; // producer: its own ack word; consumer: the producer's ack (remote)
+    unsigned long long* seq; // this end's message counter (local)
+    unsigned int* done;      // CTAs of this step that finished (local)
 };
 struct VecTab {
     double* v[MAX_VEC];
 };
 
+__device__ unsigned int g_peer_timeout = 0;
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ void wait_geq(const unsigned long long* p, unsigned long long v) {
+    for (long long spin = 0; ld_acquire_sys(p) < v; ++spin) {
+        if (spin > (1ll << 24)) {   // ~4 s at 256 ns per poll
+            atomicOr(&g_peer_timeout, 1u);
+            return;
+        }
+        __nanosleep(256);
+    }
+}
+
 __global__ void __launch_bounds__(256) phase_kernel(const Step* __restrict__ steps, VecTab vt) {
     const Step st = steps[blockIdx.y];
     double* V = vt.v[st.vec];
+    __shared__ unsigned long long s_target;
+    if (st.role != ROLE_NONE) {
+        if (threadIdx.x == 0) {
+            const unsigned long long s = *reinterpret_cast<volatile unsigned long long*>(st.seq);
+            s_target = s + 1;
+            if (st.role == ROLE_PRODUCER) wait_geq(st.ack, s);   // the previous message was consumed
+            else wait_geq(st.sig, s + 1);                        // this message has arrived
+        }
+        __syncthreads();
+    }
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < st.n; k += (int64_t)gridDim.x * blockDim.x) {
         const int32_t i = st.idx[k];
         switch (st.op) {
@@ -117,6 +164,16 @@ __global__ void __launch_bounds__(256) phase_kernel(const Step* __restrict__ ste
             case OP_ZERO: V[i] = 0.0; break;
             case OP_DIFF: st.buf[k] = V[i] - st.buf[k]; break;
             default: atomicAdd(V + i, st.buf[k]); break;
+        }
+    }
+    if (st.role != ROLE_NONE) {
+        __threadfence_system();   // this CTA's payload stores (producer) / reads (consumer) are done
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(st.done, 1u) == gridDim.x - 1) {   // the step's last CTA
+            *st.done = 0;
+            *st.seq = s_target;
+            __threadfence_system();
+            st_release_sys(st.role == ROLE_PRODUCER ? st.sig : st.ack, s_target);
         }
     }
 }
@@ -156,6 +213,17 @@ struct DNb {
     double *cs_buf = nullptr, *hs_buf = nullptr, *rs_buf = nullptr;   // rs: reverse halo (hr -> owner)
     double *cr_in = nullptr, *hr_in = nullptr, *rr_in = nullptr;      // rr: reverse halo received at hs
     std::vector<void*> allocs;
+    // peer transport, per message type t (0 corrections, 1 halo, 2 reverse halo):
+    // producing end: the consumer's receive buffer and flag, own ack; consuming end: own flag, the
+    // producer's ack; each end its own sequence counter and CTA counter
+    double* out_buf[3] = {nullptr, nullptr, nullptr};
+    unsigned long long *out_sig[3] = {nullptr, nullptr, nullptr}, *my_ack[3] = {nullptr, nullptr, nullptr};
+    unsigned long long *my_flag[3] = {nullptr, nullptr, nullptr}, *peer_ack[3] = {nullptr, nullptr, nullptr};
+    unsigned long long *seq_p[3] = {nullptr, nullptr, nullptr}, *seq_c[3] = {nullptr, nullptr, nullptr};
+    unsigned int *done_p[3] = {nullptr, nullptr, nullptr}, *done_c[3] = {nullptr, nullptr, nullptr};
+    int64_t n_out(int t) const { return t == 0 ? ncs : t == 1 ? nhs : nhr; }   // produced entries
+    int64_t n_in(int t) const { return t == 0 ? ncr : t == 1 ? nhr : nhs; }    // consumed entries
+    double*& in_buf(int t) { return t == 0 ? cr_in : t == 1 ? hr_in : rr_in; }
 };
 
 struct DSub {                     // one local subdomain on one partitioned level
@@ -202,7 +270,11 @@ struct mgd_ctx {
     std::vector<std::vector<int32_t*>> plist;   // [K][nl] device colour-major patch lists (MV)
     std::vector<std::vector<std::vector<int64_t>>> coffs;   // [K][nl] colour offsets (MV)
     cudaStream_t stream = nullptr;
-    bool via_comm = false;
+    bool via_comm = false;                      // every exchange through NCCL (verification)
+    bool peer = false;                          // peer-memory transport (via_comm = 2)
+    void* peer_block = nullptr;                 // receive buffers + flags + acks (exported by CUDA IPC)
+    void* sync_block = nullptr;                 // sequence / CTA counters (local)
+    std::vector<void*> peer_opened;             // other processes' peer blocks (cudaIpcOpenMemHandle)
     // pack / unpack phases per level
     struct LvPhases {
         Phase zero_gw, pack_c, add_c, pack_h, unpack_h, pack_r, add_r, diff_c;
@@ -533,7 +605,173 @@ void mgd_destroy(mgd_ctx* m) {
                       m->dot_part})
         if (p) cudaFree(p);
     if (m->h_nrm) cudaFreeHost(m->h_nrm);
+    for (void* p : m->peer_opened) cudaIpcCloseMemHandle(p);
+    if (m->peer_block) cudaFree(m->peer_block);
+    if (m->sync_block) cudaFree(m->sync_block);
     delete m;
+}
+
+
+// ---- peer-memory transport setup (via_comm = 2) --------------------------------------------
+// One allocation per process holds the receive buffers, flags and ack words of all its message
+// ends; it is exported with CUDA IPC and the other processes map it (cudaIpcOpenMemHandle:
+// NVLink peer access between GPUs).  Each process publishes the offsets of its ends, keyed by
+// (type, level, source, destination, role), together with its IPC handle in one NCCL all-gather at
+// setup; subdomains of the same process use plain pointers.
+static rav_status peer_setup(mgd_ctx* m) {
+    struct Ent { int64_t t, k, src, dst, role, off_buf, off_flag, pad; };   // role 0 consumer end, 1 producer end
+    struct Slot { int k, i, j, t, role; size_t ob, of; };
+    std::vector<Ent> mine;
+    std::vector<Slot> slots;
+    size_t bytes = 0;
+    auto take = [&](size_t b) {
+        const size_t o = bytes;
+        bytes += (b + 255) & ~(size_t)255;
+        return o;
+    };
+    bool any_remote = false;
+    for (int k = 0; k < m->K; ++k)
+        for (int i = 0; i < m->nl; ++i) {
+            DSub& S = m->lv[k][i];
+            for (int j = 0; j < (int)S.nb.size(); ++j) {
+                DNb& B = S.nb[j];
+                any_remote = any_remote || B.peer_local < 0;
+                for (int t = 0; t < 3; ++t) {
+                    if (B.n_in(t)) {
+                        const size_t ob = take(sizeof(double) * (size_t)B.n_in(t)), of = take(8);
+                        slots.push_back({k, i, j, t, 0, ob, of});
+                        mine.push_back({t, k, B.peer, S.gid, 0, (int64_t)ob, (int64_t)of, 0});
+                    }
+                    if (B.n_out(t)) {
+                        const size_t of = take(8);
+                        slots.push_back({k, i, j, t, 1, 0, of});
+                        mine.push_back({t, k, S.gid, B.peer, 1, 0, (int64_t)of, 0});
+                    }
+                }
+            }
+        }
+    RAV_CUDA(cudaMalloc(&m->peer_block, std::max<size_t>(bytes, 256)));
+    RAV_CUDA(cudaMemset(m->peer_block, 0, std::max<size_t>(bytes, 256)));
+    const size_t ns = std::max<size_t>(1, slots.size());
+    RAV_CUDA(cudaMalloc(&m->sync_block, 16 * ns));
+    RAV_CUDA(cudaMemset(m->sync_block, 0, 16 * ns));
+    char* base = static_cast<char*>(m->peer_block);
+    auto* seqs = static_cast<unsigned long long*>(m->sync_block);
+    auto* dones = reinterpret_cast<unsigned int*>(seqs + ns);
+    for (size_t q = 0; q < slots.size(); ++q) {
+        const Slot& z = slots[q];
+        DNb& B = m->lv[z.k][z.i].nb[z.j];
+        if (z.role == 0) {
+            B.in_buf(z.t) = reinterpret_cast<double*>(base + z.ob);
+            B.my_flag[z.t] = reinterpret_cast<unsigned long long*>(base + z.of);
+            B.seq_c[z.t] = seqs + q;
+            B.done_c[z.t] = dones + q;
+        } else {
+            B.my_ack[z.t] = reinterpret_cast<unsigned long long*>(base + z.of);
+            B.seq_p[z.t] = seqs + q;
+            B.done_p[z.t] = dones + q;
+        }
+    }
+    // the other ends: local subdomains directly
+    for (int k = 0; k < m->K; ++k)
+        for (int i = 0; i < m->nl; ++i) {
+            DSub& S = m->lv[k][i];
+            for (DNb& B : S.nb) {
+                if (B.peer_local < 0) continue;
+                DNb* R = nullptr;
+                for (DNb& c : m->lv[k][B.peer_local].nb)
+                    if (c.peer == S.gid) R = &c;
+                if (!R) { set_error("mgd_setup: peer transport: no reverse neighbour"); return RAV_ERR_ARG; }
+                for (int t = 0; t < 3; ++t) {
+                    if (B.n_out(t)) { B.out_buf[t] = R->in_buf(t); B.out_sig[t] = R->my_flag[t]; }
+                    if (B.n_in(t)) B.peer_ack[t] = R->my_ack[t];
+                }
+            }
+        }
+    if (any_remote) {   // other processes: IPC handles and offset tables through one NCCL all-gather
+        if (!m->comm->nc) { set_error("mgd_setup: the peer transport between processes needs NCCL for setup"); return RAV_ERR_ARG; }
+        const NcclApi& N = nccl();
+        const int np = m->comm->nprocs;
+        int64_t *dcnt = nullptr, *dtab = nullptr;
+        RAV_CUDA(cudaMalloc(&dcnt, sizeof(int64_t) * (np + 1)));
+        const int64_t cnt = (int64_t)mine.size();
+        RAV_CUDA(cudaMemcpy(dcnt + np, &cnt, sizeof(int64_t), cudaMemcpyHostToDevice));
+        RAV_NCCL(N.AllGather(dcnt + np, dcnt, 1, ncclInt64, m->comm->nc, m->stream));
+        std::vector<int64_t> counts(np);
+        RAV_CUDA(cudaMemcpyAsync(counts.data(), dcnt, sizeof(int64_t) * np, cudaMemcpyDeviceToHost, m->stream));
+        RAV_CUDA(cudaStreamSynchronize(m->stream));
+        const int64_t mx = *std::max_element(counts.begin(), counts.end());
+        const int64_t row = 8 + 8 * mx;   // IPC handle (64 bytes) + entries
+        std::vector<int64_t> h(row, 0);
+        cudaIpcMemHandle_t hd;
+        RAV_CUDA(cudaIpcGetMemHandle(&hd, m->peer_block));
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        memcpy(h.data(), &hd, 64);
+        if (cnt) memcpy(h.data() + 8, mine.data(), sizeof(Ent) * mine.size());
+        RAV_CUDA(cudaMalloc(&dtab, sizeof(int64_t) * row * (np + 1)));
+        RAV_CUDA(cudaMemcpy(dtab + row * np, h.data(), sizeof(int64_t) * row, cudaMemcpyHostToDevice));
+        RAV_NCCL(N.AllGather(dtab + row * np, dtab, (size_t)row, ncclInt64, m->comm->nc, m->stream));
+        std::vector<int64_t> all((size_t)row * np);
+        RAV_CUDA(cudaMemcpyAsync(all.data(), dtab, sizeof(int64_t) * row * np, cudaMemcpyDeviceToHost, m->stream));
+        RAV_CUDA(cudaStreamSynchronize(m->stream));
+        cudaFree(dcnt);
+        cudaFree(dtab);
+        std::vector<char*> bases(np, nullptr);
+        auto base_of = [&](int q) -> char* {
+            if (!bases[q]) {
+                cudaIpcMemHandle_t hq;
+                memcpy(&hq, all.data() + (size_t)row * q, 64);
+                void* p = nullptr;
+                if (cudaIpcOpenMemHandle(&p, hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    cudaGetLastError();
+                    return nullptr;
+                }
+                m->peer_opened.push_back(p);
+                bases[q] = static_cast<char*>(p);
+            }
+            return bases[q];
+        };
+        auto find = [&](int q, int64_t t, int64_t k, int64_t src, int64_t dst, int64_t role) -> const Ent* {
+            const Ent* e = reinterpret_cast<const Ent*>(all.data() + (size_t)row * q + 8);
+            for (int64_t u = 0; u < counts[q]; ++u)
+                if (e[u].t == t && e[u].k == k && e[u].src == src && e[u].dst == dst && e[u].role == role) return e + u;
+            return nullptr;
+        };
+        for (int k = 0; k < m->K; ++k)
+            for (int i = 0; i < m->nl; ++i) {
+                DSub& S = m->lv[k][i];
+                for (DNb& B : S.nb) {
+                    if (B.peer_local >= 0) continue;
+                    const int q = m->sub_proc[B.peer];
+                    char* bq = base_of(q);
+                    if (!bq) { set_error("mgd_setup: cudaIpcOpenMemHandle of process %d failed", q); return RAV_ERR_COMM; }
+                    for (int t = 0; t < 3; ++t) {
+                        if (B.n_out(t)) {
+                            const Ent* e = find(q, t, k, S.gid, B.peer, 0);
+                            if (!e) { set_error("mgd_setup: peer transport: message %d %d->%d has no receiver", t, S.gid, B.peer); return RAV_ERR_ARG; }
+                            B.out_buf[t] = reinterpret_cast<double*>(bq + e->off_buf);
+                            B.out_sig[t] = reinterpret_cast<unsigned long long*>(bq + e->off_flag);
+                        }
+                        if (B.n_in(t)) {
+                            const Ent* e = find(q, t, k, B.peer, S.gid, 1);
+                            if (!e) { set_error("mgd_setup: peer transport: message %d %d->%d has no sender", t, B.peer, S.gid); return RAV_ERR_ARG; }
+                            B.peer_ack[t] = reinterpret_cast<unsigned long long*>(bq + e->off_flag);
+                        }
+                    }
+                }
+            }
+    }
+    return RAV_OK;
+}
+
+static rav_status peer_check() {   // a bounded wait of the peer transport timed out
+    unsigned int h = 0;
+    RAV_CUDA(cudaMemcpyFromSymbol(&h, g_peer_timeout, sizeof(h)));
+    if (h) {
+        set_error("mgd: a peer-transport wait timed out (a peer did not reach the same exchange)");
+        return RAV_ERR_COMM;
+    }
+    return RAV_OK;
 }
 
 rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, int n_local, const int32_t* local_ids,
@@ -546,8 +784,12 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
         return RAV_ERR_ARG;
     }
     *out = nullptr;
-    if ((comm->nprocs > 1 || via_comm) && !comm->nc) {
-        set_error("mgd_setup: exchanges between processes (or via_comm) need a communicator with NCCL");
+    if ((comm->nprocs > 1 || via_comm == 1) && !comm->nc) {
+        set_error("mgd_setup: exchanges between processes (or via_comm = 1) need a communicator with NCCL");
+        return RAV_ERR_ARG;
+    }
+    if (via_comm == 2 && opts && opts->variant == RAV_VARIANT_MV) {
+        set_error("mgd_setup: the peer-memory transport (via_comm = 2) covers RAV / AV / diagonal Vanka");
         return RAV_ERR_ARG;
     }
     rav_opts o{};
@@ -562,7 +804,8 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
     m->coarse = coarse;
     m->stream = as_stream(o.stream);
     m->variant = o.variant;
-    m->via_comm = via_comm != 0;
+    m->via_comm = via_comm == 1;
+    m->peer = via_comm == 2;
     rav_status st = RAV_OK;
     std::map<int32_t, int> local_of;
     for (int i = 0; i < n_local; ++i) {
@@ -631,7 +874,7 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
                 B.peer = N.peer;
                 auto it = local_of.find(N.peer);
                 B.peer_local = it == local_of.end() ? -1 : it->second;
-                B.remote = B.peer_local < 0 || m->via_comm;
+                B.remote = B.peer_local < 0 || m->via_comm || m->peer;
                 B.ncs = N.n_corr_send; B.ncr = N.n_corr_recv; B.nhs = N.n_halo_send; B.nhr = N.n_halo_recv;
                 if (st == RAV_OK) st = upload_idx(N.corr_send, B.ncs, &B.cs, B.allocs);
                 if (st == RAV_OK) st = upload_idx(N.corr_recv, B.ncr, &B.cr, B.allocs);
@@ -640,7 +883,7 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
                 if (st == RAV_OK) st = alloc_buf(B.ncs, &B.cs_buf, B.allocs);
                 if (st == RAV_OK) st = alloc_buf(B.nhs, &B.hs_buf, B.allocs);
                 if (st == RAV_OK) st = alloc_buf(B.nhr, &B.rs_buf, B.allocs);
-                if (st == RAV_OK && B.remote) {
+                if (st == RAV_OK && B.remote && !m->peer) {   // peer transport: in the peer block
                     st = alloc_buf(B.ncr, &B.cr_in, B.allocs);
                     if (st == RAV_OK) st = alloc_buf(B.nhr, &B.hr_in, B.allocs);
                     if (st == RAV_OK) st = alloc_buf(B.nhs, &B.rr_in, B.allocs);
@@ -703,6 +946,7 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
                     B.rr_in = R->rs_buf;   // its ghost partials for my owned DoFs
                 }
             }
+    if (st == RAV_OK && m->peer) st = peer_setup(m);
     // phases and NCCL messages
     for (int k = 0; k < n_levels && st == RAV_OK; ++k) {
         auto& P = m->ph[k];
@@ -712,6 +956,23 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
             if (S.ngw) P.zero_gw.h.push_back({OP_ZERO, i, S.gw, S.ngw, nullptr});
             for (auto& B : S.nb) {
                 const int pp = m->sub_proc[B.peer];
+                if (m->peer) {   // producers write the consumers' buffers; no NCCL messages
+                    auto prod = [&](int t) {
+                        return Step{OP_GATHER, i, t == 0 ? B.cs : t == 1 ? B.hs : B.hr, B.n_out(t), B.out_buf[t],
+                                    ROLE_PRODUCER, B.out_sig[t], B.my_ack[t], B.seq_p[t], B.done_p[t]};
+                    };
+                    auto cons = [&](int t, int op) {
+                        return Step{op, i, t == 0 ? B.cr : t == 1 ? B.hr : B.hs, B.n_in(t), B.in_buf(t),
+                                    ROLE_CONSUMER, B.my_flag[t], B.peer_ack[t], B.seq_c[t], B.done_c[t]};
+                    };
+                    if (B.ncs) P.pack_c.h.push_back(prod(0));
+                    if (B.ncr) P.add_c.h.push_back(cons(0, S.add_atomic_c ? OP_ADD_ATOMIC : OP_ADD));
+                    if (B.nhs) P.pack_h.h.push_back(prod(1));
+                    if (B.nhr) P.unpack_h.h.push_back(cons(1, OP_SCATTER));
+                    if (B.nhr) P.pack_r.h.push_back(prod(2));
+                    if (B.nhs) P.add_r.h.push_back(cons(2, S.add_atomic_r ? OP_ADD_ATOMIC : OP_ADD));
+                    continue;
+                }
                 if (B.ncs) {
                     P.pack_c.h.push_back({OP_GATHER, i, B.cs, B.ncs, B.cs_buf});
                     P.diff_c.h.push_back({OP_DIFF, i, B.cs, B.ncs, B.cs_buf});
@@ -878,7 +1139,7 @@ rav_status mgd_residual_norm(mgd_ctx* m, double* const* x, const double* const* 
     RAV_CUDA(cudaStreamSynchronize(m->stream));
     *norm = sqrt(*m->h_nrm);
     m->last_launches = g_launches;
-    return RAV_OK;
+    return m->peer ? peer_check() : RAV_OK;
 }
 
 rav_status mgd_solve(mgd_ctx* m, double* const* x, const double* const* b, int pre, int post, double omega,
@@ -935,6 +1196,7 @@ rav_status mgd_solve(mgd_ctx* m, double* const* x, const double* const* b, int p
     }
     if (iters) *iters = k;
     m->last_launches = total;
+    if (st == RAV_OK && m->peer) st = peer_check();
     return st;
 }
 

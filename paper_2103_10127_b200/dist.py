@@ -730,7 +730,7 @@ def neighbor_plan(slab: "Slab", written: np.ndarray, all_infos: Sequence[Dict]) 
 
 def build_lib_dist(problem: Dict, n_levels: int, nsub: int, local_ids: Sequence[int], sub_proc: Sequence[int],
                    comm, gather=None, weights: str = "pou", variant: int = 0, agg_layers: int = 0,
-                   smooth_only: bool = False, via_comm: bool = False, balanced: bool = True, stream=None,
+                   smooth_only: bool = False, via_comm: int = 0, balanced: bool = True, stream=None,
                    deterministic: bool = False):
     """One process's share of the library-driven slab-partitioned hierarchy (mgd_setup).
 

@@ -668,7 +668,7 @@ class DistMultigrid:
     or None), colors ((offs, ids) or None).  Argument marshalling only."""
 
     def __init__(self, comm: "Comm", sub_proc: Sequence[int], local_ids: Sequence[int], subs, coarse=None,
-                 variant: int = VARIANT_ROWS, kernel: int = KERNEL_AUTO, stream=None, via_comm: bool = False,
+                 variant: int = VARIANT_ROWS, kernel: int = KERNEL_AUTO, stream=None, via_comm: int = 0,
                  deterministic: bool = False):
         K, nl = len(subs), len(local_ids)
         keep = []
@@ -717,7 +717,7 @@ class DistMultigrid:
         opts = RavOpts(variant, kernel, int(bool(deterministic)), 0, _stream(stream), int(dim))
         h = C.c_void_p()
         _check(lib.mgd_setup(comm.ctx, len(sp), sp.ctypes.data, nl, li.ctypes.data, K, arr,
-                             coarse.ctx if coarse is not None else None, C.byref(opts), int(bool(via_comm)),
+                             coarse.ctx if coarse is not None else None, C.byref(opts), int(via_comm),
                              C.byref(h)))
         self.ctx, self.nl, self.comm, self.coarse = h, nl, comm, coarse
 

@@ -18,6 +18,9 @@ one rank is assembled from pieces measured on it:
   subdomains the emulated group holds all 2(N - 1) pairs, more than any rank posts, so the
   N = 2 difference is the per-rank estimate (the N > 2 differences are reported too).  NCCL's
   self send is its on-device copy path: NVLink adds its latency (a few us per phase) -- T_link.
+* T_emul_peer(N): the same run with the peer-memory transport (mgd via_comm = 2; local
+  pointers on one GPU): the cost of its flag / fence protocol inside the pack / unpack kernels.
+  With it the per-rank exchange estimate is T_emul_peer(2) - T_emul(2) + T_link (no NCCL).
 * T_phase (strong, conservative): the exchange-phase kernels (zero / pack / add / unpack) run once
   per phase for ALL local subdomains in the emulation but once per rank on N GPUs; counted from
   the graph's launch count (mgd_last_launches for N = 2 and 4) at 3 us per launch.
@@ -92,12 +95,12 @@ def vcycle_case(name, Ns, agg_layers=0):
     comm1 = rg.Comm(1, 0, rg.Comm.unique_id())
     for N in Ns:
         row = {}
-        for via, comm in ((False, comm0), (True, comm1)):
+        for via, comm in ((0, comm0), (1, comm1), (2, comm0)):
             mgd, info = rdist.build_lib_dist(prob, c["levels"], N, list(range(N)), [0] * N, comm, via_comm=via,
                                              stream=STREAM, agg_layers=agg_layers)
             xs = [torch.zeros_like(v) for v in info["x"]]
             t = timed(lambda: mgd.vcycle(xs, info["b"], pre, post, om), 5)
-            row["T_emul_nccl_s" if via else "T_emul_s"] = t
+            row[("T_emul_s", "T_emul_nccl_s", "T_emul_peer_s")[via]] = t
             if not via:
                 subs, coarse = mgd._keep
                 row["launches_per_cycle"] = mgd.last_launches
@@ -127,14 +130,18 @@ def vcycle_case(name, Ns, agg_layers=0):
     l_sub = (r4["launches_per_cycle"] - r2["launches_per_cycle"]) / 2
     l_phase = max(0.0, r2["launches_per_cycle"] - 2 * l_sub - r2["coarse_launches_per_cycle"])
     t_nccl = r2["T_nccl_s_emulated_group"]
-    out["per_rank"] = {"launches_per_subdomain": l_sub, "phase_launches": l_phase, "T_nccl_s": t_nccl}
+    t_peer = max(0.0, r2["T_emul_peer_s"] - r2["T_emul_s"])
+    out["per_rank"] = {"launches_per_subdomain": l_sub, "phase_launches": l_phase, "T_nccl_s": t_nccl,
+                       "T_peer_protocol_s": t_peer}
     for N, row in out["N"].items():
         tc = row["T_coarse_s"]
         t_link = row["link_bytes_per_cycle"] / (LINK_GBS * 1e9) + row["phases_per_cycle"] * LINK_LAT_S
         TN = (row["T_emul_s"] - tc) / N + tc + t_nccl + t_link
         TNc = TN + (1 - 1 / N) * l_phase * LAUNCH_S
+        TNp = (row["T_emul_s"] - tc) / N + tc + t_peer + t_link
         row.update({"T_link_s": t_link, "T_N_model_s": TN, "T_N_model_conservative_s": TNc,
-                    "efficiency_strong": t1 / (N * TN), "efficiency_strong_conservative": t1 / (N * TNc)})
+                    "efficiency_strong": t1 / (N * TN), "efficiency_strong_conservative": t1 / (N * TNc),
+                    "T_N_model_peer_s": TNp, "efficiency_strong_peer": t1 / (N * TNp)})
     return out
 
 
@@ -155,12 +162,12 @@ def smooth_case(name, Ns, sweeps):
     for N in Ns:
         prob = si.config_problem(name, scale_y=N)
         row = {}
-        for via, comm in ((False, comm0), (True, comm1)):
+        for via, comm in ((0, comm0), (1, comm1), (2, comm0)):
             mgd, info = rdist.build_lib_dist(prob, 1, N, list(range(N)), [0] * N, comm, smooth_only=True,
                                              via_comm=via, stream=STREAM)
             xs = [torch.zeros_like(v) for v in info["x"]]
             t = timed(lambda: mgd.smooth(xs, info["b"], sweeps, 0.66), 3) / sweeps
-            row["T_emul_nccl_s" if via else "T_emul_s"] = t
+            row[("T_emul_s", "T_emul_nccl_s", "T_emul_peer_s")[via]] = t
             if not via:
                 subs, _ = mgd._keep
                 row["link_bytes_per_sweep"] = link_bytes(subs, 1)
@@ -174,12 +181,15 @@ def smooth_case(name, Ns, sweeps):
     comm0.close()
     comm1.close()
     t_nccl = out["N"][Ns[0]]["T_nccl_s_emulated_group"]   # N = 2: one interior rank's group
+    t_peer = max(0.0, out["N"][Ns[0]]["T_emul_peer_s"] - out["N"][Ns[0]]["T_emul_s"])
     for N, row in out["N"].items():
         t_link = row["link_bytes_per_sweep"] / (LINK_GBS * 1e9) + 2 * LINK_LAT_S
         extra = max(0.0, row["T_emul_s"] - N * t1)
         TN = t1 + extra + t_nccl + t_link
+        TNp = t1 + extra + t_peer + t_link
         row.update({"T_extra_s": extra, "T_nccl_s": t_nccl, "T_link_s": t_link, "T_N_model_s": TN,
-                    "efficiency_weak": t1 / TN})
+                    "efficiency_weak": t1 / TN, "T_peer_protocol_s": t_peer, "T_N_model_peer_s": TNp,
+                    "efficiency_weak_peer": t1 / TNp})
     return out
 
 

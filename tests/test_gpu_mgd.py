@@ -3,8 +3,12 @@ section 8 rows a11 / b / e).  One GPU is available to the tests, so a multi-GPU 
 by one process driving R subdomains on the same device: the exchanges between them are device
 reads of the neighbour's packed buffers (no kernel waits on another).  With via_comm the same
 exchanges go through a one-rank NCCL communicator's self sends / receives, i.e. the NCCL code
-path of the multi-process run (ordering, sizes, graph capture of NCCL calls).  Results are
-gathered from the owned DoFs and compared with the single-domain oracle entry by entry."""
+path of the multi-process run (ordering, sizes, graph capture of NCCL calls).  With via_comm = 2
+the exchanges use the peer-memory transport: the pack kernels store into the consumer's receive
+buffer and release its flag, the unpack kernels acquire it and release the producer's ack (local
+subdomains: plain pointers; between processes the same kernels run on CUDA IPC mappings).
+Results are gathered from the owned DoFs and compared with the single-domain oracle entry by
+entry."""
 import numpy as np
 import pytest
 import torch
@@ -29,7 +33,7 @@ def rdist():
 
 
 def _comm(rg, via_comm):
-    return rg.Comm(1, 0, rg.Comm.unique_id() if via_comm else None)
+    return rg.Comm(1, 0, rg.Comm.unique_id() if via_comm == 1 else None)
 
 
 def _gather(info, xs, n):
@@ -51,11 +55,15 @@ SMOOTH_CASES = [
     (si.problem(2, (33, 29), si.KIND_CAVITY, eta="fourier"), "own", 0, 0.66, 3, False),
     (si.problem(2, (36, 30), si.KIND_MMS, eta="fourier"), "full", 1, 0.1, 2, True),
     (si.problem(3, (5, 4, 12), si.KIND_CAVITY, eta="fourier"), "pou", 0, 0.66, 3, True),
+    (si.problem(2, (48, 40), si.KIND_MMS, eta="fourier"), "pou", 0, 0.66, 4, 2),
+    (si.problem(2, (36, 30), si.KIND_MMS, eta="fourier"), "full", 1, 0.1, 2, 2),
+    (si.problem(3, (5, 4, 12), si.KIND_CAVITY, eta="fourier"), "pou", 0, 0.66, 3, 2),
 ]
 
 
 @pytest.mark.parametrize("case", SMOOTH_CASES, ids=["2d-pou-4", "2d-pou-4-nccl", "2d-own-3", "2d-diag-2-nccl",
-                                                    "3d-pou-3-nccl"])
+                                                    "3d-pou-3-nccl", "2d-pou-4-peer", "2d-diag-2-peer",
+                                                    "3d-pou-3-peer"])
 def test_mgd_sweeps_match_oracle(rg, rdist, case):
     prob, weights, variant, omega, R, via = case
     comm = _comm(rg, via)
@@ -105,10 +113,13 @@ VC_CASES = [
     (si.problem(2, (64, 64), si.KIND_MMS, eta="fourier"), 5, 4, True, 1e-8, False),
     (si.problem(2, (32, 32), si.KIND_CAVITY, eta="fourier"), 4, 2, True, 1e-10, True),
     (si.problem(3, (8, 8, 16), si.KIND_CAVITY, eta="fourier"), 3, 3, True, 1e-8, False),
+    (si.problem(2, (64, 64), si.KIND_MMS, eta="fourier"), 5, 3, 2, 1e-8, True),
+    (si.problem(3, (8, 8, 16), si.KIND_CAVITY, eta="fourier"), 3, 3, 2, 1e-8, False),
 ]
 
 
-@pytest.mark.parametrize("case", VC_CASES, ids=["2d-mms-3-det", "2d-mms-4-nccl", "2d-cav-2-nccl-det", "3d-3-nccl"])
+@pytest.mark.parametrize("case", VC_CASES, ids=["2d-mms-3-det", "2d-mms-4-nccl", "2d-cav-2-nccl-det", "3d-3-nccl",
+                                                "2d-mms-3-peer-det", "3d-3-peer"])
 def test_mgd_solve_matches_oracle(rg, rdist, case):
     prob, levels, R, via, rtol, det = case
     comm = _comm(rg, via)
@@ -156,3 +167,33 @@ def test_mgd_rejects_mismatched_lists(rg, rdist):
     with pytest.raises(rg.RavError) as ei:
         rg.DistMultigrid(comm, [0, 0], [0, 1], [subs])
     assert ei.value.status == 1
+
+
+def test_mgd_peer_transport_equals_local_exchange(rg, rdist):
+    """The peer-memory transport moves the same values in the same order as the local exchange:
+    after 3 x 2 sweeps (graph-captured; flags and sequence numbers advance on every replay) the
+    iterates are bitwise equal (deterministic mode), and the transport's bounded waits never
+    timed out (mgd_residual_norm reports a timeout as an error)."""
+    prob = si.problem(2, (40, 48), si.KIND_MMS, eta="fourier")
+    n = oracle.assemble(prob)["n"]
+    out = []
+    for via in (0, 2):
+        comm = _comm(rg, via)
+        mgd, info = rdist.build_lib_dist(prob, 1, 3, [0, 1, 2], [0, 0, 0], comm, smooth_only=True, via_comm=via,
+                                         deterministic=True)
+        xs = _scatter(info, si.initial_guess(n, seed=5))
+        for _ in range(3):
+            mgd.smooth(xs, info["b"], 2, 0.66)
+        torch.cuda.synchronize()
+        out.append([x.clone() for x in xs])
+        assert np.isfinite(mgd.residual_norm(xs, info["b"]))
+        mgd.close()
+    for a, b in zip(*out):
+        assert torch.equal(a, b)
+
+
+def test_mgd_peer_transport_rejects_mv(rg, rdist):
+    prob = si.problem(2, (24, 24), si.KIND_MMS, eta="fourier")
+    with pytest.raises(rg.RavError):
+        rdist.build_lib_dist(prob, 1, 2, [0, 1], [0, 0], _comm(rg, 0), weights="full", variant=2, smooth_only=True,
+                             via_comm=2)
