@@ -117,6 +117,7 @@ struct Step {
     unsigned long long* ack; // producer: its own ack word; consumer: the producer's ack (remote)
     unsigned long long* seq; // this end's message counter (local)
     unsigned int* done;      // CTAs of this step that finished (local)
+    int sys;                 // the other end is another process / GPU: system-scope fences, else GPU scope
 };
 struct VecTab {
     double* v[MAX_VEC];
@@ -124,16 +125,18 @@ struct VecTab {
 
 __device__ unsigned int g_peer_timeout = 0;
 
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p, int sys) {
     unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v, int sys) {
+    if (sys) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ void wait_geq(const unsigned long long* p, unsigned long long v) {
-    for (long long spin = 0; ld_acquire_sys(p) < v; ++spin) {
+__device__ void wait_geq(const unsigned long long* p, unsigned long long v, int sys) {
+    for (long long spin = 0; ld_acquire(p, sys) < v; ++spin) {
         if (spin > (1ll << 24)) {   // ~4 s at 256 ns per poll
             atomicOr(&g_peer_timeout, 1u);
             return;
@@ -150,8 +153,8 @@ __global__ void __launch_bounds__(256) phase_kernel(const Step* __restrict__ ste
         if (threadIdx.x == 0) {
             const unsigned long long s = *reinterpret_cast<volatile unsigned long long*>(st.seq);
             s_target = s + 1;
-            if (st.role == ROLE_PRODUCER) wait_geq(st.ack, s);   // the previous message was consumed
-            else wait_geq(st.sig, s + 1);                        // this message has arrived
+            if (st.role == ROLE_PRODUCER) wait_geq(st.ack, s, st.sys);   // the previous message was consumed
+            else wait_geq(st.sig, s + 1, st.sys);                        // this message has arrived
         }
         __syncthreads();
     }
@@ -167,13 +170,18 @@ __global__ void __launch_bounds__(256) phase_kernel(const Step* __restrict__ ste
         }
     }
     if (st.role != ROLE_NONE) {
-        __threadfence_system();   // this CTA's payload stores (producer) / reads (consumer) are done
+        // the CTA's payload stores (producer) / reads (consumer) are ordered before thread 0's fence by
+        // the barrier, the CTAs' fences + counter before the last CTA's, and that one before its release
+        // of the flag / ack (release at system scope when the other end is another GPU): causality is
+        // transitive in the PTX memory model, so one GPU-scope fence per CTA and one system-scope
+        // release per message suffice (a system fence per CTA cost ~4 us per launch)
         __syncthreads();
+        if (threadIdx.x == 0) __threadfence();
         if (threadIdx.x == 0 && atomicAdd(st.done, 1u) == gridDim.x - 1) {   // the step's last CTA
+            __threadfence();
             *st.done = 0;
             *st.seq = s_target;
-            __threadfence_system();
-            st_release_sys(st.role == ROLE_PRODUCER ? st.sig : st.ack, s_target);
+            st_release(st.role == ROLE_PRODUCER ? st.sig : st.ack, s_target, st.sys);
         }
     }
 }
@@ -959,11 +967,13 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
                 if (m->peer) {   // producers write the consumers' buffers; no NCCL messages
                     auto prod = [&](int t) {
                         return Step{OP_GATHER, i, t == 0 ? B.cs : t == 1 ? B.hs : B.hr, B.n_out(t), B.out_buf[t],
-                                    ROLE_PRODUCER, B.out_sig[t], B.my_ack[t], B.seq_p[t], B.done_p[t]};
+                                    ROLE_PRODUCER, B.out_sig[t], B.my_ack[t], B.seq_p[t], B.done_p[t],
+                                    B.peer_local < 0};
                     };
                     auto cons = [&](int t, int op) {
                         return Step{op, i, t == 0 ? B.cr : t == 1 ? B.hr : B.hs, B.n_in(t), B.in_buf(t),
-                                    ROLE_CONSUMER, B.my_flag[t], B.peer_ack[t], B.seq_c[t], B.done_c[t]};
+                                    ROLE_CONSUMER, B.my_flag[t], B.peer_ack[t], B.seq_c[t], B.done_c[t],
+                                    B.peer_local < 0};
                     };
                     if (B.ncs) P.pack_c.h.push_back(prod(0));
                     if (B.ncr) P.add_c.h.push_back(cons(0, S.add_atomic_c ? OP_ADD_ATOMIC : OP_ADD));
