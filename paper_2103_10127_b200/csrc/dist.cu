@@ -91,7 +91,8 @@ bool is_dev(const void* p) {
 }
 
 // ---- pack / unpack: one launch per phase, grid.y = message --------------------------------
-enum { OP_GATHER = 0, OP_SCATTER = 1, OP_ADD = 2, OP_ZERO = 3, OP_DIFF = 4, OP_ADD_ATOMIC = 5 };
+enum { OP_GATHER = 0, OP_SCATTER = 1, OP_ADD = 2, OP_ZERO = 3, OP_DIFF = 4, OP_ADD_ATOMIC = 5, OP_ADD_CLEAR = 6,
+       OP_ADD_ATOMIC_CLEAR = 7 };   // *_CLEAR: the receive buffer is an accumulator (fused sweep): zero it
 constexpr int MAX_VEC = 64;
 
 // Peer-memory transport (mgd_setup via_comm = 2): a message is written by the producer's pack
@@ -166,6 +167,8 @@ __global__ void __launch_bounds__(256) phase_kernel(const Step* __restrict__ ste
             case OP_ADD: V[i] += st.buf[k]; break;
             case OP_ZERO: V[i] = 0.0; break;
             case OP_DIFF: st.buf[k] = V[i] - st.buf[k]; break;
+            case OP_ADD_CLEAR: V[i] += st.buf[k]; st.buf[k] = 0.0; break;
+            case OP_ADD_ATOMIC_CLEAR: atomicAdd(V + i, st.buf[k]); st.buf[k] = 0.0; break;
             default: atomicAdd(V + i, st.buf[k]); break;
         }
     }
@@ -183,6 +186,17 @@ __global__ void __launch_bounds__(256) phase_kernel(const Step* __restrict__ ste
             *st.seq = s_target;
             st_release(st.role == ROLE_PRODUCER ? st.sig : st.ack, s_target, st.sys);
         }
+    }
+}
+
+// per patch: does it write (weight > 0) a ghost-written DoF (rmap >= 0)?  (fused sweep)
+__global__ void pflag_kernel(int64_t np, const int64_t* __restrict__ offs, const int32_t* __restrict__ dofs,
+                             const double* __restrict__ w, const int32_t* __restrict__ rmap, uint8_t* __restrict__ pflag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x) {
+        uint8_t f = 0;
+        for (int64_t k = offs[i]; k < offs[i + 1]; ++k)
+            if (w[k] > 0.0 && rmap[dofs[k]] >= 0) f = 1;
+        pflag[i] = f;
     }
 }
 
@@ -246,6 +260,11 @@ struct DSub {                     // one local subdomain on one partitioned leve
     XStruct xs;                   // its stencil form (rav_subdomain grids), used when xs.on
     double *x = nullptr, *b = nullptr, *r = nullptr;   // x, b: levels > 0 (level 0: caller's)
     bool add_atomic_c = false, add_atomic_r = false;   // corr_recv / halo_send lists overlap
+    // the interface exchange fused into the sweep (peer transport): the sweep's scatter adds the
+    // ghost-written DoFs' corrections straight into the consumers' receive buffers (Outbox)
+    Outbox ob;
+    int32_t* rmap = nullptr;      // per local DoF: (q << 24) | slot, else -1
+    uint8_t* pflag = nullptr;     // per patch: writes a ghost-written DoF
 };
 
 }  // namespace
@@ -282,6 +301,8 @@ struct mgd_ctx {
     bool peer = false;                          // peer-memory transport (via_comm = 2)
     void* peer_block = nullptr;                 // receive buffers + flags + acks (exported by CUDA IPC)
     void* sync_block = nullptr;                 // sequence / CTA counters (local)
+    bool fused = false;                         // peer transport with the exchange fused into the sweep
+    void* ob_block = nullptr;                   // the fused sweeps' sequence / CTA counters
     std::vector<void*> peer_opened;             // other processes' peer blocks (cudaIpcOpenMemHandle)
     // pack / unpack phases per level
     struct LvPhases {
@@ -418,11 +439,14 @@ rav_status dist_sweeps(mgd_ctx* m, int k, const std::vector<double*>& x, const s
         const bool from_b = x_zero && it == 0;
         if (!from_b) {
             for (int i = 0; i < m->nl; ++i) RAV_TRY(launch_residual(L[i].sm->A, x[i], b[i], L[i].sm->r, s));
-            RAV_TRY(run_phase(P.zero_gw, vx, s));
+            if (!m->fused) RAV_TRY(run_phase(P.zero_gw, vx, s));
         }
-        for (int i = 0; i < m->nl; ++i)
-            RAV_TRY(launch_sweep(L[i].sm->P, L[i].sm->F, from_b ? b[i] : L[i].sm->r, x[i], omega, s));
-        RAV_TRY(run_phase(P.pack_c, vx, s));
+        for (int i = 0; i < m->nl; ++i) {
+            const double* ri = from_b ? b[i] : L[i].sm->r;
+            if (m->fused) RAV_TRY(launch_schur_sweep_ob(L[i].sm->P, L[i].sm->F, ri, x[i], omega, L[i].ob, s));
+            else RAV_TRY(launch_sweep(L[i].sm->P, L[i].sm->F, ri, x[i], omega, s));
+        }
+        if (!m->fused) RAV_TRY(run_phase(P.pack_c, vx, s));
         RAV_TRY(run_msgs(m, P.m_corr, s));
         RAV_TRY(run_phase(P.add_c, vx, s));
         RAV_TRY(run_phase(P.pack_h, vx, s));
@@ -614,6 +638,12 @@ void mgd_destroy(mgd_ctx* m) {
         if (p) cudaFree(p);
     if (m->h_nrm) cudaFreeHost(m->h_nrm);
     for (void* p : m->peer_opened) cudaIpcCloseMemHandle(p);
+    for (auto& L : m->lv)
+        for (auto& S : L) {
+            if (S.rmap) cudaFree(S.rmap);
+            if (S.pflag) cudaFree(S.pflag);
+        }
+    if (m->ob_block) cudaFree(m->ob_block);
     if (m->peer_block) cudaFree(m->peer_block);
     if (m->sync_block) cudaFree(m->sync_block);
     delete m;
@@ -814,6 +844,7 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
     m->variant = o.variant;
     m->via_comm = via_comm == 1;
     m->peer = via_comm == 2;
+    m->fused = m->peer && o.variant != RAV_VARIANT_MV && o.variant != RAV_VARIANT_DIAG && !o.deterministic;
     rav_status st = RAV_OK;
     std::map<int32_t, int> local_of;
     for (int i = 0; i < n_local; ++i) {
@@ -906,6 +937,53 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
             }
             S.add_atomic_c = !unique_union(lc);
             S.add_atomic_r = !unique_union(lr);
+            if (m->fused) {   // the ghost-written DoFs' slots in the consumers' receive buffers
+                if (!schur_fusable(S.sm->P, S.sm->F) || S.nb.size() > 2) {
+                    set_error("mgd_setup: level %d subdomain %d: the fused exchange needs the Schur sweep kernels "
+                              "and at most two neighbours", k, S.gid);
+                    st = RAV_ERR_ARG;
+                    break;
+                }
+                std::vector<int32_t> rm((size_t)std::max<int64_t>(1, S.n), -1);
+                int q = 0;
+                for (int j = 0; j < D.n_neighbors; ++j) {
+                    const rav_neighbor& N = D.neighbors[j];
+                    if (N.n_corr_send <= 0) continue;
+                    if (N.n_corr_send >= (1 << 24)) { set_error("mgd_setup: message too long for the fused exchange"); st = RAV_ERR_ARG; break; }
+                    for (int64_t u = 0; u < N.n_corr_send; ++u) rm[N.corr_send[u]] = (q << 24) | (int32_t)u;
+                    ++q;
+                }
+                if (st != RAV_OK) break;
+                cudaError_t e = cudaMalloc(&S.rmap, sizeof(int32_t) * rm.size());
+                if (e == cudaSuccess) e = cudaMemcpy(S.rmap, rm.data(), sizeof(int32_t) * rm.size(), cudaMemcpyHostToDevice);
+                if (e == cudaSuccess) e = cudaMalloc(&S.pflag, std::max<int64_t>(1, S.sm->P.n_patches));
+                if (e != cudaSuccess) { set_error("mgd_setup: %s", cudaGetErrorString(e)); st = RAV_ERR_OOM; break; }
+                const int64_t np = S.sm->P.n_patches;
+                pflag_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(cdiv(np, 256), 4096)), 256, 0, m->stream>>>(
+                    np, S.sm->P.offs, S.sm->P.dofs, S.sm->P.w, S.rmap, S.pflag);
+                count_launch();
+                if (cudaGetLastError() != cudaSuccess) { set_error("mgd_setup: pflag kernel failed"); st = RAV_ERR_CUDA; break; }
+                // writers per launch: chunks of 32 patches (thread layout) or patches (per-patch layout)
+                std::vector<uint8_t> hf((size_t)std::max<int64_t>(1, np));
+                if (cudaMemcpy(hf.data(), S.pflag, (size_t)np, cudaMemcpyDeviceToHost) != cudaSuccess) { st = RAV_ERR_CUDA; break; }
+                unsigned int nw = 0;
+                if (S.sm->F.layout == 4) {
+                    const int64_t nch = (np + 31) / 32;
+                    std::vector<uint8_t> cw((size_t)nch, 0);
+                    for (int64_t c = 0; c < nch; ++c) {
+                        for (int64_t u = c * 32; u < std::min<int64_t>(np, c * 32 + 32); ++u) cw[c] |= hf[u];
+                        nw += cw[c];
+                    }
+                    // rotate the trailing run of writer chunks (the slab's last vertex layers) to the front
+                    int64_t first = nch;
+                    for (int64_t c = nch - 1; c >= 0 && (cw[c] || nch - c <= 64); --c)
+                        if (cw[c]) first = c;
+                    S.ob.rot = first < nch && first > nch / 2 ? nch - first : 0;
+                } else {
+                    for (int64_t u = 0; u < np; ++u) nw += hf[u] != 0;
+                }
+                S.ob.nflag = nw;
+            }
             // transfer to the next level (levels < K-1: its windows; last: the agglomerated level)
             if (D.P_coarse.n_rows > 0) {
                 if (D.P_coarse.n_rows != S.n) {
@@ -955,6 +1033,41 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
                 }
             }
     if (st == RAV_OK && m->peer) st = peer_setup(m);
+    if (st == RAV_OK && m->fused) {   // outboxes: consumers = neighbours receiving corrections
+        unsigned int* tmo = nullptr;
+        if (cudaGetSymbolAddress(reinterpret_cast<void**>(&tmo), g_peer_timeout) != cudaSuccess) {
+            set_error("mgd_setup: cudaGetSymbolAddress failed");
+            st = RAV_ERR_CUDA;
+        }
+        const size_t nsub = (size_t)m->K * m->nl;
+        if (st == RAV_OK && cudaMalloc(&m->ob_block, 16 * std::max<size_t>(1, nsub)) != cudaSuccess) st = RAV_ERR_OOM;
+        if (st == RAV_OK && cudaMemset(m->ob_block, 0, 16 * std::max<size_t>(1, nsub)) != cudaSuccess) st = RAV_ERR_CUDA;
+        auto* seqs = static_cast<unsigned long long*>(m->ob_block);
+        auto* dones = reinterpret_cast<unsigned int*>(seqs + std::max<size_t>(1, nsub));
+        for (int k = 0; k < m->K && st == RAV_OK; ++k)
+            for (int i = 0; i < m->nl; ++i) {
+                DSub& S = m->lv[k][i];
+                Outbox& O = S.ob;
+                O.rmap = S.rmap;
+                O.pflag = S.pflag;
+                O.nq = 0;
+                for (DNb& B : S.nb) {
+                    if (!B.ncs) continue;
+                    O.buf[O.nq] = B.out_buf[0];
+                    O.sig[O.nq] = B.out_sig[0];
+                    O.ack[O.nq] = B.my_ack[0];
+                    O.sys[O.nq] = B.peer_local < 0;
+                    ++O.nq;
+                }
+                if (O.nq > 0 && O.nflag == 0) {
+                    set_error("mgd_setup: level %d subdomain %d sends corrections but no patch writes a ghost DoF", k, S.gid);
+                    st = RAV_ERR_ARG;
+                }
+                O.seq = seqs + (size_t)k * m->nl + i;
+                O.done = dones + (size_t)k * m->nl + i;
+                O.timeout = tmo;
+            }
+    }
     // phases and NCCL messages
     for (int k = 0; k < n_levels && st == RAV_OK; ++k) {
         auto& P = m->ph[k];
@@ -975,8 +1088,10 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
                                     ROLE_CONSUMER, B.my_flag[t], B.peer_ack[t], B.seq_c[t], B.done_c[t],
                                     B.peer_local < 0};
                     };
-                    if (B.ncs) P.pack_c.h.push_back(prod(0));
-                    if (B.ncr) P.add_c.h.push_back(cons(0, S.add_atomic_c ? OP_ADD_ATOMIC : OP_ADD));
+                    if (B.ncs && !m->fused) P.pack_c.h.push_back(prod(0));   // fused: the sweep produces
+                    if (B.ncr)
+                        P.add_c.h.push_back(cons(0, m->fused ? (S.add_atomic_c ? OP_ADD_ATOMIC_CLEAR : OP_ADD_CLEAR)
+                                                             : (S.add_atomic_c ? OP_ADD_ATOMIC : OP_ADD)));
                     if (B.nhs) P.pack_h.h.push_back(prod(1));
                     if (B.nhr) P.unpack_h.h.push_back(cons(1, OP_SCATTER));
                     if (B.nhr) P.pack_r.h.push_back(prod(2));

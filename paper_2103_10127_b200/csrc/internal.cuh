@@ -169,6 +169,117 @@ rav_status launch_mv_color(const Csr& A, const Factors& F, int64_t ncol, const i
                            double* x, double omega, cudaStream_t s);
 rav_status launch_schur_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
                               cudaStream_t s);
+
+// ---- the interface exchange fused into the sweep (mgd peer transport, dist.cu) ----------------
+// The corrections a subdomain's patches make to DoFs a neighbour owns (ghost-written DoFs) are
+// added by the sweep's own scatter straight into that neighbour's receive buffer (over NVLink when
+// it is another GPU), instead of into x followed by a pack kernel and a message.  The sweep waits
+// (thread 0 of each CTA) for the consumers' acks of the previous message before any scatter, and
+// its last CTA releases the consumers' flags.
+struct Outbox {
+    const int32_t* rmap = nullptr;          // per local DoF: (q << 24) | slot for ghost-written DoFs, else -1
+    const uint8_t* pflag = nullptr;         // per patch: 1 when it writes a ghost-written DoF
+    int nq = 0;                             // consumers (<= 2: the slab's neighbours)
+    double* buf[2] = {nullptr, nullptr};    // consumer q's receive buffer for these corrections
+    unsigned long long* sig[2] = {nullptr, nullptr};   // consumer q's flag
+    unsigned long long* ack[2] = {nullptr, nullptr};   // own ack words (released by consumer q)
+    int sys[2] = {0, 0};                    // consumer q is another GPU: system-scope release
+    unsigned long long* seq = nullptr;      // this producer's message counter
+    unsigned int* done = nullptr;           // writers of the launch that finished
+    unsigned int nflag = 0;                 // writers per launch: chunks (thread kernel) / patches (warp
+                                            // kernel) holding a ghost-writing patch
+    int64_t rot = 0;                        // thread kernel: warp w takes chunk (w - rot) mod nchunks, so
+                                            // the trailing writer chunks run in the first wave, not the last
+    unsigned int* timeout = nullptr;        // set when a bounded wait expires
+};
+
+__device__ __forceinline__ unsigned long long ob_ld_acquire(const unsigned long long* p, int sys) {
+    unsigned long long v;
+    if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void ob_st_release(unsigned long long* p, unsigned long long v, int sys) {
+    if (sys) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// spin until *p >= v (bounded: ~4 s, then *err |= 1 and go on -- never a hung GPU)
+__device__ __forceinline__ void ob_wait_geq(const unsigned long long* p, unsigned long long v, int sys,
+                                            unsigned int* err) {
+    for (long long spin = 0; ob_ld_acquire(p, sys) < v; ++spin) {
+        if (spin > (1ll << 24)) {
+            if (err) atomicOr(err, 1u);
+            return;
+        }
+        __nanosleep(256);
+    }
+}
+// the hot-loop view of an Outbox, passed by value (a reference to the kernel parameter would put
+// the whole struct in local memory)
+struct ObView {
+    const int32_t* rmap;
+    const uint8_t* pflag;
+    double* buf0;
+    double* buf1;
+    const unsigned long long* ack0;
+    const unsigned long long* ack1;
+    const unsigned long long* seq;
+    unsigned int* timeout;
+    int nq, sys0, sys1;
+    int64_t rot;
+};
+__device__ __forceinline__ ObView ob_view(const Outbox& o) {
+    return ObView{o.rmap, o.pflag, o.buf[0], o.buf[1], o.ack[0], o.ack[1], o.seq, o.timeout, o.nq, o.sys[0], o.sys[1],
+                  o.rot};
+}
+// before a thread's first store into a receive buffer: the consumers have consumed the previous
+// message (ack >= this launch's message number - 1; *seq changes only at the launch's end)
+__device__ __forceinline__ void ob_wait_acks(const ObView& o) {
+    const unsigned long long s = *reinterpret_cast<const volatile unsigned long long*>(o.seq);
+    if (o.nq > 0) ob_wait_geq(o.ack0, s, o.sys0, o.timeout);
+    if (o.nq > 1) ob_wait_geq(o.ack1, s, o.sys1, o.timeout);
+}
+// *p += v as a fire-and-forget reduction (kernels that also hold fences compiled atomicAdd to
+// returning ATOMG: +15% on the sweep)
+__device__ __forceinline__ void red_add(double* p, double v) {
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+// x[dof] += v, or the consumer's receive buffer when dof is ghost-written (patches with pflag)
+__device__ __forceinline__ void ob_add(const ObView& o, bool flagged, double* x, int dof, double v) {
+    if (flagged) {
+        const int m = o.rmap[dof];
+        if (m >= 0) {
+            red_add((m >> 24 ? o.buf1 : o.buf0) + (m & 0xffffff), v);
+            return;
+        }
+    }
+    red_add(x + dof, v);
+}
+// after a writer (a chunk / patch with ghost-writing patches; every lane of the warp calls it) has
+// made its scatters: fence, count it; the launch's last writer releases the consumers' flags with
+// the next message number.  Only writers count -- a single counter hit by every warp of the grid
+// cost ~15% of the sweep -- and only writers' stores go to the receive buffers (the stores to x
+// reach the consumer's add kernel through the kernel boundary).  Static indices: the parameter
+// stays in constant space.
+__device__ __forceinline__ void ob_writer_done(const Outbox& o) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+        __threadfence();
+        if (atomicAdd(o.done, 1u) == o.nflag - 1) {
+            __threadfence();
+            *o.done = 0;
+            const unsigned long long t = *reinterpret_cast<volatile unsigned long long*>(o.seq) + 1;
+            *o.seq = t;
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (q < o.nq) ob_st_release(o.sig[q], t, o.sys[q]);
+        }
+    }
+}
+// can the sweep of this smoother run fused (the Schur thread kernel, or the per-patch warp kernel)?
+bool schur_fusable(const PatchSet& P, const Factors& F);
+rav_status launch_schur_sweep_ob(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
+                                 const Outbox& ob, cudaStream_t s);
 rav_status export_schur_rows(const PatchSet& P, const Factors& F, int64_t nvel, double* rows, cudaStream_t s);
 
 // ---- sweep.cu -------------------------------------------------------------------------

@@ -782,8 +782,10 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
 // instead of atomics; det_gather_kernel adds them to x in ascending patch order (rav_opts.deterministic)
 // NDP: node indices from (nbase[i], pattern table ntbl[npid[i] * NN + j]) instead of the ND array
 // RA: r is 16-byte aligned (checked at launch): node gathers without the per-load alignment test
-template <int MT, int D, int NRB = 0, bool DET = false, bool NDP = false, bool RA = false>   // NRB > 0: compile-time rect pairs
-__global__ void __launch_bounds__(128, 4) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
+// OB: the interface exchange fused into the sweep (Outbox, internal.cuh): ghost-written DoFs of
+// flagged patches go to the consumers' receive buffers
+template <int MT, int D, int NRB, bool DET, bool NDP, bool RA, bool OB>
+__device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, int NN, int64_t pairs,
                                                                  const double2* __restrict__ W,
                                                                  const int32_t* __restrict__ ND,
                                                                  const int32_t* __restrict__ npid,
@@ -794,19 +796,23 @@ __global__ void __launch_bounds__(128, 4) schur_sweep_thread_kernel(int64_t np, 
                                                                  const double* __restrict__ AUX,
                                                                  const double* __restrict__ r,
                                                                  double* __restrict__ x, double omega,
-                                                                 double* __restrict__ cbuf, int pf) {
+                                                                 double* __restrict__ cbuf, int pf, ObView ob) {
     constexpr int TRI = MT * (MT + 1) / 2 + MT * D;
     constexpr int TRI_PAD = TRI + (TRI & 1);
     constexpr int RC = MT + D;   // entries per rectangular column
-    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;   // warp -> chunk
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;   // warp -> chunk
+    const int64_t chunk = OB && ob.rot ? (gw < ob.rot ? gw + nchunks - ob.rot : gw - ob.rot) : gw;
     const int lane = threadIdx.x & 31;
     const int64_t i = chunk * 32 + lane;
     pdl_trigger();
-    if (chunk >= nchunks) return;
+    if (gw >= nchunks) return;
     const double2* wp = W + chunk * pairs * 32 + lane;
     const int32_t* np_ = NDP ? nullptr : ND + chunk * (int64_t)NN * 32 + lane;
     const int32_t* ntp = NDP ? ntbl + (int64_t)npid[i] * NN : nullptr;   // L1-resident pattern row
     const int32_t nb0 = NDP ? nbase[i] : 0;
+    const bool flagged = OB && i < np && ob.pflag[i];   // loaded early: needed only at the scatter
+    // warp-uniform: the chunks without a ghost-writing patch (nearly all) keep the plain scatter
+    const bool fw = OB && __any_sync(0xffffffffu, flagged);
 #define ND_AT(j) (NDP ? nb0 + __ldg(ntp + (j)) : __ldcs(np_ + (j) * 32))
     {   // before r exists: the chunk's node indices and first factor lines into L2
         const char* wc = reinterpret_cast<const char*>(W + chunk * pairs * 32);
@@ -901,33 +907,69 @@ __global__ void __launch_bounds__(128, 4) schur_sweep_thread_kernel(int64_t np, 
     if (i >= np) return;   // padding slots of the last chunk
     const int m = NR[i];
     double* cb = DET ? cbuf + i * (MT * D + 1) : nullptr;
+    // the scatter (restricted prolongation, Eq. 13): one straight-line loop per target kind,
+    // the warp-uniform branch outside it (a branch per store turned the reductions into returning
+    // atomics under divergence management)
+    auto scatter = [&](auto&& add) {
 #pragma unroll
-    for (int k = 0; k < MT; ++k) {
-        if (k < m) {
-            const double wk = omega * aux[k * 32];
-            const int nd = ND_AT(k);
+        for (int k = 0; k < MT; ++k) {
+            if (k < m) {
+                const double wk = omega * aux[k * 32];
+                const int nd = ND_AT(k);
 #pragma unroll
-            for (int c = 0; c < D; ++c) {
-                const double gk = gR[k][c];
-                const double v = wk * fma(gk, t, acc[k][c]);
-                if (DET) cb[k * D + c] = v;
-                else atomicAdd(x + nd + c, v);
+                for (int c = 0; c < D; ++c) add(nd + c, wk * fma(gR[k][c], t, acc[k][c]), k * D + c);
             }
         }
+    };
+    if constexpr (DET) {
+        scatter([&](int, double v, int slot) { cb[slot] = v; });
+    } else if constexpr (OB) {
+        if (fw) {
+            if (flagged) ob_wait_acks(ob);
+            scatter([&](int dof, double v, int) { ob_add(ob, flagged, x, dof, v); });
+        } else {
+            scatter([&](int dof, double v, int) { red_add(x + dof, v); });
+        }
+    } else {
+        scatter([&](int dof, double v, int) { atomicAdd(x + dof, v); });
     }
     const double wpr = aux[MT * 32];
     if (wpr != 0.0) {
         if (DET) cb[MT * D] = omega * wpr * (-t);
+        else if (OB) red_add(x + pd, omega * wpr * (-t));
         else atomicAdd(x + pd, omega * wpr * (-t));
     }
 }
 
 #undef ND_AT
 
+template <int MT, int D, int NRB = 0, bool DET = false, bool NDP = false, bool RA = false, bool OB = false>
+__global__ void __launch_bounds__(128, 4) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
+                                                                 const double2* __restrict__ W,
+                                                                 const int32_t* __restrict__ ND,
+                                                                 const int32_t* __restrict__ npid,
+                                                                 const int32_t* __restrict__ nbase,
+                                                                 const int32_t* __restrict__ ntbl,
+                                                                 const int32_t* __restrict__ PD,
+                                                                 const int32_t* __restrict__ NR,
+                                                                 const double* __restrict__ AUX,
+                                                                 const double* __restrict__ r,
+                                                                 double* __restrict__ x, double omega,
+                                                                 double* __restrict__ cbuf, int pf, Outbox ob) {
+    schur_thread_body<MT, D, NRB, DET, NDP, RA, OB>(np, nchunks, NN, pairs, W, ND, npid, nbase, ntbl, PD, NR, AUX, r,
+                                                    x, omega, cbuf, pf, ob_view(ob));
+    if constexpr (OB) {   // a writer: this warp's chunk holds a ghost-writing patch
+        const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        const int64_t chunk = ob.rot ? (gw < ob.rot ? gw + nchunks - ob.rot : gw - ob.rot) : gw;
+        const int64_t i = chunk * 32 + (threadIdx.x & 31);
+        if (__any_sync(0xffffffffu, gw < nchunks && i < np && ob.pflag[i])) ob_writer_done(ob);
+    }
+}
+
 // one patch per warp (3D and large patches): lane k owns restricted node k
 // MTC > 0: compile-time number of restricted nodes (27 for the 3D PoU interior shape): the column
 // loads then use immediate offsets from a running pointer instead of 64-bit index arithmetic
-template <int D, bool DET = false, int WB = 8, int MTC = 0>
+template <int D, bool DET = false, int WB = 8, int MTC = 0, bool OB = false>
 __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int MT, int nnmax,
                                                                const int64_t* __restrict__ foffs,
                                                                const int64_t* __restrict__ nodeoffs,
@@ -936,8 +978,10 @@ __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int M
                                                                const int32_t* __restrict__ nresn,
                                                                const double* __restrict__ fac,
                                                                const double* __restrict__ r, double* __restrict__ x,
-                                                               double omega, double* __restrict__ cbuf, int wpf) {
+                                                               double omega, double* __restrict__ cbuf, int wpf,
+                                                               Outbox ob) {
     extern __shared__ double sm[];
+    const ObView obv = ob_view(ob);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* rl = sm + (size_t)warp * nnmax * D;
     for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < np; i += (int64_t)gridDim.x * 8) {
@@ -1020,17 +1064,23 @@ __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int M
         if (lane < nresn[i]) {
             const double wk = omega * aux[lane];
             const int nd = nodes[no + lane];
+            const bool flagged = OB && obv.pflag[i];
+            if (OB && flagged) ob_wait_acks(obv);
 #pragma unroll
             for (int c = 0; c < D; ++c) {
                 const double v = wk * fma(g[lane * D + c], t, acc[c]);
                 if (DET) cb[lane * D + c] = v;
+                else if (OB) ob_add(obv, flagged, x, nd + c, v);
                 else atomicAdd(x + nd + c, v);
             }
         }
         if (lane == 0) {
             if (DET) cb[MT * D] = omega * aux[MT] * (-t);
+            else if (OB) red_add(x + pdof[i], omega * aux[MT] * (-t));
             else atomicAdd(x + pdof[i], omega * aux[MT] * (-t));
         }
+        if constexpr (OB)   // a writer: this patch is ghost-writing (warp-uniform: one patch per warp)
+            if (obv.pflag[i]) ob_writer_done(ob);
         __syncwarp();
     }
 }
@@ -1729,17 +1779,18 @@ rav_status launch_mv_color(const Csr& A, const Factors& F, int64_t ncol, const i
     return RAV_OK;
 }
 
-template <int MT, bool DET>
+template <int MT, bool DET, bool OB = false>
 static void launch_schur_thread(int64_t np, const Factors& F, const double* r, double* x, double omega,
-                                cudaStream_t s) {
+                                cudaStream_t s, const Outbox& ob = Outbox{}) {
     const double2* W = reinterpret_cast<const double2*>(F.facT);
     // 2D PoU interior shape (25 nodes, 9 restricted): compile-time rectangular loop (122 -> 113 us at c2)
     const bool shape = MT == 9 && F.NN == 25;
     const bool ra = (reinterpret_cast<uintptr_t>(r) & 15) == 0;
-    auto kern = F.npid ? (shape ? (ra ? schur_sweep_thread_kernel<MT, 2, 8, DET, true, true>
-                                      : schur_sweep_thread_kernel<MT, 2, 8, DET, true>)
-                                : schur_sweep_thread_kernel<MT, 2, 0, DET, true>)
-                       : shape ? schur_sweep_thread_kernel<MT, 2, 8, DET> : schur_sweep_thread_kernel<MT, 2, 0, DET>;
+    auto kern = F.npid ? (shape ? (ra ? schur_sweep_thread_kernel<MT, 2, 8, DET, true, true, OB>
+                                      : schur_sweep_thread_kernel<MT, 2, 8, DET, true, false, OB>)
+                                : schur_sweep_thread_kernel<MT, 2, 0, DET, true, false, OB>)
+                       : shape ? schur_sweep_thread_kernel<MT, 2, 8, DET, false, false, OB>
+                               : schur_sweep_thread_kernel<MT, 2, 0, DET, false, false, OB>;
     // rectangular blocks prefetched ahead by the bulk-copy unit (0: off).  Measured (rav_apply alone):
     // c2 115.0 / 109.7 / 108.9 / 110.3 / 117.0 us for 0 / 1 / 2 / 3 / 5; c3 1606 -> 1474 us at 2
     static const int pf = [] {
@@ -1748,17 +1799,22 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
     }();
     launch_maybe_pdl(kern, dim3((unsigned)cdiv(F.nchunks * 32, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
                      (const int32_t*)F.DT, (const int32_t*)F.npid, (const int32_t*)F.nbase, (const int32_t*)F.ntbl,
-                     (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, pf);
+                     (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, pf, ob);
 }
 
-template <int D, bool DET>
-static void launch_schur_perpatch(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
-                                  cudaStream_t s) {
-    static const int64_t cta_max = [] {   // patch count below which a CTA (8 warps) takes one patch
+static int64_t schur_cta_max() {   // patch count below which a CTA (8 warps) takes one patch
+    static const int64_t cta_max = [] {
         const char* e = getenv("RAV_SCHUR_CTA_MAX");
         return e ? atoll(e) : 2048;
     }();
-    if (P.n_patches < cta_max && F.MT <= 32) {   // coarse levels: a CTA per patch (latency)
+    return cta_max;
+}
+
+template <int D, bool DET, bool OB = false>
+static void launch_schur_perpatch(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
+                                  cudaStream_t s, const Outbox& ob = Outbox{}) {
+    const int64_t cta_max = schur_cta_max();
+    if (!OB && P.n_patches < cta_max && F.MT <= 32) {   // coarse levels: a CTA per patch (latency)
         const size_t shmem = sizeof(double) * ((size_t)F.NN * D + 8 * 32 * (size_t)D);
         schur_sweep_cta_kernel<D, DET><<<(int)std::max<int64_t>(1, P.n_patches), 256, shmem, s>>>(
             P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD, F.NR, F.fac, r, x, omega, F.cbuf);
@@ -1783,12 +1839,12 @@ static void launch_schur_perpatch(const PatchSet& P, const Factors& F, const dou
             const char* e = getenv("RAV_SCHUR_MTC");
             return e ? atoi(e) : 1;
         }();
-        auto kern = (mtc && D == 3 && F.MT == 27) ? (wb >= 16 ? schur_sweep_warp_kernel<D, DET, 16, 27>
-                                                              : schur_sweep_warp_kernel<D, DET, 8, 27>)
-                  : wb >= 24 ? schur_sweep_warp_kernel<D, DET, 24>
-                  : wb >= 16 ? schur_sweep_warp_kernel<D, DET, 16> : schur_sweep_warp_kernel<D, DET, 8>;
+        auto kern = (mtc && D == 3 && F.MT == 27) ? (wb >= 16 ? schur_sweep_warp_kernel<D, DET, 16, 27, OB>
+                                                              : schur_sweep_warp_kernel<D, DET, 8, 27, OB>)
+                  : wb >= 24 ? schur_sweep_warp_kernel<D, DET, 24, 0, OB>
+                  : wb >= 16 ? schur_sweep_warp_kernel<D, DET, 16, 0, OB> : schur_sweep_warp_kernel<D, DET, 8, 0, OB>;
         kern<<<blocks, 256, shmem, s>>>(P.n_patches, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD, F.NR, F.fac, r, x,
-                                        omega, F.cbuf, wpf);
+                                        omega, F.cbuf, wpf, ob);
     }
 }
 
@@ -1836,6 +1892,34 @@ rav_status launch_schur_sweep(const PatchSet& P, const Factors& F, const double*
         count_launch();
         RAV_CHECK_LAUNCH();
     }
+    return RAV_OK;
+}
+
+bool schur_fusable(const PatchSet& P, const Factors& F) {
+    if (F.cbuf) return false;   // deterministic mode keeps its two-phase scatter
+    if (F.layout == 4) return F.D == 2 && (F.MT == 1 || F.MT == 2 || F.MT == 4 || F.MT == 9);
+    return F.layout == 5 && F.D >= 1 && F.D <= 3;
+}
+
+rav_status launch_schur_sweep_ob(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
+                                 const Outbox& ob, cudaStream_t s) {
+    if (!schur_fusable(P, F)) { set_error("fused sweep: unsupported factor layout"); return RAV_ERR_ARG; }
+    if (F.layout == 4) {
+        switch (F.MT) {
+            case 1: launch_schur_thread<1, false, true>(P.n_patches, F, r, x, omega, s, ob); break;
+            case 2: launch_schur_thread<2, false, true>(P.n_patches, F, r, x, omega, s, ob); break;
+            case 4: launch_schur_thread<4, false, true>(P.n_patches, F, r, x, omega, s, ob); break;
+            default: launch_schur_thread<9, false, true>(P.n_patches, F, r, x, omega, s, ob); break;
+        }
+    } else if (F.D == 3) {
+        launch_schur_perpatch<3, false, true>(P, F, r, x, omega, s, ob);
+    } else if (F.D == 2) {
+        launch_schur_perpatch<2, false, true>(P, F, r, x, omega, s, ob);
+    } else {
+        launch_schur_perpatch<1, false, true>(P, F, r, x, omega, s, ob);
+    }
+    count_launch();
+    RAV_CHECK_LAUNCH();
     return RAV_OK;
 }
 

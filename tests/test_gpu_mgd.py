@@ -115,11 +115,12 @@ VC_CASES = [
     (si.problem(3, (8, 8, 16), si.KIND_CAVITY, eta="fourier"), 3, 3, True, 1e-8, False),
     (si.problem(2, (64, 64), si.KIND_MMS, eta="fourier"), 5, 3, 2, 1e-8, True),
     (si.problem(3, (8, 8, 16), si.KIND_CAVITY, eta="fourier"), 3, 3, 2, 1e-8, False),
+    (si.problem(2, (64, 64), si.KIND_MMS, eta="fourier"), 5, 4, 2, 1e-8, False),
 ]
 
 
 @pytest.mark.parametrize("case", VC_CASES, ids=["2d-mms-3-det", "2d-mms-4-nccl", "2d-cav-2-nccl-det", "3d-3-nccl",
-                                                "2d-mms-3-peer-det", "3d-3-peer"])
+                                                "2d-mms-3-peer-det", "3d-3-peer-fused", "2d-mms-4-peer-fused"])
 def test_mgd_solve_matches_oracle(rg, rdist, case):
     prob, levels, R, via, rtol, det = case
     comm = _comm(rg, via)
@@ -197,3 +198,25 @@ def test_mgd_peer_transport_rejects_mv(rg, rdist):
     with pytest.raises(rg.RavError):
         rdist.build_lib_dist(prob, 1, 2, [0, 1], [0, 0], _comm(rg, 0), weights="full", variant=2, smooth_only=True,
                              via_comm=2)
+
+
+def test_mgd_fused_exchange_matches_local_exchange(rg, rdist):
+    """The interface exchange fused into the sweep (peer transport, non-deterministic mode: the
+    sweep's scatter adds ghost-written corrections into the owners' receive buffers) gives the
+    local exchange's iterate to rounding (the same additions, atomics in another order), through
+    graph replays of 3 x 2 sweeps, 2D thread kernel and 3D warp kernel."""
+    for prob in (si.problem(2, (40, 48), si.KIND_MMS, eta="fourier"), si.problem(3, (6, 6, 14), si.KIND_CAVITY,
+                                                                                   eta="fourier")):
+        n = oracle.assemble(prob)["n"]
+        out = []
+        for via in (0, 2):
+            mgd, info = rdist.build_lib_dist(prob, 1, 3, [0, 1, 2], [0, 0, 0], _comm(rg, via), smooth_only=True,
+                                             via_comm=via)
+            xs = _scatter(info, si.initial_guess(n, seed=7))
+            for _ in range(3):
+                mgd.smooth(xs, info["b"], 2, 0.66)
+            torch.cuda.synchronize()
+            out.append(_gather(info, xs, n))
+            assert np.isfinite(mgd.residual_norm(xs, info["b"]))
+            mgd.close()
+        assert_entrywise(out[1], out[0], np.abs(out[0]).max(), tol=1e-13, what="fused vs local exchange")
