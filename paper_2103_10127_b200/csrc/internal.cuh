@@ -41,6 +41,12 @@ struct NodeBlocked {
     // of its pattern pid[t] (tbl[pid * W + k]; A entries first, then B); col is then freed
     int32_t *pid = nullptr, *baseA = nullptr, *baseB = nullptr, *tbl = nullptr;
     int W = 0, npat = 0;
+    // B-value compression (after the column compression): the B / B^T values of a slot (its d
+    // values per B entry, in entry order) are a vector of the small table vtbl at offset vofs[t];
+    // the slice value arrays then hold only the A entries (32 A values per slice)
+    int32_t* vofs = nullptr;
+    double* vtbl = nullptr;
+    int64_t nvtbl = 0, nbvec = 0;
 };
 
 struct Csr {

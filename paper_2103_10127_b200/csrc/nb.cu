@@ -209,11 +209,14 @@ struct NbCols {
     const int32_t* __restrict__ tbl;
     int W;
     int bulk;   // prologue: the warp's whole slice into L2 by one bulk prefetch
+    const int32_t* __restrict__ vofs;   // VB: per slot, offset of its B-value vector in vtbl
+    const double* __restrict__ vtbl;
 };
 
 // XA: x is 16-byte aligned (checked once at launch), so the node gathers of the pair layout are
 // single 16-byte loads without the per-load alignment test of ld_node
-template <int D, int G, int UA, int MINB = 1, bool PAT = false, bool PR = false, bool XA = false>
+// VB: B / B^T values from the table cols.vtbl (L1-resident) instead of the slice's value stream
+template <int D, int G, int UA, int MINB = 1, bool PAT = false, bool PR = false, bool XA = false, bool VB = false>
 __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64_t nnodes, int64_t nslices, int64_t nvel,
                                                           const int32_t* __restrict__ perm,
                                                           const int32_t* __restrict__ wa,
@@ -225,6 +228,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                                                           const double* __restrict__ b, double* __restrict__ r,
                                                           double* __restrict__ part) {
     static_assert(!PR || D == 2, "pair layout is 2D only");
+    static_assert(!VB || PAT, "B-value table: compressed columns only");
     auto ldx2 = [&](const double* p, double* out) {
         if constexpr (XA) {
             const double2 v = __ldg(reinterpret_cast<const double2*>(p));
@@ -245,7 +249,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
     if (G > 1 && cols.bulk) {   // the first warp of each slice prefetches the whole slice
         const int64_t t0 = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) / G;
         const int64_t s0 = t0 / NB_C;
-        if (s0 < nslices && t0 % NB_C == 0 && (threadIdx.x & 31) == 0)
+        if (s0 < nslices && t0 % NB_C == 0 && (threadIdx.x & 31) == 0 && vptr[s0 + 1] > vptr[s0])
             bulk_prefetch_l2(v + vptr[s0], (uint32_t)((vptr[s0 + 1] - vptr[s0]) * 8));
     }
     if (G == 1) {   // before x exists: this warp's first slice lines (values, columns) into L2
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
         if (s0 < nslices) {
             const char* vb = reinterpret_cast<const char*>(v + vptr[s0]);
             if (cols.bulk) {
-                if (lane == 0) bulk_prefetch_l2(vb, (uint32_t)((vptr[s0 + 1] - vptr[s0]) * 8));
+                if (lane == 0 && vptr[s0 + 1] > vptr[s0]) bulk_prefetch_l2(vb, (uint32_t)((vptr[s0 + 1] - vptr[s0]) * 8));
                 if (PAT && lane == 1) prefetch_l2(cols.pid + s0 * NB_C);
                 if (PAT && lane == 2) prefetch_l2(cols.baseA + s0 * NB_C);
                 if (PAT && lane == 3) prefetch_l2(cols.baseB + s0 * NB_C);
@@ -277,6 +281,8 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
         // PAT: column of entry k = base + tbl[pid * W + k] (the pattern table is L1-resident)
         const int32_t* tp = PAT ? cols.tbl + (int64_t)(live ? cols.pid[t] : 0) * cols.W : nullptr;
         const int32_t bA = PAT && live ? cols.baseA[t] : 0, bB = PAT && live ? cols.baseB[t] : 0;
+        const double* vbt = VB ? cols.vtbl + (live ? cols.vofs[t] : 0) : nullptr;   // B values of the slot
+#define NB_VB2(k) (VB ? __ldg(reinterpret_cast<const double2*>(vbt) + (k)) : __ldcs(pB + (int64_t)(k) * NB_C))
 #define NB_COLA(k) (PAT ? bA + __ldg(tp + (k)) : __ldcs(cA + (k) * NB_C))
 #define NB_COLB(k) (PAT ? bB + __ldg(tp + A + (k)) : __ldcs(cB + (k) * NB_C))
         const double* vs = v + (live ? vptr[s] : 0);   // the slice's values (layout: nb_ia / nb_ib)
@@ -315,7 +321,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
 #pragma unroll 2
                     for (int k = 0; k < B; ++k) {
                         const double xp = __ldg(x + NB_COLB(k));
-                        const double2 bv = __ldcs(pB + (int64_t)k * NB_C);
+                        const double2 bv = NB_VB2(k);
                         acc[0] = fma(bv.x, xp, acc[0]);
                         acc[1] = fma(bv.y, xp, acc[1]);
                     }
@@ -333,7 +339,8 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                     for (int k = 0; k < B; ++k) {
                         const double xp = __ldg(x + NB_COLB(k));
 #pragma unroll
-                        for (int c = 0; c < D; ++c) acc[c] = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), xp, acc[c]);
+                        for (int c = 0; c < D; ++c)
+                            acc[c] = fma(VB ? __ldg(vbt + k * D + c) : __ldcs(vB + ((int64_t)k * D + c) * NB_C), xp, acc[c]);
                     }
                 }
                 const int64_t r0 = br * D;
@@ -358,7 +365,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                     for (int k = 0; k < B; ++k) {
                         double xv[2];
                         ldx2(x + NB_COLB(k), xv);
-                        const double2 bv = __ldcs(pB + (int64_t)k * NB_C);
+                        const double2 bv = NB_VB2(k);
                         acc = fma(bv.x, xv[0], acc);
                         acc = fma(bv.y, xv[1], acc);
                     }
@@ -367,7 +374,8 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                     for (int k = 0; k < B; ++k) {
                         const int cc = NB_COLB(k);
 #pragma unroll
-                        for (int c = 0; c < D; ++c) acc = fma(__ldcs(vB + ((int64_t)k * D + c) * NB_C), __ldg(x + cc + c), acc);
+                        for (int c = 0; c < D; ++c)
+                            acc = fma(VB ? __ldg(vbt + k * D + c) : __ldcs(vB + ((int64_t)k * D + c) * NB_C), __ldg(x + cc + c), acc);
                     }
                 }
                 const int64_t row = nvel + (br - nnodes);
@@ -396,7 +404,8 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
             for (int k = q; k < B; k += G) {
                 const double xp = __ldg(x + NB_COLB(k));
 #pragma unroll
-                for (int c = 0; c < D; ++c) acc[c] = fma(__ldcs(vs + nb_ib(PR, D, A, k, c, l)), xp, acc[c]);
+                for (int c = 0; c < D; ++c)
+                    acc[c] = fma(VB ? __ldg(vbt + k * D + c) : __ldcs(vs + nb_ib(PR, D, A, k, c, l)), xp, acc[c]);
             }
         } else if (br >= 0) {
 #pragma unroll UA
@@ -404,7 +413,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                 const int cc = NB_COLB(k);
 #pragma unroll
                 for (int c = 0; c < D; ++c)
-                    acc[0] = fma(__ldcs(vs + nb_ib(PR, D, A, k, c, l)), __ldg(x + cc + c), acc[0]);
+                    acc[0] = fma(VB ? __ldg(vbt + k * D + c) : __ldcs(vs + nb_ib(PR, D, A, k, c, l)), __ldg(x + cc + c), acc[0]);
             }
         }
         if (G > 1) {
@@ -431,6 +440,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
     }
 #undef NB_COLA
 #undef NB_COLB
+#undef NB_VB2
     if (part) {
         mine = warp_sum(mine);
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mine;
@@ -604,6 +614,185 @@ static rav_status nb_compress(NodeBlocked& N, cudaStream_t s) {
     return RAV_OK;
 }
 
+// ---- B-value compression ----------------------------------------------------------------------
+// The B block carries no viscosity (Eq. 6: b_jp = -(q_p, div phi_j)), so on a uniform level
+// the d values of every B / B^T entry repeat from row to row: a slot's B values (entry order,
+// d per entry) form one of a few distinct vectors.  They are hashed, deduplicated, verified
+// bitwise against a table and dropped from the streamed values (c2: half of the residual's bytes).
+// The residual reads the same values in the same order: bitwise the same result.
+__global__ void nb_bhash_kernel(int64_t nslots, int D, int pair, const int32_t* wa, const int32_t* wb,
+                                const int64_t* vptr, const double* v, uint64_t* key, int32_t* idx) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nslots; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t / NB_C;
+        const int l = (int)(t % NB_C);
+        const int A = wa[s], B = wb[s];
+        const double* vs = v + vptr[s];
+        uint64_t h = 1469598103934665603ull;
+        h = fnv(h, (uint32_t)B);
+        for (int k = 0; k < B; ++k)
+            for (int c = 0; c < D; ++c) {
+                const uint64_t u = (uint64_t)__double_as_longlong(vs[nb_ib(pair != 0, D, A, k, c, l)]);
+                h = fnv(fnv(h, (uint32_t)u), (uint32_t)(u >> 32));
+            }
+        key[t] = h;
+        idx[t] = (int32_t)t;
+    }
+}
+
+__global__ void nb_vlen_kernel(int nvec, int D, const int32_t* rep, const int32_t* wb, int64_t* len) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < nvec; p += gridDim.x * blockDim.x)
+        len[p] = (int64_t)wb[rep[p] / NB_C] * D;
+}
+
+__global__ void nb_vtbl_kernel(int nvec, int D, int pair, const int32_t* rep, const int32_t* wa, const int32_t* wb,
+                               const int64_t* vptr, const double* v, const int64_t* voff, double* vtbl) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < nvec; p += gridDim.x * blockDim.x) {
+        const int64_t t = rep[p], s = t / NB_C;
+        const int l = (int)(t % NB_C);
+        const int A = wa[s], B = wb[s];
+        for (int k = 0; k < B; ++k)
+            for (int c = 0; c < D; ++c) vtbl[voff[p] + k * D + c] = v[vptr[s] + nb_ib(pair != 0, D, A, k, c, l)];
+    }
+}
+
+// per slot: its vector's offset; verify length and every value bitwise
+__global__ void nb_vverify_kernel(int64_t nslots, int D, int pair, const int32_t* wa, const int32_t* wb,
+                                  const int64_t* vptr, const double* v, const int32_t* sidx, const int32_t* seg,
+                                  const int64_t* voff, const int64_t* vlen, const double* vtbl, int32_t* vofs,
+                                  unsigned int* err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nslots; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = sidx[i], s = t / NB_C;
+        const int p = seg[i] - 1;
+        const int l = (int)(t % NB_C);
+        const int A = wa[s], B = wb[s];
+        vofs[t] = (int32_t)voff[p];
+        if (vlen[p] != (int64_t)B * D) { atomicOr(err, 1u); continue; }
+        for (int k = 0; k < B; ++k)
+            for (int c = 0; c < D; ++c)
+                if (__double_as_longlong(v[vptr[s] + nb_ib(pair != 0, D, A, k, c, l)]) !=
+                    __double_as_longlong(vtbl[voff[p] + k * D + c]))
+                    atomicOr(err, 1u);
+    }
+}
+
+// the A part of each slice: its first 32 A values in both layouts (nb_ia < 32 A)
+__global__ void nb_asize_kernel(int64_t nslices, const int32_t* wa, int64_t* sz) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslices; s += (int64_t)gridDim.x * blockDim.x)
+        sz[s] = (int64_t)NB_C * wa[s];
+}
+__global__ void nb_acopy_kernel(int64_t nslices, const int64_t* vptr, const int64_t* vptr2, const double* v,
+                                double* v2) {
+    for (int64_t s = blockIdx.x; s < nslices; s += gridDim.x) {
+        const int64_t n = vptr2[s + 1] - vptr2[s];
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v2[vptr2[s] + i] = v[vptr[s] + i];
+    }
+}
+
+static rav_status nb_compress_bvals(NodeBlocked& N, cudaStream_t s) {
+    const int64_t ns = N.nslices * NB_C;
+    const int D = N.D;
+    uint64_t *key = nullptr, *skey = nullptr;
+    int32_t *idx = nullptr, *sidx = nullptr, *flag = nullptr, *seg = nullptr, *rep = nullptr, *vofs = nullptr;
+    int64_t *vlen = nullptr, *voff = nullptr, *asz = nullptr, *vptr2 = nullptr;
+    double *vtbl = nullptr, *v2 = nullptr;
+    unsigned int* err = nullptr;
+    void *d_tmp = nullptr, *d_tmp2 = nullptr;
+    bool ok = true;
+    int32_t nvec = 0;
+    int64_t nt = 0;
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(ns, 256), (int64_t)num_sms() * 16));
+    RAV_CUDA(cudaMallocAsync(&key, sizeof(uint64_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&skey, sizeof(uint64_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&idx, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&sidx, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&flag, sizeof(int32_t) * ns, s));
+    RAV_CUDA(cudaMallocAsync(&seg, sizeof(int32_t) * ns, s));
+    nb_bhash_kernel<<<nb, 256, 0, s>>>(ns, D, N.pair, N.wa, N.wb, N.vptr, N.val, key, idx);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    size_t tmp = 0, tmp2 = 0;
+    RAV_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, skey, idx, sidx, (int)ns, 0, 64, s));
+    RAV_CUDA(cudaMallocAsync(&d_tmp, tmp + 16, s));
+    RAV_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp, key, skey, idx, sidx, (int)ns, 0, 64, s));
+    nb_segment_kernel<<<nb, 256, 0, s>>>(ns, skey, flag);
+    count_launch();
+    RAV_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp2, flag, seg, (int)ns, s));
+    RAV_CUDA(cudaMallocAsync(&d_tmp2, tmp2 + 16, s));
+    RAV_CUDA(cub::DeviceScan::InclusiveSum(d_tmp2, tmp2, flag, seg, (int)ns, s));
+    RAV_CUDA(cudaMemcpyAsync(&nvec, seg + ns - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    RAV_CUDA(cudaStreamSynchronize(s));
+    ok = nvec > 0 && nvec <= 65536;
+    if (ok) {
+        RAV_CUDA(cudaMallocAsync(&rep, sizeof(int32_t) * nvec, s));
+        RAV_CUDA(cudaMallocAsync(&vlen, sizeof(int64_t) * nvec, s));
+        RAV_CUDA(cudaMallocAsync(&voff, sizeof(int64_t) * (nvec + 1), s));
+        int32_t* dummy_pid = nullptr;
+        RAV_CUDA(cudaMallocAsync(&dummy_pid, sizeof(int32_t) * ns, s));
+        nb_pid_kernel<<<nb, 256, 0, s>>>(ns, sidx, flag, seg, dummy_pid, rep);
+        count_launch();
+        cudaFreeAsync(dummy_pid, s);
+        nb_vlen_kernel<<<(int)cdiv(nvec, 128), 128, 0, s>>>(nvec, D, rep, N.wb, vlen);
+        count_launch();
+        RAV_TRY(gen::counts_to_rowptr(vlen, voff, nvec, s));
+        RAV_CUDA(cudaMemcpyAsync(&nt, voff + nvec, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        RAV_CUDA(cudaStreamSynchronize(s));
+        ok = nt * 8 <= (8 << 20) && nt < (1ll << 31);   // the table stays cache-sized
+    }
+    if (ok) {
+        RAV_CUDA(cudaMalloc(&vtbl, sizeof(double) * std::max<int64_t>(2, nt)));
+        RAV_CUDA(cudaMalloc(&vofs, sizeof(int32_t) * ns));
+        RAV_CUDA(cudaMallocAsync(&err, sizeof(unsigned int), s));
+        RAV_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
+        nb_vtbl_kernel<<<(int)cdiv(nvec, 128), 128, 0, s>>>(nvec, D, N.pair, rep, N.wa, N.wb, N.vptr, N.val, voff, vtbl);
+        count_launch();
+        nb_vverify_kernel<<<nb, 256, 0, s>>>(ns, D, N.pair, N.wa, N.wb, N.vptr, N.val, sidx, seg, voff, vlen, vtbl,
+                                             vofs, err);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+        unsigned int h_err = 0;
+        RAV_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(h_err), cudaMemcpyDeviceToHost, s));
+        RAV_CUDA(cudaStreamSynchronize(s));
+        ok = h_err == 0;   // a hash collision keeps the values in the stream
+    }
+    int64_t hv2 = 0, hv = 0;
+    if (ok) {   // the slices' values shrink to their A parts
+        RAV_CUDA(cudaMallocAsync(&asz, sizeof(int64_t) * N.nslices, s));
+        RAV_CUDA(cudaMalloc(&vptr2, sizeof(int64_t) * (N.nslices + 1)));
+        const int nbs = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(N.nslices, 256), (int64_t)num_sms() * 16));
+        nb_asize_kernel<<<nbs, 256, 0, s>>>(N.nslices, N.wa, asz);
+        count_launch();
+        RAV_TRY(gen::counts_to_rowptr(asz, vptr2, N.nslices, s));
+        RAV_CUDA(cudaMemcpyAsync(&hv2, vptr2 + N.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        RAV_CUDA(cudaMemcpyAsync(&hv, N.vptr + N.nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        RAV_CUDA(cudaStreamSynchronize(s));
+        RAV_CUDA(cudaMalloc(&v2, sizeof(double) * std::max<int64_t>(2, hv2)));
+        nb_acopy_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(N.nslices, (int64_t)num_sms() * 16)), 256, 0, s>>>(
+            N.nslices, N.vptr, vptr2, N.val, v2);
+        count_launch();
+        RAV_CHECK_LAUNCH();
+    }
+    for (void* p : {(void*)key, (void*)skey, (void*)idx, (void*)sidx, (void*)flag, (void*)seg, (void*)rep, (void*)vlen,
+                    (void*)voff, (void*)err, (void*)asz, d_tmp, d_tmp2})
+        if (p) cudaFreeAsync(p, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    if (!ok) {
+        for (void* p : {(void*)vtbl, (void*)vofs})
+            if (p) cudaFree(p);
+        return RAV_OK;
+    }
+    cudaFree(N.val);
+    cudaFree(N.vptr);
+    N.val = v2;
+    N.vptr = vptr2;
+    N.vofs = vofs;
+    N.vtbl = vtbl;
+    N.nvtbl = nt;
+    N.nbvec = nvec;
+    // streamed bytes: the dropped B values out, a 4-byte vector offset per slot in
+    N.bytes = N.bytes - 8 * (hv - hv2) + 4 * ns;
+    return RAV_OK;
+}
+
 rav_status nb_build(Csr& A, int64_t nvel, int D, cudaStream_t s) {
     NodeBlocked& N = A.nb;
     if (D < 2 || D > 3 || nvel <= 0 || nvel % D != 0 || A.n_rows != A.n_cols || nvel >= A.n_rows) return RAV_OK;
@@ -691,12 +880,17 @@ rav_status nb_build(Csr& A, int64_t nvel, int D, cudaStream_t s) {
         return !(e && atoi(e) == 0);
     }();
     if (compress) RAV_TRY(nb_compress(N, s));
+    static const bool bvals = [] {
+        const char* e = getenv("RAV_NB_BVALS");
+        return !(e && atoi(e) == 0);
+    }();
+    if (bvals && N.tbl) RAV_TRY(nb_compress_bvals(N, s));
     return RAV_OK;
 }
 
 void nb_free(NodeBlocked& N) {
     for (void* p : {(void*)N.perm, (void*)N.wa, (void*)N.wb, (void*)N.cptr, (void*)N.vptr, (void*)N.col, (void*)N.val,
-                    (void*)N.pid, (void*)N.baseA, (void*)N.baseB, (void*)N.tbl})
+                    (void*)N.pid, (void*)N.baseA, (void*)N.baseB, (void*)N.tbl, (void*)N.vofs, (void*)N.vtbl})
         if (p) cudaFree(p);
     N = NodeBlocked{};
 }
@@ -718,7 +912,7 @@ static void nb_launch(const NodeBlocked& N, const double* x, const double* b, do
         const char* e = getenv("RAV_NB_BULK");
         return e ? atoi(e) : 1;
     }();
-    const NbCols cols{N.col, N.pid, N.baseA, N.baseB, N.tbl, N.W, bulk};
+    const NbCols cols{N.col, N.pid, N.baseA, N.baseB, N.tbl, N.W, bulk, N.vofs, N.vtbl};
     const int bs = nb_block_threads();
     const int64_t full = cdiv(N.nslices * NB_C * G, bs);
     // with partial norms: one partial per block, the full grid when the caller's buffer holds it
@@ -728,7 +922,11 @@ static void nb_launch(const NodeBlocked& N, const double* x, const double* b, do
         const char* e = getenv("RAV_NB_MINB");
         return e ? atoi(e) : 6;
     }();
-    auto kern = N.tbl ? ((minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8, true, PR, XA>
+    auto kern = N.vtbl ? ((minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8, true, PR, XA, true>
+                         : (minb >= 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6, true, PR, XA, true>
+                         : (minb == 5 && G == 1) ? nb_residual_kernel<D, G, UA, 5, true, PR, XA, true>
+                                                 : nb_residual_kernel<D, G, UA, 1, true, PR, XA, true>)
+              : N.tbl ? ((minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8, true, PR, XA>
                          : (minb >= 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6, true, PR, XA>
                          : (minb == 5 && G == 1) ? nb_residual_kernel<D, G, UA, 5, true, PR, XA>
                                                  : nb_residual_kernel<D, G, UA, 1, true, PR, XA>)

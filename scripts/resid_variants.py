@@ -26,3 +26,6 @@ ms = e0.elapsed_time(e1) / 50
 by = sm.sweep_bytes()["residual"]
 print(f"residual {ms*1e3:8.1f} us  {by/ms/1e6:8.1f} GB/s  ({by/1e9:.3f} GB)  nnz {L['nnz']}", flush=True)
 print("patterns", "n/a")
+if len(sys.argv) > 2:
+    import numpy as np
+    np.save(sys.argv[2], r.cpu().numpy())
