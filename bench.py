@@ -984,8 +984,8 @@ def run_gpu(args):
                    "free_dofs": n, "nnz": nnz_c2, "patches": npatch_c2,
                    "sweeps_per_step": SWEEPS_PER_STEP, "omega": OMEGA, "weights": "partition of unity (R3)",
                    "l2": "inputs larger than L2 (per sweep the factored Schur rows, 0.58 GB, and the node-blocked "
-                         "operator, 0.42 GB, stream from HBM; x, r, b vectors, 19 MB each, stay L2-resident "
-                         "by design)",
+                         "operator, 0.22 GB with its B values in an L1-resident table, stream from HBM; x, r, b "
+                         "vectors, 19 MB each, stay L2-resident by design)",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,

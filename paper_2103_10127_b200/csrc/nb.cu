@@ -947,9 +947,17 @@ static int nb_lanes(const NodeBlocked& N) {
     }();
     // measured: 3D c4 98 us (G=2) vs 110 (G=1), 111 (G=4); 2D c2 G=1 best.  Small (coarse) levels
     // cannot fill the GPU with one short group per row: their long rows get a full warp (latency)
+    static const int64_t t32 = [] {   // block rows below which a row gets a full warp (32 lanes, 3D)
+        const char* e = getenv("RAV_NB_T32");
+        return e ? atoll(e) : 8192;
+    }();
+    static const int64_t t8 = [] {    // ... 8 lanes (3D) / 2 lanes (2D)
+        const char* e = getenv("RAV_NB_T8");
+        return e ? atoll(e) : 131072;
+    }();
     const int G = genv > 0 ? genv
-                           : N.nblock < 8192 ? (N.D == 3 ? 32 : 8)
-                           : N.nblock < 131072 ? (N.D == 3 ? 8 : 2)
+                           : N.nblock < t32 ? (N.D == 3 ? 32 : 8)
+                           : N.nblock < t8 ? (N.D == 3 ? 8 : 2)
                            : (N.D == 3 ? 2 : 1);
     return G >= 32 ? 32 : (G >= 8 ? 8 : (G >= 4 ? 4 : (G >= 2 ? 2 : 1)));
 }
