@@ -55,6 +55,15 @@ namespace rav {
 // computed it), so the first sweep skips its residual pass
 // x_zero: x is zero on entry (coarse-level corrections, FGMRES preconditioner applications), so the
 // first sweep's residual is b itself and is read from b instead of being computed
+// bytes of the sweep's leading factor stream the residual before it prefetches into L2 (RAV_XPF_MB)
+static int64_t xpf_bytes() {
+    static const int64_t v = [] {
+        const char* e = getenv("RAV_XPF_MB");
+        return (int64_t)((e ? atof(e) : 48.0) * 1048576.0);   // measured c2 step: 0 168.7, 32 166.5, 48 165.9, 64 166.4, 96 169.8 us
+    }();
+    return v;
+}
+
 rav_status smooth_launches(rav_ctx* c, double* x, const double* b, int nu, double omega, bool r_ready,
                            bool x_zero) {
     for (int k = 0; k < nu; ++k) {
@@ -68,7 +77,8 @@ rav_status smooth_launches(rav_ctx* c, double* x, const double* b, int nu, doubl
             RAV_TRY(launch_sweep(c->P, c->F, b, x, omega, c->stream));
             continue;
         }
-        if (!(r_ready && k == 0)) RAV_TRY(launch_residual(c->A, x, b, c->r, c->stream));
+        if (!(r_ready && k == 0))
+            RAV_TRY(launch_residual(c->A, x, b, c->r, c->stream, c->F.lead, std::min(c->F.lead_bytes, xpf_bytes())));
         RAV_TRY(launch_sweep(c->P, c->F, c->r, x, omega, c->stream));
     }
     return RAV_OK;

@@ -64,8 +64,11 @@ rav_status nb_build(Csr& A, int64_t nvel, int D, cudaStream_t s);
 void nb_free(NodeBlocked& N);
 // r = b - A x via the node-blocked / SELL copy (r may be null); if part != nullptr also one partial sum
 // of r^2 per block, with min(full grid, nblk) blocks (*used = blocks launched)
+// xpf / xpf_bytes (optional): the NEXT kernel's leading stream (the sweep's first factor chunks),
+// bulk-prefetched into L2 by the residual's last warps while the residual, bound by gather
+// latency, leaves HBM bandwidth unused
 rav_status launch_nb_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
-                              cudaStream_t s, int* used = nullptr);
+                              cudaStream_t s, int* used = nullptr, const void* xpf = nullptr, int64_t xpf_bytes = 0);
 rav_status launch_sell_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
                                 cudaStream_t s, int* used = nullptr);
 int64_t nb_full_blocks(const NodeBlocked& N);
@@ -78,7 +81,8 @@ void csr_free(Csr& A);
 rav_status csr_transpose(const Csr& A, Csr& At, cudaStream_t s);
 
 // r = b - A x
-rav_status launch_residual(const Csr& A, const double* x, const double* b, double* r, cudaStream_t s);
+rav_status launch_residual(const Csr& A, const double* x, const double* b, double* r, cudaStream_t s,
+                           const void* xpf = nullptr, int64_t xpf_bytes = 0);
 // y = alpha * A x + beta * y
 rav_status launch_spmv(const Csr& A, const double* x, double* y, double alpha, double beta, cudaStream_t s);
 // partial sums of squares of (b - A x) into part[nblk]; then total into *out (device)
@@ -139,6 +143,10 @@ struct Factors {
     int32_t* DT = nullptr;     // nchunks * NMAX * 32
     int32_t* NR = nullptr;     // nchunks * 32 restricted counts (0 for padding)
     int64_t bytes = 0;
+    // the sweep's leading factor stream in the order its first wave reads it (layout 4: facT,
+    // chunk-major; layouts 5 / 6: fac, patch-major): what a preceding residual prefetches into L2
+    const void* lead = nullptr;
+    int64_t lead_bytes = 0;
     // layout 4 node-index compression: node j of slot i = nbase[i] + ntbl[npid[i] * NN + j] (DT freed)
     int32_t *npid = nullptr, *nbase = nullptr, *ntbl = nullptr;
     int nnpat = 0;

@@ -124,9 +124,10 @@ static int spmv_blocks(int64_t n, int G) {
     return (int)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
-rav_status launch_residual(const Csr& A, const double* x, const double* b, double* r, cudaStream_t s) {
+rav_status launch_residual(const Csr& A, const double* x, const double* b, double* r, cudaStream_t s,
+                           const void* xpf, int64_t xpf_bytes) {
     if (A.n_rows == 0) return RAV_OK;
-    if (A.nb.nslices > 0) return launch_nb_residual(A, x, b, r, nullptr, 0, s);
+    if (A.nb.nslices > 0) return launch_nb_residual(A, x, b, r, nullptr, 0, s, nullptr, xpf, xpf_bytes);
     if (A.sell.nslices > 0) return launch_sell_residual(A, x, b, r, nullptr, 0, s);
     int nb = spmv_blocks(A.n_rows, A.lanes);
     if (A.lanes == 32)

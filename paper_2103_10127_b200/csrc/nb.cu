@@ -211,7 +211,11 @@ struct NbCols {
     int bulk;   // prologue: the warp's whole slice into L2 by one bulk prefetch
     const int32_t* __restrict__ vofs;   // VB: per slot, offset of its B-value vector in vtbl
     const double* __restrict__ vtbl;
+    const char* xpf;    // the next kernel's leading bytes: prefetched into L2 by the last xpf_warps warps,
+    int64_t xpf_bytes;  // NB_XPF_SEG bytes each
+    int64_t xpf_warps;
 };
+constexpr int64_t NB_XPF_SEG = 8192;
 
 // XA: x is 16-byte aligned (checked once at launch), so the node gathers of the pair layout are
 // single 16-byte loads without the per-load alignment test of ld_node
@@ -266,6 +270,16 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
             } else if (PAT) prefetch_l2(vb + (size_t)lane * 128);
             else if (lane < 16) prefetch_l2(vb + (size_t)lane * 128);
             else prefetch_l2(reinterpret_cast<const char*>(col + cptr[s0]) + (size_t)(lane - 16) * 128);
+        }
+    }
+    if (cols.xpf_warps > 0 && (threadIdx.x & 31) == 0) {   // static data: before the dependency wait
+        const int64_t tw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+        const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        const int64_t k = gw - (tw - cols.xpf_warps);
+        if (k >= 0) {
+            const int64_t off = k * NB_XPF_SEG;
+            if (off < cols.xpf_bytes)
+                bulk_prefetch_l2(cols.xpf + off, (uint32_t)min((int64_t)NB_XPF_SEG, cols.xpf_bytes - off));
         }
     }
     pdl_wait();
@@ -908,17 +922,23 @@ static int nb_block_threads() {
 
 template <int D, int G, int UA, bool PR = false, bool XA = false>
 static void nb_launch(const NodeBlocked& N, const double* x, const double* b, double* r, double* part, int nblk,
-                      cudaStream_t s, int* used) {
+                      cudaStream_t s, int* used, const void* xpf, int64_t xpf_bytes) {
     static const int bulk = [] {   // measured: c2 85.2 -> 81.1 us, c3 1549 -> 1426 us
         const char* e = getenv("RAV_NB_BULK");
         return e ? atoi(e) : 1;
     }();
-    const NbCols cols{N.col, N.pid, N.baseA, N.baseB, N.tbl, N.W, bulk, N.vofs, N.vtbl};
+    NbCols cols{N.col, N.pid, N.baseA, N.baseB, N.tbl, N.W, bulk, N.vofs, N.vtbl, nullptr, 0, 0};
     const int bs = nb_block_threads();
     const int64_t full = cdiv(N.nslices * NB_C * G, bs);
     // with partial norms: one partial per block, the full grid when the caller's buffer holds it
     const int blocks = (int)(part ? std::min<int64_t>(full, nblk) : full);
     if (used) *used = blocks;
+    if (xpf && xpf_bytes >= 16) {   // 16-byte aligned segments, at most half the grid's warps
+        const uintptr_t a = (reinterpret_cast<uintptr_t>(xpf) + 15) & ~(uintptr_t)15;
+        cols.xpf = reinterpret_cast<const char*>(a);
+        cols.xpf_bytes = (xpf_bytes - (int64_t)(a - reinterpret_cast<uintptr_t>(xpf))) & ~(int64_t)15;
+        cols.xpf_warps = std::min<int64_t>(cdiv(cols.xpf_bytes, NB_XPF_SEG), (int64_t)blocks * (bs / 32) / 2);
+    }
     static const int minb = [] {   // register cap of the one-thread-per-row variant (measured: 6 best, 102 vs 105 us)
         const char* e = getenv("RAV_NB_MINB");
         return e ? atoi(e) : 6;
@@ -966,30 +986,30 @@ static int nb_lanes(const NodeBlocked& N) {
 int64_t nb_full_blocks(const NodeBlocked& N) { return cdiv(N.nslices * NB_C * nb_lanes(N), nb_block_threads()); }
 
 rav_status launch_nb_residual(const Csr& A, const double* x, const double* b, double* r, double* part, int nblk,
-                              cudaStream_t s, int* used) {
+                              cudaStream_t s, int* used, const void* xpf, int64_t xpf_bytes) {
     const NodeBlocked& N = A.nb;
     const int G = nb_lanes(N);
     if (N.D == 3) {
-        if (G == 32) nb_launch<3, 32, 2>(N, x, b, r, part, nblk, s, used);
-        else if (G == 8) nb_launch<3, 8, 4>(N, x, b, r, part, nblk, s, used);
-        else if (G == 4) nb_launch<3, 4, 4>(N, x, b, r, part, nblk, s, used);
-        else if (G == 2) nb_launch<3, 2, 4>(N, x, b, r, part, nblk, s, used);
-        else nb_launch<3, 1, 8>(N, x, b, r, part, nblk, s, used);
+        if (G == 32) nb_launch<3, 32, 2>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
+        else if (G == 8) nb_launch<3, 8, 4>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
+        else if (G == 4) nb_launch<3, 4, 4>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
+        else if (G == 2) nb_launch<3, 2, 4>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
+        else nb_launch<3, 1, 8>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
     } else {
         if (N.pair && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && G == 1) {
-            nb_launch<2, 1, 4, true, true>(N, x, b, r, part, nblk, s, used);
+            nb_launch<2, 1, 4, true, true>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
         } else if (N.pair) {
-            if (G == 32) nb_launch<2, 32, 2, true>(N, x, b, r, part, nblk, s, used);
-            else if (G == 8) nb_launch<2, 8, 4, true>(N, x, b, r, part, nblk, s, used);
-            else if (G >= 4) nb_launch<2, 4, 4, true>(N, x, b, r, part, nblk, s, used);
-            else if (G == 2) nb_launch<2, 2, 4, true>(N, x, b, r, part, nblk, s, used);
-            else nb_launch<2, 1, 4, true>(N, x, b, r, part, nblk, s, used);
+            if (G == 32) nb_launch<2, 32, 2, true>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
+            else if (G == 8) nb_launch<2, 8, 4, true>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
+            else if (G >= 4) nb_launch<2, 4, 4, true>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
+            else if (G == 2) nb_launch<2, 2, 4, true>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
+            else nb_launch<2, 1, 4, true>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
         } else {
-            if (G == 32) nb_launch<2, 32, 2>(N, x, b, r, part, nblk, s, used);
-            else if (G == 8) nb_launch<2, 8, 4>(N, x, b, r, part, nblk, s, used);
-            else if (G >= 4) nb_launch<2, 4, 4>(N, x, b, r, part, nblk, s, used);
-            else if (G == 2) nb_launch<2, 2, 4>(N, x, b, r, part, nblk, s, used);
-            else nb_launch<2, 1, 4>(N, x, b, r, part, nblk, s, used);
+            if (G == 32) nb_launch<2, 32, 2>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
+            else if (G == 8) nb_launch<2, 8, 4>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
+            else if (G >= 4) nb_launch<2, 4, 4>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
+            else if (G == 2) nb_launch<2, 2, 4>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
+            else nb_launch<2, 1, 4>(N, x, b, r, part, nblk, s, used, xpf, xpf_bytes);
         }
     }
     count_launch();

@@ -1340,6 +1340,8 @@ rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D,
         RAV_CUDA(cudaMemcpy(F.foffs, fo.data(), sizeof(int64_t) * (P.n_patches + 1), cudaMemcpyHostToDevice));
         RAV_CUDA(cudaMemcpy(F.nodeoffs, no.data(), sizeof(int64_t) * (P.n_patches + 1), cudaMemcpyHostToDevice));
         F.bytes = (int64_t)sizeof(double) * fo.back() + sizeof(int32_t) * no.back();
+        F.lead = F.fac;
+        F.lead_bytes = (int64_t)sizeof(double) * fo.back();
         a.layout = 6;
         a.foffs = F.foffs;
         a.fac = F.fac;
@@ -1368,6 +1370,8 @@ rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D,
         RAV_CUDA(cudaMemsetAsync(F.NR, 0, sizeof(int32_t) * 32 * F.nchunks, s));
         RAV_CUDA(cudaMemsetAsync(F.WT, 0, sizeof(double) * (MT + 2) * 32 * F.nchunks, s));
         F.bytes = (int64_t)fb;
+        F.lead = F.facT;
+        F.lead_bytes = (int64_t)fb;
         a.layout = 4;
         a.NN = F.NN;
         a.pairs = F.pairs;
@@ -1403,6 +1407,8 @@ rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D,
         RAV_CUDA(cudaMemcpy(F.nodeoffs, no.data(), sizeof(int64_t) * (P.n_patches + 1), cudaMemcpyHostToDevice));
         RAV_CUDA(cudaMemsetAsync(F.fac, 0, sizeof(double) * std::max<int64_t>(1, fo.back()), s));
         F.bytes = (int64_t)sizeof(double) * fo.back() + sizeof(int32_t) * no.back();
+        F.lead = F.fac;
+        F.lead_bytes = (int64_t)sizeof(double) * fo.back();
         a.layout = 5;
         a.foffs = F.foffs;
         a.fac = F.fac;
