@@ -928,15 +928,22 @@ def run_gpu(args):
         det = {"error": f"{type(err).__name__}: {err}"[:200]}
 
     # ---- end to end through the C-ABI with host buffers ----------------------------
-    xh = x0.cpu().pin_memory()
+    # K steps = K independent problems (the seeded x0, b) in pinned host memory through
+    # rav_smooth_batch: every step copies its x and b host -> device and its result device -> host
+    # inside the timed region; the library overlaps those copies with the neighbouring steps' sweeps
+    x0h = x0.cpu()
     bh = b.cpu().pin_memory()
-    xh_np, bh_np = xh.numpy(), bh.numpy()
-    sm.smooth(xh_np, bh_np, SWEEPS_PER_STEP, OMEGA)   # warm (staging buffers, graph)
+    xh = [x0h.clone().pin_memory() for _ in range(args.steps)]
+    sm.smooth_batch(xh[:2], [bh, bh], SWEEPS_PER_STEP, OMEGA)   # warm (staging buffers, both graphs)
+    for t_ in xh[:2]:
+        t_.copy_(x0h)
     barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        sm.smooth(xh_np, bh_np, SWEEPS_PER_STEP, OMEGA)   # H2D x,b + 100 sweeps + D2H x (synchronous)
+    sm.smooth_batch(xh, [bh] * args.steps, SWEEPS_PER_STEP, OMEGA)
     e2e_s = time.perf_counter() - t0
+    if not torch.equal(xh[-1], xh[0]):   # independent identical problems: the same result (to atomics)
+        assert float((xh[-1] - xh[0]).abs().max()) <= 1e-10 * float(xh[0].abs().max()), "batch results differ"
+    del xh
     if dist is not None:
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -999,7 +1006,10 @@ def run_gpu(args):
                                         (ms_per_step / SWEEPS_PER_STEP * 1e-3) / 1e9},
         "setup_s": {"generate": t_gen, "factorize": t_factor},
         "e2e": {"value": e2e_value, "unit": "MDoF/s", "h2d_bytes_per_step": 2 * 8 * n,
-                "d2h_bytes_per_step": 8 * n},
+                "d2h_bytes_per_step": 8 * n,
+                "how": "rav_smooth_batch over the K steps as K independent problems in pinned host memory "
+                       "(wall clock around the call); each step's x, b copied in and x copied out inside the "
+                       "timed region, overlapped by the library with the neighbouring steps' sweeps"},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
     }

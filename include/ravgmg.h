@@ -274,6 +274,20 @@ rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opt
  * are part of the call).  Stream-ordered on the context stream. */
 rav_status rav_smooth(rav_ctx* ctx, double* x, const double* b, int nu, double omega);
 
+/* rav_smooth on nprob independent problems held in HOST buffers: problem k
+ * runs nu sweeps on x[k] (in/out, n_rows doubles) with right-hand side b[k]
+ * (b[k] may repeat a pointer).  The library stages them through two device
+ * buffer pairs and a copy stream of its own, so the host->device copy of
+ * problem k+1 and the device->host copy of problem k-1 overlap the sweeps of
+ * problem k (pinned host memory makes the copies asynchronous; pageable
+ * memory still works, without the overlap).  Each problem's result equals
+ * rav_smooth on it (to the atomic scatter's rounding order; bitwise in
+ * deterministic mode).  Needs a context stream (rav_opts.stream).  Returns
+ * when every x[k] holds its result.  Errors: RAV_ERR_ARG for NULL / device
+ * pointers or no stream; RAV_ERR_CUDA. */
+rav_status rav_smooth_batch(rav_ctx* ctx, int64_t nprob, double* const* x, const double* const* b, int nu,
+                            double omega);
+
 /* x += omega * sum_i R~_i^T W_i R_i r for a given residual r (device
  * pointers): one application of the smoother operator S_RAV of P:124 Eq. 13
  * to r, i.e. the sweep kernel alone (used to time it in isolation). */

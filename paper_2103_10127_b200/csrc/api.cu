@@ -229,6 +229,75 @@ rav_status rav_smooth(rav_ctx* c, double* x, const double* b, int nu, double ome
     return RAV_OK;
 }
 
+rav_status rav_smooth_batch(rav_ctx* c, int64_t nprob, double* const* x, const double* const* b, int nu,
+                            double omega) {
+    NvtxRange nvtx_range("rav_smooth_batch");
+    if (!c || nprob < 0 || nu < 0 || (nprob > 0 && (!x || !b))) { set_error("rav_smooth_batch: bad argument"); return RAV_ERR_ARG; }
+    for (int64_t k = 0; k < nprob; ++k)
+        if (!x[k] || !b[k] || is_device_ptr(x[k]) || is_device_ptr(b[k])) {
+            set_error("rav_smooth_batch: problem %lld: x and b must be host pointers", (long long)k);
+            return RAV_ERR_ARG;
+        }
+    if (c->variant == RAV_VARIANT_MV && c->coffs.empty()) {
+        set_error("rav_smooth_batch: RAV_VARIANT_MV needs rav_set_colors first");
+        return RAV_ERR_ARG;
+    }
+    g_launches = 0;
+    if (nprob == 0 || nu == 0) { c->last_launches = 0; return RAV_OK; }
+    if (!c->stream) { set_error("rav_smooth_batch: needs a context stream (rav_opts.stream)"); return RAV_ERR_ARG; }
+    const int64_t n = c->A.n_rows;
+    const size_t bytes = sizeof(double) * (size_t)n;
+    if (!c->hx) {
+        RAV_CUDA(cudaMalloc(&c->hx, bytes));
+        RAV_CUDA(cudaMalloc(&c->hb, bytes));
+    }
+    if (!c->hx2) {
+        RAV_CUDA(cudaMalloc(&c->hx2, bytes));
+        RAV_CUDA(cudaMalloc(&c->hb2, bytes));
+    }
+    if (!c->cstream) RAV_CUDA(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        if (!c->ev_in[k]) RAV_CUDA(cudaEventCreateWithFlags(&c->ev_in[k], cudaEventDisableTiming));
+        if (!c->ev_done[k]) RAV_CUDA(cudaEventCreateWithFlags(&c->ev_done[k], cudaEventDisableTiming));
+    }
+    double* X[2] = {c->hx, c->hx2};
+    double* B[2] = {c->hb, c->hb2};
+    // copy stream: in(0), in(1), out(0), in(2), out(1), ... -- in(k + 2) reuses slot k after out(k);
+    // the sweeps of problem k wait for in(k), out(k) waits for them
+    auto put = [&](int64_t k) -> rav_status {
+        const int s = (int)(k & 1);
+        RAV_CUDA(cudaMemcpyAsync(X[s], x[k], bytes, cudaMemcpyHostToDevice, c->cstream));
+        RAV_CUDA(cudaMemcpyAsync(B[s], b[k], bytes, cudaMemcpyHostToDevice, c->cstream));
+        RAV_CUDA(cudaEventRecord(c->ev_in[s], c->cstream));
+        return RAV_OK;
+    };
+    int64_t launches = 0;
+    RAV_TRY(put(0));
+    if (nprob > 1) RAV_TRY(put(1));
+    for (int64_t k = 0; k < nprob; ++k) {
+        const int s = (int)(k & 1);
+        RAV_CUDA(cudaStreamWaitEvent(c->stream, c->ev_in[s], 0));
+        int gi = c->graph[0].match(X[s], B[s], nu, 0, 0, omega) ? 0
+                 : (c->graph[1].match(X[s], B[s], nu, 0, 0, omega) ? 1 : -1);
+        if (gi < 0) {
+            gi = c->graph_next;
+            c->graph_next ^= 1;
+        }
+        int64_t l = 0;
+        RAV_TRY(run_graph(c->graph[gi], c->stream, true, X[s], B[s], nu, 0, 0, omega, l,
+                          [&]() { return smooth_launches(c, X[s], B[s], nu, omega); }));
+        launches += l;
+        RAV_CUDA(cudaEventRecord(c->ev_done[s], c->stream));
+        RAV_CUDA(cudaStreamWaitEvent(c->cstream, c->ev_done[s], 0));
+        RAV_CUDA(cudaMemcpyAsync(x[k], X[s], bytes, cudaMemcpyDeviceToHost, c->cstream));
+        if (k + 2 < nprob) RAV_TRY(put(k + 2));
+    }
+    RAV_CUDA(cudaStreamSynchronize(c->cstream));
+    RAV_CUDA(cudaStreamSynchronize(c->stream));
+    c->last_launches = launches;
+    return RAV_OK;
+}
+
 rav_status rav_residual(rav_ctx* c, const double* x, const double* b, double* r) {
     NvtxRange nvtx_range("rav_residual");
     if (!c || !x || !b || !r) { set_error("rav_residual: NULL argument"); return RAV_ERR_ARG; }
@@ -315,6 +384,16 @@ void rav_destroy(rav_ctx* c) {
     if (c->r) cudaFree(c->r);
     if (c->hx) cudaFree(c->hx);
     if (c->hb) cudaFree(c->hb);
+    if (c->hx2) cudaFree(c->hx2);
+    if (c->hb2) cudaFree(c->hb2);
+    if (c->cstream) {
+        cudaStreamSynchronize(c->cstream);
+        cudaStreamDestroy(c->cstream);
+    }
+    for (int k = 0; k < 2; ++k) {
+        if (c->ev_in[k]) cudaEventDestroy(c->ev_in[k]);
+        if (c->ev_done[k]) cudaEventDestroy(c->ev_done[k]);
+    }
     if (c->plist) cudaFree(c->plist);
     delete c;
 }

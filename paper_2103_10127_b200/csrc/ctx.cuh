@@ -42,6 +42,12 @@ struct rav_ctx {
     double* r = nullptr;        // residual work vector
     double* hx = nullptr;       // staging for host x / b
     double* hb = nullptr;
+    // rav_smooth_batch: a second staging pair, a copy stream and per-slot events (the copies of
+    // one problem overlap the sweeps of the next)
+    double* hx2 = nullptr;
+    double* hb2 = nullptr;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
     // captured sweep chains for the two most recent (x, b, nu, omega) keys: a caller that alternates
     // between two buffer pairs (double-buffered host transfers) replays without re-capturing
     GraphCache graph[2];

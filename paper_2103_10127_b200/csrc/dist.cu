@@ -956,6 +956,7 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
                 if (st != RAV_OK) break;
                 cudaError_t e = cudaMalloc(&S.rmap, sizeof(int32_t) * rm.size());
                 if (e == cudaSuccess) e = cudaMemcpy(S.rmap, rm.data(), sizeof(int32_t) * rm.size(), cudaMemcpyHostToDevice);
+                if (e == cudaSuccess) e = cudaDeviceSynchronize();   // the DMA of a pageable copy, before m->stream reads it
                 if (e == cudaSuccess) e = cudaMalloc(&S.pflag, std::max<int64_t>(1, S.sm->P.n_patches));
                 if (e != cudaSuccess) { set_error("mgd_setup: %s", cudaGetErrorString(e)); st = RAV_ERR_OOM; break; }
                 const int64_t np = S.sm->P.n_patches;
@@ -965,7 +966,10 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
                 if (cudaGetLastError() != cudaSuccess) { set_error("mgd_setup: pflag kernel failed"); st = RAV_ERR_CUDA; break; }
                 // writers per launch: chunks of 32 patches (thread layout) or patches (per-patch layout)
                 std::vector<uint8_t> hf((size_t)std::max<int64_t>(1, np));
-                if (cudaMemcpy(hf.data(), S.pflag, (size_t)np, cudaMemcpyDeviceToHost) != cudaSuccess) { st = RAV_ERR_CUDA; break; }
+                // on the setup stream (may be non-blocking: a legacy-stream cudaMemcpy would not wait
+                // for pflag_kernel and read uninitialised flags -- wrong writer counts, hung releases)
+                if (cudaMemcpyAsync(hf.data(), S.pflag, (size_t)np, cudaMemcpyDeviceToHost, m->stream) != cudaSuccess ||
+                    cudaStreamSynchronize(m->stream) != cudaSuccess) { st = RAV_ERR_CUDA; break; }
                 unsigned int nw = 0;
                 if (S.sm->F.layout == 4) {
                     const int64_t nch = (np + 31) / 32;
@@ -1195,7 +1199,8 @@ rav_status mgd_setup(rav_comm* comm, int n_sub_total, const int32_t* sub_proc, i
     if (st == RAV_OK) {
         for (auto& L : m->lv)
             for (auto& S : L) S.sm->stream = m->stream;
-        cudaError_t e = cudaStreamSynchronize(m->stream);
+        // every setup upload (legacy-stream copies included) complete before m->stream uses them
+        cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { set_error("mgd_setup: %s", cudaGetErrorString(e)); st = RAV_ERR_CUDA; }
     }
     if (st != RAV_OK) {

@@ -943,6 +943,21 @@ static void nb_launch(const NodeBlocked& N, const double* x, const double* b, do
         const char* e = getenv("RAV_NB_MINB");
         return e ? atoi(e) : 6;
     }();
+    static const int minb3 = [] {   // register cap of the 3D multi-lane variant with the B-value table
+        const char* e = getenv("RAV_NB_MINB3");
+        return e ? atoi(e) : 1;
+    }();
+    if constexpr (D == 3 && G == 2) {
+        if (N.vtbl && minb3 >= 4) {
+            auto k3 = minb3 >= 5 ? nb_residual_kernel<D, G, UA, 5, true, PR, XA, true>
+                                 : nb_residual_kernel<D, G, UA, 4, true, PR, XA, true>;
+            launch_maybe_pdl(k3, dim3(blocks), dim3(bs), 0, s, N.nblock, N.nnodes, N.nslices, N.nvel,
+                             (const int32_t*)N.perm, (const int32_t*)N.wa, (const int32_t*)N.wb,
+                             (const int64_t*)N.cptr, (const int64_t*)N.vptr, cols, (const double*)N.val, x, b, r,
+                             part);
+            return;
+        }
+    }
     auto kern = N.vtbl ? ((minb >= 8 && G == 1) ? nb_residual_kernel<D, G, UA, 8, true, PR, XA, true>
                          : (minb >= 6 && G == 1) ? nb_residual_kernel<D, G, UA, 6, true, PR, XA, true>
                          : (minb == 5 && G == 1) ? nb_residual_kernel<D, G, UA, 5, true, PR, XA, true>

@@ -95,6 +95,7 @@ def _load():
         "rav_gen_prolongation": [P(RavGrid), P(RavGrid), vp, vp, vp, vp],
         "rav_setup": [P(RavCsr), P(RavPatches), P(RavOpts), P(vp), P(i64)],
         "rav_smooth": [vp, vp, vp, C.c_int, dbl],
+        "rav_smooth_batch": [vp, i64, P(vp), P(vp), C.c_int, dbl],
         "rav_residual": [vp, vp, vp, vp],
         "rav_apply": [vp, vp, vp, dbl],
         "rav_rows_size": [vp, P(i64)],
@@ -292,6 +293,17 @@ class Smoother:
         """x <- x + omega S_RAV (b - L x), nu times (x updated in place)."""
         _check(lib.rav_smooth(self.ctx, _ptr(x), _ptr(b), int(nu), float(omega)))
         return x
+
+    def smooth_batch(self, xs, bs, nu: int, omega: float):
+        """rav_smooth on independent problems in host buffers (numpy arrays or CPU tensors, pinned
+        for overlap): x_k <- nu sweeps from x_k with rhs b_k, in place; copies overlap the sweeps."""
+        k = len(xs)
+        if len(bs) != k:
+            raise ValueError("smooth_batch: one b per x")
+        xa = (C.c_void_p * max(1, k))(*[_ptr(x) for x in xs])
+        ba = (C.c_void_p * max(1, k))(*[_ptr(b) for b in bs])
+        _check(lib.rav_smooth_batch(self.ctx, k, xa, ba, int(nu), float(omega)))
+        return xs
 
     def residual(self, x, b, r=None):
         if r is None:

@@ -220,3 +220,28 @@ def test_mgd_fused_exchange_matches_local_exchange(rg, rdist):
             assert np.isfinite(mgd.residual_norm(xs, info["b"]))
             mgd.close()
         assert_entrywise(out[1], out[0], np.abs(out[0]).max(), tol=1e-13, what="fused vs local exchange")
+
+
+def test_mgd_fused_exchange_nonblocking_stream(rg, rdist):
+    """The fused exchange set up and run on a non-blocking stream (the bench's and the scaling
+    model's setting), 2 and 4 subdomains of a slab-stacked 2D grid large enough for the thread
+    kernel: the per-patch writer flags must be read after the kernel that computes them (a legacy-
+    stream copy raced it and miscounted the writers: hung releases / a setup error).  Fused
+    iterate = local exchange's to rounding; a bounded wait that expired would raise."""
+    prob = si.problem(2, (96, 192), si.KIND_MMS, eta="fourier")   # >= 4096 patches per subdomain
+    n = oracle.assemble(prob)["n"]
+    stream = torch.cuda.Stream()
+    for N in (2, 4):
+        out = []
+        for via in (0, 2):
+            mgd, info = rdist.build_lib_dist(prob, 1, N, list(range(N)), [0] * N, _comm(rg, via), smooth_only=True,
+                                             via_comm=via, stream=stream)
+            xs = _scatter(info, si.initial_guess(n, seed=11))
+            torch.cuda.synchronize()
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    mgd.smooth(xs, info["b"], 2, 0.66)
+            torch.cuda.synchronize()
+            out.append(_gather(info, xs, n))
+            mgd.close()
+        assert_entrywise(out[1], out[0], np.abs(out[0]).max(), tol=1e-13, what=f"fused vs local, {N} subdomains")
