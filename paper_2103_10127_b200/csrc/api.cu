@@ -68,9 +68,16 @@ rav_status smooth_launches(rav_ctx* c, double* x, const double* b, int nu, doubl
                            bool x_zero) {
     for (int k = 0; k < nu; ++k) {
         if (c->variant == RAV_VARIANT_MV) {   // colour by colour, fresh local residuals (Eq. 11, 15)
-            for (size_t q = 0; q + 1 < c->coffs.size(); ++q)
-                RAV_TRY(launch_mv_color(c->A, c->F, c->coffs[q + 1] - c->coffs[q], c->plist + c->coffs[q], b, x,
-                                        omega, c->stream));
+            for (size_t q = 0; q + 1 < c->coffs.size(); ++q) {
+                if (c->A.nb.nslices > 0) {   // the colour's residual by the node-blocked kernel, then the patches
+                    RAV_TRY(launch_residual(c->A, x, b, c->r, c->stream));
+                    RAV_TRY(launch_mv_color_r(c->F, c->coffs[q + 1] - c->coffs[q], c->plist + c->coffs[q], c->r, x,
+                                              omega, c->stream));
+                } else {
+                    RAV_TRY(launch_mv_color(c->A, c->F, c->coffs[q + 1] - c->coffs[q], c->plist + c->coffs[q], b,
+                                            x, omega, c->stream));
+                }
+            }
             continue;
         }
         if (k == 0 && x_zero && !r_ready) {   // r = b - L 0 = b
@@ -109,7 +116,11 @@ rav_status rav_setup(const rav_csr* A, const rav_patches* P, const rav_opts* opt
     c->variant = o.variant;
     c->nvel = o.n_vel;
     rav_status st = csr_upload(A, c->A, c->stream);
-    if (st == RAV_OK && o.variant != RAV_VARIANT_MV && o.block_dim > 0 && o.kernel != RAV_KERNEL_WARP)
+    static const int mv_nb = [] {   // MV: colour residuals by the node-blocked kernel (0: patch rows of L)
+        const char* e = getenv("RAV_MV_NB");
+        return e ? atoi(e) : 1;
+    }();
+    if (st == RAV_OK && (o.variant != RAV_VARIANT_MV || mv_nb) && o.block_dim > 0 && o.kernel != RAV_KERNEL_WARP)
         st = nb_build(c->A, o.n_vel, o.block_dim, c->stream);
     if (st == RAV_OK && o.variant != RAV_VARIANT_MV && c->A.nb.nslices == 0) st = sell_build(c->A, c->stream);
     if (st == RAV_OK) st = patches_upload(P, A->n_rows, c->P, c->stream);

@@ -181,6 +181,9 @@ rav_status launch_diag_sweep(const PatchSet& P, const Factors& F, const double* 
                              cudaStream_t s);
 rav_status launch_mv_color(const Csr& A, const Factors& F, int64_t ncol, const int32_t* plist, const double* b,
                            double* x, double omega, cudaStream_t s);
+// one MV colour from a residual r = b - L x computed just before (instead of the patch rows of L)
+rav_status launch_mv_color_r(const Factors& F, int64_t ncol, const int32_t* plist, const double* r, double* x,
+                             double omega, cudaStream_t s);
 rav_status launch_schur_sweep(const PatchSet& P, const Factors& F, const double* r, double* x, double omega,
                               cudaStream_t s);
 

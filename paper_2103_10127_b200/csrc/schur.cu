@@ -1686,7 +1686,10 @@ __global__ void __launch_bounds__(256) diag_sweep_group_kernel(int64_t np, const
 // relaxed concurrently; each computes a fresh local residual on its own rows
 // (Eq. 15) and applies the full L_i^{-1} (Schur form, all nodes) with
 // prolongation R_i^T.  Result = sequential MV in colour order.
-template <int D>
+// RR: the colour's fresh residual r = b - L x was computed by the residual kernel just before (the
+// patches of one colour share no DoF and are not coupled through L, so it is each patch's fresh
+// local residual of Eq. 15); the kernel gathers it instead of re-reading the patch rows of L
+template <int D, bool RR = false>
 __global__ void __launch_bounds__(256) mv_color_kernel(int64_t ncol, const int32_t* __restrict__ plist, int MT,
                                                        int nnmax, const int64_t* __restrict__ foffs,
                                                        const int64_t* __restrict__ nodeoffs,
@@ -1705,6 +1708,9 @@ __global__ void __launch_bounds__(256) mv_color_kernel(int64_t ncol, const int32
         const int64_t no = nodeoffs[i];
         const int nn = (int)(nodeoffs[i + 1] - no);
         const int pd = pdof[i];
+        if constexpr (RR) {
+            for (int t = lane; t <= nn * D; t += 32) rl[t] = __ldg(b + (t < nn * D ? nodes[no + t / D] + t % D : pd));
+        } else
         // fresh local residual on the patch rows (Eq. 15): 4 lanes per row, 8 rows per pass
         for (int t0 = 0; t0 <= nn * D; t0 += 8) {
             const int t = t0 + (lane >> 2), q = lane & 3;
@@ -1761,6 +1767,25 @@ rav_status launch_diag_sweep(const PatchSet& P, const Factors& F, const double* 
         diag_sweep_kernel<2><<<blocks, 256, 0, s>>>(P.n_patches, F.foffs, F.nodeoffs, F.nodes, F.PD, F.fac, r, x, omega);
     else
         diag_sweep_kernel<1><<<blocks, 256, 0, s>>>(P.n_patches, F.foffs, F.nodeoffs, F.nodes, F.PD, F.fac, r, x, omega);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    return RAV_OK;
+}
+
+rav_status launch_mv_color_r(const Factors& F, int64_t ncol, const int32_t* plist, const double* r, double* x,
+                             double omega, cudaStream_t s) {
+    if (ncol <= 0) return RAV_OK;
+    const size_t shmem = sizeof(double) * (size_t)(F.NN * F.D + 1) * 8;
+    const int blocks = (int)std::min<int64_t>(cdiv(ncol, 8), (int64_t)num_sms() * 16);
+    if (F.D == 3)
+        mv_color_kernel<3, true><<<blocks, 256, shmem, s>>>(ncol, plist, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD,
+                                                            F.fac, nullptr, nullptr, nullptr, r, x, omega);
+    else if (F.D == 2)
+        mv_color_kernel<2, true><<<blocks, 256, shmem, s>>>(ncol, plist, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD,
+                                                            F.fac, nullptr, nullptr, nullptr, r, x, omega);
+    else
+        mv_color_kernel<1, true><<<blocks, 256, shmem, s>>>(ncol, plist, F.MT, F.NN, F.foffs, F.nodeoffs, F.nodes, F.PD,
+                                                            F.fac, nullptr, nullptr, nullptr, r, x, omega);
     count_launch();
     RAV_CHECK_LAUNCH();
     return RAV_OK;

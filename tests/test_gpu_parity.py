@@ -317,3 +317,27 @@ def test_c3_family_cycle_counts_at_512_and_1024(rg, n, levels):
     assert kg == ko, (kg, ko)
     np.testing.assert_allclose(hg, ho, rtol=1e-6, atol=1e-12 * ho[0])
     assert_entrywise(xg, xo, np.abs(xo).max(), tol=iterate_tol(n), what=f"{n}^2 V-cycle iterate")
+
+
+def test_c3_full_size_cycle_counts_match_stored_oracle(rg):
+    """BASELINE config c3 at full size (2048^2, 37.7 M DoFs, 10 levels): the GPU's V(2,2)-RAV
+    cycle count equals the oracle's, its residual history agrees to 1e-6 per cycle and its
+    final iterate to the V-cycle iterate bar at 4096 seeded DoFs.  The oracle's solve (~40 GB,
+    minutes of host time) is stored in tests/golden/c3_oracle_vcycle.json, written by
+    scripts/oracle_c3_golden.py, which calls only oracle/ (P:132 stopping rule)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c3_oracle_vcycle.json")
+    G = json.load(open(path))
+    c = si.CONFIGS["c3"]
+    mg, fine = rg.build_hierarchy(si.config_problem("c3"), c["levels"], "pou")
+    assert fine["n"] == G["n"]
+    x = torch.zeros(fine["n"], dtype=torch.float64, device="cuda")
+    x, kg, hg = mg.solve(x, fine["b"], pre=c["pre"], post=c["post"], omega=c["omega"], rtol=c["rtol"], maxit=100)
+    idx = torch.tensor(G["sample_dofs"], device="cuda")
+    xs = x[idx].cpu().numpy()
+    mg.close()
+    ho = np.array(G["history"])
+    assert kg == G["cycles"], (kg, G["cycles"])
+    np.testing.assert_allclose(hg, ho, rtol=1e-6, atol=1e-12 * ho[0])
+    assert_entrywise(xs, np.array(G["sample_x"]), G["x_absmax"], tol=iterate_tol(2048), what="c3 iterate (sampled)")
