@@ -934,8 +934,9 @@ def run_gpu(args):
     x0h = x0.cpu()
     bh = b.cpu().pin_memory()
     xh = [x0h.clone().pin_memory() for _ in range(args.steps)]
-    sm.smooth_batch(xh[:2], [bh, bh], SWEEPS_PER_STEP, OMEGA)   # warm (staging buffers, both graphs)
-    for t_ in xh[:2]:
+    nw = min(2, args.steps)
+    sm.smooth_batch(xh[:nw], [bh] * nw, SWEEPS_PER_STEP, OMEGA)   # warm (staging buffers, both graphs)
+    for t_ in xh[:nw]:
         t_.copy_(x0h)
     barrier()
     t0 = time.perf_counter()
