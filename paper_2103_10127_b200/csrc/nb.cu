@@ -314,6 +314,23 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
                 if constexpr (PR) {
                     const int A2 = A >> 1;
                     // two entries per iteration; a second iteration in flight only with the 48-register cap
+                    if constexpr (PAT) {   // offsets of pair p + 1 loaded while pair p is gathered
+                        const int2* tp2 = reinterpret_cast<const int2*>(tp);
+                        int2 on = A2 > 0 ? __ldg(tp2) : make_int2(0, 0);
+#pragma unroll (MINB <= 5 ? 2 : 1)
+                        for (int p = 0; p < A2; ++p) {
+                            const int2 o = on;
+                            if (p + 1 < A2) on = __ldg(tp2 + p + 1);
+                            const double2 a = __ldcs(pA + (int64_t)p * NB_C);
+                            double x0[2], x1[2];
+                            ldx2(x + bA + o.x, x0);
+                            ldx2(x + bA + o.y, x1);
+                            acc[0] = fma(a.x, x0[0], acc[0]);
+                            acc[1] = fma(a.x, x0[1], acc[1]);
+                            acc[0] = fma(a.y, x1[0], acc[0]);
+                            acc[1] = fma(a.y, x1[1], acc[1]);
+                        }
+                    } else
 #pragma unroll (MINB <= 5 ? 2 : 1)
                     for (int p = 0; p < A2; ++p) {
                         const double2 a = __ldcs(pA + (int64_t)p * NB_C);
@@ -553,6 +570,7 @@ static rav_status nb_compress(NodeBlocked& N, cudaStream_t s) {
     RAV_CUDA(cudaMemcpy(hwb.data(), N.wb, sizeof(int32_t) * N.nslices, cudaMemcpyDeviceToHost));
     int W = 1;
     for (int64_t k = 0; k < N.nslices; ++k) W = std::max(W, hwa[k] + hwb[k]);
+    W += W & 1;   // even row stride: entry pairs (2p, 2p + 1) of a row are one aligned 8-byte load
     uint64_t *key = nullptr, *skey = nullptr;
     int32_t *idx = nullptr, *sidx = nullptr, *flag = nullptr, *seg = nullptr, *rep = nullptr, *tw = nullptr;
     int32_t *pid = nullptr, *bA = nullptr, *bB = nullptr, *tbl = nullptr;
