@@ -150,6 +150,12 @@ struct Factors {
     // layout 4 node-index compression: node j of slot i = nbase[i] + ntbl[npid[i] * NN + j] (DT freed)
     int32_t *npid = nullptr, *nbase = nullptr, *ntbl = nullptr;
     int nnpat = 0;
+    // layout 4 weight table (with the node patterns): the restricted weights, w_p and the restricted
+    // count of a slot are those of its node pattern (PoU weights are geometric), verified bitwise;
+    // the sweep then streams only 1/S per patch (SINV) instead of the MT + 2 aux values and NR
+    double* wtab = nullptr;     // nnpat * (MT + 1): weights k < MT, then w_p
+    int32_t* ntab = nullptr;    // nnpat: restricted node count
+    double* SINV = nullptr;     // nchunks * 32: 1/S per slot
     // deterministic scatter (rav_opts.deterministic, Schur formats): per-patch correction slots and,
     // per written DoF, its slots in ascending patch order
     double* cbuf = nullptr;

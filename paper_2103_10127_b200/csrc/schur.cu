@@ -784,7 +784,7 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
 // RA: r is 16-byte aligned (checked at launch): node gathers without the per-load alignment test
 // OB: the interface exchange fused into the sweep (Outbox, internal.cuh): ghost-written DoFs of
 // flagged patches go to the consumers' receive buffers
-template <int MT, int D, int NRB, bool DET, bool NDP, bool RA, bool OB>
+template <int MT, int D, int NRB, bool DET, bool NDP, bool RA, bool OB, bool WTB = false>
 __device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, int NN, int64_t pairs,
                                                                  const double2* __restrict__ W,
                                                                  const int32_t* __restrict__ ND,
@@ -796,7 +796,11 @@ __device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, i
                                                                  const double* __restrict__ AUX,
                                                                  const double* __restrict__ r,
                                                                  double* __restrict__ x, double omega,
-                                                                 double* __restrict__ cbuf, int pf, ObView ob) {
+                                                                 double* __restrict__ cbuf, int pf, ObView ob,
+                                                                 const double* __restrict__ wtab = nullptr,
+                                                                 const int32_t* __restrict__ ntab = nullptr,
+                                                                 const double* __restrict__ SINV = nullptr) {
+    static_assert(!WTB || NDP, "the weight table is indexed by the node pattern");
     constexpr int TRI = MT * (MT + 1) / 2 + MT * D;
     constexpr int TRI_PAD = TRI + (TRI & 1);
     constexpr int RC = MT + D;   // entries per rectangular column
@@ -808,7 +812,8 @@ __device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, i
     if (gw >= nchunks) return;
     const double2* wp = W + chunk * pairs * 32 + lane;
     const int32_t* np_ = NDP ? nullptr : ND + chunk * (int64_t)NN * 32 + lane;
-    const int32_t* ntp = NDP ? ntbl + (int64_t)npid[i] * NN : nullptr;   // L1-resident pattern row
+    const int32_t pid_i = NDP ? npid[i] : 0;
+    const int32_t* ntp = NDP ? ntbl + (int64_t)pid_i * NN : nullptr;   // L1-resident pattern row
     const int32_t nb0 = NDP ? nbase[i] : 0;
     const bool flagged = OB && i < np && ob.pflag[i];   // loaded early: needed only at the scatter
     // warp-uniform: the chunks without a ghost-writing patch (nearly all) keep the plain scatter
@@ -901,11 +906,13 @@ __device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, i
             }
         }
     }
-    const double* aux = AUX + chunk * (MT + 2) * 32 + lane;
+    // WTB: weights, w_p and the restricted count from the node pattern's row (L1), 1/S from SINV
+    const double* aux = WTB ? nullptr : AUX + chunk * (MT + 2) * 32 + lane;
+    const double* wt = WTB ? wtab + (int64_t)pid_i * (MT + 1) : nullptr;
     const int pd = PD[i];
-    const double t = aux[(MT + 1) * 32] * (gacc - __ldg(r + pd));
+    const double t = (WTB ? __ldcs(SINV + i) : aux[(MT + 1) * 32]) * (gacc - __ldg(r + pd));
     if (i >= np) return;   // padding slots of the last chunk
-    const int m = NR[i];
+    const int m = WTB ? __ldg(ntab + pid_i) : NR[i];
     double* cb = DET ? cbuf + i * (MT * D + 1) : nullptr;
     // the scatter (restricted prolongation, Eq. 13): one straight-line loop per target kind,
     // the warp-uniform branch outside it (a branch per store turned the reductions into returning
@@ -914,7 +921,7 @@ __device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, i
 #pragma unroll
         for (int k = 0; k < MT; ++k) {
             if (k < m) {
-                const double wk = omega * aux[k * 32];
+                const double wk = omega * (WTB ? __ldg(wt + k) : aux[k * 32]);
                 const int nd = ND_AT(k);
 #pragma unroll
                 for (int c = 0; c < D; ++c) add(nd + c, wk * fma(gR[k][c], t, acc[k][c]), k * D + c);
@@ -933,7 +940,7 @@ __device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, i
     } else {
         scatter([&](int dof, double v, int) { atomicAdd(x + dof, v); });
     }
-    const double wpr = aux[MT * 32];
+    const double wpr = WTB ? __ldg(wt + MT) : aux[MT * 32];
     if (wpr != 0.0) {
         if (DET) cb[MT * D] = omega * wpr * (-t);
         else if (OB) red_add(x + pd, omega * wpr * (-t));
@@ -943,7 +950,8 @@ __device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, i
 
 #undef ND_AT
 
-template <int MT, int D, int NRB = 0, bool DET = false, bool NDP = false, bool RA = false, bool OB = false>
+template <int MT, int D, int NRB = 0, bool DET = false, bool NDP = false, bool RA = false, bool OB = false,
+          bool WTB = false>
 __global__ void __launch_bounds__(128, 4) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
                                                                  const double2* __restrict__ W,
                                                                  const int32_t* __restrict__ ND,
@@ -955,9 +963,12 @@ __global__ void __launch_bounds__(128, 4) schur_sweep_thread_kernel(int64_t np, 
                                                                  const double* __restrict__ AUX,
                                                                  const double* __restrict__ r,
                                                                  double* __restrict__ x, double omega,
-                                                                 double* __restrict__ cbuf, int pf, Outbox ob) {
-    schur_thread_body<MT, D, NRB, DET, NDP, RA, OB>(np, nchunks, NN, pairs, W, ND, npid, nbase, ntbl, PD, NR, AUX, r,
-                                                    x, omega, cbuf, pf, ob_view(ob));
+                                                                 double* __restrict__ cbuf, int pf, Outbox ob,
+                                                                 const double* __restrict__ wtab,
+                                                                 const int32_t* __restrict__ ntab,
+                                                                 const double* __restrict__ SINV) {
+    schur_thread_body<MT, D, NRB, DET, NDP, RA, OB, WTB>(np, nchunks, NN, pairs, W, ND, npid, nbase, ntbl, PD, NR, AUX,
+                                                         r, x, omega, cbuf, pf, ob_view(ob), wtab, ntab, SINV);
     if constexpr (OB) {   // a writer: this warp's chunk holds a ghost-writing patch
         const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
         const int64_t chunk = ob.rot ? (gw < ob.rot ? gw + nchunks - ob.rot : gw - ob.rot) : gw;
@@ -1213,6 +1224,89 @@ __global__ void nd_verify_kernel(int64_t nslots, int NN, const int32_t* ND, cons
         for (int j = 0; j < NN; ++j)
             if (q[j * 32] != base[t] + tbl[(int64_t)pid[t] * NN + j]) atomicOr(err, 1u);
     }
+}
+
+// ---- per-pattern weight table of the thread layout (see Factors::wtab) -------------------------
+__global__ void wt_rep_kernel(int64_t np, const int32_t* npid, int32_t* rep) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x)
+        atomicMin(rep + npid[i], (int32_t)i);
+}
+__global__ void wt_fill_kernel(int npat, int64_t np, int MT, const int32_t* rep, const double* AUX,
+                               const int32_t* NR, double* wtab, int32_t* ntab) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < npat; p += gridDim.x * blockDim.x) {
+        const int i = rep[p];
+        if (i >= np) {   // a pattern of padding slots only (rep kept its 0x7f7f7f7f fill)
+            for (int k = 0; k <= MT; ++k) wtab[(int64_t)p * (MT + 1) + k] = 0.0;
+            ntab[p] = 0;
+            continue;
+        }
+        const int64_t chunk = i >> 5;
+        const int lane = i & 31;
+        for (int k = 0; k <= MT; ++k) wtab[(int64_t)p * (MT + 1) + k] = AUX[(chunk * (MT + 2) + k) * 32 + lane];
+        ntab[p] = NR[i];
+    }
+}
+// every slot against its pattern's row (padding slots i >= np: weights 0, count 0 -- the sweep
+// returns before using them); SINV for all slots; Sum (NR + 1) of the real patches for the byte model
+__global__ void wt_verify_kernel(int64_t ns, int64_t np, int MT, const int32_t* npid, const double* AUX,
+                                 const int32_t* NR, const double* wtab, const int32_t* ntab, double* SINV,
+                                 unsigned int* err, unsigned long long* cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t chunk = i >> 5;
+        const int lane = (int)(i & 31);
+        SINV[i] = AUX[(chunk * (MT + 2) + MT + 1) * 32 + lane];
+        if (i >= np) continue;
+        const int p = npid[i];
+        if (ntab[p] != NR[i]) atomicOr(err, 1u);
+        for (int k = 0; k <= MT; ++k)
+            if (__double_as_longlong(wtab[(int64_t)p * (MT + 1) + k]) !=
+                __double_as_longlong(AUX[(chunk * (MT + 2) + k) * 32 + lane]))
+                atomicOr(err, 1u);
+        atomicAdd(cnt, (unsigned long long)(NR[i] + 1));
+    }
+}
+
+static rav_status schur_wt_compress(Factors& F, int64_t np, cudaStream_t s) {
+    const int64_t ns = F.nchunks * 32;
+    const int npat = F.nnpat, MT = F.MT;
+    if (npat <= 0 || (int64_t)npat * (MT + 1) * 8 > (4 << 20)) return RAV_OK;
+    int32_t* rep = nullptr;
+    unsigned int* err = nullptr;
+    unsigned long long* cnt = nullptr;
+    double *wtab = nullptr, *sinv = nullptr;
+    int32_t* ntab = nullptr;
+    RAV_CUDA(cudaMallocAsync(&rep, sizeof(int32_t) * npat, s));
+    RAV_CUDA(cudaMemsetAsync(rep, 0x7f, sizeof(int32_t) * npat, s));   // 0x7f7f7f7f: above any slot
+    RAV_CUDA(cudaMallocAsync(&err, sizeof(unsigned int), s));
+    RAV_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned int), s));
+    RAV_CUDA(cudaMallocAsync(&cnt, sizeof(unsigned long long), s));
+    RAV_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+    RAV_CUDA(cudaMalloc(&wtab, sizeof(double) * (size_t)npat * (MT + 1)));
+    RAV_CUDA(cudaMalloc(&ntab, sizeof(int32_t) * npat));
+    RAV_CUDA(cudaMalloc(&sinv, sizeof(double) * ns));
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(ns, 256), (int64_t)num_sms() * 16));
+    wt_rep_kernel<<<nb, 256, 0, s>>>(np, F.npid, rep);
+    count_launch();
+    wt_fill_kernel<<<(int)cdiv(npat, 128), 128, 0, s>>>(npat, np, MT, rep, F.WT, F.NR, wtab, ntab);
+    count_launch();
+    wt_verify_kernel<<<nb, 256, 0, s>>>(ns, np, MT, F.npid, F.WT, F.NR, wtab, ntab, sinv, err, cnt);
+    count_launch();
+    RAV_CHECK_LAUNCH();
+    unsigned int h_err = 0;
+    unsigned long long h_cnt = 0;
+    RAV_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(h_err), cudaMemcpyDeviceToHost, s));
+    RAV_CUDA(cudaMemcpyAsync(&h_cnt, cnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, s));
+    for (void* p : {(void*)rep, (void*)err, (void*)cnt}) cudaFreeAsync(p, s);
+    RAV_CUDA(cudaStreamSynchronize(s));
+    if (h_err) {
+        for (void* p : {(void*)wtab, (void*)ntab, (void*)sinv}) cudaFree(p);
+        return RAV_OK;
+    }
+    F.wtab = wtab;
+    F.ntab = ntab;
+    F.SINV = sinv;
+    F.alg_bytes -= 8 * (int64_t)h_cnt;   // the streamed weights and w_p (1/S stays, now in SINV)
+    return RAV_OK;
 }
 
 static rav_status schur_nd_compress(Factors& F, int64_t np, cudaStream_t s) {
@@ -1488,6 +1582,11 @@ rav_status schur_factorize(const Csr& A, const PatchSet& P, int64_t nvel, int D,
         if (F.npid) {   // streamed index bytes: pattern id + base + pressure DoF instead of nn + 1 indices
             const int64_t sum_nn = (P.entries - P.n_patches) / D;
             F.alg_bytes += -4 * (sum_nn + P.n_patches) + 12 * P.n_patches;
+            static const bool wt = [] {
+                const char* e = getenv("RAV_SCHUR_WTAB");
+                return !(e && atoi(e) == 0);
+            }();
+            if (wt) RAV_TRY(schur_wt_compress(F, P.n_patches, s));
         }
     }
     return RAV_OK;
@@ -1817,7 +1916,8 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
     // 2D PoU interior shape (25 nodes, 9 restricted): compile-time rectangular loop (122 -> 113 us at c2)
     const bool shape = MT == 9 && F.NN == 25;
     const bool ra = (reinterpret_cast<uintptr_t>(r) & 15) == 0;
-    auto kern = F.npid ? (shape ? (ra ? schur_sweep_thread_kernel<MT, 2, 8, DET, true, true, OB>
+    auto kern = F.npid ? (shape ? (ra ? (F.wtab ? schur_sweep_thread_kernel<MT, 2, 8, DET, true, true, OB, true>
+                                               : schur_sweep_thread_kernel<MT, 2, 8, DET, true, true, OB>)
                                       : schur_sweep_thread_kernel<MT, 2, 8, DET, true, false, OB>)
                                 : schur_sweep_thread_kernel<MT, 2, 0, DET, true, false, OB>)
                        : shape ? schur_sweep_thread_kernel<MT, 2, 8, DET, false, false, OB>
@@ -1830,7 +1930,8 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
     }();
     launch_maybe_pdl(kern, dim3((unsigned)cdiv(F.nchunks * 32, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
                      (const int32_t*)F.DT, (const int32_t*)F.npid, (const int32_t*)F.nbase, (const int32_t*)F.ntbl,
-                     (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, pf, ob);
+                     (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, pf, ob,
+                     (const double*)F.wtab, (const int32_t*)F.ntab, (const double*)F.SINV);
 }
 
 static int64_t schur_cta_max() {   // patch count below which a CTA (8 warps) takes one patch

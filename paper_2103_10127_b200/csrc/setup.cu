@@ -507,7 +507,7 @@ void factors_free(Factors& F) {
     if (F.nodes) cudaFree(F.nodes);
     if (F.nodeoffs) cudaFree(F.nodeoffs);
     for (void* p : {(void*)F.cbuf, (void*)F.det_dof, (void*)F.det_off, (void*)F.det_slot, (void*)F.npid,
-                    (void*)F.nbase, (void*)F.ntbl})
+                    (void*)F.nbase, (void*)F.ntbl, (void*)F.wtab, (void*)F.ntab, (void*)F.SINV})
         if (p) cudaFree(p);
     F = Factors{};
 }
