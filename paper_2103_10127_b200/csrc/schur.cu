@@ -843,6 +843,8 @@ __device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, i
     };
     double acc[MT][D], rr[MT][D], gR[MT][D];
     double gacc = 0.0;
+    const int pd = PD[i];
+    const double rpd = __ldg(r + pd);   // the pressure residual with the patch's other gathers, not at the end
 #pragma unroll
     for (int k = 0; k < MT; ++k) {
         const int nd = ND_AT(k);
@@ -909,8 +911,7 @@ __device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, i
     // WTB: weights, w_p and the restricted count from the node pattern's row (L1), 1/S from SINV
     const double* aux = WTB ? nullptr : AUX + chunk * (MT + 2) * 32 + lane;
     const double* wt = WTB ? wtab + (int64_t)pid_i * (MT + 1) : nullptr;
-    const int pd = PD[i];
-    const double t = (WTB ? __ldcs(SINV + i) : aux[(MT + 1) * 32]) * (gacc - __ldg(r + pd));
+    const double t = (WTB ? __ldcs(SINV + i) : aux[(MT + 1) * 32]) * (gacc - rpd);
     if (i >= np) return;   // padding slots of the last chunk
     const int m = WTB ? __ldg(ntab + pid_i) : NR[i];
     double* cb = DET ? cbuf + i * (MT * D + 1) : nullptr;
