@@ -1118,11 +1118,28 @@ __global__ void __launch_bounds__(256) schur_sweep_cta_kernel(int64_t np, int MT
     for (int64_t i = blockIdx.x; i < np; i += gridDim.x) {
         const int64_t no = nodeoffs[i];
         const int nn = (int)(nodeoffs[i + 1] - no);
-        for (int t = threadIdx.x; t < nn * D; t += blockDim.x) rl[t] = __ldg(r + nodes[no + t / D] + (t % D));
-        __syncthreads();
         const double* Y = fac + foffs[i];
         const double* g = Y + (size_t)MT * nn;
         const double* aux = g + (size_t)nn * D;
+        // warp 0's end-of-patch operands (1/S, the pressure residual, its weight, the restricted count,
+        // node and g entries) issued with the gather instead of after the column loop and the barrier
+        double e_sinv = 0.0, e_rp = 0.0, e_wl = 0.0, e_wp = 0.0, e_g[D];
+        int e_nres = 0, e_nd = 0, e_pd = 0;
+        if (warp == 0) {
+            e_pd = pdof[i];
+            e_nres = nresn[i];
+            e_sinv = aux[MT + 1];
+            e_wp = aux[MT];
+            e_rp = __ldg(r + e_pd);
+            if (lane < MT && lane < nn) {
+                e_wl = aux[lane];
+                e_nd = nodes[no + lane];
+#pragma unroll
+                for (int c = 0; c < D; ++c) e_g[c] = g[lane * D + c];
+            }
+        }
+        for (int t = threadIdx.x; t < nn * D; t += blockDim.x) rl[t] = __ldg(r + nodes[no + t / D] + (t % D));
+        __syncthreads();
         double acc[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) acc[c] = 0.0;
@@ -1142,23 +1159,22 @@ __global__ void __launch_bounds__(256) schur_sweep_cta_kernel(int64_t np, int MT
         if (warp == 0) {
             double gt = 0.0;
             for (int w = 0; w < 8; ++w) gt += gpart[w];
-            const double t = aux[MT + 1] * (gt - __ldg(r + pdof[i]));
+            const double t = e_sinv * (gt - e_rp);
             double* cb = DET ? cbuf + i * ((int64_t)MT * D + 1) : nullptr;
-            if (lane < nresn[i]) {
-                const double wk = omega * aux[lane];
-                const int nd = nodes[no + lane];
+            if (lane < e_nres) {
+                const double wk = omega * e_wl;
 #pragma unroll
                 for (int c = 0; c < D; ++c) {
                     double a = 0.0;
                     for (int w = 0; w < 8; ++w) a += part[(w * 32 + lane) * D + c];
-                    const double v = wk * fma(g[lane * D + c], t, a);
+                    const double v = wk * fma(e_g[c], t, a);
                     if (DET) cb[lane * D + c] = v;
-                    else atomicAdd(x + nd + c, v);
+                    else atomicAdd(x + e_nd + c, v);
                 }
             }
             if (lane == 0) {
-                if (DET) cb[MT * D] = omega * aux[MT] * (-t);
-                else atomicAdd(x + pdof[i], omega * aux[MT] * (-t));
+                if (DET) cb[MT * D] = omega * e_wp * (-t);
+                else atomicAdd(x + e_pd, omega * e_wp * (-t));
             }
         }
         __syncthreads();
