@@ -296,9 +296,11 @@ rav_status rav_apply(rav_ctx* ctx, const double* r, double* x, double omega);
 /* r = b - L x (device pointers).  The residual SpMV of P:104 Eq. 10.  With
  * block_dim > 0 and a Taylor-Hood structure, rav_setup keeps a node-blocked
  * copy of L (A once per node, stencil-compressed columns, the B / B^T values
- * -- which carry no viscosity -- from a verified table when they repeat); each
- * row is summed in the CSR row's order, so r equals the CSR residual up to FMA
- * contraction.  Falls back to a SELL copy of the CSR otherwise. */
+ * -- which carry no viscosity -- from a verified table when they repeat).  With
+ * one lane per row (2D fine levels) each row is summed in the CSR row's order,
+ * so r equals the CSR residual up to FMA contraction; several lanes per row (3D,
+ * coarse levels) sum interleaved partial sums (rounding-level differences).
+ * Falls back to a SELL copy of the CSR otherwise. */
 rav_status rav_residual(rav_ctx* ctx, const double* x, const double* b, double* r);
 
 /* Export the stored factor rows in the canonical layout (for parity tests):
