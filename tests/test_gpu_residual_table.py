@@ -1,9 +1,12 @@
-"""The residual's B-value table (nb.cu nb_compress_bvals; DESIGN 5.1) and the sweep-stream
-prefetch hint (Factors.lead, RAV_XPF_MB) change which bytes the kernels stream, not what they
-compute: the residual with the B / B^T values read from the table must equal, bit for bit, the
-residual with the values streamed (RAV_NB_BVALS=0), and the streamed bytes must drop by the
-B values; sweeps after residuals that prefetch the sweep's factors must equal sweeps without
-the hint bit for bit (deterministic mode, so the scatter order is fixed).
+"""The residual's B-value table (nb.cu nb_compress_bvals; DESIGN 5.1), the sweep-stream
+prefetch hint (Factors.lead, RAV_XPF_MB), the thread sweep's per-pattern weight table
+(Factors.wtab, RAV_SCHUR_WTAB) and MV's colour residuals by the node-blocked kernel (RAV_MV_NB)
+change which bytes the kernels stream, not what they compute: the residual with the B / B^T
+values read from the table must equal, bit for bit, the residual with the values streamed
+(RAV_NB_BVALS=0), and the streamed bytes must drop by the B values; sweeps after residuals that
+prefetch the sweep's factors, and sweeps with the weight table, must equal the plain sweeps bit
+for bit (deterministic mode, so the scatter order is fixed); MV's two colour-residual paths
+agree to rounding.
 
 The switches are read once per process, so each setting runs in its own Python process; the
 seeded inputs and the comparison stay here.  2D (pair layout, one lane per row) and 3D (two
@@ -66,3 +69,44 @@ def test_sweep_prefetch_hint_bitwise_equal(tmp_path):
     off = _run(tmp_path, "nopf", {"RAV_XPF_MB": "0"})
     for name in ("2d", "2d_small", "3d"):
         assert np.array_equal(on[name + "_x"].view(np.int64), off[name + "_x"].view(np.int64)), name
+
+
+def test_sweep_weight_table_bitwise_equal(tmp_path):
+    """Per-pattern PoU weights (verified bitwise at setup) give the sweeps of the streamed AUX
+    weights bit for bit, and stream fewer bytes."""
+    on = _run(tmp_path, "wt", {"RAV_SCHUR_WTAB": "1"})
+    off = _run(tmp_path, "nowt", {"RAV_SCHUR_WTAB": "0"})
+    for name in ("2d", "2d_small", "3d"):
+        assert np.array_equal(on[name + "_x"].view(np.int64), off[name + "_x"].view(np.int64)), name
+
+
+MV_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import seeded_inputs as si
+from paper_2103_10127_b200 import ravgmg as rg
+prob = si.problem(2, (64, 72), si.KIND_MMS, eta="fourier")
+G = rg.gen_level(prob, "full")
+sm = rg.Smoother(G, G, variant=rg.VARIANT_MV)
+offs, ids = rg.multicolor(prob)
+sm.set_colors(offs, ids)
+x = torch.tensor(si.initial_guess(G["n"], seed=5), device="cuda")
+sm.smooth(x, G["b"], 3, 0.66)
+torch.cuda.synchronize()
+np.save({path!r}, x.cpu().numpy())
+"""
+
+
+def test_mv_colour_residual_paths_agree(tmp_path):
+    """MV's colour residual from the node-blocked kernel (default) and from the patch rows of L
+    (RAV_MV_NB=0) are the same fresh local residuals (same-colour patches are uncoupled through
+    L), so 3 MV sweeps agree to rounding."""
+    out = []
+    for v in ("1", "0"):
+        path = str(tmp_path / f"mv{v}.npy")
+        e = dict(os.environ)
+        e["RAV_MV_NB"] = v
+        subprocess.run([sys.executable, "-c", MV_CHILD.format(root=ROOT, path=path)], env=e, check=True, timeout=600)
+        out.append(np.load(path))
+    scale = np.abs(out[1]).max()
+    assert np.abs(out[0] - out[1]).max() <= 1e-12 * scale
