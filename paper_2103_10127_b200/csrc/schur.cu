@@ -1007,6 +1007,11 @@ __global__ void __launch_bounds__(256) schur_sweep_warp_kernel(int64_t np, int M
         }
         const int64_t no = nodeoffs[i];
         const int nn = (int)(nodeoffs[i + 1] - no);
+        if (lane == 0) {   // the operands of the chain's end (weights, 1/S, counts, pressure DoF) into L2 now
+            prefetch_l2(fac + foffs[i] + (size_t)(MTC > 0 ? MTC : MT) * nn + (size_t)nn * D);
+            prefetch_l2(pdof + i);
+            prefetch_l2(nresn + i);
+        }
         {   // gather r of the patch's nodes: lane takes nodes lane + 32u (independent index loads first)
             int nd[4];
 #pragma unroll
