@@ -421,6 +421,20 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
         double acc[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) acc[c] = 0.0;
+        // the row's right-hand side, loaded now (not after the accumulation and the group sum): lane q
+        // finalises the components c = q, q + G, ... of a node row (lane 0 a pressure row); the
+        // butterfly group sum leaves the same total in every lane of the group
+        // (3D only: in 2D the extra registers cost more occupancy than the early loads save)
+        constexpr bool EB = D == 3;
+        constexpr int CPL = (D + G - 1) / G;   // components per lane
+        double be[CPL];
+#pragma unroll
+        for (int u = 0; u < CPL; ++u) {
+            const int c = q + u * G;
+            be[u] = 0.0;
+            if (EB && br >= 0 && br < nnodes && c < D) be[u] = __ldg(b + br * D + c);
+            else if (EB && br >= nnodes && c == 0) be[u] = __ldg(b + nvel + (br - nnodes));
+        }
         if (br >= 0 && br < nnodes) {
 #pragma unroll UA
             for (int k = q; k < A; k += G) {
@@ -452,7 +466,7 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
 #pragma unroll
             for (int c = 0; c < D; ++c) acc[c] = group_sum<G>(acc[c]);
         }
-        if (q == 0 && br >= 0) {
+        if (!EB && q == 0 && br >= 0) {
             if (br < nnodes) {
                 const int64_t r0 = br * D;
 #pragma unroll
@@ -464,6 +478,28 @@ __global__ void __launch_bounds__(256, MINB) nb_residual_kernel(int64_t n, int64
             } else {
                 const int64_t row = nvel + (br - nnodes);
                 const double rr = b[row] - acc[0];
+                if (r) r[row] = rr;
+                mine += rr * rr;
+            }
+        }
+        if (EB && br >= 0) {
+            if (br < nnodes) {
+                const int64_t r0 = br * D;
+#pragma unroll
+                for (int u = 0; u < CPL; ++u) {
+                    const int c = q + u * G;
+                    if (c < D) {
+                        double a = acc[0];
+#pragma unroll
+                        for (int cc = 1; cc < D; ++cc) a = c == cc ? acc[cc] : a;
+                        const double rr = be[u] - a;
+                        if (r) r[r0 + c] = rr;
+                        mine += rr * rr;
+                    }
+                }
+            } else if (q == 0) {
+                const int64_t row = nvel + (br - nnodes);
+                const double rr = be[0] - acc[0];
                 if (r) r[row] = rr;
                 mine += rr * rr;
             }
