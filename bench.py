@@ -572,6 +572,41 @@ def run_adaptive_study(rg, si, stream, max_levels=7):
     return out
 
 
+class LineGuard:
+    """Keeps the N > 1 bench line if a measurement added after it stalls: when `limit_s` passes
+    before finish(), rank 0 prints the line as it stands (plus "extras_timeout_s") and every rank
+    exits 0 without the communicator teardown (which would wait on the stalled collective)."""
+
+    def __init__(self, line, rank, limit_s, exit_fn=os._exit, out=None):
+        self.line, self.rank, self.limit_s = line, rank, limit_s
+        self.exit_fn, self.out = exit_fn, out
+        self.lock = threading.Lock()
+        self.done = False
+        self.timer = threading.Timer(limit_s, self._expire)
+        self.timer.daemon = True
+        self.timer.start()
+
+    def _expire(self):
+        with self.lock:
+            if self.done:
+                return
+            self.done = True
+            if self.rank == 0:
+                snap = {k: v for k, v in list(self.line.items())}
+                snap["extras_timeout_s"] = self.limit_s
+                print(json.dumps(snap, default=str), file=self.out or sys.stdout, flush=True)
+        self.exit_fn(0)
+
+    def finish(self) -> bool:
+        """True: the caller prints the line; False: the limit already fired and printed it."""
+        with self.lock:
+            if self.done:
+                return False
+            self.done = True
+        self.timer.cancel()
+        return True
+
+
 def _transport():
     """RAV_MGD_TRANSPORT=peer: the peer-memory transport (mgd_setup via_comm = 2: pack kernels store
     into the neighbour's receive buffer over NVLink and release its flag); default nccl."""
@@ -793,8 +828,15 @@ def run_gpu_dist(args):
     mgd.close()
     del mgd, info, x, x0, b
     torch.cuda.empty_cache()
+    # The sweep line above is the contract's line; what follows only adds keys to it.  If an added
+    # measurement stalls on some rank (a collective waiting on a rank that raised), every rank
+    # leaves after the limit and rank 0 still prints the line, with the stall named in it.
+    guard = LineGuard(line, rank, float(os.environ.get("RAV_BENCH_EXTRAS_LIMIT_S", "900")))
     if not args.no_smoothers:
-        line["c5_smoothers"] = run_dist_c5(rdist, rg, si, stream, dist, ws, rank, comm, gather)
+        try:
+            line["c5_smoothers"] = run_dist_c5(rdist, rg, si, stream, dist, ws, rank, comm, gather)
+        except Exception as e:  # report, keep the sweep line
+            line["c5_smoothers"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if not args.no_vcycle:
         vc = {}
         for name in ("c3", "c4"):
@@ -803,6 +845,8 @@ def run_gpu_dist(args):
             except Exception as e:  # report, keep the sweep line
                 vc[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
         line["vcycle"] = vc
+    if not guard.finish():
+        return 0
     if rank == 0:
         print(json.dumps(line), flush=True)
     comm.close()
