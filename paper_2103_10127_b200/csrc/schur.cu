@@ -784,7 +784,12 @@ __global__ void __launch_bounds__(NT) schur_factor_kernel(SchurArgs a) {
 // RA: r is 16-byte aligned (checked at launch): node gathers without the per-load alignment test
 // OB: the interface exchange fused into the sweep (Outbox, internal.cuh): ghost-written DoFs of
 // flagged patches go to the consumers' receive buffers
-template <int MT, int D, int NRB, bool DET, bool NDP, bool RA, bool OB, bool WTB = false>
+// PA: warp-level pre-aggregation of the scatter (x-neighbouring patches share the nodes of one
+// column of their restricted 3 x 3 blocks): a lane adds its right neighbour's contribution to a
+// shared node to its own before the atomic, the neighbour skips that atomic.  The match is by node
+// index on both lanes (the same predicate), so any patch shape is handled correctly; only the
+// slot pairs tried ((2,0), (5,3), (8,6): R9's lexicographic order) assume the interior pattern.
+template <int MT, int D, int NRB, bool DET, bool NDP, bool RA, bool OB, bool WTB = false, bool PA = false>
 __device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, int NN, int64_t pairs,
                                                                  const double2* __restrict__ W,
                                                                  const int32_t* __restrict__ ND,
@@ -912,6 +917,44 @@ __device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, i
     const double* aux = WTB ? nullptr : AUX + chunk * (MT + 2) * 32 + lane;
     const double* wt = WTB ? wtab + (int64_t)pid_i * (MT + 1) : nullptr;
     const double t = (WTB ? __ldcs(SINV + i) : aux[(MT + 1) * 32]) * (gacc - rpd);
+    if constexpr (PA) {
+        static_assert(MT == 9 && WTB && !DET && !OB, "pre-aggregated scatter: the 2D PoU table kernel");
+        const bool live = i < np;   // the padding slots of the last chunk take part in the shuffles
+        const int m = live ? __ldg(ntab + pid_i) : 0;
+        int ndk[MT];
+        double val[MT][D];
+#pragma unroll
+        for (int k = 0; k < MT; ++k) {
+            ndk[k] = k < m ? ND_AT(k) : -1;
+            const double wk = k < m ? omega * __ldg(wt + k) : 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) val[k][c] = wk * fma(gR[k][c], t, acc[k][c]);
+        }
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            const int kr = 3 * p + 2, kl = 3 * p;
+            const int pn = __shfl_down_sync(0xffffffffu, ndk[kl], 1);
+            const int on = __shfl_up_sync(0xffffffffu, ndk[kr], 1);
+            const bool take = lane < 31 && ndk[kr] >= 0 && pn == ndk[kr];
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const double pvc = __shfl_down_sync(0xffffffffu, val[kl][c], 1);
+                if (take) val[kr][c] += pvc;
+            }
+            if (lane > 0 && ndk[kl] >= 0 && on == ndk[kl]) ndk[kl] = -1;   // the left neighbour adds it
+        }
+        if (!live) return;
+#pragma unroll
+        for (int k = 0; k < MT; ++k) {
+            if (ndk[k] >= 0) {
+#pragma unroll
+                for (int c = 0; c < D; ++c) atomicAdd(x + ndk[k] + c, val[k][c]);
+            }
+        }
+        const double wpr = __ldg(wt + MT);
+        if (wpr != 0.0) atomicAdd(x + pd, omega * wpr * (-t));
+        return;
+    }
     if (i >= np) return;   // padding slots of the last chunk
     const int m = WTB ? __ldg(ntab + pid_i) : NR[i];
     double* cb = DET ? cbuf + i * (MT * D + 1) : nullptr;
@@ -952,7 +995,7 @@ __device__ __forceinline__ void schur_thread_body(int64_t np, int64_t nchunks, i
 #undef ND_AT
 
 template <int MT, int D, int NRB = 0, bool DET = false, bool NDP = false, bool RA = false, bool OB = false,
-          bool WTB = false>
+          bool WTB = false, bool PA = false>
 __global__ void __launch_bounds__(128, 4) schur_sweep_thread_kernel(int64_t np, int64_t nchunks, int NN, int64_t pairs,
                                                                  const double2* __restrict__ W,
                                                                  const int32_t* __restrict__ ND,
@@ -968,7 +1011,7 @@ __global__ void __launch_bounds__(128, 4) schur_sweep_thread_kernel(int64_t np, 
                                                                  const double* __restrict__ wtab,
                                                                  const int32_t* __restrict__ ntab,
                                                                  const double* __restrict__ SINV) {
-    schur_thread_body<MT, D, NRB, DET, NDP, RA, OB, WTB>(np, nchunks, NN, pairs, W, ND, npid, nbase, ntbl, PD, NR, AUX,
+    schur_thread_body<MT, D, NRB, DET, NDP, RA, OB, WTB, PA>(np, nchunks, NN, pairs, W, ND, npid, nbase, ntbl, PD, NR, AUX,
                                                          r, x, omega, cbuf, pf, ob_view(ob), wtab, ntab, SINV);
     if constexpr (OB) {   // a writer: this warp's chunk holds a ghost-writing patch
         const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1944,6 +1987,15 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
                                 : schur_sweep_thread_kernel<MT, 2, 0, DET, true, false, OB>)
                        : shape ? schur_sweep_thread_kernel<MT, 2, 8, DET, false, false, OB>
                                : schur_sweep_thread_kernel<MT, 2, 0, DET, false, false, OB>;
+    // the pre-aggregated scatter (PA) for the 2D PoU table kernel; RAV_SCHUR_PA=0: off.  Measured (B200,
+    // profiles/r02pa_*): sweep alone c2 96.5 -> 95.2 us, c3 1358 -> 1337 us; c2 step 16.01 -> 15.70 ms
+    static const int pa = [] {
+        const char* e = getenv("RAV_SCHUR_PA");
+        return e ? atoi(e) : 1;
+    }();
+    if constexpr (MT == 9 && !DET && !OB) {
+        if (pa && F.npid && shape && ra && F.wtab) kern = schur_sweep_thread_kernel<9, 2, 8, false, true, true, false, true, true>;
+    }
     // rectangular blocks prefetched ahead by the bulk-copy unit (0: off).  Measured (rav_apply alone):
     // c2 115.0 / 109.7 / 108.9 / 110.3 / 117.0 us for 0 / 1 / 2 / 3 / 5; c3 1606 -> 1474 us at 2
     static const int pf = [] {
