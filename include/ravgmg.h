@@ -245,7 +245,12 @@ typedef struct {
     int32_t deterministic;      /* 1: run-to-run bitwise reproducible scatter (R16): the sweep writes
                                    every correction to its own slot and a second kernel adds them
                                    to x per DoF in ascending patch order (no atomics).  Schur formats
-                                   only (RAV_ERR_ARG otherwise); MV is deterministic by construction */
+                                   only (RAV_ERR_ARG otherwise); MV is deterministic by construction.
+                                   0: corrections are added with floating-point reductions in
+                                   arrival order; the 2D thread sweep first sums, inside a warp, the
+                                   corrections of x-neighbouring patches to a shared node (DESIGN 5.1,
+                                   RAV_SCHUR_PA): Eq. 13's sum in another order, equal to the
+                                   oracle's to rounding, not run-to-run bitwise */
     int64_t n_vel;              /* DoFs < n_vel are velocity (needed by DIAG and SCHUR) */
     void*   stream;             /* cudaStream_t */
     int32_t block_dim;          /* velocity components interleaved as dof = block_dim * node + c
