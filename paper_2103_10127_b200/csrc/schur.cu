@@ -1997,10 +1997,12 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
         if (pa && F.npid && shape && ra && F.wtab) kern = schur_sweep_thread_kernel<9, 2, 8, false, true, true, false, true, true>;
     }
     // rectangular blocks prefetched ahead by the bulk-copy unit (0: off).  Measured (rav_apply alone):
-    // c2 115.0 / 109.7 / 108.9 / 110.3 / 117.0 us for 0 / 1 / 2 / 3 / 5; c3 1606 -> 1474 us at 2
+    // c2 115.0 / 109.7 / 108.9 / 110.3 / 117.0 us for 0 / 1 / 2 / 3 / 5; c3 1606 -> 1474 us at 2.  Re-tuned with
+    // the weight table and the pre-aggregated scatter (profiles/r02k_*): c2 101.9 / 92.5 / 95.2 / 96.0 us for
+    // 0 / 1 / 2 / 3, c3 1470 / 1336 / 1338 us for 0 / 1 / 2: one block ahead is the default
     static const int pf = [] {
         const char* e = getenv("RAV_SCHUR_PF");
-        return e ? atoi(e) : 2;
+        return e ? atoi(e) : 1;
     }();
     launch_maybe_pdl(kern, dim3((unsigned)cdiv(F.nchunks * 32, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
                      (const int32_t*)F.DT, (const int32_t*)F.npid, (const int32_t*)F.nbase, (const int32_t*)F.ntbl,
