@@ -969,7 +969,7 @@ static int nb_block_threads() {
     static const int bs = [] {
         const char* e = getenv("RAV_NB_BS");
         const int v = e ? atoi(e) : 128;
-        return v == 128 ? 128 : 256;
+        return v == 128 || v == 64 ? v : 256;
     }();
     return bs;
 }

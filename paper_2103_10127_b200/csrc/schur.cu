@@ -2004,7 +2004,15 @@ static void launch_schur_thread(int64_t np, const Factors& F, const double* r, d
         const char* e = getenv("RAV_SCHUR_PF");
         return e ? atoi(e) : 1;
     }();
-    launch_maybe_pdl(kern, dim3((unsigned)cdiv(F.nchunks * 32, 128)), dim3(128), 0, s, np, F.nchunks, F.NN, F.pairs, W,
+    // threads per block (a chunk per warp; the register budget gives 16 warps per SM at any of these).
+    // One-warp blocks let an SM take the next chunk as soon as one warp retires instead of when four
+    // have: c2 sweep 92.9 / 91.3 / 91.15 us at 128 / 64 / 32 (profiles/r02n_bs_sweep.txt), c3 equal
+    static const int bs = [] {
+        const char* e = getenv("RAV_SCHUR_BS");
+        const int v = e ? atoi(e) : 32;
+        return v == 128 || v == 64 ? v : 32;
+    }();
+    launch_maybe_pdl(kern, dim3((unsigned)cdiv(F.nchunks * 32, bs)), dim3(bs), 0, s, np, F.nchunks, F.NN, F.pairs, W,
                      (const int32_t*)F.DT, (const int32_t*)F.npid, (const int32_t*)F.nbase, (const int32_t*)F.ntbl,
                      (const int32_t*)F.PD, (const int32_t*)F.NR, (const double*)F.WT, r, x, omega, F.cbuf, pf, ob,
                      (const double*)F.wtab, (const int32_t*)F.ntab, (const double*)F.SINV);
